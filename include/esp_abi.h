@@ -1,0 +1,291 @@
+/* esp_abi.h — C ABI of the B200-native ESP (elastic sequence parallelism)
+ * data path. Plain pointers and sizes only; no C++ or torch types cross it.
+ *
+ * Two families of entry points:
+ *
+ *  (1) Pure host planning functions — B200-side restatements of the
+ *      reference's hot-path placement mechanics, bit-exact with them:
+ *        esp_kv_bytes_per_token      <- cluster.cpp:30-34   (kv_bytes_per_token)
+ *        esp_plan_prefill_scale_down <- scheduler.cpp:663-713 (plan_prefill_scale_down)
+ *        esp_plan_decode_step        <- scheduler.cpp:726-804 (plan_decode_step_core)
+ *        esp_assign_masters          <- esp_mechanics.cpp:220-238
+ *        esp_decode_step_comm        <- esp_mechanics.cpp:240-264
+ *        esp_build_ring_schedule     <- esp_mechanics.cpp:24-70
+ *        esp_proactive_scale_down    <- esp_mechanics.cpp:78-136
+ *        esp_reactive_migrate        <- esp_mechanics.cpp:138-218
+ *        esp_sib_prefill_time / esp_sib_decode_time <- cost_model.cpp:169-187
+ *
+ *  (2) The runtime (executor): each elastic instance (reference
+ *      ElasticInstance, cluster.hpp:69-78) is a GPU-resident slice of one
+ *      token-granular paged KV pool (reference KvPool, cluster.hpp:102-128).
+ *      The reference engine commits placements at Engine::apply_decision
+ *      (engine.cpp:246-490); a Policy decorator calls
+ *        esp_prefill      for every PrefillPlan    (state.hpp:83-96)
+ *        esp_decode_step  for every DecodeStepPlan (state.hpp:98-107)
+ *        esp_move_kv      for every KvMove         (state.hpp:67-72)
+ *        esp_free_request when a request finishes / is evicted (engine.cpp:119-166)
+ *      and the device page tables then hold exactly the reference's
+ *      Request.placement (cluster.hpp:44, :63) and ElasticInstance.kv_used.
+ *
+ * Error convention: every int-returning call returns ESP_OK (0) or one of the
+ * negative codes below, mapped 1:1 to the reference taxonomy
+ * (types.hpp:48-109); nothing throws across the ABI. esp_last_error() gives a
+ * thread-local message for the last failure on the calling thread.
+ *
+ * Threading: one caller thread per runtime (the reference engine is strictly
+ * single-threaded, engine.hpp:45). Calls return after their results are
+ * host-visible. Caller owns every array it passes (borrowed for the call);
+ * the runtime owns device memory, weights, slabs and page tables.
+ */
+#ifndef ESP_ABI_H_
+#define ESP_ABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define ESP_ABI_VERSION 1
+
+/* ---- error codes (reference types.hpp:48-109) --------------------------- */
+enum esp_status {
+  ESP_OK = 0,
+  ESP_ERR_CONFIG = -1,           /* ConfigError               types.hpp:53-56  */
+  ESP_ERR_INFEASIBLE = -2,       /* InfeasiblePlanError       types.hpp:83-86  */
+  ESP_ERR_INTERNAL = -3,         /* InternalError             types.hpp:95-98  */
+  ESP_ERR_CAPACITY = -4,         /* AllocResult{ok=false}     cluster.hpp:95-98 */
+  ESP_ERR_MASTER_FULL = -5,      /* DecodeCommResult{ok=false} esp_mechanics.hpp:104-110 */
+  ESP_ERR_UNKNOWN_STRATEGY = -6, /* UnknownStrategyError      types.hpp:58-65  */
+  ESP_ERR_CUDA = -7,             /* device failure (no reference counterpart) */
+  ESP_ERR_NO_DEVICE = -8         /* compute requested from a placement-only runtime */
+};
+
+const char* esp_last_error(void);
+int32_t esp_abi_version(void);
+
+/* ---- (1) pure host planning --------------------------------------------- */
+
+/* 2 * layers * hidden_dim * bytes_per_element (cluster.cpp:30-34). Returns -1
+ * (and sets ESP_ERR_CONFIG message) on a non-positive field. */
+int64_t esp_kv_bytes_per_token(int32_t layers, int32_t hidden_dim, int32_t kv_heads,
+                               int32_t bytes_per_element);
+
+/* plan_prefill_scale_down (scheduler.cpp:663-713).
+ * in : instances[d] ring order (PrefillPlan.instances), free[d] free slots per
+ *      instance (the scheduler's free_override view), input_lens[n_req] in
+ *      PrefillPlan.requests order.
+ * out: decode_instances[d] (ascending survivors), *n_decode;
+ *      per request r: place_n[r] (instance, tokens) pairs in FILL ORDER at
+ *      place_inst[r*d + p], place_tok[r*d + p] (a request's tokens are laid
+ *      contiguously over them in that order); *ring_volume = (d-1)*sum(len).
+ * Returns ESP_ERR_INFEASIBLE when the batch KV exceeds the interval. */
+int esp_plan_prefill_scale_down(const int32_t* instances, const int64_t* free, int32_t d,
+                                const int64_t* input_lens, int32_t n_req,
+                                int32_t* decode_instances, int32_t* n_decode,
+                                int32_t* place_inst, int64_t* place_tok, int32_t* place_n,
+                                int64_t* ring_volume);
+
+/* One strategy row of the scaling information base (cost_model.hpp:47-52). */
+typedef struct esp_sib_record {
+  int32_t dop, tp;
+  double alpha_p, beta_p, gamma_p;          /* prefill  cost_model.hpp:31-35 */
+  double alpha_d, beta_d, gamma_d;          /* decode   cost_model.hpp:40-45 */
+  int32_t compute_bound_batch_threshold;
+  double tipping_ms;
+} esp_sib_record;
+
+/* Sib::prefill_time_sums / decode_time (cost_model.cpp:169-187). Return a
+ * negative time and ESP_ERR_UNKNOWN_STRATEGY message if (dop,tp) is absent. */
+double esp_sib_prefill_time(const esp_sib_record* sib, int32_t n_rec, int32_t dop, int32_t tp,
+                            double sum_len, double sum_len_sq);
+double esp_sib_decode_time(const esp_sib_record* sib, int32_t n_rec, int32_t dop, int32_t tp,
+                           int32_t batch_size, int64_t resident_kv, int32_t n_masters);
+
+/* plan_decode_step_core (scheduler.cpp:726-804).
+ * free_inst/free_tok: free slots keyed by instance (n_free entries, must cover
+ * members and idle). idle_pool/n_idle: in-out, consumed from the front.
+ * out: *feasible, masters[*n_masters] ascending, add_instances[*n_add]. */
+int esp_plan_decode_step(const int32_t* members, int32_t d, int32_t batch_size,
+                         const int32_t* free_inst, const int64_t* free_tok, int32_t n_free,
+                         int32_t* idle_pool, int32_t* n_idle,
+                         const esp_sib_record* sib, int32_t n_rec, int32_t tp,
+                         int32_t enable_scale_up,
+                         int32_t* feasible, int32_t* masters, int32_t* n_masters,
+                         int32_t* add_instances, int32_t* n_add);
+
+/* assign_masters (esp_mechanics.cpp:220-238): master_of[i] is the master of
+ * batch[i] (requests dealt in ascending id to the least-loaded master, lowest
+ * id on ties). */
+int esp_assign_masters(const int64_t* batch, int32_t b, const int32_t* masters, int32_t k,
+                       int32_t* master_of);
+
+/* decode_step_comm (esp_mechanics.cpp:240-264). masters[k] with counts[k]
+ * requests each, free slots master_free[k]; group width d.
+ * Returns ESP_ERR_MASTER_FULL with *full_master set on the first (ascending
+ * id) master without room for its appends. */
+int esp_decode_step_comm(int32_t d, const int32_t* masters, const int32_t* counts,
+                         const int64_t* master_free, int32_t k,
+                         int64_t* query_volume, int64_t* overlappable_volume,
+                         int32_t* full_master);
+
+/* build_ring_schedule (esp_mechanics.cpp:45-70): round r < d-1, position i
+ * sends the block that started at (i-r) mod d to (i+1) mod d.
+ * out arrays have (d-1)*d entries, row-major [round][position]. */
+int esp_build_ring_schedule(const int32_t* group, const int64_t* segment_tokens, int32_t d,
+                            int32_t* from, int32_t* to, int64_t* volume,
+                            int64_t* total_comm_volume);
+
+/* proactive_scale_down (esp_mechanics.cpp:78-136) for one aggregate target
+ * placement (n_target entries). free_inst/free_tok give pool free slots. */
+int esp_proactive_scale_down(const int32_t* ring, const int64_t* segment_tokens, int32_t d,
+                             const int32_t* sources, int32_t n_sources,
+                             const int32_t* targets, int32_t n_targets,
+                             const int32_t* target_inst, const int64_t* target_tok,
+                             int32_t n_target,
+                             const int32_t* free_inst, const int64_t* free_tok, int32_t n_free,
+                             int64_t* extra_migration_volume,
+                             int64_t* transient_buffer_tokens);
+
+/* reactive_migrate (esp_mechanics.cpp:138-218), the migration baseline. */
+int esp_reactive_migrate(const int32_t* sources, int32_t n_sources, const int32_t* targets,
+                         int32_t n_targets, int64_t total_tokens,
+                         const int32_t* free_inst, const int64_t* free_tok, int32_t n_free,
+                         int32_t* feasible, int32_t* blocked_instance,
+                         int64_t* per_source_headroom, int32_t* final_inst,
+                         int64_t* final_tok, int32_t* n_final, int64_t* migration_volume);
+
+/* ---- (2) runtime ---------------------------------------------------------- */
+
+typedef struct esp_runtime esp_runtime;
+
+/* Llama-architecture geometry (LWM-7B: 32, 4096, 32, 128, 11008, 32000). */
+typedef struct esp_model_config {
+  int32_t layers;
+  int32_t hidden;     /* = heads * head_dim */
+  int32_t heads;      /* query heads == kv heads (MHA, as LWM-7B) */
+  int32_t head_dim;   /* 64 or 128 */
+  int32_t ffn;        /* multiple of 128 */
+  int32_t vocab;
+  float rms_eps;      /* 1e-5 */
+  float rope_theta;   /* 10000 */
+  uint64_t weight_seed;
+} esp_model_config;
+
+/* n_instances elastic instances. instance_device[i] is the CUDA device
+ * ordinal of instance i (several instances may share a device); NULL creates
+ * a PLACEMENT-ONLY runtime (page tables and slot allocators, no device
+ * memory, no kernels: compute calls then fail with ESP_ERR_NO_DEVICE).
+ * kv_capacity_tokens: token slots per instance (ElasticInstance.kv_capacity);
+ * <= 0 sizes it from free HBM. */
+int esp_runtime_create(const esp_model_config* cfg, int32_t n_instances,
+                       const int32_t* instance_device, int64_t kv_capacity_tokens,
+                       esp_runtime** out);
+void esp_runtime_destroy(esp_runtime* rt);
+
+int esp_instance_info(const esp_runtime* rt, int32_t instance, int64_t* capacity,
+                      int64_t* used);
+
+/* ESP prefill of one PrefillPlan (state.hpp:83-96) as a striped ring over
+ * ring[dop] with proactive scale-down: every token's K/V lands in a page slot
+ * of its resting instance (retain pairs) during the ring pass itself. */
+typedef struct esp_prefill_args {
+  int32_t n_requests;
+  const int64_t* request_ids;      /* PrefillPlan.requests (longest first)   */
+  const int64_t* input_lens;
+  const int32_t* tokens;           /* concatenated prompts; NULL if placement-only */
+  int32_t dop;
+  const int32_t* ring;             /* PrefillPlan.instances                  */
+  const int32_t* retain_n;         /* per request: #(instance, tokens) pairs */
+  const int32_t* retain_instance;  /* concatenated, token order              */
+  const int64_t* retain_tokens;
+  int32_t* first_token_out;        /* [n_requests] greedy token, nullable    */
+  float* logits_out;               /* [n_requests x vocab] fp32, nullable    */
+  double* device_ms_out;           /* device time of the pass, nullable      */
+} esp_prefill_args;
+int esp_prefill(esp_runtime* rt, const esp_prefill_args* args);
+
+/* One multi-master decoding iteration (DecodeStepPlan, state.hpp:98-107):
+ * members = group instances after scale-up, masters = plan.masters. The
+ * runtime recomputes assign_masters exactly as the engine does
+ * (engine.cpp:401), appends each request's new KV token on its master, runs
+ * split-KV attention on every instance holding the request's KV and combines
+ * the partial (o, lse) at the master. */
+typedef struct esp_decode_args {
+  int32_t n_members;
+  const int32_t* members;
+  int32_t n_masters;
+  const int32_t* masters;
+  int32_t batch_size;
+  const int64_t* batch;            /* GroupState.batch                      */
+  const int32_t* in_tokens;        /* [b] or NULL: each request's last token */
+  int32_t* out_tokens;             /* [b] greedy tokens, nullable            */
+  float* logits_out;               /* [b x vocab], nullable                  */
+  double* device_ms_out;
+} esp_decode_args;
+int esp_decode_step(esp_runtime* rt, const esp_decode_args* args);
+
+/* KvMove (state.hpp:67-72): move `tokens` of request's KV from -> to (the
+ * request's most recent tokens on `from` go first). */
+int esp_move_kv(esp_runtime* rt, int64_t request, int32_t from, int32_t to, int64_t tokens);
+
+/* Releases every slot of the request (finish / evict / recompute). */
+int esp_free_request(esp_runtime* rt, int64_t request);
+
+/* Page-table readback for parity: (instance, token count) pairs ascending by
+ * instance — exactly the shape of the reference KvPlacement map. */
+int esp_query_placement(const esp_runtime* rt, int64_t request, int32_t* inst,
+                        int64_t* tokens, int32_t cap, int32_t* n);
+
+/* Recounts, ON THE DEVICE, the slots each instance's slab has assigned and
+ * checks them against the host counters and page tables (the device-side
+ * analogue of KvPool::check_conservation, cluster.cpp:113-132). */
+int esp_check_conservation(esp_runtime* rt);
+
+/* Token history of a request (prompt + generated), for parity tests. */
+int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int32_t cap,
+                       int32_t* n);
+
+/* Measured ProfileSample records ({"kind":"profile","dop","tp","lengths",
+ * "measured_ms"}, cost_model.cpp:243-248) appended to a JSONL file. */
+int esp_dump_profiles(const esp_runtime* rt, const char* path);
+
+/* Count of kernel launches issued by this runtime so far. */
+int64_t esp_launch_count(const esp_runtime* rt);
+
+/* ---- kernel-level hooks (device pointers; for parity/roofline tests) ------- */
+
+/* D[M,N] (bf16, row-major) = A[M,K] (bf16, row-major) x B[N,K]^T (bf16,
+ * row-major = K-major). epilogue: 0 store, 1 D += (residual add, D is read). */
+int esp_k_gemm(const void* A, const void* B, void* D, int32_t M, int32_t N, int32_t K,
+               int32_t epilogue, void* stream);
+
+/* Striped ring attention for one instance (ring position i of d) against d
+ * KV blocks, bf16 [rows x heads*head_dim] row-major buffers, fp32 softmax.
+ * kv_k[r], kv_v[r], kv_len[r], origin[r] describe round r's block. */
+int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
+                         const void* const* kv_k, const void* const* kv_v,
+                         const int32_t* kv_len, const int32_t* origin, void* out,
+                         int32_t heads, int32_t head_dim, void* stream);
+
+/* Split-KV paged decode attention + LSE combine over n_chunks chunks of
+ * slots: request b's query q[b], chunk c reads slots slot_idx[c][0..n) from
+ * slab (k_slab, v_slab rows of heads*head_dim bf16). */
+int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_slab,
+                           const void* const* v_slab, const int32_t* const* slot_idx,
+                           const int32_t* n_slots, const int32_t* chunk_req, int32_t n_chunks,
+                           void* out, int32_t heads, int32_t head_dim, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESP_ABI_H_ */

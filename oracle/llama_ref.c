@@ -1,0 +1,334 @@
+/* CPU numeric oracle — TEST INFRASTRUCTURE ONLY (tests/, smoke(), bench.py's
+ * cpu_baseline leg). Never linked into or called by the product path.
+ *
+ * The reference (espsim) has no numeric path: SPEC.md:14 and :283 put
+ * attention numerics out of scope, so there is no reference function to
+ * restate line by line. This file restates the computation the ESP data path
+ * must reproduce, from the paper's own statement that ESP at any degree,
+ * placement or master set has "the same accuracy as the original
+ * implementations": a DENSE, single-device, causal
+ * Llama-2-architecture forward (LWM-1M-Text = Llama-2-7B arch)
+ *   embed -> L x [RMSNorm -> QKV -> RoPE -> causal softmax attention -> O
+ *   (+res) -> RMSNorm -> SiLU(gate)*up -> down (+res)] -> RMSNorm -> LM head
+ *   -> greedy argmax,
+ * prefill of the whole prompt followed by KV-cached decode steps, one token
+ * appended per step (KV count after step s = input_len + s, engine.cpp:408-419).
+ * Parity of this oracle is therefore UNPINNED by the reference (no golden
+ * vectors exist for numerics); the placement side is pinned
+ * separately against the compiled reference.
+ *
+ * Weights are the seeded synthetic weights of
+ * paper_2404_09526_b200/csrc/kernels/synthetic.h, restated here bit-exactly
+ * (splitmix64 -> 4-term Irwin-Hall -> one fp32 multiply -> bf16 RNE).
+ *
+ * emulate_bf16 = 1 rounds to bf16 at the points where the GPU path stores
+ * bf16 (residual stream, norm outputs, q/k/v after RoPE, attention output,
+ * SiLU*up); 0 keeps everything fp32 (the "fp32 check mode").
+ */
+#include <math.h>
+#include <omp.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  int32_t layers, hidden, heads, head_dim, ffn, vocab;
+  float rms_eps, rope_theta;
+  uint64_t weight_seed;
+} llama_cfg;
+
+enum { T_EMBED = 1, T_Q = 2, T_K = 3, T_V = 4, T_O = 5, T_GATE = 6, T_UP = 7, T_DOWN = 8, T_LM = 9 };
+
+static uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+static float bf16_round(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return f; /* inf / nan */
+  u += 0x7fffu + ((u >> 16) & 1u);                 /* round to nearest even */
+  u &= 0xffff0000u;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+/* synthetic.h: synthetic_weight(), then __float2bfloat16_rn. */
+float llama_ref_weight(uint64_t seed, int tensor, int layer, int64_t row, int64_t col,
+                       int64_t cols) {
+  const uint64_t idx = (uint64_t)row * (uint64_t)cols + (uint64_t)col;
+  const uint64_t key = ((uint64_t)tensor << 56) ^ ((uint64_t)layer << 48) ^ idx;
+  const uint64_t h = splitmix64(seed ^ splitmix64(key));
+  const int32_t s = (int32_t)(h & 0xFFFF) + (int32_t)((h >> 16) & 0xFFFF) +
+                    (int32_t)((h >> 32) & 0xFFFF) + (int32_t)(h >> 48);
+  const float x = (float)(s - 131070) * 5.2857997e-07f;
+  return bf16_round(x);
+}
+
+static float* make_weight(const llama_cfg* c, int tensor, int layer, int64_t rows, int64_t cols) {
+  float* w = (float*)malloc(sizeof(float) * rows * cols);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t k = 0; k < cols; ++k) {
+      w[r * cols + k] = llama_ref_weight(c->weight_seed, tensor, layer, r, k, cols);
+    }
+  }
+  return w;
+}
+
+/* Y[t][o] = sum_k X[t][k] * W[o][k]  (nn.Linear layout), 4x4 register blocks. */
+static void gemm_nt(const float* X, int64_t T, int64_t K, const float* W, int64_t O, float* Y) {
+  const int64_t tb = (T + 3) / 4, ob = (O + 3) / 4;
+#pragma omp parallel for collapse(2) schedule(dynamic, 4)
+  for (int64_t oi = 0; oi < ob; ++oi) {
+    for (int64_t ti = 0; ti < tb; ++ti) {
+      const int64_t t0 = ti * 4, o0 = oi * 4;
+      float acc[4][4] = {{0}};
+      const float* x[4];
+      const float* w[4];
+      for (int j = 0; j < 4; ++j) {
+        x[j] = X + (t0 + j < T ? t0 + j : t0) * K;
+        w[j] = W + (o0 + j < O ? o0 + j : o0) * K;
+      }
+      for (int a = 0; a < 4; ++a) {
+        for (int b = 0; b < 4; ++b) {
+          float s = 0.f;
+          const float* xa = x[a];
+          const float* wb = w[b];
+#pragma omp simd reduction(+ : s)
+          for (int64_t k = 0; k < K; ++k) s += xa[k] * wb[k];
+          acc[a][b] = s;
+        }
+      }
+      for (int a = 0; a < 4; ++a) {
+        if (t0 + a >= T) continue;
+        for (int b = 0; b < 4; ++b) {
+          if (o0 + b < O) Y[(t0 + a) * O + o0 + b] = acc[a][b];
+        }
+      }
+    }
+  }
+}
+
+static void rmsnorm(const float* x, int64_t T, int64_t H, float eps, int rb, float* y) {
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t) {
+    double ss = 0;
+    for (int64_t i = 0; i < H; ++i) ss += (double)x[t * H + i] * x[t * H + i];
+    const float inv = 1.0f / sqrtf((float)(ss / (double)H) + eps);
+    for (int64_t i = 0; i < H; ++i) {
+      const float v = x[t * H + i] * inv; /* gamma = 1 */
+      y[t * H + i] = rb ? bf16_round(v) : v;
+    }
+  }
+}
+
+static void rope_rows(float* q, int64_t T, int heads, int hd, const int64_t* pos, float theta) {
+  const int half = hd / 2;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t) {
+    for (int h = 0; h < heads; ++h) {
+      float* v = q + t * (int64_t)heads * hd + (int64_t)h * hd;
+      for (int j = 0; j < half; ++j) {
+        const float inv_freq = powf(theta, -(float)(2 * j) / (float)hd);
+        const float ang = (float)pos[t] * inv_freq;
+        const float c = cosf(ang), s = sinf(ang);
+        const float x1 = v[j], x2 = v[j + half];
+        v[j] = x1 * c - x2 * s;
+        v[j + half] = x2 * c + x1 * s;
+      }
+    }
+  }
+}
+
+typedef struct {
+  float *wq, *wk, *wv, *wo, *wg, *wu, *wd;
+} layer_w;
+
+typedef struct {
+  llama_cfg c;
+  float *emb, *lm;
+  layer_w* L;
+  float **kc, **vc; /* per layer KV cache [cap x H] */
+  int64_t cap, len;
+  int rb;
+} model;
+
+static void model_init(model* m, const llama_cfg* c, int64_t cap, int rb) {
+  m->c = *c;
+  m->rb = rb;
+  const int64_t H = c->hidden, F = c->ffn, V = c->vocab;
+  m->emb = make_weight(c, T_EMBED, 0, V, H);
+  m->lm = make_weight(c, T_LM, 0, V, H);
+  m->L = (layer_w*)calloc((size_t)c->layers, sizeof(layer_w));
+  m->kc = (float**)calloc((size_t)c->layers, sizeof(float*));
+  m->vc = (float**)calloc((size_t)c->layers, sizeof(float*));
+  for (int l = 0; l < c->layers; ++l) {
+    m->L[l].wq = make_weight(c, T_Q, l, H, H);
+    m->L[l].wk = make_weight(c, T_K, l, H, H);
+    m->L[l].wv = make_weight(c, T_V, l, H, H);
+    m->L[l].wo = make_weight(c, T_O, l, H, H);
+    m->L[l].wg = make_weight(c, T_GATE, l, F, H);
+    m->L[l].wu = make_weight(c, T_UP, l, F, H);
+    m->L[l].wd = make_weight(c, T_DOWN, l, H, F);
+    m->kc[l] = (float*)malloc(sizeof(float) * cap * H);
+    m->vc[l] = (float*)malloc(sizeof(float) * cap * H);
+  }
+  m->cap = cap;
+  m->len = 0;
+}
+
+static void model_free(model* m) {
+  free(m->emb);
+  free(m->lm);
+  for (int l = 0; l < m->c.layers; ++l) {
+    free(m->L[l].wq); free(m->L[l].wk); free(m->L[l].wv); free(m->L[l].wo);
+    free(m->L[l].wg); free(m->L[l].wu); free(m->L[l].wd);
+    free(m->kc[l]); free(m->vc[l]);
+  }
+  free(m->L);
+  free(m->kc);
+  free(m->vc);
+}
+
+/* Runs T new tokens (positions len..len+T-1) through the model, appending
+ * their K/V; writes fp32 logits of the LAST new token into `logits`. */
+static void forward(model* m, const int32_t* tok, int64_t T, float* logits) {
+  const llama_cfg* c = &m->c;
+  const int64_t H = c->hidden, F = c->ffn, V = c->vocab;
+  const int heads = c->heads, hd = c->head_dim;
+  const int rb = m->rb;
+  const int64_t p0 = m->len;
+  float* x = (float*)malloc(sizeof(float) * T * H);
+  float* xn = (float*)malloc(sizeof(float) * T * H);
+  float* q = (float*)malloc(sizeof(float) * T * H);
+  float* k = (float*)malloc(sizeof(float) * T * H);
+  float* v = (float*)malloc(sizeof(float) * T * H);
+  float* att = (float*)malloc(sizeof(float) * T * H);
+  float* tmp = (float*)malloc(sizeof(float) * T * H);
+  float* g = (float*)malloc(sizeof(float) * T * F);
+  float* u = (float*)malloc(sizeof(float) * T * F);
+  int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * T);
+  for (int64_t t = 0; t < T; ++t) {
+    pos[t] = p0 + t;
+    memcpy(x + t * H, m->emb + (int64_t)tok[t] * H, sizeof(float) * H);
+  }
+  const float scale = 1.0f / sqrtf((float)hd);
+  for (int l = 0; l < c->layers; ++l) {
+    layer_w* w = &m->L[l];
+    rmsnorm(x, T, H, c->rms_eps, rb, xn);
+    gemm_nt(xn, T, H, w->wq, H, q);
+    gemm_nt(xn, T, H, w->wk, H, k);
+    gemm_nt(xn, T, H, w->wv, H, v);
+    rope_rows(q, T, heads, hd, pos, c->rope_theta);
+    rope_rows(k, T, heads, hd, pos, c->rope_theta);
+    if (rb) {
+      for (int64_t i = 0; i < T * H; ++i) {
+        q[i] = bf16_round(q[i]);
+        k[i] = bf16_round(k[i]);
+        v[i] = bf16_round(v[i]);
+      }
+    }
+    memcpy(m->kc[l] + p0 * H, k, sizeof(float) * T * H);
+    memcpy(m->vc[l] + p0 * H, v, sizeof(float) * T * H);
+    const float* K = m->kc[l];
+    const float* Vc = m->vc[l];
+#pragma omp parallel for collapse(2) schedule(dynamic, 8)
+    for (int64_t t = 0; t < T; ++t) {
+      for (int h = 0; h < heads; ++h) {
+        const int64_t nk = p0 + t + 1; /* causal: keys 0..pos */
+        const float* qv = q + t * H + (int64_t)h * hd;
+        float* sc = (float*)malloc(sizeof(float) * nk);
+        float mx = -3.0e38f;
+        for (int64_t j = 0; j < nk; ++j) {
+          const float* kv = K + j * H + (int64_t)h * hd;
+          float s = 0.f;
+#pragma omp simd reduction(+ : s)
+          for (int d = 0; d < hd; ++d) s += qv[d] * kv[d];
+          s *= scale;
+          sc[j] = s;
+          if (s > mx) mx = s;
+        }
+        double sum = 0;
+        for (int64_t j = 0; j < nk; ++j) {
+          sc[j] = expf(sc[j] - mx);
+          sum += sc[j];
+        }
+        float o[128];
+        for (int d = 0; d < hd; ++d) o[d] = 0.f;
+        for (int64_t j = 0; j < nk; ++j) {
+          const float p = sc[j];
+          const float* vv = Vc + j * H + (int64_t)h * hd;
+          for (int d = 0; d < hd; ++d) o[d] += p * vv[d];
+        }
+        float* dst = att + t * H + (int64_t)h * hd;
+        for (int d = 0; d < hd; ++d) {
+          const float r = (float)(o[d] / sum);
+          dst[d] = rb ? bf16_round(r) : r;
+        }
+        free(sc);
+      }
+    }
+    gemm_nt(att, T, H, w->wo, H, tmp);
+    for (int64_t i = 0; i < T * H; ++i) {
+      const float r = x[i] + tmp[i];
+      x[i] = rb ? bf16_round(r) : r;
+    }
+    rmsnorm(x, T, H, c->rms_eps, rb, xn);
+    gemm_nt(xn, T, H, w->wg, F, g);
+    gemm_nt(xn, T, H, w->wu, F, u);
+    for (int64_t i = 0; i < T * F; ++i) {
+      const float a = g[i] / (1.0f + expf(-g[i])) * u[i];
+      g[i] = rb ? bf16_round(a) : a;
+    }
+    gemm_nt(g, T, F, w->wd, H, tmp);
+    for (int64_t i = 0; i < T * H; ++i) {
+      const float r = x[i] + tmp[i];
+      x[i] = rb ? bf16_round(r) : r;
+    }
+  }
+  rmsnorm(x + (T - 1) * H, 1, H, c->rms_eps, rb, xn);
+  gemm_nt(xn, 1, H, m->lm, V, logits);
+  m->len += T;
+  free(x); free(xn); free(q); free(k); free(v); free(att); free(tmp); free(g); free(u);
+  free(pos);
+}
+
+static int32_t argmax(const float* l, int64_t V) {
+  int64_t b = 0;
+  for (int64_t i = 1; i < V; ++i) {
+    if (l[i] > l[b]) b = i;
+  }
+  return (int32_t)b;
+}
+
+/* Prefill `prompt` (S tokens), then n_steps decode steps. Step s feeds
+ * forced[s-1] when forced != NULL (teacher forcing on the GPU's tokens), else
+ * the oracle's own previous greedy token. out_tokens[0..n_steps] and
+ * out_logits[(n_steps+1) x vocab] (nullable) hold each step's greedy token
+ * and logits. Returns 0. */
+int llama_ref_generate(const llama_cfg* c, const int32_t* prompt, int64_t S, int n_steps,
+                       const int32_t* forced, int emulate_bf16, int32_t* out_tokens,
+                       float* out_logits, int n_threads) {
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+  model m;
+  model_init(&m, c, S + n_steps + 1, emulate_bf16);
+  float* lg = (float*)malloc(sizeof(float) * c->vocab);
+  forward(&m, prompt, S, lg);
+  out_tokens[0] = argmax(lg, c->vocab);
+  if (out_logits) memcpy(out_logits, lg, sizeof(float) * c->vocab);
+  for (int s = 1; s <= n_steps; ++s) {
+    int32_t in = forced ? forced[s - 1] : out_tokens[s - 1];
+    forward(&m, &in, 1, lg);
+    out_tokens[s] = argmax(lg, c->vocab);
+    if (out_logits) memcpy(out_logits + (int64_t)s * c->vocab, lg, sizeof(float) * c->vocab);
+  }
+  free(lg);
+  model_free(&m);
+  return 0;
+}
+
+int llama_ref_max_threads(void) { return omp_get_max_threads(); }

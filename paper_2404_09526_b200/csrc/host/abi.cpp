@@ -1,0 +1,438 @@
+// extern "C" surface (include/esp_abi.h). Exceptions stop here: each entry
+// point maps esp::Error to its status code and records the message in a
+// thread-local buffer for esp_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.h"
+#include "esp_abi.h"
+#include "planner.hpp"
+#include "runtime.hpp"
+
+struct esp_runtime {
+  esp::Runtime* impl;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ESP_OK;
+  } catch (const esp::Error& e) {
+    g_last_error = e.what();
+    return e.code();
+  } catch (const std::exception& e) {
+    g_last_error = std::string("internal: ") + e.what();
+    return ESP_ERR_INTERNAL;
+  }
+}
+
+esp::Sib make_sib(const esp_sib_record* sib, int32_t n) {
+  std::vector<esp::SibRecord> recs;
+  for (int32_t i = 0; i < n; ++i) {
+    esp::SibRecord r;
+    r.dop = sib[i].dop;
+    r.tp = sib[i].tp;
+    r.alpha_p = sib[i].alpha_p;
+    r.beta_p = sib[i].beta_p;
+    r.gamma_p = sib[i].gamma_p;
+    r.alpha_d = sib[i].alpha_d;
+    r.beta_d = sib[i].beta_d;
+    r.gamma_d = sib[i].gamma_d;
+    r.threshold = sib[i].compute_bound_batch_threshold;
+    r.tipping_ms = sib[i].tipping_ms;
+    recs.push_back(r);
+  }
+  return esp::Sib(std::move(recs));
+}
+
+std::map<int32_t, int64_t> free_map(const int32_t* inst, const int64_t* tok, int32_t n) {
+  std::map<int32_t, int64_t> m;
+  for (int32_t i = 0; i < n; ++i) m[inst[i]] = tok[i];
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* esp_last_error(void) { return g_last_error.c_str(); }
+int32_t esp_abi_version(void) { return ESP_ABI_VERSION; }
+
+int64_t esp_kv_bytes_per_token(int32_t layers, int32_t hidden_dim, int32_t kv_heads,
+                               int32_t bytes_per_element) {
+  int64_t out = -1;
+  guarded([&] { out = esp::kv_bytes_per_token(layers, hidden_dim, kv_heads, bytes_per_element); });
+  return out;
+}
+
+int esp_plan_prefill_scale_down(const int32_t* instances, const int64_t* free, int32_t d,
+                                const int64_t* input_lens, int32_t n_req,
+                                int32_t* decode_instances, int32_t* n_decode,
+                                int32_t* place_inst, int64_t* place_tok, int32_t* place_n,
+                                int64_t* ring_volume) {
+  return guarded([&] {
+    auto p = esp::plan_prefill_scale_down(std::vector<int32_t>(instances, instances + d),
+                                          std::vector<int64_t>(free, free + d),
+                                          std::vector<int64_t>(input_lens, input_lens + n_req));
+    *n_decode = static_cast<int32_t>(p.decode_instances.size());
+    std::copy(p.decode_instances.begin(), p.decode_instances.end(), decode_instances);
+    for (int32_t r = 0; r < n_req; ++r) {
+      place_n[r] = static_cast<int32_t>(p.fill[r].size());
+      for (size_t j = 0; j < p.fill[r].size(); ++j) {
+        place_inst[r * d + j] = p.fill[r][j].first;
+        place_tok[r * d + j] = p.fill[r][j].second;
+      }
+    }
+    *ring_volume = p.ring_volume;
+  });
+}
+
+double esp_sib_prefill_time(const esp_sib_record* sib, int32_t n_rec, int32_t dop, int32_t tp,
+                            double sum_len, double sum_len_sq) {
+  double out = -1;
+  if (guarded([&] { out = make_sib(sib, n_rec).prefill_time_sums(sum_len, sum_len_sq, dop, tp); }) !=
+      ESP_OK) {
+    return -1;
+  }
+  return out;
+}
+
+double esp_sib_decode_time(const esp_sib_record* sib, int32_t n_rec, int32_t dop, int32_t tp,
+                           int32_t batch_size, int64_t resident_kv, int32_t n_masters) {
+  double out = -1;
+  if (guarded([&] {
+        out = make_sib(sib, n_rec).decode_time(batch_size, resident_kv, dop, tp, n_masters);
+      }) != ESP_OK) {
+    return -1;
+  }
+  return out;
+}
+
+int esp_plan_decode_step(const int32_t* members, int32_t d, int32_t batch_size,
+                         const int32_t* free_inst, const int64_t* free_tok, int32_t n_free,
+                         int32_t* idle_pool, int32_t* n_idle, const esp_sib_record* sib,
+                         int32_t n_rec, int32_t tp, int32_t enable_scale_up, int32_t* feasible,
+                         int32_t* masters, int32_t* n_masters, int32_t* add_instances,
+                         int32_t* n_add) {
+  return guarded([&] {
+    std::vector<int32_t> idle(idle_pool, idle_pool + *n_idle);
+    auto plan = esp::plan_decode_step(std::vector<int32_t>(members, members + d), batch_size,
+                                      free_map(free_inst, free_tok, n_free), idle,
+                                      make_sib(sib, n_rec), tp, enable_scale_up != 0);
+    *feasible = plan.feasible ? 1 : 0;
+    *n_masters = static_cast<int32_t>(plan.masters.size());
+    std::copy(plan.masters.begin(), plan.masters.end(), masters);
+    *n_add = static_cast<int32_t>(plan.add_instances.size());
+    std::copy(plan.add_instances.begin(), plan.add_instances.end(), add_instances);
+    *n_idle = static_cast<int32_t>(idle.size());
+    std::copy(idle.begin(), idle.end(), idle_pool);
+  });
+}
+
+int esp_assign_masters(const int64_t* batch, int32_t b, const int32_t* masters, int32_t k,
+                       int32_t* master_of) {
+  return guarded([&] {
+    auto a = esp::assign_masters(std::vector<int64_t>(batch, batch + b),
+                                 std::vector<int32_t>(masters, masters + k));
+    std::map<int64_t, int32_t> of;
+    for (const auto& [m, rs] : a) {
+      for (int64_t r : rs) of[r] = m;
+    }
+    for (int32_t i = 0; i < b; ++i) master_of[i] = of[batch[i]];
+  });
+}
+
+int esp_decode_step_comm(int32_t d, const int32_t* masters, const int32_t* counts,
+                         const int64_t* master_free, int32_t k, int64_t* query_volume,
+                         int64_t* overlappable_volume, int32_t* full_master) {
+  *full_master = -1;
+  return guarded([&] {
+    std::map<int32_t, std::vector<int64_t>> assign;
+    std::map<int32_t, int64_t> free;
+    int64_t next = 0;
+    for (int32_t i = 0; i < k; ++i) {
+      auto& v = assign[masters[i]];
+      for (int32_t j = 0; j < counts[i]; ++j) v.push_back(next++);
+      free[masters[i]] = master_free[i];
+    }
+    try {
+      auto c = esp::decode_step_comm(d, assign, free);
+      *query_volume = c.query_volume;
+      *overlappable_volume = c.overlappable_volume;
+    } catch (const esp::MasterFullError& e) {
+      *full_master = e.instance;
+      throw;
+    }
+  });
+}
+
+int esp_build_ring_schedule(const int32_t* group, const int64_t* segment_tokens, int32_t d,
+                            int32_t* from, int32_t* to, int64_t* volume,
+                            int64_t* total_comm_volume) {
+  return guarded([&] {
+    if (d < 0) throw esp::InfeasiblePlanError("negative ring width");
+    auto ring = esp::build_ring_schedule(std::vector<int32_t>(group, group + d),
+                                         std::vector<int64_t>(segment_tokens, segment_tokens + d));
+    for (int32_t r = 0; r + 1 < d; ++r) {
+      for (int32_t i = 0; i < d; ++i) {
+        const auto& t = ring.rounds[r][i];
+        from[r * d + i] = t.from;
+        to[r * d + i] = t.to;
+        volume[r * d + i] = t.volume;
+      }
+    }
+    *total_comm_volume = ring.total_comm_volume();
+  });
+}
+
+int esp_proactive_scale_down(const int32_t* ring, const int64_t* segment_tokens, int32_t d,
+                             const int32_t* sources, int32_t n_sources, const int32_t* targets,
+                             int32_t n_targets, const int32_t* target_inst,
+                             const int64_t* target_tok, int32_t n_target,
+                             const int32_t* free_inst, const int64_t* free_tok, int32_t n_free,
+                             int64_t* extra_migration_volume,
+                             int64_t* transient_buffer_tokens) {
+  return guarded([&] {
+    auto sched = esp::build_ring_schedule(std::vector<int32_t>(ring, ring + d),
+                                          std::vector<int64_t>(segment_tokens, segment_tokens + d));
+    esp::FillOrder tp;
+    for (int32_t i = 0; i < n_target; ++i) tp.emplace_back(target_inst[i], target_tok[i]);
+    auto r = esp::proactive_scale_down(sched, std::vector<int32_t>(sources, sources + n_sources),
+                                       std::vector<int32_t>(targets, targets + n_targets), tp,
+                                       free_map(free_inst, free_tok, n_free));
+    *extra_migration_volume = r.extra_migration_volume;
+    *transient_buffer_tokens = r.transient_buffer_tokens;
+  });
+}
+
+int esp_reactive_migrate(const int32_t* sources, int32_t n_sources, const int32_t* targets,
+                         int32_t n_targets, int64_t total_tokens, const int32_t* free_inst,
+                         const int64_t* free_tok, int32_t n_free, int32_t* feasible,
+                         int32_t* blocked_instance, int64_t* per_source_headroom,
+                         int32_t* final_inst, int64_t* final_tok, int32_t* n_final,
+                         int64_t* migration_volume) {
+  return guarded([&] {
+    auto r = esp::reactive_migrate(free_map(free_inst, free_tok, n_free),
+                                   std::vector<int32_t>(sources, sources + n_sources),
+                                   std::vector<int32_t>(targets, targets + n_targets),
+                                   total_tokens);
+    *feasible = r.feasible ? 1 : 0;
+    *blocked_instance = r.blocked_instance;
+    *per_source_headroom = r.per_source_headroom;
+    *migration_volume = r.migration_volume;
+    int32_t n = 0;
+    for (const auto& [i, t] : r.final_placement) {
+      final_inst[n] = i;
+      final_tok[n] = t;
+      ++n;
+    }
+    *n_final = n;
+  });
+}
+
+// ---- runtime -------------------------------------------------------------------
+int esp_runtime_create(const esp_model_config* cfg, int32_t n_instances,
+                       const int32_t* instance_device, int64_t kv_capacity_tokens,
+                       esp_runtime** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto* rt = new esp_runtime{nullptr};
+    try {
+      rt->impl = new esp::Runtime(*cfg, n_instances, instance_device, kv_capacity_tokens);
+    } catch (...) {
+      delete rt;
+      throw;
+    }
+    *out = rt;
+  });
+}
+
+void esp_runtime_destroy(esp_runtime* rt) {
+  if (!rt) return;
+  delete rt->impl;
+  delete rt;
+}
+
+int esp_instance_info(const esp_runtime* rt, int32_t instance, int64_t* capacity,
+                      int64_t* used) {
+  return guarded([&] { rt->impl->instance_info(instance, capacity, used); });
+}
+
+int esp_prefill(esp_runtime* rt, const esp_prefill_args* args) {
+  return guarded([&] { rt->impl->prefill(*args); });
+}
+
+int esp_decode_step(esp_runtime* rt, const esp_decode_args* args) {
+  return guarded([&] { rt->impl->decode_step(*args); });
+}
+
+int esp_move_kv(esp_runtime* rt, int64_t request, int32_t from, int32_t to, int64_t tokens) {
+  return guarded([&] { rt->impl->move_kv(request, from, to, tokens); });
+}
+
+int esp_free_request(esp_runtime* rt, int64_t request) {
+  return guarded([&] { rt->impl->free_request(request); });
+}
+
+int esp_query_placement(const esp_runtime* rt, int64_t request, int32_t* inst, int64_t* tokens,
+                        int32_t cap, int32_t* n) {
+  return guarded([&] { rt->impl->query_placement(request, inst, tokens, cap, n); });
+}
+
+int esp_check_conservation(esp_runtime* rt) {
+  return guarded([&] { rt->impl->check_conservation(); });
+}
+
+int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int32_t cap,
+                       int32_t* n) {
+  return guarded([&] { rt->impl->request_tokens(request, out, cap, n); });
+}
+
+int esp_dump_profiles(const esp_runtime* rt, const char* path) {
+  return guarded([&] { rt->impl->dump_profiles(path); });
+}
+
+int64_t esp_launch_count(const esp_runtime* rt) {
+  (void)rt;
+  return esp::k::launch_count();
+}
+
+// ---- kernel-level hooks ---------------------------------------------------------
+int esp_k_gemm(const void* A, const void* B, void* D, int32_t M, int32_t N, int32_t K,
+               int32_t epilogue, void* stream) {
+  return guarded([&] {
+    esp::k::GemmEpilogue ep;
+    if (epilogue == 0) ep.kind = esp::k::kEpiStore;
+    else if (epilogue == 1) ep.kind = esp::k::kEpiResidual;
+    else if (epilogue == 2) ep.kind = esp::k::kEpiStoreF32;
+    else if (epilogue == 3) ep.kind = esp::k::kEpiSiluMul;
+    else throw esp::ConfigError("unknown epilogue");
+    ep.out = D;
+    ep.ldo = epilogue == 3 ? N / 2 : N;
+    esp::k::gemm(static_cast<const esp::k::bf16*>(A), K, static_cast<const esp::k::bf16*>(B), K,
+                 M, N, K, ep, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw esp::CudaError(cudaGetErrorString(e));
+  });
+}
+
+int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
+                         const void* const* kv_k, const void* const* kv_v, const int32_t* kv_len,
+                         const int32_t* origin, void* out, int32_t heads, int32_t head_dim,
+                         void* stream) {
+  // Test hook: stages q and the d KV blocks into one buffer (rows: q, then
+  // block 0..d-1) so the production kernel runs on exactly its layout.
+  return guarded([&] {
+    if (d < 1 || d > esp::k::kMaxRounds) throw esp::ConfigError("d out of range");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t hidden = static_cast<int64_t>(heads) * head_dim;
+    int64_t rows = q_len;
+    std::vector<int32_t> row0(static_cast<size_t>(d));
+    for (int r = 0; r < d; ++r) {
+      row0[r] = static_cast<int32_t>(rows);
+      rows += kv_len[r];
+    }
+    using esp::k::bf16;
+    bf16 *Q = nullptr, *K = nullptr, *V = nullptr, *O = nullptr;
+    const size_t bytes = static_cast<size_t>(rows) * hidden * 2;
+    cudaMalloc(&Q, bytes);
+    cudaMalloc(&K, bytes);
+    cudaMalloc(&V, bytes);
+    cudaMalloc(&O, bytes);
+    cudaMemcpyAsync(Q, q, static_cast<size_t>(q_len) * hidden * 2, cudaMemcpyDeviceToDevice, s);
+    for (int r = 0; r < d; ++r) {
+      cudaMemcpyAsync(K + row0[r] * hidden, kv_k[r], static_cast<size_t>(kv_len[r]) * hidden * 2,
+                      cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(V + row0[r] * hidden, kv_v[r], static_cast<size_t>(kv_len[r]) * hidden * 2,
+                      cudaMemcpyDeviceToDevice, s);
+    }
+    esp::k::RingSegment sg{};
+    sg.q_row0 = 0;
+    sg.q_len = q_len;
+    sg.n_rounds = d;
+    for (int r = 0; r < d; ++r) {
+      sg.kv_row0[r] = row0[r];
+      sg.kv_len[r] = kv_len[r];
+      sg.shift[r] = origin[r] > pos_i ? 1 : 0;
+    }
+    std::vector<int32_t> work;
+    for (int qt = 0; qt < esp::k::q_tiles(q_len); ++qt) {
+      for (int h = 0; h < heads; ++h) {
+        work.push_back(0);
+        work.push_back((qt << 8) | h);
+      }
+    }
+    esp::k::RingSegment* dseg = nullptr;
+    int32_t* dwork = nullptr;
+    cudaMalloc(&dseg, sizeof(sg));
+    cudaMalloc(&dwork, work.size() * 4);
+    cudaMemcpyAsync(dseg, &sg, sizeof(sg), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(dwork, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s);
+    esp::k::ring_attention(Q, K, V, O, static_cast<int>(rows), heads, head_dim, dseg, 1, dwork,
+                           static_cast<int>(work.size() / 2),
+                           1.0f / std::sqrt(static_cast<float>(head_dim)), s);
+    cudaMemcpyAsync(out, O, static_cast<size_t>(q_len) * hidden * 2, cudaMemcpyDeviceToDevice, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(Q);
+    cudaFree(K);
+    cudaFree(V);
+    cudaFree(O);
+    cudaFree(dseg);
+    cudaFree(dwork);
+    if (e != cudaSuccess) throw esp::CudaError(cudaGetErrorString(e));
+  });
+}
+
+int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_slab,
+                           const void* const* v_slab, const int32_t* const* slot_idx,
+                           const int32_t* n_slots, const int32_t* chunk_req, int32_t n_chunks,
+                           void* out, int32_t heads, int32_t head_dim, void* stream) {
+  return guarded([&] {
+    if (n_chunks > esp::k::kMaxSlabs) throw esp::ConfigError("too many chunks for the hook");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    esp::k::DecodeSlabs slabs{};
+    std::vector<esp::k::DecodeChunk> ch;
+    std::vector<std::pair<int32_t, int>> by_row;
+    for (int c = 0; c < n_chunks; ++c) by_row.emplace_back(chunk_req[c], c);
+    std::stable_sort(by_row.begin(), by_row.end());
+    std::vector<int32_t> row_start(static_cast<size_t>(batch) + 1, 0);
+    for (const auto& [row, c] : by_row) {
+      slabs.k[c] = static_cast<const esp::k::bf16*>(k_slab[c]);
+      slabs.v[c] = static_cast<const esp::k::bf16*>(v_slab[c]);
+      ch.push_back({slot_idx[c], n_slots[c], row, c, 0});
+      row_start[row + 1]++;
+    }
+    for (int r = 0; r < batch; ++r) row_start[r + 1] += row_start[r];
+    esp::k::DecodeChunk* dch = nullptr;
+    int32_t* drs = nullptr;
+    float *po = nullptr, *pml = nullptr;
+    cudaMalloc(&dch, ch.size() * sizeof(esp::k::DecodeChunk) + 16);
+    cudaMalloc(&drs, row_start.size() * 4);
+    cudaMalloc(&po, static_cast<size_t>(n_chunks) * heads * head_dim * 4 + 16);
+    cudaMalloc(&pml, static_cast<size_t>(n_chunks) * heads * 2 * 4 + 16);
+    cudaMemcpyAsync(dch, ch.data(), ch.size() * sizeof(esp::k::DecodeChunk), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(drs, row_start.data(), row_start.size() * 4, cudaMemcpyHostToDevice, s);
+    const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
+    esp::k::decode_attention(static_cast<const esp::k::bf16*>(q), dch, n_chunks, slabs, heads,
+                             head_dim, scale, po, pml, s);
+    esp::k::decode_combine(po, pml, drs, batch, heads, head_dim, static_cast<esp::k::bf16*>(out), s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(dch);
+    cudaFree(drs);
+    cudaFree(po);
+    cudaFree(pml);
+    if (e != cudaSuccess) throw esp::CudaError(cudaGetErrorString(e));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,955 @@
+// ESP runtime / executor. See runtime.hpp and include/esp_abi.h.
+//
+// Data layout in HBM (per device):
+//   weights  : embed [V x H], per layer Wqkv [3H x H] (q|k|v rows), Wo [H x H],
+//              Wgu [2F x H] (128-row blocks: 64 gate rows, 64 up rows),
+//              Wd [H x F], RMSNorm gammas [H]; final norm; LM head [V x H].
+//   KV slabs : per instance K and V, [layers][capacity][H] bf16 — one token
+//              slot is one page (token-granular PagedAttention),
+//              8 KiB per layer per K/V row at LWM-7B shape.
+//   prefill  : ring stripe buffers Q/K/V/attn [S x H] in ring-position-major,
+//              request-major, stripe order (the O(bsh/d) circulating buffer of
+//              PAPER.md:264 for all co-located ring positions).
+#include "runtime.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <numeric>
+#include <set>
+#include <sstream>
+
+#include "../kernels/kernels.h"
+#include "../kernels/synthetic.h"
+
+namespace esp {
+
+using k::bf16;
+
+struct LayerW {
+  bf16 *wqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;
+  bf16 *norm1 = nullptr, *norm2 = nullptr;
+};
+
+struct DeviceCtx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bf16* embed = nullptr;
+  bf16* lm_head = nullptr;
+  bf16* final_norm = nullptr;
+  std::vector<LayerW> layers;
+  float2* rope = nullptr;
+  int rope_max = 0;
+  std::vector<InstanceId> slabs;  // slab index -> instance id
+  // activations / scratch
+  DevBuf x, xn, q, kb, vb, attn, h, logits, tok, pos, rinst, rslot, segs, work, last_rows,
+      out_tok, chunks, row_start, part_o, part_ml, counts, result;
+  std::vector<void*> weight_allocs;
+};
+
+namespace {
+
+constexpr int kDecodeChunk = 256;
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    cuda_ok(cudaSetDevice(d), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+void Runtime::check_cuda(const char* what) { cuda_ok(cudaGetLastError(), what); }
+
+template <typename T>
+T* Runtime::scratch(DevBuf& b, size_t n) {
+  const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
+  if (b.bytes < bytes) {
+    if (b.ptr) cuda_ok(cudaFree(b.ptr), "cudaFree");
+    b.ptr = nullptr;
+    size_t want = std::max(bytes, b.bytes * 3 / 2);
+    cuda_ok(cudaMalloc(&b.ptr, want), "cudaMalloc(scratch)");
+    b.bytes = want;
+  }
+  return static_cast<T*>(b.ptr);
+}
+
+Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
+                 int64_t kv_capacity)
+    : cfg_(cfg) {
+  if (n_instances <= 0) throw ConfigError("need at least one instance");
+  if (cfg.layers <= 0 || cfg.hidden <= 0 || cfg.heads <= 0 || cfg.head_dim <= 0 ||
+      cfg.ffn <= 0 || cfg.vocab <= 0) {
+    throw ConfigError("model config fields must be positive");
+  }
+  if (cfg.heads * cfg.head_dim != cfg.hidden) throw ConfigError("hidden != heads * head_dim");
+  instances_.resize(static_cast<size_t>(n_instances));
+  for (int i = 0; i < n_instances; ++i) instances_[i].id = i;
+
+  if (devices == nullptr) {  // placement-only runtime: counters and page tables
+    if (kv_capacity <= 0) throw ConfigError("placement-only runtime needs kv_capacity > 0");
+    for (auto& in : instances_) in.capacity = kv_capacity;
+  } else {
+    if (cfg.head_dim != 64 && cfg.head_dim != 128) throw ConfigError("head_dim must be 64 or 128");
+    if (cfg.hidden % 256 != 0 || cfg.ffn % 64 != 0 || cfg.vocab % 128 != 0) {
+      throw ConfigError("hidden % 256, ffn % 64 and vocab % 128 must be 0");
+    }
+    int ndev = 0;
+    cuda_ok(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    std::map<int, DeviceCtx*> by_dev;
+    for (int i = 0; i < n_instances; ++i) {
+      const int d = devices[i];
+      if (d < 0 || d >= ndev) throw ConfigError("instance device ordinal out of range");
+      if (!by_dev.count(d)) {
+        devices_.push_back(std::make_unique<DeviceCtx>());
+        devices_.back()->device = d;
+        by_dev[d] = devices_.back().get();
+      }
+      DeviceCtx* dc = by_dev[d];
+      if (static_cast<int>(dc->slabs.size()) >= k::kMaxSlabs) {
+        throw ConfigError("too many instances on one device");
+      }
+      instances_[i].device = d;
+      instances_[i].slab = static_cast<int>(dc->slabs.size());
+      dc->slabs.push_back(i);
+    }
+    const int64_t bpt = kv_bytes_per_token(cfg.layers, cfg.hidden, cfg.heads, 2);
+    for (auto& dcp : devices_) {
+      DeviceCtx& dc = *dcp;
+      init_device(dc);
+      DeviceGuard g(dc.device);
+      int64_t cap = kv_capacity;
+      if (cap <= 0) {
+        size_t free_b = 0, total_b = 0;
+        cuda_ok(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        const int64_t reserve = static_cast<int64_t>(12) << 30;  // prefill activations
+        const int64_t avail = static_cast<int64_t>(free_b) - reserve;
+        cap = avail / (static_cast<int64_t>(dc.slabs.size()) * bpt);
+        if (cap <= 0) throw ConfigError("no HBM left for KV slabs");
+      }
+      for (InstanceId id : dc.slabs) {
+        InstanceRec& in = instances_[id];
+        in.capacity = cap;
+        const size_t bytes = static_cast<size_t>(cap) * static_cast<size_t>(bpt) / 2;
+        cuda_ok(cudaMalloc(&in.k_slab, bytes), "cudaMalloc(K slab)");
+        cuda_ok(cudaMalloc(&in.v_slab, bytes), "cudaMalloc(V slab)");
+      }
+    }
+  }
+  for (auto& in : instances_) {
+    if (in.capacity > INT32_MAX) throw ConfigError("kv_capacity exceeds int32 slot ids");
+    in.free_stack.resize(static_cast<size_t>(in.capacity));
+    // back() is slot 0: fresh slots come out in ascending order.
+    for (int64_t s = 0; s < in.capacity; ++s) {
+      in.free_stack[static_cast<size_t>(s)] = static_cast<int32_t>(in.capacity - 1 - s);
+    }
+  }
+}
+
+Runtime::~Runtime() {
+  for (auto& [id, r] : requests_) {
+    for (auto& [i, pl] : r.pages) {
+      if (pl.dev) cudaFree(pl.dev);
+    }
+  }
+  for (auto& in : instances_) {
+    if (in.k_slab) cudaFree(in.k_slab);
+    if (in.v_slab) cudaFree(in.v_slab);
+  }
+  for (auto& dcp : devices_) {
+    DeviceCtx& dc = *dcp;
+    cudaSetDevice(dc.device);
+    for (void* p : dc.weight_allocs) cudaFree(p);
+    DevBuf* bufs[] = {&dc.x, &dc.xn, &dc.q, &dc.kb, &dc.vb, &dc.attn, &dc.h, &dc.logits,
+                      &dc.tok, &dc.pos, &dc.rinst, &dc.rslot, &dc.segs, &dc.work,
+                      &dc.last_rows, &dc.out_tok, &dc.chunks, &dc.row_start, &dc.part_o,
+                      &dc.part_ml, &dc.counts, &dc.result};
+    for (DevBuf* b : bufs) {
+      if (b->ptr) cudaFree(b->ptr);
+    }
+    if (dc.rope) cudaFree(dc.rope);
+    if (dc.e0) cudaEventDestroy(dc.e0);
+    if (dc.e1) cudaEventDestroy(dc.e1);
+    if (dc.stream) cudaStreamDestroy(dc.stream);
+  }
+}
+
+void Runtime::init_device(DeviceCtx& dc) {
+  DeviceGuard g(dc.device);
+  cuda_ok(cudaStreamCreateWithFlags(&dc.stream, cudaStreamNonBlocking), "stream");
+  cuda_ok(cudaEventCreate(&dc.e0), "event");
+  cuda_ok(cudaEventCreate(&dc.e1), "event");
+  const int64_t H = cfg_.hidden, F = cfg_.ffn, V = cfg_.vocab;
+  auto alloc = [&](int64_t n) {
+    void* p = nullptr;
+    cuda_ok(cudaMalloc(&p, static_cast<size_t>(n) * sizeof(bf16)), "cudaMalloc(weights)");
+    dc.weight_allocs.push_back(p);
+    return static_cast<bf16*>(p);
+  };
+  const uint64_t seed = cfg_.weight_seed;
+  cudaStream_t s = dc.stream;
+  dc.embed = alloc(V * H);
+  k::init_weight(dc.embed, V, H, seed, k::kTensorEmbed, 0, 0, s);
+  dc.lm_head = alloc(V * H);
+  k::init_weight(dc.lm_head, V, H, seed, k::kTensorLmHead, 0, 0, s);
+  dc.final_norm = alloc(H);
+  k::fill_bf16(dc.final_norm, H, 1.0f, s);
+  dc.layers.resize(static_cast<size_t>(cfg_.layers));
+  for (int l = 0; l < cfg_.layers; ++l) {
+    LayerW& w = dc.layers[l];
+    w.wqkv = alloc(3 * H * H);
+    k::init_weight(w.wqkv, 3 * H, H, seed, k::kTensorQ, l, 1, s);
+    w.wo = alloc(H * H);
+    k::init_weight(w.wo, H, H, seed, k::kTensorO, l, 0, s);
+    w.wgu = alloc(2 * F * H);
+    k::init_weight(w.wgu, 2 * F, H, seed, k::kTensorGate, l, 2, s);
+    w.wd = alloc(H * F);
+    k::init_weight(w.wd, H, F, seed, k::kTensorDown, l, 0, s);
+    w.norm1 = alloc(H);
+    k::fill_bf16(w.norm1, H, 1.0f, s);
+    w.norm2 = alloc(H);
+    k::fill_bf16(w.norm2, H, 1.0f, s);
+  }
+  check_cuda("init weights");
+  cuda_ok(cudaStreamSynchronize(s), "init weights sync");
+}
+
+InstanceRec& Runtime::inst(InstanceId i) {
+  if (i < 0 || i >= static_cast<int>(instances_.size())) {
+    throw InternalError("placement names unknown instance");
+  }
+  return instances_[static_cast<size_t>(i)];
+}
+const InstanceRec& Runtime::inst(InstanceId i) const {
+  return const_cast<Runtime*>(this)->inst(i);
+}
+RequestRec& Runtime::req(RequestId r) {
+  auto it = requests_.find(r);
+  if (it == requests_.end()) throw InternalError("unknown request " + std::to_string(r));
+  return it->second;
+}
+const RequestRec& Runtime::req(RequestId r) const { return const_cast<Runtime*>(this)->req(r); }
+
+std::vector<int32_t> Runtime::take_slots(InstanceRec& in, int64_t n) {
+  if (in.used + n > in.capacity || static_cast<int64_t>(in.free_stack.size()) < n) {
+    throw CapacityError(in.id, "instance " + std::to_string(in.id) + " lacks free slots");
+  }
+  std::vector<int32_t> out(in.free_stack.end() - n, in.free_stack.end());
+  std::reverse(out.begin(), out.end());
+  in.free_stack.resize(in.free_stack.size() - static_cast<size_t>(n));
+  in.used += n;
+  return out;
+}
+
+void Runtime::release_slots(InstanceRec& in, const std::vector<int32_t>& s) {
+  if (in.used < static_cast<int64_t>(s.size())) {
+    throw InternalError("freeing more KV than instance " + std::to_string(in.id) + " holds");
+  }
+  for (auto it = s.rbegin(); it != s.rend(); ++it) in.free_stack.push_back(*it);
+  in.used -= static_cast<int64_t>(s.size());
+}
+
+void Runtime::sync_pages(PageList& pl, cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(pl.slots.size());
+  if (pl.dev_n == n && pl.dev) return;
+  if (pl.dev_cap < n || !pl.dev) {
+    int64_t cap = std::max<int64_t>({n, 64, pl.dev_cap * 2});
+    int32_t* p = nullptr;
+    cuda_ok(cudaMalloc(&p, static_cast<size_t>(cap) * sizeof(int32_t)), "cudaMalloc(pages)");
+    if (pl.dev) {
+      cuda_ok(cudaStreamSynchronize(s), "sync pages");
+      cudaFree(pl.dev);
+    }
+    pl.dev = p;
+    pl.dev_cap = cap;
+    pl.dev_n = 0;
+  }
+  if (pl.dev_n > n) pl.dev_n = 0;  // shrunk: rewrite
+  cuda_ok(cudaMemcpyAsync(pl.dev + pl.dev_n, pl.slots.data() + pl.dev_n,
+                          static_cast<size_t>(n - pl.dev_n) * sizeof(int32_t),
+                          cudaMemcpyHostToDevice, s),
+          "upload pages");
+  pl.dev_n = n;
+}
+
+DeviceCtx& Runtime::device_of(const std::vector<InstanceId>& ids, const char* what) {
+  if (devices_.empty()) {
+    throw NoDeviceError(std::string(what) + " needs a device runtime (placement-only)");
+  }
+  int dev = -1;
+  for (InstanceId i : ids) {
+    const int d = inst(i).device;
+    if (dev >= 0 && d != dev) {
+      throw ConfigError(std::string(what) +
+                        ": instances on different devices are not supported in this build");
+    }
+    dev = d;
+  }
+  for (auto& dcp : devices_) {
+    if (dcp->device == dev) return *dcp;
+  }
+  throw InternalError("device context missing");
+}
+
+// ---- prefill -------------------------------------------------------------------
+void Runtime::prefill(const esp_prefill_args& a) {
+  const int n = a.n_requests, d = a.dop;
+  if (n <= 0 || d <= 0) throw InternalError("prefill plan without requests or instances");
+  if (!a.request_ids || !a.input_lens || !a.ring || !a.retain_n || !a.retain_instance ||
+      !a.retain_tokens) {
+    throw ConfigError("prefill: null argument");
+  }
+  if (d > k::kMaxRounds) throw ConfigError("prefill: dop exceeds 8");
+  std::vector<InstanceId> ring(a.ring, a.ring + d);
+  {
+    std::set<InstanceId> seen;
+    for (InstanceId i : ring) {
+      inst(i);
+      if (!seen.insert(i).second) throw InternalError("ring repeats an instance");
+    }
+  }
+  // Validate the resting placement (engine.cpp:327-345) before touching any
+  // counter: the allocation is atomic like KvPool::allocate (cluster.cpp:88-99).
+  std::map<InstanceId, int64_t> need;
+  int64_t off = 0;
+  for (int r = 0; r < n; ++r) {
+    const RequestId rid = a.request_ids[r];
+    if (requests_.count(rid) && requests_.at(rid).kv_tokens() > 0) {
+      throw InternalError("prefill plan names a request that already holds KV");
+    }
+    if (a.input_lens[r] <= 0) throw InternalError("prefill of an empty request");
+    int64_t tot = 0;
+    for (int p = 0; p < a.retain_n[r]; ++p) {
+      const int64_t t = a.retain_tokens[off + p];
+      if (t < 0) throw InternalError("negative placement entry");
+      inst(a.retain_instance[off + p]);
+      need[a.retain_instance[off + p]] += t;
+      tot += t;
+    }
+    off += a.retain_n[r];
+    if (tot != a.input_lens[r]) throw InternalError("prefill placement does not cover the input");
+  }
+  for (const auto& [i, t] : need) {
+    if (inst(i).used + t > inst(i).capacity) {
+      throw CapacityError(i, "prefill placement overflows instance " + std::to_string(i));
+    }
+  }
+  if (!devices_.empty() && !a.tokens) throw ConfigError("prefill: tokens required on a device runtime");
+  DeviceCtx* dcp = devices_.empty() ? nullptr : &device_of(ring, "prefill");
+  if (dcp) {
+    for (const auto& [i, t] : need) {
+      if (inst(i).device != dcp->device) {
+        throw ConfigError("prefill: resting instance on another device is not supported");
+      }
+    }
+  }
+
+  // Allocate resting slots; tok_inst/tok_slot give each prompt token's page.
+  std::vector<std::vector<int32_t>> tok_slab(static_cast<size_t>(n)), tok_slot(static_cast<size_t>(n));
+  off = 0;
+  int64_t tok_off = 0;
+  std::vector<int64_t> tok_base(static_cast<size_t>(n));
+  for (int r = 0; r < n; ++r) {
+    const RequestId rid = a.request_ids[r];
+    RequestRec& rr = requests_[rid];
+    rr.id = rid;
+    rr.input_len = a.input_lens[r];
+    rr.tokens.clear();
+    if (a.tokens) rr.tokens.assign(a.tokens + tok_off, a.tokens + tok_off + a.input_lens[r]);
+    tok_base[r] = tok_off;
+    tok_off += a.input_lens[r];
+    auto& ts = tok_slab[r];
+    auto& tl = tok_slot[r];
+    ts.reserve(static_cast<size_t>(rr.input_len));
+    tl.reserve(static_cast<size_t>(rr.input_len));
+    for (int p = 0; p < a.retain_n[r]; ++p) {
+      const InstanceId i = a.retain_instance[off + p];
+      const int64_t t = a.retain_tokens[off + p];
+      if (t == 0) continue;
+      InstanceRec& in = inst(i);
+      std::vector<int32_t> slots = take_slots(in, t);
+      PageList& pl = rr.pages[i];
+      pl.slots.insert(pl.slots.end(), slots.begin(), slots.end());
+      for (int32_t s : slots) {
+        ts.push_back(in.slab);
+        tl.push_back(s);
+      }
+    }
+    off += a.retain_n[r];
+  }
+  if (!dcp) return;  // placement-only: page tables are the whole effect
+
+  DeviceCtx& dc = *dcp;
+  DeviceGuard g(dc.device);
+  cudaStream_t s = dc.stream;
+  const int H = cfg_.hidden;
+
+  // Stripe rows: ring-position-major, then request, then stripe index
+  // (token t of request r lives at position t mod d, stripe index t / d).
+  std::vector<std::vector<int32_t>> row0(static_cast<size_t>(d), std::vector<int32_t>(static_cast<size_t>(n)));
+  std::vector<int32_t> h_tok, h_pos, h_inst, h_slot;
+  int rows = 0;
+  for (int i = 0; i < d; ++i) {
+    for (int r = 0; r < n; ++r) {
+      row0[i][r] = rows;
+      const int64_t len = a.input_lens[r];
+      for (int64_t t = i; t < len; t += d) {
+        h_tok.push_back(a.tokens[tok_base[r] + t]);
+        h_pos.push_back(static_cast<int32_t>(t));
+        h_inst.push_back(tok_slab[r][static_cast<size_t>(t)]);
+        h_slot.push_back(tok_slot[r][static_cast<size_t>(t)]);
+        ++rows;
+      }
+    }
+  }
+  auto stripe_len = [&](int i, int r) -> int32_t {
+    const int64_t len = a.input_lens[r];
+    return len > i ? static_cast<int32_t>((len - i + d - 1) / d) : 0;
+  };
+  // Ring segments: position i meets, in round rd, the block of origin
+  // (i - rd) mod d (build_ring_schedule, esp_mechanics.cpp:59-68).
+  std::vector<k::RingSegment> segs;
+  std::vector<int32_t> work;
+  std::vector<std::pair<int64_t, int>> order;  // (cost, work index) for LPT order
+  for (int i = 0; i < d; ++i) {
+    for (int r = 0; r < n; ++r) {
+      const int32_t ql = stripe_len(i, r);
+      if (ql == 0) continue;
+      k::RingSegment sg{};
+      sg.q_row0 = row0[i][r];
+      sg.q_len = ql;
+      sg.n_rounds = d;
+      for (int rd = 0; rd < d; ++rd) {
+        const int o = RingSchedule::origin(i, rd, d);
+        sg.kv_row0[rd] = row0[o][r];
+        sg.kv_len[rd] = stripe_len(o, r);
+        sg.shift[rd] = o > i ? 1 : 0;
+      }
+      const int seg_idx = static_cast<int>(segs.size());
+      segs.push_back(sg);
+      for (int qt = 0; qt < k::q_tiles(ql); ++qt) {
+        int64_t cost = 0;
+        for (int rd = 0; rd < d; ++rd) {
+          const int64_t vis = std::min<int64_t>(sg.kv_len[rd],
+                                                std::min(qt * 128 + 127, ql - 1) - sg.shift[rd] + 1);
+          cost += vis > 0 ? (vis + 127) / 128 : 0;
+        }
+        for (int hd = 0; hd < cfg_.heads; ++hd) {
+          order.emplace_back(cost, static_cast<int>(work.size() / 2));
+          work.push_back(seg_idx);
+          work.push_back((qt << 8) | hd);
+        }
+      }
+    }
+  }
+  // Longest work first (persistent CTAs take items round-robin).
+  std::stable_sort(order.begin(), order.end(),
+                   [](const auto& x, const auto& y) { return x.first > y.first; });
+  std::vector<int32_t> work_sorted;
+  work_sorted.reserve(work.size());
+  for (const auto& o : order) {
+    work_sorted.push_back(work[2 * o.second]);
+    work_sorted.push_back(work[2 * o.second + 1]);
+  }
+
+  // RoPE table covering every position of the batch.
+  int64_t max_len = 0;
+  for (int r = 0; r < n; ++r) max_len = std::max(max_len, a.input_lens[r]);
+  if (dc.rope_max < max_len) {
+    int want = 4096;
+    while (want < max_len) want *= 2;
+    if (dc.rope) cudaFree(dc.rope);
+    cuda_ok(cudaMalloc(&dc.rope, static_cast<size_t>(want) * cfg_.head_dim / 2 * sizeof(float2)),
+            "cudaMalloc(rope)");
+    k::rope_table(dc.rope, want, cfg_.head_dim, cfg_.rope_theta, s);
+    dc.rope_max = want;
+  }
+
+  int32_t* d_tok = scratch<int32_t>(dc.tok, rows);
+  int32_t* d_pos = scratch<int32_t>(dc.pos, rows);
+  int32_t* d_inst = scratch<int32_t>(dc.rinst, rows);
+  int32_t* d_slot = scratch<int32_t>(dc.rslot, rows);
+  k::RingSegment* d_segs = scratch<k::RingSegment>(dc.segs, segs.size());
+  int32_t* d_work = scratch<int32_t>(dc.work, work_sorted.size());
+  cuda_ok(cudaMemcpyAsync(d_tok, h_tok.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_pos, h_pos.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_inst, h_inst.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_slot, h_slot.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(k::RingSegment),
+                          cudaMemcpyHostToDevice, s),
+          "h2d");
+  cuda_ok(cudaMemcpyAsync(d_work, work_sorted.data(), work_sorted.size() * 4,
+                          cudaMemcpyHostToDevice, s),
+          "h2d");
+
+  bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(rows) * H);
+  cuda_ok(cudaEventRecord(dc.e0, s), "event");
+  k::embed(d_tok, dc.embed, x, rows, H, s);
+  forward_layers_prefill(dc, rows, segs, work_sorted);
+
+  // Last prompt token of each request: position len-1 lives at ring position
+  // (len-1) mod d, stripe index (len-1) / d.
+  std::vector<int32_t> last(static_cast<size_t>(n));
+  for (int r = 0; r < n; ++r) {
+    const int64_t t = a.input_lens[r] - 1;
+    last[r] = row0[t % d][r] + static_cast<int32_t>(t / d);
+  }
+  int32_t* d_last = scratch<int32_t>(dc.last_rows, n);
+  cuda_ok(cudaMemcpyAsync(d_last, last.data(), n * 4, cudaMemcpyHostToDevice, s), "h2d");
+  bf16* xn = scratch<bf16>(dc.xn, static_cast<size_t>(std::max(rows, n)) * H);
+  k::rmsnorm(x, d_last, dc.final_norm, xn, n, H, cfg_.rms_eps, s);
+  float* logits = scratch<float>(dc.logits, static_cast<size_t>(n) * cfg_.vocab);
+  k::GemmEpilogue ep;
+  ep.kind = k::kEpiStoreF32;
+  ep.out = logits;
+  ep.ldo = cfg_.vocab;
+  k::gemm(xn, H, dc.lm_head, H, n, cfg_.vocab, H, ep, s);
+  int32_t* d_out = scratch<int32_t>(dc.out_tok, n);
+  k::argmax_rows(logits, n, cfg_.vocab, d_out, s);
+  cuda_ok(cudaEventRecord(dc.e1, s), "event");
+  check_cuda("prefill launch");
+  std::vector<int32_t> first(static_cast<size_t>(n));
+  cuda_ok(cudaMemcpyAsync(first.data(), d_out, n * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  if (a.logits_out) {
+    cuda_ok(cudaMemcpyAsync(a.logits_out, logits, static_cast<size_t>(n) * cfg_.vocab * 4,
+                            cudaMemcpyDeviceToHost, s),
+            "d2h");
+  }
+  cuda_ok(cudaStreamSynchronize(s), "prefill");
+  float ms = 0;
+  cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
+  if (a.device_ms_out) *a.device_ms_out = ms;
+  for (int r = 0; r < n; ++r) {
+    requests_[a.request_ids[r]].tokens.push_back(first[r]);
+    if (a.first_token_out) a.first_token_out[r] = first[r];
+  }
+  ProfileRec pr{d, std::vector<int64_t>(a.input_lens, a.input_lens + n), ms};
+  profiles_.push_back(std::move(pr));
+}
+
+void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
+                                     const std::vector<k::RingSegment>& segs,
+                                     const std::vector<int32_t>& work) {
+  cudaStream_t s = dc.stream;
+  const int H = cfg_.hidden, F = cfg_.ffn;
+  bf16* x = static_cast<bf16*>(dc.x.ptr);
+  bf16* xn = scratch<bf16>(dc.xn, static_cast<size_t>(rows) * H);
+  bf16* q = scratch<bf16>(dc.q, static_cast<size_t>(rows) * H);
+  bf16* kb = scratch<bf16>(dc.kb, static_cast<size_t>(rows) * H);
+  bf16* vb = scratch<bf16>(dc.vb, static_cast<size_t>(rows) * H);
+  bf16* attn = scratch<bf16>(dc.attn, static_cast<size_t>(rows) * H);
+  bf16* hbuf = scratch<bf16>(dc.h, static_cast<size_t>(rows) * F);
+  const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
+  const int n_work = static_cast<int>(work.size() / 2);
+  for (int l = 0; l < cfg_.layers; ++l) {
+    const LayerW& w = dc.layers[l];
+    k::rmsnorm(x, nullptr, w.norm1, xn, rows, H, cfg_.rms_eps, s);
+    // QKV projection; epilogue: RoPE, ring stripe write, and the proactive
+    // retention write of every token's K/V into its resting page slot.
+    k::GemmEpilogue ep;
+    ep.kind = k::kEpiQkvRope;
+    ep.q_out = q;
+    ep.k_out = kb;
+    ep.v_out = vb;
+    ep.pos = static_cast<const int32_t*>(dc.pos.ptr);
+    ep.rope = dc.rope;
+    ep.hidden = H;
+    ep.head_dim = cfg_.head_dim;
+    ep.row_inst = static_cast<const int32_t*>(dc.rinst.ptr);
+    ep.row_slot = static_cast<const int32_t*>(dc.rslot.ptr);
+    for (size_t j = 0; j < dc.slabs.size(); ++j) {
+      const InstanceRec& in = instances_[dc.slabs[j]];
+      const int64_t lo = static_cast<int64_t>(l) * in.capacity * H;
+      ep.slab_k[j] = static_cast<bf16*>(in.k_slab) + lo;
+      ep.slab_v[j] = static_cast<bf16*>(in.v_slab) + lo;
+    }
+    k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s);
+    // Striped ring attention over all d rounds.
+    k::ring_attention(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
+                      static_cast<const k::RingSegment*>(dc.segs.ptr),
+                      static_cast<int>(segs.size()), static_cast<const int32_t*>(dc.work.ptr),
+                      n_work, scale, s);
+    k::GemmEpilogue eo;
+    eo.kind = k::kEpiResidual;
+    eo.out = x;
+    eo.ldo = H;
+    k::gemm(attn, H, w.wo, H, rows, H, H, eo, s);
+    k::rmsnorm(x, nullptr, w.norm2, xn, rows, H, cfg_.rms_eps, s);
+    k::GemmEpilogue eg;
+    eg.kind = k::kEpiSiluMul;
+    eg.out = hbuf;
+    eg.ldo = F;
+    k::gemm(xn, H, w.wgu, H, rows, 2 * F, H, eg, s);
+    k::GemmEpilogue ed;
+    ed.kind = k::kEpiResidual;
+    ed.out = x;
+    ed.ldo = H;
+    k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s);
+  }
+}
+
+// ---- decode ----------------------------------------------------------------------
+void Runtime::decode_step(const esp_decode_args& a) {
+  const int b = a.batch_size;
+  if (b <= 0) throw InternalError("decode step with neither batch nor chunk");
+  if (a.n_masters <= 0 || !a.masters) throw InternalError("decode step without masters");
+  std::vector<InstanceId> members(a.members, a.members + a.n_members);
+  std::vector<InstanceId> masters(a.masters, a.masters + a.n_masters);
+  for (InstanceId m : masters) inst(m);
+  for (InstanceId m : members) inst(m);
+  std::vector<RequestId> batch(a.batch, a.batch + b);
+  for (RequestId r : batch) {
+    if (req(r).kv_tokens() == 0) throw InternalError("decode of a request without KV");
+  }
+  // Masters exactly as the engine assigns them (engine.cpp:401,
+  // esp_mechanics.cpp:220-238), then the append feasibility of
+  // decode_step_comm (esp_mechanics.cpp:240-264).
+  auto assign = assign_masters(batch, masters);
+  std::map<InstanceId, Tokens> free;
+  for (const auto& in : instances_) free[in.id] = in.capacity - in.used;
+  decode_step_comm(static_cast<int>(members.size()), assign, free);
+
+  std::map<RequestId, int32_t> in_tok;
+  for (int i = 0; i < b; ++i) {
+    RequestRec& rr = req(batch[i]);
+    if (a.in_tokens) {
+      in_tok[batch[i]] = a.in_tokens[i];
+    } else if (!rr.tokens.empty()) {
+      in_tok[batch[i]] = rr.tokens.back();
+    } else if (!devices_.empty()) {
+      throw ConfigError("decode: no token history for request");
+    }
+  }
+  // Rows ordered by master, then request id (the assignment order).
+  struct Row {
+    RequestId r;
+    InstanceId master;
+    int32_t token, pos, slot;
+  };
+  std::vector<Row> rows_v;
+  std::vector<InstanceId> involved = members;
+  for (const auto& [m, reqs] : assign) {
+    for (RequestId r : reqs) {
+      RequestRec& rr = req(r);
+      const int32_t pos = static_cast<int32_t>(rr.kv_tokens());
+      std::vector<int32_t> slot = take_slots(inst(m), 1);
+      rr.pages[m].slots.push_back(slot[0]);
+      rows_v.push_back({r, m, in_tok[r], pos, slot[0]});
+      for (const auto& kv : rr.pages) involved.push_back(kv.first);
+    }
+  }
+  if (devices_.empty()) {
+    for (const Row& rw : rows_v) {
+      if (a.in_tokens) req(rw.r).tokens.push_back(rw.token);
+    }
+    return;
+  }
+  DeviceCtx& dc = device_of(involved, "decode_step");
+  DeviceGuard g(dc.device);
+  cudaStream_t s = dc.stream;
+  const int H = cfg_.hidden, F = cfg_.ffn;
+
+  std::vector<int32_t> h_tok, h_pos, h_inst, h_slot, h_row_start;
+  std::vector<k::DecodeChunk> chunks;
+  for (int i = 0; i < b; ++i) {
+    const Row& rw = rows_v[i];
+    h_tok.push_back(rw.token);
+    h_pos.push_back(rw.pos);
+    h_inst.push_back(inst(rw.master).slab);
+    h_slot.push_back(rw.slot);
+    h_row_start.push_back(static_cast<int32_t>(chunks.size()));
+    RequestRec& rr = req(rw.r);
+    // Split-KV work: every instance holding the request's KV contributes a
+    // partial over its own slots (multi-master distributed decoding).
+    for (auto& [iid, pl] : rr.pages) {
+      if (pl.slots.empty()) continue;
+      sync_pages(pl, s);
+      const int64_t nsl = static_cast<int64_t>(pl.slots.size());
+      for (int64_t c0 = 0; c0 < nsl; c0 += kDecodeChunk) {
+        k::DecodeChunk ch{};
+        ch.slots = pl.dev + c0;
+        ch.n = static_cast<int32_t>(std::min<int64_t>(kDecodeChunk, nsl - c0));
+        ch.row = i;
+        ch.slab = inst(iid).slab;
+        chunks.push_back(ch);
+      }
+    }
+  }
+  h_row_start.push_back(static_cast<int32_t>(chunks.size()));
+  const int n_chunks = static_cast<int>(chunks.size());
+  int64_t max_pos = 0;
+  for (const Row& rw : rows_v) max_pos = std::max<int64_t>(max_pos, rw.pos + 1);
+  if (dc.rope_max < max_pos) {
+    int want = 4096;
+    while (want < max_pos) want *= 2;
+    if (dc.rope) {
+      cuda_ok(cudaStreamSynchronize(s), "sync");
+      cudaFree(dc.rope);
+    }
+    cuda_ok(cudaMalloc(&dc.rope, static_cast<size_t>(want) * cfg_.head_dim / 2 * sizeof(float2)),
+            "cudaMalloc(rope)");
+    k::rope_table(dc.rope, want, cfg_.head_dim, cfg_.rope_theta, s);
+    dc.rope_max = want;
+  }
+  int32_t* d_tok = scratch<int32_t>(dc.tok, b);
+  int32_t* d_pos = scratch<int32_t>(dc.pos, b);
+  int32_t* d_inst = scratch<int32_t>(dc.rinst, b);
+  int32_t* d_slot = scratch<int32_t>(dc.rslot, b);
+  int32_t* d_rs = scratch<int32_t>(dc.row_start, b + 1);
+  k::DecodeChunk* d_chunks = scratch<k::DecodeChunk>(dc.chunks, chunks.size());
+  cuda_ok(cudaMemcpyAsync(d_tok, h_tok.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_pos, h_pos.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_inst, h_inst.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_slot, h_slot.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_rs, h_row_start.data(), (b + 1) * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_chunks, chunks.data(), chunks.size() * sizeof(k::DecodeChunk),
+                          cudaMemcpyHostToDevice, s),
+          "h2d");
+  bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(b) * H);
+  bf16* xn = scratch<bf16>(dc.xn, static_cast<size_t>(b) * H);
+  bf16* q = scratch<bf16>(dc.q, static_cast<size_t>(b) * H);
+  bf16* attn = scratch<bf16>(dc.attn, static_cast<size_t>(b) * H);
+  bf16* hbuf = scratch<bf16>(dc.h, static_cast<size_t>(b) * F);
+  float* part_o = scratch<float>(dc.part_o, static_cast<size_t>(n_chunks) * cfg_.heads * cfg_.head_dim);
+  float* part_ml = scratch<float>(dc.part_ml, static_cast<size_t>(n_chunks) * cfg_.heads * 2);
+  const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
+
+  cuda_ok(cudaEventRecord(dc.e0, s), "event");
+  k::embed(d_tok, dc.embed, x, b, H, s);
+  for (int l = 0; l < cfg_.layers; ++l) {
+    const LayerW& w = dc.layers[l];
+    k::rmsnorm(x, nullptr, w.norm1, xn, b, H, cfg_.rms_eps, s);
+    k::GemmEpilogue ep;
+    ep.kind = k::kEpiQkvRope;
+    ep.q_out = q;
+    ep.pos = d_pos;
+    ep.rope = dc.rope;
+    ep.hidden = H;
+    ep.head_dim = cfg_.head_dim;
+    ep.row_inst = d_inst;  // append: the new token's K/V go to its master's slot
+    ep.row_slot = d_slot;
+    k::DecodeSlabs slabs{};
+    for (size_t j = 0; j < dc.slabs.size(); ++j) {
+      const InstanceRec& in = instances_[dc.slabs[j]];
+      const int64_t lo = static_cast<int64_t>(l) * in.capacity * H;
+      ep.slab_k[j] = static_cast<bf16*>(in.k_slab) + lo;
+      ep.slab_v[j] = static_cast<bf16*>(in.v_slab) + lo;
+      slabs.k[j] = ep.slab_k[j];
+      slabs.v[j] = ep.slab_v[j];
+    }
+    k::gemm(xn, H, w.wqkv, H, b, 3 * H, H, ep, s);
+    k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale, part_o,
+                        part_ml, s);
+    k::decode_combine(part_o, part_ml, d_rs, b, cfg_.heads, cfg_.head_dim, attn, s);
+    k::GemmEpilogue eo;
+    eo.kind = k::kEpiResidual;
+    eo.out = x;
+    eo.ldo = H;
+    k::gemm(attn, H, w.wo, H, b, H, H, eo, s);
+    k::rmsnorm(x, nullptr, w.norm2, xn, b, H, cfg_.rms_eps, s);
+    k::GemmEpilogue eg;
+    eg.kind = k::kEpiSiluMul;
+    eg.out = hbuf;
+    eg.ldo = F;
+    k::gemm(xn, H, w.wgu, H, b, 2 * F, H, eg, s);
+    k::GemmEpilogue ed;
+    ed.kind = k::kEpiResidual;
+    ed.out = x;
+    ed.ldo = H;
+    k::gemm(hbuf, F, w.wd, F, b, H, F, ed, s);
+  }
+  k::rmsnorm(x, nullptr, dc.final_norm, xn, b, H, cfg_.rms_eps, s);
+  float* logits = scratch<float>(dc.logits, static_cast<size_t>(b) * cfg_.vocab);
+  k::GemmEpilogue ef;
+  ef.kind = k::kEpiStoreF32;
+  ef.out = logits;
+  ef.ldo = cfg_.vocab;
+  k::gemm(xn, H, dc.lm_head, H, b, cfg_.vocab, H, ef, s);
+  int32_t* d_out = scratch<int32_t>(dc.out_tok, b);
+  k::argmax_rows(logits, b, cfg_.vocab, d_out, s);
+  cuda_ok(cudaEventRecord(dc.e1, s), "event");
+  check_cuda("decode launch");
+  std::vector<int32_t> out(static_cast<size_t>(b));
+  cuda_ok(cudaMemcpyAsync(out.data(), d_out, b * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  std::vector<float> lg;
+  if (a.logits_out) {
+    lg.resize(static_cast<size_t>(b) * cfg_.vocab);
+    cuda_ok(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  }
+  cuda_ok(cudaStreamSynchronize(s), "decode");
+  float ms = 0;
+  cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
+  if (a.device_ms_out) *a.device_ms_out = ms;
+  // Results back in the caller's batch order.
+  std::map<RequestId, int> row_of;
+  for (int i = 0; i < b; ++i) row_of[rows_v[i].r] = i;
+  for (int i = 0; i < b; ++i) {
+    const int ri = row_of[batch[i]];
+    RequestRec& rr = req(batch[i]);
+    if (a.in_tokens) rr.tokens.push_back(a.in_tokens[i]);
+    rr.tokens.push_back(out[ri]);
+    if (a.out_tokens) a.out_tokens[i] = out[ri];
+    if (a.logits_out) {
+      std::memcpy(a.logits_out + static_cast<size_t>(i) * cfg_.vocab,
+                  lg.data() + static_cast<size_t>(ri) * cfg_.vocab, cfg_.vocab * sizeof(float));
+    }
+  }
+}
+
+// ---- KV moves, frees, readback -------------------------------------------------------
+void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t tokens) {
+  RequestRec& rr = req(r);
+  InstanceRec& src = inst(from);
+  InstanceRec& dst = inst(to);
+  auto it = rr.pages.find(from);
+  if (tokens < 0 || it == rr.pages.end() ||
+      static_cast<int64_t>(it->second.slots.size()) < tokens) {
+    throw InternalError("migration moves KV the request does not hold");
+  }
+  if (tokens == 0 || from == to) return;
+  if (dst.used + tokens > dst.capacity) throw CapacityError(to, "migration target lacks room");
+  PageList& spl = it->second;
+  std::vector<int32_t> moving(spl.slots.end() - tokens, spl.slots.end());
+  std::vector<int32_t> dslots = take_slots(dst, tokens);
+  if (!devices_.empty()) {
+    if (src.device != dst.device) {
+      throw ConfigError("move_kv across devices is not supported in this build");
+    }
+    DeviceCtx& dc = device_of({from, to}, "move_kv");
+    DeviceGuard g(dc.device);
+    int32_t* d_a = scratch<int32_t>(dc.tok, static_cast<size_t>(tokens));
+    int32_t* d_b = scratch<int32_t>(dc.pos, static_cast<size_t>(tokens));
+    cuda_ok(cudaMemcpyAsync(d_a, moving.data(), tokens * 4, cudaMemcpyHostToDevice, dc.stream), "h2d");
+    cuda_ok(cudaMemcpyAsync(d_b, dslots.data(), tokens * 4, cudaMemcpyHostToDevice, dc.stream), "h2d");
+    k::copy_slots(static_cast<bf16*>(src.k_slab), static_cast<bf16*>(src.v_slab), d_a,
+                  static_cast<bf16*>(dst.k_slab), static_cast<bf16*>(dst.v_slab), d_b,
+                  static_cast<int>(tokens), cfg_.layers, src.capacity, dst.capacity,
+                  cfg_.hidden, dc.stream);
+    check_cuda("move_kv");
+    cuda_ok(cudaStreamSynchronize(dc.stream), "move_kv");
+  }
+  spl.slots.resize(spl.slots.size() - static_cast<size_t>(tokens));
+  if (spl.dev_n > static_cast<int64_t>(spl.slots.size())) spl.dev_n = static_cast<int64_t>(spl.slots.size());
+  release_slots(src, moving);
+  PageList& dpl = rr.pages[to];
+  dpl.slots.insert(dpl.slots.end(), dslots.begin(), dslots.end());
+  if (spl.slots.empty()) {
+    if (spl.dev) cudaFree(spl.dev);
+    rr.pages.erase(from);
+  }
+}
+
+void Runtime::free_request(RequestId r) {
+  auto it = requests_.find(r);
+  if (it == requests_.end()) return;
+  for (auto& [i, pl] : it->second.pages) {
+    release_slots(inst(i), pl.slots);
+    if (pl.dev) cudaFree(pl.dev);
+  }
+  requests_.erase(it);
+}
+
+void Runtime::query_placement(RequestId r, int32_t* out_inst, int64_t* out_tok, int32_t cap,
+                              int32_t* n) const {
+  auto it = requests_.find(r);
+  int32_t cnt = 0;
+  if (it != requests_.end()) {
+    for (const auto& [i, pl] : it->second.pages) {
+      if (pl.slots.empty()) continue;
+      if (cnt < cap) {
+        out_inst[cnt] = i;
+        out_tok[cnt] = static_cast<int64_t>(pl.slots.size());
+      }
+      ++cnt;
+    }
+  }
+  *n = cnt;
+}
+
+void Runtime::instance_info(InstanceId i, int64_t* cap, int64_t* used) const {
+  const InstanceRec& in = inst(i);
+  if (cap) *cap = in.capacity;
+  if (used) *used = in.used;
+}
+
+void Runtime::request_tokens(RequestId r, int32_t* out, int32_t cap, int32_t* n) const {
+  const RequestRec& rr = req(r);
+  const int32_t cnt = static_cast<int32_t>(rr.tokens.size());
+  for (int32_t i = 0; i < std::min(cap, cnt); ++i) out[i] = rr.tokens[i];
+  *n = cnt;
+}
+
+void Runtime::check_conservation() {
+  // Host counters vs page tables (KvPool::check_conservation, cluster.cpp:113-132).
+  std::map<InstanceId, int64_t> held;
+  for (const auto& [rid, rr] : requests_) {
+    for (const auto& [i, pl] : rr.pages) held[i] += static_cast<int64_t>(pl.slots.size());
+  }
+  for (const auto& in : instances_) {
+    if (in.used != held[in.id]) {
+      throw InternalError("instance " + std::to_string(in.id) +
+                          " used counter drifted from placements");
+    }
+    if (in.used > in.capacity) {
+      throw InternalError("instance " + std::to_string(in.id) + " holds more KV than its capacity");
+    }
+    if (in.used + static_cast<int64_t>(in.free_stack.size()) != in.capacity) {
+      throw InternalError("instance " + std::to_string(in.id) + " free list drifted");
+    }
+  }
+  if (devices_.empty()) return;
+  // Device page tables: recount every slot on the device.
+  for (auto& in : instances_) {
+    DeviceCtx& dc = device_of({in.id}, "check_conservation");
+    DeviceGuard g(dc.device);
+    cudaStream_t s = dc.stream;
+    int32_t* counts = scratch<int32_t>(dc.counts, static_cast<size_t>(in.capacity) + 1);
+    int32_t* res = scratch<int32_t>(dc.result, 2);
+    cuda_ok(cudaMemsetAsync(counts, 0, (static_cast<size_t>(in.capacity) + 1) * 4, s), "memset");
+    cuda_ok(cudaMemsetAsync(res, 0, 8, s), "memset");
+    for (auto& [rid, rr] : requests_) {
+      auto it = rr.pages.find(in.id);
+      if (it == rr.pages.end() || it->second.slots.empty()) continue;
+      sync_pages(it->second, s);
+      k::count_slots(it->second.dev, static_cast<int64_t>(it->second.slots.size()), counts,
+                     static_cast<int>(in.capacity), s);
+    }
+    k::check_counts(counts, static_cast<int>(in.capacity), res, s);
+    int32_t h[2] = {0, 0};
+    cuda_ok(cudaMemcpyAsync(h, res, 8, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_ok(cudaStreamSynchronize(s), "conservation");
+    if (h[0] != in.used || h[1] != 0) {
+      throw InternalError("device page tables of instance " + std::to_string(in.id) +
+                          " disagree: " + std::to_string(h[0]) + " slots mapped, " +
+                          std::to_string(h[1]) + " conflicts, host used " +
+                          std::to_string(in.used));
+    }
+  }
+}
+
+void Runtime::dump_profiles(const std::string& path) const {
+  std::ofstream out(path, std::ios::app);
+  if (!out) throw ConfigError("cannot write profile file: " + path);
+  for (const ProfileRec& p : profiles_) {
+    out << "{\"dop\": " << p.dop << ", \"tp\": 1, \"kind\": \"profile\", \"lengths\": [";
+    for (size_t i = 0; i < p.lengths.size(); ++i) out << (i ? ", " : "") << p.lengths[i];
+    out << "], \"measured_ms\": " << p.ms << "}\n";
+  }
+}
+
+}  // namespace esp

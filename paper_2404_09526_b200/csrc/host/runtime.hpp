@@ -1,0 +1,110 @@
+// The ESP runtime: elastic instances as GPU-resident slices of one
+// token-granular paged KV pool, plus the executor that realizes the
+// reference scheduler's PrefillPlan / DecodeStepPlan / KvMove decisions with
+// the sm_100a kernels. See include/esp_abi.h for the contract.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "esp_abi.h"
+#include "planner.hpp"
+
+namespace esp {
+
+namespace k {
+struct RingSegment;
+}
+
+// One request's slots on one instance, in token order, with a lazily
+// synchronized device mirror the kernels read.
+struct PageList {
+  std::vector<int32_t> slots;
+  int32_t* dev = nullptr;
+  int64_t dev_cap = 0;
+  int64_t dev_n = 0;  // prefix of `slots` already on the device
+};
+
+struct RequestRec {
+  RequestId id = -1;
+  int64_t input_len = 0;
+  std::vector<int32_t> tokens;  // prompt, then generated tokens
+  std::map<InstanceId, PageList> pages;
+  int64_t kv_tokens() const {
+    int64_t n = 0;
+    for (const auto& kv : pages) n += static_cast<int64_t>(kv.second.slots.size());
+    return n;
+  }
+};
+
+struct InstanceRec {
+  InstanceId id = -1;
+  int device = -1;
+  int slab = -1;  // index among the instances co-located on the device
+  int64_t capacity = 0;
+  int64_t used = 0;
+  std::vector<int32_t> free_stack;  // back() is the next slot handed out
+  void* k_slab = nullptr;           // [layers][capacity][hidden] bf16
+  void* v_slab = nullptr;
+};
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct DeviceCtx;
+
+struct ProfileRec {
+  int dop;
+  std::vector<int64_t> lengths;
+  double ms;
+};
+
+class Runtime {
+ public:
+  Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
+          int64_t kv_capacity);
+  ~Runtime();
+
+  void prefill(const esp_prefill_args& a);
+  void decode_step(const esp_decode_args& a);
+  void move_kv(RequestId r, InstanceId from, InstanceId to, int64_t tokens);
+  void free_request(RequestId r);
+  void query_placement(RequestId r, int32_t* inst, int64_t* tok, int32_t cap, int32_t* n) const;
+  void instance_info(InstanceId i, int64_t* cap, int64_t* used) const;
+  void check_conservation();
+  void request_tokens(RequestId r, int32_t* out, int32_t cap, int32_t* n) const;
+  void dump_profiles(const std::string& path) const;
+  bool placement_only() const { return devices_.empty(); }
+
+ private:
+  InstanceRec& inst(InstanceId i);
+  const InstanceRec& inst(InstanceId i) const;
+  RequestRec& req(RequestId r);
+  const RequestRec& req(RequestId r) const;
+  std::vector<int32_t> take_slots(InstanceRec& in, int64_t n);
+  void release_slots(InstanceRec& in, const std::vector<int32_t>& s);
+  void sync_pages(PageList& pl, cudaStream_t s);
+  DeviceCtx& device_of(const std::vector<InstanceId>& ids, const char* what);
+  void init_device(DeviceCtx& dc);
+  void forward_layers_prefill(DeviceCtx& dc, int rows, const std::vector<k::RingSegment>& segs,
+                              const std::vector<int32_t>& work);
+  template <typename T>
+  T* scratch(DevBuf& b, size_t n);
+  void* upload(DeviceCtx& dc, const void* src, size_t bytes);
+  void check_cuda(const char* what);
+
+  esp_model_config cfg_;
+  std::vector<InstanceRec> instances_;
+  std::map<RequestId, RequestRec> requests_;
+  std::vector<std::unique_ptr<DeviceCtx>> devices_;  // empty: placement-only
+  std::vector<ProfileRec> profiles_;
+};
+
+}  // namespace esp

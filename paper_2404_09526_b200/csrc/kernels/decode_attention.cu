@@ -1,0 +1,207 @@
+// K3 + K4: multi-master distributed decoding (LoongServe PAPER.md:272-284).
+//
+// K3 (split-KV paged attention): every instance that holds part of a
+// request's KV computes a partial attention of the request's new query over
+// its own token slots. A request's slots on one instance are split into
+// chunks of <= kChunk tokens; one CTA handles one (chunk, head). The slab
+// layout is [layer][slot][heads*head_dim] bf16, so one token's K row of one
+// head is head_dim*2 contiguous bytes: head_dim/8 lanes each issue one
+// 128-bit non-caching load (ld.global.nc.L1::no_allocate.v4) per token, the
+// dot product is reduced with warp shuffles, and the online softmax runs per
+// token in registers. Output: (o, m, l) per (chunk, head), fp32.
+//
+// K4 (LSE combine at the master): o = sum_c e^{m_c-M} o_c / sum_c e^{m_c-M} l_c
+// over all chunks of the request, on every instance that held its KV.
+#include <cfloat>
+#include <stdexcept>
+
+#include "kernels.h"
+
+namespace esp::k {
+
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+    const float2 x = __bfloat1622float2(b);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kWarps * 32)
+    decode_attention_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
+                            const DecodeSlabs slabs, int heads, float scale_log2,
+                            float* __restrict__ part_o, float* __restrict__ part_ml) {
+  constexpr int LPT = HD / 8;     // lanes per token
+  constexpr int TPW = 32 / LPT;   // tokens per warp step
+  const int ci = blockIdx.x, head = blockIdx.y;
+  const DecodeChunk ch = chunks[ci];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / LPT;          // token group within the warp
+  const int dl = lane % LPT;           // dim slice: dims [8*dl, 8*dl+8)
+  const int hidden = heads * HD;
+
+  float qf[8];
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(q + static_cast<int64_t>(ch.row) * hidden +
+                                                head * HD + dl * 8),
+                qf);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) qf[e] *= scale_log2;
+
+  const bf16* kb = slabs.k[ch.slab] + head * HD + dl * 8;
+  const bf16* vb = slabs.v[ch.slab] + head * HD + dl * 8;
+  float m = -INFINITY, l = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+  const int step = kWarps * TPW;
+  for (int t0 = warp * TPW + sub; t0 < ch.n; t0 += step * kUnroll) {
+    uint4 kr[kUnroll], vr[kUnroll];
+    bool ok[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int t = t0 + u * step;
+      ok[u] = t < ch.n;
+      if (ok[u]) {
+        const int64_t off = static_cast<int64_t>(__ldg(&ch.slots[t])) * hidden;
+        kr[u] = ld_nc_v4(kb + off);
+        vr[u] = ld_nc_v4(vb + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      float kf[8];
+      float s = 0.f;
+      if (ok[u]) {
+        bf16x8_to_f32(kr[u], kf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s = fmaf(qf[e], kf[e], s);
+      }
+#pragma unroll
+      for (int w = LPT / 2; w >= 1; w >>= 1) s += __shfl_xor_sync(0xffffffff, s, w);
+      if (ok[u]) {
+        const float m_new = fmaxf(m, s);
+        const float corr = exp2f(m - m_new);
+        const float p = exp2f(s - m_new);
+        float vf[8];
+        bf16x8_to_f32(vr[u], vf);
+        l = l * corr + p;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = fmaf(o[e], corr, p * vf[e]);
+        m = m_new;
+      }
+    }
+  }
+  // Merge the TPW token groups of the warp (lanes with equal dl).
+#pragma unroll
+  for (int w = LPT; w < 32; w <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffff, m, w);
+    const float l2 = __shfl_xor_sync(0xffffffff, l, w);
+    const float mm = fmaxf(m, m2);
+    const float c1 = m == -INFINITY ? 0.f : exp2f(m - mm);
+    const float c2 = m2 == -INFINITY ? 0.f : exp2f(m2 - mm);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float o2 = __shfl_xor_sync(0xffffffff, o[e], w);
+      o[e] = o[e] * c1 + o2 * c2;
+    }
+    l = l * c1 + l2 * c2;
+    m = mm;
+  }
+  // Merge warps through shared memory.
+  __shared__ float sm_m[kWarps], sm_l[kWarps];
+  __shared__ float sm_o[kWarps][HD];
+  if (sub == 0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sm_o[warp][dl * 8 + e] = o[e];
+    if (dl == 0) {
+      sm_m[warp] = m;
+      sm_l[warp] = l;
+    }
+  }
+  __syncthreads();
+  const int64_t pidx = static_cast<int64_t>(ci) * heads + head;
+  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+    float mm = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) mm = fmaxf(mm, sm_m[w]);
+    float acc = 0.f, ll = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float c = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - mm);
+      acc += c * sm_o[w][d];
+      ll += c * sm_l[w];
+    }
+    part_o[pidx * HD + d] = acc;
+    if (d == 0) {
+      part_ml[pidx * 2] = mm;
+      part_ml[pidx * 2 + 1] = ll;
+    }
+  }
+}
+
+__global__ void decode_combine_kernel(const float* __restrict__ part_o,
+                                      const float* __restrict__ part_ml,
+                                      const int32_t* __restrict__ row_start, int heads, int hd,
+                                      bf16* __restrict__ out) {
+  const int row = blockIdx.x, head = blockIdx.y;
+  const int c0 = row_start[row], c1 = row_start[row + 1];
+  float mm = -INFINITY;
+  for (int c = c0; c < c1; ++c) mm = fmaxf(mm, part_ml[(static_cast<int64_t>(c) * heads + head) * 2]);
+  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
+    float acc = 0.f, ll = 0.f;
+    for (int c = c0; c < c1; ++c) {
+      const int64_t p = static_cast<int64_t>(c) * heads + head;
+      const float mc = part_ml[p * 2];
+      const float w = mc == -INFINITY ? 0.f : exp2f(mc - mm);
+      acc += w * part_o[p * hd + d];
+      ll += w * part_ml[p * 2 + 1];
+    }
+    out[static_cast<int64_t>(row) * heads * hd + head * hd + d] =
+        __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
+  }
+}
+
+}  // namespace
+
+void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
+                      const DecodeSlabs& slabs, int heads, int head_dim, float scale,
+                      float* part_o, float* part_ml, cudaStream_t s) {
+  if (n_chunks <= 0) return;
+  const dim3 grid(n_chunks, heads);
+  const float sl2 = scale * 1.4426950408889634f;
+  if (head_dim == 128) {
+    decode_attention_kernel<128><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads, sl2,
+                                                             part_o, part_ml);
+  } else if (head_dim == 64) {
+    decode_attention_kernel<64><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads, sl2,
+                                                            part_o, part_ml);
+  } else {
+    throw std::runtime_error("decode_attention: head_dim must be 64 or 128");
+  }
+  count_launch();
+}
+
+void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
+                    int rows, int heads, int head_dim, bf16* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  decode_combine_kernel<<<dim3(rows, heads), head_dim, 0, s>>>(part_o, part_ml, row_start,
+                                                               heads, head_dim, out);
+  count_launch();
+}
+
+}  // namespace esp::k

@@ -1,0 +1,403 @@
+// K2/K5: persistent warp-specialized bf16 GEMM on 5th-gen tensor cores.
+//
+//   D[M x N] = A[M x K] . B[N x K]^T      (A activations, B nn.Linear weights)
+//
+// One CTA per SM. TMA (SWIZZLE_128B) streams 128 x 64 A tiles and BN x 64 B
+// tiles through a STAGES-deep mbarrier ring; one elected thread issues
+// tcgen05.mma (M=128, N=BN, K=16) into a double-buffered fp32 TMEM
+// accumulator; four epilogue warps drain TMEM with tcgen05.ld while the next
+// tile's MMAs run, and apply the fused epilogue:
+//   store / residual-add (O and down projections) / fp32 (LM head) /
+//   SiLU(gate)*up (gate_up projection) / QKV split + RoPE + ring-stripe write +
+//   proactive-retention write into the page slot of the token's resting
+//   instance (the QKV projection of ESP prefill; the KV append of decode).
+#include <cuda.h>
+
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace esp::k {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+  constexpr int kGroup = 16;  // m-blocks per raster group (L2 reuse of B)
+  const int per_group = kGroup * num_n;
+  const int g = tile / per_group;
+  const int first = g * kGroup;
+  const int gsize = min(num_m - first, kGroup);
+  const int t = tile % per_group;
+  mb = first + t % gsize;
+  nb = t / gsize;
+}
+
+__device__ __forceinline__ void store_row_bf16(bf16* dst, const uint32_t (&r)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    d[i] = make_uint4(
+        ptx::pack_bf16(__uint_as_float(r[8 * i + 0]), __uint_as_float(r[8 * i + 1])),
+        ptx::pack_bf16(__uint_as_float(r[8 * i + 2]), __uint_as_float(r[8 * i + 3])),
+        ptx::pack_bf16(__uint_as_float(r[8 * i + 4]), __uint_as_float(r[8 * i + 5])),
+        ptx::pack_bf16(__uint_as_float(r[8 * i + 6]), __uint_as_float(r[8 * i + 7])));
+  }
+}
+
+__device__ __forceinline__ void store_vals_bf16(bf16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    d[i] = make_uint4(ptx::pack_bf16(v[8 * i + 0], v[8 * i + 1]),
+                      ptx::pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                      ptx::pack_bf16(v[8 * i + 4], v[8 * i + 5]),
+                      ptx::pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+  }
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t tacc, int m,
+                                              bool valid, int nb, int N) {
+  uint32_t r[32];
+  if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      ptx::tmem_ld_32x32b_x32(tacc + c, r);
+      ptx::tmem_wait_ld();
+      if (!valid) continue;
+      const int64_t off = static_cast<int64_t>(m) * ep.ldo + nb * BN + c;
+      if (ep.kind == kEpiStoreF32) {
+        float4* d = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + off);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          d[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                             __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        }
+      } else if (ep.kind == kEpiStore) {
+        store_row_bf16(static_cast<bf16*>(ep.out) + off, r);
+      } else {
+        bf16* dst = static_cast<bf16*>(ep.out) + off;
+        const uint4* src = reinterpret_cast<const uint4*>(dst);
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 o = src[i];
+          const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = ptx::unpack_bf16(w[j]);
+            v[8 * i + 2 * j] = f.x + __uint_as_float(r[8 * i + 2 * j]);
+            v[8 * i + 2 * j + 1] = f.y + __uint_as_float(r[8 * i + 2 * j + 1]);
+          }
+        }
+        store_vals_bf16(dst, v);
+      }
+    }
+  } else if (ep.kind == kEpiSiluMul) {
+    // Physical rows of the gate_up weight come in 128-row blocks: 64 gate
+    // rows then the 64 matching up rows.
+    uint32_t u[32];
+#pragma unroll 1
+    for (int p = 0; p < BN / 128; ++p) {
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        ptx::tmem_ld_32x32b_x32(tacc + p * 128 + c, r);
+        ptx::tmem_ld_32x32b_x32(tacc + p * 128 + 64 + c, u);
+        ptx::tmem_wait_ld();
+        if (!valid) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float g = __uint_as_float(r[i]);
+          v[i] = g / (1.0f + __expf(-g)) * __uint_as_float(u[i]);
+        }
+        const int64_t col = static_cast<int64_t>(nb) * (BN / 2) + p * 64 + c;
+        store_vals_bf16(static_cast<bf16*>(ep.out) + static_cast<int64_t>(m) * ep.ldo + col, v);
+      }
+    }
+  } else {  // kEpiQkvRope
+    const int n0 = nb * BN;
+    const int region = n0 / ep.hidden;  // 0 q, 1 k, 2 v
+    const int col0 = n0 - region * ep.hidden;
+    const int hd = ep.head_dim, half = hd >> 1;
+    int inst = -1, slot = 0, pos = 0;
+    if (valid) {
+      pos = ep.pos[m];
+      if (ep.row_inst) {
+        inst = ep.row_inst[m];
+        slot = ep.row_slot ? ep.row_slot[m] : 0;
+      }
+    }
+    bf16* dst_main =
+        region == 0 ? ep.q_out : (region == 1 ? ep.k_out : ep.v_out);
+    bf16* dst_slab = nullptr;
+    if (region > 0 && inst >= 0) {
+      dst_slab = (region == 1 ? ep.slab_k[inst] : ep.slab_v[inst]) +
+                 static_cast<int64_t>(slot) * ep.hidden;
+    }
+    const int64_t row_off = static_cast<int64_t>(m) * ep.hidden;
+    if (region == 2) {
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        ptx::tmem_ld_32x32b_x32(tacc + c, r);
+        ptx::tmem_wait_ld();
+        if (!valid) continue;
+        if (dst_main) store_row_bf16(dst_main + row_off + col0 + c, r);
+        if (dst_slab) store_row_bf16(dst_slab + col0 + c, r);
+      }
+    } else {
+      uint32_t h[32];
+      const float2* cs_row = ep.rope + static_cast<int64_t>(pos) * half;
+#pragma unroll 1
+      for (int hb = 0; hb < BN; hb += hd) {
+#pragma unroll 1
+        for (int j = 0; j < half; j += 32) {
+          ptx::tmem_ld_32x32b_x32(tacc + hb + j, r);
+          ptx::tmem_ld_32x32b_x32(tacc + hb + j + half, h);
+          ptx::tmem_wait_ld();
+          if (!valid) continue;
+          float lo[32], hi[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float2 cs = cs_row[j + e];
+            const float x1 = __uint_as_float(r[e]), x2 = __uint_as_float(h[e]);
+            lo[e] = x1 * cs.x - x2 * cs.y;
+            hi[e] = x2 * cs.x + x1 * cs.y;
+          }
+          const int c_lo = col0 + hb + j, c_hi = c_lo + half;
+          if (dst_main) {
+            store_vals_bf16(dst_main + row_off + c_lo, lo);
+            store_vals_bf16(dst_main + row_off + c_hi, hi);
+          }
+          if (dst_slab) {
+            store_vals_bf16(dst_slab + c_lo, lo);
+            store_vals_bf16(dst_slab + c_hi, hi);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                      const __grid_constant__ GemmEpilogue ep) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + BM - 1) / BM, num_n = N / BN, num_k = K / BK;
+  const int tiles = num_m * num_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t keep = ptx::policy_evict_last();
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
+          ptx::tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, mb * BM);
+          ptx::tma_load_2d_hint(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, nb * BN,
+                                keep);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        const uint32_t use = static_cast<uint32_t>(lt >> 1);
+        ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a0 = ptx::smem_u32(sA + stage * C::kABytes);
+          const uint32_t b0 = ptx::smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            ptx::umma_f16_ss(d_tmem, ptx::make_sdesc_sw128(a0 + k * 32, 16, 1024),
+                             ptx::make_sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                             (kb | k) != 0);
+          }
+          ptx::tc_commit(&empty[stage]);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t quad = warp & 3;
+    const int row = static_cast<int>(quad * 32 + lane);
+    int lt = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++lt) {
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int acc = lt & 1;
+      const uint32_t use = static_cast<uint32_t>(lt >> 1);
+      ptx::mbar_wait(&tfull[acc], use & 1);
+      ptx::tc_fence_after();
+      const uint32_t tacc = tmem_base + acc * BN + ((quad * 32) << 16);
+      const int m = mb * BM + row;
+      epilogue_tile<BN>(ep, tacc, m, m < M, nb, N);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+// ---- host: tensor maps -----------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        p == nullptr) {
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    }
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+}  // namespace
+
+// bf16 [rows x cols] row-major (row pitch ld elements), box box_rows x 64,
+// 128-byte swizzle (the UMMA K-major SW128 canonical layout).
+CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t ld,
+                           int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                           dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  }
+  return m;
+}
+
+template <int BN>
+static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
+                        const GemmEpilogue& ep, cudaStream_t s) {
+  using C = Cfg<BN>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_bf16_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmem);
+  });
+  const CUtensorMap ta = make_tmap_bf16(A, M, K, lda, BM);
+  const CUtensorMap tb = make_tmap_bf16(B, N, K, ldb, BN);
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_bf16_tcgen05<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, ep);
+  count_launch();
+}
+
+void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
+          const GemmEpilogue& ep, cudaStream_t s) {
+  if (M <= 0) return;
+  if (N % 128 != 0 || K % 64 != 0) throw std::runtime_error("gemm: N%128 or K%64 != 0");
+  const bool n256 = N % 256 == 0;
+  const int tiles256 = ((M + BM - 1) / BM) * (N / 256);
+  // Small-M (decode, LM head) GEMMs are weight-bandwidth bound: prefer the
+  // narrower tile when the wide one would leave SMs idle.
+  if (n256 && tiles256 >= num_sms()) {
+    launch_gemm<256>(A, lda, B, ldb, M, N, K, ep, s);
+  } else {
+    launch_gemm<128>(A, lda, B, ldb, M, N, K, ep, s);
+  }
+}
+
+}  // namespace esp::k

@@ -1,0 +1,114 @@
+// Host-side launchers of the sm_100a kernels of the ESP data path.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace esp::k {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int kMaxSlabs = 16;  // instances co-located on one device
+
+enum EpiKind : int {
+  kEpiStore = 0,     // D = acc (bf16)
+  kEpiResidual = 1,  // D += acc (bf16 in place): O-proj / down-proj + residual
+  kEpiStoreF32 = 2,  // D = acc (fp32): LM-head logits
+  kEpiSiluMul = 3,   // gate/up interleaved in 64-row blocks -> silu(g)*u (bf16)
+  kEpiQkvRope = 4,   // q,k,v split + RoPE + ring stripe write + page retention
+};
+
+struct GemmEpilogue {
+  int kind = kEpiStore;
+  void* out = nullptr;  // store / residual / f32 / silu output
+  int ldo = 0;          // elements
+  // kEpiQkvRope ----------------------------------------------------------
+  bf16* q_out = nullptr;  // [M x hidden]
+  bf16* k_out = nullptr;  // [M x hidden] ring stripe buffer, nullable
+  bf16* v_out = nullptr;
+  const int32_t* pos = nullptr;   // [M] token position
+  const float2* rope = nullptr;   // [max_pos x head_dim/2] (cos, sin)
+  int hidden = 0, head_dim = 0;
+  const int32_t* row_inst = nullptr;  // [M] slab index of the resting page, -1 none
+  const int32_t* row_slot = nullptr;  // [M] slot within that slab
+  bf16* slab_k[kMaxSlabs] = {};       // per co-located instance, this layer's base
+  bf16* slab_v[kMaxSlabs] = {};
+};
+
+// D[M x N] = A[M x K] . B[N x K]^T with the epilogue above. A and B are
+// row-major bf16 (both K-major). N % 128 == 0, K % 64 == 0, any M.
+void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
+          const GemmEpilogue& ep, cudaStream_t s);
+
+// ---- attention ------------------------------------------------------------
+constexpr int kMaxRounds = 8;
+
+// One (ring position, request) segment of striped ring attention: the local
+// query stripe rows [q_row0, q_row0+q_len) meet, in round r, the KV stripe
+// rows [kv_row0[r], +kv_len[r]) that started at ring position origin[r].
+// Key b (stripe index) is visible to query a iff b < a, or b == a and
+// origin <= pos_i (striped causal mask; shift[r] = origin > pos_i).
+struct RingSegment {
+  int32_t q_row0, q_len;
+  int32_t n_rounds;
+  int32_t kv_row0[kMaxRounds];
+  int32_t kv_len[kMaxRounds];
+  int32_t shift[kMaxRounds];
+};
+
+// Attention over segments; q/k/v/out are [rows x heads*head_dim] bf16.
+// Persistent tcgen05 kernel; work = (segment, 128-row q tile, head).
+void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_rows,
+                    int heads, int head_dim, const RingSegment* d_segs, int n_segs,
+                    const int32_t* d_work, int n_work, float scale, cudaStream_t s);
+
+// Work-list builder helper: number of 128-row q tiles of a segment.
+inline int q_tiles(int q_len) { return (q_len + 127) / 128; }
+
+// ---- decode ---------------------------------------------------------------
+// One chunk of one request's KV on one instance: slots slot_idx[0..n).
+struct DecodeChunk {
+  const int32_t* slots;
+  int32_t n;
+  int32_t row;   // request row in the decode batch
+  int32_t slab;  // index into the slab pointer arrays
+  int32_t pad;
+};
+struct DecodeSlabs {
+  const bf16* k[kMaxSlabs];
+  const bf16* v[kMaxSlabs];
+};
+// Split-KV paged attention: partial (o, m, l) per (chunk, head) into
+// part_o [n_chunks x heads x head_dim] fp32 and part_ml [n_chunks x heads x 2].
+void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
+                      const DecodeSlabs& slabs, int heads, int head_dim, float scale,
+                      float* part_o, float* part_ml, cudaStream_t s);
+// LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
+void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
+                    int rows, int heads, int head_dim, bf16* out, cudaStream_t s);
+
+// ---- small fused ops --------------------------------------------------------
+void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,
+           cudaStream_t s);
+// y[r] = rmsnorm(x[src_row[r] or r]) * gamma
+void rmsnorm(const bf16* x, const int32_t* src_rows, const bf16* gamma, bf16* y, int rows,
+             int hidden, float eps, cudaStream_t s);
+void argmax_rows(const float* logits, int rows, int vocab, int32_t* out, cudaStream_t s);
+void rope_table(float2* table, int max_pos, int head_dim, float theta, cudaStream_t s);
+void init_weight(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor, int layer,
+                 int layout, cudaStream_t s);
+void fill_bf16(bf16* dst, int64_t n, float v, cudaStream_t s);
+// Page-table conservation: counts how often each slot appears (atomic).
+void count_slots(const int32_t* slots, int64_t n, int32_t* counts, int capacity,
+                 cudaStream_t s);
+void check_counts(const int32_t* counts, int capacity, int32_t* result /*[2]*/, cudaStream_t s);
+// KV move: copy slab rows (all layers) between slots / slabs.
+void copy_slots(const bf16* src_k, const bf16* src_v, const int32_t* src_slots, bf16* dst_k,
+                bf16* dst_v, const int32_t* dst_slots, int n, int layers, int64_t src_cap,
+                int64_t dst_cap, int hidden, cudaStream_t s);
+
+int64_t launch_count();
+void count_launch();
+
+}  // namespace esp::k

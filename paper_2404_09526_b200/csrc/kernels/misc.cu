@@ -1,0 +1,260 @@
+// K6: small fused ops of the ESP data path (memory-bound, CUDA cores):
+// embedding gather, RMSNorm (optionally gathering rows), greedy argmax, RoPE
+// table, seeded synthetic weights, and the page-table / KV-slot utilities
+// (device-side conservation recount, KV slot moves).
+#include <atomic>
+#include <cfloat>
+
+#include "kernels.h"
+#include "synthetic.h"
+
+namespace esp::k {
+
+namespace {
+std::atomic<int64_t> g_launches{0};
+}
+int64_t launch_count() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1); }
+
+namespace {
+
+__global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __restrict__ table,
+                             bf16* __restrict__ x, int hidden) {
+  const int r = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<int64_t>(tokens[r]) * hidden);
+  uint4* dst = reinterpret_cast<uint4*>(x + static_cast<int64_t>(r) * hidden);
+  for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void rmsnorm_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ src_rows,
+                               const bf16* __restrict__ gamma, bf16* __restrict__ y, int hidden,
+                               float eps) {
+  const int r = blockIdx.x;
+  const int sr = src_rows ? src_rows[r] : r;
+  const bf16* xr = x + static_cast<int64_t>(sr) * hidden;
+  float ss = 0.f;
+  for (int i = threadIdx.x * 8; i < hidden; i += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(xr + i);
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(p[j]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  }
+  __shared__ float red[32];
+  for (int w = 16; w >= 1; w >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, w);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int w = 16; w >= 1; w >>= 1) t += __shfl_xor_sync(0xffffffff, t, w);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / static_cast<float>(hidden) + eps);
+  bf16* yr = y + static_cast<int64_t>(r) * hidden;
+  for (int i = threadIdx.x * 8; i < hidden; i += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(xr + i);
+    const uint4 g = *reinterpret_cast<const uint4*>(gamma + i);
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+    const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&g);
+    uint4 o;
+    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(p[j]);
+      const float2 gg = __bfloat1622float2(gp[j]);
+      op[j] = __floats2bfloat162_rn(f.x * inv * gg.x, f.y * inv * gg.y);
+    }
+    *reinterpret_cast<uint4*>(yr + i) = o;
+  }
+}
+
+__global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int32_t* __restrict__ out) {
+  const int r = blockIdx.x;
+  const float* lr = logits + static_cast<int64_t>(r) * vocab;
+  float best = -FLT_MAX;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = lr[i];
+    if (v > best || (v == best && i < bi)) {
+      best = v;
+      bi = i;
+    }
+  }
+  for (int w = 16; w >= 1; w >>= 1) {
+    const float b2 = __shfl_xor_sync(0xffffffff, best, w);
+    const int i2 = __shfl_xor_sync(0xffffffff, bi, w);
+    if (b2 > best || (b2 == best && i2 < bi)) {
+      best = b2;
+      bi = i2;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  if ((threadIdx.x & 31) == 0) {
+    sb[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w) {
+      if (sb[w] > best || (sb[w] == best && si[w] < bi)) {
+        best = sb[w];
+        bi = si[w];
+      }
+    }
+    out[r] = bi;
+  }
+}
+
+__global__ void rope_table_kernel(float2* table, int max_pos, int half, float theta, int hd) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(max_pos) * half) return;
+  const int p = static_cast<int>(i / half), j = static_cast<int>(i % half);
+  const float inv_freq = powf(theta, -static_cast<float>(2 * j) / static_cast<float>(hd));
+  const float ang = static_cast<float>(p) * inv_freq;
+  float s, c;
+  sincosf(ang, &s, &c);
+  table[i] = make_float2(c, s);
+}
+
+// layout 0: plain [rows x cols]; 1: fused QKV [3*cols x cols] (q|k|v rows);
+// 2: gate_up [rows x cols] in 128-row blocks of 64 gate + 64 up rows.
+__global__ void init_weight_kernel(bf16* dst, int64_t rows, int64_t cols, uint64_t seed,
+                                   int tensor, int layer, int layout) {
+  const int64_t n = rows * cols;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pr = i / cols, c = i % cols;
+    int t = tensor;
+    int64_t lr = pr;
+    if (layout == 1) {
+      t = tensor + static_cast<int>(pr / cols);  // Q, K, V ids are consecutive
+      lr = pr % cols;
+    } else if (layout == 2) {
+      const int64_t blk = pr / 128, w = pr % 128;
+      t = w < 64 ? kTensorGate : kTensorUp;
+      lr = blk * 64 + (w % 64);
+    }
+    dst[i] = __float2bfloat16_rn(synthetic_weight(seed, t, layer, lr, c, cols));
+  }
+}
+
+__global__ void fill_kernel(bf16* dst, int64_t n, float v) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    dst[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void count_slots_kernel(const int32_t* slots, int64_t n, int32_t* counts, int cap) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int s = slots[i];
+    if (s >= 0 && s < cap) atomicAdd(&counts[s], 1);
+    else atomicAdd(&counts[cap], 1);  // out-of-range sentinel
+  }
+}
+
+// result[0] = number of slots assigned (count > 0), result[1] = slots assigned
+// more than once + out-of-range entries.
+__global__ void check_counts_kernel(const int32_t* counts, int cap, int32_t* result) {
+  int used = 0, bad = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+    used += counts[i] > 0;
+    bad += counts[i] > 1;
+  }
+  for (int w = 16; w >= 1; w >>= 1) {
+    used += __shfl_xor_sync(0xffffffff, used, w);
+    bad += __shfl_xor_sync(0xffffffff, bad, w);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&result[0], used);
+    atomicAdd(&result[1], bad);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&result[1], counts[cap]);
+}
+
+__global__ void copy_slots_kernel(const bf16* __restrict__ sk, const bf16* __restrict__ sv,
+                                  const int32_t* __restrict__ ss, bf16* __restrict__ dk,
+                                  bf16* __restrict__ dv, const int32_t* __restrict__ ds,
+                                  int layers, int64_t scap, int64_t dcap, int hidden) {
+  const int t = blockIdx.x, layer = blockIdx.y;
+  const int64_t so = (static_cast<int64_t>(layer) * scap + ss[t]) * hidden;
+  const int64_t dof = (static_cast<int64_t>(layer) * dcap + ds[t]) * hidden;
+  const uint4* a = reinterpret_cast<const uint4*>(sk + so);
+  const uint4* b = reinterpret_cast<const uint4*>(sv + so);
+  uint4* c = reinterpret_cast<uint4*>(dk + dof);
+  uint4* d = reinterpret_cast<uint4*>(dv + dof);
+  for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) {
+    c[i] = a[i];
+    d[i] = b[i];
+  }
+}
+
+}  // namespace
+
+void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,
+           cudaStream_t s) {
+  if (rows <= 0) return;
+  embed_kernel<<<rows, 128, 0, s>>>(tokens, table, x, hidden);
+  count_launch();
+}
+
+void rmsnorm(const bf16* x, const int32_t* src_rows, const bf16* gamma, bf16* y, int rows,
+             int hidden, float eps, cudaStream_t s) {
+  if (rows <= 0) return;
+  const int threads = hidden >= 2048 ? 256 : 64;
+  rmsnorm_kernel<<<rows, threads, 0, s>>>(x, src_rows, gamma, y, hidden, eps);
+  count_launch();
+}
+
+void argmax_rows(const float* logits, int rows, int vocab, int32_t* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  argmax_kernel<<<rows, 1024, 0, s>>>(logits, vocab, out);
+  count_launch();
+}
+
+void rope_table(float2* table, int max_pos, int head_dim, float theta, cudaStream_t s) {
+  const int half = head_dim / 2;
+  const int64_t n = static_cast<int64_t>(max_pos) * half;
+  rope_table_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(table, max_pos, half,
+                                                                           theta, head_dim);
+  count_launch();
+}
+
+void init_weight(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor, int layer,
+                 int layout, cudaStream_t s) {
+  init_weight_kernel<<<4096, 256, 0, s>>>(dst, rows, cols, seed, tensor, layer, layout);
+  count_launch();
+}
+
+void fill_bf16(bf16* dst, int64_t n, float v, cudaStream_t s) {
+  fill_kernel<<<1024, 256, 0, s>>>(dst, n, v);
+  count_launch();
+}
+
+void count_slots(const int32_t* slots, int64_t n, int32_t* counts, int capacity,
+                 cudaStream_t s) {
+  if (n <= 0) return;
+  count_slots_kernel<<<256, 256, 0, s>>>(slots, n, counts, capacity);
+  count_launch();
+}
+
+void check_counts(const int32_t* counts, int capacity, int32_t* result, cudaStream_t s) {
+  check_counts_kernel<<<256, 256, 0, s>>>(counts, capacity, result);
+  count_launch();
+}
+
+void copy_slots(const bf16* src_k, const bf16* src_v, const int32_t* src_slots, bf16* dst_k,
+                bf16* dst_v, const int32_t* dst_slots, int n, int layers, int64_t src_cap,
+                int64_t dst_cap, int hidden, cudaStream_t s) {
+  if (n <= 0) return;
+  copy_slots_kernel<<<dim3(n, layers), 128, 0, s>>>(src_k, src_v, src_slots, dst_k, dst_v,
+                                                    dst_slots, layers, src_cap, dst_cap, hidden);
+  count_launch();
+}
+
+}  // namespace esp::k

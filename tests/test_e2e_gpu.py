@@ -1,0 +1,124 @@
+"""End-to-end parity of the ESP data path on a B200: the reference engine's
+recorded decisions (tests/golden) are executed through the C-ABI with real
+kernels; page tables must equal the engine's placements at every step
+(bit-exact) and the generated tokens/logits must match the dense CPU oracle
+(oracle/llama_ref.c, bf16-emulation mode) within the stated tolerance:
+
+  logits: max|gpu - oracle| / max|oracle| <= 5e-2 per step (bf16 weights and
+          activations; the oracle rounds at the same points but accumulates in
+          a different order and keeps P in fp32);
+  greedy tokens: equal to the oracle's argmax unless the oracle's top-1 vs
+          chosen-token logit gap is < 2e-2 (a near-tie under bf16 rounding).
+The oracle is teacher-forced with the GPU's own tokens so one near-tie cannot
+cascade."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import llama_ref
+from paper_2404_09526_b200 import abi
+from tests import replay
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+LOGIT_TOL = 5e-2
+TIE_GAP = 2e-2
+
+
+def check_against_oracle(shape, prompt, toks, logits):
+    n_steps = len(toks) - 1
+    ref_tok, ref_lg = llama_ref.generate(shape, prompt, n_steps, forced=toks[:n_steps],
+                                         emulate_bf16=True)
+    exact = 0
+    for s in range(n_steps + 1):
+        err = np.abs(logits[s] - ref_lg[s]).max() / (np.abs(ref_lg[s]).max() + 1e-6)
+        assert err < LOGIT_TOL, (s, err)
+        gap = ref_lg[s].max() - ref_lg[s][toks[s]]
+        assert toks[s] == ref_tok[s] or gap < TIE_GAP, (s, toks[s], ref_tok[s], gap)
+        exact += int(toks[s] == ref_tok[s])
+    return exact / (n_steps + 1)
+
+
+class Recorder:
+    def __init__(self, rt):
+        self.rt = rt
+        self.logits = {}
+        self.prompts = {}
+
+    def prefill(self, p, retain):
+        toks = np.concatenate([replay.prompt_tokens(r, n) for r, n in zip(p["requests"], p["input_lens"])])
+        for r, n in zip(p["requests"], p["input_lens"]):
+            self.prompts[r] = replay.prompt_tokens(r, n)
+            self.logits[r] = []
+        first, lg, _ = self.rt.prefill(p["requests"], p["input_lens"], p["instances"], retain,
+                                       tokens=toks, want_logits=True)
+        for i, r in enumerate(p["requests"]):
+            self.logits[r].append(lg[i])
+
+    def decode(self, d, members):
+        out, lg, _ = self.rt.decode_step(members, d["masters"], d["batch"], want_logits=True)
+        for i, r in enumerate(d["batch"]):
+            self.logits[r].append(lg[i])
+
+
+def test_config1_tiny_esp_prefill_and_decode():
+    """Config 1: 4K-token prompt, ESP prefill as a 2-instance striped ring with
+    scale-down 2->1 (proactive retention onto instance 0), 64 decode steps."""
+    path = os.path.join(GOLD, "scenario_config1_tiny.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    rec = Recorder(rt)
+    # the final decode appends the 64th token; finish frees it
+    replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
+    # tokens are gone with the freed request: rebuild from recorded logits
+    toks = [int(np.argmax(l)) for l in rec.logits[0]]
+    frac = check_against_oracle(abi.TINY, rec.prompts[0], toks, rec.logits[0])
+    assert frac >= 0.9
+
+
+def test_config1_tight_scale_up_mid_decode():
+    """cap 4096: prefill scales 2->1, then decode scales up 1->2 and the KV of
+    one request spans two instances (multi-instance split-KV + LSE combine)."""
+    path = os.path.join(GOLD, "scenario_config1_tiny_tight.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    rec = Recorder(rt)
+    replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
+    toks = [int(np.argmax(l)) for l in rec.logits[0]]
+    check_against_oracle(abi.TINY, rec.prompts[0], toks, rec.logits[0])
+
+
+def test_tiny_multi_request_batches_and_masters():
+    """8 requests over 4 instances: varlen multi-request ring prefills,
+    multi-master decode, scale-up/down, displaced-KV moves."""
+    path = os.path.join(GOLD, "scenario_tiny_multi.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    rec = Recorder(rt)
+    replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
+    for r, lgs in rec.logits.items():
+        toks = [int(np.argmax(l)) for l in lgs]
+        check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8])
+def test_esp_degree_invariance(d):
+    """The same prompt prefilled at ESP degree d (striped ring over d
+    co-located instances, retention onto 2 survivors) gives the oracle's
+    logits; a decode step over the retained pages matches too."""
+    S = 1500 + d
+    shape = abi.TINY
+    prompt = np.random.default_rng(d).integers(0, shape.vocab, S).astype(np.int32)
+    rt = abi.Runtime(shape, d + 1, devices=[0] * (d + 1), kv_capacity=1000)
+    ring = list(range(d))
+    retain = [[(d, 1000), (0, S - 1000)]] if d > 1 else [[(0, 1000), (1, S - 1000)]]
+    first, lg, _ = rt.prefill([5], [S], ring, retain, tokens=prompt, want_logits=True)
+    assert rt.placement(5) == {i: t for i, t in retain[0]}
+    members = sorted({i for i, _ in retain[0]})
+    out, lg2, _ = rt.decode_step(members, [members[0]], [5], want_logits=True)
+    rt.check_conservation()
+    check_against_oracle(shape, prompt, [int(first[0]), int(out[0])], [lg[0], lg2[0]])
