@@ -255,6 +255,15 @@ int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int
  * "measured_ms"}, cost_model.cpp:243-248) appended to a JSONL file. */
 int esp_dump_profiles(const esp_runtime* rt, const char* path);
 
+/* Per-phase device timing (CUDA events around each launch on the runtime's
+ * stream) while profiling is on. Phases: 0 embed, 1 rmsnorm, 2 QKV GEMM(+RoPE
+ * +ring write+retention), 3 ring attention, 4 O GEMM, 5 gate_up GEMM, 6 down
+ * GEMM, 7 LM head, 8 argmax, 9 decode attention, 10 LSE combine.
+ * esp_phase_times returns and resets the accumulated ms / launch counts. */
+#define ESP_N_PHASES 11
+int esp_set_profiling(esp_runtime* rt, int32_t on);
+int esp_phase_times(esp_runtime* rt, double* ms, int64_t* launches, int32_t n);
+
 /* Count of kernel launches issued by this runtime so far. */
 int64_t esp_launch_count(const esp_runtime* rt);
 

@@ -91,7 +91,7 @@ EXPORTED_SYMBOLS = [
     "esp_runtime_create", "esp_runtime_destroy", "esp_instance_info", "esp_prefill",
     "esp_decode_step", "esp_move_kv", "esp_free_request", "esp_query_placement",
     "esp_check_conservation", "esp_request_tokens", "esp_dump_profiles",
-    "esp_launch_count", "esp_k_gemm", "esp_k_ring_attention", "esp_k_decode_attention",
+    "esp_launch_count", "esp_set_profiling", "esp_phase_times", "esp_k_gemm", "esp_k_ring_attention", "esp_k_decode_attention",
 ]
 
 
@@ -178,6 +178,9 @@ def lib() -> C.CDLL:
         h.esp_request_tokens.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
                                          C.c_int32, C.POINTER(C.c_int32)]
         h.esp_dump_profiles.argtypes = [C.c_void_p, C.c_char_p]
+        h.esp_set_profiling.argtypes = [C.c_void_p, C.c_int32]
+        h.esp_phase_times.argtypes = [C.c_void_p, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int64), C.c_int32]
         h.esp_k_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                  C.c_int32, C.c_int32, C.c_void_p]
         h.esp_k_ring_attention.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
@@ -541,6 +544,20 @@ class Runtime:
         check(lib().esp_request_tokens(self._h, request, _ptr(out, C.c_int32), n.value,
                                        C.byref(n)))
         return [int(x) for x in out[:n.value]]
+
+    PHASES = ["embed", "rmsnorm", "qkv_gemm", "ring_attention", "o_gemm", "gate_up_gemm",
+              "down_gemm", "lm_head", "argmax", "decode_attention", "lse_combine"]
+
+    def set_profiling(self, on: bool):
+        check(lib().esp_set_profiling(self._h, 1 if on else 0))
+
+    def phase_times(self):
+        """{phase: (ms, launches)} accumulated since the last call (then reset)."""
+        n = len(self.PHASES)
+        ms = np.zeros(n, np.float64)
+        ln = np.zeros(n, np.int64)
+        check(lib().esp_phase_times(self._h, _ptr(ms, C.c_double), _ptr(ln, C.c_int64), n))
+        return {p: (float(ms[i]), int(ln[i])) for i, p in enumerate(self.PHASES)}
 
     def dump_profiles(self, path: str):
         check(lib().esp_dump_profiles(self._h, path.encode()))

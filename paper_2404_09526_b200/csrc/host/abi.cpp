@@ -302,6 +302,14 @@ int esp_dump_profiles(const esp_runtime* rt, const char* path) {
   return guarded([&] { rt->impl->dump_profiles(path); });
 }
 
+int esp_set_profiling(esp_runtime* rt, int32_t on) {
+  return guarded([&] { rt->impl->set_profiling(on != 0); });
+}
+
+int esp_phase_times(esp_runtime* rt, double* ms, int64_t* launches, int32_t n) {
+  return guarded([&] { rt->impl->phase_times(ms, launches, n); });
+}
+
 int64_t esp_launch_count(const esp_runtime* rt) {
   (void)rt;
   return esp::k::launch_count();

@@ -89,6 +89,53 @@ T* Runtime::scratch(DevBuf& b, size_t n) {
   return static_cast<T*>(b.ptr);
 }
 
+template <typename F>
+void Runtime::timed(int phase, cudaStream_t s, F&& f) {
+  if (!profiling_) {
+    f();
+    return;
+  }
+  auto get = [&]() {
+    if (event_pool_.empty()) {
+      cudaEvent_t e;
+      cuda_ok(cudaEventCreate(&e), "event");
+      return e;
+    }
+    cudaEvent_t e = event_pool_.back();
+    event_pool_.pop_back();
+    return e;
+  };
+  PhaseEvent pe{phase, get(), get()};
+  cuda_ok(cudaEventRecord(pe.a, s), "event");
+  f();
+  cuda_ok(cudaEventRecord(pe.b, s), "event");
+  pending_.push_back(pe);
+}
+
+// Call after the stream synchronized: folds recorded event pairs into totals.
+void Runtime::collect_phase_events() {
+  for (const PhaseEvent& pe : pending_) {
+    float ms = 0;
+    cuda_ok(cudaEventElapsedTime(&ms, pe.a, pe.b), "elapsed");
+    phase_ms_[pe.phase] += ms;
+    phase_n_[pe.phase] += 1;
+    event_pool_.push_back(pe.a);
+    event_pool_.push_back(pe.b);
+  }
+  pending_.clear();
+}
+
+void Runtime::phase_times(double* ms, int64_t* launches, int n) {
+  for (int i = 0; i < n && i < kPhCount; ++i) {
+    if (ms) ms[i] = phase_ms_[i];
+    if (launches) launches[i] = phase_n_[i];
+  }
+  for (int i = 0; i < kPhCount; ++i) {
+    phase_ms_[i] = 0;
+    phase_n_[i] = 0;
+  }
+}
+
 Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
                  int64_t kv_capacity)
     : cfg_(cfg) {
@@ -162,6 +209,11 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
 }
 
 Runtime::~Runtime() {
+  for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+  for (const PhaseEvent& pe : pending_) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
   for (auto& [id, r] : requests_) {
     for (auto& [i, pl] : r.pages) {
       if (pl.dev) cudaFree(pl.dev);
@@ -499,7 +551,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
 
   bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(rows) * H);
   cuda_ok(cudaEventRecord(dc.e0, s), "event");
-  k::embed(d_tok, dc.embed, x, rows, H, s);
+  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s); });
   forward_layers_prefill(dc, rows, segs, work_sorted);
 
   // Last prompt token of each request: position len-1 lives at ring position
@@ -512,15 +564,15 @@ void Runtime::prefill(const esp_prefill_args& a) {
   int32_t* d_last = scratch<int32_t>(dc.last_rows, n);
   cuda_ok(cudaMemcpyAsync(d_last, last.data(), n * 4, cudaMemcpyHostToDevice, s), "h2d");
   bf16* xn = scratch<bf16>(dc.xn, static_cast<size_t>(std::max(rows, n)) * H);
-  k::rmsnorm(x, d_last, dc.final_norm, xn, n, H, cfg_.rms_eps, s);
+  timed(kPhNorm, s, [&] { k::rmsnorm(x, d_last, dc.final_norm, xn, n, H, cfg_.rms_eps, s); });
   float* logits = scratch<float>(dc.logits, static_cast<size_t>(n) * cfg_.vocab);
   k::GemmEpilogue ep;
   ep.kind = k::kEpiStoreF32;
   ep.out = logits;
   ep.ldo = cfg_.vocab;
-  k::gemm(xn, H, dc.lm_head, H, n, cfg_.vocab, H, ep, s);
+  timed(kPhLmHead, s, [&] { k::gemm(xn, H, dc.lm_head, H, n, cfg_.vocab, H, ep, s); });
   int32_t* d_out = scratch<int32_t>(dc.out_tok, n);
-  k::argmax_rows(logits, n, cfg_.vocab, d_out, s);
+  timed(kPhArgmax, s, [&] { k::argmax_rows(logits, n, cfg_.vocab, d_out, s); });
   cuda_ok(cudaEventRecord(dc.e1, s), "event");
   check_cuda("prefill launch");
   std::vector<int32_t> first(static_cast<size_t>(n));
@@ -531,6 +583,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
             "d2h");
   }
   cuda_ok(cudaStreamSynchronize(s), "prefill");
+  collect_phase_events();
   float ms = 0;
   cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
   if (a.device_ms_out) *a.device_ms_out = ms;
@@ -558,7 +611,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
   const int n_work = static_cast<int>(work.size() / 2);
   for (int l = 0; l < cfg_.layers; ++l) {
     const LayerW& w = dc.layers[l];
-    k::rmsnorm(x, nullptr, w.norm1, xn, rows, H, cfg_.rms_eps, s);
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, rows, H, cfg_.rms_eps, s); });
     // QKV projection; epilogue: RoPE, ring stripe write, and the proactive
     // retention write of every token's K/V into its resting page slot.
     k::GemmEpilogue ep;
@@ -578,28 +631,30 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
       ep.slab_k[j] = static_cast<bf16*>(in.k_slab) + lo;
       ep.slab_v[j] = static_cast<bf16*>(in.v_slab) + lo;
     }
-    k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s);
+    timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     // Striped ring attention over all d rounds.
-    k::ring_attention(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
-                      static_cast<const k::RingSegment*>(dc.segs.ptr),
-                      static_cast<int>(segs.size()), static_cast<const int32_t*>(dc.work.ptr),
-                      n_work, scale, s);
+    timed(kPhAttention, s, [&] {
+      k::ring_attention(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
+                        static_cast<const k::RingSegment*>(dc.segs.ptr),
+                        static_cast<int>(segs.size()), static_cast<const int32_t*>(dc.work.ptr),
+                        n_work, scale, s);
+    });
     k::GemmEpilogue eo;
     eo.kind = k::kEpiResidual;
     eo.out = x;
     eo.ldo = H;
-    k::gemm(attn, H, w.wo, H, rows, H, H, eo, s);
-    k::rmsnorm(x, nullptr, w.norm2, xn, rows, H, cfg_.rms_eps, s);
+    timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, rows, H, cfg_.rms_eps, s); });
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = hbuf;
     eg.ldo = F;
-    k::gemm(xn, H, w.wgu, H, rows, 2 * F, H, eg, s);
+    timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, rows, 2 * F, H, eg, s); });
     k::GemmEpilogue ed;
     ed.kind = k::kEpiResidual;
     ed.out = x;
     ed.ldo = H;
-    k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s);
+    timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s); });
   }
 }
 
@@ -730,10 +785,10 @@ void Runtime::decode_step(const esp_decode_args& a) {
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
 
   cuda_ok(cudaEventRecord(dc.e0, s), "event");
-  k::embed(d_tok, dc.embed, x, b, H, s);
+  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, b, H, s); });
   for (int l = 0; l < cfg_.layers; ++l) {
     const LayerW& w = dc.layers[l];
-    k::rmsnorm(x, nullptr, w.norm1, xn, b, H, cfg_.rms_eps, s);
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, b, H, cfg_.rms_eps, s); });
     k::GemmEpilogue ep;
     ep.kind = k::kEpiQkvRope;
     ep.q_out = q;
@@ -752,36 +807,40 @@ void Runtime::decode_step(const esp_decode_args& a) {
       slabs.k[j] = ep.slab_k[j];
       slabs.v[j] = ep.slab_v[j];
     }
-    k::gemm(xn, H, w.wqkv, H, b, 3 * H, H, ep, s);
-    k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale, part_o,
-                        part_ml, s);
-    k::decode_combine(part_o, part_ml, d_rs, b, cfg_.heads, cfg_.head_dim, attn, s);
+    timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, b, 3 * H, H, ep, s); });
+    timed(kPhDecodeAttn, s, [&] {
+      k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
+                          part_o, part_ml, s);
+    });
+    timed(kPhCombine, s, [&] {
+      k::decode_combine(part_o, part_ml, d_rs, b, cfg_.heads, cfg_.head_dim, attn, s);
+    });
     k::GemmEpilogue eo;
     eo.kind = k::kEpiResidual;
     eo.out = x;
     eo.ldo = H;
-    k::gemm(attn, H, w.wo, H, b, H, H, eo, s);
-    k::rmsnorm(x, nullptr, w.norm2, xn, b, H, cfg_.rms_eps, s);
+    timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, b, H, H, eo, s); });
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, b, H, cfg_.rms_eps, s); });
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = hbuf;
     eg.ldo = F;
-    k::gemm(xn, H, w.wgu, H, b, 2 * F, H, eg, s);
+    timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, b, 2 * F, H, eg, s); });
     k::GemmEpilogue ed;
     ed.kind = k::kEpiResidual;
     ed.out = x;
     ed.ldo = H;
-    k::gemm(hbuf, F, w.wd, F, b, H, F, ed, s);
+    timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, b, H, F, ed, s); });
   }
-  k::rmsnorm(x, nullptr, dc.final_norm, xn, b, H, cfg_.rms_eps, s);
+  timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, dc.final_norm, xn, b, H, cfg_.rms_eps, s); });
   float* logits = scratch<float>(dc.logits, static_cast<size_t>(b) * cfg_.vocab);
   k::GemmEpilogue ef;
   ef.kind = k::kEpiStoreF32;
   ef.out = logits;
   ef.ldo = cfg_.vocab;
-  k::gemm(xn, H, dc.lm_head, H, b, cfg_.vocab, H, ef, s);
+  timed(kPhLmHead, s, [&] { k::gemm(xn, H, dc.lm_head, H, b, cfg_.vocab, H, ef, s); });
   int32_t* d_out = scratch<int32_t>(dc.out_tok, b);
-  k::argmax_rows(logits, b, cfg_.vocab, d_out, s);
+  timed(kPhArgmax, s, [&] { k::argmax_rows(logits, b, cfg_.vocab, d_out, s); });
   cuda_ok(cudaEventRecord(dc.e1, s), "event");
   check_cuda("decode launch");
   std::vector<int32_t> out(static_cast<size_t>(b));
@@ -792,6 +851,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
     cuda_ok(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
   }
   cuda_ok(cudaStreamSynchronize(s), "decode");
+  collect_phase_events();
   float ms = 0;
   cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
   if (a.device_ms_out) *a.device_ms_out = ms;

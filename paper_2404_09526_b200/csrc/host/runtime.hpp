@@ -82,6 +82,14 @@ class Runtime {
   void request_tokens(RequestId r, int32_t* out, int32_t cap, int32_t* n) const;
   void dump_profiles(const std::string& path) const;
   bool placement_only() const { return devices_.empty(); }
+  void set_profiling(bool on) { profiling_ = on; }
+  void phase_times(double* ms, int64_t* launches, int n);
+
+  // Phases of the data path timed with CUDA events when profiling is on.
+  enum Phase {
+    kPhEmbed = 0, kPhNorm, kPhQkv, kPhAttention, kPhOProj, kPhGateUp, kPhDown, kPhLmHead,
+    kPhArgmax, kPhDecodeAttn, kPhCombine, kPhCount
+  };
 
  private:
   InstanceRec& inst(InstanceId i);
@@ -97,6 +105,9 @@ class Runtime {
                               const std::vector<int32_t>& work);
   template <typename T>
   T* scratch(DevBuf& b, size_t n);
+  template <typename F>
+  void timed(int phase, cudaStream_t s, F&& f);
+  void collect_phase_events();
   void* upload(DeviceCtx& dc, const void* src, size_t bytes);
   void check_cuda(const char* what);
 
@@ -105,6 +116,15 @@ class Runtime {
   std::map<RequestId, RequestRec> requests_;
   std::vector<std::unique_ptr<DeviceCtx>> devices_;  // empty: placement-only
   std::vector<ProfileRec> profiles_;
+  bool profiling_ = false;
+  struct PhaseEvent {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<PhaseEvent> pending_;
+  std::vector<cudaEvent_t> event_pool_;
+  double phase_ms_[kPhCount] = {};
+  int64_t phase_n_[kPhCount] = {};
 };
 
 }  // namespace esp

@@ -69,12 +69,14 @@ __global__ void __launch_bounds__(kWarps * 32)
   float m = -INFINITY, l = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   const int step = kWarps * TPW;
-  for (int t0 = warp * TPW + sub; t0 < ch.n; t0 += step * kUnroll) {
+  // The loop bound is warp-uniform (full-mask shuffles inside); lanes past
+  // the end of the chunk just carry ok[u] = false.
+  for (int tw = warp * TPW; tw < ch.n; tw += step * kUnroll) {
     uint4 kr[kUnroll], vr[kUnroll];
     bool ok[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int t = t0 + u * step;
+      const int t = tw + sub + u * step;
       ok[u] = t < ch.n;
       if (ok[u]) {
         const int64_t off = static_cast<int64_t>(__ldg(&ch.slots[t])) * hidden;

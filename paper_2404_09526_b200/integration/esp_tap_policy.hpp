@@ -1,0 +1,228 @@
+// EspTapPolicy — the drop-in boundary on the reference side.
+//
+// A decorator over the reference's only plugin interface, espsim::Policy
+// (proj/include/espsim/policies.hpp:43-71), injected through Engine's
+// constructor (engine.hpp:48-49). Engine::run calls policy_->schedule() and
+// immediately apply_decision() with nothing in between (engine.cpp:680-681),
+// so a decision seen here is exactly the decision the engine commits. For
+// every decision the tap drives the B200 runtime through the C-ABI
+// (include/esp_abi.h) in apply_decision's order (engine.cpp:246-490):
+//   MigrationPlan.moves -> esp_move_kv         (engine.cpp:260-309)
+//   PrefillPlan         -> esp_prefill          (engine.cpp:311-363)
+//   DecodeStepPlan      -> esp_decode_step      (engine.cpp:365-489)
+// and before that reconciles the changes the engine makes outside
+// apply_decision: finished / rejected / evicted requests are freed
+// (engine.cpp:119-166) and "displaced" KV (resolve_foreign_kv,
+// engine.cpp:587-648) is moved. It then verifies that every request's device
+// page table equals Request.placement and every instance's used slots equal
+// ElasticInstance.kv_used, throwing espsim::InternalError on any mismatch —
+// the engine aborts exactly as on its own conservation failure
+// (cluster.cpp:113-132). Decisions are returned unchanged, so the engine's
+// behaviour (and its event log) is identical to the untapped run.
+//
+// Header-only; include after the espsim headers and link libesp_b200.so.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <memory>
+#include <random>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "esp_abi.h"
+#include "espsim/policies.hpp"
+#include "espsim/state.hpp"
+
+namespace esp_integration {
+
+// Prompt token ids of a request (the simulator's requests carry none).
+using TokenSource = std::function<std::vector<int32_t>(espsim::RequestId, espsim::TokenCount)>;
+
+inline std::vector<int32_t> synthetic_tokens(espsim::RequestId id, espsim::TokenCount n,
+                                             int32_t vocab = 32000) {
+  std::mt19937_64 rng(0x5eedULL ^ static_cast<uint64_t>(id));
+  std::vector<int32_t> t(static_cast<size_t>(n));
+  for (auto& x : t) x = static_cast<int32_t>(rng() % static_cast<uint64_t>(vocab));
+  return t;
+}
+
+// Maps a C-ABI status onto the reference's exception taxonomy.
+inline void check(int rc) {
+  if (rc == ESP_OK) return;
+  const std::string msg = std::string("esp: ") + esp_last_error();
+  switch (rc) {
+    case ESP_ERR_CONFIG: throw espsim::ConfigError(msg);
+    case ESP_ERR_INFEASIBLE: throw espsim::InfeasiblePlanError(msg);
+    case ESP_ERR_UNKNOWN_STRATEGY: throw espsim::UnknownStrategyError(msg);
+    default: throw espsim::InternalError(msg);
+  }
+}
+
+class EspTapPolicy final : public espsim::Policy {
+ public:
+  EspTapPolicy(std::unique_ptr<espsim::Policy> inner, esp_runtime* rt, bool with_tokens,
+               TokenSource tokens = nullptr)
+      : inner_(std::move(inner)), rt_(rt), with_tokens_(with_tokens),
+        tokens_(tokens ? std::move(tokens) : TokenSource([](espsim::RequestId r, espsim::TokenCount n) {
+          return synthetic_tokens(r, n);
+        })) {}
+
+  std::string name() const override { return inner_->name(); }
+
+  void init(espsim::SimState& state, const espsim::Sib& sib,
+            const espsim::SchedulerParams& params) override {
+    Policy::init(state, sib, params);
+    inner_->init(state, sib, params);
+  }
+
+  std::optional<std::string> admit(const espsim::SimState& state,
+                                   const espsim::Request& req) const override {
+    return inner_->admit(state, req);
+  }
+
+  espsim::ScheduleDecision schedule(const espsim::SimState& state,
+                                    const espsim::BandwidthModel& bw) override {
+    reconcile(state);
+    verify(state);
+    espsim::ScheduleDecision d = inner_->schedule(state, bw);
+    execute(state, d);
+    ++decisions_;
+    return d;
+  }
+
+  int64_t decisions() const { return decisions_; }
+  int64_t verified_requests() const { return verified_; }
+
+ private:
+  std::map<int32_t, int64_t> device_placement(espsim::RequestId r) const {
+    int32_t inst[64];
+    int64_t tok[64];
+    int32_t n = 0;
+    check(esp_query_placement(rt_, r, inst, tok, 64, &n));
+    std::map<int32_t, int64_t> m;
+    for (int32_t i = 0; i < std::min(n, 64); ++i) m[inst[i]] = tok[i];
+    return m;
+  }
+
+  void reconcile(const espsim::SimState& s) {
+    for (auto it = live_.begin(); it != live_.end();) {
+      const espsim::Request& q = s.requests[static_cast<size_t>(*it)];
+      if (q.phase == espsim::Phase::kFinished || q.phase == espsim::Phase::kRejected ||
+          q.placement.empty()) {
+        check(esp_free_request(rt_, *it));  // finish / evict-and-recompute
+        it = live_.erase(it);
+        continue;
+      }
+      // Engine-internal KV moves (displaced KV): surplus -> deficit.
+      auto have = device_placement(*it);
+      std::vector<std::pair<int32_t, int64_t>> surplus, deficit;
+      std::set<int32_t> ids;
+      for (auto& kv : have) ids.insert(kv.first);
+      for (auto& kv : q.placement) ids.insert(kv.first);
+      for (int32_t i : ids) {
+        const int64_t h = have.count(i) ? have[i] : 0;
+        const int64_t w = q.placement.count(i) ? q.placement.at(i) : 0;
+        if (h > w) surplus.emplace_back(i, h - w);
+        if (w > h) deficit.emplace_back(i, w - h);
+      }
+      size_t a = 0, b = 0;
+      while (a < surplus.size() && b < deficit.size()) {
+        const int64_t mv = std::min(surplus[a].second, deficit[b].second);
+        check(esp_move_kv(rt_, *it, surplus[a].first, deficit[b].first, mv));
+        if ((surplus[a].second -= mv) == 0) ++a;
+        if ((deficit[b].second -= mv) == 0) ++b;
+      }
+      ++it;
+    }
+  }
+
+  void verify(const espsim::SimState& s) {
+    for (espsim::RequestId r : live_) {
+      std::map<int32_t, int64_t> want(s.requests[static_cast<size_t>(r)].placement.begin(),
+                                      s.requests[static_cast<size_t>(r)].placement.end());
+      if (device_placement(r) != want) {
+        throw espsim::InternalError("device page table of request " + std::to_string(r) +
+                                    " drifted from its KV placement");
+      }
+      ++verified_;
+    }
+    for (const auto& inst : s.pool.instances()) {
+      int64_t cap = 0, used = 0;
+      check(esp_instance_info(rt_, inst.id, &cap, &used));
+      if (used != inst.kv_used) {
+        throw espsim::InternalError("device slots of instance " + std::to_string(inst.id) +
+                                    " drifted from kv_used");
+      }
+    }
+  }
+
+  void execute(const espsim::SimState& s, const espsim::ScheduleDecision& d) {
+    for (const espsim::MigrationPlan& m : d.migrations) {
+      for (const espsim::KvMove& mv : m.moves) {
+        check(esp_move_kv(rt_, mv.request, mv.from, mv.to, mv.tokens));
+      }
+    }
+    for (const espsim::PrefillPlan& p : d.prefills) {
+      std::vector<int64_t> ids(p.requests.begin(), p.requests.end()), lens;
+      std::vector<int32_t> ring(p.instances.begin(), p.instances.end()), rn, ri, toks;
+      std::vector<int64_t> rt;
+      for (espsim::RequestId r : p.requests) {
+        const espsim::TokenCount n = s.requests[static_cast<size_t>(r)].input_len;
+        lens.push_back(n);
+        const espsim::KvPlacement& pl = p.placement.at(r);
+        rn.push_back(static_cast<int32_t>(pl.size()));
+        for (const auto& [inst, tok] : pl) {
+          ri.push_back(inst);
+          rt.push_back(tok);
+        }
+        if (with_tokens_) {
+          auto t = tokens_(r, n);
+          toks.insert(toks.end(), t.begin(), t.end());
+        }
+        live_.insert(r);
+      }
+      esp_prefill_args a{};
+      a.n_requests = static_cast<int32_t>(ids.size());
+      a.request_ids = ids.data();
+      a.input_lens = lens.data();
+      a.tokens = with_tokens_ ? toks.data() : nullptr;
+      a.dop = static_cast<int32_t>(ring.size());
+      a.ring = ring.data();
+      a.retain_n = rn.data();
+      a.retain_instance = ri.data();
+      a.retain_tokens = rt.data();
+      check(esp_prefill(rt_, &a));
+    }
+    for (const espsim::DecodeStepPlan& p : d.decode_steps) {
+      const espsim::GroupState& gs = s.groups.at(p.group);
+      std::vector<int32_t> members(gs.group.instances.begin(), gs.group.instances.end());
+      members.insert(members.end(), p.add_instances.begin(), p.add_instances.end());
+      std::sort(members.begin(), members.end());
+      std::vector<int32_t> masters(p.masters.begin(), p.masters.end());
+      std::vector<int64_t> batch(gs.batch.begin(), gs.batch.end());
+      if (batch.empty()) continue;
+      esp_decode_args a{};
+      a.n_members = static_cast<int32_t>(members.size());
+      a.members = members.data();
+      a.n_masters = static_cast<int32_t>(masters.size());
+      a.masters = masters.data();
+      a.batch_size = static_cast<int32_t>(batch.size());
+      a.batch = batch.data();
+      check(esp_decode_step(rt_, &a));
+    }
+  }
+
+  std::unique_ptr<espsim::Policy> inner_;
+  esp_runtime* rt_;
+  bool with_tokens_;
+  TokenSource tokens_;
+  std::set<espsim::RequestId> live_;
+  int64_t decisions_ = 0;
+  int64_t verified_ = 0;
+};
+
+}  // namespace esp_integration

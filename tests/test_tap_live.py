@@ -1,0 +1,32 @@
+"""Live drop-in test: the UNMODIFIED reference engine (compiled in place from
+/root/reference by oracle/Makefile) runs with EspTapPolicy
+(paper_2404_09526_b200/integration/esp_tap_policy.hpp) around its own
+policy, driving the B200 runtime's C-ABI; page tables are verified against
+Request.placement at every schedule() call and the event log must equal the
+untapped run's. Skipped where the reference is absent (the GPU box)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = "/root/reference"
+JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "proj", "src")), reason="reference absent")
+def test_tap_policy_live(tmp_path):
+    subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "reference"], check=True,
+                   stdout=subprocess.DEVNULL)
+    exe = tmp_path / "tap_live"
+    lib_dir = os.path.join(ROOT, "paper_2404_09526_b200")
+    subprocess.run(
+        ["g++", "-std=c++20", "-O1", f"-I{REF}/proj/include", f"-I{JSON_INC}",
+         f"-I{ROOT}/include", f"-I{lib_dir}/integration", f"-I{ROOT}/oracle/shim",
+         os.path.join(ROOT, "tests", "cpp", "tap_live.cpp"),
+         os.path.join(ROOT, "oracle", "_ref", "libespsim_ref.a"),
+         f"-L{lib_dir}", "-lesp_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)],
+        check=True)
+    out = subprocess.run([str(exe), REF], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert out.stdout.count("events identical") == 3, out.stdout
