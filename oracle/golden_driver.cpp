@@ -527,8 +527,17 @@ void mechanics(const std::string& ref, const std::string& outdir) {
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc >= 4 && std::string(argv[1]) == "fit") {
+    // The measured-SIB loop: B200 ProfileSample records
+    // (esp_dump_profiles) -> the reference's own Sib::load / fit_all / save
+    // (cost_model.cpp:202-281), i.e. what `espsim fit-sib` does.
+    Sib sib = Sib::load(argv[2]);
+    sib.fit_all();
+    sib.save(argv[3]);
+    return 0;
+  }
   if (argc < 3) {
-    std::cerr << "usage: golden_driver <reference_root> <outdir>\n";
+    std::cerr << "usage: golden_driver <reference_root> <outdir> | fit <profiles> <out>\n";
     return 2;
   }
   const std::string ref = argv[1], outdir = argv[2];

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -373,8 +375,12 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
       sg.kv_len[r] = kv_len[r];
       sg.shift[r] = origin[r] > pos_i ? 1 : 0;
     }
+    // Same variant selection as the runtime: v2 (query-tile pairs) unless
+    // ESP_ATTN_V1 is set.
+    const bool pairs = std::getenv("ESP_ATTN_V1") == nullptr;
+    const int span = pairs ? 2 : 1;
     std::vector<int32_t> work;
-    for (int qt = 0; qt < esp::k::q_tiles(q_len); ++qt) {
+    for (int qt = 0; qt < (esp::k::q_tiles(q_len) + span - 1) / span; ++qt) {
       for (int h = 0; h < heads; ++h) {
         work.push_back(0);
         work.push_back((qt << 8) | h);
@@ -386,9 +392,14 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
     cudaMalloc(&dwork, work.size() * 4);
     cudaMemcpyAsync(dseg, &sg, sizeof(sg), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(dwork, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s);
-    esp::k::ring_attention(Q, K, V, O, static_cast<int>(rows), heads, head_dim, dseg, 1, dwork,
-                           static_cast<int>(work.size() / 2),
-                           1.0f / std::sqrt(static_cast<float>(head_dim)), s);
+    const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
+    if (pairs) {
+      esp::k::ring_attention_pairs(Q, K, V, O, static_cast<int>(rows), heads, head_dim, dseg,
+                                   dwork, static_cast<int>(work.size() / 2), scale, s);
+    } else {
+      esp::k::ring_attention(Q, K, V, O, static_cast<int>(rows), heads, head_dim, dseg, 1, dwork,
+                             static_cast<int>(work.size() / 2), scale, s);
+    }
     cudaMemcpyAsync(out, O, static_cast<size_t>(q_len) * hidden * 2, cudaMemcpyDeviceToDevice, s);
     const cudaError_t e = cudaStreamSynchronize(s);
     cudaFree(Q);

@@ -494,17 +494,23 @@ void Runtime::prefill(const esp_prefill_args& a) {
       }
       const int seg_idx = static_cast<int>(segs.size());
       segs.push_back(sg);
-      for (int qt = 0; qt < k::q_tiles(ql); ++qt) {
+      // One work item per (query tile, head) for v1, per (query-tile pair,
+      // head) for v2; cost = visible KV tiles (LPT ordering below).
+      const int span = attn_pairs_ ? 2 : 1;
+      const int n_items = (k::q_tiles(ql) + span - 1) / span;
+      for (int qi = 0; qi < n_items; ++qi) {
         int64_t cost = 0;
-        for (int rd = 0; rd < d; ++rd) {
-          const int64_t vis = std::min<int64_t>(sg.kv_len[rd],
-                                                std::min(qt * 128 + 127, ql - 1) - sg.shift[rd] + 1);
-          cost += vis > 0 ? (vis + 127) / 128 : 0;
+        for (int qt = qi * span; qt < std::min(k::q_tiles(ql), (qi + 1) * span); ++qt) {
+          for (int rd = 0; rd < d; ++rd) {
+            const int64_t vis = std::min<int64_t>(
+                sg.kv_len[rd], std::min(qt * 128 + 127, ql - 1) - sg.shift[rd] + 1);
+            cost += vis > 0 ? (vis + 127) / 128 : 0;
+          }
         }
         for (int hd = 0; hd < cfg_.heads; ++hd) {
           order.emplace_back(cost, static_cast<int>(work.size() / 2));
           work.push_back(seg_idx);
-          work.push_back((qt << 8) | hd);
+          work.push_back((qi << 8) | hd);
         }
       }
     }
@@ -634,10 +640,16 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
     timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     // Striped ring attention over all d rounds.
     timed(kPhAttention, s, [&] {
-      k::ring_attention(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
-                        static_cast<const k::RingSegment*>(dc.segs.ptr),
-                        static_cast<int>(segs.size()), static_cast<const int32_t*>(dc.work.ptr),
-                        n_work, scale, s);
+      if (attn_pairs_) {
+        k::ring_attention_pairs(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
+                                static_cast<const k::RingSegment*>(dc.segs.ptr),
+                                static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
+      } else {
+        k::ring_attention(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
+                          static_cast<const k::RingSegment*>(dc.segs.ptr),
+                          static_cast<int>(segs.size()),
+                          static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
+      }
     });
     k::GemmEpilogue eo;
     eo.kind = k::kEpiResidual;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <string>
@@ -117,6 +118,8 @@ class Runtime {
   std::vector<std::unique_ptr<DeviceCtx>> devices_;  // empty: placement-only
   std::vector<ProfileRec> profiles_;
   bool profiling_ = false;
+  // K1 variant: v2 (two query tiles per CTA, P in TMEM) unless ESP_ATTN_V1=1.
+  bool attn_pairs_ = std::getenv("ESP_ATTN_V1") == nullptr;
   struct PhaseEvent {
     int phase;
     cudaEvent_t a, b;

@@ -63,6 +63,12 @@ void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int 
                     int heads, int head_dim, const RingSegment* d_segs, int n_segs,
                     const int32_t* d_work, int n_work, float scale, cudaStream_t s);
 
+// v2: two 128-row query tiles per CTA (P kept in TMEM); work items are
+// (segment, query-tile PAIR, head). Same semantics as ring_attention.
+void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out,
+                          int total_rows, int heads, int head_dim, const RingSegment* d_segs,
+                          const int32_t* d_work, int n_work, float scale, cudaStream_t s);
+
 // Work-list builder helper: number of 128-row q tiles of a segment.
 inline int q_tiles(int q_len) { return (q_len + 127) / 128; }
 

@@ -1,0 +1,456 @@
+// K1 (v2): striped ring attention, two query tiles per CTA.
+//
+// Same math and striped-causal mask as ring_attention.cu (v1), restructured
+// so the tensor core never waits on one softmax:
+//   * a CTA owns 256 query rows = two 128-row tiles (t = 0, 1) of the same
+//     (segment, head); both share every K/V tile loaded by TMA;
+//   * TMEM = S0 | S1 | O0 | O1 (512 columns). Tile t's softmax reads S_t,
+//     writes P_t (bf16, 2 per 32-bit column) back over S_t, and the MMA warp
+//     issues O_t += P_t V with A read straight from TMEM (no smem round trip);
+//   * the MMA warp interleaves the tiles: PV_0,j  S_0,j+1  PV_1,j  S_1,j+1 —
+//     while softmax WG 0 works on S_0,j+1 the tensor core runs tile 1's PV and
+//     S, and vice versa;
+//   * warp-group register split with setmaxnreg (producer/MMA WG shrinks,
+//     the two softmax WGs grow).
+// The union of the two tiles' visible KV tiles is streamed once; tile 0
+// (earlier queries) skips the causal tail it cannot see.
+#include <cuda.h>
+
+#include <mutex>
+#include <stdexcept>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace esp::k {
+
+CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t ld,
+                           int box_rows);
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int kStages = 2;
+constexpr int kThreads = 384;
+constexpr float kRescaleThreshold = 8.0f;
+
+template <int HD>
+struct Cfg2 {
+  static constexpr int kBoxes = HD / 64;
+  static constexpr int kQBytes = BM * HD * 2;
+  static constexpr int kKvBytes = BN * HD * 2;
+  static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + 1024 + 512;
+};
+
+__device__ __forceinline__ int tiles_visible(const RingSegment& sg, int r, int q0) {
+  const int a_max = min(q0 + BM - 1, sg.q_len - 1);
+  const int vis = min(sg.kv_len[r], a_max - sg.shift[r] + 1);
+  return vis <= 0 ? 0 : (vis + BN - 1) / BN;
+}
+
+struct Item {
+  int seg, pair, head;
+  int q0[2];
+  bool act1;  // tile 1 exists (q rows past q_len are not a tile)
+};
+
+__device__ __forceinline__ Item load_item(const int32_t* work, int w,
+                                          const RingSegment* segs) {
+  Item it;
+  it.seg = __ldg(&work[2 * w]);
+  const int packed = __ldg(&work[2 * w + 1]);
+  it.pair = packed >> 8;
+  it.head = packed & 0xFF;
+  it.q0[0] = it.pair * 2 * BM;
+  it.q0[1] = it.q0[0] + BM;
+  it.act1 = it.q0[1] < segs[it.seg].q_len;
+  return it;
+}
+
+// Iterates the union KV-tile sequence of an item: (round r, tile tt) and
+// whether each query tile sees it.
+struct Steps {
+  const RingSegment* sg;
+  int q_own;  // q0 of the tile that owns the union (tile 1 if active)
+  int q0t0;
+  int r = 0, tt = 0, n_r = 0, n0_r = 0;
+  __device__ void begin(const RingSegment* s, const Item& it) {
+    sg = s;
+    q_own = it.act1 ? it.q0[1] : it.q0[0];
+    q0t0 = it.q0[0];
+    r = -1;
+    tt = 0;
+    n_r = 0;
+    advance_round();
+  }
+  __device__ void advance_round() {
+    do {
+      ++r;
+      if (r >= sg->n_rounds) return;
+      n_r = tiles_visible(*sg, r, q_own);
+      n0_r = tiles_visible(*sg, r, q0t0);
+      tt = 0;
+    } while (n_r == 0);
+  }
+  __device__ bool valid() const { return r < sg->n_rounds; }
+  __device__ void next() {
+    if (++tt >= n_r) advance_round();
+  }
+  __device__ int kv_row() const { return sg->kv_row0[r] + tt * BN; }
+  __device__ bool active0() const { return tt < n0_r; }
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 1)
+    ring_attention_v2(const __grid_constant__ CUtensorMap tmQ,
+                      const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ out,
+                      int hidden, const RingSegment* __restrict__ segs,
+                      const int32_t* __restrict__ work, int n_work, float scale_log2) {
+  using C = Cfg2<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;                                 // [2][kQBytes]
+  uint8_t* sK = sQ + 2 * C::kQBytes;                  // [kStages][kKvBytes]
+  uint8_t* sV = sK + kStages * C::kKvBytes;           // [kStages][kKvBytes]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * C::kKvBytes);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + kStages;
+  uint64_t* v_full = k_empty + kStages;
+  uint64_t* v_empty = v_full + kStages;
+  uint64_t* s_full = v_empty + kStages;  // [2] per query tile
+  uint64_t* p_full = s_full + 2;         // [2]
+  uint64_t* o_done = p_full + 2;         // [2]
+  uint64_t* o_free = o_done + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmQ);
+    ptx::tma_prefetch_desc(&tmK);
+    ptx::tma_prefetch_desc(&tmV);
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&o_done[t], 1);
+      ptx::mbar_init(&o_free[t], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s[2] = {tmem, tmem + BN};
+  const uint32_t t_o[2] = {tmem + 2 * BN, tmem + 2 * BN + HD};
+
+  if (warp < 4) {
+    ptx::setmaxnreg_dec<104>();
+    if (warp == 0 && lane == 0) {
+      // ---------------------------------------------------------- producer
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0, items = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++items) {
+        const Item it = load_item(work, w, segs);
+        const RingSegment* sg = &segs[it.seg];
+        ptx::mbar_wait(q_empty, (items & 1) ^ 1);
+        ptx::mbar_expect_tx(q_full, C::kQBytes * (it.act1 ? 2 : 1));
+        for (int t = 0; t < (it.act1 ? 2 : 1); ++t) {
+          for (int b = 0; b < C::kBoxes; ++b) {
+            ptx::tma_load_2d(sQ + t * C::kQBytes + b * (BM * 128), &tmQ, q_full,
+                             it.head * HD + b * 64, sg->q_row0 + it.q0[t]);
+          }
+        }
+        Steps st;
+        for (st.begin(sg, it); st.valid(); st.next()) {
+          const int row = st.kv_row();
+          ptx::mbar_wait(&k_empty[ks], kph ^ 1);
+          ptx::mbar_expect_tx(&k_full[ks], C::kKvBytes);
+          for (int b = 0; b < C::kBoxes; ++b) {
+            ptx::tma_load_2d(sK + ks * C::kKvBytes + b * (BN * 128), &tmK, &k_full[ks],
+                             it.head * HD + b * 64, row);
+          }
+          if (++ks == kStages) { ks = 0; kph ^= 1; }
+          ptx::mbar_wait(&v_empty[vs], vph ^ 1);
+          ptx::mbar_expect_tx(&v_full[vs], C::kKvBytes);
+          for (int b = 0; b < C::kBoxes; ++b) {
+            ptx::tma_load_2d(sV + vs * C::kKvBytes + b * (BN * 128), &tmV, &v_full[vs],
+                             it.head * HD + b * 64, row);
+          }
+          if (++vs == kStages) { vs = 0; vph ^= 1; }
+        }
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc_s = ptx::make_idesc_bf16(BM, BN, false, false);
+      constexpr uint32_t idesc_o = ptx::make_idesc_bf16(BM, HD, false, true);
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0, items = 0;
+      uint32_t cnt[2] = {0, 0};    // per-tile global step count (barrier phases)
+      uint32_t titems[2] = {0, 0}; // per-tile item count (o_free phases)
+      const uint32_t q_addr[2] = {ptx::smem_u32(sQ), ptx::smem_u32(sQ + C::kQBytes)};
+      auto issue_s = [&](int t, uint32_t k_addr) {
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k >> 2) * (BM * 128) + (k & 3) * 32;
+          ptx::umma_f16_ss(t_s[t], ptx::make_sdesc_sw128(q_addr[t] + off, 16, 1024),
+                           ptx::make_sdesc_sw128(k_addr + off, 16, 1024), idesc_s, k != 0);
+        }
+        ptx::tc_commit(&s_full[t]);
+      };
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++items) {
+        const Item it = load_item(work, w, segs);
+        const RingSegment* sg = &segs[it.seg];
+        const bool act[2] = {true, it.act1};
+        ptx::mbar_wait(q_full, items & 1);
+        ptx::tc_fence_after();
+        Steps st;
+        st.begin(sg, it);
+        // Prologue: S_t,0 for every tile that sees the first KV tile.
+        {
+          ptx::mbar_wait(&k_full[ks], kph);
+          ptx::tc_fence_after();
+          const uint32_t k_addr = ptx::smem_u32(sK + ks * C::kKvBytes);
+          if (st.active0()) issue_s(0, k_addr);
+          if (act[1]) issue_s(1, k_addr);
+          ptx::tc_commit(&k_empty[ks]);
+          if (++ks == kStages) { ks = 0; kph ^= 1; }
+        }
+        bool first_pv[2] = {true, true};
+        while (st.valid()) {
+          const bool a_now[2] = {st.active0(), act[1]};
+          Steps nx = st;
+          nx.next();
+          const bool has_next = nx.valid();
+          const bool a_next[2] = {has_next && nx.active0(), has_next && act[1]};
+          ptx::mbar_wait(&v_full[vs], vph);
+          uint32_t k_addr = 0;
+          if (has_next) {
+            ptx::mbar_wait(&k_full[ks], kph);
+            k_addr = ptx::smem_u32(sK + ks * C::kKvBytes);
+          }
+          const uint32_t v_addr = ptx::smem_u32(sV + vs * C::kKvBytes);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (a_now[t]) {
+              if (first_pv[t]) ptx::mbar_wait(&o_free[t], (titems[t] & 1) ^ 1);
+              ptx::mbar_wait(&p_full[t], cnt[t] & 1);
+              ptx::tc_fence_after();
+#pragma unroll
+              for (int k = 0; k < BN / 16; ++k) {
+                ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8,
+                                 ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024),
+                                 idesc_o, (!first_pv[t] || k != 0) ? 1u : 0u);
+              }
+              ptx::tc_commit(&o_done[t]);
+              first_pv[t] = false;
+              ++cnt[t];
+            }
+            // S_t of the next step overwrites P_t in TMEM: issued after PV_t
+            // (tcgen05.mma executes in issue order). A tile idle at this step
+            // (tile 0 past its causal limit in this round) may be active again
+            // at the next round's first step.
+            if (a_next[t]) {
+              ptx::tc_fence_after();
+              issue_s(t, k_addr);
+            }
+          }
+          ptx::tc_commit(&v_empty[vs]);
+          if (++vs == kStages) { vs = 0; vph ^= 1; }
+          if (has_next) {
+            ptx::tc_commit(&k_empty[ks]);
+            if (++ks == kStages) { ks = 0; kph ^= 1; }
+          }
+          st = nx;
+        }
+        ptx::tc_commit(q_empty);
+        for (int t = 0; t < 2; ++t) titems[t] += act[t] ? 1 : 0;
+      }
+    }
+  } else {
+    ptx::setmaxnreg_inc<192>();
+    // ------------------------------------------------------------ softmax
+    const int t = (warp >= 8) ? 1 : 0;
+    const uint32_t quad = warp & 3;
+    const int row = static_cast<int>(quad * 32 + lane);
+    const uint32_t lane_off = (quad * 32) << 16;
+    uint32_t cnt = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const Item it = load_item(work, w, segs);
+      if (t == 1 && !it.act1) continue;
+      const RingSegment* sg = &segs[it.seg];
+      const int q0 = it.q0[t];
+      const int a = q0 + row;
+      float m_run = -INFINITY, l_run = 0.f;
+      int j = 0;
+      Steps st;
+      for (st.begin(sg, it); st.valid(); st.next()) {
+        if (t == 0 && !st.active0()) continue;
+        const int b0 = st.tt * BN;
+        const int shift = sg->shift[st.r];
+        const int kv_len = sg->kv_len[st.r];
+        ptx::mbar_wait(&s_full[t], cnt & 1);
+        ptx::tc_fence_after();
+        uint32_t s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
+          ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 32 * c, chunk);
+        }
+        ptx::tmem_wait_ld();
+        const bool full_tile = (b0 + BN - 1 <= q0 - shift) && (b0 + BN <= kv_len);
+        float mx = -INFINITY;
+        if (full_tile) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
+        } else {
+          const int lim = min(a - shift - b0, kv_len - 1 - b0);
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            if (c > lim) s[c] = __float_as_uint(-INFINITY);
+            mx = fmaxf(mx, __uint_as_float(s[c]));
+          }
+        }
+        const float m_tile = mx * scale_log2;
+        const float m_new = fmaxf(m_run, m_tile);
+        const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY)
+                                               : (m_new > m_run + kRescaleThreshold);
+        float alpha = 1.f;
+        if (need) {
+          alpha = m_run == -INFINITY ? 0.f : ptx::ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        const float m_sub = m_run == -INFINITY ? 0.f : m_run;
+        // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
+        // precede the write of s[c], c <= 2c), then P over S_t in TMEM.
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float p0 = ptx::ex2(fmaf(__uint_as_float(s[2 * c]), scale_log2, -m_sub));
+          const float p1 = ptx::ex2(fmaf(__uint_as_float(s[2 * c + 1]), scale_log2, -m_sub));
+          sum += p0 + p1;
+          s[c] = ptx::pack_bf16(p0, p1);
+        }
+        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        if (j > 0 && __any_sync(0xffffffff, need)) {
+          // O holds PV_{j-1}: wait for it, then rescale in TMEM (rare: only
+          // when a row max grew by more than 2^8).
+          ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t o[32];
+            ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            ptx::tmem_st_32x32b_x32(t_o[t] + lane_off + c, o);
+          }
+        }
+        ptx::tmem_wait_st();
+        l_run = l_run * alpha + sum;
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[t]);
+        ++cnt;
+        ++j;
+      }
+      // Final O / l for this tile's rows.
+      ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
+      ptx::tc_fence_after();
+      const bool valid = a < sg->q_len;
+      const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+      bf16* orow = out + static_cast<int64_t>(sg->q_row0 + a) * hidden + it.head * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
+        ptx::tmem_wait_ld();
+        if (valid) {
+          uint4* d = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            d[i] = make_uint4(ptx::pack_bf16(__uint_as_float(o[8 * i]) * inv_l,
+                                             __uint_as_float(o[8 * i + 1]) * inv_l),
+                              ptx::pack_bf16(__uint_as_float(o[8 * i + 2]) * inv_l,
+                                             __uint_as_float(o[8 * i + 3]) * inv_l),
+                              ptx::pack_bf16(__uint_as_float(o[8 * i + 4]) * inv_l,
+                                             __uint_as_float(o[8 * i + 5]) * inv_l),
+                              ptx::pack_bf16(__uint_as_float(o[8 * i + 6]) * inv_l,
+                                             __uint_as_float(o[8 * i + 7]) * inv_l));
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&o_free[t]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+int sm_count2() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int HD>
+void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_rows, int heads,
+             const RingSegment* segs, const int32_t* work, int n_work, float scale,
+             cudaStream_t s) {
+  using C = Cfg2<HD>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(ring_attention_v2<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmem);
+  });
+  const int hidden = heads * HD;
+  const CUtensorMap tq = make_tmap_bf16(q, total_rows, hidden, hidden, BM);
+  const CUtensorMap tk = make_tmap_bf16(k, total_rows, hidden, hidden, BN);
+  const CUtensorMap tv = make_tmap_bf16(v, total_rows, hidden, hidden, BN);
+  const int grid = n_work < sm_count2() ? n_work : sm_count2();
+  ring_attention_v2<HD><<<grid, kThreads, C::kSmem, s>>>(tq, tk, tv, out, hidden, segs, work,
+                                                         n_work, scale * 1.4426950408889634f);
+  count_launch();
+}
+
+}  // namespace
+
+// Work items for v2 are (segment, 256-row query-tile PAIR, head).
+void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out,
+                          int total_rows, int heads, int head_dim, const RingSegment* d_segs,
+                          const int32_t* d_work, int n_work, float scale, cudaStream_t s) {
+  if (n_work <= 0) return;
+  if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
+  if (head_dim == 128) {
+    launch2<128>(q, k, v, out, total_rows, heads, d_segs, d_work, n_work, scale, s);
+  } else if (head_dim == 64) {
+    launch2<64>(q, k, v, out, total_rows, heads, d_segs, d_work, n_work, scale, s);
+  } else {
+    throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
+  }
+}
+
+}  // namespace esp::k

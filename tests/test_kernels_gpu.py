@@ -84,12 +84,22 @@ def _ref_striped(q, ks, vs, pos_i, d, origins, heads, hd):
     return torch.einsum("hqk,khd->qhd", p, V).reshape(L, heads * hd)
 
 
+@pytest.fixture(params=["v2", "v1"])
+def attn_variant(request, monkeypatch):
+    """K1 variants: v2 (two query tiles / CTA, P in TMEM; default) and v1."""
+    if request.param == "v1":
+        monkeypatch.setenv("ESP_ATTN_V1", "1")
+    else:
+        monkeypatch.delenv("ESP_ATTN_V1", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("S,d,pos_i,heads,hd", [(128, 1, 0, 2, 128), (1000, 1, 0, 4, 128),
                                                 (4096, 1, 0, 8, 64), (2000, 2, 0, 4, 128),
                                                 (2001, 2, 1, 4, 128), (3000, 4, 2, 2, 64),
                                                 (5000, 8, 5, 2, 128), (700, 8, 0, 3, 128),
-                                                (77, 4, 3, 2, 64)])
-def test_ring_attention_striped(S, d, pos_i, heads, hd):
+                                                (77, 4, 3, 2, 64), (1500, 3, 2, 2, 128)])
+def test_ring_attention_striped(S, d, pos_i, heads, hd, attn_variant):
     torch.manual_seed(S + d + pos_i)
     H = heads * hd
     lens = [len(range(o, S, d)) for o in range(d)]
