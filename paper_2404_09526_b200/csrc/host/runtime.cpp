@@ -189,13 +189,19 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
         cap = avail / (static_cast<int64_t>(dc.slabs.size()) * bpt);
         if (cap <= 0) throw ConfigError("no HBM left for KV slabs");
       }
+      // Slabs reserve the full logical capacity as virtual address space and
+      // are backed on demand (slot high-water mark), so co-located instances
+      // only consume HBM for resident tokens.
+      const size_t row_bytes = static_cast<size_t>(cfg.hidden) * 2;
       for (InstanceId id : dc.slabs) {
         InstanceRec& in = instances_[id];
         in.capacity = cap;
-        const size_t bytes = static_cast<size_t>(cap) * static_cast<size_t>(bpt) / 2;
-        cuda_ok(cudaMalloc(&in.k_slab, bytes), "cudaMalloc(K slab)");
-        cuda_ok(cudaMalloc(&in.v_slab, bytes), "cudaMalloc(V slab)");
+        in.k_slab = std::make_unique<LazySlab>();
+        in.v_slab = std::make_unique<LazySlab>();
+        in.k_slab->reserve(dc.device, cfg.layers, cap, row_bytes);
+        in.v_slab->reserve(dc.device, cfg.layers, cap, row_bytes);
       }
+      (void)bpt;
     }
   }
   for (auto& in : instances_) {
@@ -220,8 +226,8 @@ Runtime::~Runtime() {
     }
   }
   for (auto& in : instances_) {
-    if (in.k_slab) cudaFree(in.k_slab);
-    if (in.v_slab) cudaFree(in.v_slab);
+    in.k_slab.reset();
+    in.v_slab.reset();
   }
   for (auto& dcp : devices_) {
     DeviceCtx& dc = *dcp;
@@ -303,6 +309,17 @@ std::vector<int32_t> Runtime::take_slots(InstanceRec& in, int64_t n) {
   }
   std::vector<int32_t> out(in.free_stack.end() - n, in.free_stack.end());
   std::reverse(out.begin(), out.end());
+  if (in.k_slab && n > 0) {
+    // Back the slab up to the highest slot handed out (before any counter
+    // moves, so an out-of-memory here leaves the pool untouched).
+    const int64_t top = *std::max_element(out.begin(), out.end()) + 1;
+    if (top > in.high_water) {
+      DeviceGuard g(in.device);
+      in.k_slab->ensure(top);
+      in.v_slab->ensure(top);
+      in.high_water = top;
+    }
+  }
   in.free_stack.resize(in.free_stack.size() - static_cast<size_t>(n));
   in.used += n;
   return out;
@@ -515,9 +532,18 @@ void Runtime::prefill(const esp_prefill_args& a) {
       }
     }
   }
-  // Longest work first (persistent CTAs take items round-robin).
-  std::stable_sort(order.begin(), order.end(),
-                   [](const auto& x, const auto& y) { return x.first > y.first; });
+  // Persistent CTAs take items round-robin. Heads are processed in groups
+  // whose K/V (rows x 512 B per head) fit comfortably in L2 (~64 MiB), so the
+  // concurrently running items share K/V tiles; within a group, longest work
+  // first (LPT) for balance.
+  const int64_t head_kv_bytes = static_cast<int64_t>(rows) * cfg_.head_dim * 2 * 2;
+  const int head_group =
+      static_cast<int>(std::max<int64_t>(1, (static_cast<int64_t>(64) << 20) / std::max<int64_t>(head_kv_bytes, 1)));
+  std::stable_sort(order.begin(), order.end(), [&](const auto& x, const auto& y) {
+    const int gx = (work[2 * x.second + 1] & 0xFF) / head_group;
+    const int gy = (work[2 * y.second + 1] & 0xFF) / head_group;
+    return gx != gy ? gx < gy : x.first > y.first;
+  });
   std::vector<int32_t> work_sorted;
   work_sorted.reserve(work.size());
   for (const auto& o : order) {
@@ -633,9 +659,8 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
     ep.row_slot = static_cast<const int32_t*>(dc.rslot.ptr);
     for (size_t j = 0; j < dc.slabs.size(); ++j) {
       const InstanceRec& in = instances_[dc.slabs[j]];
-      const int64_t lo = static_cast<int64_t>(l) * in.capacity * H;
-      ep.slab_k[j] = static_cast<bf16*>(in.k_slab) + lo;
-      ep.slab_v[j] = static_cast<bf16*>(in.v_slab) + lo;
+      ep.slab_k[j] = in.layer_k(l);
+      ep.slab_v[j] = in.layer_v(l);
     }
     timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     // Striped ring attention over all d rounds.
@@ -813,9 +838,8 @@ void Runtime::decode_step(const esp_decode_args& a) {
     k::DecodeSlabs slabs{};
     for (size_t j = 0; j < dc.slabs.size(); ++j) {
       const InstanceRec& in = instances_[dc.slabs[j]];
-      const int64_t lo = static_cast<int64_t>(l) * in.capacity * H;
-      ep.slab_k[j] = static_cast<bf16*>(in.k_slab) + lo;
-      ep.slab_v[j] = static_cast<bf16*>(in.v_slab) + lo;
+      ep.slab_k[j] = in.layer_k(l);
+      ep.slab_v[j] = in.layer_v(l);
       slabs.k[j] = ep.slab_k[j];
       slabs.v[j] = ep.slab_v[j];
     }
@@ -908,10 +932,9 @@ void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t token
     int32_t* d_b = scratch<int32_t>(dc.pos, static_cast<size_t>(tokens));
     cuda_ok(cudaMemcpyAsync(d_a, moving.data(), tokens * 4, cudaMemcpyHostToDevice, dc.stream), "h2d");
     cuda_ok(cudaMemcpyAsync(d_b, dslots.data(), tokens * 4, cudaMemcpyHostToDevice, dc.stream), "h2d");
-    k::copy_slots(static_cast<bf16*>(src.k_slab), static_cast<bf16*>(src.v_slab), d_a,
-                  static_cast<bf16*>(dst.k_slab), static_cast<bf16*>(dst.v_slab), d_b,
-                  static_cast<int>(tokens), cfg_.layers, src.capacity, dst.capacity,
-                  cfg_.hidden, dc.stream);
+    k::copy_slots(src.layer_k(0), src.layer_v(0), d_a, dst.layer_k(0), dst.layer_v(0), d_b,
+                  static_cast<int>(tokens), cfg_.layers, src.k_slab->layer_stride_elems(),
+                  dst.k_slab->layer_stride_elems(), cfg_.hidden, dc.stream);
     check_cuda("move_kv");
     cuda_ok(cudaStreamSynchronize(dc.stream), "move_kv");
   }

@@ -13,10 +13,15 @@
 #include <string>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "esp_abi.h"
 #include "planner.hpp"
+#include "slab.hpp"
 
 namespace esp {
+
+using k_bf16 = __nv_bfloat16;
 
 namespace k {
 struct RingSegment;
@@ -50,8 +55,15 @@ struct InstanceRec {
   int64_t capacity = 0;
   int64_t used = 0;
   std::vector<int32_t> free_stack;  // back() is the next slot handed out
-  void* k_slab = nullptr;           // [layers][capacity][hidden] bf16
-  void* v_slab = nullptr;
+  // [layers][capacity][hidden] bf16, lazily backed (slab.hpp)
+  std::unique_ptr<LazySlab> k_slab, v_slab;
+  int64_t high_water = 0;  // slots [0, high_water) are physically backed
+  k_bf16* layer_k(int l) const {
+    return static_cast<k_bf16*>(k_slab->base()) + static_cast<int64_t>(l) * k_slab->layer_stride_elems();
+  }
+  k_bf16* layer_v(int l) const {
+    return static_cast<k_bf16*>(v_slab->base()) + static_cast<int64_t>(l) * v_slab->layer_stride_elems();
+  }
 };
 
 struct DevBuf {

@@ -109,10 +109,11 @@ void fill_bf16(bf16* dst, int64_t n, float v, cudaStream_t s);
 void count_slots(const int32_t* slots, int64_t n, int32_t* counts, int capacity,
                  cudaStream_t s);
 void check_counts(const int32_t* counts, int capacity, int32_t* result /*[2]*/, cudaStream_t s);
-// KV move: copy slab rows (all layers) between slots / slabs.
+// KV move: copy slab rows (all layers) between slots / slabs. Layer l of a
+// slab starts l * layer_stride elements after its base.
 void copy_slots(const bf16* src_k, const bf16* src_v, const int32_t* src_slots, bf16* dst_k,
-                bf16* dst_v, const int32_t* dst_slots, int n, int layers, int64_t src_cap,
-                int64_t dst_cap, int hidden, cudaStream_t s);
+                bf16* dst_v, const int32_t* dst_slots, int n, int layers,
+                int64_t src_layer_stride, int64_t dst_layer_stride, int hidden, cudaStream_t s);
 
 int64_t launch_count();
 void count_launch();

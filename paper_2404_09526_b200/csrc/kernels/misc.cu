@@ -180,10 +180,10 @@ __global__ void check_counts_kernel(const int32_t* counts, int cap, int32_t* res
 __global__ void copy_slots_kernel(const bf16* __restrict__ sk, const bf16* __restrict__ sv,
                                   const int32_t* __restrict__ ss, bf16* __restrict__ dk,
                                   bf16* __restrict__ dv, const int32_t* __restrict__ ds,
-                                  int layers, int64_t scap, int64_t dcap, int hidden) {
+                                  int layers, int64_t sstride, int64_t dstride, int hidden) {
   const int t = blockIdx.x, layer = blockIdx.y;
-  const int64_t so = (static_cast<int64_t>(layer) * scap + ss[t]) * hidden;
-  const int64_t dof = (static_cast<int64_t>(layer) * dcap + ds[t]) * hidden;
+  const int64_t so = static_cast<int64_t>(layer) * sstride + static_cast<int64_t>(ss[t]) * hidden;
+  const int64_t dof = static_cast<int64_t>(layer) * dstride + static_cast<int64_t>(ds[t]) * hidden;
   const uint4* a = reinterpret_cast<const uint4*>(sk + so);
   const uint4* b = reinterpret_cast<const uint4*>(sv + so);
   uint4* c = reinterpret_cast<uint4*>(dk + dof);
@@ -249,11 +249,12 @@ void check_counts(const int32_t* counts, int capacity, int32_t* result, cudaStre
 }
 
 void copy_slots(const bf16* src_k, const bf16* src_v, const int32_t* src_slots, bf16* dst_k,
-                bf16* dst_v, const int32_t* dst_slots, int n, int layers, int64_t src_cap,
-                int64_t dst_cap, int hidden, cudaStream_t s) {
+                bf16* dst_v, const int32_t* dst_slots, int n, int layers,
+                int64_t src_layer_stride, int64_t dst_layer_stride, int hidden, cudaStream_t s) {
   if (n <= 0) return;
   copy_slots_kernel<<<dim3(n, layers), 128, 0, s>>>(src_k, src_v, src_slots, dst_k, dst_v,
-                                                    dst_slots, layers, src_cap, dst_cap, hidden);
+                                                    dst_slots, layers, src_layer_stride,
+                                                    dst_layer_stride, hidden);
   count_launch();
 }
 

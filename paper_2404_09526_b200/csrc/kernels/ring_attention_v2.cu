@@ -43,6 +43,22 @@ struct Cfg2 {
   static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + 1024 + 512;
 };
 
+// 2^x on the FMA/ALU pipes (x <= 2^7): round-to-nearest split x = n + f via
+// the 1.5*2^23 trick, Taylor cubic for 2^f on [-1/2, 1/2] (rel. err < 7e-4,
+// below the bf16 rounding P gets anyway), exponent add for 2^n. Used for a
+// quarter of the softmax exponentials so the MUFU (ex2) pipe is not the
+// co-bottleneck with the tensor core.
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(0.0555041087f, f, 0.240226507f);
+  p = fmaf(p, f, 0.693147181f);
+  p = fmaf(p, f, 1.0f);
+  const int n = __float_as_int(t) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (n << 23));
+}
+
 __device__ __forceinline__ int tiles_visible(const RingSegment& sg, int r, int q0) {
   const int a_max = min(q0 + BM - 1, sg.q_len - 1);
   const int vis = min(sg.kv_len[r], a_max - sg.shift[r] + 1);
@@ -312,18 +328,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::tmem_wait_ld();
         const bool full_tile = (b0 + BN - 1 <= q0 - shift) && (b0 + BN <= kv_len);
-        float mx = -INFINITY;
-        if (full_tile) {
-#pragma unroll
-          for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
-        } else {
+        if (!full_tile) {
           const int lim = min(a - shift - b0, kv_len - 1 - b0);
 #pragma unroll
           for (int c = 0; c < 128; ++c) {
             if (c > lim) s[c] = __float_as_uint(-INFINITY);
-            mx = fmaxf(mx, __uint_as_float(s[c]));
           }
         }
+        // Row max with 8 independent chains (ILP), then a tree.
+        float mx8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(s[k]);
+#pragma unroll
+        for (int c = 8; c < 128; c += 8) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(s[c + k]));
+        }
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         const float m_tile = mx * scale_log2;
         const float m_new = fmaxf(m_run, m_tile);
         const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY)
@@ -336,14 +358,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_sub = m_run == -INFINITY ? 0.f : m_run;
         // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
         // precede the write of s[c], c <= 2c), then P over S_t in TMEM.
-        float sum = 0.f;
+        float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
-          const float p0 = ptx::ex2(fmaf(__uint_as_float(s[2 * c]), scale_log2, -m_sub));
-          const float p1 = ptx::ex2(fmaf(__uint_as_float(s[2 * c + 1]), scale_log2, -m_sub));
-          sum += p0 + p1;
+          const float x0 = fmaf(__uint_as_float(s[2 * c]), scale_log2, -m_sub);
+          const float x1 = fmaf(__uint_as_float(s[2 * c + 1]), scale_log2, -m_sub);
+          const float p0 = ptx::ex2(x0);
+          // every 4th exponential on the FMA pipe (x1 of odd pairs)
+          const float p1 = (c & 1) ? exp2_fma(x1) : ptx::ex2(x1);
+          sum0 += p0;
+          sum1 += p1;
           s[c] = ptx::pack_bf16(p0, p1);
         }
+        const float sum = sum0 + sum1;
         ptx::tmem_st_32x32b_x32(t_s[t] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         if (j > 0 && __any_sync(0xffffffff, need)) {
