@@ -1,0 +1,115 @@
+// Private to the runtime (runtime.cpp, runtime_multi.cpp): per-domain device
+// context and small CUDA helpers.
+//
+// A "domain" is a set of co-located instances that share one stream, one set
+// of activation buffers and direct access to each other's KV slabs: normally
+// all instances of one physical GPU. With ESP_DOMAIN_PER_INSTANCE=1 every
+// instance is its own domain even on a shared GPU, which routes ring
+// prefill and multi-master decode through the cross-device transport (peer
+// copies + events) so that path runs, and is tested, on a single B200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.h"
+#include "errors.hpp"
+#include "runtime.hpp"
+
+namespace esp {
+
+using k::bf16;
+
+constexpr int kDecodeChunk = 256;
+
+struct LayerW {
+  bf16 *wqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;
+  bf16 *norm1 = nullptr, *norm2 = nullptr;
+};
+
+struct DeviceCtx {
+  int device = -1;  // physical CUDA ordinal
+  int domain = -1;  // index in Runtime::devices_
+  cudaStream_t stream = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bf16* embed = nullptr;
+  bf16* lm_head = nullptr;
+  bf16* final_norm = nullptr;
+  std::vector<LayerW> layers;
+  bool owns_weights = true;
+  float2* rope = nullptr;
+  int rope_max = 0;
+  std::vector<InstanceId> slabs;  // slab index -> instance id
+  // activations / scratch
+  DevBuf x, xn, q, kb, vb, attn, h, logits, tok, pos, rinst, rslot, segs, work, last_rows,
+      out_tok, chunks, row_start, part_o, part_ml, counts, result, kvrow, ret_rows, ret_slab,
+      ret_slot, qin, chunk_ids, row_list;
+  std::vector<void*> weight_allocs;
+  std::vector<cudaEvent_t> sync_events;  // cross-domain event pool
+  size_t sync_used = 0;
+};
+
+inline void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    cuda_ok(cudaSetDevice(d), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// A fresh event on dc's device (pooled, reset by release_sync_events).
+inline cudaEvent_t sync_event(DeviceCtx& dc) {
+  if (dc.sync_used == dc.sync_events.size()) {
+    DeviceGuard g(dc.device);
+    cudaEvent_t e;
+    cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    dc.sync_events.push_back(e);
+  }
+  return dc.sync_events[dc.sync_used++];
+}
+
+template <typename T>
+T* Runtime::scratch(DevBuf& b, size_t n) {
+  const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
+  if (b.bytes < bytes) {
+    if (b.ptr) cuda_ok(cudaFree(b.ptr), "cudaFree");
+    b.ptr = nullptr;
+    size_t want = std::max(bytes, b.bytes * 3 / 2);
+    cuda_ok(cudaMalloc(&b.ptr, want), "cudaMalloc(scratch)");
+    b.bytes = want;
+  }
+  return static_cast<T*>(b.ptr);
+}
+
+template <typename F>
+void Runtime::timed(int phase, cudaStream_t s, F&& f) {
+  if (!profiling_) {
+    f();
+    return;
+  }
+  // Created on the current device (the caller's DeviceGuard), destroyed by
+  // collect_phase_events: events may not cross devices.
+  auto get = [&]() {
+    cudaEvent_t e;
+    cuda_ok(cudaEventCreate(&e), "event");
+    return e;
+  };
+  PhaseEvent pe{phase, get(), get()};
+  cuda_ok(cudaEventRecord(pe.a, s), "event");
+  f();
+  cuda_ok(cudaEventRecord(pe.b, s), "event");
+  pending_.push_back(pe);
+}
+
+}  // namespace esp

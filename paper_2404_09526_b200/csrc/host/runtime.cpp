@@ -24,93 +24,11 @@
 
 #include "../kernels/kernels.h"
 #include "../kernels/synthetic.h"
+#include "device_ctx.hpp"
 
 namespace esp {
 
-using k::bf16;
-
-struct LayerW {
-  bf16 *wqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;
-  bf16 *norm1 = nullptr, *norm2 = nullptr;
-};
-
-struct DeviceCtx {
-  int device = -1;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  bf16* embed = nullptr;
-  bf16* lm_head = nullptr;
-  bf16* final_norm = nullptr;
-  std::vector<LayerW> layers;
-  float2* rope = nullptr;
-  int rope_max = 0;
-  std::vector<InstanceId> slabs;  // slab index -> instance id
-  // activations / scratch
-  DevBuf x, xn, q, kb, vb, attn, h, logits, tok, pos, rinst, rslot, segs, work, last_rows,
-      out_tok, chunks, row_start, part_o, part_ml, counts, result;
-  std::vector<void*> weight_allocs;
-};
-
-namespace {
-
-constexpr int kDecodeChunk = 256;
-
-void cuda_ok(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-  }
-}
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int d) {
-    cudaGetDevice(&prev);
-    cuda_ok(cudaSetDevice(d), "cudaSetDevice");
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-}  // namespace
-
 void Runtime::check_cuda(const char* what) { cuda_ok(cudaGetLastError(), what); }
-
-template <typename T>
-T* Runtime::scratch(DevBuf& b, size_t n) {
-  const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
-  if (b.bytes < bytes) {
-    if (b.ptr) cuda_ok(cudaFree(b.ptr), "cudaFree");
-    b.ptr = nullptr;
-    size_t want = std::max(bytes, b.bytes * 3 / 2);
-    cuda_ok(cudaMalloc(&b.ptr, want), "cudaMalloc(scratch)");
-    b.bytes = want;
-  }
-  return static_cast<T*>(b.ptr);
-}
-
-template <typename F>
-void Runtime::timed(int phase, cudaStream_t s, F&& f) {
-  if (!profiling_) {
-    f();
-    return;
-  }
-  auto get = [&]() {
-    if (event_pool_.empty()) {
-      cudaEvent_t e;
-      cuda_ok(cudaEventCreate(&e), "event");
-      return e;
-    }
-    cudaEvent_t e = event_pool_.back();
-    event_pool_.pop_back();
-    return e;
-  };
-  PhaseEvent pe{phase, get(), get()};
-  cuda_ok(cudaEventRecord(pe.a, s), "event");
-  f();
-  cuda_ok(cudaEventRecord(pe.b, s), "event");
-  pending_.push_back(pe);
-}
 
 // Call after the stream synchronized: folds recorded event pairs into totals.
 void Runtime::collect_phase_events() {
@@ -119,8 +37,8 @@ void Runtime::collect_phase_events() {
     cuda_ok(cudaEventElapsedTime(&ms, pe.a, pe.b), "elapsed");
     phase_ms_[pe.phase] += ms;
     phase_n_[pe.phase] += 1;
-    event_pool_.push_back(pe.a);
-    event_pool_.push_back(pe.b);
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
   }
   pending_.clear();
 }

@@ -158,9 +158,11 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 __global__ void decode_combine_kernel(const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml,
-                                      const int32_t* __restrict__ row_start, int heads, int hd,
+                                      const int32_t* __restrict__ row_start,
+                                      const int32_t* __restrict__ rows, int heads, int hd,
                                       bf16* __restrict__ out) {
-  const int row = blockIdx.x, head = blockIdx.y;
+  const int orow = blockIdx.x, head = blockIdx.y;
+  const int row = rows ? rows[orow] : orow;
   const int c0 = row_start[row], c1 = row_start[row + 1];
   float mm = -INFINITY;
   for (int c = c0; c < c1; ++c) mm = fmaxf(mm, part_ml[(static_cast<int64_t>(c) * heads + head) * 2]);
@@ -173,8 +175,24 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
       acc += w * part_o[p * hd + d];
       ll += w * part_ml[p * 2 + 1];
     }
-    out[static_cast<int64_t>(row) * heads * hd + head * hd + d] =
+    out[static_cast<int64_t>(orow) * heads * hd + head * hd + d] =
         __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
+  }
+}
+
+__global__ void retain_rows_kernel(const bf16* __restrict__ k, const bf16* __restrict__ v,
+                                   const int32_t* __restrict__ rows,
+                                   const int32_t* __restrict__ slab,
+                                   const int32_t* __restrict__ slot, const DecodeSlabs dst,
+                                   int hidden) {
+  const int i = blockIdx.x;
+  const int64_t so = static_cast<int64_t>(rows[i]) * hidden;
+  const int64_t d = static_cast<int64_t>(slot[i]) * hidden;
+  bf16* dk = const_cast<bf16*>(dst.k[slab[i]]) + d;
+  bf16* dv = const_cast<bf16*>(dst.v[slab[i]]) + d;
+  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
+    *reinterpret_cast<uint4*>(dk + c) = *reinterpret_cast<const uint4*>(k + so + c);
+    *reinterpret_cast<uint4*>(dv + c) = *reinterpret_cast<const uint4*>(v + so + c);
   }
 }
 
@@ -202,7 +220,23 @@ void decode_combine(const float* part_o, const float* part_ml, const int32_t* ro
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s) {
   if (rows <= 0) return;
   decode_combine_kernel<<<dim3(rows, heads), head_dim, 0, s>>>(part_o, part_ml, row_start,
-                                                               heads, head_dim, out);
+                                                               nullptr, heads, head_dim, out);
+  count_launch();
+}
+
+void decode_combine_rows(const float* part_o, const float* part_ml, const int32_t* row_start,
+                         const int32_t* rows, int n, int heads, int head_dim, bf16* out,
+                         cudaStream_t s) {
+  if (n <= 0) return;
+  decode_combine_kernel<<<dim3(n, heads), head_dim, 0, s>>>(part_o, part_ml, row_start, rows,
+                                                            heads, head_dim, out);
+  count_launch();
+}
+
+void retain_rows(const bf16* k, const bf16* v, const int32_t* rows, const int32_t* slab,
+                 const int32_t* slot, int n, const DecodeSlabs& dst, int hidden, cudaStream_t s) {
+  if (n <= 0) return;
+  retain_rows_kernel<<<n, 128, 0, s>>>(k, v, rows, slab, slot, dst, hidden);
   count_launch();
 }
 

@@ -154,7 +154,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t t
       dst_slab = (region == 1 ? ep.slab_k[inst] : ep.slab_v[inst]) +
                  static_cast<int64_t>(slot) * ep.hidden;
     }
-    const int64_t row_off = static_cast<int64_t>(m) * ep.hidden;
+    // q rows follow the GEMM rows; k/v rows may be remapped (ring gather
+    // buffers hold every ring position's rows in global order).
+    const int64_t row_off =
+        static_cast<int64_t>((region > 0 && ep.kv_rows && valid) ? ep.kv_rows[m] : m) * ep.hidden;
     if (region == 2) {
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {

@@ -32,6 +32,7 @@ struct GemmEpilogue {
   int hidden = 0, head_dim = 0;
   const int32_t* row_inst = nullptr;  // [M] slab index of the resting page, -1 none
   const int32_t* row_slot = nullptr;  // [M] slot within that slab
+  const int32_t* kv_rows = nullptr;   // [M] row of k_out/v_out for GEMM row m (null: m)
   bf16* slab_k[kMaxSlabs] = {};       // per co-located instance, this layer's base
   bf16* slab_v[kMaxSlabs] = {};
 };
@@ -93,6 +94,15 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);
+// Same, for a subset of rows: out row i combines global row rows[i].
+void decode_combine_rows(const float* part_o, const float* part_ml, const int32_t* row_start,
+                         const int32_t* rows, int n, int heads, int head_dim, bf16* out,
+                         cudaStream_t s);
+
+// Proactive retention on pass: copies K/V rows of a ring block that arrived
+// from another device into their resting page slots (one layer).
+void retain_rows(const bf16* k, const bf16* v, const int32_t* rows, const int32_t* slab,
+                 const int32_t* slot, int n, const DecodeSlabs& dst, int hidden, cudaStream_t s);
 
 // ---- small fused ops --------------------------------------------------------
 void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,

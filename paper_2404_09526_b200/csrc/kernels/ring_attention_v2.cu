@@ -43,20 +43,48 @@ struct Cfg2 {
   static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + 1024 + 512;
 };
 
-// 2^x on the FMA/ALU pipes (x <= 2^7): round-to-nearest split x = n + f via
-// the 1.5*2^23 trick, Taylor cubic for 2^f on [-1/2, 1/2] (rel. err < 7e-4,
-// below the bf16 rounding P gets anyway), exponent add for 2^n. Used for a
-// quarter of the softmax exponentials so the MUFU (ex2) pipe is not the
-// co-bottleneck with the tensor core.
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -126.0f);
-  const float t = x + 12582912.0f;
-  const float f = x - (t - 12582912.0f);
-  float p = fmaf(0.0555041087f, f, 0.240226507f);
-  p = fmaf(p, f, 0.693147181f);
-  p = fmaf(p, f, 1.0f);
-  const int n = __float_as_int(t) - 0x4B400000;
-  return __int_as_float(__float_as_int(p) + (n << 23));
+// Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): half the FMA-pipe
+// instructions of the softmax.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a pair on the FMA/ALU pipes (x <= 2^7): round-to-nearest split
+// x = n + f with the 1.5*2^23 trick, Taylor cubic for 2^f on [-1/2, 1/2]
+// (rel. err < 7e-4, under the bf16 rounding P gets anyway), 2^n by adding n
+// to the exponent field. Used for a quarter of the softmax exponentials so the
+// MUFU (ex2) pipe — shared by both softmax warpgroups of an SM sub-partition —
+// stops being the co-bottleneck with the tensor core.
+__device__ __forceinline__ void exp2_fma2(float x0, float x1, float& p0, float& p1) {
+  const uint64_t x = f2pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t t = fadd2(x, magic);
+  const uint64_t r = fadd2(t, f2pack(-12582912.0f, -12582912.0f));
+  const uint64_t f = ffma2(r, f2pack(-1.0f, -1.0f), x);
+  uint64_t p = ffma2(f2pack(0.0555041087f, 0.0555041087f), f, f2pack(0.240226507f, 0.240226507f));
+  p = ffma2(p, f, f2pack(0.693147181f, 0.693147181f));
+  p = ffma2(p, f, f2pack(1.0f, 1.0f));
+  float t0, t1, q0, q1;
+  f2unpack(t, t0, t1);
+  f2unpack(p, q0, q1);
+  // (n << 23) with n = bits(t) - 0x4B400000 equals bits(t) << 23 mod 2^32.
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
 }
 
 __device__ __forceinline__ int tiles_visible(const RingSegment& sg, int r, int q0) {
@@ -358,19 +386,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_sub = m_run == -INFINITY ? 0.f : m_run;
         // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
         // precede the write of s[c], c <= 2c), then P over S_t in TMEM.
-        float sum0 = 0.f, sum1 = 0.f;
+        const uint64_t scale2 = f2pack(scale_log2, scale_log2);
+        const uint64_t negm2 = f2pack(-m_sub, -m_sub);
+        uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
-          const float x0 = fmaf(__uint_as_float(s[2 * c]), scale_log2, -m_sub);
-          const float x1 = fmaf(__uint_as_float(s[2 * c + 1]), scale_log2, -m_sub);
-          const float p0 = ptx::ex2(x0);
-          // every 4th exponential on the FMA pipe (x1 of odd pairs)
-          const float p1 = (c & 1) ? exp2_fma(x1) : ptx::ex2(x1);
-          sum0 += p0;
-          sum1 += p1;
+          float x0, x1, p0, p1;
+          f2unpack(ffma2(f2pack(__uint_as_float(s[2 * c]), __uint_as_float(s[2 * c + 1])),
+                         scale2, negm2),
+                   x0, x1);
+          if ((c & 3) == 3) {
+            exp2_fma2(x0, x1, p0, p1);  // 1 pair in 4 on the FMA pipe
+          } else {
+            p0 = ptx::ex2(x0);
+            p1 = ptx::ex2(x1);
+          }
+          if (c & 1) {
+            sum2b = fadd2(sum2b, f2pack(p0, p1));
+          } else {
+            sum2a = fadd2(sum2a, f2pack(p0, p1));
+          }
           s[c] = ptx::pack_bf16(p0, p1);
         }
-        const float sum = sum0 + sum1;
+        float sa0, sa1, sb0, sb1;
+        f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
+        (void)sb0;
+        (void)sb1;
+        const float sum = sa0 + sa1;
         ptx::tmem_st_32x32b_x32(t_s[t] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         if (j > 0 && __any_sync(0xffffffff, need)) {
