@@ -393,11 +393,12 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
     cudaMemcpyAsync(dseg, &sg, sizeof(sg), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(dwork, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s);
     const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
+    const int nr = static_cast<int>(rows);
     if (pairs) {
-      esp::k::ring_attention_pairs(Q, K, V, O, static_cast<int>(rows), heads, head_dim, dseg,
-                                   dwork, static_cast<int>(work.size() / 2), scale, s);
+      esp::k::ring_attention_pairs(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork,
+                                   static_cast<int>(work.size() / 2), scale, s);
     } else {
-      esp::k::ring_attention(Q, K, V, O, static_cast<int>(rows), heads, head_dim, dseg, 1, dwork,
+      esp::k::ring_attention(Q, K, V, O, nr, nr, heads, head_dim, dseg, 1, dwork,
                              static_cast<int>(work.size() / 2), scale, s);
     }
     cudaMemcpyAsync(out, O, static_cast<size_t>(q_len) * hidden * 2, cudaMemcpyDeviceToDevice, s);
@@ -428,7 +429,7 @@ int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_sl
     for (const auto& [row, c] : by_row) {
       slabs.k[c] = static_cast<const esp::k::bf16*>(k_slab[c]);
       slabs.v[c] = static_cast<const esp::k::bf16*>(v_slab[c]);
-      ch.push_back({slot_idx[c], n_slots[c], row, c, 0});
+      ch.push_back({slot_idx[c], n_slots[c], row, c, static_cast<int32_t>(ch.size())});
       row_start[row + 1]++;
     }
     for (int r = 0; r < batch; ++r) row_start[r + 1] += row_start[r];

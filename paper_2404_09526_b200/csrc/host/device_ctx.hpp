@@ -51,6 +51,11 @@ struct DeviceCtx {
   size_t sync_used = 0;
 };
 
+// Work list of the ring-attention kernels (pairs: v2) for `segs`, in the
+// order persistent CTAs should take it (runtime_multi.cpp).
+void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bool pairs,
+                          int64_t kv_rows, int head_dim, std::vector<int32_t>& work_sorted);
+
 inline void cuda_ok(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));

@@ -76,27 +76,54 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
     }
     int ndev = 0;
     cuda_ok(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-    std::map<int, DeviceCtx*> by_dev;
+    // Co-location domains: one per physical GPU, or one per instance when
+    // ESP_DOMAIN_PER_INSTANCE is set (exercises the cross-device transport
+    // on a single GPU).
+    const bool per_instance = std::getenv("ESP_DOMAIN_PER_INSTANCE") != nullptr;
+    std::map<int, DeviceCtx*> by_key;
     for (int i = 0; i < n_instances; ++i) {
       const int d = devices[i];
       if (d < 0 || d >= ndev) throw ConfigError("instance device ordinal out of range");
-      if (!by_dev.count(d)) {
+      const int key = per_instance ? i : d;
+      if (!by_key.count(key)) {
         devices_.push_back(std::make_unique<DeviceCtx>());
         devices_.back()->device = d;
-        by_dev[d] = devices_.back().get();
+        devices_.back()->domain = static_cast<int>(devices_.size()) - 1;
+        by_key[key] = devices_.back().get();
       }
-      DeviceCtx* dc = by_dev[d];
+      DeviceCtx* dc = by_key[key];
       if (static_cast<int>(dc->slabs.size()) >= k::kMaxSlabs) {
         throw ConfigError("too many instances on one device");
       }
       instances_[i].device = d;
+      instances_[i].domain = dc->domain;
       instances_[i].slab = static_cast<int>(dc->slabs.size());
       dc->slabs.push_back(i);
     }
+    // Peer access between distinct GPUs (NVLink / NVSwitch): ring blocks,
+    // broadcast queries and partial outputs move by peer copies.
+    std::set<int> phys;
+    for (auto& dcp : devices_) phys.insert(dcp->device);
+    for (int a : phys) {
+      for (int b : phys) {
+        if (a == b) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, a, b);
+        if (can) {
+          DeviceGuard g(a);
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_ok(e, "peer access");
+          cudaGetLastError();
+        }
+      }
+    }
     const int64_t bpt = kv_bytes_per_token(cfg.layers, cfg.hidden, cfg.heads, 2);
+    std::map<int, const DeviceCtx*> weights_of;
     for (auto& dcp : devices_) {
       DeviceCtx& dc = *dcp;
-      init_device(dc);
+      auto wit = weights_of.find(dc.device);
+      init_device(dc, wit == weights_of.end() ? nullptr : wit->second);
+      if (wit == weights_of.end()) weights_of[dc.device] = &dc;
       DeviceGuard g(dc.device);
       int64_t cap = kv_capacity;
       if (cap <= 0) {
@@ -104,7 +131,9 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
         cuda_ok(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
         const int64_t reserve = static_cast<int64_t>(12) << 30;  // prefill activations
         const int64_t avail = static_cast<int64_t>(free_b) - reserve;
-        cap = avail / (static_cast<int64_t>(dc.slabs.size()) * bpt);
+        int64_t on_device = 0;
+        for (const auto& in : instances_) on_device += in.device == dc.device ? 1 : 0;
+        cap = avail / (on_device * bpt);
         if (cap <= 0) throw ConfigError("no HBM left for KV slabs");
       }
       // Slabs reserve the full logical capacity as virtual address space and
@@ -154,22 +183,46 @@ Runtime::~Runtime() {
     DevBuf* bufs[] = {&dc.x, &dc.xn, &dc.q, &dc.kb, &dc.vb, &dc.attn, &dc.h, &dc.logits,
                       &dc.tok, &dc.pos, &dc.rinst, &dc.rslot, &dc.segs, &dc.work,
                       &dc.last_rows, &dc.out_tok, &dc.chunks, &dc.row_start, &dc.part_o,
-                      &dc.part_ml, &dc.counts, &dc.result};
+                      &dc.part_ml, &dc.counts, &dc.result, &dc.kvrow, &dc.ret_rows,
+                      &dc.ret_slab, &dc.ret_slot, &dc.qin, &dc.chunk_ids, &dc.row_list};
     for (DevBuf* b : bufs) {
       if (b->ptr) cudaFree(b->ptr);
     }
     if (dc.rope) cudaFree(dc.rope);
+    for (cudaEvent_t e : dc.sync_events) cudaEventDestroy(e);
     if (dc.e0) cudaEventDestroy(dc.e0);
     if (dc.e1) cudaEventDestroy(dc.e1);
     if (dc.stream) cudaStreamDestroy(dc.stream);
   }
 }
 
-void Runtime::init_device(DeviceCtx& dc) {
+void Runtime::ensure_rope(DeviceCtx& dc, int64_t max_pos) {
+  if (dc.rope_max >= max_pos) return;
+  int want = 4096;
+  while (want < max_pos) want *= 2;
+  if (dc.rope) {
+    cuda_ok(cudaStreamSynchronize(dc.stream), "sync");
+    cudaFree(dc.rope);
+  }
+  cuda_ok(cudaMalloc(&dc.rope, static_cast<size_t>(want) * cfg_.head_dim / 2 * sizeof(float2)),
+          "cudaMalloc(rope)");
+  k::rope_table(dc.rope, want, cfg_.head_dim, cfg_.rope_theta, dc.stream);
+  dc.rope_max = want;
+}
+
+void Runtime::init_device(DeviceCtx& dc, const DeviceCtx* share) {
   DeviceGuard g(dc.device);
   cuda_ok(cudaStreamCreateWithFlags(&dc.stream, cudaStreamNonBlocking), "stream");
   cuda_ok(cudaEventCreate(&dc.e0), "event");
   cuda_ok(cudaEventCreate(&dc.e1), "event");
+  if (share != nullptr) {  // another domain on the same GPU owns the weights
+    dc.embed = share->embed;
+    dc.lm_head = share->lm_head;
+    dc.final_norm = share->final_norm;
+    dc.layers = share->layers;
+    dc.owns_weights = false;
+    return;
+  }
   const int64_t H = cfg_.hidden, F = cfg_.ffn, V = cfg_.vocab;
   auto alloc = [&](int64_t n) {
     void* p = nullptr;
@@ -274,23 +327,26 @@ void Runtime::sync_pages(PageList& pl, cudaStream_t s) {
   pl.dev_n = n;
 }
 
+DeviceCtx* Runtime::single_domain(const std::vector<InstanceId>& ids) {
+  if (devices_.empty()) return nullptr;
+  int dom = -1;
+  for (InstanceId i : ids) {
+    const int d = inst(i).domain;
+    if (dom >= 0 && d != dom) return nullptr;
+    dom = d;
+  }
+  return dom < 0 ? nullptr : devices_[static_cast<size_t>(dom)].get();
+}
+
 DeviceCtx& Runtime::device_of(const std::vector<InstanceId>& ids, const char* what) {
   if (devices_.empty()) {
     throw NoDeviceError(std::string(what) + " needs a device runtime (placement-only)");
   }
-  int dev = -1;
-  for (InstanceId i : ids) {
-    const int d = inst(i).device;
-    if (dev >= 0 && d != dev) {
-      throw ConfigError(std::string(what) +
-                        ": instances on different devices are not supported in this build");
-    }
-    dev = d;
+  DeviceCtx* dc = single_domain(ids);
+  if (!dc) {
+    throw ConfigError(std::string(what) + ": instances span co-location domains");
   }
-  for (auto& dcp : devices_) {
-    if (dcp->device == dev) return *dcp;
-  }
-  throw InternalError("device context missing");
+  return *dc;
 }
 
 // ---- prefill -------------------------------------------------------------------
@@ -337,11 +393,21 @@ void Runtime::prefill(const esp_prefill_args& a) {
     }
   }
   if (!devices_.empty() && !a.tokens) throw ConfigError("prefill: tokens required on a device runtime");
-  DeviceCtx* dcp = devices_.empty() ? nullptr : &device_of(ring, "prefill");
-  if (dcp) {
+  // One co-location domain: the batched single-domain pass. Several: ring
+  // transport between domains (runtime_multi.cpp), where a token can only
+  // be retained by a domain the ring passes through (proactive_scale_down's
+  // targets-within-the-group rule, esp_mechanics.cpp:96-108).
+  std::vector<InstanceId> all_ids = ring;
+  for (const auto& kv : need) all_ids.push_back(kv.first);
+  DeviceCtx* dcp = devices_.empty() ? nullptr : single_domain(all_ids);
+  const bool multi = !devices_.empty() && dcp == nullptr;
+  if (multi) {
+    std::set<int> ring_domains;
+    for (InstanceId i : ring) ring_domains.insert(inst(i).domain);
     for (const auto& [i, t] : need) {
-      if (inst(i).device != dcp->device) {
-        throw ConfigError("prefill: resting instance on another device is not supported");
+      if (t > 0 && !ring_domains.count(inst(i).domain)) {
+        throw InfeasiblePlanError("resting instance " + std::to_string(i) +
+                                  " is outside the prefill ring's devices");
       }
     }
   }
@@ -373,13 +439,17 @@ void Runtime::prefill(const esp_prefill_args& a) {
       PageList& pl = rr.pages[i];
       pl.slots.insert(pl.slots.end(), slots.begin(), slots.end());
       for (int32_t s : slots) {
-        ts.push_back(in.slab);
+        ts.push_back(i);  // resting instance id of the token
         tl.push_back(s);
       }
     }
     off += a.retain_n[r];
   }
-  if (!dcp) return;  // placement-only: page tables are the whole effect
+  if (devices_.empty()) return;  // placement-only: page tables are the whole effect
+  if (multi) {
+    prefill_multi(a, ring, tok_slab, tok_slot, tok_base);
+    return;
+  }
 
   DeviceCtx& dc = *dcp;
   DeviceGuard g(dc.device);
@@ -398,7 +468,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
       for (int64_t t = i; t < len; t += d) {
         h_tok.push_back(a.tokens[tok_base[r] + t]);
         h_pos.push_back(static_cast<int32_t>(t));
-        h_inst.push_back(tok_slab[r][static_cast<size_t>(t)]);
+        h_inst.push_back(inst(tok_slab[r][static_cast<size_t>(t)]).slab);
         h_slot.push_back(tok_slot[r][static_cast<size_t>(t)]);
         ++rows;
       }
@@ -411,8 +481,6 @@ void Runtime::prefill(const esp_prefill_args& a) {
   // Ring segments: position i meets, in round rd, the block of origin
   // (i - rd) mod d (build_ring_schedule, esp_mechanics.cpp:59-68).
   std::vector<k::RingSegment> segs;
-  std::vector<int32_t> work;
-  std::vector<std::pair<int64_t, int>> order;  // (cost, work index) for LPT order
   for (int i = 0; i < d; ++i) {
     for (int r = 0; r < n; ++r) {
       const int32_t ql = stripe_len(i, r);
@@ -427,60 +495,16 @@ void Runtime::prefill(const esp_prefill_args& a) {
         sg.kv_len[rd] = stripe_len(o, r);
         sg.shift[rd] = o > i ? 1 : 0;
       }
-      const int seg_idx = static_cast<int>(segs.size());
       segs.push_back(sg);
-      // One work item per (query tile, head) for v1, per (query-tile pair,
-      // head) for v2; cost = visible KV tiles (LPT ordering below).
-      const int span = attn_pairs_ ? 2 : 1;
-      const int n_items = (k::q_tiles(ql) + span - 1) / span;
-      for (int qi = 0; qi < n_items; ++qi) {
-        int64_t cost = 0;
-        for (int qt = qi * span; qt < std::min(k::q_tiles(ql), (qi + 1) * span); ++qt) {
-          for (int rd = 0; rd < d; ++rd) {
-            const int64_t vis = std::min<int64_t>(
-                sg.kv_len[rd], std::min(qt * 128 + 127, ql - 1) - sg.shift[rd] + 1);
-            cost += vis > 0 ? (vis + 127) / 128 : 0;
-          }
-        }
-        for (int hd = 0; hd < cfg_.heads; ++hd) {
-          order.emplace_back(cost, static_cast<int>(work.size() / 2));
-          work.push_back(seg_idx);
-          work.push_back((qi << 8) | hd);
-        }
-      }
     }
   }
-  // Persistent CTAs take items round-robin. Heads are processed in groups
-  // whose K/V (rows x 512 B per head) fit comfortably in L2 (~64 MiB), so the
-  // concurrently running items share K/V tiles; within a group, longest work
-  // first (LPT) for balance.
-  const int64_t head_kv_bytes = static_cast<int64_t>(rows) * cfg_.head_dim * 2 * 2;
-  const int head_group =
-      static_cast<int>(std::max<int64_t>(1, (static_cast<int64_t>(64) << 20) / std::max<int64_t>(head_kv_bytes, 1)));
-  std::stable_sort(order.begin(), order.end(), [&](const auto& x, const auto& y) {
-    const int gx = (work[2 * x.second + 1] & 0xFF) / head_group;
-    const int gy = (work[2 * y.second + 1] & 0xFF) / head_group;
-    return gx != gy ? gx < gy : x.first > y.first;
-  });
   std::vector<int32_t> work_sorted;
-  work_sorted.reserve(work.size());
-  for (const auto& o : order) {
-    work_sorted.push_back(work[2 * o.second]);
-    work_sorted.push_back(work[2 * o.second + 1]);
-  }
+  build_attention_work(segs, cfg_.heads, attn_pairs_, rows, cfg_.head_dim, work_sorted);
 
   // RoPE table covering every position of the batch.
   int64_t max_len = 0;
   for (int r = 0; r < n; ++r) max_len = std::max(max_len, a.input_lens[r]);
-  if (dc.rope_max < max_len) {
-    int want = 4096;
-    while (want < max_len) want *= 2;
-    if (dc.rope) cudaFree(dc.rope);
-    cuda_ok(cudaMalloc(&dc.rope, static_cast<size_t>(want) * cfg_.head_dim / 2 * sizeof(float2)),
-            "cudaMalloc(rope)");
-    k::rope_table(dc.rope, want, cfg_.head_dim, cfg_.rope_theta, s);
-    dc.rope_max = want;
-  }
+  ensure_rope(dc, max_len);
 
   int32_t* d_tok = scratch<int32_t>(dc.tok, rows);
   int32_t* d_pos = scratch<int32_t>(dc.pos, rows);
@@ -584,11 +608,11 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
     // Striped ring attention over all d rounds.
     timed(kPhAttention, s, [&] {
       if (attn_pairs_) {
-        k::ring_attention_pairs(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
+        k::ring_attention_pairs(q, kb, vb, attn, rows, rows, cfg_.heads, cfg_.head_dim,
                                 static_cast<const k::RingSegment*>(dc.segs.ptr),
                                 static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
       } else {
-        k::ring_attention(q, kb, vb, attn, rows, cfg_.heads, cfg_.head_dim,
+        k::ring_attention(q, kb, vb, attn, rows, rows, cfg_.heads, cfg_.head_dim,
                           static_cast<const k::RingSegment*>(dc.segs.ptr),
                           static_cast<int>(segs.size()),
                           static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
@@ -646,11 +670,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
     }
   }
   // Rows ordered by master, then request id (the assignment order).
-  struct Row {
-    RequestId r;
-    InstanceId master;
-    int32_t token, pos, slot;
-  };
+  using Row = DecodeRow;
   std::vector<Row> rows_v;
   std::vector<InstanceId> involved = members;
   for (const auto& [m, reqs] : assign) {
@@ -667,6 +687,10 @@ void Runtime::decode_step(const esp_decode_args& a) {
     for (const Row& rw : rows_v) {
       if (a.in_tokens) req(rw.r).tokens.push_back(rw.token);
     }
+    return;
+  }
+  if (single_domain(involved) == nullptr) {
+    decode_multi(a, rows_v, batch);
     return;
   }
   DeviceCtx& dc = device_of(involved, "decode_step");
@@ -696,6 +720,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
         ch.n = static_cast<int32_t>(std::min<int64_t>(kDecodeChunk, nsl - c0));
         ch.row = i;
         ch.slab = inst(iid).slab;
+        ch.out = static_cast<int32_t>(chunks.size());
         chunks.push_back(ch);
       }
     }
@@ -704,18 +729,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
   const int n_chunks = static_cast<int>(chunks.size());
   int64_t max_pos = 0;
   for (const Row& rw : rows_v) max_pos = std::max<int64_t>(max_pos, rw.pos + 1);
-  if (dc.rope_max < max_pos) {
-    int want = 4096;
-    while (want < max_pos) want *= 2;
-    if (dc.rope) {
-      cuda_ok(cudaStreamSynchronize(s), "sync");
-      cudaFree(dc.rope);
-    }
-    cuda_ok(cudaMalloc(&dc.rope, static_cast<size_t>(want) * cfg_.head_dim / 2 * sizeof(float2)),
-            "cudaMalloc(rope)");
-    k::rope_table(dc.rope, want, cfg_.head_dim, cfg_.rope_theta, s);
-    dc.rope_max = want;
-  }
+  ensure_rope(dc, max_pos);
   int32_t* d_tok = scratch<int32_t>(dc.tok, b);
   int32_t* d_pos = scratch<int32_t>(dc.pos, b);
   int32_t* d_inst = scratch<int32_t>(dc.rinst, b);

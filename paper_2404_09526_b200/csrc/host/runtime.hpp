@@ -51,7 +51,8 @@ struct RequestRec {
 struct InstanceRec {
   InstanceId id = -1;
   int device = -1;
-  int slab = -1;  // index among the instances co-located on the device
+  int domain = -1;  // index of the DeviceCtx (co-location domain) owning the slab
+  int slab = -1;    // index among the instances of that domain
   int64_t capacity = 0;
   int64_t used = 0;
   std::vector<int32_t> free_stack;  // back() is the next slot handed out
@@ -113,7 +114,23 @@ class Runtime {
   void release_slots(InstanceRec& in, const std::vector<int32_t>& s);
   void sync_pages(PageList& pl, cudaStream_t s);
   DeviceCtx& device_of(const std::vector<InstanceId>& ids, const char* what);
-  void init_device(DeviceCtx& dc);
+  // The single domain holding all `ids`, or nullptr when they span domains.
+  DeviceCtx* single_domain(const std::vector<InstanceId>& ids);
+  void init_device(DeviceCtx& dc, const DeviceCtx* share_weights);
+  void ensure_rope(DeviceCtx& dc, int64_t max_pos);
+  // Cross-domain executors (runtime_multi.cpp): ring transport by peer
+  // copies + events, retention on pass, query broadcast / partial gather.
+  void prefill_multi(const esp_prefill_args& a, const std::vector<InstanceId>& ring,
+                     const std::vector<std::vector<int32_t>>& tok_inst,
+                     const std::vector<std::vector<int32_t>>& tok_slot,
+                     const std::vector<int64_t>& tok_base);
+  struct DecodeRow {
+    RequestId r;
+    InstanceId master;
+    int32_t token, pos, slot;
+  };
+  void decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows,
+                    const std::vector<RequestId>& batch);
   void forward_layers_prefill(DeviceCtx& dc, int rows, const std::vector<k::RingSegment>& segs,
                               const std::vector<int32_t>& work);
   template <typename T>

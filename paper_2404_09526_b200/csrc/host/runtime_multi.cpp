@@ -1,0 +1,726 @@
+// Cross-domain ESP executors: a prefill ring or a decode group whose
+// instances live in different co-location domains (different GPUs, or —
+// with ESP_DOMAIN_PER_INSTANCE — different domains of one GPU).
+//
+// Prefill (build_ring_schedule esp_mechanics.cpp:45-70)
+//   Every domain computes embed / QKV / O / MLP for the stripe rows of its own
+//   ring positions. K/V blocks then travel the ring exactly as the reference
+//   schedules them: in round r position i forwards the block of origin
+//   (i - r) mod d to position i+1. A hop between domains is one peer copy per
+//   block into the receiver's gather buffer, ordered by CUDA events. A hop
+//   inside a domain is free, because co-located positions share the buffer.
+//   Proactive scale-down without extra traffic: a token whose resting
+//   instance lives in another domain is written into its page slot by THAT
+//   domain when the block passes through it (retain_rows), never migrated.
+//
+// Decode (multi-master)
+//   Masters run their requests' dense layers. Each layer:
+//   - every master domain's query rows are broadcast to the domains holding
+//     the requests' KV;
+//   - each of those domains computes split-KV partials over its own slots;
+//   - the partials are gathered back to the master domain and LSE-combined.
+//
+// Everything is stream-ordered with events. Write-after-read hazards on the
+// gather, query and partial buffers across layers are fenced with events
+// recorded after each peer copy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "device_ctx.hpp"
+#include "runtime.hpp"
+
+namespace esp {
+
+void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bool pairs,
+                          int64_t kv_rows, int head_dim, std::vector<int32_t>& work_sorted) {
+  std::vector<int32_t> work;
+  std::vector<std::pair<int64_t, int>> order;  // (cost, item)
+  const int span = pairs ? 2 : 1;
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const k::RingSegment& sg = segs[si];
+    const int n_items = (k::q_tiles(sg.q_len) + span - 1) / span;
+    for (int qi = 0; qi < n_items; ++qi) {
+      int64_t cost = 0;
+      for (int qt = qi * span; qt < std::min(k::q_tiles(sg.q_len), (qi + 1) * span); ++qt) {
+        for (int rd = 0; rd < sg.n_rounds; ++rd) {
+          const int64_t vis = std::min<int64_t>(
+              sg.kv_len[rd], std::min(qt * 128 + 127, sg.q_len - 1) - sg.shift[rd] + 1);
+          cost += vis > 0 ? (vis + 127) / 128 : 0;
+        }
+      }
+      for (int hd = 0; hd < heads; ++hd) {
+        order.emplace_back(cost, static_cast<int>(work.size() / 2));
+        work.push_back(static_cast<int32_t>(si));
+        work.push_back((qi << 8) | hd);
+      }
+    }
+  }
+  // Persistent CTAs take items round-robin: heads in groups whose K/V fit
+  // comfortably in L2 (~64 MiB) so concurrent items share K/V tiles, longest
+  // work first within a group.
+  const int64_t head_kv_bytes = kv_rows * head_dim * 2 * 2;
+  const int head_group = static_cast<int>(
+      std::max<int64_t>(1, (static_cast<int64_t>(64) << 20) / std::max<int64_t>(head_kv_bytes, 1)));
+  std::stable_sort(order.begin(), order.end(), [&](const auto& x, const auto& y) {
+    const int gx = (work[2 * x.second + 1] & 0xFF) / head_group;
+    const int gy = (work[2 * y.second + 1] & 0xFF) / head_group;
+    return gx != gy ? gx < gy : x.first > y.first;
+  });
+  work_sorted.clear();
+  work_sorted.reserve(work.size());
+  for (const auto& o : order) {
+    work_sorted.push_back(work[2 * o.second]);
+    work_sorted.push_back(work[2 * o.second + 1]);
+  }
+}
+
+namespace {
+
+template <typename T>
+void h2d(T* dst, const std::vector<T>& src, cudaStream_t s) {
+  if (src.empty()) return;
+  cuda_ok(cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s),
+          "h2d");
+}
+
+void peer_copy(void* dst, int dst_dev, const void* src, int src_dev, size_t bytes,
+               cudaStream_t s) {
+  if (bytes == 0) return;
+  cuda_ok(cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, bytes, s), "peer copy");
+}
+
+}  // namespace
+
+// ---- prefill -------------------------------------------------------------------
+void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<InstanceId>& ring,
+                            const std::vector<std::vector<int32_t>>& tok_inst,
+                            const std::vector<std::vector<int32_t>>& tok_slot,
+                            const std::vector<int64_t>& tok_base) {
+  const int n = a.n_requests, d = a.dop, H = cfg_.hidden, F = cfg_.ffn;
+  auto stripe_len = [&](int i, int r) -> int32_t {
+    const int64_t len = a.input_lens[r];
+    return len > i ? static_cast<int32_t>((len - i + d - 1) / d) : 0;
+  };
+  // Global rows in ring-position-major order, as the single-domain pass.
+  std::vector<std::vector<int32_t>> row0(static_cast<size_t>(d), std::vector<int32_t>(static_cast<size_t>(n)));
+  std::vector<int32_t> blk0(static_cast<size_t>(d) + 1);
+  int rows = 0;
+  for (int i = 0; i < d; ++i) {
+    blk0[i] = rows;
+    for (int r = 0; r < n; ++r) {
+      row0[i][r] = rows;
+      rows += stripe_len(i, r);
+    }
+  }
+  blk0[d] = rows;
+  std::vector<int> dom_of(static_cast<size_t>(d));
+  std::set<int> dom_set;
+  for (int i = 0; i < d; ++i) {
+    dom_of[i] = inst(ring[i]).domain;
+    dom_set.insert(dom_of[i]);
+  }
+  struct Part {
+    std::vector<int> positions;
+    std::map<int, int32_t> local_row0;  // ring position -> first local row
+    int rows = 0;
+    std::vector<int32_t> tok, pos, rinst, rslot, kvrow, ret_rows, ret_slab, ret_slot;
+    std::vector<k::RingSegment> segs;
+    std::vector<int32_t> work;
+    std::vector<std::pair<int, int32_t>> last;  // (request index, local row)
+  };
+  std::map<int, Part> parts;
+  for (int dom : dom_set) parts[dom];
+  for (int i = 0; i < d; ++i) {
+    Part& p = parts[dom_of[i]];
+    p.positions.push_back(i);
+    p.local_row0[i] = p.rows;
+    for (int r = 0; r < n; ++r) {
+      const int64_t len = a.input_lens[r];
+      for (int64_t t = i; t < len; t += d) {
+        const int32_t g = row0[i][r] + static_cast<int32_t>(t / d);
+        const InstanceRec& rest = inst(tok_inst[r][static_cast<size_t>(t)]);
+        const int32_t slot = tok_slot[r][static_cast<size_t>(t)];
+        p.tok.push_back(a.tokens[tok_base[r] + t]);
+        p.pos.push_back(static_cast<int32_t>(t));
+        p.kvrow.push_back(g);
+        if (rest.domain == dom_of[i]) {  // retained at the origin, in the QKV epilogue
+          p.rinst.push_back(rest.slab);
+          p.rslot.push_back(slot);
+        } else {  // retained on pass by the resting domain
+          p.rinst.push_back(-1);
+          p.rslot.push_back(0);
+          Part& q = parts[rest.domain];
+          q.ret_rows.push_back(g);
+          q.ret_slab.push_back(rest.slab);
+          q.ret_slot.push_back(slot);
+        }
+      }
+      const int64_t t_last = len - 1;
+      if (t_last % d == i) {
+        p.last.emplace_back(r, p.rows + (row0[i][r] - blk0[i]) + static_cast<int32_t>(t_last / d));
+      }
+    }
+    p.rows += blk0[i + 1] - blk0[i];
+  }
+  for (auto& [dom, p] : parts) {
+    for (int i : p.positions) {
+      for (int r = 0; r < n; ++r) {
+        const int32_t ql = stripe_len(i, r);
+        if (ql == 0) continue;
+        k::RingSegment sg{};
+        sg.q_row0 = p.local_row0[i] + (row0[i][r] - blk0[i]);
+        sg.q_len = ql;
+        sg.n_rounds = d;
+        for (int rd = 0; rd < d; ++rd) {
+          const int o = RingSchedule::origin(i, rd, d);
+          sg.kv_row0[rd] = row0[o][r];
+          sg.kv_len[rd] = stripe_len(o, r);
+          sg.shift[rd] = o > i ? 1 : 0;
+        }
+        p.segs.push_back(sg);
+      }
+    }
+    build_attention_work(p.segs, cfg_.heads, attn_pairs_, rows, cfg_.head_dim, p.work);
+  }
+
+  int64_t max_len = 0;
+  for (int r = 0; r < n; ++r) max_len = std::max(max_len, a.input_lens[r]);
+  // Per-domain setup: uploads, embedding.
+  for (auto& [dom, p] : parts) {
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    cudaStream_t s = dc.stream;
+    dc.sync_used = 0;
+    ensure_rope(dc, max_len);
+    const size_t lr = static_cast<size_t>(std::max(p.rows, 1));
+    h2d(scratch<int32_t>(dc.tok, lr), p.tok, s);
+    h2d(scratch<int32_t>(dc.pos, lr), p.pos, s);
+    h2d(scratch<int32_t>(dc.rinst, lr), p.rinst, s);
+    h2d(scratch<int32_t>(dc.rslot, lr), p.rslot, s);
+    h2d(scratch<int32_t>(dc.kvrow, lr), p.kvrow, s);
+    h2d(scratch<int32_t>(dc.ret_rows, p.ret_rows.size() + 1), p.ret_rows, s);
+    h2d(scratch<int32_t>(dc.ret_slab, p.ret_slab.size() + 1), p.ret_slab, s);
+    h2d(scratch<int32_t>(dc.ret_slot, p.ret_slot.size() + 1), p.ret_slot, s);
+    h2d(scratch<k::RingSegment>(dc.segs, p.segs.size() + 1), p.segs, s);
+    h2d(scratch<int32_t>(dc.work, p.work.size() + 1), p.work, s);
+    scratch<bf16>(dc.x, lr * H);
+    scratch<bf16>(dc.xn, lr * H);
+    scratch<bf16>(dc.q, lr * H);
+    scratch<bf16>(dc.attn, lr * H);
+    scratch<bf16>(dc.h, lr * F);
+    scratch<bf16>(dc.kb, static_cast<size_t>(rows) * H);  // gather buffers: every block
+    scratch<bf16>(dc.vb, static_cast<size_t>(rows) * H);
+    cuda_ok(cudaEventRecord(dc.e0, s), "event");
+    if (p.rows > 0) {
+      timed(kPhEmbed, s, [&] {
+        k::embed(static_cast<int32_t*>(dc.tok.ptr), dc.embed, static_cast<bf16*>(dc.x.ptr),
+                 p.rows, H, s);
+      });
+    }
+  }
+
+  const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
+  std::map<int, std::vector<cudaEvent_t>> readers;  // copies reading a domain's gather buffer
+  for (int l = 0; l < cfg_.layers; ++l) {
+    std::map<int, std::vector<cudaEvent_t>> ready;  // domain -> block -> event (nullptr: absent)
+    for (auto& [dom, p] : parts) ready[dom].assign(static_cast<size_t>(d), nullptr);
+    // 1. per-domain norm + QKV (+RoPE, + retention at the origin).
+    for (auto& [dom, p] : parts) {
+      DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+      DeviceGuard g(dc.device);
+      cudaStream_t s = dc.stream;
+      for (cudaEvent_t e : readers[dom]) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
+      readers[dom].clear();
+      if (p.rows == 0) {  // empty stripes (prompt shorter than the ring): nothing to send
+        cudaEvent_t e = sync_event(dc);
+        cuda_ok(cudaEventRecord(e, s), "event");
+        for (int i : p.positions) ready[dom][i] = e;
+        continue;
+      }
+      const LayerW& w = dc.layers[l];
+      bf16* x = static_cast<bf16*>(dc.x.ptr);
+      bf16* xn = static_cast<bf16*>(dc.xn.ptr);
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, p.rows, H, cfg_.rms_eps, s); });
+      k::GemmEpilogue ep;
+      ep.kind = k::kEpiQkvRope;
+      ep.q_out = static_cast<bf16*>(dc.q.ptr);
+      ep.k_out = static_cast<bf16*>(dc.kb.ptr);
+      ep.v_out = static_cast<bf16*>(dc.vb.ptr);
+      ep.kv_rows = static_cast<int32_t*>(dc.kvrow.ptr);
+      ep.pos = static_cast<int32_t*>(dc.pos.ptr);
+      ep.rope = dc.rope;
+      ep.hidden = H;
+      ep.head_dim = cfg_.head_dim;
+      ep.row_inst = static_cast<int32_t*>(dc.rinst.ptr);
+      ep.row_slot = static_cast<int32_t*>(dc.rslot.ptr);
+      for (size_t j = 0; j < dc.slabs.size(); ++j) {
+        ep.slab_k[j] = instances_[dc.slabs[j]].layer_k(l);
+        ep.slab_v[j] = instances_[dc.slabs[j]].layer_v(l);
+      }
+      timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, p.rows, 3 * H, H, ep, s); });
+      cudaEvent_t e = sync_event(dc);
+      cuda_ok(cudaEventRecord(e, s), "event");
+      for (int i : p.positions) ready[dom][i] = e;
+    }
+    // 2. ring transport in the reference's round order.
+    for (int r = 0; r + 1 < d; ++r) {
+      for (int i = 0; i < d; ++i) {
+        const int o = RingSchedule::origin(i, r, d);
+        const int src = dom_of[i], dst = dom_of[(i + 1) % d];
+        if (src == dst || ready[dst][o] != nullptr) continue;
+        if (ready[src][o] == nullptr) throw InternalError("ring block forwarded before it arrived");
+        DeviceCtx& sd = *devices_[static_cast<size_t>(src)];
+        DeviceCtx& dd = *devices_[static_cast<size_t>(dst)];
+        DeviceGuard g(dd.device);
+        cuda_ok(cudaStreamWaitEvent(dd.stream, ready[src][o], 0), "wait");
+        const size_t off = static_cast<size_t>(blk0[o]) * H;
+        const size_t bytes = static_cast<size_t>(blk0[o + 1] - blk0[o]) * H * sizeof(bf16);
+        peer_copy(static_cast<bf16*>(dd.kb.ptr) + off, dd.device,
+                  static_cast<bf16*>(sd.kb.ptr) + off, sd.device, bytes, dd.stream);
+        peer_copy(static_cast<bf16*>(dd.vb.ptr) + off, dd.device,
+                  static_cast<bf16*>(sd.vb.ptr) + off, sd.device, bytes, dd.stream);
+        cudaEvent_t e = sync_event(dd);
+        cuda_ok(cudaEventRecord(e, dd.stream), "event");
+        ready[dst][o] = e;
+        readers[src].push_back(e);
+      }
+    }
+    // 3. retention on pass, attention, O, MLP — all local to each domain.
+    for (auto& [dom, p] : parts) {
+      DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+      DeviceGuard g(dc.device);
+      cudaStream_t s = dc.stream;
+      k::DecodeSlabs slabs{};
+      for (size_t j = 0; j < dc.slabs.size(); ++j) {
+        slabs.k[j] = instances_[dc.slabs[j]].layer_k(l);
+        slabs.v[j] = instances_[dc.slabs[j]].layer_v(l);
+      }
+      k::retain_rows(static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr),
+                     static_cast<int32_t*>(dc.ret_rows.ptr), static_cast<int32_t*>(dc.ret_slab.ptr),
+                     static_cast<int32_t*>(dc.ret_slot.ptr), static_cast<int>(p.ret_rows.size()),
+                     slabs, H, s);
+      if (p.rows == 0) continue;
+      const LayerW& w = dc.layers[l];
+      bf16* x = static_cast<bf16*>(dc.x.ptr);
+      bf16* xn = static_cast<bf16*>(dc.xn.ptr);
+      bf16* attn = static_cast<bf16*>(dc.attn.ptr);
+      bf16* hbuf = static_cast<bf16*>(dc.h.ptr);
+      const int n_work = static_cast<int>(p.work.size() / 2);
+      timed(kPhAttention, s, [&] {
+        const bf16* qd = static_cast<bf16*>(dc.q.ptr);
+        // Q rows are this domain's local rows, K/V rows are global.
+        if (attn_pairs_) {
+          k::ring_attention_pairs(qd, static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr),
+                                  attn, p.rows, rows, cfg_.heads, cfg_.head_dim,
+                                  static_cast<k::RingSegment*>(dc.segs.ptr),
+                                  static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
+        } else {
+          k::ring_attention(qd, static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr),
+                            attn, p.rows, rows, cfg_.heads, cfg_.head_dim,
+                            static_cast<k::RingSegment*>(dc.segs.ptr),
+                            static_cast<int>(p.segs.size()), static_cast<int32_t*>(dc.work.ptr),
+                            n_work, scale, s);
+        }
+      });
+      k::GemmEpilogue eo;
+      eo.kind = k::kEpiResidual;
+      eo.out = x;
+      eo.ldo = H;
+      timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, p.rows, H, H, eo, s); });
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, p.rows, H, cfg_.rms_eps, s); });
+      k::GemmEpilogue eg;
+      eg.kind = k::kEpiSiluMul;
+      eg.out = hbuf;
+      eg.ldo = F;
+      timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, p.rows, 2 * F, H, eg, s); });
+      k::GemmEpilogue ed;
+      ed.kind = k::kEpiResidual;
+      ed.out = x;
+      ed.ldo = H;
+      timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, p.rows, H, F, ed, s); });
+    }
+  }
+
+  // 4. LM head + greedy token where each request's last prompt token lives.
+  std::vector<int32_t> first(static_cast<size_t>(n), -1);
+  std::map<int, std::vector<int32_t>> out_tok;
+  std::map<int, std::vector<float>> out_lg;
+  for (auto& [dom, p] : parts) {
+    if (p.last.empty()) continue;
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    cudaStream_t s = dc.stream;
+    const int nl = static_cast<int>(p.last.size());
+    std::vector<int32_t> lrows;
+    for (const auto& [r, row] : p.last) lrows.push_back(row);
+    int32_t* d_last = scratch<int32_t>(dc.last_rows, lrows.size());
+    h2d(d_last, lrows, s);
+    bf16* xn = static_cast<bf16*>(dc.xn.ptr);
+    timed(kPhNorm, s, [&] {
+      k::rmsnorm(static_cast<bf16*>(dc.x.ptr), d_last, dc.final_norm, xn, nl, H, cfg_.rms_eps, s);
+    });
+    float* logits = scratch<float>(dc.logits, static_cast<size_t>(nl) * cfg_.vocab);
+    k::GemmEpilogue ep;
+    ep.kind = k::kEpiStoreF32;
+    ep.out = logits;
+    ep.ldo = cfg_.vocab;
+    timed(kPhLmHead, s, [&] { k::gemm(xn, H, dc.lm_head, H, nl, cfg_.vocab, H, ep, s); });
+    int32_t* d_out = scratch<int32_t>(dc.out_tok, nl);
+    timed(kPhArgmax, s, [&] { k::argmax_rows(logits, nl, cfg_.vocab, d_out, s); });
+    out_tok[dom].resize(static_cast<size_t>(nl));
+    cuda_ok(cudaMemcpyAsync(out_tok[dom].data(), d_out, nl * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    if (a.logits_out) {
+      out_lg[dom].resize(static_cast<size_t>(nl) * cfg_.vocab);
+      cuda_ok(cudaMemcpyAsync(out_lg[dom].data(), logits, out_lg[dom].size() * 4,
+                              cudaMemcpyDeviceToHost, s),
+              "d2h");
+    }
+  }
+  double ms_max = 0;
+  for (auto& [dom, p] : parts) {
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    cuda_ok(cudaEventRecord(dc.e1, dc.stream), "event");
+    check_cuda("prefill (multi-domain) launch");
+  }
+  for (auto& [dom, p] : parts) {
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    cuda_ok(cudaStreamSynchronize(dc.stream), "prefill (multi-domain)");
+    float ms = 0;
+    cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
+    ms_max = std::max<double>(ms_max, ms);
+  }
+  collect_phase_events();
+  for (auto& [dom, p] : parts) {
+    for (size_t j = 0; j < p.last.size(); ++j) {
+      const int r = p.last[j].first;
+      first[r] = out_tok[dom][j];
+      if (a.logits_out) {
+        std::memcpy(a.logits_out + static_cast<size_t>(r) * cfg_.vocab,
+                    out_lg[dom].data() + j * cfg_.vocab, cfg_.vocab * sizeof(float));
+      }
+    }
+  }
+  if (a.device_ms_out) *a.device_ms_out = ms_max;
+  for (int r = 0; r < n; ++r) {
+    requests_[a.request_ids[r]].tokens.push_back(first[r]);
+    if (a.first_token_out) a.first_token_out[r] = first[r];
+  }
+  profiles_.push_back(ProfileRec{d, std::vector<int64_t>(a.input_lens, a.input_lens + n), ms_max});
+}
+
+// ---- decode ------------------------------------------------------------------------
+void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows_v,
+                           const std::vector<RequestId>& batch) {
+  const int b = static_cast<int>(rows_v.size());
+  const int H = cfg_.hidden, F = cfg_.ffn, heads = cfg_.heads, hd = cfg_.head_dim;
+  // Row g's master domain; per master domain its rows (ascending g).
+  std::vector<int> mdom(static_cast<size_t>(b));
+  std::map<int, std::vector<int32_t>> mrows;
+  for (int g = 0; g < b; ++g) {
+    mdom[g] = inst(rows_v[g].master).domain;
+    mrows[mdom[g]].push_back(g);
+  }
+  std::map<int, std::map<int32_t, int32_t>> local_of;  // domain -> global row -> local
+  for (auto& [dom, rs] : mrows) {
+    for (size_t j = 0; j < rs.size(); ++j) local_of[dom][rs[j]] = static_cast<int32_t>(j);
+  }
+  // Chunks ordered by (master domain, KV domain, row, instance): the partials
+  // one KV domain owes one master domain form one contiguous range.
+  struct Ch {
+    int md, xd;
+    int32_t row;
+    InstanceId inst;
+    const int32_t* slots;
+    int32_t n;
+  };
+  std::vector<Ch> all;
+  for (int g = 0; g < b; ++g) {
+    RequestRec& rr = req(rows_v[g].r);
+    for (auto& [iid, pl] : rr.pages) {
+      if (pl.slots.empty()) continue;
+      DeviceCtx& xc = *devices_[static_cast<size_t>(inst(iid).domain)];
+      DeviceGuard gd(xc.device);
+      sync_pages(pl, xc.stream);
+      const int64_t nsl = static_cast<int64_t>(pl.slots.size());
+      for (int64_t c0 = 0; c0 < nsl; c0 += kDecodeChunk) {
+        all.push_back({mdom[g], inst(iid).domain, g, iid, pl.dev + c0,
+                       static_cast<int32_t>(std::min<int64_t>(kDecodeChunk, nsl - c0))});
+      }
+    }
+  }
+  std::stable_sort(all.begin(), all.end(), [](const Ch& x, const Ch& y) {
+    return x.md != y.md ? x.md < y.md : (x.xd != y.xd ? x.xd < y.xd : x.row < y.row);
+  });
+  const int n_chunks = static_cast<int>(all.size());
+  std::map<int, std::vector<k::DecodeChunk>> xchunks;              // per KV domain
+  std::map<std::pair<int, int>, std::pair<int, int>> range_of;     // (md, xd) -> [c0, c1)
+  std::map<int, std::set<int32_t>> q_need;                          // xd -> rows it needs
+  std::vector<std::vector<int32_t>> chunks_of_row(static_cast<size_t>(b));
+  for (int c = 0; c < n_chunks; ++c) {
+    const Ch& ch = all[static_cast<size_t>(c)];
+    xchunks[ch.xd].push_back({ch.slots, ch.n, ch.row, inst(ch.inst).slab, c});
+    auto key = std::make_pair(ch.md, ch.xd);
+    auto it = range_of.find(key);
+    if (it == range_of.end()) range_of[key] = {c, c + 1};
+    else it->second.second = c + 1;
+    q_need[ch.xd].insert(ch.row);
+    chunks_of_row[ch.row].push_back(c);
+  }
+  std::vector<int32_t> row_start(static_cast<size_t>(b) + 1, 0), chunk_ids;
+  for (int g = 0; g < b; ++g) {
+    row_start[g] = static_cast<int32_t>(chunk_ids.size());
+    chunk_ids.insert(chunk_ids.end(), chunks_of_row[g].begin(), chunks_of_row[g].end());
+  }
+  row_start[b] = static_cast<int32_t>(chunk_ids.size());
+  std::set<int> doms;
+  for (auto& kv : mrows) doms.insert(kv.first);
+  for (auto& kv : xchunks) doms.insert(kv.first);
+
+  int64_t max_pos = 0;
+  for (const DecodeRow& rw : rows_v) max_pos = std::max<int64_t>(max_pos, rw.pos + 1);
+  for (int dom : doms) {
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    cudaStream_t s = dc.stream;
+    dc.sync_used = 0;
+    ensure_rope(dc, max_pos);
+    scratch<bf16>(dc.qin, static_cast<size_t>(b) * H);
+    scratch<float>(dc.part_o, static_cast<size_t>(std::max(n_chunks, 1)) * heads * hd);
+    scratch<float>(dc.part_ml, static_cast<size_t>(std::max(n_chunks, 1)) * heads * 2);
+    if (xchunks.count(dom)) {
+      h2d(scratch<k::DecodeChunk>(dc.chunks, xchunks[dom].size()), xchunks[dom], s);
+    }
+    cuda_ok(cudaEventRecord(dc.e0, s), "event");
+    if (!mrows.count(dom)) continue;
+    const std::vector<int32_t>& rs = mrows[dom];
+    std::vector<int32_t> tok, pos, rinst, rslot;
+    for (int32_t gr : rs) {
+      tok.push_back(rows_v[gr].token);
+      pos.push_back(rows_v[gr].pos);
+      rinst.push_back(inst(rows_v[gr].master).slab);
+      rslot.push_back(rows_v[gr].slot);
+    }
+    const size_t nl = rs.size();
+    h2d(scratch<int32_t>(dc.tok, nl), tok, s);
+    h2d(scratch<int32_t>(dc.pos, nl), pos, s);
+    h2d(scratch<int32_t>(dc.rinst, nl), rinst, s);
+    h2d(scratch<int32_t>(dc.rslot, nl), rslot, s);
+    h2d(scratch<int32_t>(dc.row_start, row_start.size()), row_start, s);
+    h2d(scratch<int32_t>(dc.chunk_ids, chunk_ids.size() + 1), chunk_ids, s);
+    h2d(scratch<int32_t>(dc.row_list, nl), rs, s);
+    scratch<bf16>(dc.x, nl * H);
+    scratch<bf16>(dc.xn, nl * H);
+    scratch<bf16>(dc.q, nl * H);
+    scratch<bf16>(dc.attn, nl * H);
+    scratch<bf16>(dc.h, nl * F);
+    timed(kPhEmbed, s, [&] {
+      k::embed(static_cast<int32_t*>(dc.tok.ptr), dc.embed, static_cast<bf16*>(dc.x.ptr),
+               static_cast<int>(nl), H, s);
+    });
+  }
+  const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
+  std::map<int, std::vector<cudaEvent_t>> q_readers, part_readers;
+  for (int l = 0; l < cfg_.layers; ++l) {
+    std::map<int, cudaEvent_t> q_ready, part_ready;
+    // 1. masters: norm + QKV (+RoPE, the new token's K/V appended at the master).
+    for (auto& [dom, rs] : mrows) {
+      DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+      DeviceGuard g(dc.device);
+      cudaStream_t s = dc.stream;
+      for (cudaEvent_t e : q_readers[dom]) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
+      q_readers[dom].clear();
+      const int nl = static_cast<int>(rs.size());
+      const LayerW& w = dc.layers[l];
+      bf16* x = static_cast<bf16*>(dc.x.ptr);
+      bf16* xn = static_cast<bf16*>(dc.xn.ptr);
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, nl, H, cfg_.rms_eps, s); });
+      k::GemmEpilogue ep;
+      ep.kind = k::kEpiQkvRope;
+      ep.q_out = static_cast<bf16*>(dc.q.ptr);
+      ep.pos = static_cast<int32_t*>(dc.pos.ptr);
+      ep.rope = dc.rope;
+      ep.hidden = H;
+      ep.head_dim = hd;
+      ep.row_inst = static_cast<int32_t*>(dc.rinst.ptr);
+      ep.row_slot = static_cast<int32_t*>(dc.rslot.ptr);
+      for (size_t j = 0; j < dc.slabs.size(); ++j) {
+        ep.slab_k[j] = instances_[dc.slabs[j]].layer_k(l);
+        ep.slab_v[j] = instances_[dc.slabs[j]].layer_v(l);
+      }
+      timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, nl, 3 * H, H, ep, s); });
+      cudaEvent_t e = sync_event(dc);
+      cuda_ok(cudaEventRecord(e, s), "event");
+      q_ready[dom] = e;
+    }
+    // 2. query broadcast to the KV domains, split-KV partials there.
+    for (auto& [xd, chs] : xchunks) {
+      DeviceCtx& xc = *devices_[static_cast<size_t>(xd)];
+      DeviceGuard g(xc.device);
+      cudaStream_t s = xc.stream;
+      for (cudaEvent_t e : part_readers[xd]) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
+      part_readers[xd].clear();
+      for (auto& [md, rs] : mrows) {
+        DeviceCtx& mc = *devices_[static_cast<size_t>(md)];
+        bool waited = false;
+        // maximal runs of this master domain's rows that xd needs
+        for (size_t j = 0; j < rs.size();) {
+          if (!q_need[xd].count(rs[j])) {
+            ++j;
+            continue;
+          }
+          size_t k2 = j + 1;
+          while (k2 < rs.size() && q_need[xd].count(rs[k2]) && rs[k2] == rs[k2 - 1] + 1) ++k2;
+          if (!waited) {
+            cuda_ok(cudaStreamWaitEvent(s, q_ready[md], 0), "wait");
+            waited = true;
+          }
+          peer_copy(static_cast<bf16*>(xc.qin.ptr) + static_cast<size_t>(rs[j]) * H, xc.device,
+                    static_cast<bf16*>(mc.q.ptr) + j * H, mc.device, (k2 - j) * H * sizeof(bf16), s);
+          j = k2;
+        }
+        if (waited) {
+          cudaEvent_t e = sync_event(xc);
+          cuda_ok(cudaEventRecord(e, s), "event");
+          q_readers[md].push_back(e);
+        }
+      }
+      k::DecodeSlabs slabs{};
+      for (size_t j = 0; j < xc.slabs.size(); ++j) {
+        slabs.k[j] = instances_[xc.slabs[j]].layer_k(l);
+        slabs.v[j] = instances_[xc.slabs[j]].layer_v(l);
+      }
+      timed(kPhDecodeAttn, s, [&] {
+        k::decode_attention(static_cast<bf16*>(xc.qin.ptr),
+                            static_cast<k::DecodeChunk*>(xc.chunks.ptr),
+                            static_cast<int>(chs.size()), slabs, heads, hd, scale,
+                            static_cast<float*>(xc.part_o.ptr), static_cast<float*>(xc.part_ml.ptr), s);
+      });
+      cudaEvent_t e = sync_event(xc);
+      cuda_ok(cudaEventRecord(e, s), "event");
+      part_ready[xd] = e;
+    }
+    // 3. partial gather + LSE combine at the masters, then the dense layers.
+    for (auto& [md, rs] : mrows) {
+      DeviceCtx& mc = *devices_[static_cast<size_t>(md)];
+      DeviceGuard g(mc.device);
+      cudaStream_t s = mc.stream;
+      for (auto& [key, rg] : range_of) {
+        if (key.first != md) continue;
+        const int xd = key.second;
+        cuda_ok(cudaStreamWaitEvent(s, part_ready[xd], 0), "wait");
+        if (xd == md) continue;
+        DeviceCtx& xc = *devices_[static_cast<size_t>(xd)];
+        const size_t c0 = static_cast<size_t>(rg.first), c1 = static_cast<size_t>(rg.second);
+        peer_copy(static_cast<float*>(mc.part_o.ptr) + c0 * heads * hd, mc.device,
+                  static_cast<float*>(xc.part_o.ptr) + c0 * heads * hd, xc.device,
+                  (c1 - c0) * heads * hd * sizeof(float), s);
+        peer_copy(static_cast<float*>(mc.part_ml.ptr) + c0 * heads * 2, mc.device,
+                  static_cast<float*>(xc.part_ml.ptr) + c0 * heads * 2, xc.device,
+                  (c1 - c0) * heads * 2 * sizeof(float), s);
+        cudaEvent_t e = sync_event(mc);
+        cuda_ok(cudaEventRecord(e, s), "event");
+        part_readers[xd].push_back(e);
+      }
+      const int nl = static_cast<int>(rs.size());
+      const LayerW& w = mc.layers[l];
+      bf16* x = static_cast<bf16*>(mc.x.ptr);
+      bf16* xn = static_cast<bf16*>(mc.xn.ptr);
+      bf16* attn = static_cast<bf16*>(mc.attn.ptr);
+      bf16* hbuf = static_cast<bf16*>(mc.h.ptr);
+      timed(kPhCombine, s, [&] {
+        k::decode_combine_rows(static_cast<float*>(mc.part_o.ptr), static_cast<float*>(mc.part_ml.ptr),
+                               static_cast<int32_t*>(mc.row_start.ptr),
+                               static_cast<int32_t*>(mc.chunk_ids.ptr),
+                               static_cast<int32_t*>(mc.row_list.ptr), nl, heads, hd, attn, s);
+      });
+      k::GemmEpilogue eo;
+      eo.kind = k::kEpiResidual;
+      eo.out = x;
+      eo.ldo = H;
+      timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, nl, H, H, eo, s); });
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, nl, H, cfg_.rms_eps, s); });
+      k::GemmEpilogue eg;
+      eg.kind = k::kEpiSiluMul;
+      eg.out = hbuf;
+      eg.ldo = F;
+      timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, nl, 2 * F, H, eg, s); });
+      k::GemmEpilogue ed;
+      ed.kind = k::kEpiResidual;
+      ed.out = x;
+      ed.ldo = H;
+      timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, nl, H, F, ed, s); });
+    }
+  }
+  // 4. LM head + greedy token at each master.
+  std::map<int, std::vector<int32_t>> out_tok;
+  std::map<int, std::vector<float>> out_lg;
+  for (auto& [md, rs] : mrows) {
+    DeviceCtx& mc = *devices_[static_cast<size_t>(md)];
+    DeviceGuard g(mc.device);
+    cudaStream_t s = mc.stream;
+    const int nl = static_cast<int>(rs.size());
+    bf16* xn = static_cast<bf16*>(mc.xn.ptr);
+    timed(kPhNorm, s, [&] {
+      k::rmsnorm(static_cast<bf16*>(mc.x.ptr), nullptr, mc.final_norm, xn, nl, H, cfg_.rms_eps, s);
+    });
+    float* logits = scratch<float>(mc.logits, static_cast<size_t>(nl) * cfg_.vocab);
+    k::GemmEpilogue ef;
+    ef.kind = k::kEpiStoreF32;
+    ef.out = logits;
+    ef.ldo = cfg_.vocab;
+    timed(kPhLmHead, s, [&] { k::gemm(xn, H, mc.lm_head, H, nl, cfg_.vocab, H, ef, s); });
+    int32_t* d_out = scratch<int32_t>(mc.out_tok, nl);
+    timed(kPhArgmax, s, [&] { k::argmax_rows(logits, nl, cfg_.vocab, d_out, s); });
+    out_tok[md].resize(static_cast<size_t>(nl));
+    cuda_ok(cudaMemcpyAsync(out_tok[md].data(), d_out, nl * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    if (a.logits_out) {
+      out_lg[md].resize(static_cast<size_t>(nl) * cfg_.vocab);
+      cuda_ok(cudaMemcpyAsync(out_lg[md].data(), logits, out_lg[md].size() * 4,
+                              cudaMemcpyDeviceToHost, s),
+              "d2h");
+    }
+  }
+  double ms_max = 0;
+  for (int dom : doms) {
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    cuda_ok(cudaEventRecord(dc.e1, dc.stream), "event");
+    check_cuda("decode (multi-domain) launch");
+  }
+  for (int dom : doms) {
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    cuda_ok(cudaStreamSynchronize(dc.stream), "decode (multi-domain)");
+    float ms = 0;
+    cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
+    ms_max = std::max<double>(ms_max, ms);
+  }
+  collect_phase_events();
+  if (a.device_ms_out) *a.device_ms_out = ms_max;
+  std::map<RequestId, std::pair<int, int>> where;  // request -> (domain, local row)
+  for (auto& [md, rs] : mrows) {
+    for (size_t j = 0; j < rs.size(); ++j) where[rows_v[rs[j]].r] = {md, static_cast<int>(j)};
+  }
+  for (int i = 0; i < b; ++i) {
+    const auto [md, j] = where.at(batch[i]);
+    RequestRec& rr = req(batch[i]);
+    const int32_t tok = out_tok[md][static_cast<size_t>(j)];
+    if (a.in_tokens) rr.tokens.push_back(a.in_tokens[i]);
+    rr.tokens.push_back(tok);
+    if (a.out_tokens) a.out_tokens[i] = tok;
+    if (a.logits_out) {
+      std::memcpy(a.logits_out + static_cast<size_t>(i) * cfg_.vocab,
+                  out_lg[md].data() + static_cast<size_t>(j) * cfg_.vocab,
+                  cfg_.vocab * sizeof(float));
+    }
+  }
+}
+
+}  // namespace esp

@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
   }
   __syncthreads();
-  const int64_t pidx = static_cast<int64_t>(ci) * heads + head;
+  (void)ci;
+  const int64_t pidx = static_cast<int64_t>(ch.out) * heads + head;
   for (int d = threadIdx.x; d < HD; d += blockDim.x) {
     float mm = -INFINITY;
 #pragma unroll
@@ -159,17 +160,21 @@ __global__ void __launch_bounds__(kWarps * 32)
 __global__ void decode_combine_kernel(const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml,
                                       const int32_t* __restrict__ row_start,
+                                      const int32_t* __restrict__ chunk_ids,
                                       const int32_t* __restrict__ rows, int heads, int hd,
                                       bf16* __restrict__ out) {
   const int orow = blockIdx.x, head = blockIdx.y;
   const int row = rows ? rows[orow] : orow;
   const int c0 = row_start[row], c1 = row_start[row + 1];
   float mm = -INFINITY;
-  for (int c = c0; c < c1; ++c) mm = fmaxf(mm, part_ml[(static_cast<int64_t>(c) * heads + head) * 2]);
+  for (int c = c0; c < c1; ++c) {
+    const int64_t ci = chunk_ids ? chunk_ids[c] : c;
+    mm = fmaxf(mm, part_ml[(ci * heads + head) * 2]);
+  }
   for (int d = threadIdx.x; d < hd; d += blockDim.x) {
     float acc = 0.f, ll = 0.f;
     for (int c = c0; c < c1; ++c) {
-      const int64_t p = static_cast<int64_t>(c) * heads + head;
+      const int64_t p = static_cast<int64_t>(chunk_ids ? chunk_ids[c] : c) * heads + head;
       const float mc = part_ml[p * 2];
       const float w = mc == -INFINITY ? 0.f : exp2f(mc - mm);
       acc += w * part_o[p * hd + d];
@@ -219,17 +224,17 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s) {
   if (rows <= 0) return;
-  decode_combine_kernel<<<dim3(rows, heads), head_dim, 0, s>>>(part_o, part_ml, row_start,
-                                                               nullptr, heads, head_dim, out);
+  decode_combine_kernel<<<dim3(rows, heads), head_dim, 0, s>>>(
+      part_o, part_ml, row_start, nullptr, nullptr, heads, head_dim, out);
   count_launch();
 }
 
 void decode_combine_rows(const float* part_o, const float* part_ml, const int32_t* row_start,
-                         const int32_t* rows, int n, int heads, int head_dim, bf16* out,
-                         cudaStream_t s) {
+                         const int32_t* chunk_ids, const int32_t* rows, int n, int heads,
+                         int head_dim, bf16* out, cudaStream_t s) {
   if (n <= 0) return;
-  decode_combine_kernel<<<dim3(n, heads), head_dim, 0, s>>>(part_o, part_ml, row_start, rows,
-                                                            heads, head_dim, out);
+  decode_combine_kernel<<<dim3(n, heads), head_dim, 0, s>>>(part_o, part_ml, row_start,
+                                                            chunk_ids, rows, heads, head_dim, out);
   count_launch();
 }
 

@@ -58,16 +58,17 @@ struct RingSegment {
   int32_t shift[kMaxRounds];
 };
 
-// Attention over segments; q/k/v/out are [rows x heads*head_dim] bf16.
+// Attention over segments; q/out are [q_rows x heads*head_dim] and k/v
+// [kv_rows x heads*head_dim] bf16 (segments index rows of each).
 // Persistent tcgen05 kernel; work = (segment, 128-row q tile, head).
-void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_rows,
-                    int heads, int head_dim, const RingSegment* d_segs, int n_segs,
+void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
+                    int kv_rows, int heads, int head_dim, const RingSegment* d_segs, int n_segs,
                     const int32_t* d_work, int n_work, float scale, cudaStream_t s);
 
 // v2: two 128-row query tiles per CTA (P kept in TMEM); work items are
 // (segment, query-tile PAIR, head). Same semantics as ring_attention.
-void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out,
-                          int total_rows, int heads, int head_dim, const RingSegment* d_segs,
+void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
+                          int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
                           const int32_t* d_work, int n_work, float scale, cudaStream_t s);
 
 // Work-list builder helper: number of 128-row q tiles of a segment.
@@ -78,9 +79,9 @@ inline int q_tiles(int q_len) { return (q_len + 127) / 128; }
 struct DecodeChunk {
   const int32_t* slots;
   int32_t n;
-  int32_t row;   // request row in the decode batch
+  int32_t row;   // request row in the decode batch (row of q)
   int32_t slab;  // index into the slab pointer arrays
-  int32_t pad;
+  int32_t out;   // index of this chunk's partial in part_o / part_ml
 };
 struct DecodeSlabs {
   const bf16* k[kMaxSlabs];
@@ -94,10 +95,11 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);
-// Same, for a subset of rows: out row i combines global row rows[i].
+// Same, for a subset of rows: out row i combines global row rows[i], whose
+// partials are chunk_ids[row_start[g] .. row_start[g+1]).
 void decode_combine_rows(const float* part_o, const float* part_ml, const int32_t* row_start,
-                         const int32_t* rows, int n, int heads, int head_dim, bf16* out,
-                         cudaStream_t s);
+                         const int32_t* chunk_ids, const int32_t* rows, int n, int heads,
+                         int head_dim, bf16* out, cudaStream_t s);
 
 // Proactive retention on pass: copies K/V rows of a ring block that arrived
 // from another device into their resting page slots (one layer).

@@ -382,8 +382,8 @@ int sm_count() {
 }
 
 template <int HD>
-void launch(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_rows, int heads,
-            const RingSegment* segs, const int32_t* work, int n_work, float scale,
+void launch(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
+            int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
             cudaStream_t s) {
   using C = ACfg<HD>;
   static std::once_flag once;
@@ -392,9 +392,9 @@ void launch(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_ro
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const int hidden = heads * HD;
-  const CUtensorMap tq = make_tmap_bf16(q, total_rows, hidden, hidden, BM);
-  const CUtensorMap tk = make_tmap_bf16(k, total_rows, hidden, hidden, BN);
-  const CUtensorMap tv = make_tmap_bf16(v, total_rows, hidden, hidden, BN);
+  const CUtensorMap tq = make_tmap_bf16(q, q_rows, hidden, hidden, BM);
+  const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
+  const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count() ? n_work : sm_count();
   ring_attention_tcgen05<HD><<<grid, kThreads, C::kSmem, s>>>(
       tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f);
@@ -403,16 +403,16 @@ void launch(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_ro
 
 }  // namespace
 
-void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_rows,
-                    int heads, int head_dim, const RingSegment* d_segs, int n_segs,
+void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
+                    int kv_rows, int heads, int head_dim, const RingSegment* d_segs, int n_segs,
                     const int32_t* d_work, int n_work, float scale, cudaStream_t s) {
   (void)n_segs;
   if (n_work <= 0) return;
   if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
   if (head_dim == 128) {
-    launch<128>(q, k, v, out, total_rows, heads, d_segs, d_work, n_work, scale, s);
+    launch<128>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s);
   } else if (head_dim == 64) {
-    launch<64>(q, k, v, out, total_rows, heads, d_segs, d_work, n_work, scale, s);
+    launch<64>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s);
   } else {
     throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
   }

@@ -486,8 +486,8 @@ int sm_count2() {
 }
 
 template <int HD>
-void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_rows, int heads,
-             const RingSegment* segs, const int32_t* work, int n_work, float scale,
+void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
+             int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s) {
   using C = Cfg2<HD>;
   static std::once_flag once;
@@ -496,9 +496,9 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_r
                          C::kSmem);
   });
   const int hidden = heads * HD;
-  const CUtensorMap tq = make_tmap_bf16(q, total_rows, hidden, hidden, BM);
-  const CUtensorMap tk = make_tmap_bf16(k, total_rows, hidden, hidden, BN);
-  const CUtensorMap tv = make_tmap_bf16(v, total_rows, hidden, hidden, BN);
+  const CUtensorMap tq = make_tmap_bf16(q, q_rows, hidden, hidden, BM);
+  const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
+  const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
   ring_attention_v2<HD><<<grid, kThreads, C::kSmem, s>>>(tq, tk, tv, out, hidden, segs, work,
                                                          n_work, scale * 1.4426950408889634f);
@@ -508,15 +508,15 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int total_r
 }  // namespace
 
 // Work items for v2 are (segment, 256-row query-tile PAIR, head).
-void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out,
-                          int total_rows, int heads, int head_dim, const RingSegment* d_segs,
+void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
+                          int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
                           const int32_t* d_work, int n_work, float scale, cudaStream_t s) {
   if (n_work <= 0) return;
   if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
   if (head_dim == 128) {
-    launch2<128>(q, k, v, out, total_rows, heads, d_segs, d_work, n_work, scale, s);
+    launch2<128>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s);
   } else if (head_dim == 64) {
-    launch2<64>(q, k, v, out, total_rows, heads, d_segs, d_work, n_work, scale, s);
+    launch2<64>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s);
   } else {
     throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
   }

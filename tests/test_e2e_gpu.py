@@ -26,6 +26,20 @@ LOGIT_TOL = 5e-2
 TIE_GAP = 2e-2
 
 
+@pytest.fixture(autouse=True, params=["colocated", "domain_per_instance"])
+def transport(request, monkeypatch):
+    """colocated: instances of one GPU share buffers (zero-copy ring).
+    domain_per_instance: every instance is its own co-location domain, so the
+    ring moves K/V blocks by peer copies in the reference's round order,
+    remote-origin tokens are retained on pass, and decode broadcasts queries /
+    gathers partials between domains — the cross-GPU data path, on one GPU."""
+    if request.param == "domain_per_instance":
+        monkeypatch.setenv("ESP_DOMAIN_PER_INSTANCE", "1")
+    else:
+        monkeypatch.delenv("ESP_DOMAIN_PER_INSTANCE", raising=False)
+    return request.param
+
+
 def check_against_oracle(shape, prompt, toks, logits):
     n_steps = len(toks) - 1
     ref_tok, ref_lg = llama_ref.generate(shape, prompt, n_steps, forced=toks[:n_steps],
@@ -113,9 +127,10 @@ def test_esp_degree_invariance(d):
     S = 1500 + d
     shape = abi.TINY
     prompt = np.random.default_rng(d).integers(0, shape.vocab, S).astype(np.int32)
-    rt = abi.Runtime(shape, d + 1, devices=[0] * (d + 1), kv_capacity=1000)
+    rt = abi.Runtime(shape, d, devices=[0] * d, kv_capacity=1000 if d > 1 else 2000)
     ring = list(range(d))
-    retain = [[(d, 1000), (0, S - 1000)]] if d > 1 else [[(0, 1000), (1, S - 1000)]]
+    # scale-down onto 2 survivors of the ring (the last position and the first)
+    retain = [[(d - 1, 1000), (0, S - 1000)]] if d > 1 else [[(0, S)]]
     first, lg, _ = rt.prefill([5], [S], ring, retain, tokens=prompt, want_logits=True)
     assert rt.placement(5) == {i: t for i, t in retain[0]}
     members = sorted({i for i, _ in retain[0]})
