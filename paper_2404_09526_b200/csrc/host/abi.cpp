@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -394,9 +395,38 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
     cudaMemcpyAsync(dwork, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s);
     const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
     const int nr = static_cast<int>(rows);
-    if (pairs) {
-      esp::k::ring_attention_pairs(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork,
-                                   static_cast<int>(work.size() / 2), scale, s);
+    const int n_work = static_cast<int>(work.size() / 2);
+    if (pairs && std::getenv("ESP_ATTN_PROF") != nullptr) {
+      // Cycle accounting of the v2 pipeline roles, printed to stderr.
+      const int grid = std::min(n_work, 148);
+      uint64_t* dprof = nullptr;
+      cudaMalloc(&dprof, static_cast<size_t>(grid) * 32 * 8);
+      cudaMemsetAsync(dprof, 0, static_cast<size_t>(grid) * 32 * 8, s);
+      esp::k::ring_attention_pairs_profiled(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork,
+                                            n_work, scale, s, dprof);
+      std::vector<uint64_t> h(static_cast<size_t>(grid) * 32);
+      cudaMemcpyAsync(h.data(), dprof, h.size() * 8, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      cudaFree(dprof);
+      const char* names[4][8] = {
+          {"q_empty", "k_empty", "v_empty", "-", "-", "-", "-", "total"},
+          {"q_full", "k_full", "v_full", "p_full0", "p_full1", "o_free", "-", "total"},
+          {"s_wait", "step", "s_readback", "rescale_wait", "rescales", "steps", "final_wait", "total"},
+          {"s_wait", "step", "s_readback", "rescale_wait", "rescales", "steps", "final_wait", "total"}};
+      const char* roles[4] = {"producer", "mma", "softmax0", "softmax1"};
+      for (int r = 0; r < 4; ++r) {
+        std::fprintf(stderr, "[attn-prof] %-9s", roles[r]);
+        for (int c = 0; c < 8; ++c) {
+          if (names[r][c][0] == '-') continue;
+          double sum = 0;
+          for (int b = 0; b < grid; ++b) sum += static_cast<double>(h[(b * 4 + r) * 8 + c]);
+          std::fprintf(stderr, " %s=%.0f", names[r][c], sum / grid);
+        }
+        std::fprintf(stderr, "\n");
+      }
+    } else if (pairs) {
+      esp::k::ring_attention_pairs(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork, n_work,
+                                   scale, s);
     } else {
       esp::k::ring_attention(Q, K, V, O, nr, nr, heads, head_dim, dseg, 1, dwork,
                              static_cast<int>(work.size() / 2), scale, s);

@@ -71,6 +71,15 @@ void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out
                           int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
                           const int32_t* d_work, int n_work, float scale, cudaStream_t s);
 
+// Instrumented v2 (clock64 accounting): prof holds grid x 4 roles x 8 u64
+// (producer: q_empty,k_empty,v_empty waits; MMA: q_full,k_full,v_full,
+// p_full[0],p_full[1],o_free waits; softmax t: s_full wait, step, S readback,
+// rescale o_done wait, rescales, steps, final wait; slot 7 = role total).
+void ring_attention_pairs_profiled(const bf16* q, const bf16* k, const bf16* v, bf16* out,
+                                   int q_rows, int kv_rows, int heads, int head_dim,
+                                   const RingSegment* d_segs, const int32_t* d_work, int n_work,
+                                   float scale, cudaStream_t s, uint64_t* prof);
+
 // Work-list builder helper: number of 128-row q tiles of a segment.
 inline int q_tiles(int q_len) { return (q_len + 127) / 128; }
 

@@ -145,14 +145,36 @@ struct Steps {
   __device__ bool active0() const { return tt < n0_r; }
 };
 
-template <int HD>
+// Opt-in cycle accounting (kProf): per CTA, 4 roles x 8 counters of clock64
+// cycles spent waiting on each barrier / computing; see esp_k_ring_attention.
+#define ESP_PROF_WAIT(slot, expr)                  \
+  do {                                             \
+    if constexpr (kProf) {                         \
+      const uint64_t _t0 = clock64();              \
+      expr;                                        \
+      prof_acc[slot] += clock64() - _t0;           \
+    } else {                                       \
+      expr;                                        \
+    }                                              \
+  } while (0)
+
+template <int HD, bool kProf>
 __global__ void __launch_bounds__(kThreads, 1)
     ring_attention_v2(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ out,
                       int hidden, const RingSegment* __restrict__ segs,
-                      const int32_t* __restrict__ work, int n_work, float scale_log2) {
+                      const int32_t* __restrict__ work, int n_work, float scale_log2,
+                      uint64_t* __restrict__ prof) {
   using C = Cfg2<HD>;
+  uint64_t prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const uint64_t prof_t_begin = kProf ? clock64() : 0;
+  auto prof_store = [&](int role) {
+    if constexpr (kProf) {
+      prof_acc[7] = clock64() - prof_t_begin;
+      for (int i = 0; i < 8; ++i) prof[(blockIdx.x * 4 + role) * 8 + i] = prof_acc[i];
+    }
+  };
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -210,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++items) {
         const Item it = load_item(work, w, segs);
         const RingSegment* sg = &segs[it.seg];
-        ptx::mbar_wait(q_empty, (items & 1) ^ 1);
+        ESP_PROF_WAIT(0, ptx::mbar_wait(q_empty, (items & 1) ^ 1));
         ptx::mbar_expect_tx(q_full, C::kQBytes * (it.act1 ? 2 : 1));
         for (int t = 0; t < (it.act1 ? 2 : 1); ++t) {
           for (int b = 0; b < C::kBoxes; ++b) {
@@ -221,14 +243,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         Steps st;
         for (st.begin(sg, it); st.valid(); st.next()) {
           const int row = st.kv_row();
-          ptx::mbar_wait(&k_empty[ks], kph ^ 1);
+          ESP_PROF_WAIT(1, ptx::mbar_wait(&k_empty[ks], kph ^ 1));
           ptx::mbar_expect_tx(&k_full[ks], C::kKvBytes);
           for (int b = 0; b < C::kBoxes; ++b) {
             ptx::tma_load_2d(sK + ks * C::kKvBytes + b * (BN * 128), &tmK, &k_full[ks],
                              it.head * HD + b * 64, row);
           }
           if (++ks == kStages) { ks = 0; kph ^= 1; }
-          ptx::mbar_wait(&v_empty[vs], vph ^ 1);
+          ESP_PROF_WAIT(2, ptx::mbar_wait(&v_empty[vs], vph ^ 1));
           ptx::mbar_expect_tx(&v_full[vs], C::kKvBytes);
           for (int b = 0; b < C::kBoxes; ++b) {
             ptx::tma_load_2d(sV + vs * C::kKvBytes + b * (BN * 128), &tmV, &v_full[vs],
@@ -237,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++vs == kStages) { vs = 0; vph ^= 1; }
         }
       }
+      prof_store(0);
     } else if (warp == 1 && lane == 0) {
       // ---------------------------------------------------------- MMA issuer
       constexpr uint32_t idesc_s = ptx::make_idesc_bf16(BM, BN, false, false);
@@ -259,13 +282,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Item it = load_item(work, w, segs);
         const RingSegment* sg = &segs[it.seg];
         const bool act[2] = {true, it.act1};
-        ptx::mbar_wait(q_full, items & 1);
+        ESP_PROF_WAIT(0, ptx::mbar_wait(q_full, items & 1));
         ptx::tc_fence_after();
         Steps st;
         st.begin(sg, it);
         // Prologue: S_t,0 for every tile that sees the first KV tile.
         {
-          ptx::mbar_wait(&k_full[ks], kph);
+          ESP_PROF_WAIT(1, ptx::mbar_wait(&k_full[ks], kph));
           ptx::tc_fence_after();
           const uint32_t k_addr = ptx::smem_u32(sK + ks * C::kKvBytes);
           if (st.active0()) issue_s(0, k_addr);
@@ -280,18 +303,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           nx.next();
           const bool has_next = nx.valid();
           const bool a_next[2] = {has_next && nx.active0(), has_next && act[1]};
-          ptx::mbar_wait(&v_full[vs], vph);
+          ESP_PROF_WAIT(2, ptx::mbar_wait(&v_full[vs], vph));
           uint32_t k_addr = 0;
           if (has_next) {
-            ptx::mbar_wait(&k_full[ks], kph);
+            ESP_PROF_WAIT(1, ptx::mbar_wait(&k_full[ks], kph));
             k_addr = ptx::smem_u32(sK + ks * C::kKvBytes);
           }
           const uint32_t v_addr = ptx::smem_u32(sV + vs * C::kKvBytes);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             if (a_now[t]) {
-              if (first_pv[t]) ptx::mbar_wait(&o_free[t], (titems[t] & 1) ^ 1);
-              ptx::mbar_wait(&p_full[t], cnt[t] & 1);
+              if (first_pv[t]) ESP_PROF_WAIT(5, ptx::mbar_wait(&o_free[t], (titems[t] & 1) ^ 1));
+              ESP_PROF_WAIT(3 + t, ptx::mbar_wait(&p_full[t], cnt[t] & 1));
               ptx::tc_fence_after();
 #pragma unroll
               for (int k = 0; k < BN / 16; ++k) {
@@ -323,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_commit(q_empty);
         for (int t = 0; t < 2; ++t) titems[t] += act[t] ? 1 : 0;
       }
+      prof_store(1);
     }
   } else {
     ptx::setmaxnreg_inc<192>();
@@ -346,7 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b0 = st.tt * BN;
         const int shift = sg->shift[st.r];
         const int kv_len = sg->kv_len[st.r];
-        ptx::mbar_wait(&s_full[t], cnt & 1);
+        ESP_PROF_WAIT(0, ptx::mbar_wait(&s_full[t], cnt & 1));
+        const uint64_t prof_t_step = kProf ? clock64() : 0;
         ptx::tc_fence_after();
         uint32_t s[128];
 #pragma unroll
@@ -355,6 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 32 * c, chunk);
         }
         ptx::tmem_wait_ld();
+        if constexpr (kProf) prof_acc[2] += clock64() - prof_t_step;  // S readback
         const bool full_tile = (b0 + BN - 1 <= q0 - shift) && (b0 + BN <= kv_len);
         if (!full_tile) {
           const int lim = min(a - shift - b0, kv_len - 1 - b0);
@@ -418,7 +444,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j > 0 && __any_sync(0xffffffff, need)) {
           // O holds PV_{j-1}: wait for it, then rescale in TMEM (rare: only
           // when a row max grew by more than 2^8).
-          ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
+          if constexpr (kProf) prof_acc[4] += 1;  // rescale count
+          ESP_PROF_WAIT(3, ptx::mbar_wait(&o_done[t], (cnt - 1) & 1));
           ptx::tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < HD; c += 32) {
@@ -434,11 +461,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run = l_run * alpha + sum;
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_full[t]);
+        if constexpr (kProf) {
+          prof_acc[1] += clock64() - prof_t_step;  // softmax step (S ready -> P ready)
+          prof_acc[5] += 1;
+        }
         ++cnt;
         ++j;
       }
       // Final O / l for this tile's rows.
-      ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
+      ESP_PROF_WAIT(6, ptx::mbar_wait(&o_done[t], (cnt - 1) & 1));
       ptx::tc_fence_after();
       const bool valid = a < sg->q_len;
       const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -466,6 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&o_free[t]);
     }
+    if (quad == 0 && lane == 0) prof_store(2 + t);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -485,24 +517,41 @@ int sm_count2() {
   return n;
 }
 
-template <int HD>
+template <int HD, bool kProf>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
-             cudaStream_t s) {
+             cudaStream_t s, uint64_t* prof) {
   using C = Cfg2<HD>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(ring_attention_v2<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::kSmem);
+    cudaFuncSetAttribute(ring_attention_v2<HD, kProf>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const int hidden = heads * HD;
   const CUtensorMap tq = make_tmap_bf16(q, q_rows, hidden, hidden, BM);
   const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
   const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
-  ring_attention_v2<HD><<<grid, kThreads, C::kSmem, s>>>(tq, tk, tv, out, hidden, segs, work,
-                                                         n_work, scale * 1.4426950408889634f);
+  ring_attention_v2<HD, kProf><<<grid, kThreads, C::kSmem, s>>>(
+      tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof);
   count_launch();
+}
+
+template <bool kProf>
+void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
+               int heads, int head_dim, const RingSegment* d_segs, const int32_t* d_work,
+               int n_work, float scale, cudaStream_t s, uint64_t* prof) {
+  if (n_work <= 0) return;
+  if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
+  if (head_dim == 128) {
+    launch2<128, kProf>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s,
+                        prof);
+  } else if (head_dim == 64) {
+    launch2<64, kProf>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s,
+                       prof);
+  } else {
+    throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
+  }
 }
 
 }  // namespace
@@ -511,15 +560,16 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
 void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
                           int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
                           const int32_t* d_work, int n_work, float scale, cudaStream_t s) {
-  if (n_work <= 0) return;
-  if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
-  if (head_dim == 128) {
-    launch2<128>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s);
-  } else if (head_dim == 64) {
-    launch2<64>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s);
-  } else {
-    throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
-  }
+  dispatch2<false>(q, k, v, out, q_rows, kv_rows, heads, head_dim, d_segs, d_work, n_work, scale,
+                   s, nullptr);
+}
+
+void ring_attention_pairs_profiled(const bf16* q, const bf16* k, const bf16* v, bf16* out,
+                                   int q_rows, int kv_rows, int heads, int head_dim,
+                                   const RingSegment* d_segs, const int32_t* d_work, int n_work,
+                                   float scale, cudaStream_t s, uint64_t* prof) {
+  dispatch2<true>(q, k, v, out, q_rows, kv_rows, heads, head_dim, d_segs, d_work, n_work, scale,
+                  s, prof);
 }
 
 }  // namespace esp::k
