@@ -30,14 +30,22 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 256;
 
-template <int BN>
+// kSkinny (M <= 32: decode, LM head of a few rows): only 32 A rows are loaded
+// per stage. The UMMA (M = 128) still reads a 128-row A tile; its rows 32..127
+// alias the following stages' A rows (garbage rows of D that are never
+// stored), so a stage costs 4 KB of A instead of 16 KB and the pipeline keeps
+// 9 weight tiles in flight per SM — these GEMMs are weight-streaming bound.
+template <int BN, bool kSkinny>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
-  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kARows = kSkinny ? 32 : BM;
+  static constexpr int kStages = kSkinny ? 9 : (BN == 256 ? 4 : 6);
+  static constexpr int kAStride = kARows * BK * 2;  // A bytes per stage
+  static constexpr int kAPad = kSkinny ? (BM - kARows) * BK * 2 : 0;
+  static constexpr int kARegion = kStages * kAStride + kAPad;
   static constexpr int kBBytes = BN * BK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTxBytes = kAStride + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kSmem = kARegion + kStages * kBBytes + 1024 + 256;
 };
 
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
@@ -78,14 +86,19 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t tacc, int m,
                                               bool valid, int nb, int N) {
   uint32_t r[32];
-  if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32) {
+  if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32 ||
+      ep.kind == kEpiAtomicF32) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       ptx::tmem_ld_32x32b_x32(tacc + c, r);
       ptx::tmem_wait_ld();
       if (!valid) continue;
       const int64_t off = static_cast<int64_t>(m) * ep.ldo + nb * BN + c;
-      if (ep.kind == kEpiStoreF32) {
+      if (ep.kind == kEpiAtomicF32) {
+        float* d = static_cast<float*>(ep.out) + off;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) atomicAdd(d + i, __uint_as_float(r[i]));
+      } else if (ep.kind == kEpiStoreF32) {
         float4* d = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + off);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -201,18 +214,21 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t t
   }
 }
 
-template <int BN>
+// Work unit u = (output tile u / k_splits, K slice u % k_splits). With
+// k_splits > 1 the epilogue must be kEpiAtomicF32 (fp32 reduction into a
+// workspace, finalized by residual_finalize).
+template <int BN, bool kSkinny>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-                      const __grid_constant__ GemmEpilogue ep) {
-  using C = Cfg<BN>;
+                      int k_splits, const __grid_constant__ GemmEpilogue ep) {
+  using C = Cfg<BN, kSkinny>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* sB = smem + C::kARegion;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -239,20 +255,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_m = (M + BM - 1) / BM, num_n = N / BN, num_k = K / BK;
-  const int tiles = num_m * num_n;
+  const int units = num_m * num_n * k_splits;
+  const int kb_per = (num_k + k_splits - 1) / k_splits;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       const uint64_t keep = ptx::policy_evict_last();
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
-        for (int kb = 0; kb < num_k; ++kb) {
+        tile_coords(u / k_splits, num_m, num_n, mb, nb);
+        const int kb0 = (u % k_splits) * kb_per, kb1 = min(num_k, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
-          ptx::tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, mb * BM);
+          ptx::mbar_expect_tx(&full[stage], C::kTxBytes);
+          ptx::tma_load_2d(sA + stage * C::kAStride, &tmA, &full[stage], kb * BK, mb * BM);
           ptx::tma_load_2d_hint(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, nb * BN,
                                 keep);
           if (++stage == C::kStages) {
@@ -268,22 +286,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++lt) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
         const int acc = lt & 1;
         const uint32_t use = static_cast<uint32_t>(lt >> 1);
+        const int kb0 = (u % k_splits) * kb_per, kb1 = min(num_k, kb0 + kb_per);
         ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a0 = ptx::smem_u32(sA + stage * C::kABytes);
+          const uint32_t a0 = ptx::smem_u32(sA + stage * C::kAStride);
           const uint32_t b0 = ptx::smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             ptx::umma_f16_ss(d_tmem, ptx::make_sdesc_sw128(a0 + k * 32, 16, 1024),
                              ptx::make_sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
-                             (kb | k) != 0);
+                             (kb != kb0 || k != 0) ? 1u : 0u);
           }
           ptx::tc_commit(&empty[stage]);
           if (++stage == C::kStages) {
@@ -298,9 +317,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t quad = warp & 3;
     const int row = static_cast<int>(quad * 32 + lane);
     int lt = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++lt) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
       int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords(u / k_splits, num_m, num_n, mb, nb);
       const int acc = lt & 1;
       const uint32_t use = static_cast<uint32_t>(lt >> 1);
       ptx::mbar_wait(&tfull[acc], use & 1);
@@ -371,35 +390,91 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
-template <int BN>
+template <int BN, bool kSkinny>
 static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
-                        const GemmEpilogue& ep, cudaStream_t s) {
-  using C = Cfg<BN>;
+                        int k_splits, const GemmEpilogue& ep, cudaStream_t s) {
+  using C = Cfg<BN, kSkinny>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_bf16_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::kSmem);
+    cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, kSkinny>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
-  const CUtensorMap ta = make_tmap_bf16(A, M, K, lda, BM);
+  const CUtensorMap ta = make_tmap_bf16(A, M, K, lda, C::kARows);
   const CUtensorMap tb = make_tmap_bf16(B, N, K, ldb, BN);
-  const int tiles = ((M + BM - 1) / BM) * (N / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_bf16_tcgen05<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, ep);
+  const int units = ((M + BM - 1) / BM) * (N / BN) * k_splits;
+  const int grid = units < num_sms() ? units : num_sms();
+  gemm_bf16_tcgen05<BN, kSkinny><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, k_splits, ep);
   count_launch();
+}
+
+__global__ void residual_finalize_kernel(bf16* __restrict__ x, int ldx, float* __restrict__ ws,
+                                         int M, int N) {
+  const int64_t n_elems = static_cast<int64_t>(M) * N;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_elems;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = i / N, n = i % N;
+    bf16* p = x + m * ldx + n;
+    *p = __float2bfloat16_rn(__bfloat162float(*p) + ws[i]);
+    ws[i] = 0.f;  // leave the workspace zeroed for the next split-K GEMM
+  }
+}
+
+// Zero-initialised fp32 split-K workspace of the current device (kept zeroed
+// by residual_finalize_kernel after each use).
+float* splitk_workspace(size_t elems, cudaStream_t s) {
+  static std::unordered_map<int, std::pair<float*, size_t>> ws;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto& w = ws[dev];
+  if (w.second < elems) {
+    if (w.first) {
+      cudaStreamSynchronize(s);
+      cudaFree(w.first);
+    }
+    w.second = std::max(elems, static_cast<size_t>(1) << 20);
+    if (cudaMalloc(&w.first, w.second * sizeof(float)) != cudaSuccess) {
+      throw std::runtime_error("split-K workspace allocation failed");
+    }
+    cudaMemsetAsync(w.first, 0, w.second * sizeof(float), s);
+  }
+  return w.first;
 }
 
 void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
           const GemmEpilogue& ep, cudaStream_t s) {
   if (M <= 0) return;
   if (N % 128 != 0 || K % 64 != 0) throw std::runtime_error("gemm: N%128 or K%64 != 0");
+  if (M <= 32) {
+    // Decode-shaped: weight-streaming bound. Skinny pipeline; when the N
+    // tiles alone cannot occupy the SMs (O / down projections), split K and
+    // reduce in fp32 before the residual add.
+    const int tiles = N / 128, num_k = K / BK;
+    if (ep.kind == kEpiResidual && tiles < num_sms()) {
+      int k_splits = std::min(num_k, (2 * num_sms() + tiles - 1) / tiles);
+      const int kb_per = (num_k + k_splits - 1) / k_splits;
+      k_splits = (num_k + kb_per - 1) / kb_per;  // no empty K slice
+      float* w = splitk_workspace(static_cast<size_t>(M) * N, s);
+      GemmEpilogue ea;
+      ea.kind = kEpiAtomicF32;
+      ea.out = w;
+      ea.ldo = N;
+      launch_gemm<128, true>(A, lda, B, ldb, M, N, K, k_splits, ea, s);
+      const int64_t n_elems = static_cast<int64_t>(M) * N;
+      residual_finalize_kernel<<<static_cast<unsigned>(std::min<int64_t>((n_elems + 255) / 256, 1024)),
+                                 256, 0, s>>>(static_cast<bf16*>(ep.out), ep.ldo, w, M, N);
+      count_launch();
+      return;
+    }
+    launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 1, ep, s);
+    return;
+  }
   const bool n256 = N % 256 == 0;
   const int tiles256 = ((M + BM - 1) / BM) * (N / 256);
-  // Small-M (decode, LM head) GEMMs are weight-bandwidth bound: prefer the
-  // narrower tile when the wide one would leave SMs idle.
+  // Prefer the wide tile unless it would leave SMs idle.
   if (n256 && tiles256 >= num_sms()) {
-    launch_gemm<256>(A, lda, B, ldb, M, N, K, ep, s);
+    launch_gemm<256, false>(A, lda, B, ldb, M, N, K, 1, ep, s);
   } else {
-    launch_gemm<128>(A, lda, B, ldb, M, N, K, ep, s);
+    launch_gemm<128, false>(A, lda, B, ldb, M, N, K, 1, ep, s);
   }
 }
 

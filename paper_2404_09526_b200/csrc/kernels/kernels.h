@@ -17,6 +17,7 @@ enum EpiKind : int {
   kEpiStoreF32 = 2,  // D = acc (fp32): LM-head logits
   kEpiSiluMul = 3,   // gate/up interleaved in 64-row blocks -> silu(g)*u (bf16)
   kEpiQkvRope = 4,   // q,k,v split + RoPE + ring stripe write + page retention
+  kEpiAtomicF32 = 5, // D += acc (fp32 atomics): split-K partial sums (internal)
 };
 
 struct GemmEpilogue {

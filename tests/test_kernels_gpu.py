@@ -45,6 +45,23 @@ def test_gemm_f32_and_residual():
     assert _rel(d2, r.float() + ref) < 1e-2
 
 
+@pytest.mark.parametrize("M,N,K", [(16, 4096, 4096), (16, 4096, 11008), (1, 512, 1536),
+                                   (32, 1024, 640)])
+def test_gemm_skinny_splitk_residual(M, N, K):
+    """Decode-shaped residual GEMMs take the skinny split-K path (fp32
+    reduction in a workspace, then residual add)."""
+    torch.manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", dtype=torch.bfloat16)
+    r = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+    d = r.clone()
+    for _ in range(2):  # second call checks the workspace was re-zeroed
+        d = r.clone()
+        abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, 1)
+    torch.cuda.synchronize()
+    assert _rel(d, r.float() + a.float() @ b.float().t()) < 1e-2
+
+
 def test_gemm_silu_mul():
     torch.manual_seed(2)
     M, F, K = 200, 384, 256
