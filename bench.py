@@ -258,6 +258,8 @@ def run_gpu(args):
         line["decode"] = bench_decode(rt, abi, args, np, hbm)
     if rank == 0 and not args.skip_esp_sweep:
         line["esp_degrees"] = bench_esp_sweep(abi, args, np, tf_sust)
+    if rank == 0 and not args.skip_config3:
+        line["config3_128k"] = bench_config3(abi, args, np, tf_sust)
     rt.close()
     if rank == 0 and not args.skip_cpu:
         try:
@@ -304,6 +306,33 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
             "phase_ms": {p: round(v[0] / max(len(ms), 1), 4) for p, v in ph.items() if v[1] > 0}}
 
 
+def bench_config3(abi, args, np, tf_sust):
+    """BASELINE config 3 with the reference's recorded PrefillPlan
+    (tests/golden/scenario_config3_128k.jsonl): 131072-token prompt, ESP ring
+    over 8 instances (kv_capacity 65600 each, co-located on this GPU, KV slabs
+    backed on demand), proactive scale-down 8->2 onto {0: 65600, 1: 65472}."""
+    S, cap = 131072, 65600
+    rt = abi.Runtime(abi.LWM_7B, 8, devices=[int(os.environ.get("LOCAL_RANK", "0"))] * 8,
+                     kv_capacity=cap)
+    prompt = np.random.default_rng(3).integers(0, V, S).astype(np.int32)
+    retain = [[(0, 65600), (1, 65472)]]
+    ms = []
+    for k in range(2):  # one warm-up, one timed
+        _, _, t = rt.prefill([k], [S], list(range(8)), retain, tokens=prompt)
+        placement = rt.placement(k)
+        rt.free_request(k)
+        if k > 0:
+            ms.append(t)
+    rt.close()
+    step = ms[0]
+    return {"tokens_per_s": S / (step / 1e3), "ms_per_step": step,
+            "tflops": prefill_flops(S) / (step / 1e3) / 1e12,
+            "frac": prefill_flops(S) / (step / 1e3) / 1e12 / tf_sust,
+            "placement_after_prefill": placement,
+            "config": "config3: LWM-7B 128K prefill, ESP d=8 (8 co-located instances), "
+                      "scale-down 8->2 by proactive retention (reference plan)"}
+
+
 def bench_esp_sweep(abi, args, np, tf_sust):
     """ESP degree d in {2,4,8} on ONE GPU: d co-located instances run the
     striped ring (d rounds per layer) with retention onto the reference's own
@@ -344,6 +373,7 @@ def main():
     ap.add_argument("--skip-decode", action="store_true")
     ap.add_argument("--skip-esp-sweep", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-config3", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -281,37 +281,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, false, false);
-      int stage = 0;
-      uint32_t phase = 0;
-      int lt = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
-        const int acc = lt & 1;
-        const uint32_t use = static_cast<uint32_t>(lt >> 1);
-        const int kb0 = (u % k_splits) * kb_per, kb1 = min(num_k, kb0 + kb_per);
-        ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+    // Whole warp runs the uniform loop (descriptors in uniform registers);
+    // one elected lane issues each tcgen05.mma / commit.
+    const bool leader = ptx::elect_one();
+    constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, false, false);
+    int stage = 0;
+    uint32_t phase = 0;
+    int lt = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      const uint32_t use = static_cast<uint32_t>(lt >> 1);
+      const int kb0 = (u % k_splits) * kb_per, kb1 = min(num_k, kb0 + kb_per);
+      ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t a0 = ptx::smem_u32(sA + stage * C::kAStride);
-          const uint32_t b0 = ptx::smem_u32(sB + stage * C::kBBytes);
+        const uint32_t a0 = ptx::smem_u32(sA + stage * C::kAStride);
+        const uint32_t b0 = ptx::smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            ptx::umma_f16_ss(d_tmem, ptx::make_sdesc_sw128(a0 + k * 32, 16, 1024),
-                             ptx::make_sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
-                             (kb != kb0 || k != 0) ? 1u : 0u);
-          }
-          ptx::tc_commit(&empty[stage]);
-          if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t da = ptx::make_sdesc_sw128(a0 + k * 32, 16, 1024);
+          const uint64_t db = ptx::make_sdesc_sw128(b0 + k * 32, 16, 1024);
+          if (leader) ptx::umma_f16_ss(d_tmem, da, db, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
         }
-        ptx::tc_commit(&tfull[acc]);
+        if (leader) ptx::tc_commit(&empty[stage]);
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (leader) ptx::tc_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     const uint32_t quad = warp & 3;

@@ -260,8 +260,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       prof_store(0);
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
+      // The whole warp runs the (warp-uniform) loop so descriptors live in
+      // uniform registers; one elected lane issues each tcgen05.mma/commit.
+      // (A single-lane loop costs an R2UR per operand per MMA, which made
+      // issue — not the tensor core — the bottleneck for 128x128x16 MMAs.)
+      const bool leader = ptx::elect_one();
       constexpr uint32_t idesc_s = ptx::make_idesc_bf16(BM, BN, false, false);
       constexpr uint32_t idesc_o = ptx::make_idesc_bf16(BM, HD, false, true);
       int ks = 0, vs = 0;
@@ -269,14 +274,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t cnt[2] = {0, 0};    // per-tile global step count (barrier phases)
       uint32_t titems[2] = {0, 0}; // per-tile item count (o_free phases)
       const uint32_t q_addr[2] = {ptx::smem_u32(sQ), ptx::smem_u32(sQ + C::kQBytes)};
+      auto commit = [&](uint64_t* bar) {
+        if (leader) ptx::tc_commit(bar);
+        __syncwarp();
+      };
       auto issue_s = [&](int t, uint32_t k_addr) {
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k >> 2) * (BM * 128) + (k & 3) * 32;
-          ptx::umma_f16_ss(t_s[t], ptx::make_sdesc_sw128(q_addr[t] + off, 16, 1024),
-                           ptx::make_sdesc_sw128(k_addr + off, 16, 1024), idesc_s, k != 0);
+          const uint64_t da = ptx::make_sdesc_sw128(q_addr[t] + off, 16, 1024);
+          const uint64_t db = ptx::make_sdesc_sw128(k_addr + off, 16, 1024);
+          if (leader) ptx::umma_f16_ss(t_s[t], da, db, idesc_s, k != 0);
         }
-        ptx::tc_commit(&s_full[t]);
+        commit(&s_full[t]);
       };
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++items) {
         const Item it = load_item(work, w, segs);
@@ -293,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t k_addr = ptx::smem_u32(sK + ks * C::kKvBytes);
           if (st.active0()) issue_s(0, k_addr);
           if (act[1]) issue_s(1, k_addr);
-          ptx::tc_commit(&k_empty[ks]);
+          commit(&k_empty[ks]);
           if (++ks == kStages) { ks = 0; kph ^= 1; }
         }
         bool first_pv[2] = {true, true};
@@ -318,11 +328,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::tc_fence_after();
 #pragma unroll
               for (int k = 0; k < BN / 16; ++k) {
-                ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8,
-                                 ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024),
-                                 idesc_o, (!first_pv[t] || k != 0) ? 1u : 0u);
+                const uint64_t dv = ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024);
+                if (leader) {
+                  ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8, dv, idesc_o,
+                                   (!first_pv[t] || k != 0) ? 1u : 0u);
+                }
               }
-              ptx::tc_commit(&o_done[t]);
+              commit(&o_done[t]);
               first_pv[t] = false;
               ++cnt[t];
             }
@@ -335,18 +347,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               issue_s(t, k_addr);
             }
           }
-          ptx::tc_commit(&v_empty[vs]);
+          commit(&v_empty[vs]);
           if (++vs == kStages) { vs = 0; vph ^= 1; }
           if (has_next) {
-            ptx::tc_commit(&k_empty[ks]);
+            commit(&k_empty[ks]);
             if (++ks == kStages) { ks = 0; kph ^= 1; }
           }
           st = nx;
         }
-        ptx::tc_commit(q_empty);
+        commit(q_empty);
         for (int t = 0; t < 2; ++t) titems[t] += act[t] ? 1 : 0;
       }
-      prof_store(1);
+      if (lane == 0) prof_store(1);
     }
   } else {
     ptx::setmaxnreg_inc<192>();
