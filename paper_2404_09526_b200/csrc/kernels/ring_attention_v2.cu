@@ -10,8 +10,13 @@
 //   * the MMA warp interleaves the tiles: PV_0,j  S_0,j+1  PV_1,j  S_1,j+1 —
 //     while softmax WG 0 works on S_0,j+1 the tensor core runs tile 1's PV and
 //     S, and vice versa;
-//   * warp-group register split with setmaxnreg (producer/MMA WG shrinks,
-//     the two softmax WGs grow).
+//   * each tile's softmax runs on TWO warpgroups (one per 64-column half of
+//     S): the row max is exchanged once per step through shared memory and a
+//     256-thread named barrier, the row-sum halves are merged only at the
+//     end; two warps per SM sub-partition per tile hide the max->exp->pack
+//     latency chain that a single warpgroup exposes;
+//   * warp-group register split with setmaxnreg (producer/MMA WG keeps its
+//     launch budget, the four softmax WGs grow).
 // The union of the two tiles' visible KV tiles is streamed once; tile 0
 // (earlier queries) skips the causal tail it cannot see.
 #include <cuda.h>
@@ -32,7 +37,8 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int kStages = 2;
-constexpr int kThreads = 384;
+constexpr int kThreads = 640;        // WG0 (TMA, MMA, TMEM alloc) + 4 softmax WGs
+constexpr int kSoftmaxThreads = 256;  // per query tile: 2 warpgroups
 constexpr float kRescaleThreshold = 8.0f;
 
 template <int HD>
@@ -40,7 +46,9 @@ struct Cfg2 {
   static constexpr int kBoxes = HD / 64;
   static constexpr int kQBytes = BM * HD * 2;
   static constexpr int kKvBytes = BN * HD * 2;
-  static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + 1024 + 512;
+  // row-max exchange [tile][parity][half][row] + row-sum exchange [tile][half][row]
+  static constexpr int kXchgBytes = (2 * 2 * 2 * BM + 2 * 2 * BM) * 4;
+  static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + kXchgBytes + 1024 + 512;
 };
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): half the FMA-pipe
@@ -181,7 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQ = smem;                                 // [2][kQBytes]
   uint8_t* sK = sQ + 2 * C::kQBytes;                  // [kStages][kKvBytes]
   uint8_t* sV = sK + kStages * C::kKvBytes;           // [kStages][kKvBytes]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * C::kKvBytes);
+  float* xchg_max = reinterpret_cast<float*>(sV + kStages * C::kKvBytes);  // [2][2][2][BM]
+  float* xchg_sum = xchg_max + 2 * 2 * 2 * BM;                              // [2][2][BM]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg_sum + 2 * 2 * BM);
   uint64_t* q_full = bars;
   uint64_t* q_empty = bars + 1;
   uint64_t* k_full = bars + 2;
@@ -209,9 +219,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&p_full[t], kSoftmaxThreads);
       ptx::mbar_init(&o_done[t], 1);
-      ptx::mbar_init(&o_free[t], 128);
+      ptx::mbar_init(&o_free[t], kSoftmaxThreads);
     }
     ptx::fence_barrier_init();
   }
@@ -224,7 +234,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_o[2] = {tmem + 2 * BN, tmem + 2 * BN + HD};
 
   if (warp < 4) {
-    ptx::setmaxnreg_dec<104>();
     if (warp == 0 && lane == 0) {
       // ---------------------------------------------------------- producer
       int ks = 0, vs = 0;
@@ -361,12 +370,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) prof_store(1);
     }
   } else {
-    ptx::setmaxnreg_inc<192>();
+    ptx::setmaxnreg_inc<104>();
     // ------------------------------------------------------------ softmax
-    const int t = (warp >= 8) ? 1 : 0;
+    // Warps 4..19: tile t = sw / 8, column half h = (sw / 4) % 2, TMEM lane
+    // quadrant = warp % 4. Thread = one query row x 64 score columns.
+    const int sw = static_cast<int>(warp) - 4;
+    const int t = sw >> 3;
+    const int h = (sw >> 2) & 1;
     const uint32_t quad = warp & 3;
     const int row = static_cast<int>(quad * 32 + lane);
     const uint32_t lane_off = (quad * 32) << 16;
+    constexpr int HO = HD / 2;  // O columns owned by this half
+    float* my_max = xchg_max + (t * 2 * 2) * BM;  // [parity][half][row]
+    float* my_sum = xchg_sum + (t * 2) * BM;      // [half][row]
+    const uint32_t bar_id = 1 + static_cast<uint32_t>(t);
     uint32_t cnt = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const Item it = load_item(work, w, segs);
@@ -374,44 +391,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       const RingSegment* sg = &segs[it.seg];
       const int q0 = it.q0[t];
       const int a = q0 + row;
-      float m_run = -INFINITY, l_run = 0.f;
+      float m_run = -INFINITY, l_half = 0.f;
       int j = 0;
       Steps st;
       for (st.begin(sg, it); st.valid(); st.next()) {
         if (t == 0 && !st.active0()) continue;
-        const int b0 = st.tt * BN;
+        const int b0 = st.tt * BN + 64 * h;  // first key of this half
         const int shift = sg->shift[st.r];
         const int kv_len = sg->kv_len[st.r];
         ESP_PROF_WAIT(0, ptx::mbar_wait(&s_full[t], cnt & 1));
         const uint64_t prof_t_step = kProf ? clock64() : 0;
         ptx::tc_fence_after();
-        uint32_t s[128];
+        uint32_t s[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
-          ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 32 * c, chunk);
+          ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 64 * h + 32 * c, chunk);
         }
         ptx::tmem_wait_ld();
         if constexpr (kProf) prof_acc[2] += clock64() - prof_t_step;  // S readback
-        const bool full_tile = (b0 + BN - 1 <= q0 - shift) && (b0 + BN <= kv_len);
-        if (!full_tile) {
-          const int lim = min(a - shift - b0, kv_len - 1 - b0);
+        const bool full_half = (b0 + 63 <= q0 - shift) && (b0 + 64 <= kv_len);
+        if (!full_half) {
+          const int lim = min(a - shift - b0, kv_len - 1 - b0);  // visible iff c <= lim
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
+          for (int c = 0; c < 64; ++c) {
             if (c > lim) s[c] = __float_as_uint(-INFINITY);
           }
         }
-        // Row max with 8 independent chains (ILP), then a tree.
         float mx8[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(s[k]);
 #pragma unroll
-        for (int c = 8; c < 128; c += 8) {
+        for (int c = 8; c < 64; c += 8) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(s[c + k]));
         }
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        // Row max across the two halves (double-buffered by step parity).
+        float* slot = my_max + (cnt & 1) * 2 * BM;
+        slot[h * BM + row] = mx;
+        ptx::named_bar_sync(bar_id, kSoftmaxThreads);
+        mx = fmaxf(mx, slot[(h ^ 1) * BM + row]);
         const float m_tile = mx * scale_log2;
         const float m_new = fmaxf(m_run, m_tile);
         const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY)
@@ -422,13 +443,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_run = m_new;
         }
         const float m_sub = m_run == -INFINITY ? 0.f : m_run;
-        // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
-        // precede the write of s[c], c <= 2c), then P over S_t in TMEM.
+        // P in place: s[c] <- bf16x2(p[2c], p[2c+1]), then into this half's
+        // 32 P columns of S_t in TMEM.
         const uint64_t scale2 = f2pack(scale_log2, scale_log2);
         const uint64_t negm2 = f2pack(-m_sub, -m_sub);
         uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int c = 0; c < 32; ++c) {
           float x0, x1, p0, p1;
           f2unpack(ffma2(f2pack(__uint_as_float(s[2 * c]), __uint_as_float(s[2 * c + 1])),
                          scale2, negm2),
@@ -446,31 +467,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           s[c] = ptx::pack_bf16(p0, p1);
         }
-        float sa0, sa1, sb0, sb1;
+        float sa0, sa1;
         f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
-        (void)sb0;
-        (void)sb1;
-        const float sum = sa0 + sa1;
-        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32 * h,
+                                *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         if (j > 0 && __any_sync(0xffffffff, need)) {
-          // O holds PV_{j-1}: wait for it, then rescale in TMEM (rare: only
-          // when a row max grew by more than 2^8).
-          if constexpr (kProf) prof_acc[4] += 1;  // rescale count
+          // O holds PV_{j-1}: wait for it, then rescale this half's columns
+          // in TMEM (rare: only when a row max grew by more than 2^8).
+          if constexpr (kProf) prof_acc[4] += 1;
           ESP_PROF_WAIT(3, ptx::mbar_wait(&o_done[t], (cnt - 1) & 1));
           ptx::tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < HD; c += 32) {
+          for (int c = 0; c < HO; c += 32) {
             uint32_t o[32];
-            ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
+            ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + HO * h + c, o);
             ptx::tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            ptx::tmem_st_32x32b_x32(t_o[t] + lane_off + c, o);
+            ptx::tmem_st_32x32b_x32(t_o[t] + lane_off + HO * h + c, o);
           }
         }
         ptx::tmem_wait_st();
-        l_run = l_run * alpha + sum;
+        l_half = l_half * alpha + (sa0 + sa1);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_full[t]);
         if constexpr (kProf) {
@@ -480,16 +498,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++cnt;
         ++j;
       }
-      // Final O / l for this tile's rows.
+      // Final O / l: merge the two halves' row sums, normalise own columns.
+      my_sum[h * BM + row] = l_half;
+      ptx::named_bar_sync(bar_id, kSoftmaxThreads);
+      const float l_run = l_half + my_sum[(h ^ 1) * BM + row];
       ESP_PROF_WAIT(6, ptx::mbar_wait(&o_done[t], (cnt - 1) & 1));
       ptx::tc_fence_after();
       const bool valid = a < sg->q_len;
       const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-      bf16* orow = out + static_cast<int64_t>(sg->q_row0 + a) * hidden + it.head * HD;
+      bf16* orow = out + static_cast<int64_t>(sg->q_row0 + a) * hidden + it.head * HD + HO * h;
 #pragma unroll 1
-      for (int c = 0; c < HD; c += 32) {
+      for (int c = 0; c < HO; c += 32) {
         uint32_t o[32];
-        ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
+        ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + HO * h + c, o);
         ptx::tmem_wait_ld();
         if (valid) {
           uint4* d = reinterpret_cast<uint4*>(orow + c);
@@ -506,10 +527,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      // The sum exchange slot is rewritten by the next item: no thread may run
+      // ahead before its partner has read it.
+      ptx::named_bar_sync(bar_id, kSoftmaxThreads);
       ptx::tc_fence_before();
       ptx::mbar_arrive(&o_free[t]);
     }
-    if (quad == 0 && lane == 0) prof_store(2 + t);
+    if (quad == 0 && lane == 0 && h == 0) prof_store(2 + t);
   }
   ptx::tc_fence_before();
   __syncthreads();
