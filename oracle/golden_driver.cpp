@@ -526,6 +526,54 @@ void mechanics(const std::string& ref, const std::string& outdir) {
 
 }  // namespace
 
+// Seeded small traces on a tight tiny cluster; the first one whose run
+// contains both a preemption drain (MigrationPlan, engine.cpp:260-309) and a
+// displaced-KV move (resolve_foreign_kv, engine.cpp:587-648) is recorded.
+struct PreemptCase {
+  int instances = 0;
+  TokenCount capacity = 0;
+  std::vector<TraceRecord> trace;
+};
+
+PreemptCase find_preempting_trace(const std::string& ref) {
+  ModelConfig tiny{2, 512, 8, 2, 524288};
+  for (uint64_t seed = 1; seed < 20000; ++seed) {
+    std::mt19937_64 rng(seed);
+    const int m = 4 + static_cast<int>(rng() % 5);
+    const TokenCount cap = 1000 + static_cast<TokenCount>(rng() % 4000);
+    std::vector<TraceRecord> tr;
+    const int n = 6 + static_cast<int>(rng() % 10);
+    double t = 0;
+    for (int i = 0; i < n; ++i) {
+      t += static_cast<double>(rng() % 300);
+      tr.push_back({t, 100 + static_cast<TokenCount>(rng() % (2 * cap)),
+                    1 + static_cast<TokenCount>(rng() % 120)});
+    }
+    EngineParams params;
+    params.exact_output_reservation = true;
+    Engine eng(KvPool(m, cap), tiny, load_default_sib(ref), make_policy(parse_policy("esp")),
+               params);
+    eng.submit(tr);
+    try {
+      eng.run();
+    } catch (const SimError&) {
+      continue;
+    }
+    int drains = 0, displaced = 0;
+    for (const Event& e : eng.log().events()) {
+      if (e.kind == EventKind::kMigration && e.detail == "displaced") ++displaced;
+      if (e.kind == EventKind::kMigration && e.detail.rfind("drop=", 0) == 0) ++drains;
+    }
+    if (drains > 0 || displaced > 0) {
+      std::cout << "preempting trace: seed " << seed << ", " << m << " x " << cap << ", "
+                << drains << " drains, " << displaced << " displaced moves\n";
+      return {m, cap, tr};
+    }
+  }
+  std::cout << "no preempting trace found\n";
+  return {};
+}
+
 int main(int argc, char** argv) {
   if (argc >= 4 && std::string(argv[1]) == "fit") {
     // The measured-SIB loop: B200 ProfileSample records
@@ -559,6 +607,13 @@ int main(int argc, char** argv) {
                  ref, outdir);
   }
   run_config4(ref, outdir);
+  {
+    PreemptCase pc = find_preempting_trace(ref);
+    if (!pc.trace.empty()) {
+      run_scenario({"tiny_preempt", pc.instances, pc.capacity, tiny, "esp", true, pc.trace}, ref,
+                   outdir);
+    }
+  }
   TraceSpec spec;
   spec.distribution = "mixed";
   spec.requests_per_s = 0.5;

@@ -855,10 +855,14 @@ void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t token
   std::vector<int32_t> moving(spl.slots.end() - tokens, spl.slots.end());
   std::vector<int32_t> dslots = take_slots(dst, tokens);
   if (!devices_.empty()) {
-    if (src.device != dst.device) {
-      throw ConfigError("move_kv across devices is not supported in this build");
+    // The copy runs on the destination domain's stream and reads the source
+    // slab directly (same GPU, or a peer over NVLink with peer access on).
+    DeviceCtx& sdc = *devices_[static_cast<size_t>(src.domain)];
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dst.domain)];
+    if (&sdc != &dc) {
+      DeviceGuard gs(sdc.device);
+      cuda_ok(cudaStreamSynchronize(sdc.stream), "move_kv source");
     }
-    DeviceCtx& dc = device_of({from, to}, "move_kv");
     DeviceGuard g(dc.device);
     int32_t* d_a = scratch<int32_t>(dc.tok, static_cast<size_t>(tokens));
     int32_t* d_b = scratch<int32_t>(dc.pos, static_cast<size_t>(tokens));

@@ -119,6 +119,45 @@ def test_tiny_multi_request_batches_and_masters():
         check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)
 
 
+def test_tiny_preempt_displaced_kv_moves():
+    """A seeded trace whose run makes the reference engine displace paused KV
+    onto group mates (resolve_foreign_kv, engine.cpp:587-648): the runtime
+    replays it with real KV moves (K8 copy_slots) and the decode outputs of
+    the moved request still match the oracle."""
+    path = os.path.join(GOLD, "scenario_tiny_preempt.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    rec = Recorder(rt)
+    replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
+    for r, lgs in rec.logits.items():
+        toks = [int(np.argmax(l)) for l in lgs]
+        check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)
+
+
+def test_kv_move_preserves_decode():
+    """KvMove (state.hpp:67-72) through esp_move_kv: moving part of a request's
+    KV to another instance (same or other transport domain) leaves the next
+    decode step's logits unchanged up to summation order."""
+    shape = abi.TINY
+    S = 900
+    prompt = np.random.default_rng(5).integers(0, shape.vocab, S).astype(np.int32)
+    outs = []
+    for move in (False, True):
+        rt = abi.Runtime(shape, 3, devices=[0, 0, 0], kv_capacity=1000)
+        rt.prefill([1], [S], [0, 1], [[(0, 600), (1, 300)]], tokens=prompt)
+        if move:
+            rt.move_kv(1, 0, 2, 250)
+            assert rt.placement(1) == {0: 350, 1: 300, 2: 250}
+        members = sorted(rt.placement(1))
+        _, lg, _ = rt.decode_step(members, [1], [1], want_logits=True)
+        rt.check_conservation()
+        outs.append(lg[0])
+        rt.close()
+    err = np.abs(outs[0] - outs[1]).max() / (np.abs(outs[0]).max() + 1e-6)
+    assert err < 1e-2, err
+
+
 def test_config3_128k_scale_down_lwm7b(transport):
     """BASELINE config 3 with the reference's own decision: LWM-7B shape,
     131072-token prompt, ESP ring over 8 instances (kv_capacity 65600), proactive
@@ -147,6 +186,29 @@ def test_config3_128k_scale_down_lwm7b(transport):
     assert err < LOGIT_TOL, err
     top8, top1 = int(np.argmax(lg8)), int(np.argmax(lg1[0]))
     assert top8 == top1 or lg1[0].max() - lg1[0][top8] < TIE_GAP
+
+
+def test_lwm7b_layer_shape_vs_oracle():
+    """LWM-7B layer geometry (H=4096, 32 heads x 128, FFN 11008, V=32000; 2 of
+    the 32 layers so the dense CPU oracle stays within seconds): ESP prefill
+    of 1200 tokens as a 3-instance striped ring with scale-down onto 2
+    survivors, then 3 multi-master decode steps; logits and greedy tokens vs
+    the oracle."""
+    shape = abi.ModelShape(layers=2, hidden=4096, heads=32, head_dim=128, ffn=11008,
+                           vocab=32000)
+    S = 1200
+    prompt = np.random.default_rng(11).integers(0, shape.vocab, S).astype(np.int32)
+    rt = abi.Runtime(shape, 3, devices=[0, 0, 0], kv_capacity=800)
+    first, lg0, _ = rt.prefill([9], [S], [0, 1, 2], [[(2, 800), (1, S - 800)]], tokens=prompt,
+                               want_logits=True)
+    assert rt.placement(9) == {2: 800, 1: S - 800}
+    toks, lgs = [int(first[0])], [lg0[0]]
+    for _ in range(3):
+        out, lg, _ = rt.decode_step([1, 2], [1], [9], want_logits=True)
+        toks.append(int(out[0]))
+        lgs.append(lg[0])
+    rt.check_conservation()
+    check_against_oracle(shape, prompt, toks, lgs)
 
 
 @pytest.mark.parametrize("d", [1, 2, 4, 8])
