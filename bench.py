@@ -46,6 +46,17 @@ def attn_flops_per_layer(S: int) -> float:
     return 2.0 * H * S * (S + 1)
 
 
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full capture (profiles/kernel_traffic.json,
+    written by tools/ncu_summary.py --traffic), or None."""
+    p = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f).get(kernel)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -241,7 +252,11 @@ def run_gpu(args):
                    "l2": "inputs larger than L2 (13.5 GB weights, 256 MB activations per pass)"},
         "roofline": {"bound": "tensor", "kernel": "ring_attention_tcgen05",
                      "achieved": att_achieved, "peak": tf_sust, "unit": "TFLOP/s",
-                     "frac": att_achieved / tf_sust, "traffic": None,
+                     "frac": att_achieved / tf_sust,
+                     "traffic": ncu_traffic("ring_attention_v2"),
+                     "traffic_note": "DRAM bytes per launch from profiles/kernel_traffic.json "
+                                     "(ncu --set full, 32K d=1); algorithmic Q+K+V+O = "
+                                     f"{4 * S * H * 2:.3e} B",
                      "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
                      "algorithmic": f"2*H*S*(S+1) = {attn_flops_per_layer(S):.4e} FLOP per launch "
                                     f"(one layer), avg launch {att_avg:.3f} ms"},
@@ -301,6 +316,7 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
             "config": f"config4 scaled to 1 GPU: batch {b} x {ctx}-token contexts, 1 instance, 1 master",
             "roofline": {"bound": "hbm", "kernel": "decode_attention (split-KV paged)",
                          "achieved": att_gbs, "peak": hbm, "unit": "GB/s", "frac": att_gbs / hbm,
+                         "traffic": ncu_traffic("decode_attention_kernel"),
                          "algorithmic": f"K+V bytes of one layer = 2*H*2*sum(ctx) = {kv_bytes / L:.4e} B per launch"},
             "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
             "phase_ms": {p: round(v[0] / max(len(ms), 1), 4) for p, v in ph.items() if v[1] > 0}}

@@ -15,7 +15,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__cycles_elapsed.avg.per_second", "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
 
 
-def rep(path):
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def rep(path, traffic=None):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -26,6 +29,13 @@ def rep(path):
         if k in hdr:
             i = hdr.index(k)
             print(f"  {k} = {vals[i]} {units[i]}")
+    if traffic is not None:
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(k)
+            tot += float(vals[i].replace(",", "")) * UNIT[units[i]]
+        short = name.split("(")[0].split("::")[-1].split("<")[0]
+        traffic[short] = tot
 
 
 def launches(path):
@@ -49,6 +59,20 @@ def launches(path):
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
+    # --traffic OUT.json: also write DRAM bytes per launch of each captured
+    # kernel (read by bench.py for roofline.traffic).
+    args = sys.argv[1:]
+    out_json = None
+    if args and args[0] == "--traffic":
+        out_json, args = args[1], args[2:]
+    traffic = {} if out_json else None
+    for p in args:
         print(f"== {p}")
-        (launches if p.endswith(".csv") else rep)(p)
+        if p.endswith(".csv"):
+            launches(p)
+        else:
+            rep(p, traffic)
+    if out_json:
+        import json
+        with open(out_json, "w") as f:
+            json.dump(traffic, f, indent=1)
