@@ -14,6 +14,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -342,6 +343,148 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// CTA-pair variant for the large prefill GEMMs: a cluster of two CTAs on one
+// TPC owns a 256 x 256 output tile. Each CTA TMA-loads its 128 A rows and its
+// 128 B rows (32 KB per K block instead of 48 KB for a 1-CTA 128 x 256 tile),
+// the leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256), and each CTA
+// drains its own 128 accumulator rows through the same fused epilogue.
+namespace pair {
+constexpr int kTileM = 256, kTileN = 256, kRows = 128;
+constexpr int kStageBytes = 2 * kRows * BK * 2;  // A half + B half
+constexpr int kStages = 6;
+constexpr int kTmemCols = 512;
+constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+}  // namespace pair
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                           const __grid_constant__ GemmEpilogue ep) {
+  using namespace pair;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;                        // [stage][128 x 64]
+  uint8_t* sB = smem + kStages * kRows * BK * 2;  // [stage][128 x 64]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 8);  // one arrival per epilogue warp of both CTAs
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + kTileM - 1) / kTileM, num_n = N / kTileN, num_k = K / BK;
+  const int units = num_m * num_n;
+  const int cid = static_cast<int>(ptx::cluster_id_x());
+  const int ncl = static_cast<int>(ptx::nclusters_x());
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_lead = ptx::mapa(ptx::smem_u32(full), 0);
+      const uint64_t keep = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        int mb, nb;
+        tile_coords(u, num_m, num_n, mb, nb);
+        const int a_row = mb * kTileM + static_cast<int>(rank) * kRows;
+        const int b_row = nb * kTileN + static_cast<int>(rank) * kRows;
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) ptx::mbar_expect_tx(&full[stage], 2 * kStageBytes);
+          const uint32_t bar = full_lead + stage * 8;
+          ptx::tma_load_2d_pair(sA + stage * kRows * BK * 2, &tmA, bar, kb * BK, a_row, keep);
+          ptx::tma_load_2d_pair(sB + stage * kRows * BK * 2, &tmB, bar, kb * BK, b_row, keep);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      const bool leader = ptx::elect_one();
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(kTileM, kTileN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      for (int u = cid; u < units; u += ncl, ++lt) {
+        const int acc = lt & 1;
+        const uint32_t use = static_cast<uint32_t>(lt >> 1);
+        ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kTileN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a0 = ptx::smem_u32(sA + stage * kRows * BK * 2);
+          const uint32_t b0 = ptx::smem_u32(sB + stage * kRows * BK * 2);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = ptx::make_sdesc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t db = ptx::make_sdesc_sw128(b0 + k * 32, 16, 1024);
+            if (leader) ptx::umma_f16_ss_pair(d_tmem, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          if (leader) ptx::tc_commit_pair(&empty[stage], 0x3);
+          __syncwarp();
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (leader) ptx::tc_commit_pair(&tfull[acc], 0x3);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t quad = warp & 3;
+    const int row = static_cast<int>(quad * 32 + lane);
+    const uint32_t tempty_lead = ptx::mapa(ptx::smem_u32(tempty), 0);
+    int lt = 0;
+    for (int u = cid; u < units; u += ncl, ++lt) {
+      int mb, nb;
+      tile_coords(u, num_m, num_n, mb, nb);
+      const int acc = lt & 1;
+      const uint32_t use = static_cast<uint32_t>(lt >> 1);
+      ptx::mbar_wait(&tfull[acc], use & 1);
+      ptx::tc_fence_after();
+      const uint32_t tacc = tmem_base + acc * kTileN + ((quad * 32) << 16);
+      const int m = mb * kTileM + static_cast<int>(rank) * kRows + row;
+      epilogue_tile<kTileN>(ep, tacc, m, m < M, nb, N);
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(tempty_lead + acc * 8);
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_pair<pair::kTmemCols>(tmem_base);
+  }
+}
+
 // ---- host: tensor maps -----------------------------------------------------
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -410,6 +553,51 @@ static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, i
   count_launch();
 }
 
+// Co-resident CTA pairs of the current device (normally num_sms / 2).
+static int pair_clusters() {
+  static std::unordered_map<int, int> cache;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  cudaFuncSetAttribute(gemm_bf16_tcgen05_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       pair::kSmem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * num_sms());
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pair::kSmem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tcgen05_pair, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[dev] = n;
+  return n;
+}
+
+static bool launch_gemm_pair(const bf16* A, int lda, const bf16* B, int ldb, int M, int N,
+                             int K, const GemmEpilogue& ep, cudaStream_t s) {
+  if (getenv("ESP_GEMM_NO_PAIR") != nullptr || M < pair::kTileM || N % pair::kTileN != 0) return false;
+  if (ep.kind == kEpiQkvRope && ep.hidden % pair::kTileN != 0) return false;
+  const int clusters = pair_clusters();
+  const int units = ((M + pair::kTileM - 1) / pair::kTileM) * (N / pair::kTileN);
+  if (clusters <= 0 || units < clusters) return false;
+  const CUtensorMap ta = make_tmap_bf16(A, M, K, lda, pair::kRows);
+  const CUtensorMap tb = make_tmap_bf16(B, N, K, ldb, pair::kRows);
+  gemm_bf16_tcgen05_pair<<<2 * clusters, kThreads, pair::kSmem, s>>>(ta, tb, M, N, K, ep);
+  count_launch();
+  return true;
+}
+
 __global__ void residual_finalize_kernel(bf16* __restrict__ x, int ldx, float* __restrict__ ws,
                                          int M, int N) {
   const int64_t n_elems = static_cast<int64_t>(M) * N;
@@ -471,6 +659,7 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 1, ep, s);
     return;
   }
+  if (launch_gemm_pair(A, lda, B, ldb, M, N, K, ep, s)) return;
   const bool n256 = N % 256 == 0;
   const int tiles256 = ((M + BM - 1) / BM) * (N / 256);
   // Prefer the wide tile unless it would leave SMs idle.

@@ -79,6 +79,37 @@ def test_gemm_silu_mul():
     assert _rel(d, ref) < 1e-2
 
 
+@pytest.mark.parametrize("M,N,K,epi", [(4096, 4096, 512, 0), (4000, 4096, 320, 1),
+                                       (9000, 2560, 256, 2), (4097, 4608, 192, 3)])
+def test_gemm_cta_pair_matches_single_cta(M, N, K, epi, monkeypatch):
+    """Large GEMMs run on CTA pairs (tcgen05.mma.cta_group::2, 256 x 256
+    tiles). Same K order as the 1-CTA kernel, so outputs are bit-identical;
+    both also match the fp32 reference."""
+    torch.manual_seed(M + N)
+    a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.1
+    odt = torch.float32 if epi == 2 else torch.bfloat16
+    ncols = N // 2 if epi == 3 else N
+    r = torch.randn(M, ncols, device="cuda", dtype=torch.bfloat16)
+    outs = []
+    for no_pair in (False, True):
+        if no_pair:
+            monkeypatch.setenv("ESP_GEMM_NO_PAIR", "1")
+        d = r.clone() if epi == 1 else torch.empty(M, ncols, device="cuda", dtype=odt)
+        abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi)
+        torch.cuda.synchronize()
+        outs.append(d)
+    monkeypatch.delenv("ESP_GEMM_NO_PAIR")
+    assert torch.equal(outs[0], outs[1])
+    ref = a.float() @ b.float().t()
+    if epi == 1:
+        ref = r.float() + ref
+    elif epi == 3:
+        g = ref.view(M, -1, 2, 64)
+        ref = (torch.nn.functional.silu(g[:, :, 0]) * g[:, :, 1]).reshape(M, ncols)
+    assert _rel(outs[0], ref) < (1e-5 if epi == 2 else 1e-2)
+
+
 def _ref_striped(q, ks, vs, pos_i, d, origins, heads, hd):
     """fp32 reference: query stripe a (position a*d+pos_i) vs key stripe b of
     origin o (position b*d+o): visible iff b*d+o <= a*d+pos_i."""
