@@ -15,6 +15,7 @@
 #include "../kernels/kernels.h"
 #include "esp_abi.h"
 #include "planner.hpp"
+#include "device_ctx.hpp"
 #include "runtime.hpp"
 
 struct esp_runtime {
@@ -380,13 +381,9 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
     // ESP_ATTN_V1 is set.
     const bool pairs = std::getenv("ESP_ATTN_V1") == nullptr;
     const int span = pairs ? 2 : 1;
-    std::vector<int32_t> work;
-    for (int qt = 0; qt < (esp::k::q_tiles(q_len) + span - 1) / span; ++qt) {
-      for (int h = 0; h < heads; ++h) {
-        work.push_back(0);
-        work.push_back((qt << 8) | h);
-      }
-    }
+    (void)span;
+    std::vector<int32_t> work;  // the runtime's work order (LPT, head groups)
+    esp::build_attention_work({sg}, heads, pairs, rows, head_dim, work);
     esp::k::RingSegment* dseg = nullptr;
     int32_t* dwork = nullptr;
     cudaMalloc(&dseg, sizeof(sg));
@@ -411,8 +408,8 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
       const char* names[4][8] = {
           {"q_empty", "k_empty", "v_empty", "-", "-", "-", "-", "total"},
           {"q_full", "k_full", "v_full", "p_full0", "p_full1", "o_free", "-", "total"},
-          {"s_wait", "step", "s_readback", "rescale_wait", "rescales", "steps", "final_wait", "total"},
-          {"s_wait", "step", "s_readback", "rescale_wait", "rescales", "steps", "final_wait", "total"}};
+          {"s_wait", "step", "to_ld", "to_max", "to_st_issue", "steps", "final_wait", "total"},
+          {"s_wait", "step", "to_ld", "to_max", "to_st_issue", "steps", "final_wait", "total"}};
       const char* roles[4] = {"producer", "mma", "softmax0", "softmax1"};
       for (int r = 0; r < 4; ++r) {
         std::fprintf(stderr, "[attn-prof] %-9s", roles[r]);
@@ -427,6 +424,25 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
     } else if (pairs) {
       esp::k::ring_attention_pairs(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork, n_work,
                                    scale, s);
+      if (const char* rep = std::getenv("ESP_ATTN_REPEAT")) {
+        // Kernel study: time n more launches on the staged buffers (stderr).
+        const int n = std::max(1, std::atoi(rep));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+        for (int i = 0; i < n; ++i) {
+          esp::k::ring_attention_pairs(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork, n_work,
+                                       scale, s);
+        }
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        std::fprintf(stderr, "[attn-time] %.4f ms/launch over %d launches\n", ms / n, n);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
     } else {
       esp::k::ring_attention(Q, K, V, O, nr, nr, heads, head_dim, dseg, 1, dwork,
                              static_cast<int>(work.size() / 2), scale, s);

@@ -10,17 +10,13 @@
 //   * the MMA warp interleaves the tiles: PV_0,j  S_0,j+1  PV_1,j  S_1,j+1 —
 //     while softmax WG 0 works on S_0,j+1 the tensor core runs tile 1's PV and
 //     S, and vice versa;
-//   * each tile's softmax runs on TWO warpgroups (one per 64-column half of
-//     S): the row max is exchanged once per step through shared memory and a
-//     256-thread named barrier, the row-sum halves are merged only at the
-//     end; two warps per SM sub-partition per tile hide the max->exp->pack
-//     latency chain that a single warpgroup exposes;
-//   * warp-group register split with setmaxnreg (producer/MMA WG keeps its
-//     launch budget, the four softmax WGs grow).
+//   * warp-group register split with setmaxnreg (producer/MMA WG shrinks,
+//     the two softmax WGs grow).
 // The union of the two tiles' visible KV tiles is streamed once; tile 0
 // (earlier queries) skips the causal tail it cannot see.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 
@@ -37,18 +33,16 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int kStages = 2;
-constexpr int kThreads = 640;        // WG0 (TMA, MMA, TMEM alloc) + 4 softmax WGs
-constexpr int kSoftmaxThreads = 256;  // per query tile: 2 warpgroups
+constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;
+constexpr int kDefaultPoly8 = 2;
 
 template <int HD>
 struct Cfg2 {
   static constexpr int kBoxes = HD / 64;
   static constexpr int kQBytes = BM * HD * 2;
   static constexpr int kKvBytes = BN * HD * 2;
-  // row-max exchange [tile][parity][half][row] + row-sum exchange [tile][half][row]
-  static constexpr int kXchgBytes = (2 * 2 * 2 * BM + 2 * 2 * BM) * 4;
-  static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + kXchgBytes + 1024 + 512;
+  static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + 1024 + 512;
 };
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): half the FMA-pipe
@@ -72,12 +66,18 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return d;
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 // 2^x for a pair on the FMA/ALU pipes (x <= 2^7): round-to-nearest split
 // x = n + f with the 1.5*2^23 trick, Taylor cubic for 2^f on [-1/2, 1/2]
 // (rel. err < 7e-4, under the bf16 rounding P gets anyway), 2^n by adding n
-// to the exponent field. Used for a quarter of the softmax exponentials so the
-// MUFU (ex2) pipe — shared by both softmax warpgroups of an SM sub-partition —
-// stops being the co-bottleneck with the tensor core.
+// to the exponent field. Used for kPoly8/8 of the softmax exponentials so the
+// MUFU (ex2) pipe (16/clk/SM, shared by both softmax warpgroups) stops being
+// the co-bottleneck with the tensor core.
 __device__ __forceinline__ void exp2_fma2(float x0, float x1, float& p0, float& p1) {
   const uint64_t x = f2pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
   const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
@@ -166,7 +166,7 @@ struct Steps {
     }                                              \
   } while (0)
 
-template <int HD, bool kProf>
+template <int HD, bool kProf, int kPoly8>
 __global__ void __launch_bounds__(kThreads, 1)
     ring_attention_v2(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
@@ -189,9 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQ = smem;                                 // [2][kQBytes]
   uint8_t* sK = sQ + 2 * C::kQBytes;                  // [kStages][kKvBytes]
   uint8_t* sV = sK + kStages * C::kKvBytes;           // [kStages][kKvBytes]
-  float* xchg_max = reinterpret_cast<float*>(sV + kStages * C::kKvBytes);  // [2][2][2][BM]
-  float* xchg_sum = xchg_max + 2 * 2 * 2 * BM;                              // [2][2][BM]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xchg_sum + 2 * 2 * BM);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * C::kKvBytes);
   uint64_t* q_full = bars;
   uint64_t* q_empty = bars + 1;
   uint64_t* k_full = bars + 2;
@@ -219,9 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[t], kSoftmaxThreads);
+      ptx::mbar_init(&p_full[t], 128);
       ptx::mbar_init(&o_done[t], 1);
-      ptx::mbar_init(&o_free[t], kSoftmaxThreads);
+      ptx::mbar_init(&o_free[t], 128);
     }
     ptx::fence_barrier_init();
   }
@@ -234,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_o[2] = {tmem + 2 * BN, tmem + 2 * BN + HD};
 
   if (warp < 4) {
+    ptx::setmaxnreg_dec<104>();
     if (warp == 0 && lane == 0) {
       // ---------------------------------------------------------- producer
       int ks = 0, vs = 0;
@@ -370,20 +369,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) prof_store(1);
     }
   } else {
-    ptx::setmaxnreg_inc<104>();
+    ptx::setmaxnreg_inc<192>();
     // ------------------------------------------------------------ softmax
-    // Warps 4..19: tile t = sw / 8, column half h = (sw / 4) % 2, TMEM lane
-    // quadrant = warp % 4. Thread = one query row x 64 score columns.
-    const int sw = static_cast<int>(warp) - 4;
-    const int t = sw >> 3;
-    const int h = (sw >> 2) & 1;
+    const int t = (warp >= 8) ? 1 : 0;
     const uint32_t quad = warp & 3;
     const int row = static_cast<int>(quad * 32 + lane);
     const uint32_t lane_off = (quad * 32) << 16;
-    constexpr int HO = HD / 2;  // O columns owned by this half
-    float* my_max = xchg_max + (t * 2 * 2) * BM;  // [parity][half][row]
-    float* my_sum = xchg_sum + (t * 2) * BM;      // [half][row]
-    const uint32_t bar_id = 1 + static_cast<uint32_t>(t);
     uint32_t cnt = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const Item it = load_item(work, w, segs);
@@ -391,48 +382,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       const RingSegment* sg = &segs[it.seg];
       const int q0 = it.q0[t];
       const int a = q0 + row;
-      float m_run = -INFINITY, l_half = 0.f;
+      float m_run = -INFINITY, l_run = 0.f;
       int j = 0;
       Steps st;
       for (st.begin(sg, it); st.valid(); st.next()) {
         if (t == 0 && !st.active0()) continue;
-        const int b0 = st.tt * BN + 64 * h;  // first key of this half
+        const int b0 = st.tt * BN;
         const int shift = sg->shift[st.r];
         const int kv_len = sg->kv_len[st.r];
         ESP_PROF_WAIT(0, ptx::mbar_wait(&s_full[t], cnt & 1));
         const uint64_t prof_t_step = kProf ? clock64() : 0;
         ptx::tc_fence_after();
-        uint32_t s[64];
+        uint32_t s[128];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < 4; ++c) {
           uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
-          ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 64 * h + 32 * c, chunk);
+          ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 32 * c, chunk);
         }
         ptx::tmem_wait_ld();
         if constexpr (kProf) prof_acc[2] += clock64() - prof_t_step;  // S readback
-        const bool full_half = (b0 + 63 <= q0 - shift) && (b0 + 64 <= kv_len);
-        if (!full_half) {
-          const int lim = min(a - shift - b0, kv_len - 1 - b0);  // visible iff c <= lim
+        const bool full_tile = (b0 + BN - 1 <= q0 - shift) && (b0 + BN <= kv_len);
+        if (!full_tile) {
+          const int lim = min(a - shift - b0, kv_len - 1 - b0);
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
+          for (int c = 0; c < 128; ++c) {
             if (c > lim) s[c] = __float_as_uint(-INFINITY);
           }
         }
+        // Row max with 8 independent chains of 3-input max (FMNMX3), then a tree.
         float mx8[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(s[k]);
-#pragma unroll
-        for (int c = 8; c < 64; c += 8) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(s[c + k]));
+        for (int k = 0; k < 8; ++k) {
+          mx8[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]),
+                         __uint_as_float(s[120 + k]));
         }
-        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        // Row max across the two halves (double-buffered by step parity).
-        float* slot = my_max + (cnt & 1) * 2 * BM;
-        slot[h * BM + row] = mx;
-        ptx::named_bar_sync(bar_id, kSoftmaxThreads);
-        mx = fmaxf(mx, slot[(h ^ 1) * BM + row]);
+#pragma unroll
+        for (int c = 16; c < 120; c += 16) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            mx8[k] = fmax3(mx8[k], __uint_as_float(s[c + k]), __uint_as_float(s[c + 8 + k]));
+          }
+        }
+        const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
+                               fmaxf(mx8[6], mx8[7]));
+        if constexpr (kProf) prof_acc[3] += clock64() - prof_t_step;  // ..through row max
         const float m_tile = mx * scale_log2;
         const float m_new = fmaxf(m_run, m_tile);
         const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY)
@@ -443,19 +436,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_run = m_new;
         }
         const float m_sub = m_run == -INFINITY ? 0.f : m_run;
-        // P in place: s[c] <- bf16x2(p[2c], p[2c+1]), then into this half's
-        // 32 P columns of S_t in TMEM.
+        // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
+        // precede the write of s[c], c <= 2c), then P over S_t in TMEM.
         const uint64_t scale2 = f2pack(scale_log2, scale_log2);
         const uint64_t negm2 = f2pack(-m_sub, -m_sub);
         uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < 64; ++c) {
           float x0, x1, p0, p1;
           f2unpack(ffma2(f2pack(__uint_as_float(s[2 * c]), __uint_as_float(s[2 * c + 1])),
                          scale2, negm2),
                    x0, x1);
-          if ((c & 3) == 3) {
-            exp2_fma2(x0, x1, p0, p1);  // 1 pair in 4 on the FMA pipe
+          if (((c * kPoly8) & 7) < kPoly8) {
+            exp2_fma2(x0, x1, p0, p1);  // kPoly8 pairs in 8 on the FMA pipe
           } else {
             p0 = ptx::ex2(x0);
             p1 = ptx::ex2(x1);
@@ -467,28 +460,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           s[c] = ptx::pack_bf16(p0, p1);
         }
-        float sa0, sa1;
+        float sa0, sa1, sb0, sb1;
         f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
-        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32 * h,
-                                *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        (void)sb0;
+        (void)sb1;
+        const float sum = sa0 + sa1;
+        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P store issue
         if (j > 0 && __any_sync(0xffffffff, need)) {
-          // O holds PV_{j-1}: wait for it, then rescale this half's columns
-          // in TMEM (rare: only when a row max grew by more than 2^8).
-          if constexpr (kProf) prof_acc[4] += 1;
-          ESP_PROF_WAIT(3, ptx::mbar_wait(&o_done[t], (cnt - 1) & 1));
+          // O holds PV_{j-1}: wait for it, then rescale in TMEM (rare: only
+          // when a row max grew by more than 2^8).
+          ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < HO; c += 32) {
+          for (int c = 0; c < HD; c += 32) {
             uint32_t o[32];
-            ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + HO * h + c, o);
+            ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
             ptx::tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            ptx::tmem_st_32x32b_x32(t_o[t] + lane_off + HO * h + c, o);
+            ptx::tmem_st_32x32b_x32(t_o[t] + lane_off + c, o);
           }
         }
         ptx::tmem_wait_st();
-        l_half = l_half * alpha + (sa0 + sa1);
+        l_run = l_run * alpha + sum;
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_full[t]);
         if constexpr (kProf) {
@@ -498,19 +494,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++cnt;
         ++j;
       }
-      // Final O / l: merge the two halves' row sums, normalise own columns.
-      my_sum[h * BM + row] = l_half;
-      ptx::named_bar_sync(bar_id, kSoftmaxThreads);
-      const float l_run = l_half + my_sum[(h ^ 1) * BM + row];
+      // Final O / l for this tile's rows.
       ESP_PROF_WAIT(6, ptx::mbar_wait(&o_done[t], (cnt - 1) & 1));
       ptx::tc_fence_after();
       const bool valid = a < sg->q_len;
       const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-      bf16* orow = out + static_cast<int64_t>(sg->q_row0 + a) * hidden + it.head * HD + HO * h;
+      bf16* orow = out + static_cast<int64_t>(sg->q_row0 + a) * hidden + it.head * HD;
 #pragma unroll 1
-      for (int c = 0; c < HO; c += 32) {
+      for (int c = 0; c < HD; c += 32) {
         uint32_t o[32];
-        ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + HO * h + c, o);
+        ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
         ptx::tmem_wait_ld();
         if (valid) {
           uint4* d = reinterpret_cast<uint4*>(orow + c);
@@ -527,13 +520,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      // The sum exchange slot is rewritten by the next item: no thread may run
-      // ahead before its partner has read it.
-      ptx::named_bar_sync(bar_id, kSoftmaxThreads);
       ptx::tc_fence_before();
       ptx::mbar_arrive(&o_free[t]);
     }
-    if (quad == 0 && lane == 0 && h == 0) prof_store(2 + t);
+    if (quad == 0 && lane == 0) prof_store(2 + t);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -553,14 +543,14 @@ int sm_count2() {
   return n;
 }
 
-template <int HD, bool kProf>
+template <int HD, bool kProf, int kPoly8>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s, uint64_t* prof) {
   using C = Cfg2<HD>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(ring_attention_v2<HD, kProf>,
+    cudaFuncSetAttribute(ring_attention_v2<HD, kProf, kPoly8>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const int hidden = heads * HD;
@@ -568,7 +558,7 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
   const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
   const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
-  ring_attention_v2<HD, kProf><<<grid, kThreads, C::kSmem, s>>>(
+  ring_attention_v2<HD, kProf, kPoly8><<<grid, kThreads, C::kSmem, s>>>(
       tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof);
   count_launch();
 }
@@ -579,12 +569,24 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
                int n_work, float scale, cudaStream_t s, uint64_t* prof) {
   if (n_work <= 0) return;
   if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
+  // Exponentials computed on the FMA pipe, in eighths (MUFU/FMA balance);
+  // ESP_ATTN_POLY overrides for kernel studies.
+  static const int poly = [] {
+    const char* e = getenv("ESP_ATTN_POLY");
+    return e ? atoi(e) : kDefaultPoly8;
+  }();
+#define ESP_LAUNCH2(HD_, P_)                                                                \
+  launch2<HD_, kProf, P_>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, \
+                          s, prof)
   if (head_dim == 128) {
-    launch2<128, kProf>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s,
-                        prof);
+    switch (poly) {
+      case 2: ESP_LAUNCH2(128, 2); break;
+      case 3: ESP_LAUNCH2(128, 3); break;
+      case 5: ESP_LAUNCH2(128, 5); break;
+      default: ESP_LAUNCH2(128, 4); break;
+    }
   } else if (head_dim == 64) {
-    launch2<64, kProf>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s,
-                       prof);
+    ESP_LAUNCH2(64, kDefaultPoly8);
   } else {
     throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
   }

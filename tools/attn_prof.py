@@ -1,14 +1,30 @@
 """Ring-attention kernel study at the LWM-7B 32K shape (one 32768-token
-stripe, 32 heads x 128): CUDA-event time of the production kernel and, with
-ESP_ATTN_PROF=1, the per-role cycle accounting of the instrumented build."""
-import math
+stripe, 32 heads x 128): CUDA-event time of the production kernel over
+ESP_ATTN_REPEAT launches on staged buffers (printed by the hook as
+[attn-time]) with the SM clock sampled meanwhile, and, with ESP_ATTN_PROF=1,
+the per-role cycle accounting of the instrumented build."""
 import os
+import statistics
 import sys
+import threading
+import time
 
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2404_09526_b200 import abi  # noqa: E402
+
+
+def sample_clocks(stop, out):
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        while not stop.is_set():
+            out.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            time.sleep(0.02)
+    except Exception as e:  # noqa: BLE001
+        print(f"clock sampling unavailable: {e}", file=sys.stderr)
 
 
 def main():
@@ -27,22 +43,25 @@ def main():
                              out.data_ptr(), heads, hd)
 
     os.environ.pop("ESP_ATTN_PROF", None)
-    for variant in ("v2", "v1"):
-        if variant == "v1":
-            os.environ["ESP_ATTN_V1"] = "1"
-        else:
-            os.environ.pop("ESP_ATTN_V1", None)
-        run()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(3):
-            run()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 3  # includes the hook's staging copies
-        print(f"{variant}: {ms:.3f} ms/launch (with staging), {flop / ms / 1e9:.0f} TFLOP/s")
     os.environ.pop("ESP_ATTN_V1", None)
+    run()
+    torch.cuda.synchronize()
+    n = int(os.environ.get("REPEAT", "10"))
+    os.environ["ESP_ATTN_REPEAT"] = str(n)
+    clocks, stop = [], threading.Event()
+    th = threading.Thread(target=sample_clocks, args=(stop, clocks))
+    th.start()
+    t0 = time.time()
+    run()
+    torch.cuda.synchronize()
+    wall = time.time() - t0
+    stop.set()
+    th.join()
+    os.environ.pop("ESP_ATTN_REPEAT")
+    sys.stderr.flush()
+    mhz = statistics.median(clocks) if clocks else float("nan")
+    print(f"flop/launch {flop:.4e}; wall {wall:.2f}s for {n} launches; "
+          f"SM clock median {mhz:.0f} MHz over {len(clocks)} samples", flush=True)
     os.environ["ESP_ATTN_PROF"] = "1"
     run()
     torch.cuda.synchronize()

@@ -16,13 +16,18 @@ run() {  # name timeout cmd...
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv | tee gpurun_out/gpu.txt
 for s in $STEPS; do
   case $s in
-    tests) run t_kernels 900 python -m pytest tests/test_kernels_gpu.py -v --timeout 120 ;;
+    tests) run t_kernels 400 python -m pytest tests/test_kernels_gpu.py -v --timeout 120 --timeout-method=thread ;;
     smoke) run smoke 300 python -c "import __graft_entry__ as g; g.smoke()" ;;
-    e2e) run t_e2e 1200 python -m pytest tests/test_e2e_gpu.py -v --timeout 400 ;;
-    gputests) run t_gpu 1800 python -m pytest tests -m gpu -q --timeout 400 ;;
+    e2e) run t_e2e 1200 python -m pytest tests/test_e2e_gpu.py -v --timeout 400 --timeout-method=thread ;;
+    gputests) run t_gpu 1800 python -m pytest tests -m gpu -q --timeout 400 --timeout-method=thread ;;
     bench) run bench 900 python bench.py ;;
     benchq) run bench_quick 600 python bench.py --steps 2 --warmup 1 --skip-cpu ;;
     kbench) run kbench 300 python tools/kbench.py ;;
+    aprof) run attn_prof 300 python tools/attn_prof.py ;;
+    apoly)
+      for r in 1 2; do for p in 2 3 4 5; do
+        export ESP_ATTN_POLY=$p; run attn_poly${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_POLY
+      done; done ;;
     ncu)
       run ncu_launches 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --skip-decode \
