@@ -140,15 +140,17 @@ def barrier(dist):
 
 # ---- CPU baseline: the dense oracle on the host cores --------------------------
 
-def cpu_sample(seconds_hint=True):
+def cpu_sample(default_tokens=512):
     """One bounded sample of the workload on the host: ONE of the 32 LWM-7B
     layers prefilling S_CPU tokens (dense fp32 oracle, all host threads), then
-    FLOP-extrapolated to the full 32-layer, 32768-token prefill."""
+    FLOP-extrapolated to the full 32-layer, 32768-token prefill. The GPU arm's
+    cpu_baseline uses 2048 tokens (~10 s on 16 cores); each reference-arm step
+    512 (~1 s) so a K-step run stays within minutes."""
     import numpy as np
 
     from oracle import llama_ref
     from paper_2404_09526_b200.abi import ModelShape
-    S_CPU = int(os.environ.get("ESP_BENCH_CPU_TOKENS", "512"))
+    S_CPU = int(os.environ.get("ESP_BENCH_CPU_TOKENS", str(default_tokens)))
     shape = ModelShape(layers=1, hidden=H, heads=32, head_dim=128, ffn=F, vocab=V)
     prompt = np.random.default_rng(7).integers(0, V, S_CPU).astype(np.int32)
     threads = os.cpu_count() or 1
@@ -278,7 +280,7 @@ def run_gpu(args):
     rt.close()
     if rank == 0 and not args.skip_cpu:
         try:
-            line["cpu_baseline"] = cpu_sample()
+            line["cpu_baseline"] = cpu_sample(2048)
         except Exception as e:  # report, never hide
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     if rank == 0:

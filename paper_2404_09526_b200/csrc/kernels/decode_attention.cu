@@ -50,7 +50,10 @@ __global__ void __launch_bounds__(kWarps * 32)
                             float* __restrict__ part_o, float* __restrict__ part_ml) {
   constexpr int LPT = HD / 8;     // lanes per token
   constexpr int TPW = 32 / LPT;   // tokens per warp step
-  const int ci = blockIdx.x, head = blockIdx.y;
+  // blockIdx.x = head (fastest): the CTAs resident at a time cover every head
+  // of a few chunks, so each token's whole K/V row (all heads, contiguous) is
+  // read at about the same time (DRAM page locality).
+  const int head = blockIdx.x, ci = blockIdx.y;
   const DecodeChunk ch = chunks[ci];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / LPT;          // token group within the warp
@@ -207,7 +210,8 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
                       float* part_o, float* part_ml, cudaStream_t s) {
   if (n_chunks <= 0) return;
-  const dim3 grid(n_chunks, heads);
+  if (n_chunks > 65535) throw std::runtime_error("decode_attention: more than 65535 chunks");
+  const dim3 grid(heads, n_chunks);
   const float sl2 = scale * 1.4426950408889634f;
   if (head_dim == 128) {
     decode_attention_kernel<128><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads, sl2,

@@ -13,8 +13,10 @@
 //   instance (the QKV projection of ESP prefill; the KV append of decode).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -83,16 +85,60 @@ __device__ __forceinline__ void store_vals_bf16(bf16* dst, const float (&v)[32])
   }
 }
 
-template <int BN>
-__device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t tacc, int m,
+// Accumulator sources of the epilogue: TMEM (the GEMM kernels) or an fp32
+// row in global memory (the stream-K finalize of skinny GEMMs).
+struct TmemAcc {
+  uint32_t base;
+  __device__ __forceinline__ void load(int c, uint32_t (&r)[32]) const {
+    ptx::tmem_ld_32x32b_x32(base + c, r);
+  }
+  __device__ __forceinline__ void wait() const { ptx::tmem_wait_ld(); }
+};
+// Sum, in segment order (deterministic), of the fp32 partial rows that the
+// stream-K segments of one tile left in their workspace slots.
+struct SegSumAcc {
+  const float* row;  // segment 0's row
+  int nseg;
+  int64_t stride;    // floats between consecutive segments' slots
+  __device__ __forceinline__ void load(int c, uint32_t (&r)[32]) const {
+    float4 v[8];  // all loads of a segment in flight together (L2 latency)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldcg(reinterpret_cast<const float4*>(row + c) + i);
+    for (int sg = 1; sg < nseg; ++sg) {
+      float4 w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        w[i] = __ldcg(reinterpret_cast<const float4*>(row + sg * stride + c) + i);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i].x += w[i].x;
+        v[i].y += w[i].y;
+        v[i].z += w[i].z;
+        v[i].w += w[i].w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      r[4 * i] = __float_as_uint(v[i].x);
+      r[4 * i + 1] = __float_as_uint(v[i].y);
+      r[4 * i + 2] = __float_as_uint(v[i].z);
+      r[4 * i + 3] = __float_as_uint(v[i].w);
+    }
+  }
+  __device__ __forceinline__ void wait() const {}
+};
+
+template <int BN, typename Acc>
+__device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc& acc, int m,
                                               bool valid, int nb, int N) {
   uint32_t r[32];
   if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32 ||
       ep.kind == kEpiAtomicF32) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
-      ptx::tmem_ld_32x32b_x32(tacc + c, r);
-      ptx::tmem_wait_ld();
+      acc.load(c, r);
+      acc.wait();
       if (!valid) continue;
       const int64_t off = static_cast<int64_t>(m) * ep.ldo + nb * BN + c;
       if (ep.kind == kEpiAtomicF32) {
@@ -134,9 +180,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t t
     for (int p = 0; p < BN / 128; ++p) {
 #pragma unroll 1
       for (int c = 0; c < 64; c += 32) {
-        ptx::tmem_ld_32x32b_x32(tacc + p * 128 + c, r);
-        ptx::tmem_ld_32x32b_x32(tacc + p * 128 + 64 + c, u);
-        ptx::tmem_wait_ld();
+        acc.load(p * 128 + c, r);
+        acc.load(p * 128 + 64 + c, u);
+        acc.wait();
         if (!valid) continue;
         float v[32];
 #pragma unroll
@@ -175,8 +221,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t t
     if (region == 2) {
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
-        ptx::tmem_ld_32x32b_x32(tacc + c, r);
-        ptx::tmem_wait_ld();
+        acc.load(c, r);
+        acc.wait();
         if (!valid) continue;
         if (dst_main) store_row_bf16(dst_main + row_off + col0 + c, r);
         if (dst_slab) store_row_bf16(dst_slab + col0 + c, r);
@@ -188,9 +234,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t t
       for (int hb = 0; hb < BN; hb += hd) {
 #pragma unroll 1
         for (int j = 0; j < half; j += 32) {
-          ptx::tmem_ld_32x32b_x32(tacc + hb + j, r);
-          ptx::tmem_ld_32x32b_x32(tacc + hb + j + half, h);
-          ptx::tmem_wait_ld();
+          acc.load(hb + j, r);
+          acc.load(hb + j + half, h);
+          acc.wait();
           if (!valid) continue;
           float lo[32], hi[32];
 #pragma unroll
@@ -215,14 +261,49 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, uint32_t t
   }
 }
 
-// Work unit u = (output tile u / k_splits, K slice u % k_splits). With
-// k_splits > 1 the epilogue must be kEpiAtomicF32 (fp32 reduction into a
-// workspace, finalized by residual_finalize).
+// Work of one persistent CTA: whole output tiles round-robin (kb_per_cta ==
+// 0), or stream-K (kb_per_cta > 0): the (tile, K block) space is cut into
+// equal contiguous ranges of kb_per_cta K blocks, one per CTA, each range
+// split at tile boundaries into segments whose partial sums the epilogue
+// (kEpiAtomicF32) adds into an fp32 workspace.
+struct WorkRange {
+  int next, end, num_k, stride;
+  bool stream;
+  __device__ WorkRange(int tiles, int num_k_, int kb_per_cta) : num_k(num_k_) {
+    stream = kb_per_cta > 0;
+    if (stream) {
+      next = static_cast<int>(blockIdx.x) * kb_per_cta;
+      end = min(tiles * num_k, next + kb_per_cta);
+      stride = 0;
+    } else {
+      next = static_cast<int>(blockIdx.x);
+      end = tiles;
+      stride = static_cast<int>(gridDim.x);
+    }
+  }
+  __device__ bool get(int& tile, int& kb0, int& kb1) {
+    if (next >= end) return false;
+    if (stream) {
+      tile = next / num_k;
+      kb0 = next - tile * num_k;
+      kb1 = min(num_k, kb0 + (end - next));
+      next += kb1 - kb0;
+    } else {
+      tile = next;
+      kb0 = 0;
+      kb1 = num_k;
+      next += stride;
+    }
+    return true;
+  }
+};
+
 template <int BN, bool kSkinny>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-                      int k_splits, const __grid_constant__ GemmEpilogue ep) {
+                      int kb_per_cta, const __grid_constant__ GemmEpilogue ep,
+                      float* __restrict__ ws, int* __restrict__ tile_kb) {
   using C = Cfg<BN, kSkinny>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -234,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile uint32_t* last_flag = tmem_slot + 1;
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   if (warp == 0 && lane == 0) {
@@ -256,18 +338,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_m = (M + BM - 1) / BM, num_n = N / BN, num_k = K / BK;
-  const int units = num_m * num_n * k_splits;
-  const int kb_per = (num_k + k_splits - 1) / k_splits;
+  const int tiles = num_m * num_n;
+  WorkRange work(tiles, num_k, kb_per_cta);
+  int tile, kb0, kb1;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       const uint64_t keep = ptx::policy_evict_last();
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      while (work.get(tile, kb0, kb1)) {
         int mb, nb;
-        tile_coords(u / k_splits, num_m, num_n, mb, nb);
-        const int kb0 = (u % k_splits) * kb_per, kb1 = min(num_k, kb0 + kb_per);
+        tile_coords(tile, num_m, num_n, mb, nb);
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], C::kTxBytes);
@@ -289,10 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int lt = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+    for (; work.get(tile, kb0, kb1); ++lt) {
       const int acc = lt & 1;
       const uint32_t use = static_cast<uint32_t>(lt >> 1);
-      const int kb0 = (u % k_splits) * kb_per, kb1 = min(num_k, kb0 + kb_per);
       ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -321,18 +402,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t quad = warp & 3;
     const int row = static_cast<int>(quad * 32 + lane);
     int lt = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+    for (; work.get(tile, kb0, kb1); ++lt) {
       int mb, nb;
-      tile_coords(u / k_splits, num_m, num_n, mb, nb);
+      tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = lt & 1;
       const uint32_t use = static_cast<uint32_t>(lt >> 1);
       ptx::mbar_wait(&tfull[acc], use & 1);
       ptx::tc_fence_after();
       const uint32_t tacc = tmem_base + acc * BN + ((quad * 32) << 16);
       const int m = mb * BM + row;
-      epilogue_tile<BN>(ep, tacc, m, m < M, nb, N);
+      if (!work.stream) {
+        epilogue_tile<BN>(ep, TmemAcc{tacc}, m, m < M, nb, N);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        continue;
+      }
+      // Stream-K: store this segment's fp32 partial rows in its own
+      // workspace slot (no atomics), free the accumulator, and count the
+      // tile's K blocks; the CTA that completes the tile sums the slots in
+      // segment order and applies the real epilogue.
+      const int max_seg = (num_k + kb_per_cta - 1) / kb_per_cta + 1;
+      const int first_cta = tile * num_k / kb_per_cta;
+      const int last_cta = ((tile + 1) * num_k - 1) / kb_per_cta;
+      const int64_t slot_floats = static_cast<int64_t>(M) * BN;
+      float* tile_ws = ws + static_cast<int64_t>(tile) * max_seg * slot_floats;
+      float* my_row = tile_ws + (static_cast<int>(blockIdx.x) - first_cta) * slot_floats +
+                      static_cast<int64_t>(m) * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tacc + c, r);
+        ptx::tmem_wait_ld();
+        if (m < M) {
+          float4* d = reinterpret_cast<float4*>(my_row + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            __stcg(d + i, make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                      __uint_as_float(r[4 * i + 2]),
+                                      __uint_as_float(r[4 * i + 3])));
+          }
+        }
+      }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
+      __threadfence();
+      ptx::named_bar_sync(1, 128);
+      if (threadIdx.x == 128) {
+        const int done = atomicAdd(&tile_kb[tile], kb1 - kb0) + (kb1 - kb0);
+        *last_flag = done == num_k ? 1u : 0u;
+      }
+      ptx::named_bar_sync(1, 128);
+      if (*last_flag) {
+        __threadfence();
+        if (m < M) {
+          const SegSumAcc sum{tile_ws + static_cast<int64_t>(m) * BN, last_cta - first_cta + 1,
+                              slot_floats};
+          epilogue_tile<BN>(ep, sum, m, true, nb, N);
+        }
+        if (threadIdx.x == 128) tile_kb[tile] = 0;
+      }
+      ptx::named_bar_sync(1, 128);  // last_flag is rewritten by the next segment
     }
   }
   ptx::tc_fence_before();
@@ -471,7 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const uint32_t tacc = tmem_base + acc * kTileN + ((quad * 32) << 16);
       const int m = mb * kTileM + static_cast<int>(rank) * kRows + row;
-      epilogue_tile<kTileN>(ep, tacc, m, m < M, nb, N);
+      epilogue_tile<kTileN>(ep, TmemAcc{tacc}, m, m < M, nb, N);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(tempty_lead + acc * 8);
@@ -538,7 +667,8 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
 
 template <int BN, bool kSkinny>
 static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
-                        int k_splits, const GemmEpilogue& ep, cudaStream_t s) {
+                        int kb_per_cta, const GemmEpilogue& ep, cudaStream_t s,
+                        float* ws = nullptr, int* tile_kb = nullptr) {
   using C = Cfg<BN, kSkinny>;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -547,9 +677,11 @@ static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, i
   });
   const CUtensorMap ta = make_tmap_bf16(A, M, K, lda, C::kARows);
   const CUtensorMap tb = make_tmap_bf16(B, N, K, ldb, BN);
-  const int units = ((M + BM - 1) / BM) * (N / BN) * k_splits;
-  const int grid = units < num_sms() ? units : num_sms();
-  gemm_bf16_tcgen05<BN, kSkinny><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, k_splits, ep);
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
+                                  : std::min(tiles, num_sms());
+  gemm_bf16_tcgen05<BN, kSkinny><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, kb_per_cta,
+                                                                  ep, ws, tile_kb);
   count_launch();
 }
 
@@ -598,37 +730,38 @@ static bool launch_gemm_pair(const bf16* A, int lda, const bf16* B, int ldb, int
   return true;
 }
 
-__global__ void residual_finalize_kernel(bf16* __restrict__ x, int ldx, float* __restrict__ ws,
-                                         int M, int N) {
-  const int64_t n_elems = static_cast<int64_t>(M) * N;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_elems;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t m = i / N, n = i % N;
-    bf16* p = x + m * ldx + n;
-    *p = __float2bfloat16_rn(__bfloat162float(*p) + ws[i]);
-    ws[i] = 0.f;  // leave the workspace zeroed for the next split-K GEMM
-  }
-}
-
-// Zero-initialised fp32 split-K workspace of the current device (kept zeroed
-// by residual_finalize_kernel after each use).
-float* splitk_workspace(size_t elems, cudaStream_t s) {
-  static std::unordered_map<int, std::pair<float*, size_t>> ws;
+// Stream-K workspace per (device, stream) — concurrent GEMMs on different
+// streams of one device never share it: fp32 partial-row slots [tile][segment]
+// [M x 128], and one zero-initialised K-block counter per output tile at the
+// end of the buffer (the CTA that completes a tile re-zeroes it).
+struct StreamKWs {
+  float* sums;
+  int* tile_kb;
+};
+StreamKWs streamk_workspace(size_t elems, size_t tiles, cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<char*, size_t>> ws;
   int dev = 0;
   cudaGetDevice(&dev);
-  auto& w = ws[dev];
-  if (w.second < elems) {
+  std::lock_guard<std::mutex> g(mu);
+  auto& w = ws[{dev, s}];
+  const size_t sum_bytes = (elems * sizeof(float) + 255) & ~static_cast<size_t>(255);
+  const size_t need = sum_bytes + tiles * sizeof(int);
+  if (w.second < need) {
     if (w.first) {
       cudaStreamSynchronize(s);
       cudaFree(w.first);
     }
-    w.second = std::max(elems, static_cast<size_t>(1) << 20);
-    if (cudaMalloc(&w.first, w.second * sizeof(float)) != cudaSuccess) {
-      throw std::runtime_error("split-K workspace allocation failed");
+    w.second = std::max(need * 2, static_cast<size_t>(8) << 20);
+    if (cudaMalloc(&w.first, w.second) != cudaSuccess) {
+      throw std::runtime_error("stream-K workspace allocation failed");
     }
-    cudaMemsetAsync(w.first, 0, w.second * sizeof(float), s);
+    cudaMemsetAsync(w.first, 0, w.second, s);
   }
-  return w.first;
+  // Counters live at the END of the buffer so their offset does not depend
+  // on this call's slot layout (all counters are zero between calls).
+  return {reinterpret_cast<float*>(w.first),
+          reinterpret_cast<int*>(w.first + w.second) - tiles};
 }
 
 void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
@@ -636,27 +769,28 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
   if (M <= 0) return;
   if (N % 128 != 0 || K % 64 != 0) throw std::runtime_error("gemm: N%128 or K%64 != 0");
   if (M <= 32) {
-    // Decode-shaped: weight-streaming bound. Skinny pipeline; when the N
-    // tiles alone cannot occupy the SMs (O / down projections), split K and
-    // reduce in fp32 before the residual add.
-    const int tiles = N / 128, num_k = K / BK;
-    if (ep.kind == kEpiResidual && tiles < num_sms()) {
-      int k_splits = std::min(num_k, (2 * num_sms() + tiles - 1) / tiles);
-      const int kb_per = (num_k + k_splits - 1) / k_splits;
-      k_splits = (num_k + kb_per - 1) / kb_per;  // no empty K slice
-      float* w = splitk_workspace(static_cast<size_t>(M) * N, s);
-      GemmEpilogue ea;
-      ea.kind = kEpiAtomicF32;
-      ea.out = w;
-      ea.ldo = N;
-      launch_gemm<128, true>(A, lda, B, ldb, M, N, K, k_splits, ea, s);
-      const int64_t n_elems = static_cast<int64_t>(M) * N;
-      residual_finalize_kernel<<<static_cast<unsigned>(std::min<int64_t>((n_elems + 255) / 256, 1024)),
-                                 256, 0, s>>>(static_cast<bf16*>(ep.out), ep.ldo, w, M, N);
-      count_launch();
+    // Decode-shaped: weight-streaming bound. Skinny pipeline, stream-K over
+    // (tile, K block) so every SM streams the same number of weight tiles
+    // whatever N / 128 is (96 QKV tiles, 172 gate_up tiles, 32 O tiles on
+    // 148 SMs); the CTA completing a tile applies the fused epilogue to its
+    // fp32 partial sums.
+    const int tiles = N / 128, total = tiles * (K / BK);
+    // Stream-K pays only when the tiles leave most SMs idle AND each tile is
+    // long enough to amortise the fixup tail (~10 us: partial store, counter,
+    // in-order sum): the down projection (32 tiles x 172 K blocks: 40 -> 29
+    // us). O (32 x 64) and the wide projections stream faster as whole tiles
+    // (tools/skinny_probe.py).
+    const bool streamk = 2 * tiles < num_sms() && K / BK >= 128;
+    if (getenv("ESP_GEMM_NO_STREAMK") != nullptr ||
+        (getenv("ESP_GEMM_STREAMK_ALL") == nullptr && !streamk)) {
+      launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 0, ep, s);
       return;
     }
-    launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 1, ep, s);
+    const int per = (total + num_sms() - 1) / num_sms();
+    const int max_seg = (K / BK + per - 1) / per + 1;
+    const StreamKWs w =
+        streamk_workspace(static_cast<size_t>(tiles) * max_seg * M * 128, tiles, s);
+    launch_gemm<128, true>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
     return;
   }
   if (launch_gemm_pair(A, lda, B, ldb, M, N, K, ep, s)) return;
@@ -664,9 +798,9 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
   const int tiles256 = ((M + BM - 1) / BM) * (N / 256);
   // Prefer the wide tile unless it would leave SMs idle.
   if (n256 && tiles256 >= num_sms()) {
-    launch_gemm<256, false>(A, lda, B, ldb, M, N, K, 1, ep, s);
+    launch_gemm<256, false>(A, lda, B, ldb, M, N, K, 0, ep, s);
   } else {
-    launch_gemm<128, false>(A, lda, B, ldb, M, N, K, 1, ep, s);
+    launch_gemm<128, false>(A, lda, B, ldb, M, N, K, 0, ep, s);
   }
 }
 

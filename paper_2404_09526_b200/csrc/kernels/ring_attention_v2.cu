@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* v_full = k_empty + kStages;
   uint64_t* v_empty = v_full + kStages;
   uint64_t* s_full = v_empty + kStages;  // [2] per query tile
-  uint64_t* p_full = s_full + 2;         // [2]
-  uint64_t* o_done = p_full + 2;         // [2]
+  uint64_t* p_full = s_full + 2;         // [2 tiles][2 key halves]
+  uint64_t* o_done = p_full + 4;         // [2]
   uint64_t* o_free = o_done + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&p_full[2 * t], 128);
+      ptx::mbar_init(&p_full[2 * t + 1], 128);
       ptx::mbar_init(&o_done[t], 1);
       ptx::mbar_init(&o_free[t], 128);
     }
@@ -332,14 +333,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int t = 0; t < 2; ++t) {
             if (a_now[t]) {
               if (first_pv[t]) ESP_PROF_WAIT(5, ptx::mbar_wait(&o_free[t], (titems[t] & 1) ^ 1));
-              ESP_PROF_WAIT(3 + t, ptx::mbar_wait(&p_full[t], cnt[t] & 1));
-              ptx::tc_fence_after();
 #pragma unroll
-              for (int k = 0; k < BN / 16; ++k) {
-                const uint64_t dv = ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024);
-                if (leader) {
-                  ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8, dv, idesc_o,
-                                   (!first_pv[t] || k != 0) ? 1u : 0u);
+              for (int half = 0; half < 2; ++half) {
+                ESP_PROF_WAIT(3 + t, ptx::mbar_wait(&p_full[2 * t + half], cnt[t] & 1));
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int k = 4 * half; k < 4 * half + 4; ++k) {
+                  const uint64_t dv = ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024);
+                  if (leader) {
+                    ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8, dv, idesc_o,
+                                     (!first_pv[t] || k != 0) ? 1u : 0u);
+                  }
                 }
               }
               commit(&o_done[t]);
@@ -402,8 +406,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_wait_ld();
         if constexpr (kProf) prof_acc[2] += clock64() - prof_t_step;  // S readback
         const bool full_tile = (b0 + BN - 1 <= q0 - shift) && (b0 + BN <= kv_len);
+        const int lim = min(a - shift - b0, kv_len - 1 - b0);  // visible iff c <= lim
         if (!full_tile) {
-          const int lim = min(a - shift - b0, kv_len - 1 - b0);
 #pragma unroll
           for (int c = 0; c < 128; ++c) {
             if (c > lim) s[c] = __float_as_uint(-INFINITY);
@@ -436,41 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_run = m_new;
         }
         const float m_sub = m_run == -INFINITY ? 0.f : m_run;
-        // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
-        // precede the write of s[c], c <= 2c), then P over S_t in TMEM.
-        const uint64_t scale2 = f2pack(scale_log2, scale_log2);
-        const uint64_t negm2 = f2pack(-m_sub, -m_sub);
-        uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          float x0, x1, p0, p1;
-          f2unpack(ffma2(f2pack(__uint_as_float(s[2 * c]), __uint_as_float(s[2 * c + 1])),
-                         scale2, negm2),
-                   x0, x1);
-          if (((c * kPoly8) & 7) < kPoly8) {
-            exp2_fma2(x0, x1, p0, p1);  // kPoly8 pairs in 8 on the FMA pipe
-          } else {
-            p0 = ptx::ex2(x0);
-            p1 = ptx::ex2(x1);
-          }
-          if (c & 1) {
-            sum2b = fadd2(sum2b, f2pack(p0, p1));
-          } else {
-            sum2a = fadd2(sum2a, f2pack(p0, p1));
-          }
-          s[c] = ptx::pack_bf16(p0, p1);
-        }
-        float sa0, sa1, sb0, sb1;
-        f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
-        (void)sb0;
-        (void)sb1;
-        const float sum = sa0 + sa1;
-        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-        if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P store issue
         if (j > 0 && __any_sync(0xffffffff, need)) {
-          // O holds PV_{j-1}: wait for it, then rescale in TMEM (rare: only
-          // when a row max grew by more than 2^8).
+          // O holds PV_{j-1} (complete: S_j, issued after it, is done) —
+          // rescale it in TMEM before PV_j accumulates (rare: only when a row
+          // max grew by more than 2^8).
           ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll 1
@@ -483,10 +456,61 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_st_32x32b_x32(t_o[t] + lane_off + c, o);
           }
         }
-        ptx::tmem_wait_st();
-        l_run = l_run * alpha + sum;
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&p_full[t]);
+        // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
+        // precede the write of s[c], c <= 2c), then P over S_t in TMEM, in two
+        // halves of 64 keys: the MMA warp starts PV on keys 0..63 while keys
+        // 64..127 are still being exponentiated.
+        const uint64_t scale2 = f2pack(scale_log2, scale_log2);
+        const uint64_t negm2 = f2pack(-m_sub, -m_sub);
+        uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (half == 1) {
+            // Re-read S for keys 64..127 (intact: P so far covers columns
+            // 0..31) so the second half's exponentials cannot be scheduled
+            // ahead of the first half's P store and arrive.
+#pragma unroll
+            for (int c = 2; c < 4; ++c) {
+              uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
+              ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 32 * c, chunk);
+            }
+            ptx::tmem_wait_ld();
+            if (!full_tile) {  // the causal mask again on the re-read half
+#pragma unroll
+              for (int c = 64; c < 128; ++c) {
+                if (c > lim) s[c] = __float_as_uint(-INFINITY);
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 32 * half; c < 32 * half + 32; ++c) {
+            float x0, x1, p0, p1;
+            f2unpack(ffma2(f2pack(__uint_as_float(s[2 * c]), __uint_as_float(s[2 * c + 1])),
+                           scale2, negm2),
+                     x0, x1);
+            if (((c * kPoly8) & 7) < kPoly8) {
+              exp2_fma2(x0, x1, p0, p1);  // kPoly8 pairs in 8 on the FMA pipe
+            } else {
+              p0 = ptx::ex2(x0);
+              p1 = ptx::ex2(x1);
+            }
+            if (c & 1) {
+              sum2b = fadd2(sum2b, f2pack(p0, p1));
+            } else {
+              sum2a = fadd2(sum2a, f2pack(p0, p1));
+            }
+            s[c] = ptx::pack_bf16(p0, p1);
+          }
+          ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32 * half,
+                                  *reinterpret_cast<uint32_t(*)[32]>(&s[32 * half]));
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&p_full[2 * t + half]);
+        }
+        if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P stored
+        float sa0, sa1;
+        f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
+        l_run = l_run * alpha + (sa0 + sa1);
         if constexpr (kProf) {
           prof_acc[1] += clock64() - prof_t_step;  // softmax step (S ready -> P ready)
           prof_acc[5] += 1;

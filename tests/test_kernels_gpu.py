@@ -48,8 +48,8 @@ def test_gemm_f32_and_residual():
 @pytest.mark.parametrize("M,N,K", [(16, 4096, 4096), (16, 4096, 11008), (1, 512, 1536),
                                    (32, 1024, 640)])
 def test_gemm_skinny_splitk_residual(M, N, K):
-    """Decode-shaped residual GEMMs take the skinny split-K path (fp32
-    reduction in a workspace, then residual add)."""
+    """Decode-shaped residual GEMMs take the skinny stream-K path (fp32
+    reduction in a workspace, then the residual add in the finalize)."""
     torch.manual_seed(M + N + K)
     a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
     b = torch.randn(N, K, device="cuda", dtype=torch.bfloat16)
@@ -60,6 +60,34 @@ def test_gemm_skinny_splitk_residual(M, N, K):
         abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, 1)
     torch.cuda.synchronize()
     assert _rel(d, r.float() + a.float() @ b.float().t()) < 1e-2
+
+
+@pytest.mark.parametrize("M", [1, 16, 32])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", ["streamk", "tiles"])
+def test_gemm_skinny_epilogues(M, epi, mode, monkeypatch):
+    """Decode-shaped GEMMs, both skinny schedules: stream-K (per-segment fp32
+    partial slots, the CTA completing a tile sums them in order and applies
+    the fused epilogue) and whole tiles; store, residual, fp32, SiLU(gate)*up."""
+    monkeypatch.setenv("ESP_GEMM_STREAMK_ALL" if mode == "streamk" else "ESP_GEMM_NO_STREAMK", "1")
+    torch.manual_seed(M * 10 + epi)
+    N, K = 22016 if epi == 3 else 12288, 4096
+    a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.05
+    ncols = N // 2 if epi == 3 else N
+    r = torch.randn(M, ncols, device="cuda", dtype=torch.bfloat16)
+    for _ in range(2):  # second call checks the tile counters were reset
+        d = r.clone() if epi == 1 else torch.empty(
+            M, ncols, device="cuda", dtype=torch.float32 if epi == 2 else torch.bfloat16)
+        abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi)
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float().t()
+    if epi == 1:
+        ref = r.float() + ref
+    if epi == 3:
+        g = ref.view(M, -1, 2, 64)
+        ref = (torch.nn.functional.silu(g[:, :, 0]) * g[:, :, 1]).reshape(M, ncols)
+    assert _rel(d, ref) < (1e-5 if epi == 2 else 1e-2)
 
 
 def test_gemm_silu_mul():

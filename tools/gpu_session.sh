@@ -24,6 +24,14 @@ for s in $STEPS; do
     benchq) run bench_quick 600 python bench.py --steps 2 --warmup 1 --skip-cpu ;;
     kbench) run kbench 300 python tools/kbench.py ;;
     aprof) run attn_prof 300 python tools/attn_prof.py ;;
+    skinny)
+      run skinny 300 python tools/skinny_probe.py
+      run ncu_skinny 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/skinny_launches.csv python tools/skinny_probe.py ;;
+    appong)
+      for r in 1 2; do for p in 0 1; do
+        export ESP_ATTN_PINGPONG=$p; run attn_pp${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_PINGPONG
+      done; done ;;
     apoly)
       for r in 1 2; do for p in 2 3 4 5; do
         export ESP_ATTN_POLY=$p; run attn_poly${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_POLY
