@@ -277,6 +277,8 @@ def run_gpu(args):
         line["esp_degrees"] = bench_esp_sweep(abi, args, np, tf_sust)
     if rank == 0 and not args.skip_config3:
         line["config3_128k"] = bench_config3(abi, args, np, tf_sust)
+    if rank == 0 and not args.skip_scale_down:
+        line["scale_down"] = bench_scale_down(abi, args, np)
     rt.close()
     if rank == 0 and not args.skip_cpu:
         try:
@@ -351,6 +353,48 @@ def bench_config3(abi, args, np, tf_sust):
                       "scale-down 8->2 by proactive retention (reference plan)"}
 
 
+def bench_scale_down(abi, args, np):
+    """SURVEY §8(d) migration-hidden: proactive scale-down (retention fused in
+    the QKV epilogue) vs the reactive baseline (prefill keeping KV spread over
+    the ring, then K8 moving the dropped instances' tokens to the survivors).
+    S = args.seq, ring of 8 co-located instances, survivors {0, 1}.
+    hidden = 1 - (T_prefill(retain on survivors) - T_prefill(spread)) / T_move."""
+    S, d = args.seq, 8
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    rt = abi.Runtime(abi.LWM_7B, d, devices=[dev] * d, kv_capacity=S)
+    prompt = np.random.default_rng(11).integers(0, V, S).astype(np.int32)
+    share = S // d
+    spread = [[(i, share) for i in range(d)]]
+    onto2 = [[(0, S // 2), (1, S - S // 2)]]
+    t_spread, t_scale, t_move, rid = [], [], [], 0
+    for it in range(2):  # one warm-up round, one timed
+        for retain, acc in ((spread, t_spread), (onto2, t_scale)):
+            _, _, t = rt.prefill([rid], [S], list(range(d)), retain, tokens=prompt)
+            if it:
+                acc.append(t)
+            if retain is spread:
+                # reactive baseline: move instances 2..7's tokens to 0 / 1
+                t0 = time.perf_counter()
+                for src in range(2, d):
+                    rt.move_kv(rid, src, src % 2, share)
+                if it:
+                    t_move.append((time.perf_counter() - t0) * 1e3)
+                placement = rt.placement(rid)
+                assert sorted(placement.items()) == [(0, S // 2), (1, S - S // 2)], placement
+            rt.free_request(rid)
+            rid += 1
+    rt.close()
+    moved = (d - 2) * share
+    extra = t_scale[0] - t_spread[0]
+    return {"config": f"LWM-7B {S}-token prefill, ring of {d} co-located instances, "
+                      f"scale-down {d}->2",
+            "t_prefill_retain_on_survivors_ms": t_scale[0],
+            "t_prefill_spread_ms": t_spread[0],
+            "t_reactive_move_ms": t_move[0], "moved_tokens": moved,
+            "moved_bytes": moved * 2 * L * H * 2,
+            "migration_hidden": max(0.0, min(1.0, 1.0 - extra / t_move[0]))}
+
+
 def bench_esp_sweep(abi, args, np, tf_sust):
     """ESP degree d in {2,4,8} on ONE GPU: d co-located instances run the
     striped ring (d rounds per layer) with retention onto the reference's own
@@ -392,6 +436,7 @@ def main():
     ap.add_argument("--skip-esp-sweep", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-config3", action="store_true")
+    ap.add_argument("--skip-scale-down", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

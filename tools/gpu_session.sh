@@ -33,24 +33,24 @@ for s in $STEPS; do
         export ESP_ATTN_PINGPONG=$p; run attn_pp${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_PINGPONG
       done; done ;;
     apoly)
-      for r in 1 2; do for p in 2 3 4 5; do
+      for r in 1 2; do for p in 0 1 2 3 4; do
         export ESP_ATTN_POLY=$p; run attn_poly${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_POLY
       done; done ;;
     ncu)
       run ncu_launches 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --skip-decode \
-        --skip-esp-sweep --skip-cpu --skip-config3
+        --skip-esp-sweep --skip-cpu --skip-config3 --skip-scale-down
       run ncu_attn 900 ncu --set full --clock-control none --import-source on \
         -k regex:ring_attention -s 2 -c 1 -o gpurun_out/prof_attn -f python bench.py --steps 1 \
-        --warmup 0 --skip-decode --skip-esp-sweep --skip-cpu --skip-config3
+        --warmup 0 --skip-decode --skip-esp-sweep --skip-cpu --skip-config3 --skip-scale-down
       run ncu_gemm 900 ncu --set full --clock-control none --import-source on \
         -k regex:gemm_bf16 -s 10 -c 1 -o gpurun_out/prof_gemm -f python bench.py --steps 1 \
-        --warmup 0 --skip-decode --skip-esp-sweep --skip-cpu --skip-config3
+        --warmup 0 --skip-decode --skip-esp-sweep --skip-cpu --skip-config3 --skip-scale-down
       ;;
     ncu_decode)
       run ncu_decode 900 ncu --set full --clock-control none --import-source on \
         -k regex:decode_attention -s 40 -c 1 -o gpurun_out/prof_decode -f python bench.py \
-        --steps 1 --warmup 1 --skip-esp-sweep --skip-cpu --skip-config3 --seq 4096
+        --steps 1 --warmup 1 --skip-esp-sweep --skip-cpu --skip-config3 --skip-scale-down --seq 4096
       ;;
   esac
 done
