@@ -606,7 +606,8 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
     switch (poly) {
       case 2: ESP_LAUNCH2(128, 2); break;
       case 3: ESP_LAUNCH2(128, 3); break;
-      case 5: ESP_LAUNCH2(128, 5); break;
+      case 0: ESP_LAUNCH2(128, 0); break;
+      case 1: ESP_LAUNCH2(128, 1); break;
       default: ESP_LAUNCH2(128, 4); break;
     }
   } else if (head_dim == 64) {
