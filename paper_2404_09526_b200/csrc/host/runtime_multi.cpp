@@ -135,6 +135,14 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
   };
   std::map<int, Part> parts;
   for (int dom : dom_set) parts[dom];
+  // Transport: fused push (default) — the QKV epilogue of each domain stores
+  // its K/V rows into every domain's gather buffer and each token's K/V into
+  // its resting page slot wherever that is (peer stores), so the ring's
+  // all-gather and the retention ride inside the GEMM; or the copy-engine
+  // ring in the reference's round order (ESP_RING_COPY=1).
+  const bool push = std::getenv("ESP_RING_COPY") == nullptr &&
+                    instances_.size() <= static_cast<size_t>(k::kMaxSlabs) &&
+                    dom_set.size() <= static_cast<size_t>(k::kMaxPeers) + 1;
   for (int i = 0; i < d; ++i) {
     Part& p = parts[dom_of[i]];
     p.positions.push_back(i);
@@ -148,7 +156,10 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         p.tok.push_back(a.tokens[tok_base[r] + t]);
         p.pos.push_back(static_cast<int32_t>(t));
         p.kvrow.push_back(g);
-        if (rest.domain == dom_of[i]) {  // retained at the origin, in the QKV epilogue
+        if (push) {  // retained by the origin's QKV epilogue, local or peer store
+          p.rinst.push_back(static_cast<int32_t>(tok_inst[r][static_cast<size_t>(t)]));
+          p.rslot.push_back(slot);
+        } else if (rest.domain == dom_of[i]) {  // retained at the origin, in the QKV epilogue
           p.rinst.push_back(rest.slab);
           p.rslot.push_back(slot);
         } else {  // retained on pass by the resting domain
@@ -226,7 +237,9 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
 
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
   std::map<int, std::vector<cudaEvent_t>> readers;  // copies reading a domain's gather buffer
+  std::map<int, cudaEvent_t> attn_done;  // push: domain's attention of the previous layer
   for (int l = 0; l < cfg_.layers; ++l) {
+    std::map<int, cudaEvent_t> qkv_done;  // push: domain's QKV (and its pushes) of this layer
     std::map<int, std::vector<cudaEvent_t>> ready;  // domain -> block -> event (nullptr: absent)
     for (auto& [dom, p] : parts) ready[dom].assign(static_cast<size_t>(d), nullptr);
     // 1. per-domain norm + QKV (+RoPE, + retention at the origin).
@@ -236,10 +249,16 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       cudaStream_t s = dc.stream;
       for (cudaEvent_t e : readers[dom]) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
       readers[dom].clear();
+      if (push) {  // peers' gather buffers are free once their previous attention is done
+        for (auto& [od, e] : attn_done) {
+          if (od != dom) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
+        }
+      }
       if (p.rows == 0) {  // empty stripes (prompt shorter than the ring): nothing to send
         cudaEvent_t e = sync_event(dc);
         cuda_ok(cudaEventRecord(e, s), "event");
         for (int i : p.positions) ready[dom][i] = e;
+        qkv_done[dom] = e;
         continue;
       }
       const LayerW& w = dc.layers[l];
@@ -258,17 +277,32 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       ep.head_dim = cfg_.head_dim;
       ep.row_inst = static_cast<int32_t*>(dc.rinst.ptr);
       ep.row_slot = static_cast<int32_t*>(dc.rslot.ptr);
-      for (size_t j = 0; j < dc.slabs.size(); ++j) {
-        ep.slab_k[j] = instances_[dc.slabs[j]].layer_k(l);
-        ep.slab_v[j] = instances_[dc.slabs[j]].layer_v(l);
+      if (push) {
+        for (size_t j = 0; j < instances_.size(); ++j) {
+          ep.slab_k[j] = instances_[j].layer_k(l);
+          ep.slab_v[j] = instances_[j].layer_v(l);
+        }
+        for (auto& [od, op] : parts) {
+          if (od == dom) continue;
+          DeviceCtx& pc = *devices_[static_cast<size_t>(od)];
+          ep.k_peer[ep.n_peer] = static_cast<bf16*>(pc.kb.ptr);
+          ep.v_peer[ep.n_peer] = static_cast<bf16*>(pc.vb.ptr);
+          ++ep.n_peer;
+        }
+      } else {
+        for (size_t j = 0; j < dc.slabs.size(); ++j) {
+          ep.slab_k[j] = instances_[dc.slabs[j]].layer_k(l);
+          ep.slab_v[j] = instances_[dc.slabs[j]].layer_v(l);
+        }
       }
       timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, p.rows, 3 * H, H, ep, s); });
       cudaEvent_t e = sync_event(dc);
       cuda_ok(cudaEventRecord(e, s), "event");
       for (int i : p.positions) ready[dom][i] = e;
+      qkv_done[dom] = e;
     }
-    // 2. ring transport in the reference's round order.
-    for (int r = 0; r + 1 < d; ++r) {
+    // 2. ring transport in the reference's round order (copy mode only).
+    for (int r = 0; !push && r + 1 < d; ++r) {
       for (int i = 0; i < d; ++i) {
         const int o = RingSchedule::origin(i, r, d);
         const int src = dom_of[i], dst = dom_of[(i + 1) % d];
@@ -295,6 +329,11 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
       DeviceGuard g(dc.device);
       cudaStream_t s = dc.stream;
+      if (push) {  // every domain's K/V rows must have landed here
+        for (auto& [od, e] : qkv_done) {
+          if (od != dom) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
+        }
+      }
       k::DecodeSlabs slabs{};
       for (size_t j = 0; j < dc.slabs.size(); ++j) {
         slabs.k[j] = instances_[dc.slabs[j]].layer_k(l);
@@ -327,6 +366,11 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
                             n_work, scale, s);
         }
       });
+      if (push) {  // peers may overwrite this gather buffer with the next layer
+        cudaEvent_t e = sync_event(dc);
+        cuda_ok(cudaEventRecord(e, s), "event");
+        attn_done[dom] = e;
+      }
       k::GemmEpilogue eo;
       eo.kind = k::kEpiResidual;
       eo.out = x;

@@ -226,6 +226,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
         if (!valid) continue;
         if (dst_main) store_row_bf16(dst_main + row_off + col0 + c, r);
         if (dst_slab) store_row_bf16(dst_slab + col0 + c, r);
+        for (int pr = 0; pr < ep.n_peer; ++pr) store_row_bf16(ep.v_peer[pr] + row_off + col0 + c, r);
       }
     } else {
       uint32_t h[32];
@@ -254,6 +255,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
           if (dst_slab) {
             store_vals_bf16(dst_slab + c_lo, lo);
             store_vals_bf16(dst_slab + c_hi, hi);
+          }
+          if (region == 1) {
+            for (int pr = 0; pr < ep.n_peer; ++pr) {
+              store_vals_bf16(ep.k_peer[pr] + row_off + c_lo, lo);
+              store_vals_bf16(ep.k_peer[pr] + row_off + c_hi, hi);
+            }
           }
         }
       }

@@ -10,6 +10,7 @@ namespace esp::k {
 using bf16 = __nv_bfloat16;
 
 constexpr int kMaxSlabs = 16;  // instances co-located on one device
+constexpr int kMaxPeers = 7;   // other transport domains of one ESP ring
 
 enum EpiKind : int {
   kEpiStore = 0,     // D = acc (bf16)
@@ -36,6 +37,13 @@ struct GemmEpilogue {
   const int32_t* kv_rows = nullptr;   // [M] row of k_out/v_out for GEMM row m (null: m)
   bf16* slab_k[kMaxSlabs] = {};       // per co-located instance, this layer's base
   bf16* slab_v[kMaxSlabs] = {};
+  // Fused ring transport (ESP prefill across transport domains): every K/V
+  // row is also stored, at the same row, into each peer domain's gather
+  // buffer (peer / NVLink stores from the epilogue) — the all-gather of the
+  // ring's K/V blocks happens inside the QKV GEMM.
+  int n_peer = 0;
+  bf16* k_peer[kMaxPeers] = {};
+  bf16* v_peer[kMaxPeers] = {};
 };
 
 // D[M x N] = A[M x K] . B[N x K]^T with the epilogue above. A and B are

@@ -26,17 +26,25 @@ LOGIT_TOL = 5e-2
 TIE_GAP = 2e-2
 
 
-@pytest.fixture(autouse=True, params=["colocated", "domain_per_instance"])
+@pytest.fixture(autouse=True, params=["colocated", "domain_push", "domain_copy"])
 def transport(request, monkeypatch):
     """colocated: instances of one GPU share buffers (zero-copy ring).
-    domain_per_instance: every instance is its own co-location domain, so the
-    ring moves K/V blocks by peer copies in the reference's round order,
-    remote-origin tokens are retained on pass, and decode broadcasts queries /
-    gathers partials between domains — the cross-GPU data path, on one GPU."""
-    if request.param == "domain_per_instance":
+    domain_*: every instance is its own co-location domain (ESP_DOMAIN_PER_
+    INSTANCE), the cross-GPU data path on one GPU. domain_push (default
+    transport): each domain's QKV epilogue stores its K/V rows into every
+    domain's gather buffer and each token's K/V into its resting slot (peer
+    stores), ordered by events. domain_copy (ESP_RING_COPY): the ring moves K/V
+    blocks by peer copies in the reference's round order and remote-origin
+    tokens are retained on pass. Decode broadcasts queries / gathers partials
+    between domains in both."""
+    if request.param.startswith("domain"):
         monkeypatch.setenv("ESP_DOMAIN_PER_INSTANCE", "1")
     else:
         monkeypatch.delenv("ESP_DOMAIN_PER_INSTANCE", raising=False)
+    if request.param == "domain_copy":
+        monkeypatch.setenv("ESP_RING_COPY", "1")
+    else:
+        monkeypatch.delenv("ESP_RING_COPY", raising=False)
     return request.param
 
 
@@ -166,7 +174,7 @@ def test_config3_128k_scale_down_lwm7b(transport):
     dense CPU oracle cannot run 128K x 32 layers, so numerics are checked by
     ESP-degree invariance: a d=1 prefill of the same prompt gives the same
     logits (within tolerance) and greedy token."""
-    if transport == "domain_per_instance":
+    if transport.startswith("domain"):
         pytest.skip("8 transport domains x 7B activations exceed one GPU's HBM")
     path = os.path.join(GOLD, "scenario_config3_128k.jsonl")
     head, steps, _ = replay.load(path)
