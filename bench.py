@@ -279,6 +279,7 @@ def run_gpu(args):
         line["config3_128k"] = bench_config3(abi, args, np, tf_sust)
     if rank == 0 and not args.skip_scale_down:
         line["scale_down"] = bench_scale_down(abi, args, np)
+        line["transport"] = bench_transport(abi, args, np)
     rt.close()
     if rank == 0 and not args.skip_cpu:
         try:
@@ -393,6 +394,48 @@ def bench_scale_down(abi, args, np):
             "t_reactive_move_ms": t_move[0], "moved_tokens": moved,
             "moved_bytes": moved * 2 * L * H * 2,
             "migration_hidden": max(0.0, min(1.0, 1.0 - extra / t_move[0]))}
+
+
+def bench_transport(abi, args, np):
+    """Cross-domain ESP transport on one GPU (ESP_DOMAIN_PER_INSTANCE=1: every
+    instance its own domain, the multi-GPU code path): a d-instance ring
+    prefill with the fused push (K/V all-gather + retention as peer stores in
+    the QKV epilogue) vs the copy-engine ring (ESP_RING_COPY). Both move the
+    same (d-1)/d of every K/V block per domain; on one GPU the 'peer' is HBM,
+    so this measures transport overhead, not NVLink bandwidth."""
+    S, d = min(args.seq, 16384), 4
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    prompt = np.random.default_rng(13).integers(0, V, S).astype(np.int32)
+    share = S // d
+    retain = [[(i, share) for i in range(d)]]
+    out = {"config": f"LWM-7B {S}-token prefill, ring of {d} instances, one transport domain "
+                     f"each (one GPU)",
+           "ring_bytes_per_layer": (d - 1) * S * H * 2 * 2}
+    saved = {k: os.environ.get(k) for k in ("ESP_DOMAIN_PER_INSTANCE", "ESP_RING_COPY")}
+    try:
+        os.environ["ESP_DOMAIN_PER_INSTANCE"] = "1"
+        for mode in ("push", "copy"):
+            if mode == "copy":
+                os.environ["ESP_RING_COPY"] = "1"
+            else:
+                os.environ.pop("ESP_RING_COPY", None)
+            rt = abi.Runtime(abi.LWM_7B, d, devices=[dev] * d, kv_capacity=share + 64)
+            ms = []
+            for k in range(2):
+                _, _, t = rt.prefill([k], [S], list(range(d)), retain, tokens=prompt)
+                rt.free_request(k)
+                if k:
+                    ms.append(t)
+            rt.close()
+            out[f"{mode}_ms"] = ms[0]
+            out[f"{mode}_tokens_per_s"] = S / (ms[0] / 1e3)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return out
 
 
 def bench_esp_sweep(abi, args, np, tf_sust):
