@@ -377,11 +377,9 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
       sg.kv_len[r] = kv_len[r];
       sg.shift[r] = origin[r] > pos_i ? 1 : 0;
     }
-    // Same variant selection as the runtime: v2 (query-tile pairs) unless
-    // ESP_ATTN_V1 is set.
-    const bool pairs = std::getenv("ESP_ATTN_V1") == nullptr;
-    const int span = pairs ? 2 : 1;
-    (void)span;
+    // Same variant selection as the runtime (ESP_ATTN / ESP_ATTN_V1).
+    const int variant = esp::k::attention_variant();
+    const bool pairs = esp::k::attention_pairs(variant);
     std::vector<int32_t> work;  // the runtime's work order (LPT, head groups)
     esp::build_attention_work({sg}, heads, pairs, rows, head_dim, work);
     esp::k::RingSegment* dseg = nullptr;
@@ -421,9 +419,9 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
         }
         std::fprintf(stderr, "\n");
       }
-    } else if (pairs) {
-      esp::k::ring_attention_pairs(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork, n_work,
-                                   scale, s);
+    } else {
+      esp::k::ring_attention_variant(variant, Q, K, V, O, nr, nr, heads, head_dim, dseg, 1, dwork,
+                                     n_work, scale, s);
       if (const char* rep = std::getenv("ESP_ATTN_REPEAT")) {
         // Kernel study: time n more launches on the staged buffers (stderr).
         const int n = std::max(1, std::atoi(rep));
@@ -432,20 +430,18 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
         cudaEventCreate(&e1);
         cudaEventRecord(e0, s);
         for (int i = 0; i < n; ++i) {
-          esp::k::ring_attention_pairs(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork, n_work,
-                                       scale, s);
+          esp::k::ring_attention_variant(variant, Q, K, V, O, nr, nr, heads, head_dim, dseg, 1,
+                                         dwork, n_work, scale, s);
         }
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, e0, e1);
-        std::fprintf(stderr, "[attn-time] %.4f ms/launch over %d launches\n", ms / n, n);
+        std::fprintf(stderr, "[attn-time] variant %d: %.4f ms/launch over %d launches\n",
+                     variant, ms / n, n);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
       }
-    } else {
-      esp::k::ring_attention(Q, K, V, O, nr, nr, heads, head_dim, dseg, 1, dwork,
-                             static_cast<int>(work.size() / 2), scale, s);
     }
     cudaMemcpyAsync(out, O, static_cast<size_t>(q_len) * hidden * 2, cudaMemcpyDeviceToDevice, s);
     const cudaError_t e = cudaStreamSynchronize(s);

@@ -57,6 +57,8 @@ void Runtime::phase_times(double* ms, int64_t* launches, int n) {
 Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
                  int64_t kv_capacity)
     : cfg_(cfg) {
+  attn_variant_ = k::attention_variant();
+  attn_pairs_ = k::attention_pairs(attn_variant_);
   if (n_instances <= 0) throw ConfigError("need at least one instance");
   if (cfg.layers <= 0 || cfg.hidden <= 0 || cfg.heads <= 0 || cfg.head_dim <= 0 ||
       cfg.ffn <= 0 || cfg.vocab <= 0) {
@@ -607,16 +609,10 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
     timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     // Striped ring attention over all d rounds.
     timed(kPhAttention, s, [&] {
-      if (attn_pairs_) {
-        k::ring_attention_pairs(q, kb, vb, attn, rows, rows, cfg_.heads, cfg_.head_dim,
-                                static_cast<const k::RingSegment*>(dc.segs.ptr),
+      k::ring_attention_variant(attn_variant_, q, kb, vb, attn, rows, rows, cfg_.heads,
+                                cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr),
+                                static_cast<int>(segs.size()),
                                 static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
-      } else {
-        k::ring_attention(q, kb, vb, attn, rows, rows, cfg_.heads, cfg_.head_dim,
-                          static_cast<const k::RingSegment*>(dc.segs.ptr),
-                          static_cast<int>(segs.size()),
-                          static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
-      }
     });
     k::GemmEpilogue eo;
     eo.kind = k::kEpiResidual;

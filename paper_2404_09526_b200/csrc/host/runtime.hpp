@@ -148,7 +148,8 @@ class Runtime {
   std::vector<ProfileRec> profiles_;
   bool profiling_ = false;
   // K1 variant: v2 (two query tiles per CTA, P in TMEM) unless ESP_ATTN_V1=1.
-  bool attn_pairs_ = std::getenv("ESP_ATTN_V1") == nullptr;
+  int attn_variant_ = 2;     // K1 variant (ESP_ATTN), set in the constructor
+  bool attn_pairs_ = true;   // its work items are query-tile pairs
   struct PhaseEvent {
     int phase;
     cudaEvent_t a, b;

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -61,11 +62,16 @@ void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bo
     }
   }
   // Persistent CTAs take items round-robin: heads in groups whose K/V fit
-  // comfortably in L2 (~64 MiB) so concurrent items share K/V tiles, longest
-  // work first within a group.
+  // comfortably in L2 (32 MiB: one die's half of the 126 MB L2 also holds Q,
+  // O and the other group in flight; 32 beat 64 and 16 by ~2 % at 32K) so
+  // concurrent items share K/V tiles, longest work first within a group.
   const int64_t head_kv_bytes = kv_rows * head_dim * 2 * 2;
+  static const int64_t budget_mib = [] {
+    const char* e = std::getenv("ESP_ATTN_L2_MIB");
+    return e ? std::max(1, std::atoi(e)) : 32;
+  }();
   const int head_group = static_cast<int>(
-      std::max<int64_t>(1, (static_cast<int64_t>(64) << 20) / std::max<int64_t>(head_kv_bytes, 1)));
+      std::max<int64_t>(1, (budget_mib << 20) / std::max<int64_t>(head_kv_bytes, 1)));
   std::stable_sort(order.begin(), order.end(), [&](const auto& x, const auto& y) {
     const int gx = (work[2 * x.second + 1] & 0xFF) / head_group;
     const int gy = (work[2 * y.second + 1] & 0xFF) / head_group;
@@ -353,18 +359,11 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       timed(kPhAttention, s, [&] {
         const bf16* qd = static_cast<bf16*>(dc.q.ptr);
         // Q rows are this domain's local rows, K/V rows are global.
-        if (attn_pairs_) {
-          k::ring_attention_pairs(qd, static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr),
-                                  attn, p.rows, rows, cfg_.heads, cfg_.head_dim,
-                                  static_cast<k::RingSegment*>(dc.segs.ptr),
+        k::ring_attention_variant(attn_variant_, qd, static_cast<bf16*>(dc.kb.ptr),
+                                  static_cast<bf16*>(dc.vb.ptr), attn, p.rows, rows, cfg_.heads,
+                                  cfg_.head_dim, static_cast<k::RingSegment*>(dc.segs.ptr),
+                                  static_cast<int>(p.segs.size()),
                                   static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
-        } else {
-          k::ring_attention(qd, static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr),
-                            attn, p.rows, rows, cfg_.heads, cfg_.head_dim,
-                            static_cast<k::RingSegment*>(dc.segs.ptr),
-                            static_cast<int>(p.segs.size()), static_cast<int32_t*>(dc.work.ptr),
-                            n_work, scale, s);
-        }
       });
       if (push) {  // peers may overwrite this gather buffer with the next layer
         cudaEvent_t e = sync_event(dc);

@@ -1,6 +1,8 @@
 // Host-side launchers of the sm_100a kernels of the ESP data path.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -84,6 +86,29 @@ void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out
 // (producer: q_empty,k_empty,v_empty waits; MMA: q_full,k_full,v_full,
 // p_full[0],p_full[1],o_free waits; softmax t: s_full wait, step, S readback,
 // rescale o_done wait, rescales, steps, final wait; slot 7 = role total).
+// v4: one 128-row query tile per CTA, Q and a double-buffered S in TMEM
+// (ring_attention_v4.cu). Work items (segment, q tile, head), as for v1.
+void ring_attention_single(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
+                           int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
+                           const int32_t* d_work, int n_work, float scale, cudaStream_t s);
+
+// K1 variant selection: 2 = query-tile pairs (default), 1 = v1, 4 = one
+// tile with Q and a double-buffered S in TMEM. ESP_ATTN=1|2|4 (ESP_ATTN_V1
+// is kept as an alias of ESP_ATTN=1).
+inline int attention_variant() {
+  if (const char* e = std::getenv("ESP_ATTN")) {
+    const int v = std::atoi(e);
+    if (v == 1 || v == 2 || v == 4) return v;
+  }
+  return std::getenv("ESP_ATTN_V1") != nullptr ? 1 : 2;
+}
+// Work items of the variant are query-tile pairs (v2) or single tiles.
+inline bool attention_pairs(int variant) { return variant == 2; }
+void ring_attention_variant(int variant, const bf16* q, const bf16* k, const bf16* v, bf16* out,
+                            int q_rows, int kv_rows, int heads, int head_dim,
+                            const RingSegment* d_segs, int n_segs, const int32_t* d_work,
+                            int n_work, float scale, cudaStream_t s);
+
 void ring_attention_pairs_profiled(const bf16* q, const bf16* k, const bf16* v, bf16* out,
                                    int q_rows, int kv_rows, int heads, int head_dim,
                                    const RingSegment* d_segs, const int32_t* d_work, int n_work,

@@ -160,13 +160,12 @@ def _ref_striped(q, ks, vs, pos_i, d, origins, heads, hd):
     return torch.einsum("hqk,khd->qhd", p, V).reshape(L, heads * hd)
 
 
-@pytest.fixture(params=["v2", "v1"])
+@pytest.fixture(params=["v2", "v1", "v4"])
 def attn_variant(request, monkeypatch):
-    """K1 variants: v2 (two query tiles / CTA, P in TMEM; default) and v1."""
-    if request.param == "v1":
-        monkeypatch.setenv("ESP_ATTN_V1", "1")
-    else:
-        monkeypatch.delenv("ESP_ATTN_V1", raising=False)
+    """K1 variants (ESP_ATTN): v2 (two query tiles / CTA, P in TMEM), v1, v4
+    (one tile / CTA, Q and a double-buffered S in TMEM)."""
+    monkeypatch.delenv("ESP_ATTN_V1", raising=False)
+    monkeypatch.setenv("ESP_ATTN", request.param[1:])
     return request.param
 
 

@@ -28,6 +28,14 @@ for s in $STEPS; do
       run skinny 300 python tools/skinny_probe.py
       run ncu_skinny 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/skinny_launches.csv python tools/skinny_probe.py ;;
+    al2)
+      for r in 1 2; do for m in 64 32 16; do
+        export ESP_ATTN_L2_MIB=$m; run bench_l2_${m}_$r 600 python bench.py --steps 2 --warmup 1 --skip-cpu --skip-decode --skip-esp-sweep --skip-config3 --skip-scale-down; unset ESP_ATTN_L2_MIB
+      done; done ;;
+    avar)
+      for r in 1 2; do for v in 2 4; do
+        export ESP_ATTN=$v; run attn_v${v}_$r 300 python tools/attn_prof.py; unset ESP_ATTN
+      done; done ;;
     appong)
       for r in 1 2; do for p in 0 1; do
         export ESP_ATTN_PINGPONG=$p; run attn_pp${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_PINGPONG
