@@ -241,3 +241,53 @@ def test_esp_degree_invariance(d):
     out, lg2, _ = rt.decode_step(members, [master], [5], want_logits=True)
     rt.check_conservation()
     check_against_oracle(shape, prompt, [int(first[0]), int(out[0])], [lg[0], lg2[0]])
+
+
+def test_config5_mixed_trace_tiny():
+    """BASELINE config 5: the reference ESP scheduler's decisions on the mixed
+    trace (gen_trace("mixed", seed 7), 24 requests of 5..311,945 tokens, 8
+    instances x 317,000 slots, 24 ring prefills with scale-down, 2,027
+    multi-master decode steps) executed with real kernels on the tiny model
+    (the LWM-7B KV of this trace, 8 x 317,000 x 512 KiB, needs 8 GPUs). Page
+    tables equal the engine's placements at every schedule() call; the short
+    requests' first tokens and logits match the dense oracle."""
+    path = os.path.join(GOLD, "scenario_config5_mixed.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    lens = {r["id"]: r["input_len"] for r in head["requests"]}
+    checked = {r for r, n in lens.items() if 20 <= n <= 1024}
+    keep_steps = 3
+    logits = {r: [] for r in checked}
+    tokens = {r: [] for r in checked}
+    stats = {"prefill_tok": 0, "prefill_ms": 0.0, "decode_tok": 0, "decode_ms": 0.0}
+
+    def on_prefill(p, retain):
+        toks = np.concatenate([replay.prompt_tokens(r, n) for r, n in zip(p["requests"], p["input_lens"])])
+        want = any(r in checked for r in p["requests"])
+        first, lg, ms = rt.prefill(p["requests"], p["input_lens"], p["instances"], retain,
+                                   tokens=toks, want_logits=want)
+        stats["prefill_tok"] += int(sum(p["input_lens"]))
+        stats["prefill_ms"] += ms
+        for i, r in enumerate(p["requests"]):
+            if r in checked:
+                logits[r].append(lg[i])
+                tokens[r].append(int(first[i]))
+
+    def on_decode(d, members):
+        want = any(r in checked and len(logits[r]) <= keep_steps for r in d["batch"])
+        out, lg, ms = rt.decode_step(members, d["masters"], d["batch"], want_logits=want)
+        stats["decode_tok"] += len(d["batch"])
+        stats["decode_ms"] += ms
+        for i, r in enumerate(d["batch"]):
+            if r in checked and len(logits[r]) <= keep_steps:
+                logits[r].append(lg[i])
+                tokens[r].append(int(out[i]))
+
+    replay.replay(rt, path, on_prefill=on_prefill, on_decode=on_decode)
+    rt.check_conservation()
+    for r in sorted(checked):
+        check_against_oracle(abi.TINY, replay.prompt_tokens(r, lens[r]), tokens[r], logits[r])
+    print(f"config5 tiny: prefill {stats['prefill_tok']} tok in {stats['prefill_ms']:.1f} ms, "
+          f"decode {stats['decode_tok']} tok in {stats['decode_ms']:.1f} ms")
+    assert stats["decode_tok"] >= 2027
