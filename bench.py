@@ -302,15 +302,19 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
         rt.prefill([r], [ctx], [0], [[(0, ctx)]], tokens=rng.integers(0, V, ctx).astype(np.int32))
     for _ in range(args.warmup):
         rt.decode_step([0], [0], list(range(b)))
-    rt.phase_times()
-    rt.set_profiling(True)
+    # Timed steps run without per-phase events (they would add a gap between
+    # every launch); one more pass of the same length gives the phase split.
     ms = []
     for _ in range(args.steps):
         ms.append(rt.decode_step([0], [0], list(range(b)))[2])
+    rt.phase_times()
+    rt.set_profiling(True)
+    for _ in range(args.steps):
+        rt.decode_step([0], [0], list(range(b)))
     rt.set_profiling(False)
     ph = rt.phase_times()
     step = sum(ms) / len(ms)
-    ctx_now = ctx + args.warmup + args.steps // 2 + 1
+    ctx_now = ctx + args.warmup + args.steps + 1
     kv_bytes = 2.0 * L * H * 2 * b * ctx_now
     w_bytes = 2.0 * (L * (4 * H * H + 3 * H * F) + 2 * V * H)
     att_ms, att_n = ph["decode_attention"]

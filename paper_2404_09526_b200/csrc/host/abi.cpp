@@ -471,21 +471,26 @@ int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_sl
     for (const auto& [row, c] : by_row) {
       slabs.k[c] = static_cast<const esp::k::bf16*>(k_slab[c]);
       slabs.v[c] = static_cast<const esp::k::bf16*>(v_slab[c]);
-      ch.push_back({slot_idx[c], n_slots[c], row, c, static_cast<int32_t>(ch.size())});
-      row_start[row + 1]++;
+      // split into the runtime's chunk size, as esp_decode_step does
+      for (int32_t c0 = 0; c0 < n_slots[c]; c0 += esp::decode_chunk()) {
+        ch.push_back({slot_idx[c] + c0, std::min<int32_t>(esp::decode_chunk(), n_slots[c] - c0), row,
+                      c, static_cast<int32_t>(ch.size())});
+        row_start[row + 1]++;
+      }
     }
+    const int32_t n_parts = static_cast<int32_t>(ch.size());
     for (int r = 0; r < batch; ++r) row_start[r + 1] += row_start[r];
     esp::k::DecodeChunk* dch = nullptr;
     int32_t* drs = nullptr;
     float *po = nullptr, *pml = nullptr;
     cudaMalloc(&dch, ch.size() * sizeof(esp::k::DecodeChunk) + 16);
     cudaMalloc(&drs, row_start.size() * 4);
-    cudaMalloc(&po, static_cast<size_t>(n_chunks) * heads * head_dim * 4 + 16);
-    cudaMalloc(&pml, static_cast<size_t>(n_chunks) * heads * 2 * 4 + 16);
+    cudaMalloc(&po, static_cast<size_t>(n_parts) * heads * head_dim * 4 + 16);
+    cudaMalloc(&pml, static_cast<size_t>(n_parts) * heads * 2 * 4 + 16);
     cudaMemcpyAsync(dch, ch.data(), ch.size() * sizeof(esp::k::DecodeChunk), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(drs, row_start.data(), row_start.size() * 4, cudaMemcpyHostToDevice, s);
     const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
-    esp::k::decode_attention(static_cast<const esp::k::bf16*>(q), dch, n_chunks, slabs, heads,
+    esp::k::decode_attention(static_cast<const esp::k::bf16*>(q), dch, n_parts, slabs, heads,
                              head_dim, scale, po, pml, s);
     esp::k::decode_combine(po, pml, drs, batch, heads, head_dim, static_cast<esp::k::bf16*>(out), s);
     const cudaError_t e = cudaStreamSynchronize(s);

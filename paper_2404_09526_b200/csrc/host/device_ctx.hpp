@@ -15,6 +15,8 @@
 #include <vector>
 
 #include "../kernels/kernels.h"
+#include <cstdlib>
+
 #include "errors.hpp"
 #include "runtime.hpp"
 
@@ -22,7 +24,17 @@ namespace esp {
 
 using k::bf16;
 
-constexpr int kDecodeChunk = 256;
+// Split-KV chunk: slots of one request on one instance per decode CTA.
+// ESP_DECODE_CHUNK overrides (tuning; 32..1024).
+constexpr int kDecodeChunkDefault = 512;
+inline int decode_chunk() {
+  static const int c = [] {
+    const char* e = std::getenv("ESP_DECODE_CHUNK");
+    const int v = e ? std::atoi(e) : kDecodeChunkDefault;
+    return v < 32 ? 32 : (v > 1024 ? 1024 : v);
+  }();
+  return c;
+}
 
 struct LayerW {
   bf16 *wqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;

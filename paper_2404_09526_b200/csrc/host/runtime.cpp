@@ -710,10 +710,10 @@ void Runtime::decode_step(const esp_decode_args& a) {
       if (pl.slots.empty()) continue;
       sync_pages(pl, s);
       const int64_t nsl = static_cast<int64_t>(pl.slots.size());
-      for (int64_t c0 = 0; c0 < nsl; c0 += kDecodeChunk) {
+      for (int64_t c0 = 0; c0 < nsl; c0 += decode_chunk()) {
         k::DecodeChunk ch{};
         ch.slots = pl.dev + c0;
-        ch.n = static_cast<int32_t>(std::min<int64_t>(kDecodeChunk, nsl - c0));
+        ch.n = static_cast<int32_t>(std::min<int64_t>(decode_chunk(), nsl - c0));
         ch.row = i;
         ch.slab = inst(iid).slab;
         ch.out = static_cast<int32_t>(chunks.size());

@@ -492,9 +492,9 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
       DeviceGuard gd(xc.device);
       sync_pages(pl, xc.stream);
       const int64_t nsl = static_cast<int64_t>(pl.slots.size());
-      for (int64_t c0 = 0; c0 < nsl; c0 += kDecodeChunk) {
+      for (int64_t c0 = 0; c0 < nsl; c0 += decode_chunk()) {
         all.push_back({mdom[g], inst(iid).domain, g, iid, pl.dev + c0,
-                       static_cast<int32_t>(std::min<int64_t>(kDecodeChunk, nsl - c0))});
+                       static_cast<int32_t>(std::min<int64_t>(decode_chunk(), nsl - c0))});
       }
     }
   }

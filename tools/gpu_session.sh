@@ -55,6 +55,13 @@ for s in $STEPS; do
         -k regex:gemm_bf16 -s 10 -c 1 -o gpurun_out/prof_gemm -f python bench.py --steps 1 \
         --warmup 0 --skip-decode --skip-esp-sweep --skip-cpu --skip-config3 --skip-scale-down
       ;;
+    dprobe)
+      for r in 1 2; do
+        eval "set -- ${DPROBE_VARIANTS:-\"ESP_DECODE_ATTN=1\" \"ESP_DECODE_STAGES=2\"}"; for v in "$@"; do
+          echo "== $v" >> gpurun_out/dprobe.log
+          env $v timeout 300 python tools/decode_probe.py >> gpurun_out/dprobe.log 2>&1
+        done
+      done ;;
     ncu_decode)
       run ncu_decode 900 ncu --set full --clock-control none --import-source on \
         -k regex:decode_attention -s 40 -c 1 -o gpurun_out/prof_decode -f python bench.py \
