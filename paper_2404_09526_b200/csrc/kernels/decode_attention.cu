@@ -17,6 +17,7 @@
 #include <stdexcept>
 
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace esp::k {
 
@@ -54,6 +55,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   // blockIdx.x = head (fastest): the CTAs resident at a time cover every head
   // of a few chunks, so each token's whole K/V row (all heads, contiguous) is
   // read at about the same time (DRAM page locality).
+  ptx::griddep_wait();  // q and the appended K/V come from the QKV GEMM
+  ptx::griddep_launch();
   const int head = blockIdx.x, ci = blockIdx.y;
   const DecodeChunk ch = chunks[ci];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -335,6 +338,8 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
                                       const int32_t* __restrict__ chunk_ids,
                                       const int32_t* __restrict__ rows, int heads, int hd,
                                       bf16* __restrict__ out) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
   const int orow = blockIdx.x, head = blockIdx.y;
   const int row = rows ? rows[orow] : orow;
   const int c0 = row_start[row], c1 = row_start[row + 1];
@@ -407,7 +412,7 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
     // ESP_DECODE_V1=<unroll><min blocks per SM> tuning variants of v1
     const char* tv = std::getenv("ESP_DECODE_V1");
     const int tune = tv ? std::atoi(tv) : 0;
-#define ESP_V1(U, B) decode_attention_kernel<128, U, B><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads, sl2, part_o, part_ml)
+#define ESP_V1(U, B) launch_pdl(4, decode_attention_kernel<128, U, B>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml)
     switch (tune) {
       case 41: ESP_V1(4, 1); break;
       case 410: ESP_V1(4, 10); break;
@@ -436,8 +441,9 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s) {
   if (rows <= 0) return;
-  decode_combine_kernel<<<dim3(rows, heads), head_dim, 0, s>>>(
-      part_o, part_ml, row_start, nullptr, nullptr, heads, head_dim, out);
+  launch_pdl(8, decode_combine_kernel, dim3(rows, heads), dim3(head_dim), 0, s, part_o, part_ml,
+             row_start, static_cast<const int32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+             heads, head_dim, out);
   count_launch();
 }
 
@@ -445,7 +451,7 @@ void decode_combine_rows(const float* part_o, const float* part_ml, const int32_
                          const int32_t* chunk_ids, const int32_t* rows, int n, int heads,
                          int head_dim, bf16* out, cudaStream_t s) {
   if (n <= 0) return;
-  decode_combine_kernel<<<dim3(n, heads), head_dim, 0, s>>>(part_o, part_ml, row_start,
+  launch_pdl(8, decode_combine_kernel, dim3(n, heads), dim3(head_dim), 0, s, part_o, part_ml, row_start,
                                                             chunk_ids, rows, heads, head_dim, out);
   count_launch();
 }

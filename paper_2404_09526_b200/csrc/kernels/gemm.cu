@@ -21,6 +21,7 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                       int kb_per_cta, const __grid_constant__ GemmEpilogue ep,
-                      float* __restrict__ ws, int* __restrict__ tile_kb) {
+                      float* __restrict__ ws, int* __restrict__ tile_kb, int b_mode) {
   using C = Cfg<BN, kSkinny>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -353,7 +354,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t keep = ptx::policy_evict_last();
+      // b_mode bit 0: B is pre-tiled ([N/BN][K/BK][BN][BK], each K block of
+      // a tile 16 KB contiguous); bits 1-2: L2 hint for B (0 evict_last,
+      // 1 evict_first, 2 none).
+      const int hint = (b_mode >> 1) & 3;
+      const uint64_t keep = hint == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
       while (work.get(tile, kb0, kb1)) {
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
@@ -361,8 +366,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], C::kTxBytes);
           ptx::tma_load_2d(sA + stage * C::kAStride, &tmA, &full[stage], kb * BK, mb * BM);
-          ptx::tma_load_2d_hint(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, nb * BN,
-                                keep);
+          const int bx = (b_mode & 1) ? 0 : kb * BK;
+          const int by = (b_mode & 1) ? (nb * num_k + kb) * BN : nb * BN;
+          if (hint == 2) {
+            ptx::tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], bx, by);
+          } else {
+            ptx::tma_load_2d_hint(sB + stage * C::kBBytes, &tmB, &full[stage], bx, by, keep);
+          }
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -477,6 +487,291 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
   }
+}
+
+// Decode-shaped GEMM with the operands swapped (D^T = W . X^T): the weight
+// tile is the UMMA's M = 128 operand and the <= 32 activation rows are its
+// N = NT operand, so the tensor core does 128 x NT x 64 per K block instead
+// of 128 x 128 x 64 with 7/8 of the rows wasted (which made the M = 128
+// skinny kernel tensor-bound at ~50 GB/s of weights per SM). Weight tiles
+// (16 KB) stream through kStages stages with an evict-first L2 hint; the
+// NT x 64 activation tile rides along (L2-resident). The accumulator is
+// 128 TMEM lanes (output columns) x NT columns (tokens); the epilogue warps
+// transpose it through shared memory into NT fp32 rows and then run the same
+// fused epilogues as the other GEMMs (thread = output row) — or, under
+// stream-K, store the rows as partial sums for the tile's last CTA.
+namespace swp {
+constexpr int kStages = 10;
+template <int NT>
+struct Cfg {
+  static constexpr int kWBytes = 128 * BK * 2;     // 16 KB
+  static constexpr int kXBytes = NT * BK * 2;      // 2 or 4 KB
+  static constexpr int kTx = kWBytes + kXBytes;
+  static constexpr int kTBytes = NT * 128 * 4;     // transposed accumulator
+  static constexpr int kSmem = kStages * (kWBytes + kXBytes) + kTBytes + 1024 + 256;
+  static constexpr int kTmemCols = NT * 2 < 32 ? 32 : NT * 2;
+};
+}  // namespace swp
+
+struct RowAcc {  // one fp32 row in shared memory
+  const float* row;
+  __device__ __forceinline__ void load(int c, uint32_t (&r)[32]) const {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(row[c + i]);
+  }
+  __device__ __forceinline__ void wait() const {}
+};
+
+// Fused epilogue of one 128-column tile from its row-major fp32 image in
+// shared memory. Store / residual / fp32 kinds: four threads per row, 32
+// columns each (independent global reads in flight); the kinds that pair
+// columns 64 apart (SiLU gate/up, RoPE halves) run one thread per row.
+__device__ __forceinline__ void swap_epilogue(const GemmEpilogue& ep, const float* sT, int M,
+                                              int t, int tile, int N) {
+  if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32) {
+    const int m = t >> 2, j = t & 3;
+    if (m < M) epilogue_tile<32>(ep, RowAcc{sT + m * 128 + j * 32}, m, true, tile * 4 + j, N);
+  } else if (t < M) {
+    epilogue_tile<128>(ep, RowAcc{sT + t * 128}, t, true, tile, N);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_skinny_swap(const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ CUtensorMap tmW, int M, int N, int K,
+                     int kb_per_cta, const __grid_constant__ GemmEpilogue ep,
+                     float* __restrict__ ws, int* __restrict__ tile_kb,
+                     unsigned long long* __restrict__ trace) {
+  using C = swp::Cfg<NT>;
+  auto gtime = [] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  };
+  unsigned long long* tr = trace ? trace + blockIdx.x * 8 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtime();
+  constexpr int S = swp::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = sW + S * C::kWBytes;
+  float* sT = reinterpret_cast<float*>(sX + S * C::kXBytes);  // [NT][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sT) + C::kTBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile uint32_t* last_flag = tmem_slot + 1;
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmX);
+    ptx::tma_prefetch_desc(&tmW);
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
+
+  const int num_n = N / 128, num_k = K / BK;
+  WorkRange work(num_n, num_k, kb_per_cta);
+  int tile, kb0, kb1;
+
+  ptx::griddep_launch();
+  if (warp == 0) {
+    if (lane == 0) {
+      // PDL: the first S weight tiles do not depend on the previous kernel
+      // and are requested before griddepcontrol.wait (they stream while the
+      // previous kernel drains); their activation tiles follow the wait.
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t stream_once = ptx::policy_evict_first();
+      int pre_kb[S];
+      int n_pre = 0;
+      bool waited = false;
+      auto release = [&] {
+        ptx::griddep_wait();
+        for (int i = 0; i < n_pre; ++i) {
+          ptx::tma_load_2d(sX + i * C::kXBytes, &tmX, &full[i], pre_kb[i] * BK, 0);
+        }
+        waited = true;
+      };
+      while (work.get(tile, kb0, kb1)) {
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_expect_tx(&full[stage], C::kTx);
+          ptx::tma_load_2d_hint(sW + stage * C::kWBytes, &tmW, &full[stage], kb * BK, tile * 128,
+                                stream_once);
+          if (waited) {
+            ptx::tma_load_2d(sX + stage * C::kXBytes, &tmX, &full[stage], kb * BK, 0);
+          } else {
+            pre_kb[n_pre++] = kb;
+            if (n_pre == S) release();
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (!waited) release();
+    }
+  } else if (warp == 1) {
+    const bool leader = ptx::elect_one();
+    constexpr uint32_t idesc = ptx::make_idesc_bf16(128, NT, false, false);
+    int stage = 0;
+    uint32_t phase = 0;
+    int lt = 0;
+    for (; work.get(tile, kb0, kb1); ++lt) {
+      const int acc = lt & 1;
+      const uint32_t use = static_cast<uint32_t>(lt >> 1);
+      ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * NT;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        if (tr && lt == 0 && kb == kb0 && lane == 0) tr[2] = gtime();
+        const uint32_t w0 = ptx::smem_u32(sW + stage * C::kWBytes);
+        const uint32_t x0 = ptx::smem_u32(sX + stage * C::kXBytes);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t dw = ptx::make_sdesc_sw128(w0 + k * 32, 16, 1024);
+          const uint64_t dx = ptx::make_sdesc_sw128(x0 + k * 32, 16, 1024);
+          if (leader) ptx::umma_f16_ss(d_tmem, dw, dx, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+        }
+        if (leader) ptx::tc_commit(&empty[stage]);
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (leader) ptx::tc_commit(&tfull[acc]);
+      __syncwarp();
+    }
+    if (tr && lane == 0) tr[3] = gtime();
+  } else if (warp >= 4) {
+    ptx::griddep_wait();  // residual / outputs are the previous kernels' data
+    const uint32_t quad = warp & 3;
+    const int t = static_cast<int>(quad * 32 + lane);  // output column of the tile
+    int lt = 0;
+    for (; work.get(tile, kb0, kb1); ++lt) {
+      const int acc = lt & 1;
+      const uint32_t use = static_cast<uint32_t>(lt >> 1);
+      ptx::mbar_wait(&tfull[acc], use & 1);
+      ptx::tc_fence_after();
+      if (tr && t == 0 && lt == 0) tr[6] = gtime();
+      const uint32_t tacc = tmem_base + acc * NT + ((quad * 32) << 16);
+      // sT is reused tile after tile: the previous tile's readers are done
+      // (barrier at the end of the previous iteration).
+      if constexpr (NT == 16) {
+        uint32_t r[16];
+        ptx::tmem_ld_32x32b_x16(tacc, r);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sT[j * 128 + t] = __uint_as_float(r[j]);
+      } else {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tacc, r);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sT[j * 128 + t] = __uint_as_float(r[j]);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      ptx::named_bar_sync(1, 128);
+      if (!work.stream) {
+        swap_epilogue(ep, sT, M, t, tile, N);
+        ptx::named_bar_sync(1, 128);
+        continue;
+      }
+      const int m = t;
+      const float* my = sT + m * 128;
+      const int max_seg = (num_k + kb_per_cta - 1) / kb_per_cta + 1;
+      const int first_cta = tile * num_k / kb_per_cta;
+      const int last_cta = ((tile + 1) * num_k - 1) / kb_per_cta;
+      const int64_t slot_floats = static_cast<int64_t>(M) * 128;
+      float* tile_ws = ws + static_cast<int64_t>(tile) * max_seg * slot_floats;
+      if (m < M) {
+        float4* d = reinterpret_cast<float4*>(
+            tile_ws + (static_cast<int>(blockIdx.x) - first_cta) * slot_floats +
+            static_cast<int64_t>(m) * 128);
+        const float4* src = reinterpret_cast<const float4*>(my);
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) __stcg(d + i, src[i]);
+      }
+      __threadfence();
+      ptx::named_bar_sync(1, 128);
+      if (t == 0) {
+        const int done = atomicAdd(&tile_kb[tile], kb1 - kb0) + (kb1 - kb0);
+        *last_flag = done == num_k ? 1u : 0u;
+      }
+      ptx::named_bar_sync(1, 128);
+      if (*last_flag) {
+        __threadfence();
+        // Sum the tile's segment partials cooperatively into sT (all loads
+        // of up to 8 segments in flight at once), then the fused epilogue.
+        const int nseg = last_cta - first_cta + 1;
+        const int n4 = M * 32;  // float4s per slot
+        for (int i0 = t; i0 < n4; i0 += 4 * 128) {
+          float4 a[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int sg0 = 0; sg0 < nseg; sg0 += 8) {
+#pragma unroll
+            for (int sg = 0; sg < 8; ++sg) {
+              if (sg0 + sg < nseg) {
+                const float4* src =
+                    reinterpret_cast<const float4*>(tile_ws + (sg0 + sg) * slot_floats);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const int idx = i0 + i * 128;
+                  if (idx < n4) {
+                    const float4 w = __ldcg(src + idx);
+                    a[i].x += w.x;
+                    a[i].y += w.y;
+                    a[i].z += w.z;
+                    a[i].w += w.w;
+                  }
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int idx = i0 + i * 128;
+            if (idx < n4) reinterpret_cast<float4*>(sT)[idx] = a[i];
+          }
+        }
+        ptx::named_bar_sync(1, 128);
+        swap_epilogue(ep, sT, M, t, tile, N);
+        if (t == 0) tile_kb[tile] = 0;
+      }
+      ptx::named_bar_sync(1, 128);
+    }
+    if (tr && t == 0) tr[4] = gtime();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+  if (tr && threadIdx.x == 0) tr[5] = gtime();
 }
 
 // CTA-pair variant for the large prefill GEMMs: a cluster of two CTAs on one
@@ -672,6 +967,12 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
+// Study knob (tools/skinny_probe.py): ESP_GEMM_B_MODE, see the producer.
+static int gemm_b_mode() {
+  const char* e = getenv("ESP_GEMM_B_MODE");
+  return e ? atoi(e) : 0;
+}
+
 template <int BN, bool kSkinny>
 static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
                         int kb_per_cta, const GemmEpilogue& ep, cudaStream_t s,
@@ -683,13 +984,59 @@ static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, i
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const CUtensorMap ta = make_tmap_bf16(A, M, K, lda, C::kARows);
-  const CUtensorMap tb = make_tmap_bf16(B, N, K, ldb, BN);
+  const int b_mode = gemm_b_mode();
+  const CUtensorMap tb = (b_mode & 1) ? make_tmap_bf16(B, static_cast<int64_t>(N) * (K / BK), BK, BK, BN)
+                                      : make_tmap_bf16(B, N, K, ldb, BN);
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
                                   : std::min(tiles, num_sms());
   gemm_bf16_tcgen05<BN, kSkinny><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, kb_per_cta,
-                                                                  ep, ws, tile_kb);
+                                                                  ep, ws, tile_kb, b_mode);
   count_launch();
+}
+
+template <int NT>
+static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
+                               int kb_per_cta, const GemmEpilogue& ep, cudaStream_t s,
+                               float* ws, int* tile_kb) {
+  using C = swp::Cfg<NT>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_skinny_swap<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmem);
+  });
+  const CUtensorMap tx = make_tmap_bf16(A, M, K, lda, NT);
+  const CUtensorMap tw = make_tmap_bf16(B, N, K, ldb, 128);
+  const int tiles = N / 128;
+  const int grid = kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
+                                  : std::min(tiles, num_sms());
+  // Study: ESP_GEMM_TRACE=<file> appends per-CTA globaltimer stamps (entry,
+  // setup done, first stage landed, last MMA, first tile drained, epilogue
+  // done, exit) of every skinny launch to <file> (synchronises the stream).
+  static const char* trace_path = getenv("ESP_GEMM_TRACE");
+  unsigned long long* trace = nullptr;
+  if (trace_path) {
+    cudaMalloc(&trace, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace, 0, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long), s);
+  }
+  launch_pdl(1, gemm_skinny_swap<NT>, dim3(grid), dim3(kThreads), C::kSmem, s, tx, tw, M, N, K,
+             kb_per_cta, ep, ws, tile_kb, trace);
+  count_launch();
+  if (trace) {
+    std::vector<unsigned long long> h(static_cast<size_t>(grid) * 8);
+    cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(trace);
+    if (FILE* f = fopen(trace_path, "a")) {
+      fprintf(f, "launch N=%d K=%d M=%d per=%d grid=%d\n", N, K, M, kb_per_cta, grid);
+      for (int b = 0; b < grid; ++b) {
+        fprintf(f, "%d", b);
+        for (int i = 0; i < 7; ++i) fprintf(f, " %llu", h[static_cast<size_t>(b) * 8 + i]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
 }
 
 // Co-resident CTA pairs of the current device (normally num_sms / 2).
@@ -782,22 +1129,28 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     // 148 SMs); the CTA completing a tile applies the fused epilogue to its
     // fp32 partial sums.
     const int tiles = N / 128, total = tiles * (K / BK);
-    // Stream-K pays only when the tiles leave most SMs idle AND each tile is
-    // long enough to amortise the fixup tail (~10 us: partial store, counter,
-    // in-order sum): the down projection (32 tiles x 172 K blocks: 40 -> 29
-    // us). O (32 x 64) and the wide projections stream faster as whole tiles
-    // (tools/skinny_probe.py).
-    const bool streamk = 2 * tiles < num_sms() && K / BK >= 128;
+    // Stream-K pays when whole tiles would leave most SMs idle (one SM
+    // streams ~82 GB/s of weights, an even share of HBM is ~44 GB/s): O and
+    // down (32 tiles) go from 15.3 / 37.5 us to 13.8 / 21.5 us; QKV (96
+    // tiles) and the wider projections are faster as whole tiles because the
+    // fixup handshake (~5 us) costs more than the imbalance
+    // (tools/skinny_probe.py, swap-AB kernel with PDL).
+    const bool old = getenv("ESP_GEMM_SKINNY_OLD") != nullptr;
+    const bool streamk = 2 * tiles < num_sms();
     if (getenv("ESP_GEMM_NO_STREAMK") != nullptr ||
         (getenv("ESP_GEMM_STREAMK_ALL") == nullptr && !streamk)) {
-      launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 0, ep, s);
+      if (old) launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 0, ep, s);
+      else if (M <= 16) launch_skinny_swap<16>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      else launch_skinny_swap<32>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       return;
     }
     const int per = (total + num_sms() - 1) / num_sms();
     const int max_seg = (K / BK + per - 1) / per + 1;
     const StreamKWs w =
         streamk_workspace(static_cast<size_t>(tiles) * max_seg * M * 128, tiles, s);
-    launch_gemm<128, true>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
+    if (old) launch_gemm<128, true>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
+    else if (M <= 16) launch_skinny_swap<16>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
+    else launch_skinny_swap<32>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
     return;
   }
   if (launch_gemm_pair(A, lda, B, ldb, M, N, K, ep, s)) return;

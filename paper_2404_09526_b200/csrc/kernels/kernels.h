@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <utility>
 
 namespace esp::k {
 
@@ -172,5 +173,28 @@ void copy_slots(const bf16* src_k, const bf16* src_v, const int32_t* src_slots, 
 
 int64_t launch_count();
 void count_launch();
+
+// Launch with programmatic stream serialization (PDL) unless ESP_PDL=0: the
+// kernel may start while the previous kernel of the stream drains; every
+// kernel launched this way executes griddepcontrol.wait before it reads or
+// writes anything a predecessor touches (only weights are read earlier).
+// cls: 1 skinny GEMM, 2 norm/embed/argmax, 4 decode attention, 8 combine
+// (ESP_PDL=<mask>, default 11 = all but decode attention; ESP_PDL=0 off).
+bool pdl_enabled(int cls);
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled(cls) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace esp::k

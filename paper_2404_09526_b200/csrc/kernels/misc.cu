@@ -6,6 +6,7 @@
 #include <cfloat>
 
 #include "kernels.h"
+#include "ptx.cuh"
 #include "synthetic.h"
 
 namespace esp::k {
@@ -15,11 +16,22 @@ std::atomic<int64_t> g_launches{0};
 }
 int64_t launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
+bool pdl_enabled(int cls) {
+  static const int mask = [] {
+    const char* e = std::getenv("ESP_PDL");
+    // Default: GEMMs, norms and the combine (decode attention with PDL was
+    // measured 0.7 ms/step slower on 16 x 8K: its early-resident CTAs).
+    return e == nullptr ? 11 : std::atoi(e);
+  }();
+  return (mask & cls) != 0;
+}
 
 namespace {
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __restrict__ table,
                              bf16* __restrict__ x, int hidden) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
   const int r = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<int64_t>(tokens[r]) * hidden);
   uint4* dst = reinterpret_cast<uint4*>(x + static_cast<int64_t>(r) * hidden);
@@ -29,6 +41,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __r
 __global__ void rmsnorm_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ src_rows,
                                const bf16* __restrict__ gamma, bf16* __restrict__ y, int hidden,
                                float eps) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
   const int r = blockIdx.x;
   const int sr = src_rows ? src_rows[r] : r;
   const bf16* xr = x + static_cast<int64_t>(sr) * hidden;
@@ -72,6 +86,8 @@ __global__ void rmsnorm_kernel(const bf16* __restrict__ x, const int32_t* __rest
 }
 
 __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int32_t* __restrict__ out) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
   const int r = blockIdx.x;
   const float* lr = logits + static_cast<int64_t>(r) * vocab;
   float best = -FLT_MAX;
@@ -199,7 +215,7 @@ __global__ void copy_slots_kernel(const bf16* __restrict__ sk, const bf16* __res
 void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,
            cudaStream_t s) {
   if (rows <= 0) return;
-  embed_kernel<<<rows, 128, 0, s>>>(tokens, table, x, hidden);
+  launch_pdl(2, embed_kernel, dim3(rows), dim3(128), 0, s, tokens, table, x, hidden);
   count_launch();
 }
 
@@ -207,13 +223,13 @@ void rmsnorm(const bf16* x, const int32_t* src_rows, const bf16* gamma, bf16* y,
              int hidden, float eps, cudaStream_t s) {
   if (rows <= 0) return;
   const int threads = hidden >= 2048 ? 256 : 64;
-  rmsnorm_kernel<<<rows, threads, 0, s>>>(x, src_rows, gamma, y, hidden, eps);
+  launch_pdl(2, rmsnorm_kernel, dim3(rows), dim3(threads), 0, s, x, src_rows, gamma, y, hidden, eps);
   count_launch();
 }
 
 void argmax_rows(const float* logits, int rows, int vocab, int32_t* out, cudaStream_t s) {
   if (rows <= 0) return;
-  argmax_kernel<<<rows, 1024, 0, s>>>(logits, vocab, out);
+  launch_pdl(2, argmax_kernel, dim3(rows), dim3(1024), 0, s, logits, vocab, out);
   count_launch();
 }
 
