@@ -343,19 +343,53 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
   const int orow = blockIdx.x, head = blockIdx.y;
   const int row = rows ? rows[orow] : orow;
   const int c0 = row_start[row], c1 = row_start[row + 1];
-  float mm = -INFINITY;
-  for (int c = c0; c < c1; ++c) {
-    const int64_t ci = chunk_ids ? chunk_ids[c] : c;
-    mm = fmaxf(mm, part_ml[(ci * heads + head) * 2]);
+  // Chunk weights in shared memory, computed in parallel (one thread per
+  // chunk): w_c = e^{m_c - M}, L = sum_c w_c l_c. Then every thread sums its
+  // dims over the chunks with independent loads.
+  constexpr int kMaxC = 256;
+  __shared__ float sw[kMaxC];
+  __shared__ int64_t sp[kMaxC];
+  __shared__ float red[2][32];
+  const int nc = c1 - c0;
+  float mloc = -INFINITY;
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    const int64_t p = static_cast<int64_t>(chunk_ids ? chunk_ids[c0 + c] : c0 + c) * heads + head;
+    if (c < kMaxC) sp[c] = p;
+    mloc = fmaxf(mloc, part_ml[p * 2]);
   }
+  for (int w = 16; w >= 1; w >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffff, mloc, w));
+  if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = mloc;
+  __syncthreads();
+  float mm = -INFINITY;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) mm = fmaxf(mm, red[0][i]);
+  float lloc = 0.f;
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    const int64_t p = c < kMaxC ? sp[c]
+                                : static_cast<int64_t>(chunk_ids ? chunk_ids[c0 + c] : c0 + c) * heads + head;
+    const float mc = part_ml[p * 2];
+    const float wc = mc == -INFINITY ? 0.f : exp2f(mc - mm);
+    if (c < kMaxC) sw[c] = wc;
+    lloc += wc * part_ml[p * 2 + 1];
+  }
+  for (int w = 16; w >= 1; w >>= 1) lloc += __shfl_xor_sync(0xffffffff, lloc, w);
+  if ((threadIdx.x & 31) == 0) red[1][threadIdx.x >> 5] = lloc;
+  __syncthreads();
+  float ll = 0.f;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) ll += red[1][i];
   for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    float acc = 0.f, ll = 0.f;
-    for (int c = c0; c < c1; ++c) {
-      const int64_t p = static_cast<int64_t>(chunk_ids ? chunk_ids[c] : c) * heads + head;
+    float acc = 0.f;
+    int c = 0;
+    for (; c + 4 <= nc && c + 4 <= kMaxC; c += 4) {
+      const float o0 = part_o[sp[c] * hd + d], o1 = part_o[sp[c + 1] * hd + d];
+      const float o2 = part_o[sp[c + 2] * hd + d], o3 = part_o[sp[c + 3] * hd + d];
+      acc += sw[c] * o0 + sw[c + 1] * o1 + sw[c + 2] * o2 + sw[c + 3] * o3;
+    }
+    for (; c < nc; ++c) {
+      const int64_t p = c < kMaxC ? sp[c]
+                                  : static_cast<int64_t>(chunk_ids ? chunk_ids[c0 + c] : c0 + c) * heads + head;
       const float mc = part_ml[p * 2];
-      const float w = mc == -INFINITY ? 0.f : exp2f(mc - mm);
-      acc += w * part_o[p * hd + d];
-      ll += w * part_ml[p * 2 + 1];
+      const float wc = c < kMaxC ? sw[c] : (mc == -INFINITY ? 0.f : exp2f(mc - mm));
+      acc += wc * part_o[p * hd + d];
     }
     out[static_cast<int64_t>(orow) * heads * hd + head * hd + d] =
         __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);

@@ -1136,7 +1136,11 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     // fixup handshake (~5 us) costs more than the imbalance
     // (tools/skinny_probe.py, swap-AB kernel with PDL).
     const bool old = getenv("ESP_GEMM_SKINNY_OLD") != nullptr;
-    const bool streamk = 2 * tiles < num_sms();
+    static const int sk_min_kb = [] {
+      const char* e = getenv("ESP_GEMM_SK_MIN_KB");
+      return e ? atoi(e) : 0;
+    }();
+    const bool streamk = 2 * tiles < num_sms() && K / BK >= sk_min_kb;
     if (getenv("ESP_GEMM_NO_STREAMK") != nullptr ||
         (getenv("ESP_GEMM_STREAMK_ALL") == nullptr && !streamk)) {
       if (old) launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 0, ep, s);

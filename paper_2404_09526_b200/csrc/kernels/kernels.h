@@ -179,7 +179,7 @@ void count_launch();
 // kernel launched this way executes griddepcontrol.wait before it reads or
 // writes anything a predecessor touches (only weights are read earlier).
 // cls: 1 skinny GEMM, 2 norm/embed/argmax, 4 decode attention, 8 combine
-// (ESP_PDL=<mask>, default 11 = all but decode attention; ESP_PDL=0 off).
+// (ESP_PDL=<mask>, default 3 = GEMMs + norms; ESP_PDL=0 off).
 bool pdl_enabled(int cls);
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

@@ -19,9 +19,9 @@ void count_launch() { g_launches.fetch_add(1); }
 bool pdl_enabled(int cls) {
   static const int mask = [] {
     const char* e = std::getenv("ESP_PDL");
-    // Default: GEMMs, norms and the combine (decode attention with PDL was
+    // Default: GEMMs and norms (decode attention with PDL was
     // measured 0.7 ms/step slower on 16 x 8K: its early-resident CTAs).
-    return e == nullptr ? 11 : std::atoi(e);
+    return e == nullptr ? 3 : std::atoi(e);
   }();
   return (mask & cls) != 0;
 }
