@@ -275,6 +275,8 @@ def run_gpu(args):
         line["decode"] = bench_decode(rt, abi, args, np, hbm)
     if rank == 0 and not args.skip_esp_sweep:
         line["esp_degrees"] = bench_esp_sweep(abi, args, np, tf_sust)
+    if rank == 0 and not args.skip_decode and not args.skip_esp_sweep:
+        line["decode_esp_degrees"] = bench_decode_degrees(abi, args, np, hbm)
     if rank == 0 and not args.skip_config3:
         line["config3_128k"] = bench_config3(abi, args, np, tf_sust)
     if rank == 0 and not args.skip_scale_down:
@@ -329,6 +331,40 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
                          "algorithmic": f"K+V bytes of one layer = 2*H*2*sum(ctx) = {kv_bytes / L:.4e} B per launch"},
             "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
             "phase_ms": {p: round(v[0] / max(len(ms), 1), 4) for p, v in ph.items() if v[1] > 0}}
+
+
+def bench_decode_degrees(abi, args, np, hbm):
+    """Multi-master distributed decoding at ESP degree d = 2/4/8 on co-located
+    instances: each request's KV (ctx tokens) is spread evenly over the d
+    group members, k = min(2, d) masters (requests dealt by assign_masters),
+    split-KV partials on every member, LSE combine at the master; same batch
+    and total KV bytes as the d = 1 decode line."""
+    b, ctx = args.decode_batch, args.decode_ctx
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    steps = max(3, args.steps)
+    out = {}
+    for d in (2, 4, 8):
+        share = ctx // d
+        rt = abi.Runtime(abi.LWM_7B, d, devices=[dev] * d,
+                         kv_capacity=b * share + b * (steps + args.warmup + 8))
+        rng = np.random.default_rng(17)
+        members = list(range(d))
+        masters = members[:min(2, d)]
+        for r in range(b):
+            rt.prefill([r], [share * d], members, [[(i, share) for i in members]],
+                       tokens=rng.integers(0, V, share * d).astype(np.int32))
+        for _ in range(args.warmup):
+            rt.decode_step(members, masters, list(range(b)))
+        ms = [rt.decode_step(members, masters, list(range(b)))[2] for _ in range(steps)]
+        rt.close()
+        step = sum(ms) / len(ms)
+        kv_bytes = 2.0 * L * H * 2 * b * (share * d + args.warmup + steps // 2 + 1)
+        w_bytes = 2.0 * (L * (4 * H * H + 3 * H * F) + 2 * V * H)
+        out[str(d)] = {"tokens_per_s": b / (step / 1e3), "ms_per_step": step,
+                       "masters": len(masters),
+                       "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
+                       "instances": f"{d} co-located on 1 GPU, KV {share} tokens/request/instance"}
+    return out
 
 
 def bench_config3(abi, args, np, tf_sust):
