@@ -51,7 +51,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define ESP_ABI_VERSION 1
+#define ESP_ABI_VERSION 2
 
 /* ---- error codes (reference types.hpp:48-109) --------------------------- */
 enum esp_status {
@@ -227,6 +227,23 @@ typedef struct esp_decode_args {
   int32_t* out_tokens;             /* [b] greedy tokens, nullable            */
   float* logits_out;               /* [b x vocab], nullable                  */
   double* device_ms_out;
+  /* Chunked prefill riding on this step (DecodeStepPlan.chunk_request /
+   * chunk_tokens / chunk_placement, state.hpp:98-107; the chunked policy,
+   * policies.cpp:297-405; committed at engine.cpp:432-462). chunk_tokens == 0:
+   * none (a zero-initialised struct has no chunk). The chunk's tokens take slots on chunk_instance[i] (chunk_tokens_on[i]
+   * tokens each, ascending instance = KvPlacement order); its queries attend
+   * to every earlier token of the request and causally within the chunk.
+   * chunk_final = 1 when the chunk completes the prompt (engine.cpp:570-579):
+   * the request's first generated token is written to *chunk_first_token_out. */
+  int64_t chunk_request;
+  int64_t chunk_tokens;
+  int32_t chunk_n;
+  const int32_t* chunk_instance;
+  const int64_t* chunk_tokens_on;
+  const int32_t* chunk_token_ids;  /* [chunk_tokens] prompt ids, NULL on a placement-only runtime */
+  int32_t chunk_final;
+  int32_t* chunk_first_token_out;  /* nullable */
+  float* chunk_logits_out;         /* [vocab] when chunk_final, nullable */
 } esp_decode_args;
 int esp_decode_step(esp_runtime* rt, const esp_decode_args* args);
 

@@ -112,10 +112,19 @@ json decision_json(const ScheduleDecision& d, const SimState& s) {
   json ds = json::array();
   for (const DecodeStepPlan& p : d.decode_steps) {
     const GroupState& gs = s.groups.at(p.group);
-    ds.push_back({{"group", p.group}, {"members", gs.group.instances},
-                  {"add_instances", p.add_instances}, {"masters", p.masters},
-                  {"batch", gs.batch}, {"chunk_request", p.chunk_request},
-                  {"chunk_tokens", p.chunk_tokens}});
+    json step{{"group", p.group}, {"members", gs.group.instances},
+              {"add_instances", p.add_instances}, {"masters", p.masters},
+              {"batch", gs.batch}, {"chunk_request", p.chunk_request},
+              {"chunk_tokens", p.chunk_tokens}};
+    if (p.chunk_request >= 0) {
+      // chunked prefill (policies.cpp:297-405): where the chunk's KV goes and
+      // how much of the prompt precedes it (engine.cpp:432-462)
+      const Request& q = s.requests[p.chunk_request];
+      step["chunk_placement"] = placement_json(p.chunk_placement);
+      step["chunk_prefilled"] = q.prefilled;
+      step["chunk_input_len"] = q.input_len;
+    }
+    ds.push_back(step);
   }
   j["decode_steps"] = ds;
   return j;
@@ -614,6 +623,15 @@ int main(int argc, char** argv) {
                    outdir);
     }
   }
+  // the baseline policies on the same data path — chunked
+  // prefill (chunks ride on decode steps) and prefill/decode disaggregation
+  // (engine-internal "handoff" KV moves, engine.cpp:194-244).
+  run_scenario({"tiny_chunked", 2, 20000, tiny, "chunked:512", true,
+                {{0, 1500, 6}, {0, 700, 5}, {30, 2100, 4}, {60, 300, 7}, {90, 900, 3}}},
+               ref, outdir);
+  run_scenario({"tiny_disagg", 2, 20000, tiny, "disagg:1+1", true,
+                {{0, 1500, 6}, {0, 700, 5}, {30, 2100, 4}, {60, 300, 7}, {90, 900, 3}}},
+               ref, outdir);
   TraceSpec spec;
   spec.distribution = "mixed";
   spec.requests_per_s = 0.5;

@@ -141,6 +141,15 @@ class DecodeArgs(C.Structure):
         ("out_tokens", C.POINTER(C.c_int32)),
         ("logits_out", C.POINTER(C.c_float)),
         ("device_ms_out", C.POINTER(C.c_double)),
+        ("chunk_request", C.c_int64),
+        ("chunk_tokens", C.c_int64),
+        ("chunk_n", C.c_int32),
+        ("chunk_instance", C.POINTER(C.c_int32)),
+        ("chunk_tokens_on", C.POINTER(C.c_int64)),
+        ("chunk_token_ids", C.POINTER(C.c_int32)),
+        ("chunk_final", C.c_int32),
+        ("chunk_first_token_out", C.POINTER(C.c_int32)),
+        ("chunk_logits_out", C.POINTER(C.c_float)),
     ]
 
 
@@ -490,7 +499,12 @@ class Runtime:
         check(lib().esp_prefill(self._h, C.byref(args)))
         return first, logits, ms.value
 
-    def decode_step(self, members, masters, batch, in_tokens=None, want_logits=False):
+    def decode_step(self, members, masters, batch, in_tokens=None, want_logits=False,
+                    chunk=None):
+        """chunk: optional dict(request, placement=[(instance, tokens)...],
+        tokens=<prompt ids of the chunk>, final=bool) — a chunked-prefill chunk
+        riding on this step. Returns (out_tokens, logits, ms) and, with a
+        chunk, sets chunk['first_token'] / chunk['logits'] when final."""
         b = len(batch)
         mem = _arr(np.int32, members)
         mas = _arr(np.int32, masters)
@@ -513,7 +527,29 @@ class Runtime:
             logits = np.zeros((b, self.shape.vocab), np.float32)
             args.logits_out = _ptr(logits, C.c_float)
         args.device_ms_out = C.pointer(ms)
+        args.chunk_request = -1
+        if chunk is not None:
+            ci = _arr(np.int32, [p[0] for p in chunk["placement"]])
+            ct = _arr(np.int64, [p[1] for p in chunk["placement"]])
+            args.chunk_request = chunk["request"]
+            args.chunk_tokens = int(sum(p[1] for p in chunk["placement"]))
+            args.chunk_n = len(chunk["placement"])
+            args.chunk_instance = _ptr(ci, C.c_int32)
+            args.chunk_tokens_on = _ptr(ct, C.c_int64)
+            if chunk.get("tokens") is not None:
+                cids = _arr(np.int32, chunk["tokens"])
+                args.chunk_token_ids = _ptr(cids, C.c_int32)
+            args.chunk_final = 1 if chunk.get("final") else 0
+            cfirst = np.full(1, -1, np.int32)
+            args.chunk_first_token_out = _ptr(cfirst, C.c_int32)
+            clog = None
+            if chunk.get("final") and want_logits:
+                clog = np.zeros(self.shape.vocab, np.float32)
+                args.chunk_logits_out = _ptr(clog, C.c_float)
         check(lib().esp_decode_step(self._h, C.byref(args)))
+        if chunk is not None:
+            chunk["first_token"] = int(cfirst[0])
+            chunk["logits"] = clog
         return out, logits, ms.value
 
     def move_kv(self, request, src, dst, tokens):

@@ -636,23 +636,61 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
 // ---- decode ----------------------------------------------------------------------
 void Runtime::decode_step(const esp_decode_args& a) {
   const int b = a.batch_size;
-  if (b <= 0) throw InternalError("decode step with neither batch nor chunk");
-  if (a.n_masters <= 0 || !a.masters) throw InternalError("decode step without masters");
+  const bool has_chunk = a.chunk_tokens > 0;
+  if (b <= 0 && !has_chunk) throw InternalError("decode step with neither batch nor chunk");
+  if (b > 0 && (a.n_masters <= 0 || !a.masters)) throw InternalError("decode step without masters");
   std::vector<InstanceId> members(a.members, a.members + a.n_members);
-  std::vector<InstanceId> masters(a.masters, a.masters + a.n_masters);
+  std::vector<InstanceId> masters;
+  if (a.masters) masters.assign(a.masters, a.masters + a.n_masters);
   for (InstanceId m : masters) inst(m);
   for (InstanceId m : members) inst(m);
   std::vector<RequestId> batch(a.batch, a.batch + b);
   for (RequestId r : batch) {
     if (req(r).kv_tokens() == 0) throw InternalError("decode of a request without KV");
   }
+  // Chunked prefill riding on the step (engine.cpp:432-462): validate before
+  // any slot is taken.
+  std::vector<std::pair<InstanceId, int64_t>> chunk_place;
+  if (has_chunk) {
+    if (a.chunk_n <= 0 || !a.chunk_instance || !a.chunk_tokens_on) {
+      throw InternalError("chunk without a placement");
+    }
+    int64_t tot = 0;
+    for (int i = 0; i < a.chunk_n; ++i) {
+      inst(a.chunk_instance[i]);
+      if (a.chunk_tokens_on[i] < 0) throw InternalError("negative chunk placement entry");
+      chunk_place.emplace_back(a.chunk_instance[i], a.chunk_tokens_on[i]);
+      tot += a.chunk_tokens_on[i];
+    }
+    if (tot != a.chunk_tokens) throw InternalError("chunk size inconsistent with its placement");
+    for (RequestId r : batch) {
+      if (r == a.chunk_request) throw InternalError("chunk names a request of the decode batch");
+    }
+    if (!devices_.empty() && !a.chunk_token_ids) {
+      throw ConfigError("decode_step: chunk token ids required on a device runtime");
+    }
+  }
   // Masters exactly as the engine assigns them (engine.cpp:401,
   // esp_mechanics.cpp:220-238), then the append feasibility of
   // decode_step_comm (esp_mechanics.cpp:240-264).
-  auto assign = assign_masters(batch, masters);
-  std::map<InstanceId, Tokens> free;
-  for (const auto& in : instances_) free[in.id] = in.capacity - in.used;
-  decode_step_comm(static_cast<int>(members.size()), assign, free);
+  std::map<InstanceId, std::vector<RequestId>> assign;
+  if (b > 0) {
+    assign = assign_masters(batch, masters);
+    std::map<InstanceId, Tokens> free;
+    for (const auto& in : instances_) free[in.id] = in.capacity - in.used;
+    decode_step_comm(static_cast<int>(members.size()), assign, free);
+  }
+  if (has_chunk) {
+    // The appends are committed first, then the chunk (engine.cpp:408-462).
+    std::map<InstanceId, int64_t> need;
+    for (const auto& [m, reqs] : assign) need[m] += static_cast<int64_t>(reqs.size());
+    for (const auto& [i, t] : chunk_place) need[i] += t;
+    for (const auto& [i, t] : need) {
+      if (inst(i).used + t > inst(i).capacity) {
+        throw CapacityError(i, "chunk placement overflows instance " + std::to_string(i));
+      }
+    }
+  }
 
   std::map<RequestId, int32_t> in_tok;
   for (int i = 0; i < b; ++i) {
@@ -679,13 +717,49 @@ void Runtime::decode_step(const esp_decode_args& a) {
       for (const auto& kv : rr.pages) involved.push_back(kv.first);
     }
   }
+  // Chunk: earlier tokens of the request (any order: all precede the chunk),
+  // then the chunk's own slots in token order (ascending instance).
+  const int c = has_chunk ? static_cast<int>(a.chunk_tokens) : 0;
+  std::vector<int32_t> prev_slab, prev_slot, ch_slab, ch_slot, ch_inst;
+  int64_t p_prev = 0;
+  if (has_chunk) {
+    RequestRec& rr = requests_[a.chunk_request];
+    rr.id = a.chunk_request;
+    p_prev = rr.kv_tokens();
+    for (const auto& [i, pl] : rr.pages) {
+      for (int32_t sl : pl.slots) {
+        prev_slab.push_back(inst(i).slab);
+        prev_slot.push_back(sl);
+      }
+      involved.push_back(i);
+    }
+    for (const auto& [i, t] : chunk_place) {
+      if (t == 0) continue;
+      std::vector<int32_t> sl = take_slots(inst(i), t);
+      PageList& pl = rr.pages[i];
+      pl.slots.insert(pl.slots.end(), sl.begin(), sl.end());
+      for (int32_t x : sl) {
+        ch_slab.push_back(inst(i).slab);
+        ch_slot.push_back(x);
+        ch_inst.push_back(i);
+      }
+      involved.push_back(i);
+    }
+    if (a.chunk_token_ids) rr.tokens.insert(rr.tokens.end(), a.chunk_token_ids, a.chunk_token_ids + c);
+    rr.input_len = p_prev + c;
+  }
   if (devices_.empty()) {
     for (const Row& rw : rows_v) {
       if (a.in_tokens) req(rw.r).tokens.push_back(rw.token);
     }
+    if (a.chunk_first_token_out) *a.chunk_first_token_out = -1;
     return;
   }
   if (single_domain(involved) == nullptr) {
+    if (has_chunk) {
+      throw ConfigError("chunked prefill across transport domains is not supported; "
+                        "co-locate the chunked group's instances");
+    }
     decode_multi(a, rows_v, batch);
     return;
   }
@@ -693,6 +767,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
   DeviceGuard g(dc.device);
   cudaStream_t s = dc.stream;
   const int H = cfg_.hidden, F = cfg_.ffn;
+  const int rows = b + c;
 
   std::vector<int32_t> h_tok, h_pos, h_inst, h_slot, h_row_start;
   std::vector<k::DecodeChunk> chunks;
@@ -722,38 +797,80 @@ void Runtime::decode_step(const esp_decode_args& a) {
     }
   }
   h_row_start.push_back(static_cast<int32_t>(chunks.size()));
+  for (int i = 0; i < c; ++i) {
+    h_tok.push_back(a.chunk_token_ids[i]);
+    h_pos.push_back(static_cast<int32_t>(p_prev + i));
+    h_inst.push_back(ch_slab[i]);
+    h_slot.push_back(ch_slot[i]);
+  }
   const int n_chunks = static_cast<int>(chunks.size());
-  int64_t max_pos = 0;
+  int64_t max_pos = p_prev + c;
   for (const Row& rw : rows_v) max_pos = std::max<int64_t>(max_pos, rw.pos + 1);
   ensure_rope(dc, max_pos);
-  int32_t* d_tok = scratch<int32_t>(dc.tok, b);
-  int32_t* d_pos = scratch<int32_t>(dc.pos, b);
-  int32_t* d_inst = scratch<int32_t>(dc.rinst, b);
-  int32_t* d_slot = scratch<int32_t>(dc.rslot, b);
+  int32_t* d_tok = scratch<int32_t>(dc.tok, rows);
+  int32_t* d_pos = scratch<int32_t>(dc.pos, rows);
+  int32_t* d_inst = scratch<int32_t>(dc.rinst, rows);
+  int32_t* d_slot = scratch<int32_t>(dc.rslot, rows);
   int32_t* d_rs = scratch<int32_t>(dc.row_start, b + 1);
-  k::DecodeChunk* d_chunks = scratch<k::DecodeChunk>(dc.chunks, chunks.size());
-  cuda_ok(cudaMemcpyAsync(d_tok, h_tok.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
-  cuda_ok(cudaMemcpyAsync(d_pos, h_pos.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
-  cuda_ok(cudaMemcpyAsync(d_inst, h_inst.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
-  cuda_ok(cudaMemcpyAsync(d_slot, h_slot.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
+  k::DecodeChunk* d_chunks = scratch<k::DecodeChunk>(dc.chunks, std::max<size_t>(chunks.size(), 1));
+  cuda_ok(cudaMemcpyAsync(d_tok, h_tok.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_pos, h_pos.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_inst, h_inst.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_slot, h_slot.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
   cuda_ok(cudaMemcpyAsync(d_rs, h_row_start.data(), (b + 1) * 4, cudaMemcpyHostToDevice, s), "h2d");
-  cuda_ok(cudaMemcpyAsync(d_chunks, chunks.data(), chunks.size() * sizeof(k::DecodeChunk),
-                          cudaMemcpyHostToDevice, s),
-          "h2d");
-  bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(b) * H);
-  bf16* xn = scratch<bf16>(dc.xn, static_cast<size_t>(b) * H);
-  bf16* q = scratch<bf16>(dc.q, static_cast<size_t>(b) * H);
-  bf16* attn = scratch<bf16>(dc.attn, static_cast<size_t>(b) * H);
-  bf16* hbuf = scratch<bf16>(dc.h, static_cast<size_t>(b) * F);
-  float* part_o = scratch<float>(dc.part_o, static_cast<size_t>(n_chunks) * cfg_.heads * cfg_.head_dim);
-  float* part_ml = scratch<float>(dc.part_ml, static_cast<size_t>(n_chunks) * cfg_.heads * 2);
+  if (!chunks.empty()) {
+    cuda_ok(cudaMemcpyAsync(d_chunks, chunks.data(), chunks.size() * sizeof(k::DecodeChunk),
+                            cudaMemcpyHostToDevice, s),
+            "h2d");
+  }
+  // Chunk attention: gather list (earlier tokens, then the chunk) and one
+  // ring segment of d = 1 whose causal offset is the chunk's start:
+  // query a (position p_prev + a) sees key b iff b <= a + p_prev.
+  const int kv_n = static_cast<int>(p_prev) + c;
+  int32_t* d_gslab = nullptr;
+  int32_t* d_gslot = nullptr;
+  std::vector<int32_t> work_sorted;
+  if (has_chunk) {
+    std::vector<int32_t> gslab = prev_slab, gslot = prev_slot;
+    gslab.insert(gslab.end(), ch_slab.begin(), ch_slab.end());
+    gslot.insert(gslot.end(), ch_slot.begin(), ch_slot.end());
+    d_gslab = scratch<int32_t>(dc.ret_slab, kv_n);
+    d_gslot = scratch<int32_t>(dc.ret_slot, kv_n);
+    cuda_ok(cudaMemcpyAsync(d_gslab, gslab.data(), kv_n * 4, cudaMemcpyHostToDevice, s), "h2d");
+    cuda_ok(cudaMemcpyAsync(d_gslot, gslot.data(), kv_n * 4, cudaMemcpyHostToDevice, s), "h2d");
+    k::RingSegment sg{};
+    sg.q_row0 = b;
+    sg.q_len = c;
+    sg.n_rounds = 1;
+    sg.kv_row0[0] = 0;
+    sg.kv_len[0] = kv_n;
+    sg.shift[0] = -static_cast<int32_t>(p_prev);
+    std::vector<k::RingSegment> segs{sg};
+    build_attention_work(segs, cfg_.heads, attn_pairs_, kv_n, cfg_.head_dim, work_sorted);
+    k::RingSegment* d_segs = scratch<k::RingSegment>(dc.segs, 1);
+    int32_t* d_work = scratch<int32_t>(dc.work, work_sorted.size());
+    cuda_ok(cudaMemcpyAsync(d_segs, &sg, sizeof(sg), cudaMemcpyHostToDevice, s), "h2d");
+    cuda_ok(cudaMemcpyAsync(d_work, work_sorted.data(), work_sorted.size() * 4,
+                            cudaMemcpyHostToDevice, s),
+            "h2d");
+  }
+  bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(rows) * H);
+  bf16* xn = scratch<bf16>(dc.xn, static_cast<size_t>(rows) * H);
+  bf16* q = scratch<bf16>(dc.q, static_cast<size_t>(rows) * H);
+  bf16* attn = scratch<bf16>(dc.attn, static_cast<size_t>(rows) * H);
+  bf16* hbuf = scratch<bf16>(dc.h, static_cast<size_t>(rows) * F);
+  bf16* kg = has_chunk ? scratch<bf16>(dc.kb, static_cast<size_t>(kv_n) * H) : nullptr;
+  bf16* vg = has_chunk ? scratch<bf16>(dc.vb, static_cast<size_t>(kv_n) * H) : nullptr;
+  float* part_o = scratch<float>(dc.part_o, static_cast<size_t>(std::max(n_chunks, 1)) * cfg_.heads * cfg_.head_dim);
+  float* part_ml = scratch<float>(dc.part_ml, static_cast<size_t>(std::max(n_chunks, 1)) * cfg_.heads * 2);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
+  const int n_work = static_cast<int>(work_sorted.size() / 2);
 
   cuda_ok(cudaEventRecord(dc.e0, s), "event");
-  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, b, H, s); });
+  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s); });
   for (int l = 0; l < cfg_.layers; ++l) {
     const LayerW& w = dc.layers[l];
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, b, H, cfg_.rms_eps, s); });
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, rows, H, cfg_.rms_eps, s); });
     k::GemmEpilogue ep;
     ep.kind = k::kEpiQkvRope;
     ep.q_out = q;
@@ -761,7 +878,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
     ep.rope = dc.rope;
     ep.hidden = H;
     ep.head_dim = cfg_.head_dim;
-    ep.row_inst = d_inst;  // append: the new token's K/V go to its master's slot
+    ep.row_inst = d_inst;  // append: the new tokens' K/V go to their page slots
     ep.row_slot = d_slot;
     k::DecodeSlabs slabs{};
     for (size_t j = 0; j < dc.slabs.size(); ++j) {
@@ -771,47 +888,73 @@ void Runtime::decode_step(const esp_decode_args& a) {
       slabs.k[j] = ep.slab_k[j];
       slabs.v[j] = ep.slab_v[j];
     }
-    timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, b, 3 * H, H, ep, s); });
-    timed(kPhDecodeAttn, s, [&] {
-      k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
-                          part_o, part_ml, s);
-    });
-    timed(kPhCombine, s, [&] {
-      k::decode_combine(part_o, part_ml, d_rs, b, cfg_.heads, cfg_.head_dim, attn, s);
-    });
+    timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
+    if (b > 0) {
+      timed(kPhDecodeAttn, s, [&] {
+        k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
+                            part_o, part_ml, s);
+      });
+      timed(kPhCombine, s, [&] {
+        k::decode_combine(part_o, part_ml, d_rs, b, cfg_.heads, cfg_.head_dim, attn, s);
+      });
+    }
+    if (has_chunk) {
+      timed(kPhAttention, s, [&] {
+        k::gather_rows(slabs, d_gslab, d_gslot, kv_n, kg, vg, H, s);
+        k::ring_attention_variant(attn_variant_, q, kg, vg, attn, rows, kv_n, cfg_.heads,
+                                  cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr),
+                                  1, static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
+      });
+    }
     k::GemmEpilogue eo;
     eo.kind = k::kEpiResidual;
     eo.out = x;
     eo.ldo = H;
-    timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, b, H, H, eo, s); });
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, b, H, cfg_.rms_eps, s); });
+    timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, rows, H, cfg_.rms_eps, s); });
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = hbuf;
     eg.ldo = F;
-    timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, b, 2 * F, H, eg, s); });
+    timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, rows, 2 * F, H, eg, s); });
     k::GemmEpilogue ed;
     ed.kind = k::kEpiResidual;
     ed.out = x;
     ed.ldo = H;
-    timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, b, H, F, ed, s); });
+    timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s); });
   }
-  timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, dc.final_norm, xn, b, H, cfg_.rms_eps, s); });
-  float* logits = scratch<float>(dc.logits, static_cast<size_t>(b) * cfg_.vocab);
-  k::GemmEpilogue ef;
-  ef.kind = k::kEpiStoreF32;
-  ef.out = logits;
-  ef.ldo = cfg_.vocab;
-  timed(kPhLmHead, s, [&] { k::gemm(xn, H, dc.lm_head, H, b, cfg_.vocab, H, ef, s); });
-  int32_t* d_out = scratch<int32_t>(dc.out_tok, b);
-  timed(kPhArgmax, s, [&] { k::argmax_rows(logits, b, cfg_.vocab, d_out, s); });
+  // Output rows: the decode rows, then the chunk's last token when the chunk
+  // completes the prompt (its first generated token, engine.cpp:570-579).
+  const bool chunk_out = has_chunk && a.chunk_final != 0;
+  const int n_out = b + (chunk_out ? 1 : 0);
+  std::vector<int32_t> out_rows(static_cast<size_t>(b));
+  for (int i = 0; i < b; ++i) out_rows[i] = i;
+  if (chunk_out) out_rows.push_back(rows - 1);
+  int32_t* d_out_rows = scratch<int32_t>(dc.last_rows, n_out);
+  cuda_ok(cudaMemcpyAsync(d_out_rows, out_rows.data(), n_out * 4, cudaMemcpyHostToDevice, s), "h2d");
+  timed(kPhNorm, s, [&] {
+    k::rmsnorm(x, (n_out == rows) ? nullptr : d_out_rows, dc.final_norm, xn, n_out, H,
+               cfg_.rms_eps, s);
+  });
+  float* logits = scratch<float>(dc.logits, static_cast<size_t>(std::max(n_out, 1)) * cfg_.vocab);
+  int32_t* d_out = scratch<int32_t>(dc.out_tok, std::max(n_out, 1));
+  if (n_out > 0) {
+    k::GemmEpilogue ef;
+    ef.kind = k::kEpiStoreF32;
+    ef.out = logits;
+    ef.ldo = cfg_.vocab;
+    timed(kPhLmHead, s, [&] { k::gemm(xn, H, dc.lm_head, H, n_out, cfg_.vocab, H, ef, s); });
+    timed(kPhArgmax, s, [&] { k::argmax_rows(logits, n_out, cfg_.vocab, d_out, s); });
+  }
   cuda_ok(cudaEventRecord(dc.e1, s), "event");
   check_cuda("decode launch");
-  std::vector<int32_t> out(static_cast<size_t>(b));
-  cuda_ok(cudaMemcpyAsync(out.data(), d_out, b * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  std::vector<int32_t> out(static_cast<size_t>(std::max(n_out, 1)));
+  if (n_out > 0) {
+    cuda_ok(cudaMemcpyAsync(out.data(), d_out, n_out * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  }
   std::vector<float> lg;
-  if (a.logits_out) {
-    lg.resize(static_cast<size_t>(b) * cfg_.vocab);
+  if ((a.logits_out && b > 0) || (chunk_out && a.chunk_logits_out)) {
+    lg.resize(static_cast<size_t>(n_out) * cfg_.vocab);
     cuda_ok(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
   }
   cuda_ok(cudaStreamSynchronize(s), "decode");
@@ -831,6 +974,18 @@ void Runtime::decode_step(const esp_decode_args& a) {
     if (a.logits_out) {
       std::memcpy(a.logits_out + static_cast<size_t>(i) * cfg_.vocab,
                   lg.data() + static_cast<size_t>(ri) * cfg_.vocab, cfg_.vocab * sizeof(float));
+    }
+  }
+  if (has_chunk) {
+    if (chunk_out) {
+      requests_[a.chunk_request].tokens.push_back(out[b]);
+      if (a.chunk_first_token_out) *a.chunk_first_token_out = out[b];
+      if (a.chunk_logits_out) {
+        std::memcpy(a.chunk_logits_out, lg.data() + static_cast<size_t>(b) * cfg_.vocab,
+                    cfg_.vocab * sizeof(float));
+      }
+    } else if (a.chunk_first_token_out) {
+      *a.chunk_first_token_out = -1;
     }
   }
 }

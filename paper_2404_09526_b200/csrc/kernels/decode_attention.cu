@@ -412,7 +412,31 @@ __global__ void retain_rows_kernel(const bf16* __restrict__ k, const bf16* __res
   }
 }
 
+// Contiguous K/V rows of a request gathered from its page slots (one layer):
+// out_k/out_v[i] = slab_{slab[i]}[slot[i]] (the chunked-prefill attention's
+// key/value rows).
+__global__ void gather_rows_kernel(const DecodeSlabs src, const int32_t* __restrict__ slab,
+                                   const int32_t* __restrict__ slot, bf16* __restrict__ out_k,
+                                   bf16* __restrict__ out_v, int hidden) {
+  const int i = blockIdx.x;
+  const int64_t so = static_cast<int64_t>(slot[i]) * hidden;
+  const int64_t d = static_cast<int64_t>(i) * hidden;
+  const bf16* sk = src.k[slab[i]] + so;
+  const bf16* sv = src.v[slab[i]] + so;
+  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
+    *reinterpret_cast<uint4*>(out_k + d + c) = *reinterpret_cast<const uint4*>(sk + c);
+    *reinterpret_cast<uint4*>(out_v + d + c) = *reinterpret_cast<const uint4*>(sv + c);
+  }
+}
+
 }  // namespace
+
+void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slot, int n,
+                 bf16* out_k, bf16* out_v, int hidden, cudaStream_t s) {
+  if (n <= 0) return;
+  gather_rows_kernel<<<n, 128, 0, s>>>(src, slab, slot, out_k, out_v, hidden);
+  count_launch();
+}
 
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,

@@ -149,6 +149,9 @@ void decode_combine_rows(const float* part_o, const float* part_ml, const int32_
 // from another device into their resting page slots (one layer).
 void retain_rows(const bf16* k, const bf16* v, const int32_t* rows, const int32_t* slab,
                  const int32_t* slot, int n, const DecodeSlabs& dst, int hidden, cudaStream_t s);
+// out_k/out_v[i] = K/V row of page slot (slab[i], slot[i]) — one layer.
+void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slot, int n,
+                 bf16* out_k, bf16* out_v, int hidden, cudaStream_t s);
 
 // ---- small fused ops --------------------------------------------------------
 void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,

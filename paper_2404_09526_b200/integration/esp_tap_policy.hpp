@@ -204,7 +204,8 @@ class EspTapPolicy final : public espsim::Policy {
       std::sort(members.begin(), members.end());
       std::vector<int32_t> masters(p.masters.begin(), p.masters.end());
       std::vector<int64_t> batch(gs.batch.begin(), gs.batch.end());
-      if (batch.empty()) continue;
+      const bool chunk = p.chunk_request >= 0 && p.chunk_tokens > 0;
+      if (batch.empty() && !chunk) continue;
       esp_decode_args a{};
       a.n_members = static_cast<int32_t>(members.size());
       a.members = members.data();
@@ -212,6 +213,28 @@ class EspTapPolicy final : public espsim::Policy {
       a.masters = masters.data();
       a.batch_size = static_cast<int32_t>(batch.size());
       a.batch = batch.data();
+      // Chunked prefill riding on the step (engine.cpp:432-462, 570-579).
+      std::vector<int32_t> ci, ctoks;
+      std::vector<int64_t> ct;
+      if (chunk) {
+        const espsim::Request& q = s.requests[static_cast<size_t>(p.chunk_request)];
+        for (const auto& [inst, tok] : p.chunk_placement) {
+          ci.push_back(inst);
+          ct.push_back(tok);
+        }
+        a.chunk_request = p.chunk_request;
+        a.chunk_tokens = p.chunk_tokens;
+        a.chunk_n = static_cast<int32_t>(ci.size());
+        a.chunk_instance = ci.data();
+        a.chunk_tokens_on = ct.data();
+        a.chunk_final = q.prefilled + p.chunk_tokens == q.input_len ? 1 : 0;
+        if (with_tokens_) {
+          const auto all = tokens_(p.chunk_request, q.input_len);
+          ctoks.assign(all.begin() + q.prefilled, all.begin() + q.prefilled + p.chunk_tokens);
+          a.chunk_token_ids = ctoks.data();
+        }
+        live_.insert(p.chunk_request);
+      }
       check(esp_decode_step(rt_, &a));
     }
   }

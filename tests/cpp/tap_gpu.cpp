@@ -23,14 +23,14 @@ using namespace espsim;
 
 namespace {
 
-int run(const char* name, int instances, TokenCount cap, bool exact_output,
+int run(const char* name, const char* policy, int instances, TokenCount cap, bool exact_output,
         std::vector<TraceRecord> trace, const std::string& sib_path) {
   EngineParams params;
   params.exact_output_reservation = exact_output;
   params.bandwidth_tokens_per_ms = 800;
   ModelConfig model;  // the engine accounts KV in LWM-7B bytes (cluster.hpp:29-34)
   Engine plain(KvPool(instances, cap), model, Sib::load(sib_path),
-               make_policy(parse_policy("esp")), params);
+               make_policy(parse_policy(policy)), params);
   plain.submit(trace);
   plain.run();
 
@@ -42,7 +42,7 @@ int run(const char* name, int instances, TokenCount cap, bool exact_output,
     std::cerr << "create: " << esp_last_error() << "\n";
     return 2;
   }
-  auto tap = std::make_unique<esp_integration::EspTapPolicy>(make_policy(parse_policy("esp")),
+  auto tap = std::make_unique<esp_integration::EspTapPolicy>(make_policy(parse_policy(policy)),
                                                              rt, /*with_tokens=*/true);
   auto* tp = tap.get();
   Engine tapped(KvPool(instances, cap), model, Sib::load(sib_path), std::move(tap), params);
@@ -102,21 +102,29 @@ int main(int argc, char** argv) {
   }
   const std::string sib = argv[1];
   // BASELINE config 1: 4K-token prompt, 2 instances, 64 decode steps.
-  int rc = run("config1", 2, 200000, true, {{0, 4096, 64}}, sib);
+  int rc = run("config1", "esp", 2, 200000, true, {{0, 4096, 64}}, sib);
   // Same prompt on 2 x 4096 slots: scale-down 2->1, then scale-up 1->2 mid-decode.
-  rc |= run("config1_tight", 2, 4096, true, {{0, 4096, 64}}, sib);
+  rc |= run("config1_tight", "esp", 2, 4096, true, {{0, 4096, 64}}, sib);
   // BASELINE config 5: mixed trace, 8 instances x 317,000 slots.
   TraceSpec spec;
   spec.distribution = "mixed";
   spec.requests_per_s = 0.5;
   spec.count = 24;
   spec.seed = 7;
-  rc |= run("config5_mixed", 8, 317000, false, gen_trace(spec), sib);
+  rc |= run("config5_mixed", "esp", 8, 317000, false, gen_trace(spec), sib);
   // A denser mixed trace (96 requests at 2 req/s) on tighter instances: more
   // concurrent groups, multi-request ring batches, masters rotating.
   spec.requests_per_s = 2.0;
   spec.count = 96;
   spec.seed = 11;
-  rc |= run("mixed_96", 8, 160000, true, gen_trace(spec), sib);
+  rc |= run("mixed_96", "esp", 8, 160000, true, gen_trace(spec), sib);
+  // SURVEY §8 f3 baselines on the same kernels: chunked prefill (2048-token
+  // chunks ride on decode steps of one 8-instance group) and prefill/decode
+  // disaggregation (2 prefill + 6 decode instances, handoff KV moves).
+  spec.requests_per_s = 1.0;
+  spec.count = 48;
+  spec.seed = 5;
+  rc |= run("chunked_48", "chunked:2048", 8, 160000, true, gen_trace(spec), sib);
+  rc |= run("disagg_48", "disagg:2+6", 8, 160000, true, gen_trace(spec), sib);
   return rc;
 }

@@ -78,5 +78,12 @@ int main(int argc, char** argv) {
   spec.seed = 7;
   rc |= run("esp", 8, 317000, gen_trace(spec), sib);
   rc |= run("static-hybrid:2", 8, 300000, {{0, 32768, 4}, {5, 1000, 3}}, sib);
+  // SURVEY §8 f3 baselines on the same data path: chunked prefill (chunks
+  // ride on decode steps) and disaggregation (engine-internal handoff moves).
+  spec.requests_per_s = 2.0;
+  spec.count = 60;
+  spec.seed = 11;
+  rc |= run("chunked:2048", 8, 317000, gen_trace(spec), sib);
+  rc |= run("disagg:2+6", 8, 317000, gen_trace(spec), sib);
   return rc;
 }

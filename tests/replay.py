@@ -5,12 +5,13 @@ B200 runtime's C-ABI, exactly as the TapPolicy of INTEGRATION.md does:
   at every schedule() call
     1. reconcile engine-internal changes that happened since the last call,
        using ONLY the engine's own events: finish / evict -> esp_free_request;
-       "displaced" migrations (engine.cpp:587-648) -> esp_move_kv;
+       "displaced" (engine.cpp:587-648) and "handoff" (engine.cpp:194-244)
+       migrations -> esp_move_kv;
     2. require the runtime's page tables == the engine's Request.placement and
        ElasticInstance.kv_used (bit-exact);
     3. execute the ScheduleDecision in apply_decision order (engine.cpp:246-490):
        migrations -> esp_move_kv, prefills -> esp_prefill, decode steps ->
-       esp_decode_step.
+       esp_decode_step (with any chunked-prefill chunk riding on the step).
 """
 import json
 
@@ -41,7 +42,9 @@ def reconcile(rt, events, expected):
     for e in events:
         if e["kind"] in ("finish", "evict"):
             rt.free_request(e["request"])
-        elif e["kind"] == "migration" and e["detail"] == "displaced":
+        elif e["kind"] == "migration" and e["detail"] in ("displaced", "handoff"):
+            # engine-internal KV moves: resolve_foreign_kv (engine.cpp:587-648)
+            # and the disaggregation handoff (engine.cpp:194-244)
             displaced.add(e["request"])
     exp = placement_of(expected)
     for r in sorted(displaced):
@@ -88,7 +91,20 @@ def execute(rt, decision, head, on_prefill=None, on_decode=None):
         if on_decode is not None:
             on_decode(d, members)
         else:
-            rt.decode_step(members, d["masters"], d["batch"])
+            rt.decode_step(members, d["masters"], d["batch"], chunk=chunk_of(d))
+
+
+def chunk_of(d, tokens=None):
+    """The chunked-prefill chunk riding on a recorded decode step (None if
+    none): placement in KvPlacement order, final iff it completes the prompt
+    (engine.cpp:570-579); tokens = the full prompt of the request (sliced)."""
+    if d.get("chunk_request", -1) < 0 or d.get("chunk_tokens", 0) <= 0:
+        return None
+    p0, n = d["chunk_prefilled"], d["chunk_tokens"]
+    return {"request": d["chunk_request"],
+            "placement": [tuple(x) for x in d["chunk_placement"]],
+            "final": p0 + n == d["chunk_input_len"],
+            "tokens": None if tokens is None else tokens[p0:p0 + n]}
 
 
 def replay(rt, path, on_prefill=None, on_decode=None, conservation=False):

@@ -291,3 +291,53 @@ def test_config5_mixed_trace_tiny():
     print(f"config5 tiny: prefill {stats['prefill_tok']} tok in {stats['prefill_ms']:.1f} ms, "
           f"decode {stats['decode_tok']} tok in {stats['decode_ms']:.1f} ms")
     assert stats["decode_tok"] >= 2027
+
+
+def test_chunked_prefill_baseline_tiny(transport):
+    """SURVEY §8 f3, chunked prefill (policies.cpp:297-405): the reference's
+    "chunked:512" decisions, where 512-token prompt chunks ride on decode
+    steps of one 2-instance group (DecodeStepPlan.chunk_*, engine.cpp:432-462)
+    and alternate instances. Each chunk's queries attend to every earlier
+    token of the request (gathered from its page slots) and causally within
+    the chunk; the first token comes from the final chunk. Tokens and logits
+    must equal the dense oracle's — chunking must not change the model."""
+    if transport.startswith("domain"):
+        pytest.skip("chunked prefill runs within one transport domain")
+    path = os.path.join(GOLD, "scenario_tiny_chunked.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    prompts = {r["id"]: replay.prompt_tokens(r["id"], r["input_len"]) for r in head["requests"]}
+    toks = {r: [] for r in prompts}
+    logits = {r: [] for r in prompts}
+
+    def on_decode(d, members):
+        ch = replay.chunk_of(d, prompts.get(d["chunk_request"]))
+        out, lg, _ = rt.decode_step(members, d["masters"], d["batch"], want_logits=True, chunk=ch)
+        for i, r in enumerate(d["batch"]):
+            toks[r].append(int(out[i]))
+            logits[r].append(lg[i])
+        if ch is not None and ch["final"]:
+            toks[ch["request"]].append(ch["first_token"])
+            logits[ch["request"]].append(ch["logits"])
+
+    replay.replay(rt, path, on_decode=on_decode, conservation=True)
+    for r, p in prompts.items():
+        assert toks[r], r
+        check_against_oracle(abi.TINY, p, toks[r], logits[r])
+
+
+def test_disagg_baseline_tiny():
+    """SURVEY §8 f3, prefill/decode disaggregation (policies.cpp:409-553):
+    prefills on instance 0, the engine's handoff moves the KV to the decode
+    instance (engine.cpp:194-244, reconciled into esp_move_kv), decode there;
+    outputs equal the dense oracle's."""
+    path = os.path.join(GOLD, "scenario_tiny_disagg.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    rec = Recorder(rt)
+    replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
+    for r, lgs in rec.logits.items():
+        toks = [int(np.argmax(l)) for l in lgs]
+        check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)

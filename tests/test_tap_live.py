@@ -29,4 +29,4 @@ def test_tap_policy_live(tmp_path):
         check=True)
     out = subprocess.run([str(exe), REF], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr + out.stdout
-    assert out.stdout.count("events identical") == 3, out.stdout
+    assert out.stdout.count("events identical") == 5, out.stdout
