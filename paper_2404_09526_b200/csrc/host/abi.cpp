@@ -390,7 +390,7 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
     cudaMemcpyAsync(dwork, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s);
     const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
     const int nr = static_cast<int>(rows);
-    const int n_work = static_cast<int>(work.size() / 2);
+    const int n_work = esp::attention_n_work(work);
     if (pairs && std::getenv("ESP_ATTN_PROF") != nullptr) {
       // Cycle accounting of the v2 pipeline roles, printed to stderr.
       const int grid = std::min(n_work, 148);

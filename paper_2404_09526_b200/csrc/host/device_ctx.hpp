@@ -67,6 +67,8 @@ struct DeviceCtx {
 // order persistent CTAs should take it (runtime_multi.cpp).
 void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bool pairs,
                           int64_t kv_rows, int head_dim, std::vector<int32_t>& work_sorted);
+// Number of work items in a list built by build_attention_work.
+int attention_n_work(const std::vector<int32_t>& work);
 
 inline void cuda_ok(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {

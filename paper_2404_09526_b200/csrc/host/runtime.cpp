@@ -584,7 +584,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
   bf16* attn = scratch<bf16>(dc.attn, static_cast<size_t>(rows) * H);
   bf16* hbuf = scratch<bf16>(dc.h, static_cast<size_t>(rows) * F);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
-  const int n_work = static_cast<int>(work.size() / 2);
+  const int n_work = attention_n_work(work);
   for (int l = 0; l < cfg_.layers; ++l) {
     const LayerW& w = dc.layers[l];
     timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, rows, H, cfg_.rms_eps, s); });
@@ -864,7 +864,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
   float* part_o = scratch<float>(dc.part_o, static_cast<size_t>(std::max(n_chunks, 1)) * cfg_.heads * cfg_.head_dim);
   float* part_ml = scratch<float>(dc.part_ml, static_cast<size_t>(std::max(n_chunks, 1)) * cfg_.heads * 2);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
-  const int n_work = static_cast<int>(work_sorted.size() / 2);
+  const int n_work = attention_n_work(work_sorted);
 
   cuda_ok(cudaEventRecord(dc.e0, s), "event");
   timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s); });

@@ -39,50 +39,112 @@ namespace esp {
 
 void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bool pairs,
                           int64_t kv_rows, int head_dim, std::vector<int32_t>& work_sorted) {
-  std::vector<int32_t> work;
-  std::vector<std::pair<int64_t, int>> order;  // (cost, item)
+  struct ItemC {
+    int32_t seg, packed;
+    int64_t cost;
+  };
+  std::vector<std::vector<ItemC>> per_sh;  // items of one (segment, head)
   const int span = pairs ? 2 : 1;
   for (size_t si = 0; si < segs.size(); ++si) {
     const k::RingSegment& sg = segs[si];
     const int n_items = (k::q_tiles(sg.q_len) + span - 1) / span;
+    std::vector<int64_t> cost(static_cast<size_t>(n_items), 0);
     for (int qi = 0; qi < n_items; ++qi) {
-      int64_t cost = 0;
       for (int qt = qi * span; qt < std::min(k::q_tiles(sg.q_len), (qi + 1) * span); ++qt) {
         for (int rd = 0; rd < sg.n_rounds; ++rd) {
           const int64_t vis = std::min<int64_t>(
               sg.kv_len[rd], std::min(qt * 128 + 127, sg.q_len - 1) - sg.shift[rd] + 1);
-          cost += vis > 0 ? (vis + 127) / 128 : 0;
+          cost[qi] += vis > 0 ? (vis + 127) / 128 : 0;
         }
       }
-      for (int hd = 0; hd < heads; ++hd) {
-        order.emplace_back(cost, static_cast<int>(work.size() / 2));
-        work.push_back(static_cast<int32_t>(si));
-        work.push_back((qi << 8) | hd);
+    }
+    for (int hd = 0; hd < heads; ++hd) {
+      std::vector<ItemC> v;
+      for (int qi = 0; qi < n_items; ++qi) {
+        v.push_back({static_cast<int32_t>(si), (qi << 8) | hd, cost[qi]});
       }
+      per_sh.push_back(std::move(v));
     }
   }
-  // Persistent CTAs take items round-robin: heads in groups whose K/V fit
-  // comfortably in L2 (32 MiB: one die's half of the 126 MB L2 also holds Q,
-  // O and the other group in flight; 32 beat 64 and 16 by ~2 % at 32K) so
-  // concurrent items share K/V tiles, longest work first within a group.
-  const int64_t head_kv_bytes = kv_rows * head_dim * 2 * 2;
-  static const int64_t budget_mib = [] {
-    const char* e = std::getenv("ESP_ATTN_L2_MIB");
-    return e ? std::max(1, std::atoi(e)) : 32;
-  }();
-  const int head_group = static_cast<int>(
-      std::max<int64_t>(1, (budget_mib << 20) / std::max<int64_t>(head_kv_bytes, 1)));
-  std::stable_sort(order.begin(), order.end(), [&](const auto& x, const auto& y) {
-    const int gx = (work[2 * x.second + 1] & 0xFF) / head_group;
-    const int gy = (work[2 * y.second + 1] & 0xFF) / head_group;
-    return gx != gy ? gx < gy : x.first > y.first;
-  });
-  work_sorted.clear();
-  work_sorted.reserve(work.size());
-  for (const auto& o : order) {
-    work_sorted.push_back(work[2 * o.second]);
-    work_sorted.push_back(work[2 * o.second + 1]);
+  // Units of near-equal cost: within one (segment, head), the cheapest
+  // causal item rides with the dearest (q tiles i and n-1-i see i+1 and n-i
+  // KV tiles). Units are dealt head-major to the persistent CTAs by least
+  // load (LPT), so the CTAs advance through the heads together and the K/V of
+  // only ~2-3 heads is live in L2 at a time (the previous round-robin over a
+  // cost-sorted list let CTAs drift across head groups: 5.6x the algorithmic
+  // DRAM traffic).
+  struct Unit {
+    int head;
+    int64_t cost;
+    std::vector<ItemC> items;
+  };
+  std::vector<Unit> units;
+  for (auto& v : per_sh) {
+    std::stable_sort(v.begin(), v.end(),
+                     [](const ItemC& x, const ItemC& y) { return x.cost > y.cost; });
+    size_t lo = 0, hi = v.size();
+    while (lo < hi) {
+      Unit u;
+      u.head = v[lo].packed & 0xFF;
+      u.items.push_back(v[lo]);
+      u.cost = v[lo].cost;
+      if (hi - 1 > lo) {
+        u.items.push_back(v[hi - 1]);
+        u.cost += v[hi - 1].cost;
+      }
+      units.push_back(std::move(u));
+      ++lo;
+      --hi;
+    }
   }
+  std::stable_sort(units.begin(), units.end(), [](const Unit& x, const Unit& y) {
+    return x.head != y.head ? x.head < y.head : x.cost > y.cost;
+  });
+  static const int n_sm = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = 148;
+    }
+    return v;
+  }();
+  const int G = static_cast<int>(std::max<size_t>(1, std::min<size_t>(units.size(), n_sm)));
+  std::vector<std::vector<const Unit*>> per_cta(static_cast<size_t>(G));
+  std::vector<int64_t> load(static_cast<size_t>(G), 0);
+  for (const Unit& u : units) {
+    int best = 0;
+    for (int c = 1; c < G; ++c) {
+      if (load[c] < load[best]) best = c;
+    }
+    per_cta[best].push_back(&u);
+    load[best] += u.cost;
+  }
+  // Layout: [items: 2 ints each, CTA-contiguous][G][offsets 0..G][n_items].
+  // Kernels with a per-CTA schedule (v2) read G and the offsets; the others
+  // take the items round-robin, which covers them all as well.
+  work_sorted.clear();
+  std::vector<int32_t> offsets{0};
+  int n_items = 0;
+  for (const auto& lst : per_cta) {
+    for (const Unit* u : lst) {
+      for (const ItemC& it : u->items) {
+        work_sorted.push_back(it.seg);
+        work_sorted.push_back(it.packed);
+        ++n_items;
+      }
+    }
+    offsets.push_back(n_items);
+  }
+  (void)kv_rows;
+  (void)head_dim;
+  work_sorted.push_back(G);
+  work_sorted.insert(work_sorted.end(), offsets.begin(), offsets.end());
+  work_sorted.push_back(n_items);
+}
+
+int attention_n_work(const std::vector<int32_t>& work) {
+  return work.empty() ? 0 : work.back();
 }
 
 namespace {
@@ -355,7 +417,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
       bf16* attn = static_cast<bf16*>(dc.attn.ptr);
       bf16* hbuf = static_cast<bf16*>(dc.h.ptr);
-      const int n_work = static_cast<int>(p.work.size() / 2);
+      const int n_work = attention_n_work(p.work);
       timed(kPhAttention, s, [&] {
         const bf16* qd = static_cast<bf16*>(dc.q.ptr);
         // Q rows are this domain's local rows, K/V rows are global.

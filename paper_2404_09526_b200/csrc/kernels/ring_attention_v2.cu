@@ -229,6 +229,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // This CTA's contiguous slice of the host-built schedule (after the items:
+  // G, then G+1 offsets; build_attention_work). CTAs >= G have no work.
+  const int n_sched = __ldg(&work[2 * n_work]);
+  const int w_begin = static_cast<int>(blockIdx.x) < n_sched ? __ldg(&work[2 * n_work + 1 + blockIdx.x]) : 0;
+  const int w_end = static_cast<int>(blockIdx.x) < n_sched ? __ldg(&work[2 * n_work + 2 + blockIdx.x]) : 0;
   const uint32_t t_s[2] = {tmem, tmem + BN};
   const uint32_t t_o[2] = {tmem + 2 * BN, tmem + 2 * BN + HD};
 
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------------------------------------------------- producer
       int ks = 0, vs = 0;
       uint32_t kph = 0, vph = 0, items = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++items) {
+      for (int w = w_begin; w < w_end; ++w, ++items) {
         const Item it = load_item(work, w, segs);
         const RingSegment* sg = &segs[it.seg];
         ESP_PROF_WAIT(0, ptx::mbar_wait(q_empty, (items & 1) ^ 1));
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         commit(&s_full[t]);
       };
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++items) {
+      for (int w = w_begin; w < w_end; ++w, ++items) {
         const Item it = load_item(work, w, segs);
         const RingSegment* sg = &segs[it.seg];
         const bool act[2] = {true, it.act1};
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = static_cast<int>(quad * 32 + lane);
     const uint32_t lane_off = (quad * 32) << 16;
     uint32_t cnt = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+    for (int w = w_begin; w < w_end; ++w) {
       const Item it = load_item(work, w, segs);
       if (t == 1 && !it.act1) continue;
       const RingSegment* sg = &segs[it.seg];
