@@ -35,7 +35,7 @@ constexpr int BN = 128;
 constexpr int kStages = 2;
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;
-constexpr int kDefaultPoly8 = 2;
+constexpr int kDefaultPoly8 = 1;
 
 template <int HD>
 struct Cfg2 {
