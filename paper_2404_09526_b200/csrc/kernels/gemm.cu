@@ -536,7 +536,7 @@ __device__ __forceinline__ void swap_epilogue(const GemmEpilogue& ep, const floa
   }
 }
 
-template <int NT>
+template <int NT, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_skinny_swap(const __grid_constant__ CUtensorMap tmX,
                      const __grid_constant__ CUtensorMap tmW, int M, int N, int K,
@@ -588,6 +588,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int num_n = N / 128, num_k = K / BK;
   WorkRange work(num_n, num_k, kb_per_cta);
+  if constexpr (SPLIT > 1) {
+    // Split-K over a cluster of SPLIT CTAs: CTA rank r of cluster c computes
+    // tile c over K blocks [r, r+1) * num_k / SPLIT; the partial
+    // accumulators are summed through distributed shared memory below.
+    const int r = static_cast<int>(blockIdx.x) % SPLIT;
+    work.next = static_cast<int>(blockIdx.x) / SPLIT * num_k + r * num_k / SPLIT;
+    work.end = static_cast<int>(blockIdx.x) / SPLIT * num_k + (r + 1) * num_k / SPLIT;
+    work.stream = true;
+    work.stride = 0;
+  }
   int tile, kb0, kb1;
 
   ptx::griddep_launch();
@@ -693,6 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
+      if constexpr (SPLIT > 1) continue;  // reduced across the cluster below
       ptx::named_bar_sync(1, 128);
       if (!work.stream) {
         swap_epilogue(ep, sT, M, t, tile, N);
@@ -764,6 +775,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::named_bar_sync(1, 128);
     }
     if (tr && t == 0) tr[4] = gtime();
+  }
+  if constexpr (SPLIT > 1) {
+    // Every CTA's partial tile is in its sT; rank 0 sums the others' over
+    // DSMEM (no global workspace, no atomics) and applies the epilogue; the
+    // second cluster barrier keeps the peers' shared memory alive until then.
+    ptx::cluster_sync();
+    if (ptx::cluster_ctarank() == 0 && warp >= 4) {
+      const int t = static_cast<int>((warp & 3) * 32 + lane);
+      const int tile0 = static_cast<int>(blockIdx.x) / SPLIT;
+      const int n4 = M * 32;  // float4s of the M valid rows
+      float4* own = reinterpret_cast<float4*>(sT);
+      for (int i = t; i < n4; i += 128) {
+        float4 v = own[i];
+#pragma unroll
+        for (int r = 1; r < SPLIT; ++r) {
+          const float4 w = ptx::ld_cluster_f32x4(ptx::mapa(ptx::smem_u32(own + i), r));
+          v.x += w.x;
+          v.y += w.y;
+          v.z += w.z;
+          v.w += w.w;
+        }
+        own[i] = v;
+      }
+      ptx::named_bar_sync(1, 128);
+      swap_epilogue(ep, sT, M, t, tile0, N);
+    }
+    ptx::cluster_sync();
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -995,21 +1033,26 @@ static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, i
   count_launch();
 }
 
-template <int NT>
+template <int NT, int SPLIT>
 static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
                                int kb_per_cta, const GemmEpilogue& ep, cudaStream_t s,
                                float* ws, int* tile_kb) {
   using C = swp::Cfg<NT>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_skinny_swap<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_skinny_swap<NT, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::kSmem);
+    if (SPLIT > 1) {
+      cudaFuncSetAttribute(gemm_skinny_swap<NT, SPLIT>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
   });
   const CUtensorMap tx = make_tmap_bf16(A, M, K, lda, NT);
   const CUtensorMap tw = make_tmap_bf16(B, N, K, ldb, 128);
   const int tiles = N / 128;
-  const int grid = kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
-                                  : std::min(tiles, num_sms());
+  const int grid = SPLIT > 1 ? tiles * SPLIT
+                   : kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
+                                    : std::min(tiles, num_sms());
   // Study: ESP_GEMM_TRACE=<file> appends per-CTA globaltimer stamps (entry,
   // setup done, first stage landed, last MMA, first tile drained, epilogue
   // done, exit) of every skinny launch to <file> (synchronises the stream).
@@ -1019,8 +1062,29 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
     cudaMalloc(&trace, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long));
     cudaMemsetAsync(trace, 0, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long), s);
   }
-  launch_pdl(1, gemm_skinny_swap<NT>, dim3(grid), dim3(kThreads), C::kSmem, s, tx, tw, M, N, K,
-             kb_per_cta, ep, ws, tile_kb, trace);
+  if constexpr (SPLIT > 1) {
+    // Cluster of SPLIT CTAs per output tile (split-K reduced over DSMEM),
+    // with programmatic dependent launch like the other decode kernels.
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = SPLIT;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled(1) ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, gemm_skinny_swap<NT, SPLIT>, tx, tw, M, N, K, 0, ep, ws, tile_kb,
+                       trace);
+  } else {
+    launch_pdl(1, gemm_skinny_swap<NT, SPLIT>, dim3(grid), dim3(kThreads), C::kSmem, s, tx, tw,
+               M, N, K, kb_per_cta, ep, ws, tile_kb, trace);
+  }
   count_launch();
   if (trace) {
     std::vector<unsigned long long> h(static_cast<size_t>(grid) * 8);
@@ -1136,6 +1200,24 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     // fixup handshake (~5 us) costs more than the imbalance
     // (tools/skinny_probe.py, swap-AB kernel with PDL).
     const bool old = getenv("ESP_GEMM_SKINNY_OLD") != nullptr;
+    // Few wide tiles (O, down: 32): split-K over a cluster of 4 CTAs reduced
+    // through distributed shared memory — 128 SMs stream weights and there
+    // is no global fixup (ESP_GEMM_SPLIT=0 falls back to stream-K).
+    static const int split_env = [] {
+      const char* e = getenv("ESP_GEMM_SPLIT");
+      return e ? atoi(e) : 4;
+    }();
+    if (!old && split_env >= 2 && getenv("ESP_GEMM_NO_STREAMK") == nullptr &&
+        getenv("ESP_GEMM_STREAMK_ALL") == nullptr && tiles * 4 <= num_sms() && K / BK >= 16) {
+      if (M <= 16) launch_skinny_swap<16, 4>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      else launch_skinny_swap<32, 4>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      return;
+    }
+    if (!old && getenv("ESP_GEMM_SPLIT2_ALL") != nullptr) {  // study knob
+      if (M <= 16) launch_skinny_swap<16, 2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      else launch_skinny_swap<32, 2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      return;
+    }
     static const int sk_min_kb = [] {
       const char* e = getenv("ESP_GEMM_SK_MIN_KB");
       return e ? atoi(e) : 0;
@@ -1144,8 +1226,8 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     if (getenv("ESP_GEMM_NO_STREAMK") != nullptr ||
         (getenv("ESP_GEMM_STREAMK_ALL") == nullptr && !streamk)) {
       if (old) launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 0, ep, s);
-      else if (M <= 16) launch_skinny_swap<16>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
-      else launch_skinny_swap<32>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      else if (M <= 16) launch_skinny_swap<16, 1>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      else launch_skinny_swap<32, 1>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       return;
     }
     const int per = (total + num_sms() - 1) / num_sms();
@@ -1153,8 +1235,8 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     const StreamKWs w =
         streamk_workspace(static_cast<size_t>(tiles) * max_seg * M * 128, tiles, s);
     if (old) launch_gemm<128, true>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
-    else if (M <= 16) launch_skinny_swap<16>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
-    else launch_skinny_swap<32>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
+    else if (M <= 16) launch_skinny_swap<16, 1>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
+    else launch_skinny_swap<32, 1>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
     return;
   }
   if (launch_gemm_pair(A, lda, B, ldb, M, N, K, ep, s)) return;

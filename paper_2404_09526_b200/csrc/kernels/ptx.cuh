@@ -283,6 +283,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// 16-byte load from another CTA's shared memory (distributed shared memory).
+__device__ __forceinline__ float4 ld_cluster_f32x4(uint32_t cluster_addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_addr)
+               : "memory");
+  return v;
+}
 // TMA into this CTA's smem, completing bytes on an mbarrier that may live in
 // the peer CTA of the pair (the leader's).
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m,

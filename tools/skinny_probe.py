@@ -5,6 +5,7 @@ same shape. Modes (env of the k_gemm call):
   old_*    the M = 128 skinny kernel (ESP_GEMM_SKINNY_OLD); default: swap-AB
   tiles    whole 128-column tiles per CTA (ESP_GEMM_NO_STREAMK)
   streamk  equal (tile, K-block) ranges per SM (ESP_GEMM_STREAMK_ALL)
+  auto     the production dispatch (cluster split-K over DSMEM for <= 37 tiles)
   *_first / *_nohint   weight loads with L2 evict_first / no hint
   *_tiled  weights pre-tiled [N/128][K/64][128][64] (16 KB contiguous per load)
 SHAPES=qkv,o selects shapes; MODES=tiles,streamk_tiled selects modes."""
@@ -18,19 +19,22 @@ from paper_2404_09526_b200 import abi  # noqa: E402
 
 SHAPES = {"qkv": (12288, 4096, 0), "o": (4096, 4096, 1), "gate_up": (22016, 4096, 3),
           "down": (4096, 11008, 1), "lm_head": (32000, 4096, 2)}
-ALL_MODES = ["old_tiles", "old_streamk", "tiles", "streamk"]
+ALL_MODES = ["tiles", "streamk", "auto", "split2"]
 
 
 def set_mode(mode):
-    for k in ("ESP_GEMM_NO_STREAMK", "ESP_GEMM_STREAMK_ALL", "ESP_GEMM_B_MODE", "ESP_GEMM_SKINNY_OLD"):
+    for k in ("ESP_GEMM_NO_STREAMK", "ESP_GEMM_STREAMK_ALL", "ESP_GEMM_B_MODE", "ESP_GEMM_SKINNY_OLD",
+              "ESP_GEMM_SPLIT2_ALL"):
         os.environ.pop(k, None)
     if mode.startswith("old_"):
         os.environ["ESP_GEMM_SKINNY_OLD"] = "1"
         mode = mode[4:]
     if mode.startswith("tiles"):
         os.environ["ESP_GEMM_NO_STREAMK"] = "1"
-    else:
+    elif mode.startswith("streamk"):
         os.environ["ESP_GEMM_STREAMK_ALL"] = "1"
+    elif mode == "split2":
+        os.environ["ESP_GEMM_SPLIT2_ALL"] = "1"
     bm = (1 if "tiled" in mode else 0) | (2 if "first" in mode else 0) | (4 if "nohint" in mode else 0)
     os.environ["ESP_GEMM_B_MODE"] = str(bm)
 
@@ -82,7 +86,7 @@ def main():
             torch.cuda.synchronize()
             outs[mode] = d.float().clone()
         for k in ("ESP_GEMM_NO_STREAMK", "ESP_GEMM_STREAMK_ALL", "ESP_GEMM_B_MODE",
-                  "ESP_GEMM_SKINNY_OLD"):
+                  "ESP_GEMM_SKINNY_OLD", "ESP_GEMM_SPLIT2_ALL"):
             os.environ.pop(k, None)
         dc = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         res["cublas"] = time_calls(lambda i: torch.matmul(a, bs[i % 8].t(), out=dc))
