@@ -186,7 +186,8 @@ Runtime::~Runtime() {
                       &dc.tok, &dc.pos, &dc.rinst, &dc.rslot, &dc.segs, &dc.work,
                       &dc.last_rows, &dc.out_tok, &dc.chunks, &dc.row_start, &dc.part_o,
                       &dc.part_ml, &dc.counts, &dc.result, &dc.kvrow, &dc.ret_rows,
-                      &dc.ret_slab, &dc.ret_slot, &dc.qin, &dc.chunk_ids, &dc.row_list};
+                      &dc.ret_slab, &dc.ret_slot, &dc.qin, &dc.chunk_ids, &dc.row_list,
+                      &dc.combine_cnt};
     for (DevBuf* b : bufs) {
       if (b->ptr) cudaFree(b->ptr);
     }
@@ -865,6 +866,17 @@ void Runtime::decode_step(const esp_decode_args& a) {
   float* part_ml = scratch<float>(dc.part_ml, static_cast<size_t>(std::max(n_chunks, 1)) * cfg_.heads * 2);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
   const int n_work = attention_n_work(work_sorted);
+  // ESP_DECODE_FUSED_COMBINE=1: LSE combine inside the attention kernel.
+  static const bool fused_combine = [] {
+    const char* e = std::getenv("ESP_DECODE_FUSED_COMBINE");
+    return e != nullptr && e[0] == '1';
+  }();
+  // Fused-combine counters: zero on allocation, left zero by every launch.
+  const size_t cnt_bytes = dc.combine_cnt.bytes;
+  int* d_cnt = scratch<int>(dc.combine_cnt, static_cast<size_t>(std::max(b, 1)) * cfg_.heads);
+  if (dc.combine_cnt.bytes != cnt_bytes) {
+    cuda_ok(cudaMemsetAsync(d_cnt, 0, dc.combine_cnt.bytes, s), "memset");
+  }
 
   cuda_ok(cudaEventRecord(dc.e0, s), "event");
   timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s); });
@@ -889,7 +901,14 @@ void Runtime::decode_step(const esp_decode_args& a) {
       slabs.v[j] = ep.slab_v[j];
     }
     timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
-    if (b > 0) {
+    if (b > 0 && fused_combine) {
+      // Split-KV attention with the LSE combine fused (the last CTA of each
+      // (row, head) merges the row's chunk partials).
+      timed(kPhDecodeAttn, s, [&] {
+        k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
+                            part_o, part_ml, s, d_rs, d_cnt, attn, b);
+      });
+    } else if (b > 0) {
       timed(kPhDecodeAttn, s, [&] {
         k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
                             part_o, part_ml, s);

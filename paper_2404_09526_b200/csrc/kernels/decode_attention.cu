@@ -45,11 +45,38 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   }
 }
 
+// Fused LSE combine (single-domain decode): the last CTA to finish a (row,
+// head) merges that row's chunk partials (row_start) into the bf16 output.
+struct FusedCombine {
+  const int32_t* row_start = nullptr;  // null: partials only (combined elsewhere)
+  int* counters = nullptr;             // [rows x heads], zero between launches
+  bf16* out = nullptr;
+};
+
+template <int HD>
+__device__ __forceinline__ void combine_row_head(const float* part_o, const float* part_ml,
+                                                 int c0, int c1, int heads, int head, bf16* out) {
+  float mm = -INFINITY;
+  for (int c = c0; c < c1; ++c) mm = fmaxf(mm, __ldcg(&part_ml[(static_cast<int64_t>(c) * heads + head) * 2]));
+  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+    float acc = 0.f, ll = 0.f;
+    for (int c = c0; c < c1; ++c) {
+      const int64_t p = static_cast<int64_t>(c) * heads + head;
+      const float mc = __ldcg(&part_ml[p * 2]);
+      const float w = mc == -INFINITY ? 0.f : exp2f(mc - mm);
+      acc += w * __ldcg(&part_o[p * HD + d]);
+      ll += w * __ldcg(&part_ml[p * 2 + 1]);
+    }
+    out[d] = __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
+  }
+}
+
 template <int HD, int UNR = kUnroll, int MINB = 1>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
     decode_attention_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
                             const DecodeSlabs slabs, int heads, float scale_log2,
-                            float* __restrict__ part_o, float* __restrict__ part_ml) {
+                            float* __restrict__ part_o, float* __restrict__ part_ml,
+                            const FusedCombine fc) {
   constexpr int LPT = HD / 8;     // lanes per token
   constexpr int TPW = 32 / LPT;   // tokens per warp step
   // blockIdx.x = head (fastest): the CTAs resident at a time cover every head
@@ -160,6 +187,21 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     if (d == 0) {
       part_ml[pidx * 2] = mm;
       part_ml[pidx * 2 + 1] = ll;
+    }
+  }
+  if (fc.row_start != nullptr) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    const int c0 = __ldg(&fc.row_start[ch.row]), c1 = __ldg(&fc.row_start[ch.row + 1]);
+    int* cnt = &fc.counters[ch.row * heads + head];
+    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == c1 - c0 - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      combine_row_head<HD>(part_o, part_ml, c0, c1, heads, head,
+                           fc.out + static_cast<int64_t>(ch.row) * hidden + head * HD);
+      if (threadIdx.x == 0) *cnt = 0;
     }
   }
 }
@@ -440,8 +482,13 @@ void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slo
 
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
-                      float* part_o, float* part_ml, cudaStream_t s) {
+                      float* part_o, float* part_ml, cudaStream_t s, const int32_t* row_start,
+                      int* counters, bf16* out, int rows) {
   if (n_chunks <= 0) return;
+  FusedCombine fc;
+  fc.row_start = row_start;
+  fc.counters = counters;
+  fc.out = out;
   if (n_chunks > 65535) throw std::runtime_error("decode_attention: more than 65535 chunks");
   const dim3 grid(heads, n_chunks);
   const float sl2 = scale * 1.4426950408889634f;
@@ -464,13 +511,14 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
     }
 #undef ESP_V2
     count_launch();
+    if (row_start != nullptr) decode_combine(part_o, part_ml, row_start, rows, heads, head_dim, out, s);
     return;
   }
   if (head_dim == 128) {
     // ESP_DECODE_V1=<unroll><min blocks per SM> tuning variants of v1
     const char* tv = std::getenv("ESP_DECODE_V1");
     const int tune = tv ? std::atoi(tv) : 0;
-#define ESP_V1(U, B) launch_pdl(4, decode_attention_kernel<128, U, B>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml)
+#define ESP_V1(U, B) launch_pdl(4, decode_attention_kernel<128, U, B>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc)
     switch (tune) {
       case 41: ESP_V1(4, 1); break;
       case 410: ESP_V1(4, 10); break;
@@ -489,7 +537,7 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 #undef ESP_V1
   } else if (head_dim == 64) {
     decode_attention_kernel<64><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads, sl2,
-                                                            part_o, part_ml);
+                                                            part_o, part_ml, fc);
   } else {
     throw std::runtime_error("decode_attention: head_dim must be 64 or 128");
   }

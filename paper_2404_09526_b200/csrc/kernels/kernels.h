@@ -133,9 +133,14 @@ struct DecodeSlabs {
 };
 // Split-KV paged attention: partial (o, m, l) per (chunk, head) into
 // part_o [n_chunks x heads x head_dim] fp32 and part_ml [n_chunks x heads x 2].
+// With row_start != null the LSE combine is fused: the last CTA of each
+// (row, head) merges the row's partials into out (rows x heads*head_dim bf16);
+// counters = rows x heads ints, zero on entry and left zero.
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
-                      float* part_o, float* part_ml, cudaStream_t s);
+                      float* part_o, float* part_ml, cudaStream_t s,
+                      const int32_t* row_start = nullptr, int* counters = nullptr,
+                      bf16* out = nullptr, int rows = 0);
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);
