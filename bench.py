@@ -451,7 +451,8 @@ def bench_transport(abi, args, np):
     out = {"config": f"LWM-7B {S}-token prefill, ring of {d} instances, one transport domain "
                      f"each (one GPU)",
            "ring_bytes_per_layer": (d - 1) * S * H * 2 * 2}
-    saved = {k: os.environ.get(k) for k in ("ESP_DOMAIN_PER_INSTANCE", "ESP_RING_COPY")}
+    saved = {k: os.environ.get(k) for k in ("ESP_DOMAIN_PER_INSTANCE", "ESP_RING_COPY",
+                                            "ESP_DECODE_COPY")}
     try:
         os.environ["ESP_DOMAIN_PER_INSTANCE"] = "1"
         for mode in ("push", "copy"):
@@ -469,6 +470,36 @@ def bench_transport(abi, args, np):
             rt.close()
             out[f"{mode}_ms"] = ms[0]
             out[f"{mode}_tokens_per_s"] = S / (ms[0] / 1e3)
+        # Multi-master decode across domains (query broadcast to every domain
+        # holding KV, split-KV partials there, partial gather + LSE combine at
+        # the masters) vs the same group co-located: b=16 requests x 4096
+        # tokens spread over the d instances, 2 masters.
+        b, ctx = 16, 4096
+        os.environ.pop("ESP_RING_COPY", None)
+        for mode in ("decode_domains_push", "decode_domains_copy", "decode_colocated"):
+            os.environ.pop("ESP_DECODE_COPY", None)
+            if mode == "decode_colocated":
+                os.environ.pop("ESP_DOMAIN_PER_INSTANCE", None)
+            else:
+                os.environ["ESP_DOMAIN_PER_INSTANCE"] = "1"
+                if mode == "decode_domains_copy":
+                    os.environ["ESP_DECODE_COPY"] = "1"
+            per = ctx // d
+            rt = abi.Runtime(abi.LWM_7B, d, devices=[dev] * d, kv_capacity=b * per + 64)
+            rng = np.random.default_rng(19)
+            for r in range(b):
+                rt.prefill([r], [ctx], list(range(d)), [[(i, per) for i in range(d)]],
+                           tokens=rng.integers(0, V, ctx).astype(np.int32))
+            for _ in range(2):
+                rt.decode_step(list(range(d)), [0, 1], list(range(b)))
+            ms = [rt.decode_step(list(range(d)), [0, 1], list(range(b)))[2] for _ in range(3)]
+            rt.close()
+            out[f"{mode}_ms"] = sum(ms) / len(ms)
+        out["decode_config"] = (f"b={b} x {ctx} tokens over {d} instances, 2 masters; domains = "
+                                f"one transport domain per instance: push = q rows and split-KV "
+                                f"partials as peer stores from the QKV epilogue / attention "
+                                f"kernel, copy = peer copies; colocated = one domain. On one "
+                                f"GPU the two master domains each stream all weights")
     finally:
         for k, v in saved.items():
             if v is None:

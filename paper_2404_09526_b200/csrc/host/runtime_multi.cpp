@@ -631,8 +631,169 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
     });
   }
   const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
+  // Fused transport (default): the masters' QKV epilogues store their q rows
+  // straight into every KV domain's query buffer (the broadcast as peer
+  // stores), and each KV domain's attention kernel stores its split-KV
+  // partials straight into the master domains' partial buffers (the gather as
+  // peer stores). Only events order the domains. ESP_DECODE_COPY=1 keeps the
+  // copy-engine transport (peer copies of row runs / chunk ranges).
+  const bool copy_transport = std::getenv("ESP_DECODE_COPY") != nullptr;
+  // Per master domain: the KV domains its rows need (q destinations); per KV
+  // domain: the master domains it owes partials (PartDst entries).
+  std::map<int, std::vector<int>> q_dests;
+  std::map<int, std::vector<int>> part_dests;
+  for (auto& [key, rg] : range_of) {
+    q_dests[key.first].push_back(key.second);
+    part_dests[key.second].push_back(key.first);
+  }
+  bool fused = !copy_transport;
+  for (auto& [md, v] : q_dests) {
+    if (static_cast<int>(v.size()) > k::kMaxPeers + 1) fused = false;
+  }
+  for (auto& [xd, v] : part_dests) {
+    if (static_cast<int>(v.size()) > k::kMaxPartDst) fused = false;
+  }
+  if (fused) {
+    // chunk -> index of its master domain in the KV domain's PartDst table
+    for (auto& [xd, chs] : xchunks) {
+      const std::vector<int>& pdv = part_dests[xd];
+      for (k::DecodeChunk& ch : chs) {
+        const int md = mdom[ch.row];
+        ch.dst = static_cast<int32_t>(std::find(pdv.begin(), pdv.end(), md) - pdv.begin());
+      }
+      DeviceCtx& xc = *devices_[static_cast<size_t>(xd)];
+      DeviceGuard g(xc.device);
+      h2d(static_cast<k::DecodeChunk*>(xc.chunks.ptr), chs, xc.stream);
+    }
+  }
+  if (fused) {
+    std::map<int, cudaEvent_t> att_done, comb_done;  // previous layer's
+    for (int l = 0; l < cfg_.layers; ++l) {
+      std::map<int, cudaEvent_t> q_ready;
+      // 1. masters: norm + QKV; q rows pushed to the KV domains' qin.
+      for (auto& [md, rs] : mrows) {
+        DeviceCtx& dc = *devices_[static_cast<size_t>(md)];
+        DeviceGuard g(dc.device);
+        cudaStream_t s = dc.stream;
+        for (int xd : q_dests[md]) {  // qin readers of the previous layer
+          if (att_done.count(xd)) cuda_ok(cudaStreamWaitEvent(s, att_done[xd], 0), "wait");
+        }
+        const int nl = static_cast<int>(rs.size());
+        const LayerW& w = dc.layers[l];
+        bf16* x = static_cast<bf16*>(dc.x.ptr);
+        bf16* xn = static_cast<bf16*>(dc.xn.ptr);
+        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, nl, H, cfg_.rms_eps, s); });
+        k::GemmEpilogue ep;
+        ep.kind = k::kEpiQkvRope;
+        ep.q_out = static_cast<bf16*>(dc.q.ptr);
+        ep.pos = static_cast<int32_t*>(dc.pos.ptr);
+        ep.rope = dc.rope;
+        ep.hidden = H;
+        ep.head_dim = hd;
+        ep.row_inst = static_cast<int32_t*>(dc.rinst.ptr);
+        ep.row_slot = static_cast<int32_t*>(dc.rslot.ptr);
+        ep.q_rows = static_cast<int32_t*>(dc.row_list.ptr);  // local row -> global row
+        bool own = false;
+        for (int xd : q_dests[md]) {
+          bf16* qin = static_cast<bf16*>(devices_[static_cast<size_t>(xd)]->qin.ptr);
+          if (xd == md) {
+            ep.q_out = qin;  // this domain's own KV: its qin is the q output
+            own = true;
+          } else {
+            ep.q_peer[ep.n_qpeer++] = qin;
+          }
+        }
+        if (!own) ep.q_out = nullptr;
+        if (ep.n_qpeer > k::kMaxPeers) throw InternalError("too many query destinations");
+        for (size_t j = 0; j < dc.slabs.size(); ++j) {
+          ep.slab_k[j] = instances_[dc.slabs[j]].layer_k(l);
+          ep.slab_v[j] = instances_[dc.slabs[j]].layer_v(l);
+        }
+        timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, nl, 3 * H, H, ep, s); });
+        cudaEvent_t e = sync_event(dc);
+        cuda_ok(cudaEventRecord(e, s), "event");
+        q_ready[md] = e;
+      }
+      // 2. KV domains: split-KV partials pushed to the masters' buffers.
+      std::map<int, cudaEvent_t> att_now;
+      for (auto& [xd, chs] : xchunks) {
+        DeviceCtx& xc = *devices_[static_cast<size_t>(xd)];
+        DeviceGuard g(xc.device);
+        cudaStream_t s = xc.stream;
+        k::PartDst pd;
+        const std::vector<int>& pdv = part_dests[xd];
+        for (size_t i = 0; i < pdv.size(); ++i) {
+          const int md = pdv[i];
+          DeviceCtx& mc = *devices_[static_cast<size_t>(md)];
+          pd.o[i] = static_cast<float*>(mc.part_o.ptr);
+          pd.ml[i] = static_cast<float*>(mc.part_ml.ptr);
+          cuda_ok(cudaStreamWaitEvent(s, q_ready[md], 0), "wait");
+          // the master's combine of the previous layer has read its partials
+          if (comb_done.count(md)) cuda_ok(cudaStreamWaitEvent(s, comb_done[md], 0), "wait");
+        }
+        k::DecodeSlabs slabs{};
+        for (size_t j = 0; j < xc.slabs.size(); ++j) {
+          slabs.k[j] = instances_[xc.slabs[j]].layer_k(l);
+          slabs.v[j] = instances_[xc.slabs[j]].layer_v(l);
+        }
+        timed(kPhDecodeAttn, s, [&] {
+          k::decode_attention(static_cast<bf16*>(xc.qin.ptr),
+                              static_cast<k::DecodeChunk*>(xc.chunks.ptr),
+                              static_cast<int>(chs.size()), slabs, heads, hd, scale,
+                              static_cast<float*>(xc.part_o.ptr),
+                              static_cast<float*>(xc.part_ml.ptr), s, nullptr, nullptr, nullptr,
+                              0, &pd);
+        });
+        cudaEvent_t e = sync_event(xc);
+        cuda_ok(cudaEventRecord(e, s), "event");
+        att_now[xd] = e;
+      }
+      att_done = att_now;
+      // 3. masters: LSE combine over the pushed partials, then the dense layers.
+      std::map<int, cudaEvent_t> comb_now;
+      for (auto& [md, rs] : mrows) {
+        DeviceCtx& mc = *devices_[static_cast<size_t>(md)];
+        DeviceGuard g(mc.device);
+        cudaStream_t s = mc.stream;
+        for (int xd : q_dests[md]) cuda_ok(cudaStreamWaitEvent(s, att_done[xd], 0), "wait");
+        const int nl = static_cast<int>(rs.size());
+        const LayerW& w = mc.layers[l];
+        bf16* x = static_cast<bf16*>(mc.x.ptr);
+        bf16* xn = static_cast<bf16*>(mc.xn.ptr);
+        bf16* attn = static_cast<bf16*>(mc.attn.ptr);
+        bf16* hbuf = static_cast<bf16*>(mc.h.ptr);
+        timed(kPhCombine, s, [&] {
+          k::decode_combine_rows(static_cast<float*>(mc.part_o.ptr),
+                                 static_cast<float*>(mc.part_ml.ptr),
+                                 static_cast<int32_t*>(mc.row_start.ptr),
+                                 static_cast<int32_t*>(mc.chunk_ids.ptr),
+                                 static_cast<int32_t*>(mc.row_list.ptr), nl, heads, hd, attn, s);
+        });
+        cudaEvent_t e = sync_event(mc);
+        cuda_ok(cudaEventRecord(e, s), "event");
+        comb_now[md] = e;
+        k::GemmEpilogue eo;
+        eo.kind = k::kEpiResidual;
+        eo.out = x;
+        eo.ldo = H;
+        timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, nl, H, H, eo, s); });
+        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, nl, H, cfg_.rms_eps, s); });
+        k::GemmEpilogue eg;
+        eg.kind = k::kEpiSiluMul;
+        eg.out = hbuf;
+        eg.ldo = F;
+        timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, nl, 2 * F, H, eg, s); });
+        k::GemmEpilogue ed;
+        ed.kind = k::kEpiResidual;
+        ed.out = x;
+        ed.ldo = H;
+        timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, nl, H, F, ed, s); });
+      }
+      comb_done = comb_now;
+    }
+  }
   std::map<int, std::vector<cudaEvent_t>> q_readers, part_readers;
-  for (int l = 0; l < cfg_.layers; ++l) {
+  for (int l = 0; !fused && l < cfg_.layers; ++l) {
     std::map<int, cudaEvent_t> q_ready, part_ready;
     // 1. masters: norm + QKV (+RoPE, the new token's K/V appended at the master).
     for (auto& [dom, rs] : mrows) {

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     decode_attention_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
                             const DecodeSlabs slabs, int heads, float scale_log2,
                             float* __restrict__ part_o, float* __restrict__ part_ml,
-                            const FusedCombine fc) {
+                            const FusedCombine fc, const PartDst dst) {
   constexpr int LPT = HD / 8;     // lanes per token
   constexpr int TPW = 32 / LPT;   // tokens per warp step
   // blockIdx.x = head (fastest): the CTAs resident at a time cover every head
@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   __syncthreads();
   (void)ci;
   const int64_t pidx = static_cast<int64_t>(ch.out) * heads + head;
+  if (dst.o[0] != nullptr) {  // fused partial gather: store to the master's buffers
+    part_o = dst.o[ch.dst];
+    part_ml = dst.ml[ch.dst];
+  }
   for (int d = threadIdx.x; d < HD; d += blockDim.x) {
     float mm = -INFINITY;
 #pragma unroll
@@ -483,8 +487,9 @@ void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slo
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
                       float* part_o, float* part_ml, cudaStream_t s, const int32_t* row_start,
-                      int* counters, bf16* out, int rows) {
+                      int* counters, bf16* out, int rows, const PartDst* dst) {
   if (n_chunks <= 0) return;
+  const PartDst pd = dst ? *dst : PartDst{};
   FusedCombine fc;
   fc.row_start = row_start;
   fc.counters = counters;
@@ -497,7 +502,7 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
   // cp.async ring (v2) with ESP_DECODE_STAGES stages — slower on B200
   // (3.3-4.0 TB/s: its shared-memory ring caps resident CTAs per SM).
   const char* var = std::getenv("ESP_DECODE_ATTN");
-  if (var != nullptr && std::atoi(var) == 2) {
+  if (var != nullptr && std::atoi(var) == 2 && dst == nullptr) {
     const char* st = std::getenv("ESP_DECODE_STAGES");
     const int ns = st ? std::atoi(st) : 4;
     if (head_dim != 128 && head_dim != 64) {
@@ -518,7 +523,7 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
     // ESP_DECODE_V1=<unroll><min blocks per SM> tuning variants of v1
     const char* tv = std::getenv("ESP_DECODE_V1");
     const int tune = tv ? std::atoi(tv) : 0;
-#define ESP_V1(U, B) launch_pdl(4, decode_attention_kernel<128, U, B>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc)
+#define ESP_V1(U, B) launch_pdl(4, decode_attention_kernel<128, U, B>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd)
     switch (tune) {
       case 41: ESP_V1(4, 1); break;
       case 410: ESP_V1(4, 10); break;
@@ -537,7 +542,7 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 #undef ESP_V1
   } else if (head_dim == 64) {
     decode_attention_kernel<64><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads, sl2,
-                                                            part_o, part_ml, fc);
+                                                            part_o, part_ml, fc, pd);
   } else {
     throw std::runtime_error("decode_attention: head_dim must be 64 or 128");
   }

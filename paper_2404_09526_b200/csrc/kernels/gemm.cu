@@ -215,10 +215,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
       dst_slab = (region == 1 ? ep.slab_k[inst] : ep.slab_v[inst]) +
                  static_cast<int64_t>(slot) * ep.hidden;
     }
-    // q rows follow the GEMM rows; k/v rows may be remapped (ring gather
-    // buffers hold every ring position's rows in global order).
-    const int64_t row_off =
-        static_cast<int64_t>((region > 0 && ep.kv_rows && valid) ? ep.kv_rows[m] : m) * ep.hidden;
+    // q rows follow the GEMM rows (or q_rows); k/v rows may be remapped (ring
+    // gather buffers hold every ring position's rows in global order).
+    int row_map = m;
+    if (valid && region > 0 && ep.kv_rows) row_map = ep.kv_rows[m];
+    if (valid && region == 0 && ep.q_rows) row_map = ep.q_rows[m];
+    const int64_t row_off = static_cast<int64_t>(row_map) * ep.hidden;
     if (region == 2) {
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -261,6 +263,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
             for (int pr = 0; pr < ep.n_peer; ++pr) {
               store_vals_bf16(ep.k_peer[pr] + row_off + c_lo, lo);
               store_vals_bf16(ep.k_peer[pr] + row_off + c_hi, hi);
+            }
+          } else {
+            for (int pr = 0; pr < ep.n_qpeer; ++pr) {
+              store_vals_bf16(ep.q_peer[pr] + row_off + c_lo, lo);
+              store_vals_bf16(ep.q_peer[pr] + row_off + c_hi, hi);
             }
           }
         }

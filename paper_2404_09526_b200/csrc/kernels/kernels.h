@@ -47,6 +47,11 @@ struct GemmEpilogue {
   int n_peer = 0;
   bf16* k_peer[kMaxPeers] = {};
   bf16* v_peer[kMaxPeers] = {};
+  // Multi-master decode across domains: q rows go to row q_rows[m] of q_out
+  // and of every q_peer (the query broadcast fused into the QKV epilogue).
+  const int32_t* q_rows = nullptr;
+  int n_qpeer = 0;
+  bf16* q_peer[kMaxPeers] = {};
 };
 
 // D[M x N] = A[M x K] . B[N x K]^T with the epilogue above. A and B are
@@ -126,6 +131,16 @@ struct DecodeChunk {
   int32_t row;   // request row in the decode batch (row of q)
   int32_t slab;  // index into the slab pointer arrays
   int32_t out;   // index of this chunk's partial in part_o / part_ml
+  int32_t dst;   // PartDst entry the partial is stored to (fused gather), else 0
+};
+// Where split-KV partials go: with o[0] == null the launch's own part_o /
+// part_ml; otherwise chunk c's partial is stored to o[c.dst] / ml[c.dst] —
+// the master domain's buffers, by peer stores over NVLink (the partial
+// gather of multi-master decoding fused into the attention kernel).
+constexpr int kMaxPartDst = 8;
+struct PartDst {
+  float* o[kMaxPartDst] = {};
+  float* ml[kMaxPartDst] = {};
 };
 struct DecodeSlabs {
   const bf16* k[kMaxSlabs];
@@ -140,7 +155,7 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
                       float* part_o, float* part_ml, cudaStream_t s,
                       const int32_t* row_start = nullptr, int* counters = nullptr,
-                      bf16* out = nullptr, int rows = 0);
+                      bf16* out = nullptr, int rows = 0, const PartDst* dst = nullptr);
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);

@@ -33,18 +33,22 @@ def transport(request, monkeypatch):
     INSTANCE), the cross-GPU data path on one GPU. domain_push (default
     transport): each domain's QKV epilogue stores its K/V rows into every
     domain's gather buffer and each token's K/V into its resting slot (peer
-    stores), ordered by events. domain_copy (ESP_RING_COPY): the ring moves K/V
-    blocks by peer copies in the reference's round order and remote-origin
-    tokens are retained on pass. Decode broadcasts queries / gathers partials
-    between domains in both."""
+    stores), ordered by events; decode pushes q rows from the masters' QKV
+    epilogues and split-KV partials from the attention kernels (peer stores).
+    domain_copy (ESP_RING_COPY, ESP_DECODE_COPY): the ring moves K/V blocks by
+    peer copies in the reference's round order and remote-origin tokens are
+    retained on pass; decode broadcasts queries / gathers partials by peer
+    copies."""
     if request.param.startswith("domain"):
         monkeypatch.setenv("ESP_DOMAIN_PER_INSTANCE", "1")
     else:
         monkeypatch.delenv("ESP_DOMAIN_PER_INSTANCE", raising=False)
     if request.param == "domain_copy":
         monkeypatch.setenv("ESP_RING_COPY", "1")
+        monkeypatch.setenv("ESP_DECODE_COPY", "1")
     else:
         monkeypatch.delenv("ESP_RING_COPY", raising=False)
+        monkeypatch.delenv("ESP_DECODE_COPY", raising=False)
     return request.param
 
 
