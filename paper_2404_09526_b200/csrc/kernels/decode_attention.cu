@@ -34,6 +34,17 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
+// Kernel-parameter arrays indexed by a runtime value are copied to local
+// memory (a 256-byte stack frame per thread); an unrolled compare-select
+// keeps them in the constant bank.
+template <int N, typename T>
+__device__ __forceinline__ T pick(const T (&a)[N], int i) {
+  T r = a[0];
+#pragma unroll
+  for (int j = 1; j < N; ++j) r = (i == j) ? a[j] : r;
+  return r;
+}
+
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -98,8 +109,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
 #pragma unroll
   for (int e = 0; e < 8; ++e) qf[e] *= scale_log2;
 
-  const bf16* kb = slabs.k[ch.slab] + head * HD + dl * 8;
-  const bf16* vb = slabs.v[ch.slab] + head * HD + dl * 8;
+  const bf16* kb = pick(slabs.k, ch.slab) + head * HD + dl * 8;
+  const bf16* vb = pick(slabs.v, ch.slab) + head * HD + dl * 8;
   float m = -INFINITY, l = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   const int step = kWarps * TPW;
@@ -173,8 +184,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   (void)ci;
   const int64_t pidx = static_cast<int64_t>(ch.out) * heads + head;
   if (dst.o[0] != nullptr) {  // fused partial gather: store to the master's buffers
-    part_o = dst.o[ch.dst];
-    part_ml = dst.ml[ch.dst];
+    part_o = pick(dst.o, ch.dst);
+    part_ml = pick(dst.ml, ch.dst);
   }
   for (int d = threadIdx.x; d < HD; d += blockDim.x) {
     float mm = -INFINITY;
@@ -254,8 +265,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                 qf);
 #pragma unroll
   for (int e = 0; e < 8; ++e) qf[e] *= scale_log2;
-  const bf16* kb = slabs.k[ch.slab] + head * HD + dl * 8;
-  const bf16* vb = slabs.v[ch.slab] + head * HD + dl * 8;
+  const bf16* kb = pick(slabs.k, ch.slab) + head * HD + dl * 8;
+  const bf16* vb = pick(slabs.v, ch.slab) + head * HD + dl * 8;
   __syncthreads();
 
   const int n_stages = (ch.n + TOK_S - 1) / TOK_S;
