@@ -82,7 +82,7 @@ __device__ __forceinline__ void combine_row_head(const float* part_o, const floa
   }
 }
 
-template <int HD, int UNR = kUnroll, int MINB = 1>
+template <int HD, int UNR = kUnroll, int MINB = 1, int PF = 0>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
     decode_attention_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
                             const DecodeSlabs slabs, int heads, float scale_log2,
@@ -114,6 +114,17 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   float m = -INFINITY, l = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   const int step = kWarps * TPW;
+  // PF: the next iteration's slot ids are loaded one iteration ahead (no
+  // index -> data dependency on the critical path) and, with PF == 2, their
+  // K/V lines are prefetched into L2.
+  int cur[UNR];
+  if constexpr (PF > 0) {
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int t = warp * TPW + sub + u * step;
+      cur[u] = t < ch.n ? __ldg(&ch.slots[t]) : -1;
+    }
+  }
   // The loop bound is warp-uniform (full-mask shuffles inside); lanes past
   // the end of the chunk just carry ok[u] = false.
   for (int tw = warp * TPW; tw < ch.n; tw += step * UNR) {
@@ -124,9 +135,22 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
       const int t = tw + sub + u * step;
       ok[u] = t < ch.n;
       if (ok[u]) {
-        const int64_t off = static_cast<int64_t>(__ldg(&ch.slots[t])) * hidden;
+        const int64_t off =
+            static_cast<int64_t>(PF > 0 ? cur[u] : __ldg(&ch.slots[t])) * hidden;
         kr[u] = ld_nc_v4(kb + off);
         vr[u] = ld_nc_v4(vb + off);
+      }
+    }
+    if constexpr (PF > 0) {
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int t = tw + step * UNR + sub + u * step;
+        cur[u] = t < ch.n ? __ldg(&ch.slots[t]) : -1;
+        if (PF > 1 && cur[u] >= 0) {
+          const int64_t off = static_cast<int64_t>(cur[u]) * hidden;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kb + off));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + off));
+        }
       }
     }
 #pragma unroll
@@ -509,7 +533,9 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
   const dim3 grid(heads, n_chunks);
   const float sl2 = scale * 1.4426950408889634f;
   // Default: the register-staged v1 at <= 64 registers (8 CTAs of 4 warps
-  // per SM; measured best, 6.6-6.7 TB/s on 16 x 8K). ESP_DECODE_ATTN=2: the
+  // per SM), 3 tokens per lane in flight and the next iteration's slot ids
+  // loaded one iteration ahead: 6.81-6.85 TB/s on 16 x 8K (4 in flight
+  // without the look-ahead: 6.44-6.47; tools/decode_probe.py sweeps). ESP_DECODE_ATTN=2: the
   // cp.async ring (v2) with ESP_DECODE_STAGES stages — slower on B200
   // (3.3-4.0 TB/s: its shared-memory ring caps resident CTAs per SM).
   const char* var = std::getenv("ESP_DECODE_ATTN");
@@ -536,6 +562,15 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
     const int tune = tv ? std::atoi(tv) : 0;
 #define ESP_V1(U, B) launch_pdl(4, decode_attention_kernel<128, U, B>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd)
     switch (tune) {
+      case 481: launch_pdl(4, decode_attention_kernel<128, 4, 8, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 482: launch_pdl(4, decode_attention_kernel<128, 4, 8, 2>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 381: launch_pdl(4, decode_attention_kernel<128, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 3101: launch_pdl(4, decode_attention_kernel<128, 3, 10, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 281: launch_pdl(4, decode_attention_kernel<128, 2, 8, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 2101: launch_pdl(4, decode_attention_kernel<128, 2, 10, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 2121: launch_pdl(4, decode_attention_kernel<128, 2, 12, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 361: launch_pdl(4, decode_attention_kernel<128, 3, 6, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 282: launch_pdl(4, decode_attention_kernel<128, 2, 8, 2>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
       case 41: ESP_V1(4, 1); break;
       case 410: ESP_V1(4, 10); break;
       case 38: ESP_V1(3, 8); break;
@@ -548,12 +583,15 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
       case 212: ESP_V1(2, 12); break;
       case 88: ESP_V1(8, 8); break;
       case 86: ESP_V1(8, 6); break;
-      default: ESP_V1(4, 8);
+      case 48: ESP_V1(4, 8); break;
+      default:
+        launch_pdl(4, decode_attention_kernel<128, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q,
+                   d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd);
     }
 #undef ESP_V1
   } else if (head_dim == 64) {
-    decode_attention_kernel<64><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads, sl2,
-                                                            part_o, part_ml, fc, pd);
+    decode_attention_kernel<64, 3, 8, 1><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads,
+                                                                     sl2, part_o, part_ml, fc, pd);
   } else {
     throw std::runtime_error("decode_attention: head_dim must be 64 or 128");
   }
