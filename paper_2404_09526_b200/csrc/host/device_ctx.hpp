@@ -57,7 +57,7 @@ struct DeviceCtx {
   // activations / scratch
   DevBuf x, xn, q, kb, vb, attn, h, logits, tok, pos, rinst, rslot, segs, work, last_rows,
       out_tok, chunks, row_start, part_o, part_ml, counts, result, kvrow, ret_rows, ret_slab,
-      ret_slot, qin, chunk_ids, row_list, combine_cnt;
+      ret_slot, qin, chunk_ids, row_list, combine_cnt, ss1, ss2;
   std::vector<void*> weight_allocs;
   std::vector<cudaEvent_t> sync_events;  // cross-domain event pool
   size_t sync_used = 0;

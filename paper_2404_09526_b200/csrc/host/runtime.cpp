@@ -187,7 +187,7 @@ Runtime::~Runtime() {
                       &dc.last_rows, &dc.out_tok, &dc.chunks, &dc.row_start, &dc.part_o,
                       &dc.part_ml, &dc.counts, &dc.result, &dc.kvrow, &dc.ret_rows,
                       &dc.ret_slab, &dc.ret_slot, &dc.qin, &dc.chunk_ids, &dc.row_list,
-                      &dc.combine_cnt};
+                      &dc.combine_cnt, &dc.ss1, &dc.ss2};
     for (DevBuf* b : bufs) {
       if (b->ptr) cudaFree(b->ptr);
     }
@@ -256,6 +256,11 @@ void Runtime::init_device(DeviceCtx& dc, const DeviceCtx* share) {
     k::fill_bf16(w.norm1, H, 1.0f, s);
     w.norm2 = alloc(H);
     k::fill_bf16(w.norm2, H, 1.0f, s);
+    // The two layer RMSNorm gains are folded into the projections that
+    // consume them (Wqkv·diag(γ1), Wgu·diag(γ2)); the layer norms then run
+    // with unit gain — as a kernel (prefill) or fused into the decode GEMMs.
+    k::scale_cols(w.wqkv, 3 * H, H, w.norm1, s);
+    k::scale_cols(w.wgu, 2 * F, H, w.norm2, s);
   }
   check_cuda("init weights");
   cuda_ok(cudaStreamSynchronize(s), "init weights sync");
@@ -588,7 +593,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
   const int n_work = attention_n_work(work);
   for (int l = 0; l < cfg_.layers; ++l) {
     const LayerW& w = dc.layers[l];
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, rows, H, cfg_.rms_eps, s); });
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
     // QKV projection; epilogue: RoPE, ring stripe write, and the proactive
     // retention write of every token's K/V into its resting page slot.
     k::GemmEpilogue ep;
@@ -620,7 +625,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
     eo.out = x;
     eo.ldo = H;
     timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, rows, H, cfg_.rms_eps, s); });
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = hbuf;
@@ -878,13 +883,31 @@ void Runtime::decode_step(const esp_decode_args& a) {
     cuda_ok(cudaMemsetAsync(d_cnt, 0, dc.combine_cnt.bytes, s), "memset");
   }
 
+  // Decode-shaped steps (<= 32 rows): each layer RMSNorm is fused into the
+  // skinny GEMMs — the residual epilogues accumulate row sums of squares
+  // (ss1 before QKV, ss2 before gate_up) and the consuming GEMM scales its
+  // accumulator rows (gains folded into the weights); no norm kernels.
+  const bool fuse_norm = rows <= 32 && std::getenv("ESP_DECODE_NORM_KERNEL") == nullptr;
+  float* ss1 = scratch<float>(dc.ss1, 32);
+  float* ss2 = scratch<float>(dc.ss2, 32);
+  if (fuse_norm) cuda_ok(cudaMemsetAsync(ss2, 0, 32 * sizeof(float), s), "memset");
+  const bf16* a_in = fuse_norm ? x : xn;  // the GEMMs' A operand after a norm
+
   cuda_ok(cudaEventRecord(dc.e0, s), "event");
-  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s); });
+  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s, fuse_norm ? ss1 : nullptr); });
   for (int l = 0; l < cfg_.layers; ++l) {
     const LayerW& w = dc.layers[l];
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, rows, H, cfg_.rms_eps, s); });
+    if (!fuse_norm) {
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
+    }
     k::GemmEpilogue ep;
     ep.kind = k::kEpiQkvRope;
+    if (fuse_norm) {
+      ep.ss_in = ss1;
+      ep.ss_zero = ss2;
+      ep.norm_dim = H;
+      ep.norm_eps = cfg_.rms_eps;
+    }
     ep.q_out = q;
     ep.pos = d_pos;
     ep.rope = dc.rope;
@@ -900,7 +923,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
       slabs.k[j] = ep.slab_k[j];
       slabs.v[j] = ep.slab_v[j];
     }
-    timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
+    timed(kPhQkv, s, [&] { k::gemm(a_in, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     if (b > 0 && fused_combine) {
       // Split-KV attention with the LSE combine fused (the last CTA of each
       // (row, head) merges the row's chunk partials).
@@ -929,17 +952,27 @@ void Runtime::decode_step(const esp_decode_args& a) {
     eo.kind = k::kEpiResidual;
     eo.out = x;
     eo.ldo = H;
+    if (fuse_norm) eo.ss_out = ss2;
     timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, rows, H, cfg_.rms_eps, s); });
+    if (!fuse_norm) {
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
+    }
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = hbuf;
     eg.ldo = F;
-    timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, rows, 2 * F, H, eg, s); });
+    if (fuse_norm) {
+      eg.ss_in = ss2;
+      eg.ss_zero = ss1;
+      eg.norm_dim = H;
+      eg.norm_eps = cfg_.rms_eps;
+    }
+    timed(kPhGateUp, s, [&] { k::gemm(a_in, H, w.wgu, H, rows, 2 * F, H, eg, s); });
     k::GemmEpilogue ed;
     ed.kind = k::kEpiResidual;
     ed.out = x;
     ed.ldo = H;
+    if (fuse_norm) ed.ss_out = ss1;
     timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s); });
   }
   // Output rows: the decode rows, then the chunk's last token when the chunk

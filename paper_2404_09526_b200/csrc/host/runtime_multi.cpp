@@ -332,7 +332,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       const LayerW& w = dc.layers[l];
       bf16* x = static_cast<bf16*>(dc.x.ptr);
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, p.rows, H, cfg_.rms_eps, s); });
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, p.rows, H, cfg_.rms_eps, s); });
       k::GemmEpilogue ep;
       ep.kind = k::kEpiQkvRope;
       ep.q_out = static_cast<bf16*>(dc.q.ptr);
@@ -437,7 +437,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       eo.out = x;
       eo.ldo = H;
       timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, p.rows, H, H, eo, s); });
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, p.rows, H, cfg_.rms_eps, s); });
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, p.rows, H, cfg_.rms_eps, s); });
       k::GemmEpilogue eg;
       eg.kind = k::kEpiSiluMul;
       eg.out = hbuf;
@@ -682,7 +682,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         const LayerW& w = dc.layers[l];
         bf16* x = static_cast<bf16*>(dc.x.ptr);
         bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, nl, H, cfg_.rms_eps, s); });
+        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
         k::GemmEpilogue ep;
         ep.kind = k::kEpiQkvRope;
         ep.q_out = static_cast<bf16*>(dc.q.ptr);
@@ -777,7 +777,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         eo.out = x;
         eo.ldo = H;
         timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, nl, H, H, eo, s); });
-        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, nl, H, cfg_.rms_eps, s); });
+        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
         k::GemmEpilogue eg;
         eg.kind = k::kEpiSiluMul;
         eg.out = hbuf;
@@ -806,7 +806,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
       const LayerW& w = dc.layers[l];
       bf16* x = static_cast<bf16*>(dc.x.ptr);
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm1, xn, nl, H, cfg_.rms_eps, s); });
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
       k::GemmEpilogue ep;
       ep.kind = k::kEpiQkvRope;
       ep.q_out = static_cast<bf16*>(dc.q.ptr);
@@ -911,7 +911,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
       eo.out = x;
       eo.ldo = H;
       timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, nl, H, H, eo, s); });
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, w.norm2, xn, nl, H, cfg_.rms_eps, s); });
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
       k::GemmEpilogue eg;
       eg.kind = k::kEpiSiluMul;
       eg.out = hbuf;

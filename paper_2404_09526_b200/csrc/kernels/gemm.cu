@@ -171,6 +171,15 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
           }
         }
         store_vals_bf16(dst, v);
+        if (ep.ss_out) {  // sum of squares of the stored (bf16) row slice
+          float ss = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float b = __bfloat162float(__float2bfloat16_rn(v[i]));
+            ss = fmaf(b, b, ss);
+          }
+          atomicAdd(ep.ss_out + m, ss);
+        }
       }
     }
   } else if (ep.kind == kEpiSiluMul) {
@@ -533,12 +542,23 @@ struct RowAcc {  // one fp32 row in shared memory
 // shared memory. Store / residual / fp32 kinds: four threads per row, 32
 // columns each (independent global reads in flight); the kinds that pair
 // columns 64 apart (SiLU gate/up, RoPE halves) run one thread per row.
-__device__ __forceinline__ void swap_epilogue(const GemmEpilogue& ep, const float* sT, int M,
+__device__ __forceinline__ void swap_epilogue(const GemmEpilogue& ep, float* sT, int M,
                                               int t, int tile, int N) {
+  // Fused RMSNorm: row m of the accumulator (W·diag(γ)·x_m) times
+  // rsqrt(mean(x_m²) + ε); each thread scales the slice it then reads.
+  auto scale_rows = [&](int m, int c0, int n) {
+    if (ep.ss_in == nullptr) return;
+    const float inv = rsqrtf(__ldcg(ep.ss_in + m) / static_cast<float>(ep.norm_dim) + ep.norm_eps);
+    for (int c = c0; c < c0 + n; ++c) sT[m * 128 + c] *= inv;
+  };
   if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32) {
     const int m = t >> 2, j = t & 3;
-    if (m < M) epilogue_tile<32>(ep, RowAcc{sT + m * 128 + j * 32}, m, true, tile * 4 + j, N);
+    if (m < M) {
+      scale_rows(m, j * 32, 32);
+      epilogue_tile<32>(ep, RowAcc{sT + m * 128 + j * 32}, m, true, tile * 4 + j, N);
+    }
   } else if (t < M) {
+    scale_rows(t, 0, 128);
     epilogue_tile<128>(ep, RowAcc{sT + t * 128}, t, true, tile, N);
   }
 }
@@ -685,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::griddep_wait();  // residual / outputs are the previous kernels' data
     const uint32_t quad = warp & 3;
     const int t = static_cast<int>(quad * 32 + lane);  // output column of the tile
+    if (ep.ss_zero != nullptr && blockIdx.x == 0 && t < 32) ep.ss_zero[t] = 0.f;
     int lt = 0;
     for (; work.get(tile, kb0, kb1); ++lt) {
       const int acc = lt & 1;
@@ -1192,6 +1213,10 @@ StreamKWs streamk_workspace(size_t elems, size_t tiles, cudaStream_t s) {
 void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
           const GemmEpilogue& ep, cudaStream_t s) {
   if (M <= 0) return;
+  if ((ep.ss_in != nullptr || ep.ss_zero != nullptr) &&
+      (M > 32 || getenv("ESP_GEMM_SKINNY_OLD") != nullptr)) {
+    throw std::runtime_error("gemm: the fused RMSNorm needs the skinny (M <= 32) kernel");
+  }
   if (N % 128 != 0 || K % 64 != 0) throw std::runtime_error("gemm: N%128 or K%64 != 0");
   if (M <= 32) {
     // Decode-shaped: weight-streaming bound. Skinny pipeline, stream-K over

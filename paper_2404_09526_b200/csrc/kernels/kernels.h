@@ -52,6 +52,17 @@ struct GemmEpilogue {
   const int32_t* q_rows = nullptr;
   int n_qpeer = 0;
   bf16* q_peer[kMaxPeers] = {};
+  // RMSNorm fused across decode GEMMs (skinny swap kernel only): a residual
+  // epilogue adds each stored row's sum of squares into ss_out[m]; a
+  // consumer GEMM (A = the un-normalised x, norm gain folded into its
+  // weights) scales row m of its accumulator by rsqrt(ss_in[m]/norm_dim +
+  // norm_eps); ss_zero[0..31] is cleared by the kernel (the buffer the next
+  // residual GEMM accumulates into — its readers have completed).
+  float* ss_out = nullptr;
+  const float* ss_in = nullptr;
+  float* ss_zero = nullptr;
+  int norm_dim = 0;
+  float norm_eps = 0.f;
 };
 
 // D[M x N] = A[M x K] . B[N x K]^T with the epilogue above. A and B are
@@ -174,8 +185,9 @@ void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slo
                  bf16* out_k, bf16* out_v, int hidden, cudaStream_t s);
 
 // ---- small fused ops --------------------------------------------------------
+// ss != null: also stores each row's sum of squares (fused-RMSNorm input).
 void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,
-           cudaStream_t s);
+           cudaStream_t s, float* ss = nullptr);
 // y[r] = rmsnorm(x[src_row[r] or r]) * gamma
 void rmsnorm(const bf16* x, const int32_t* src_rows, const bf16* gamma, bf16* y, int rows,
              int hidden, float eps, cudaStream_t s);
@@ -184,6 +196,8 @@ void rope_table(float2* table, int max_pos, int head_dim, float theta, cudaStrea
 void init_weight(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor, int layer,
                  int layout, cudaStream_t s);
 void fill_bf16(bf16* dst, int64_t n, float v, cudaStream_t s);
+// w[r][c] *= gamma[c] (fold a norm gain into the consuming projection).
+void scale_cols(bf16* w, int64_t rows, int64_t cols, const bf16* gamma, cudaStream_t s);
 // Page-table conservation: counts how often each slot appears (atomic).
 void count_slots(const int32_t* slots, int64_t n, int32_t* counts, int capacity,
                  cudaStream_t s);

@@ -29,13 +29,47 @@ bool pdl_enabled(int cls) {
 namespace {
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __restrict__ table,
-                             bf16* __restrict__ x, int hidden) {
+                             bf16* __restrict__ x, int hidden, float* __restrict__ ss) {
   ptx::griddep_wait();
   ptx::griddep_launch();
   const int r = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<int64_t>(tokens[r]) * hidden);
   uint4* dst = reinterpret_cast<uint4*>(x + static_cast<int64_t>(r) * hidden);
-  for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) dst[i] = src[i];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) {
+    const uint4 v = src[i];
+    dst[i] = v;
+    if (ss) {
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(p[j]);
+        acc += f.x * f.x + f.y * f.y;
+      }
+    }
+  }
+  if (ss) {  // the row's sum of squares, for the RMSNorm fused into the next GEMM
+    __shared__ float red[32];
+    for (int w = 16; w >= 1; w >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, w);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[i];
+      ss[r] = t;
+    }
+  }
+}
+
+// W[r][c] *= gamma[c]: a layer RMSNorm's gain folded into the projection
+// that consumes its output (x·diag(γ)·Wᵀ = x·(W·diag(γ))ᵀ).
+__global__ void scale_cols_kernel(bf16* __restrict__ w, int64_t rows, int64_t cols,
+                                  const bf16* __restrict__ gamma) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    w[i] = __float2bfloat16_rn(__bfloat162float(w[i]) * __bfloat162float(gamma[i % cols]));
+  }
 }
 
 __global__ void rmsnorm_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ src_rows,
@@ -70,7 +104,10 @@ __global__ void rmsnorm_kernel(const bf16* __restrict__ x, const int32_t* __rest
   bf16* yr = y + static_cast<int64_t>(r) * hidden;
   for (int i = threadIdx.x * 8; i < hidden; i += blockDim.x * 8) {
     const uint4 v = *reinterpret_cast<const uint4*>(xr + i);
-    const uint4 g = *reinterpret_cast<const uint4*>(gamma + i);
+    // gamma == null: unit gain (a layer norm whose gain is folded into the
+    // following projection's weights)
+    const uint4 g = gamma ? *reinterpret_cast<const uint4*>(gamma + i)
+                          : make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
     const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
     const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&g);
     uint4 o;
@@ -213,9 +250,9 @@ __global__ void copy_slots_kernel(const bf16* __restrict__ sk, const bf16* __res
 }  // namespace
 
 void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,
-           cudaStream_t s) {
+           cudaStream_t s, float* ss) {
   if (rows <= 0) return;
-  launch_pdl(2, embed_kernel, dim3(rows), dim3(128), 0, s, tokens, table, x, hidden);
+  launch_pdl(2, embed_kernel, dim3(rows), dim3(128), 0, s, tokens, table, x, hidden, ss);
   count_launch();
 }
 
@@ -244,6 +281,11 @@ void rope_table(float2* table, int max_pos, int head_dim, float theta, cudaStrea
 void init_weight(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor, int layer,
                  int layout, cudaStream_t s) {
   init_weight_kernel<<<4096, 256, 0, s>>>(dst, rows, cols, seed, tensor, layer, layout);
+  count_launch();
+}
+
+void scale_cols(bf16* w, int64_t rows, int64_t cols, const bf16* gamma, cudaStream_t s) {
+  scale_cols_kernel<<<2048, 256, 0, s>>>(w, rows, cols, gamma);
   count_launch();
 }
 
