@@ -532,8 +532,9 @@ void Runtime::prefill(const esp_prefill_args& a) {
           "h2d");
 
   bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(rows) * H);
+  float* ss1 = fuse_norm_prefill() ? scratch<float>(dc.ss1, rows) : nullptr;
   cuda_ok(cudaEventRecord(dc.e0, s), "event");
-  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s); });
+  timed(kPhEmbed, s, [&] { k::embed(d_tok, dc.embed, x, rows, H, s, ss1); });
   forward_layers_prefill(dc, rows, segs, work_sorted);
 
   // Last prompt token of each request: position len-1 lives at ring position
@@ -591,9 +592,19 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
   bf16* hbuf = scratch<bf16>(dc.h, static_cast<size_t>(rows) * F);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
   const int n_work = attention_n_work(work);
+  // RMSNorm fused into the GEMMs (gains folded into the weights): the
+  // residual epilogues (and embed) accumulate each row's sum of squares, the
+  // consuming GEMM scales its accumulator rows. ss2 / ss1 are cleared before
+  // the residual GEMM that fills them (their readers have completed).
+  const bool fuse = fuse_norm_prefill();
+  float* ss1 = fuse ? scratch<float>(dc.ss1, rows) : nullptr;
+  float* ss2 = fuse ? scratch<float>(dc.ss2, rows) : nullptr;
+  const bf16* a_in = fuse ? x : xn;
   for (int l = 0; l < cfg_.layers; ++l) {
     const LayerW& w = dc.layers[l];
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
+    if (!fuse) {
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
+    }
     // QKV projection; epilogue: RoPE, ring stripe write, and the proactive
     // retention write of every token's K/V into its resting page slot.
     k::GemmEpilogue ep;
@@ -612,7 +623,12 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
       ep.slab_k[j] = in.layer_k(l);
       ep.slab_v[j] = in.layer_v(l);
     }
-    timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
+    if (fuse) {
+      ep.ss_in = ss1;
+      ep.norm_dim = H;
+      ep.norm_eps = cfg_.rms_eps;
+    }
+    timed(kPhQkv, s, [&] { k::gemm(a_in, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     // Striped ring attention over all d rounds.
     timed(kPhAttention, s, [&] {
       k::ring_attention_variant(attn_variant_, q, kb, vb, attn, rows, rows, cfg_.heads,
@@ -624,17 +640,32 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
     eo.kind = k::kEpiResidual;
     eo.out = x;
     eo.ldo = H;
+    if (fuse) {
+      eo.ss_out = ss2;
+      cuda_ok(cudaMemsetAsync(ss2, 0, static_cast<size_t>(rows) * sizeof(float), s), "memset");
+    }
     timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
-    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
+    if (!fuse) {
+      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
+    }
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = hbuf;
     eg.ldo = F;
-    timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, rows, 2 * F, H, eg, s); });
+    if (fuse) {
+      eg.ss_in = ss2;
+      eg.norm_dim = H;
+      eg.norm_eps = cfg_.rms_eps;
+    }
+    timed(kPhGateUp, s, [&] { k::gemm(a_in, H, w.wgu, H, rows, 2 * F, H, eg, s); });
     k::GemmEpilogue ed;
     ed.kind = k::kEpiResidual;
     ed.out = x;
     ed.ldo = H;
+    if (fuse) {
+      ed.ss_out = ss1;
+      cuda_ok(cudaMemsetAsync(ss1, 0, static_cast<size_t>(rows) * sizeof(float), s), "memset");
+    }
     timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s); });
   }
 }

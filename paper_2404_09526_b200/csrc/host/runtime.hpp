@@ -131,6 +131,8 @@ class Runtime {
   };
   void decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows,
                     const std::vector<RequestId>& batch);
+  // RMSNorm fused into the single-domain prefill GEMMs (ESP_PREFILL_NORM_KERNEL=1: kernels).
+  static bool fuse_norm_prefill() { return std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr; }
   void forward_layers_prefill(DeviceCtx& dc, int rows, const std::vector<k::RingSegment>& segs,
                               const std::vector<int32_t>& work);
   template <typename T>

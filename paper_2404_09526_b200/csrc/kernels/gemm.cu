@@ -130,10 +130,21 @@ struct SegSumAcc {
   __device__ __forceinline__ void wait() const {}
 };
 
+// Fused RMSNorm (GemmEpilogue.ss_in): the accumulator row m is W·diag(γ)·x_m
+// and is scaled by rsqrt(mean(x_m²) + ε) as it is read.
+__device__ __forceinline__ void scale32(uint32_t (&r)[32], float inv) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * inv);
+}
+
 template <int BN, typename Acc>
 __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc& acc, int m,
                                               bool valid, int nb, int N) {
   uint32_t r[32];
+  const bool norm = ep.ss_in != nullptr && valid;
+  const float inv =
+      norm ? rsqrtf(__ldcg(ep.ss_in + m) / static_cast<float>(ep.norm_dim) + ep.norm_eps) : 1.f;
+  float ss_acc = 0.f;  // kEpiResidual with ss_out: this tile row's sum of squares
   if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32 ||
       ep.kind == kEpiAtomicF32) {
 #pragma unroll 1
@@ -141,6 +152,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
       acc.load(c, r);
       acc.wait();
       if (!valid) continue;
+      if (norm) scale32(r, inv);
       const int64_t off = static_cast<int64_t>(m) * ep.ldo + nb * BN + c;
       if (ep.kind == kEpiAtomicF32) {
         float* d = static_cast<float*>(ep.out) + off;
@@ -172,16 +184,15 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
         }
         store_vals_bf16(dst, v);
         if (ep.ss_out) {  // sum of squares of the stored (bf16) row slice
-          float ss = 0.f;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float b = __bfloat162float(__float2bfloat16_rn(v[i]));
-            ss = fmaf(b, b, ss);
+            ss_acc = fmaf(b, b, ss_acc);
           }
-          atomicAdd(ep.ss_out + m, ss);
         }
       }
     }
+    if (ep.ss_out && valid && ep.kind == kEpiResidual) atomicAdd(ep.ss_out + m, ss_acc);
   } else if (ep.kind == kEpiSiluMul) {
     // Physical rows of the gate_up weight come in 128-row blocks: 64 gate
     // rows then the 64 matching up rows.
@@ -194,6 +205,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
         acc.load(p * 128 + 64 + c, u);
         acc.wait();
         if (!valid) continue;
+        if (norm) {
+          scale32(r, inv);
+          scale32(u, inv);
+        }
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -236,6 +251,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
         acc.load(c, r);
         acc.wait();
         if (!valid) continue;
+        if (norm) scale32(r, inv);
         if (dst_main) store_row_bf16(dst_main + row_off + col0 + c, r);
         if (dst_slab) store_row_bf16(dst_slab + col0 + c, r);
         for (int pr = 0; pr < ep.n_peer; ++pr) store_row_bf16(ep.v_peer[pr] + row_off + col0 + c, r);
@@ -251,6 +267,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
           acc.load(hb + j + half, h);
           acc.wait();
           if (!valid) continue;
+          if (norm) {
+            scale32(r, inv);
+            scale32(h, inv);
+          }
           float lo[32], hi[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
@@ -544,21 +564,10 @@ struct RowAcc {  // one fp32 row in shared memory
 // columns 64 apart (SiLU gate/up, RoPE halves) run one thread per row.
 __device__ __forceinline__ void swap_epilogue(const GemmEpilogue& ep, float* sT, int M,
                                               int t, int tile, int N) {
-  // Fused RMSNorm: row m of the accumulator (W·diag(γ)·x_m) times
-  // rsqrt(mean(x_m²) + ε); each thread scales the slice it then reads.
-  auto scale_rows = [&](int m, int c0, int n) {
-    if (ep.ss_in == nullptr) return;
-    const float inv = rsqrtf(__ldcg(ep.ss_in + m) / static_cast<float>(ep.norm_dim) + ep.norm_eps);
-    for (int c = c0; c < c0 + n; ++c) sT[m * 128 + c] *= inv;
-  };
   if (ep.kind == kEpiStore || ep.kind == kEpiResidual || ep.kind == kEpiStoreF32) {
     const int m = t >> 2, j = t & 3;
-    if (m < M) {
-      scale_rows(m, j * 32, 32);
-      epilogue_tile<32>(ep, RowAcc{sT + m * 128 + j * 32}, m, true, tile * 4 + j, N);
-    }
+    if (m < M) epilogue_tile<32>(ep, RowAcc{sT + m * 128 + j * 32}, m, true, tile * 4 + j, N);
   } else if (t < M) {
-    scale_rows(t, 0, 128);
     epilogue_tile<128>(ep, RowAcc{sT + t * 128}, t, true, tile, N);
   }
 }
@@ -1213,9 +1222,8 @@ StreamKWs streamk_workspace(size_t elems, size_t tiles, cudaStream_t s) {
 void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
           const GemmEpilogue& ep, cudaStream_t s) {
   if (M <= 0) return;
-  if ((ep.ss_in != nullptr || ep.ss_zero != nullptr) &&
-      (M > 32 || getenv("ESP_GEMM_SKINNY_OLD") != nullptr)) {
-    throw std::runtime_error("gemm: the fused RMSNorm needs the skinny (M <= 32) kernel");
+  if (ep.ss_zero != nullptr && (M > 32 || getenv("ESP_GEMM_SKINNY_OLD") != nullptr)) {
+    throw std::runtime_error("gemm: ss_zero is implemented by the skinny (M <= 32) kernel");
   }
   if (N % 128 != 0 || K % 64 != 0) throw std::runtime_error("gemm: N%128 or K%64 != 0");
   if (M <= 32) {
