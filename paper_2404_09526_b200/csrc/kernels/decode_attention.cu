@@ -82,8 +82,8 @@ __device__ __forceinline__ void combine_row_head(const float* part_o, const floa
   }
 }
 
-template <int HD, int UNR = kUnroll, int MINB = 1, int PF = 0>
-__global__ void __launch_bounds__(kWarps * 32, MINB)
+template <int HD, int UNR = kUnroll, int MINB = 1, int PF = 0, int W = kWarps>
+__global__ void __launch_bounds__(W * 32, MINB)
     decode_attention_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
                             const DecodeSlabs slabs, int heads, float scale_log2,
                             float* __restrict__ part_o, float* __restrict__ part_ml,
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   const bf16* vb = pick(slabs.v, ch.slab) + head * HD + dl * 8;
   float m = -INFINITY, l = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
-  const int step = kWarps * TPW;
+  const int step = W * TPW;
   // PF: the next iteration's slot ids are loaded one iteration ahead (no
   // index -> data dependency on the critical path) and, with PF == 2, their
   // K/V lines are prefetched into L2.
@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     m = mm;
   }
   // Merge warps through shared memory.
-  __shared__ float sm_m[kWarps], sm_l[kWarps];
-  __shared__ float sm_o[kWarps][HD];
+  __shared__ float sm_m[W], sm_l[W];
+  __shared__ float sm_o[W][HD];
   if (sub == 0) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) sm_o[warp][dl * 8 + e] = o[e];
@@ -214,10 +214,10 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   for (int d = threadIdx.x; d < HD; d += blockDim.x) {
     float mm = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) mm = fmaxf(mm, sm_m[w]);
+    for (int w = 0; w < W; ++w) mm = fmaxf(mm, sm_m[w]);
     float acc = 0.f, ll = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < W; ++w) {
       const float c = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - mm);
       acc += c * sm_o[w][d];
       ll += c * sm_l[w];
@@ -570,6 +570,10 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
       case 2101: launch_pdl(4, decode_attention_kernel<128, 2, 10, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
       case 2121: launch_pdl(4, decode_attention_kernel<128, 2, 12, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
       case 361: launch_pdl(4, decode_attention_kernel<128, 3, 6, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 3418: launch_pdl(4, decode_attention_kernel<128, 3, 4, 1, 8>, grid, dim3(8 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 2418: launch_pdl(4, decode_attention_kernel<128, 2, 4, 1, 8>, grid, dim3(8 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 31612: launch_pdl(4, decode_attention_kernel<128, 3, 16, 1, 2>, grid, dim3(2 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
+      case 3518: launch_pdl(4, decode_attention_kernel<128, 3, 5, 1, 8>, grid, dim3(8 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
       case 282: launch_pdl(4, decode_attention_kernel<128, 2, 8, 2>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
       case 41: ESP_V1(4, 1); break;
       case 410: ESP_V1(4, 10); break;
