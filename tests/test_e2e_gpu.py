@@ -345,3 +345,52 @@ def test_disagg_baseline_tiny():
     for r, lgs in rec.logits.items():
         toks = [int(np.argmax(l)) for l in lgs]
         check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)
+
+
+def test_config4_multi_master_decode_tiny(transport):
+    """BASELINE config 4 (hand-built decode state of test_scheduler.cpp:71-99):
+    16 requests x 65,536-token contexts, each spread 16,384 per instance over
+    a 4-of-8 group; the reference's three decode steps (masters [0,1], then
+    [2,3], then scale-up 4->5 with master [4]) replayed with real kernels on
+    the tiny model (the LWM-7B KV of this state, 512 GiB, needs 8 GPUs). Page
+    tables equal the engine's at every step; every step's logits equal those
+    of the same requests decoded on ONE instance with ONE master (split-KV
+    over 4-5 instances + multi-master LSE combine == dense), teacher-forced."""
+    if transport == "domain_copy":
+        pytest.skip("8 domains x 64K-token activations: covered co-located and with push")
+    path = os.path.join(GOLD, "scenario_config4_decode.jsonl")
+    head, _, _ = replay.load(path)
+    n = head["requests"][0]["input_len"]
+    prompts = {r["id"]: replay.prompt_tokens(r["id"], n) for r in head["requests"]}
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+                     kv_capacity=head["kv_capacity"])
+    firsts = {}
+    for r in head["requests"]:
+        first, _, _ = rt.prefill([r["id"]], [n], [i for i, _ in r["placement"]],
+                                 [[tuple(x) for x in r["placement"]]], tokens=prompts[r["id"]])
+        firsts[r["id"]] = int(first[0])
+    steps = []
+
+    def on_decode(d, members):
+        out, lg, _ = rt.decode_step(members, d["masters"], d["batch"], want_logits=True)
+        steps.append((list(d["batch"]), out.copy(), lg))
+
+    replay.replay(rt, path, on_decode=on_decode)
+    rt.check_conservation()
+    assert len(steps) == 3
+    rt.close()
+    del rt
+    # the dense reference: the same requests on one instance, one master
+    ref = abi.Runtime(abi.TINY, 1, devices=[0], kv_capacity=len(prompts) * (n + 8))
+    for r, p in prompts.items():
+        ref.prefill([r], [n], [0], [[(0, n)]], tokens=p)
+    prev = None
+    for batch, out, lg in steps:
+        ins = [firsts[r] for r in batch] if prev is None else [prev[r] for r in batch]
+        rout, rlg, _ = ref.decode_step([0], [0], batch, in_tokens=ins, want_logits=True)
+        for i, r in enumerate(batch):
+            err = np.abs(lg[i] - rlg[i]).max() / (np.abs(rlg[i]).max() + 1e-6)
+            assert err < LOGIT_TOL, (r, err)
+            gap = rlg[i].max() - rlg[i][out[i]]
+            assert out[i] == rout[i] or gap < TIE_GAP, (r, out[i], rout[i], gap)
+        prev = {r: int(out[i]) for i, r in enumerate(batch)}
