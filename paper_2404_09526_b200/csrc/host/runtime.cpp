@@ -793,11 +793,29 @@ void Runtime::decode_step(const esp_decode_args& a) {
     return;
   }
   if (single_domain(involved) == nullptr) {
-    if (has_chunk) {
-      throw ConfigError("chunked prefill across transport domains is not supported; "
-                        "co-locate the chunked group's instances");
+    double ms_dec = 0, ms_chunk = 0;
+    if (b > 0) {
+      esp_decode_args da = a;
+      da.device_ms_out = &ms_dec;
+      decode_multi(da, rows_v, batch);
     }
-    decode_multi(a, rows_v, batch);
+    if (has_chunk) {
+      if (instances_.size() > static_cast<size_t>(k::kMaxSlabs)) {
+        throw ConfigError("chunked prefill across domains needs <= 16 instances");
+      }
+      std::vector<std::pair<InstanceId, int32_t>> prev, cur;
+      const RequestRec& rr = requests_[a.chunk_request];
+      // earlier tokens: every slot of the request except the chunk's own
+      std::map<InstanceId, size_t> own;
+      for (size_t i = 0; i < ch_inst.size(); ++i) own[ch_inst[i]]++;
+      for (const auto& [iid, pl] : rr.pages) {
+        const size_t keep = pl.slots.size() - (own.count(iid) ? own[iid] : 0);
+        for (size_t j = 0; j < keep; ++j) prev.emplace_back(iid, pl.slots[j]);
+      }
+      for (size_t i = 0; i < ch_inst.size(); ++i) cur.emplace_back(ch_inst[i], ch_slot[i]);
+      chunk_multi(a, p_prev, prev, cur, &ms_chunk);
+    }
+    if (a.device_ms_out) *a.device_ms_out = ms_dec + ms_chunk;
     return;
   }
   DeviceCtx& dc = device_of(involved, "decode_step");

@@ -129,6 +129,12 @@ class Runtime {
     InstanceId master;
     int32_t token, pos, slot;
   };
+  // A chunked-prefill chunk whose request's KV spans transport domains: the
+  // chunk rows run in the domain of the chunk's first instance; K/V go to
+  // their page slots by (peer) stores, earlier KV is gathered by (peer) loads.
+  void chunk_multi(const esp_decode_args& a, int64_t p_prev,
+                   const std::vector<std::pair<InstanceId, int32_t>>& prev,
+                   const std::vector<std::pair<InstanceId, int32_t>>& chunk_slots, double* ms);
   void decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows,
                     const std::vector<RequestId>& batch);
   // RMSNorm fused into the single-domain prefill GEMMs (ESP_PREFILL_NORM_KERNEL=1: kernels).

@@ -521,6 +521,144 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
 }
 
 // ---- decode ------------------------------------------------------------------------
+void Runtime::chunk_multi(const esp_decode_args& a, int64_t p_prev,
+                          const std::vector<std::pair<InstanceId, int32_t>>& prev,
+                          const std::vector<std::pair<InstanceId, int32_t>>& chunk_slots,
+                          double* ms_out) {
+  const int c = static_cast<int>(a.chunk_tokens);
+  const int H = cfg_.hidden, F = cfg_.ffn;
+  DeviceCtx& dc = *devices_[static_cast<size_t>(inst(chunk_slots.front().first).domain)];
+  DeviceGuard g(dc.device);
+  cudaStream_t s = dc.stream;
+  const int kv_n = static_cast<int>(p_prev) + c;
+  // Rows: the chunk's tokens. K/V rest in page slots addressed by GLOBAL
+  // instance id (slab pointers of every instance; remote ones are peer
+  // memory over NVLink). Gather list: earlier tokens, then the chunk's own.
+  std::vector<int32_t> tok(a.chunk_token_ids, a.chunk_token_ids + c), pos, rinst, rslot, gi, gs;
+  for (int i = 0; i < c; ++i) {
+    pos.push_back(static_cast<int32_t>(p_prev + i));
+    rinst.push_back(chunk_slots[static_cast<size_t>(i)].first);
+    rslot.push_back(chunk_slots[static_cast<size_t>(i)].second);
+  }
+  for (const auto& [i, sl] : prev) {
+    gi.push_back(i);
+    gs.push_back(sl);
+  }
+  gi.insert(gi.end(), rinst.begin(), rinst.end());
+  gs.insert(gs.end(), rslot.begin(), rslot.end());
+  ensure_rope(dc, p_prev + c);
+  h2d(scratch<int32_t>(dc.tok, c), tok, s);
+  h2d(scratch<int32_t>(dc.pos, c), pos, s);
+  h2d(scratch<int32_t>(dc.rinst, c), rinst, s);
+  h2d(scratch<int32_t>(dc.rslot, c), rslot, s);
+  int32_t* d_gi = scratch<int32_t>(dc.ret_slab, kv_n);
+  int32_t* d_gs = scratch<int32_t>(dc.ret_slot, kv_n);
+  h2d(d_gi, gi, s);
+  h2d(d_gs, gs, s);
+  k::RingSegment sg{};
+  sg.q_row0 = 0;
+  sg.q_len = c;
+  sg.n_rounds = 1;
+  sg.kv_row0[0] = 0;
+  sg.kv_len[0] = kv_n;
+  sg.shift[0] = -static_cast<int32_t>(p_prev);
+  std::vector<int32_t> work;
+  build_attention_work({sg}, cfg_.heads, attn_pairs_, kv_n, cfg_.head_dim, work);
+  k::RingSegment* d_seg = scratch<k::RingSegment>(dc.segs, 1);
+  cuda_ok(cudaMemcpyAsync(d_seg, &sg, sizeof(sg), cudaMemcpyHostToDevice, s), "h2d");
+  h2d(scratch<int32_t>(dc.work, work.size()), work, s);
+  const int n_work = attention_n_work(work);
+  bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(c) * H);
+  bf16* xn = scratch<bf16>(dc.xn, static_cast<size_t>(c) * H);
+  bf16* q = scratch<bf16>(dc.q, static_cast<size_t>(c) * H);
+  bf16* attn = scratch<bf16>(dc.attn, static_cast<size_t>(c) * H);
+  bf16* hbuf = scratch<bf16>(dc.h, static_cast<size_t>(c) * F);
+  bf16* kg = scratch<bf16>(dc.kb, static_cast<size_t>(kv_n) * H);
+  bf16* vg = scratch<bf16>(dc.vb, static_cast<size_t>(kv_n) * H);
+  const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
+  cudaEvent_t t0, t1;
+  cuda_ok(cudaEventCreate(&t0), "event");
+  cuda_ok(cudaEventCreate(&t1), "event");
+  cuda_ok(cudaEventRecord(t0, s), "event");
+  k::embed(static_cast<int32_t*>(dc.tok.ptr), dc.embed, x, c, H, s);
+  for (int l = 0; l < cfg_.layers; ++l) {
+    const LayerW& w = dc.layers[l];
+    k::rmsnorm(x, nullptr, nullptr, xn, c, H, cfg_.rms_eps, s);
+    k::GemmEpilogue ep;
+    ep.kind = k::kEpiQkvRope;
+    ep.q_out = q;
+    ep.pos = static_cast<int32_t*>(dc.pos.ptr);
+    ep.rope = dc.rope;
+    ep.hidden = H;
+    ep.head_dim = cfg_.head_dim;
+    ep.row_inst = static_cast<int32_t*>(dc.rinst.ptr);  // global instance ids
+    ep.row_slot = static_cast<int32_t*>(dc.rslot.ptr);
+    k::DecodeSlabs slabs{};
+    for (size_t j = 0; j < instances_.size(); ++j) {
+      ep.slab_k[j] = instances_[j].layer_k(l);
+      ep.slab_v[j] = instances_[j].layer_v(l);
+      slabs.k[j] = ep.slab_k[j];
+      slabs.v[j] = ep.slab_v[j];
+    }
+    k::gemm(xn, H, w.wqkv, H, c, 3 * H, H, ep, s);
+    k::gather_rows(slabs, d_gi, d_gs, kv_n, kg, vg, H, s);
+    k::ring_attention_variant(attn_variant_, q, kg, vg, attn, c, kv_n, cfg_.heads, cfg_.head_dim,
+                              d_seg, 1, static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
+    k::GemmEpilogue eo;
+    eo.kind = k::kEpiResidual;
+    eo.out = x;
+    eo.ldo = H;
+    k::gemm(attn, H, w.wo, H, c, H, H, eo, s);
+    k::rmsnorm(x, nullptr, nullptr, xn, c, H, cfg_.rms_eps, s);
+    k::GemmEpilogue eg;
+    eg.kind = k::kEpiSiluMul;
+    eg.out = hbuf;
+    eg.ldo = F;
+    k::gemm(xn, H, w.wgu, H, c, 2 * F, H, eg, s);
+    k::GemmEpilogue ed;
+    ed.kind = k::kEpiResidual;
+    ed.out = x;
+    ed.ldo = H;
+    k::gemm(hbuf, F, w.wd, F, c, H, F, ed, s);
+  }
+  int32_t first = -1;
+  std::vector<float> lg;
+  if (a.chunk_final) {
+    const int32_t last = c - 1;
+    int32_t* d_last = scratch<int32_t>(dc.last_rows, 1);
+    cuda_ok(cudaMemcpyAsync(d_last, &last, 4, cudaMemcpyHostToDevice, s), "h2d");
+    k::rmsnorm(x, d_last, dc.final_norm, xn, 1, H, cfg_.rms_eps, s);
+    float* logits = scratch<float>(dc.logits, cfg_.vocab);
+    k::GemmEpilogue ef;
+    ef.kind = k::kEpiStoreF32;
+    ef.out = logits;
+    ef.ldo = cfg_.vocab;
+    k::gemm(xn, H, dc.lm_head, H, 1, cfg_.vocab, H, ef, s);
+    int32_t* d_out = scratch<int32_t>(dc.out_tok, 1);
+    k::argmax_rows(logits, 1, cfg_.vocab, d_out, s);
+    cuda_ok(cudaMemcpyAsync(&first, d_out, 4, cudaMemcpyDeviceToHost, s), "d2h");
+    if (a.chunk_logits_out) {
+      lg.resize(static_cast<size_t>(cfg_.vocab));
+      cuda_ok(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    }
+  }
+  cuda_ok(cudaEventRecord(t1, s), "event");
+  check_cuda("chunk (multi-domain) launch");
+  cuda_ok(cudaStreamSynchronize(s), "chunk");
+  float ms = 0;
+  cuda_ok(cudaEventElapsedTime(&ms, t0, t1), "elapsed");
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (ms_out) *ms_out = ms;
+  if (a.chunk_final) {
+    requests_[a.chunk_request].tokens.push_back(first);
+    if (a.chunk_first_token_out) *a.chunk_first_token_out = first;
+    if (a.chunk_logits_out) std::memcpy(a.chunk_logits_out, lg.data(), lg.size() * sizeof(float));
+  } else if (a.chunk_first_token_out) {
+    *a.chunk_first_token_out = -1;
+  }
+}
+
 void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows_v,
                            const std::vector<RequestId>& batch) {
   const int b = static_cast<int>(rows_v.size());
