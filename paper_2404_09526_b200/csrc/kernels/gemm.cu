@@ -313,6 +313,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
 struct WorkRange {
   int next, end, num_k, stride;
   bool stream;
+  int sub_lo = -1, sub_hi = -1;  // strided tiles, each over K blocks [sub_lo, sub_hi)
   __device__ WorkRange(int tiles, int num_k_, int kb_per_cta) : num_k(num_k_) {
     stream = kb_per_cta > 0;
     if (stream) {
@@ -334,8 +335,8 @@ struct WorkRange {
       next += kb1 - kb0;
     } else {
       tile = next;
-      kb0 = 0;
-      kb1 = num_k;
+      kb0 = sub_lo >= 0 ? sub_lo : 0;
+      kb1 = sub_lo >= 0 ? sub_hi : num_k;
       next += stride;
     }
     return true;
@@ -598,11 +599,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* pair_bar = tempty + 2;  // [0] partial ready (rank 0), [1] partial consumed (rank 1)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pair_bar + 2);
   volatile uint32_t* last_flag = tmem_slot + 1;
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   if (warp == 0 && lane == 0) {
+    ptx::mbar_init(&pair_bar[0], 1);
+    ptx::mbar_init(&pair_bar[1], 1);
     ptx::tma_prefetch_desc(&tmX);
     ptx::tma_prefetch_desc(&tmW);
     for (int s = 0; s < S; ++s) {
@@ -618,12 +622,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (SPLIT == -2) ptx::cluster_sync();  // the peer's barriers are initialised
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (tr && threadIdx.x == 0) tr[1] = gtime();
 
   const int num_n = N / 128, num_k = K / BK;
   WorkRange work(num_n, num_k, kb_per_cta);
+  if constexpr (SPLIT == -2) {
+    // Persistent pair split: cluster c of a 2-CTA grid walks tiles c,
+    // c + nclusters, ...; rank r covers K blocks [r, r+1) * num_k / 2 of each.
+    // Balances tile counts that do not divide the SM count (gate_up: 172
+    // tiles on 148 SMs -> at most 1.5 tiles of weights per SM instead of 2).
+    const int r = static_cast<int>(blockIdx.x) & 1;
+    work.next = static_cast<int>(blockIdx.x) >> 1;
+    work.end = num_n;
+    work.stride = static_cast<int>(gridDim.x) >> 1;
+    work.stream = false;
+    work.sub_lo = r * num_k / 2;
+    work.sub_hi = (r + 1) * num_k / 2;
+  }
   if constexpr (SPLIT > 1) {
     // Split-K over a cluster of SPLIT CTAs: CTA rank r of cluster c computes
     // tile c over K blocks [r, r+1) * num_k / SPLIT; the partial
@@ -741,6 +759,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
       if constexpr (SPLIT > 1) continue;  // reduced across the cluster below
+      if constexpr (SPLIT == -2) {
+        // rank 1 hands its partial tile to rank 0 through DSMEM; rank 0 adds
+        // it to its own, frees the peer's sT and applies the epilogue.
+        const uint32_t rank = ptx::cluster_ctarank();
+        ptx::named_bar_sync(1, 128);
+        if (rank == 1) {
+          if (t == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&pair_bar[0]), 0));
+          // sT is rewritten for the next tile only after rank 0 has read it
+          ptx::mbar_wait_cluster(&pair_bar[1], static_cast<uint32_t>(lt) & 1);
+          continue;
+        }
+        ptx::mbar_wait_cluster(&pair_bar[0], static_cast<uint32_t>(lt) & 1);
+        float4* own = reinterpret_cast<float4*>(sT);
+        for (int i = t; i < M * 32; i += 128) {
+          float4 v = own[i];
+          const float4 w = ptx::ld_cluster_f32x4(ptx::mapa(ptx::smem_u32(own + i), 1));
+          v.x += w.x;
+          v.y += w.y;
+          v.z += w.z;
+          v.w += w.w;
+          own[i] = v;
+        }
+        ptx::named_bar_sync(1, 128);
+        if (t == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&pair_bar[1]), 1));
+        swap_epilogue(ep, sT, M, t, tile, N);
+        ptx::named_bar_sync(1, 128);
+        continue;
+      }
       ptx::named_bar_sync(1, 128);
       if (!work.stream) {
         swap_epilogue(ep, sT, M, t, tile, N);
@@ -813,6 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (tr && t == 0) tr[4] = gtime();
   }
+  if constexpr (SPLIT == -2) ptx::cluster_sync();  // peers' smem alive until read
   if constexpr (SPLIT > 1) {
     // Every CTA's partial tile is in its sT; rank 0 sums the others' over
     // DSMEM (no global workspace, no atomics) and applies the epilogue; the
@@ -1079,7 +1126,7 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
   std::call_once(once, [] {
     cudaFuncSetAttribute(gemm_skinny_swap<NT, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::kSmem);
-    if (SPLIT > 1) {
+    if (SPLIT > 1 || SPLIT == -2) {
       cudaFuncSetAttribute(gemm_skinny_swap<NT, SPLIT>,
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
@@ -1087,7 +1134,8 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
   const CUtensorMap tx = make_tmap_bf16(A, M, K, lda, NT);
   const CUtensorMap tw = make_tmap_bf16(B, N, K, ldb, 128);
   const int tiles = N / 128;
-  const int grid = SPLIT > 1 ? tiles * SPLIT
+  const int grid = SPLIT > 1    ? tiles * SPLIT
+                   : SPLIT == -2 ? 2 * std::min(tiles, num_sms() / 2)
                    : kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
                                     : std::min(tiles, num_sms());
   // Study: ESP_GEMM_TRACE=<file> appends per-CTA globaltimer stamps (entry,
@@ -1099,9 +1147,11 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
     cudaMalloc(&trace, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long));
     cudaMemsetAsync(trace, 0, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long), s);
   }
-  if constexpr (SPLIT > 1) {
-    // Cluster of SPLIT CTAs per output tile (split-K reduced over DSMEM),
-    // with programmatic dependent launch like the other decode kernels.
+  if constexpr (SPLIT > 1 || SPLIT == -2) {
+    // Cluster of SPLIT CTAs per output tile (split-K reduced over DSMEM) or a
+    // persistent CTA pair (SPLIT == -2), with programmatic dependent launch
+    // like the other decode kernels.
+    constexpr int kCluster = SPLIT > 1 ? SPLIT : 2;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -1109,7 +1159,7 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = SPLIT;
+    at[0].val.clusterDim.x = kCluster;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1251,6 +1301,19 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
         getenv("ESP_GEMM_STREAMK_ALL") == nullptr && tiles * 4 <= num_sms() && K / BK >= 16) {
       if (M <= 16) launch_skinny_swap<16, 4>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       else launch_skinny_swap<32, 4>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      return;
+    }
+    // Tile counts between one and two waves (gate_up: 172 on 148 SMs): a
+    // persistent CTA pair per cluster splits every tile's K in two, so the
+    // busiest SM streams 1.5 tiles of weights instead of 2.
+    const int pairs = num_sms() / 2;
+    const bool pair_split = !old && getenv("ESP_GEMM_NO_PAIR_SPLIT") == nullptr &&
+                            getenv("ESP_GEMM_NO_STREAMK") == nullptr &&
+                            getenv("ESP_GEMM_STREAMK_ALL") == nullptr && K / BK >= 32 &&
+                            2 * ((tiles + num_sms() - 1) / num_sms()) > (tiles + pairs - 1) / pairs;
+    if (pair_split) {
+      if (M <= 16) launch_skinny_swap<16, -2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+      else launch_skinny_swap<32, -2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       return;
     }
     if (!old && getenv("ESP_GEMM_SPLIT2_ALL") != nullptr) {  // study knob

@@ -64,12 +64,16 @@ def test_gemm_skinny_splitk_residual(M, N, K):
 
 @pytest.mark.parametrize("M", [1, 16, 32])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-@pytest.mark.parametrize("mode", ["streamk", "tiles"])
+@pytest.mark.parametrize("mode", ["streamk", "tiles", "auto"])
 def test_gemm_skinny_epilogues(M, epi, mode, monkeypatch):
-    """Decode-shaped GEMMs, both skinny schedules: stream-K (per-segment fp32
-    partial slots, the CTA completing a tile sums them in order and applies
-    the fused epilogue) and whole tiles; store, residual, fp32, SiLU(gate)*up."""
-    monkeypatch.setenv("ESP_GEMM_STREAMK_ALL" if mode == "streamk" else "ESP_GEMM_NO_STREAMK", "1")
+    """Decode-shaped GEMMs, all skinny schedules: stream-K (per-segment fp32
+    partial slots, the CTA completing a tile sums them and applies the fused
+    epilogue), whole tiles, and the production dispatch ("auto": the 172-tile
+    gate_up shape runs as persistent CTA pairs splitting each tile's K, the
+    partner's partial added over DSMEM); store, residual, fp32, SiLU(gate)*up."""
+    if mode != "auto":
+        monkeypatch.setenv("ESP_GEMM_STREAMK_ALL" if mode == "streamk" else "ESP_GEMM_NO_STREAMK",
+                           "1")
     torch.manual_seed(M * 10 + epi)
     N, K = 22016 if epi == 3 else 12288, 4096
     a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
