@@ -298,7 +298,7 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
     rt_prefill.close()
     b, ctx = args.decode_batch, args.decode_ctx
     rt = abi.Runtime(abi.LWM_7B, 1, devices=[int(os.environ.get("LOCAL_RANK", "0"))],
-                     kv_capacity=b * (ctx + args.steps + args.warmup + 8))
+                     kv_capacity=b * (ctx + 2 * args.steps + args.warmup + 8))
     rng = np.random.default_rng(11)
     for r in range(b):
         rt.prefill([r], [ctx], [0], [[(0, ctx)]], tokens=rng.integers(0, V, ctx).astype(np.int32))
