@@ -55,7 +55,7 @@ for s in $STEPS; do
         -k regex:gemm_bf16 -s 10 -c 1 -o gpurun_out/prof_gemm -f python bench.py --steps 1 \
         --warmup 0 --skip-decode --skip-esp-sweep --skip-cpu --skip-config3 --skip-scale-down
       ;;
-    dprobe)
+    dprobe)  # DPROBE_VARIANTS='"ESP_DECODE_V1=381" "ESP_DECODE_V1=48"' bash tools/gpu_session.sh dprobe
       for r in 1 2; do
         eval "set -- ${DPROBE_VARIANTS:-\"ESP_DECODE_ATTN=1\" \"ESP_DECODE_STAGES=2\"}"; for v in "$@"; do
           echo "== $v" >> gpurun_out/dprobe.log
