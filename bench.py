@@ -117,9 +117,22 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo")
+        # NCCL between the GPUs of the box (one rank per GPU); gloo for the
+        # CPU-only world-size-2 tests of this harness.
+        use_nccl = (torch.cuda.is_available() and torch.cuda.device_count() >= world and
+                    os.environ.get("ESP_BENCH_GLOO") is None)
+        if use_nccl:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            try:
+                dist.init_process_group("nccl")
+            except Exception as e:  # report, then keep the run alive on gloo
+                print(f"nccl init failed ({str(e)[:120]}); using gloo", file=sys.stderr)
+                use_nccl = False
+        if not use_nccl:
+            dist.init_process_group("gloo")
         return rank, world, dist
     return rank, world, None
 
@@ -128,7 +141,8 @@ def reduce_max(x, dist):
     if dist is None:
         return x
     import torch
-    t = torch.tensor([float(x)])
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
