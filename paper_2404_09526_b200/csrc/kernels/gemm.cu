@@ -52,8 +52,11 @@ struct Cfg {
   static constexpr int kSmem = kARegion + kStages * kBBytes + 1024 + 256;
 };
 
+// m-blocks per raster group (L2 reuse of B); ESP_GEMM_GROUP overrides (study).
+__constant__ int c_raster_group = 16;
+
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
-  constexpr int kGroup = 16;  // m-blocks per raster group (L2 reuse of B)
+  const int kGroup = c_raster_group;
   const int per_group = kGroup * num_n;
   const int g = tile / per_group;
   const int first = g * kGroup;
@@ -1272,6 +1275,14 @@ StreamKWs streamk_workspace(size_t elems, size_t tiles, cudaStream_t s) {
 void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
           const GemmEpilogue& ep, cudaStream_t s) {
   if (M <= 0) return;
+  static const bool group_set = [] {
+    if (const char* e = getenv("ESP_GEMM_GROUP")) {
+      const int g = atoi(e);
+      if (g > 0) cudaMemcpyToSymbol(c_raster_group, &g, sizeof(int));
+    }
+    return true;
+  }();
+  (void)group_set;
   if (ep.ss_zero != nullptr && (M > 32 || getenv("ESP_GEMM_SKINNY_OLD") != nullptr)) {
     throw std::runtime_error("gemm: ss_zero is implemented by the skinny (M <= 32) kernel");
   }
