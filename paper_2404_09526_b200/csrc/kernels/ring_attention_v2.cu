@@ -32,7 +32,11 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int kStages = 2;
+constexpr int kStages = 2;   // V stages
+#ifndef ESP_K1_KSTAGES
+#define ESP_K1_KSTAGES 2
+#endif
+constexpr int kKStages = ESP_K1_KSTAGES;  // K stages (3 measured: no gain, 6.91-7.01 vs 6.76-6.96 ms)
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;
 constexpr int kDefaultPoly8 = 1;
@@ -42,7 +46,7 @@ struct Cfg2 {
   static constexpr int kBoxes = HD / 64;
   static constexpr int kQBytes = BM * HD * 2;
   static constexpr int kKvBytes = BN * HD * 2;
-  static constexpr int kSmem = 2 * kQBytes + 2 * kStages * kKvBytes + 1024 + 512;
+  static constexpr int kSmem = 2 * kQBytes + (kKStages + kStages) * kKvBytes + 1024 + 512;
 };
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): half the FMA-pipe
@@ -187,14 +191,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;                                 // [2][kQBytes]
-  uint8_t* sK = sQ + 2 * C::kQBytes;                  // [kStages][kKvBytes]
-  uint8_t* sV = sK + kStages * C::kKvBytes;           // [kStages][kKvBytes]
+  uint8_t* sK = sQ + 2 * C::kQBytes;                  // [kKStages][kKvBytes]
+  uint8_t* sV = sK + kKStages * C::kKvBytes;          // [kStages][kKvBytes]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * C::kKvBytes);
   uint64_t* q_full = bars;
   uint64_t* q_empty = bars + 1;
   uint64_t* k_full = bars + 2;
-  uint64_t* k_empty = k_full + kStages;
-  uint64_t* v_full = k_empty + kStages;
+  uint64_t* k_empty = k_full + kKStages;
+  uint64_t* v_full = k_empty + kKStages;
   uint64_t* v_empty = v_full + kStages;
   uint64_t* s_full = v_empty + kStages;  // [2] per query tile
   uint64_t* p_full = s_full + 2;         // [2 tiles][2 key halves]
@@ -209,9 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tma_prefetch_desc(&tmV);
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kKStages; ++s) {
       ptx::mbar_init(&k_full[s], 1);
       ptx::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&v_full[s], 1);
       ptx::mbar_init(&v_empty[s], 1);
     }
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tma_load_2d(sK + ks * C::kKvBytes + b * (BN * 128), &tmK, &k_full[ks],
                              it.head * HD + b * 64, row);
           }
-          if (++ks == kStages) { ks = 0; kph ^= 1; }
+          if (++ks == kKStages) { ks = 0; kph ^= 1; }
           ESP_PROF_WAIT(2, ptx::mbar_wait(&v_empty[vs], vph ^ 1));
           ptx::mbar_expect_tx(&v_full[vs], C::kKvBytes);
           for (int b = 0; b < C::kBoxes; ++b) {
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (st.active0()) issue_s(0, k_addr);
           if (act[1]) issue_s(1, k_addr);
           commit(&k_empty[ks]);
-          if (++ks == kStages) { ks = 0; kph ^= 1; }
+          if (++ks == kKStages) { ks = 0; kph ^= 1; }
         }
         bool first_pv[2] = {true, true};
         while (st.valid()) {
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++vs == kStages) { vs = 0; vph ^= 1; }
           if (has_next) {
             commit(&k_empty[ks]);
-            if (++ks == kStages) { ks = 0; kph ^= 1; }
+            if (++ks == kKStages) { ks = 0; kph ^= 1; }
           }
           st = nx;
         }
