@@ -496,6 +496,30 @@ def bench_transport(abi, args, np):
             rt.close()
             out[f"{mode}_ms"] = ms[0]
             out[f"{mode}_tokens_per_s"] = S / (ms[0] / 1e3)
+        # Fused-push prefill across d domains (d = 2 / 4 / 8) against the
+        # same ring co-located: the cost of the cross-domain executor.
+        os.environ.pop("ESP_RING_COPY", None)
+        sweep = {}
+        for dd in (2, 4, 8):
+            share_d = S // dd
+            ret_d = [[(i, share_d) for i in range(dd)]]
+            row = {}
+            for mode in ("domains", "colocated"):
+                if mode == "domains":
+                    os.environ["ESP_DOMAIN_PER_INSTANCE"] = "1"
+                else:
+                    os.environ.pop("ESP_DOMAIN_PER_INSTANCE", None)
+                rt = abi.Runtime(abi.LWM_7B, dd, devices=[dev] * dd, kv_capacity=share_d + 64)
+                ms = []
+                for k in range(2):
+                    _, _, t = rt.prefill([k], [S], list(range(dd)), ret_d, tokens=prompt)
+                    rt.free_request(k)
+                    if k:
+                        ms.append(t)
+                rt.close()
+                row[f"{mode}_ms"] = ms[0]
+            sweep[str(dd)] = row
+        out["prefill_push_vs_colocated"] = sweep
         # Multi-master decode across domains (query broadcast to every domain
         # holding KV, split-KV partials there, partial gather + LSE combine at
         # the masters) vs the same group co-located: b=16 requests x 4096
