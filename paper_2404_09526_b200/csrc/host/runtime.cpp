@@ -578,6 +578,49 @@ void Runtime::prefill(const esp_prefill_args& a) {
   profiles_.push_back(std::move(pr));
 }
 
+void Runtime::o_and_mlp(DeviceCtx& dc, int l, int rows, bf16* x, const bf16* attn, bf16* xn,
+                        bf16* hbuf, const NormFuse& nf, cudaStream_t s) {
+  const int H = cfg_.hidden, F = cfg_.ffn;
+  const LayerW& w = dc.layers[l];
+  const bool fuse = nf.ss_o != nullptr;
+  k::GemmEpilogue eo;
+  eo.kind = k::kEpiResidual;
+  eo.out = x;
+  eo.ldo = H;
+  if (fuse) {
+    eo.ss_out = nf.ss_o;
+    if (!nf.zero_in_kernel) {
+      cuda_ok(cudaMemsetAsync(nf.ss_o, 0, static_cast<size_t>(rows) * sizeof(float), s), "memset");
+    }
+  }
+  timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
+  if (!fuse) {
+    timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
+  }
+  k::GemmEpilogue eg;
+  eg.kind = k::kEpiSiluMul;
+  eg.out = hbuf;
+  eg.ldo = F;
+  if (fuse) {
+    eg.ss_in = nf.ss_o;
+    if (nf.zero_in_kernel) eg.ss_zero = nf.ss_d;
+    eg.norm_dim = H;
+    eg.norm_eps = cfg_.rms_eps;
+  }
+  timed(kPhGateUp, s, [&] { k::gemm(fuse ? x : xn, H, w.wgu, H, rows, 2 * F, H, eg, s); });
+  k::GemmEpilogue ed;
+  ed.kind = k::kEpiResidual;
+  ed.out = x;
+  ed.ldo = H;
+  if (fuse) {
+    ed.ss_out = nf.ss_d;
+    if (!nf.zero_in_kernel) {
+      cuda_ok(cudaMemsetAsync(nf.ss_d, 0, static_cast<size_t>(rows) * sizeof(float), s), "memset");
+    }
+  }
+  timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s); });
+}
+
 void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
                                      const std::vector<k::RingSegment>& segs,
                                      const std::vector<int32_t>& work) {
@@ -636,37 +679,12 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
                                 static_cast<int>(segs.size()),
                                 static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
     });
-    k::GemmEpilogue eo;
-    eo.kind = k::kEpiResidual;
-    eo.out = x;
-    eo.ldo = H;
+    NormFuse nf;
     if (fuse) {
-      eo.ss_out = ss2;
-      cuda_ok(cudaMemsetAsync(ss2, 0, static_cast<size_t>(rows) * sizeof(float), s), "memset");
+      nf.ss_o = ss2;
+      nf.ss_d = ss1;
     }
-    timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
-    if (!fuse) {
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
-    }
-    k::GemmEpilogue eg;
-    eg.kind = k::kEpiSiluMul;
-    eg.out = hbuf;
-    eg.ldo = F;
-    if (fuse) {
-      eg.ss_in = ss2;
-      eg.norm_dim = H;
-      eg.norm_eps = cfg_.rms_eps;
-    }
-    timed(kPhGateUp, s, [&] { k::gemm(a_in, H, w.wgu, H, rows, 2 * F, H, eg, s); });
-    k::GemmEpilogue ed;
-    ed.kind = k::kEpiResidual;
-    ed.out = x;
-    ed.ldo = H;
-    if (fuse) {
-      ed.ss_out = ss1;
-      cuda_ok(cudaMemsetAsync(ss1, 0, static_cast<size_t>(rows) * sizeof(float), s), "memset");
-    }
-    timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s); });
+    o_and_mlp(dc, l, rows, x, attn, xn, hbuf, nf, s);
   }
 }
 
@@ -997,32 +1015,13 @@ void Runtime::decode_step(const esp_decode_args& a) {
                                   1, static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
       });
     }
-    k::GemmEpilogue eo;
-    eo.kind = k::kEpiResidual;
-    eo.out = x;
-    eo.ldo = H;
-    if (fuse_norm) eo.ss_out = ss2;
-    timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, rows, H, H, eo, s); });
-    if (!fuse_norm) {
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
-    }
-    k::GemmEpilogue eg;
-    eg.kind = k::kEpiSiluMul;
-    eg.out = hbuf;
-    eg.ldo = F;
+    NormFuse nf;
     if (fuse_norm) {
-      eg.ss_in = ss2;
-      eg.ss_zero = ss1;
-      eg.norm_dim = H;
-      eg.norm_eps = cfg_.rms_eps;
+      nf.ss_o = ss2;
+      nf.ss_d = ss1;
+      nf.zero_in_kernel = true;
     }
-    timed(kPhGateUp, s, [&] { k::gemm(a_in, H, w.wgu, H, rows, 2 * F, H, eg, s); });
-    k::GemmEpilogue ed;
-    ed.kind = k::kEpiResidual;
-    ed.out = x;
-    ed.ldo = H;
-    if (fuse_norm) ed.ss_out = ss1;
-    timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, rows, H, F, ed, s); });
+    o_and_mlp(dc, l, rows, x, attn, xn, hbuf, nf, s);
   }
   // Output rows: the decode rows, then the chunk's last token when the chunk
   // completes the prompt (its first generated token, engine.cpp:570-579).

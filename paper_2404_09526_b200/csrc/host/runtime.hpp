@@ -137,6 +137,22 @@ class Runtime {
                    const std::vector<std::pair<InstanceId, int32_t>>& chunk_slots, double* ms);
   void decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows,
                     const std::vector<RequestId>& batch);
+  // The second half of a layer after attention: O projection (+ residual),
+  // RMSNorm, gate_up (SiLU·up), down projection (+ residual), on `rows` rows
+  // of dc's x / attn / xn / h buffers. Norm handling:
+  //   ss_o == null            — unit-gain norm kernel between O and gate_up;
+  //   ss_o / ss_d given       — fused: O accumulates row sums of squares into
+  //                             ss_o, gate_up scales by them, down accumulates
+  //                             into ss_d (the next layer's norm1);
+  //   zero_in_kernel          — the skinny kernels clear the next buffer
+  //                             (decode, PDL-friendly); otherwise memsets.
+  struct NormFuse {
+    float* ss_o = nullptr;
+    float* ss_d = nullptr;
+    bool zero_in_kernel = false;
+  };
+  void o_and_mlp(DeviceCtx& dc, int l, int rows, k_bf16* x, const k_bf16* attn, k_bf16* xn,
+                 k_bf16* hbuf, const NormFuse& nf, cudaStream_t s);
   // RMSNorm fused into the single-domain prefill GEMMs (ESP_PREFILL_NORM_KERNEL=1: kernels).
   static bool fuse_norm_prefill() { return std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr; }
   void forward_layers_prefill(DeviceCtx& dc, int rows, const std::vector<k::RingSegment>& segs,

@@ -432,22 +432,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         cuda_ok(cudaEventRecord(e, s), "event");
         attn_done[dom] = e;
       }
-      k::GemmEpilogue eo;
-      eo.kind = k::kEpiResidual;
-      eo.out = x;
-      eo.ldo = H;
-      timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, p.rows, H, H, eo, s); });
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, p.rows, H, cfg_.rms_eps, s); });
-      k::GemmEpilogue eg;
-      eg.kind = k::kEpiSiluMul;
-      eg.out = hbuf;
-      eg.ldo = F;
-      timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, p.rows, 2 * F, H, eg, s); });
-      k::GemmEpilogue ed;
-      ed.kind = k::kEpiResidual;
-      ed.out = x;
-      ed.ldo = H;
-      timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, p.rows, H, F, ed, s); });
+      o_and_mlp(dc, l, p.rows, x, attn, xn, hbuf, NormFuse{}, s);
     }
   }
 
@@ -604,22 +589,7 @@ void Runtime::chunk_multi(const esp_decode_args& a, int64_t p_prev,
     k::gather_rows(slabs, d_gi, d_gs, kv_n, kg, vg, H, s);
     k::ring_attention_variant(attn_variant_, q, kg, vg, attn, c, kv_n, cfg_.heads, cfg_.head_dim,
                               d_seg, 1, static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
-    k::GemmEpilogue eo;
-    eo.kind = k::kEpiResidual;
-    eo.out = x;
-    eo.ldo = H;
-    k::gemm(attn, H, w.wo, H, c, H, H, eo, s);
-    k::rmsnorm(x, nullptr, nullptr, xn, c, H, cfg_.rms_eps, s);
-    k::GemmEpilogue eg;
-    eg.kind = k::kEpiSiluMul;
-    eg.out = hbuf;
-    eg.ldo = F;
-    k::gemm(xn, H, w.wgu, H, c, 2 * F, H, eg, s);
-    k::GemmEpilogue ed;
-    ed.kind = k::kEpiResidual;
-    ed.out = x;
-    ed.ldo = H;
-    k::gemm(hbuf, F, w.wd, F, c, H, F, ed, s);
+    o_and_mlp(dc, l, c, x, attn, xn, hbuf, NormFuse{}, s);
   }
   int32_t first = -1;
   std::vector<float> lg;
@@ -910,22 +880,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         cudaEvent_t e = sync_event(mc);
         cuda_ok(cudaEventRecord(e, s), "event");
         comb_now[md] = e;
-        k::GemmEpilogue eo;
-        eo.kind = k::kEpiResidual;
-        eo.out = x;
-        eo.ldo = H;
-        timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, nl, H, H, eo, s); });
-        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
-        k::GemmEpilogue eg;
-        eg.kind = k::kEpiSiluMul;
-        eg.out = hbuf;
-        eg.ldo = F;
-        timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, nl, 2 * F, H, eg, s); });
-        k::GemmEpilogue ed;
-        ed.kind = k::kEpiResidual;
-        ed.out = x;
-        ed.ldo = H;
-        timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, nl, H, F, ed, s); });
+        o_and_mlp(mc, l, nl, x, attn, xn, hbuf, NormFuse{}, s);
       }
       comb_done = comb_now;
     }
@@ -1044,22 +999,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
                                static_cast<int32_t*>(mc.chunk_ids.ptr),
                                static_cast<int32_t*>(mc.row_list.ptr), nl, heads, hd, attn, s);
       });
-      k::GemmEpilogue eo;
-      eo.kind = k::kEpiResidual;
-      eo.out = x;
-      eo.ldo = H;
-      timed(kPhOProj, s, [&] { k::gemm(attn, H, w.wo, H, nl, H, H, eo, s); });
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
-      k::GemmEpilogue eg;
-      eg.kind = k::kEpiSiluMul;
-      eg.out = hbuf;
-      eg.ldo = F;
-      timed(kPhGateUp, s, [&] { k::gemm(xn, H, w.wgu, H, nl, 2 * F, H, eg, s); });
-      k::GemmEpilogue ed;
-      ed.kind = k::kEpiResidual;
-      ed.out = x;
-      ed.ldo = H;
-      timed(kPhDown, s, [&] { k::gemm(hbuf, F, w.wd, F, nl, H, F, ed, s); });
+      o_and_mlp(mc, l, nl, x, attn, xn, hbuf, NormFuse{}, s);
     }
   }
   // 4. LM head + greedy token at each master.
