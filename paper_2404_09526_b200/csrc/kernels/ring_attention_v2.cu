@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < (it.act1 ? 2 : 1); ++t) {
           for (int b = 0; b < C::kBoxes; ++b) {
             ptx::tma_load_2d(sQ + t * C::kQBytes + b * (BM * 128), &tmQ, q_full,
-                             it.head * HD + b * 64, sg->q_row0 + it.q0[t]);
+                             it.head * HD + b * 64, sg->q_row0 + it.q0[0] + t * BM);
           }
         }
         Steps st;
@@ -387,6 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::setmaxnreg_inc<192>();
     // ------------------------------------------------------------ softmax
     const int t = (warp >= 8) ? 1 : 0;
+    // this tile's TMEM columns (runtime t: no array indexing -> no local memory)
+    const uint32_t ts_t = tmem + t * BN, to_t = tmem + 2 * BN + t * HD;
     const uint32_t quad = warp & 3;
     const int row = static_cast<int>(quad * 32 + lane);
     const uint32_t lane_off = (quad * 32) << 16;
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Item it = load_item(work, w, segs);
       if (t == 1 && !it.act1) continue;
       const RingSegment* sg = &segs[it.seg];
-      const int q0 = it.q0[t];
+      const int q0 = (it.q0[0] + t * BM);
       const int a = q0 + row;
       float m_run = -INFINITY, l_run = 0.f;
       int j = 0;
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
-          ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 32 * c, chunk);
+          ptx::tmem_ld_32x32b_x32(ts_t + lane_off + 32 * c, chunk);
         }
         ptx::tmem_wait_ld();
         if constexpr (kProf) prof_acc[2] += clock64() - prof_t_step;  // S readback
@@ -460,11 +462,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
           for (int c = 0; c < HD; c += 32) {
             uint32_t o[32];
-            ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
+            ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
             ptx::tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            ptx::tmem_st_32x32b_x32(t_o[t] + lane_off + c, o);
+            ptx::tmem_st_32x32b_x32(to_t + lane_off + c, o);
           }
         }
         // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
@@ -483,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 2; c < 4; ++c) {
               uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
-              ptx::tmem_ld_32x32b_x32(t_s[t] + lane_off + 32 * c, chunk);
+              ptx::tmem_ld_32x32b_x32(ts_t + lane_off + 32 * c, chunk);
             }
             ptx::tmem_wait_ld();
             if (!full_tile) {  // the causal mask again on the re-read half
@@ -512,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             s[c] = ptx::pack_bf16(p0, p1);
           }
-          ptx::tmem_st_32x32b_x32(t_s[t] + lane_off + 32 * half,
+          ptx::tmem_st_32x32b_x32(ts_t + lane_off + 32 * half,
                                   *reinterpret_cast<uint32_t(*)[32]>(&s[32 * half]));
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < HD; c += 32) {
         uint32_t o[32];
-        ptx::tmem_ld_32x32b_x32(t_o[t] + lane_off + c, o);
+        ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
         ptx::tmem_wait_ld();
         if (valid) {
           uint4* d = reinterpret_cast<uint4*>(orow + c);
