@@ -33,6 +33,9 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int kStages = 2;   // V stages
+#ifndef ESP_K1_REREAD
+#define ESP_K1_REREAD 0
+#endif
 #ifndef ESP_K1_KSTAGES
 #define ESP_K1_KSTAGES 2
 #endif
@@ -479,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           if (half == 1) {
+#if ESP_K1_REREAD
             // Re-read S for keys 64..127 (intact: P so far covers columns
             // 0..31) so the second half's exponentials cannot be scheduled
             // ahead of the first half's P store and arrive.
@@ -494,6 +498,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c > lim) s[c] = __float_as_uint(-INFINITY);
               }
             }
+#else
+            // Keys 64..127 are still in registers; an empty volatile asm that
+            // "modifies" them pins the second half's exponentials after the
+            // first half's P store and arrive (no TMEM re-read).
+#pragma unroll
+            for (int c = 64; c < 128; c += 16) {
+              asm volatile(""
+                           : "+r"(s[c]), "+r"(s[c + 1]), "+r"(s[c + 2]), "+r"(s[c + 3]),
+                             "+r"(s[c + 4]), "+r"(s[c + 5]), "+r"(s[c + 6]), "+r"(s[c + 7]),
+                             "+r"(s[c + 8]), "+r"(s[c + 9]), "+r"(s[c + 10]), "+r"(s[c + 11]),
+                             "+r"(s[c + 12]), "+r"(s[c + 13]), "+r"(s[c + 14]), "+r"(s[c + 15]));
+            }
+#endif
           }
 #pragma unroll
           for (int c = 32 * half; c < 32 * half + 32; ++c) {
