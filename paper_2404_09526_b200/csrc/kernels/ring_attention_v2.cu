@@ -33,9 +33,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int kStages = 2;   // V stages
-#ifndef ESP_K1_REREAD
-#define ESP_K1_REREAD 0
-#endif
 #ifndef ESP_K1_KSTAGES
 #define ESP_K1_KSTAGES 2
 #endif
@@ -430,36 +427,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         // Row max with 8 independent chains of 3-input max (FMNMX3), then a tree.
-        float mx8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          mx8[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]),
-                         __uint_as_float(s[120 + k]));
-        }
-#pragma unroll
-        for (int c = 16; c < 120; c += 16) {
+        auto row_max = [&]() {
+          float mx8[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            mx8[k] = fmax3(mx8[k], __uint_as_float(s[c + k]), __uint_as_float(s[c + 8 + k]));
+            mx8[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]),
+                           __uint_as_float(s[120 + k]));
           }
-        }
-        const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
-                               fmaxf(mx8[6], mx8[7]));
-        if constexpr (kProf) prof_acc[3] += clock64() - prof_t_step;  // ..through row max
-        const float m_tile = mx * scale_log2;
-        const float m_new = fmaxf(m_run, m_tile);
-        const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY)
-                                               : (m_new > m_run + kRescaleThreshold);
-        float alpha = 1.f;
-        if (need) {
-          alpha = m_run == -INFINITY ? 0.f : ptx::ex2(m_run - m_new);
-          m_run = m_new;
-        }
-        const float m_sub = m_run == -INFINITY ? 0.f : m_run;
-        if (j > 0 && __any_sync(0xffffffff, need)) {
-          // O holds PV_{j-1} (complete: S_j, issued after it, is done) —
-          // rescale it in TMEM before PV_j accumulates (rare: only when a row
-          // max grew by more than 2^8).
+#pragma unroll
+          for (int c = 16; c < 120; c += 16) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              mx8[k] = fmax3(mx8[k], __uint_as_float(s[c + k]), __uint_as_float(s[c + 8 + k]));
+            }
+          }
+          return fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
+                       fmaxf(mx8[6], mx8[7]));
+        };
+        // O *= f in TMEM. O holds PV_{j-1}, complete once o_done of the
+        // previous step fired (rare: a row max grew past the threshold).
+        auto rescale_o = [&](float f) {
           ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll 1
@@ -468,50 +455,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
             ptx::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
             ptx::tmem_st_32x32b_x32(to_t + lane_off + c, o);
           }
-        }
+        };
         // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
         // precede the write of s[c], c <= 2c), then P over S_t in TMEM, in two
         // halves of 64 keys: the MMA warp starts PV on keys 0..63 while keys
         // 64..127 are still being exponentiated.
         const uint64_t scale2 = f2pack(scale_log2, scale_log2);
-        const uint64_t negm2 = f2pack(-m_sub, -m_sub);
         uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          if (half == 1) {
-#if ESP_K1_REREAD
-            // Re-read S for keys 64..127 (intact: P so far covers columns
-            // 0..31) so the second half's exponentials cannot be scheduled
-            // ahead of the first half's P store and arrive.
-#pragma unroll
-            for (int c = 2; c < 4; ++c) {
-              uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
-              ptx::tmem_ld_32x32b_x32(ts_t + lane_off + 32 * c, chunk);
-            }
-            ptx::tmem_wait_ld();
-            if (!full_tile) {  // the causal mask again on the re-read half
-#pragma unroll
-              for (int c = 64; c < 128; ++c) {
-                if (c > lim) s[c] = __float_as_uint(-INFINITY);
-              }
-            }
-#else
-            // Keys 64..127 are still in registers; an empty volatile asm that
-            // "modifies" them pins the second half's exponentials after the
-            // first half's P store and arrive (no TMEM re-read).
-#pragma unroll
-            for (int c = 64; c < 128; c += 16) {
-              asm volatile(""
-                           : "+r"(s[c]), "+r"(s[c + 1]), "+r"(s[c + 2]), "+r"(s[c + 3]),
-                             "+r"(s[c + 4]), "+r"(s[c + 5]), "+r"(s[c + 6]), "+r"(s[c + 7]),
-                             "+r"(s[c + 8]), "+r"(s[c + 9]), "+r"(s[c + 10]), "+r"(s[c + 11]),
-                             "+r"(s[c + 12]), "+r"(s[c + 13]), "+r"(s[c + 14]), "+r"(s[c + 15]));
-            }
-#endif
-          }
+        auto exp_half = [&](int half, float m_sub) {
+          const uint64_t negm2 = f2pack(-m_sub, -m_sub);
 #pragma unroll
           for (int c = 32 * half; c < 32 * half + 32; ++c) {
             float x0, x1, p0, p1;
@@ -531,16 +486,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             s[c] = ptx::pack_bf16(p0, p1);
           }
+        };
+        auto store_half = [&](int half) {
           ptx::tmem_st_32x32b_x32(ts_t + lane_off + 32 * half,
                                   *reinterpret_cast<uint32_t(*)[32]>(&s[32 * half]));
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           ptx::mbar_arrive(&p_full[2 * t + half]);
+        };
+        // Keys 64..127 are still in registers; an empty volatile asm that
+        // "modifies" them pins the second half's exponentials after the
+        // first half's P store and arrive.
+        auto pin_half1 = [&]() {
+#pragma unroll
+          for (int c = 64; c < 128; c += 16) {
+            asm volatile(""
+                         : "+r"(s[c]), "+r"(s[c + 1]), "+r"(s[c + 2]), "+r"(s[c + 3]),
+                           "+r"(s[c + 4]), "+r"(s[c + 5]), "+r"(s[c + 6]), "+r"(s[c + 7]),
+                           "+r"(s[c + 8]), "+r"(s[c + 9]), "+r"(s[c + 10]), "+r"(s[c + 11]),
+                           "+r"(s[c + 12]), "+r"(s[c + 13]), "+r"(s[c + 14]), "+r"(s[c + 15]));
+          }
+        };
+        {
+          const float mx = row_max();
+          if constexpr (kProf) prof_acc[3] += clock64() - prof_t_step;  // ..through row max
+          const float m_tile = mx * scale_log2;
+          const float m_new = fmaxf(m_run, m_tile);
+          const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY)
+                                                 : (m_new > m_run + kRescaleThreshold);
+          float alpha = 1.f;
+          if (need) {
+            alpha = m_run == -INFINITY ? 0.f : ptx::ex2(m_run - m_new);
+            m_run = m_new;
+          }
+          const float m_sub = m_run == -INFINITY ? 0.f : m_run;
+          if (j > 0 && __any_sync(0xffffffff, need)) rescale_o(alpha);
+          exp_half(0, m_sub);
+          store_half(0);
+          pin_half1();
+          exp_half(1, m_sub);
+          store_half(1);
+          if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P stored
+          float sa0, sa1;
+          f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
+          l_run = l_run * alpha + (sa0 + sa1);
         }
-        if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P stored
-        float sa0, sa1;
-        f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
-        l_run = l_run * alpha + (sa0 + sa1);
         if constexpr (kProf) {
           prof_acc[1] += clock64() - prof_t_step;  // softmax step (S ready -> P ready)
           prof_acc[5] += 1;
