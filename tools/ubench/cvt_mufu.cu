@@ -3,6 +3,7 @@
 // pipe as ex2.approx (MUFU.EX2)? Times, per SM, loops of
 //   ex2 only | cvt only | ex2 + cvt (softmax ratio: 1 pack per 2 ex2)
 //   | ex2 + integer-rounded pack (IADD + PRMT, no F2FP)
+//   | pack + ex2.approx.ftz.bf16x2 (one MUFU op per pair?) + unpack
 // with 8 warps per SM (the two softmax warpgroups). If F2FP rides the MUFU
 // pipe the mixed loop costs the sum of the two alone.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o cvt_mufu cvt_mufu.cu
@@ -29,6 +30,12 @@ __device__ __forceinline__ uint32_t int_pack(float lo, float hi) {
   return r;
 }
 
+__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 1) bench(float* out, long long* cyc, float seed) {
   float v[16];
@@ -47,6 +54,11 @@ __global__ void __launch_bounds__(256, 1) bench(float* out, long long* cyc, floa
       }
       if (MODE == 1 || MODE == 2) acc ^= cvt_pack(a, b);
       if (MODE == 3) acc ^= int_pack(a, b);
+      if (MODE == 4) {  // pack, one bf16x2 ex2 for the pair, unpack
+        const uint32_t p = ex2_bf16x2(cvt_pack(a, b));
+        a = __uint_as_float(p << 16);
+        b = __uint_as_float(p & 0xffff0000u);
+      }
       v[i] = a * -0.5f;
       v[i + 1] = b * -0.5f;
     }
@@ -83,5 +95,6 @@ int main() {
   run<1>("cvt.rn.bf16x2 (F2FP)", sms, out, cyc);
   run<2>("ex2 x2 + F2FP", sms, out, cyc);
   run<3>("ex2 x2 + IADD/PRMT pack", sms, out, cyc);
+  run<4>("F2FP + ex2.bf16x2 + unpack", sms, out, cyc);
   return 0;
 }
