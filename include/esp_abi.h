@@ -272,6 +272,24 @@ int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int
  * "measured_ms"}, cost_model.cpp:243-248) appended to a JSONL file. */
 int esp_dump_profiles(const esp_runtime* rt, const char* path);
 
+/* Measured decode steps (one per esp_decode_step that carries no chunk), as
+ * the arguments of Sib::decode_time (cost_model.cpp:175-187) the engine
+ * charges them with (engine.cpp:420-425): dop = members, batch, masters,
+ * resident = KV tokens of the batch after the append; ms = device time.
+ * Copies min(cap, available) samples; *n = available. The reference has no
+ * decode profile record (it hand-sets alpha_d/beta_d/gamma_d). */
+int esp_decode_samples(const esp_runtime* rt, int32_t* dop, int32_t* batch, int32_t* masters,
+                       int64_t* resident, double* ms, int64_t cap, int64_t* n);
+
+/* Measured-SIB fit: least squares y ~ c[0] + c[1]*x1 + c[2]*x2
+ * with fit_prefill_coefficients' admissibility rule (cost_model.cpp:86-135:
+ * unit-norm columns, most negative coefficient dropped until all >= 0).
+ * Prefill: x1 = sum of lengths, x2 = sum of squares -> alpha_p, beta_p,
+ * gamma_p. Decode: x1 = batch (/ masters above the compute-bound threshold),
+ * x2 = resident / dop -> alpha_d, beta_d, gamma_d. ESP_ERR_CONFIG when n < 3
+ * or the design is rank deficient (the reference's UnderdeterminedError). */
+int esp_fit_cost(const double* x1, const double* x2, const double* y, int64_t n, double* coef);
+
 /* Per-phase device timing (CUDA events around each launch on the runtime's
  * stream) while profiling is on. Phases: 0 embed, 1 rmsnorm, 2 QKV GEMM(+RoPE
  * +ring write+retention), 3 ring attention, 4 O GEMM, 5 gate_up GEMM, 6 down

@@ -91,6 +91,7 @@ EXPORTED_SYMBOLS = [
     "esp_runtime_create", "esp_runtime_destroy", "esp_instance_info", "esp_prefill",
     "esp_decode_step", "esp_move_kv", "esp_free_request", "esp_query_placement",
     "esp_check_conservation", "esp_request_tokens", "esp_dump_profiles",
+    "esp_decode_samples", "esp_fit_cost",
     "esp_launch_count", "esp_set_profiling", "esp_phase_times", "esp_k_gemm", "esp_k_ring_attention", "esp_k_decode_attention",
 ]
 
@@ -187,6 +188,12 @@ def lib() -> C.CDLL:
         h.esp_request_tokens.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
                                          C.c_int32, C.POINTER(C.c_int32)]
         h.esp_dump_profiles.argtypes = [C.c_void_p, C.c_char_p]
+        h.esp_decode_samples.argtypes = [C.c_void_p, C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                         C.c_int64, C.POINTER(C.c_int64)]
+        h.esp_fit_cost.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double)]
         h.esp_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         h.esp_phase_times.argtypes = [C.c_void_p, C.POINTER(C.c_double),
                                       C.POINTER(C.c_int64), C.c_int32]
@@ -597,6 +604,35 @@ class Runtime:
 
     def dump_profiles(self, path: str):
         check(lib().esp_dump_profiles(self._h, path.encode()))
+
+    def decode_samples(self) -> Dict[str, np.ndarray]:
+        """Measured decode steps: dop, batch, masters, resident, ms arrays."""
+        n = C.c_int64(0)
+        check(lib().esp_decode_samples(self._h, None, None, None, None, None, 0, C.byref(n)))
+        m = n.value
+        out = {"dop": np.zeros(m, np.int32), "batch": np.zeros(m, np.int32),
+               "masters": np.zeros(m, np.int32), "resident": np.zeros(m, np.int64),
+               "ms": np.zeros(m, np.float64)}
+        if m:
+            check(lib().esp_decode_samples(
+                self._h, _ptr(out["dop"], C.c_int32), _ptr(out["batch"], C.c_int32),
+                _ptr(out["masters"], C.c_int32), _ptr(out["resident"], C.c_int64),
+                _ptr(out["ms"], C.c_double), m, C.byref(n)))
+        return out
+
+
+def fit_cost(x1, x2, y) -> np.ndarray:
+    """[c0, c1, c2] of y ~ c0 + c1*x1 + c2*x2 (esp_fit_cost; the reference's
+    fit_prefill_coefficients rule, cost_model.cpp:86-135)."""
+    a = np.ascontiguousarray(x1, np.float64)
+    b = np.ascontiguousarray(x2, np.float64)
+    c = np.ascontiguousarray(y, np.float64)
+    if not (len(a) == len(b) == len(c)):
+        raise ValueError("fit_cost: arrays differ in length")
+    coef = np.zeros(3, np.float64)
+    check(lib().esp_fit_cost(_ptr(a, C.c_double), _ptr(b, C.c_double), _ptr(c, C.c_double),
+                             len(a), _ptr(coef, C.c_double)))
+    return coef
 
 
 def launch_count() -> int:

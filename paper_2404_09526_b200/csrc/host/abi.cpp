@@ -17,6 +17,7 @@
 #include "planner.hpp"
 #include "device_ctx.hpp"
 #include "runtime.hpp"
+#include "sib_fit.hpp"
 
 struct esp_runtime {
   esp::Runtime* impl;
@@ -304,6 +305,36 @@ int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int
 
 int esp_dump_profiles(const esp_runtime* rt, const char* path) {
   return guarded([&] { rt->impl->dump_profiles(path); });
+}
+
+int esp_decode_samples(const esp_runtime* rt, int32_t* dop, int32_t* batch, int32_t* masters,
+                       int64_t* resident, double* ms, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    if (!rt || !n) throw esp::ConfigError("decode_samples: null argument");
+    const auto& v = rt->impl->decode_profiles();
+    *n = static_cast<int64_t>(v.size());
+    const int64_t m = std::min<int64_t>(cap, *n);
+    if (m > 0 && (!dop || !batch || !masters || !resident || !ms)) {
+      throw esp::ConfigError("decode_samples: null output array");
+    }
+    for (int64_t i = 0; i < m; ++i) {
+      const auto& r = v[static_cast<size_t>(i)];
+      dop[i] = r.dop;
+      batch[i] = r.batch;
+      masters[i] = r.masters;
+      resident[i] = r.resident;
+      ms[i] = r.ms;
+    }
+  });
+}
+
+int esp_fit_cost(const double* x1, const double* x2, const double* y, int64_t n, double* coef) {
+  return guarded([&] {
+    if (n > 0 && (!x1 || !x2 || !y)) throw esp::ConfigError("fit_cost: null argument");
+    if (!coef) throw esp::ConfigError("fit_cost: null output");
+    const auto c = esp::fit_cost(x1, x2, y, n > 0 ? static_cast<size_t>(n) : 0);
+    for (int i = 0; i < 3; ++i) coef[i] = c[static_cast<size_t>(i)];
+  });
 }
 
 int esp_set_profiling(esp_runtime* rt, int32_t on) {

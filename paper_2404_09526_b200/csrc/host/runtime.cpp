@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <iomanip>
 #include <numeric>
 #include <set>
 #include <sstream>
@@ -834,6 +835,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
       chunk_multi(a, p_prev, prev, cur, &ms_chunk);
     }
     if (a.device_ms_out) *a.device_ms_out = ms_dec + ms_chunk;
+    if (b > 0 && !has_chunk) record_decode_profile(members, batch, a.n_masters, ms_dec);
     return;
   }
   DeviceCtx& dc = device_of(involved, "decode_step");
@@ -1062,6 +1064,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
   float ms = 0;
   cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
   if (a.device_ms_out) *a.device_ms_out = ms;
+  if (b > 0 && !has_chunk) record_decode_profile(members, batch, a.n_masters, ms);
   // Results back in the caller's batch order.
   std::map<RequestId, int> row_of;
   for (int i = 0; i < b; ++i) row_of[rows_v[i].r] = i;
@@ -1224,13 +1227,23 @@ void Runtime::check_conservation() {
   }
 }
 
+void Runtime::record_decode_profile(const std::vector<InstanceId>& members,
+                                    const std::vector<RequestId>& batch, int n_masters,
+                                    double ms) {
+  int64_t resident = 0;
+  for (RequestId r : batch) resident += req(r).kv_tokens();
+  decode_profiles_.push_back(DecodeProfileRec{static_cast<int>(members.size()),
+                                              static_cast<int>(batch.size()), n_masters,
+                                              resident, ms});
+}
+
 void Runtime::dump_profiles(const std::string& path) const {
   std::ofstream out(path, std::ios::app);
   if (!out) throw ConfigError("cannot write profile file: " + path);
   for (const ProfileRec& p : profiles_) {
     out << "{\"dop\": " << p.dop << ", \"tp\": 1, \"kind\": \"profile\", \"lengths\": [";
     for (size_t i = 0; i < p.lengths.size(); ++i) out << (i ? ", " : "") << p.lengths[i];
-    out << "], \"measured_ms\": " << p.ms << "}\n";
+    out << "], \"measured_ms\": " << std::setprecision(9) << p.ms << "}\n";
   }
 }
 

@@ -80,6 +80,15 @@ struct ProfileRec {
   double ms;
 };
 
+// One measured decode step (no chunk riding on it): the arguments of
+// Sib::decode_time (cost_model.cpp:175-187) as the engine computes them
+// (engine.cpp:420-425: resident = KV of the batch after the append).
+struct DecodeProfileRec {
+  int dop, batch, masters;
+  int64_t resident;
+  double ms;
+};
+
 class Runtime {
  public:
   Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
@@ -95,6 +104,7 @@ class Runtime {
   void check_conservation();
   void request_tokens(RequestId r, int32_t* out, int32_t cap, int32_t* n) const;
   void dump_profiles(const std::string& path) const;
+  const std::vector<DecodeProfileRec>& decode_profiles() const { return decode_profiles_; }
   bool placement_only() const { return devices_.empty(); }
   void set_profiling(bool on) { profiling_ = on; }
   void phase_times(double* ms, int64_t* launches, int n);
@@ -170,6 +180,9 @@ class Runtime {
   std::map<RequestId, RequestRec> requests_;
   std::vector<std::unique_ptr<DeviceCtx>> devices_;  // empty: placement-only
   std::vector<ProfileRec> profiles_;
+  std::vector<DecodeProfileRec> decode_profiles_;
+  void record_decode_profile(const std::vector<InstanceId>& members,
+                             const std::vector<RequestId>& batch, int n_masters, double ms);
   bool profiling_ = false;
   // K1 variant: v2 (two query tiles per CTA, P in TMEM) unless ESP_ATTN_V1=1.
   int attn_variant_ = 2;     // K1 variant (ESP_ATTN), set in the constructor
