@@ -68,8 +68,14 @@ int run(const char* policy, int instances, TokenCount cap, std::vector<TraceReco
   return 0;
 }
 
+// usage: tap_live <reference root> [sib.jsonl]   (default: the reference's default SIB)
 int main(int argc, char** argv) {
-  const std::string sib = std::string(argv[1]) + "/proj/configs/default_sib.jsonl";
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: tap_live <reference root> [sib.jsonl]\n");
+    return 2;
+  }
+  const std::string sib =
+      argc > 2 ? std::string(argv[2]) : std::string(argv[1]) + "/proj/configs/default_sib.jsonl";
   int rc = run("esp", 2, 200000, {{0, 4096, 64}}, sib);
   TraceSpec spec;
   spec.distribution = "mixed";

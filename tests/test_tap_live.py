@@ -14,8 +14,7 @@ REF = "/root/reference"
 JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
 
 
-@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "proj", "src")), reason="reference absent")
-def test_tap_policy_live(tmp_path):
+def _build(tmp_path):
     subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "reference"], check=True,
                    stdout=subprocess.DEVNULL)
     exe = tmp_path / "tap_live"
@@ -27,6 +26,27 @@ def test_tap_policy_live(tmp_path):
          os.path.join(ROOT, "oracle", "_ref", "libespsim_ref.a"),
          f"-L{lib_dir}", "-lesp_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)],
         check=True)
+    return exe
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "proj", "src")), reason="reference absent")
+def test_tap_policy_live(tmp_path):
+    exe = _build(tmp_path)
     out = subprocess.run([str(exe), REF], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr + out.stdout
     assert out.stdout.count("events identical") == 5, out.stdout
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "proj", "src")), reason="reference absent")
+def test_tap_policy_live_b200_sib(tmp_path):
+    """Same five scenarios with the scheduler planning on the LWM-7B SIB
+    measured on a B200 (profiles/r01s2_sib_b200_7b.jsonl, tools/calibrate_sib.py):
+    decisions change with the measured costs, the tap still realises every one
+    of them bit-exactly."""
+    exe = _build(tmp_path)
+    sib = os.path.join(ROOT, "profiles", "r01s2_sib_b200_7b.jsonl")
+    out = subprocess.run([str(exe), REF, sib], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert out.stdout.count("events identical") == 5, out.stdout
+    base = subprocess.run([str(exe), REF], capture_output=True, text=True, timeout=600)
+    assert base.stdout != out.stdout  # the measured SIB changes the plans
