@@ -302,8 +302,25 @@ def run_gpu(args):
             line["cpu_baseline"] = cpu_sample(2048)
         except Exception as e:  # report, never hide
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        line["control_plane"] = control_plane()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def control_plane():
+    """SURVEY §8 d "CPU path timing (i)": the reference engine + ESP scheduler
+    on a 2000-request mixed trace, alone and with EspTapPolicy over a
+    placement-only runtime (oracle/_ref/control_plane_bench, prebuilt where
+    the reference exists; one host thread, steady_clock)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "control_plane_bench")
+    sib = os.path.join(ROOT, "oracle", "_ref", "default_sib.jsonl")
+    if not (os.path.exists(exe) and os.path.exists(sib)):
+        return {"unavailable": "oracle/_ref/control_plane_bench not built"}
+    try:
+        out = subprocess.run([exe, sib], capture_output=True, text=True, timeout=120)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # report, never hide
+        return {"error": str(e)[:200]}
 
 
 def bench_decode(rt_prefill, abi, args, np, hbm):
