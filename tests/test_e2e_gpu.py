@@ -19,6 +19,7 @@ import pytest
 from oracle import llama_ref
 from paper_2404_09526_b200 import abi
 from tests import replay
+from tests.devices import devices
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -93,7 +94,7 @@ def test_config1_tiny_esp_prefill_and_decode():
     scale-down 2->1 (proactive retention onto instance 0), 64 decode steps."""
     path = os.path.join(GOLD, "scenario_config1_tiny.jsonl")
     head, _, _ = replay.load(path)
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     rec = Recorder(rt)
     # the final decode appends the 64th token; finish frees it
@@ -109,7 +110,7 @@ def test_config1_tight_scale_up_mid_decode():
     one request spans two instances (multi-instance split-KV + LSE combine)."""
     path = os.path.join(GOLD, "scenario_config1_tiny_tight.jsonl")
     head, _, _ = replay.load(path)
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     rec = Recorder(rt)
     replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
@@ -122,7 +123,7 @@ def test_tiny_multi_request_batches_and_masters():
     multi-master decode, scale-up/down, displaced-KV moves."""
     path = os.path.join(GOLD, "scenario_tiny_multi.jsonl")
     head, _, _ = replay.load(path)
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     rec = Recorder(rt)
     replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
@@ -138,7 +139,7 @@ def test_tiny_preempt_displaced_kv_moves():
     the moved request still match the oracle."""
     path = os.path.join(GOLD, "scenario_tiny_preempt.jsonl")
     head, _, _ = replay.load(path)
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     rec = Recorder(rt)
     replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
@@ -156,7 +157,7 @@ def test_kv_move_preserves_decode():
     prompt = np.random.default_rng(5).integers(0, shape.vocab, S).astype(np.int32)
     outs = []
     for move in (False, True):
-        rt = abi.Runtime(shape, 3, devices=[0, 0, 0], kv_capacity=1000)
+        rt = abi.Runtime(shape, 3, devices=devices(3), kv_capacity=1000)
         rt.prefill([1], [S], [0, 1], [[(0, 600), (1, 300)]], tokens=prompt)
         if move:
             rt.move_kv(1, 0, 2, 250)
@@ -182,7 +183,7 @@ def test_config3_128k_scale_down_lwm7b(transport):
         pytest.skip("8 transport domains x 7B activations exceed one GPU's HBM")
     path = os.path.join(GOLD, "scenario_config3_128k.jsonl")
     head, steps, _ = replay.load(path)
-    rt = abi.Runtime(abi.LWM_7B, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.LWM_7B, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     rec = Recorder(rt)
     replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
@@ -213,7 +214,7 @@ def test_lwm7b_layer_shape_vs_oracle():
                            vocab=32000)
     S = 1200
     prompt = np.random.default_rng(11).integers(0, shape.vocab, S).astype(np.int32)
-    rt = abi.Runtime(shape, 3, devices=[0, 0, 0], kv_capacity=800)
+    rt = abi.Runtime(shape, 3, devices=devices(3), kv_capacity=800)
     first, lg0, _ = rt.prefill([9], [S], [0, 1, 2], [[(2, 800), (1, S - 800)]], tokens=prompt,
                                want_logits=True)
     assert rt.placement(9) == {2: 800, 1: S - 800}
@@ -234,7 +235,7 @@ def test_esp_degree_invariance(d):
     S = 1500 + d
     shape = abi.TINY
     prompt = np.random.default_rng(d).integers(0, shape.vocab, S).astype(np.int32)
-    rt = abi.Runtime(shape, d, devices=[0] * d, kv_capacity=1000 if d > 1 else 2000)
+    rt = abi.Runtime(shape, d, devices=devices(d), kv_capacity=1000 if d > 1 else 2000)
     ring = list(range(d))
     # scale-down onto 2 survivors of the ring (the last position and the first)
     retain = [[(d - 1, 1000), (0, S - 1000)]] if d > 1 else [[(0, S)]]
@@ -257,7 +258,7 @@ def test_config5_mixed_trace_tiny():
     requests' first tokens and logits match the dense oracle."""
     path = os.path.join(GOLD, "scenario_config5_mixed.jsonl")
     head, _, _ = replay.load(path)
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     lens = {r["id"]: r["input_len"] for r in head["requests"]}
     checked = {r for r, n in lens.items() if 20 <= n <= 1024}
@@ -310,7 +311,7 @@ def test_chunked_prefill_baseline_tiny(transport):
     earlier KV by (peer) loads."""
     path = os.path.join(GOLD, "scenario_tiny_chunked.jsonl")
     head, _, _ = replay.load(path)
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     prompts = {r["id"]: replay.prompt_tokens(r["id"], r["input_len"]) for r in head["requests"]}
     toks = {r: [] for r in prompts}
@@ -339,7 +340,7 @@ def test_disagg_baseline_tiny():
     outputs equal the dense oracle's."""
     path = os.path.join(GOLD, "scenario_tiny_disagg.jsonl")
     head, _, _ = replay.load(path)
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     rec = Recorder(rt)
     replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
@@ -363,7 +364,7 @@ def test_config4_multi_master_decode_tiny(transport):
     head, _, _ = replay.load(path)
     n = head["requests"][0]["input_len"]
     prompts = {r["id"]: replay.prompt_tokens(r["id"], n) for r in head["requests"]}
-    rt = abi.Runtime(abi.TINY, head["instances"], devices=[0] * head["instances"],
+    rt = abi.Runtime(abi.TINY, head["instances"], devices=devices(head["instances"]),
                      kv_capacity=head["kv_capacity"])
     firsts = {}
     for r in head["requests"]:

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from paper_2404_09526_b200 import abi
+from tests.devices import devices
 from tests.test_e2e_gpu import check_against_oracle
 
 pytestmark = pytest.mark.gpu
@@ -20,7 +21,7 @@ def prompt(n, seed):
 def test_one_token_prompt(d):
     """S = 1: at d = 4 three ring positions hold no stripe of the request."""
     p = prompt(1, 3)
-    rt = abi.Runtime(abi.TINY, d, devices=[0] * d, kv_capacity=64)
+    rt = abi.Runtime(abi.TINY, d, devices=devices(d), kv_capacity=64)
     first, lg, _ = rt.prefill([0], [1], list(range(d)), [[(d - 1, 1)]], tokens=p, want_logits=True)
     assert rt.placement(0) == {d - 1: 1}
     toks, lgs = [int(first[0])], [lg[0]]
@@ -80,7 +81,7 @@ def test_split_kv_chunk_boundaries(n):
     512-slot split-KV chunk: chunk partials are LSE-combined at the master."""
     p = prompt(n, n)
     a = (2 * n) // 3
-    rt = abi.Runtime(abi.TINY, 2, devices=[0, 0], kv_capacity=2048)
+    rt = abi.Runtime(abi.TINY, 2, devices=devices(2), kv_capacity=2048)
     first, lg, _ = rt.prefill([1], [n], [0, 1], [[(0, a), (1, n - a)]], tokens=p, want_logits=True)
     out, lg2, _ = rt.decode_step([0, 1], [1], [1], want_logits=True)
     check_against_oracle(abi.TINY, p, [int(first[0]), int(out[0])], [lg[0], lg2[0]])
@@ -91,7 +92,7 @@ def test_capacity_and_master_full_errors():
     (CapacityError, AllocResult{ok=false}); a decode step whose master has no
     free slot for the appended token raises MasterFull
     (DecodeCommResult{ok=false}); the page tables are left untouched."""
-    rt = abi.Runtime(abi.TINY, 2, devices=[0, 0], kv_capacity=100)
+    rt = abi.Runtime(abi.TINY, 2, devices=devices(2), kv_capacity=100)
     with pytest.raises(abi.CapacityError):
         rt.prefill([0], [101], [0, 1], [[(0, 101)]], tokens=prompt(101, 1))
     assert rt.kv_used() == [0, 0]
