@@ -403,12 +403,10 @@ void launch_decode_v2(const dim3& grid, cudaStream_t s, const bf16* q, const Dec
                       const DecodeSlabs& slabs, int heads, float sl2, float* part_o,
                       float* part_ml) {
   constexpr int smem = NS * kWarps * kUnroll * 64 * 16;
-  static bool attr = false;
-  if (!attr) {
+  once_per_device(reinterpret_cast<const void*>(decode_attention_v2_kernel<HD, NS>), [] {
     cudaFuncSetAttribute(decode_attention_v2_kernel<HD, NS>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  });
   decode_attention_v2_kernel<HD, NS><<<grid, kWarps * 32, smem, s>>>(q, chunks, slabs, heads, sl2,
                                                                      part_o, part_ml);
 }

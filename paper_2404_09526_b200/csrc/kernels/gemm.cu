@@ -1103,8 +1103,7 @@ static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, i
                         int kb_per_cta, const GemmEpilogue& ep, cudaStream_t s,
                         float* ws = nullptr, int* tile_kb = nullptr) {
   using C = Cfg<BN, kSkinny>;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  once_per_device(reinterpret_cast<const void*>(gemm_bf16_tcgen05<BN, kSkinny>), [] {
     cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, kSkinny>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
@@ -1125,8 +1124,7 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
                                int kb_per_cta, const GemmEpilogue& ep, cudaStream_t s,
                                float* ws, int* tile_kb) {
   using C = swp::Cfg<NT>;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  once_per_device(reinterpret_cast<const void*>(gemm_skinny_swap<NT, SPLIT>), [] {
     cudaFuncSetAttribute(gemm_skinny_swap<NT, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::kSmem);
     if (SPLIT > 1 || SPLIT == -2) {

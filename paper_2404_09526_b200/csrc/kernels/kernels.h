@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
+#include <set>
 #include <utility>
 
 namespace esp::k {
@@ -232,6 +234,19 @@ inline cudaError_t launch_pdl(int cls, void (*kern)(KArgs...), dim3 grid, dim3 b
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled(cls) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Kernel function attributes (dynamic shared memory, cluster size) belong to
+// the device's context: run `set` once per (current device, kernel), so every
+// GPU of a multi-device runtime gets them.
+template <class F>
+inline void once_per_device(const void* kernel, F&& set) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.emplace(dev, kernel).second) set();
 }
 
 }  // namespace esp::k

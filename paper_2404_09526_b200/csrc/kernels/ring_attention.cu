@@ -386,8 +386,7 @@ void launch(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, 
             int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
             cudaStream_t s) {
   using C = ACfg<HD>;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  once_per_device(reinterpret_cast<const void*>(ring_attention_tcgen05<HD>), [] {
     cudaFuncSetAttribute(ring_attention_tcgen05<HD>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });

@@ -592,8 +592,7 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s, uint64_t* prof) {
   using C = Cfg2<HD>;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  once_per_device(reinterpret_cast<const void*>(ring_attention_v2<HD, kProf, kPoly8>), [] {
     cudaFuncSetAttribute(ring_attention_v2<HD, kProf, kPoly8>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });

@@ -520,8 +520,7 @@ void launch4(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s) {
   using C = Cfg4<HD>;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  once_per_device(reinterpret_cast<const void*>(ring_attention_v4<HD, kPoly8>), [] {
     cudaFuncSetAttribute(ring_attention_v4<HD, kPoly8>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
