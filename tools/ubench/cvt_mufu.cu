@@ -4,11 +4,13 @@
 //   ex2 only | cvt only | ex2 + cvt (softmax ratio: 1 pack per 2 ex2)
 //   | ex2 + integer-rounded pack (IADD + PRMT, no F2FP)
 //   | pack + ex2.approx.ftz.bf16x2 (one MUFU op per pair?) + unpack
+//   | the same with ex2.approx.f16x2
 // with 8 warps per SM (the two softmax warpgroups). If F2FP rides the MUFU
 // pipe the mixed loop costs the sum of the two alone.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o cvt_mufu cvt_mufu.cu
 #include <cstdio>
 #include <cstdint>
+#include <cuda_fp16.h>
 
 constexpr int kIters = 4096;
 
@@ -36,6 +38,12 @@ __device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
   return y;
 }
 
+__device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 1) bench(float* out, long long* cyc, float seed) {
   float v[16];
@@ -54,6 +62,13 @@ __global__ void __launch_bounds__(256, 1) bench(float* out, long long* cyc, floa
       }
       if (MODE == 1 || MODE == 2) acc ^= cvt_pack(a, b);
       if (MODE == 3) acc ^= int_pack(a, b);
+      if (MODE == 5) {  // f16x2 pack, one f16x2 ex2 for the pair, unpack
+        __half2 h = __floats2half2_rn(a, b);
+        const uint32_t p = ex2_f16x2(*reinterpret_cast<uint32_t*>(&h));
+        const __half2 q = *reinterpret_cast<const __half2*>(&p);
+        a = __low2float(q);
+        b = __high2float(q);
+      }
       if (MODE == 4) {  // pack, one bf16x2 ex2 for the pair, unpack
         const uint32_t p = ex2_bf16x2(cvt_pack(a, b));
         a = __uint_as_float(p << 16);
@@ -96,5 +111,6 @@ int main() {
   run<2>("ex2 x2 + F2FP", sms, out, cyc);
   run<3>("ex2 x2 + IADD/PRMT pack", sms, out, cyc);
   run<4>("F2FP + ex2.bf16x2 + unpack", sms, out, cyc);
+  run<5>("F2FP + ex2.f16x2 + unpack", sms, out, cyc);
   return 0;
 }
