@@ -291,6 +291,8 @@ def run_gpu(args):
         line["esp_degrees"] = bench_esp_sweep(abi, args, np, tf_sust)
     if rank == 0 and not args.skip_decode and not args.skip_esp_sweep:
         line["decode_esp_degrees"] = bench_decode_degrees(abi, args, np, hbm)
+    if rank == 0 and not args.skip_decode and not args.skip_scale_down:
+        line["chunked_prefill"] = bench_chunked(abi, args, np)
     if rank == 0 and not args.skip_config3:
         line["config3_128k"] = bench_config3(abi, args, np, tf_sust)
     if rank == 0 and not args.skip_scale_down:
@@ -374,6 +376,48 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
                          "algorithmic": f"K+V bytes of one layer = 2*H*2*sum(ctx) = {kv_bytes / L:.4e} B per launch"},
             "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
             "phase_ms": {p: round(v[0] / max(len(ms), 1), 4) for p, v in ph.items() if v[1] > 0}}
+
+
+def bench_chunked(abi, args, np):
+    """SURVEY §8 f3 baseline cost on the same kernels: a 2048-token chunk of a
+    32K-token prompt riding on the b x ctx decode step (engine.cpp:432-462),
+    one instance. For each chunk the step is timed with and without it; the
+    chunk's attention phase (gather of the request's earlier KV from its page
+    slots + K1 over it) is split out by one profiled step."""
+    b, ctx, S, C = args.decode_batch, args.decode_ctx, 32768, 2048
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    rt = abi.Runtime(abi.LWM_7B, 1, devices=[dev],
+                     kv_capacity=b * (ctx + 2 * (S // C) + 16) + S + 64)
+    rng = np.random.default_rng(23)
+    for r in range(b):
+        rt.prefill([r], [ctx], [0], [[(0, ctx)]], tokens=rng.integers(0, V, ctx).astype(np.int32))
+    prompt = rng.integers(0, V, S).astype(np.int32)
+    batch = list(range(b))
+    rows = []
+    for i in range(S // C):
+        rt.decode_step([0], [0], batch)  # plain step, same batch
+        plain = rt.decode_step([0], [0], batch)[2]
+        ch = {"request": 1000, "placement": [(0, C)], "tokens": prompt[i * C:(i + 1) * C],
+              "final": (i + 1) * C == S}
+        prof = i in (S // C // 2, S // C - 1)
+        if prof:
+            rt.phase_times()
+            rt.set_profiling(True)
+        t = rt.decode_step([0], [0], batch, chunk=ch)[2]
+        if prof:
+            rt.set_profiling(False)
+            ph = rt.phase_times()
+            rows.append({"prefilled": i * C, "step_ms": round(t, 3), "plain_ms": round(plain, 3),
+                         "chunk_ms": round(t - plain, 3),
+                         "chunk_attention_ms": round(ph["ring_attention"][0], 3),
+                         "chunk_tokens_per_s": round(C / ((t - plain) / 1e3))})
+    rt.close()
+    return {"config": f"LWM-7B, decode batch {b} x {ctx} + one {C}-token chunk of a {S}-token "
+                      "prompt per step, 1 instance (chunked-prefill baseline)",
+            "chunks": rows,
+            "note": "chunk_attention_ms = gather of the earlier KV rows from their page slots "
+                    "(K/V copied into contiguous buffers every layer) + K1 (under per-phase "
+                    "events, so the profiled step itself is slightly slower)"}
 
 
 def bench_decode_degrees(abi, args, np, hbm):
