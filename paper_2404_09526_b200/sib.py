@@ -17,7 +17,7 @@ reference's unchanged scheduler and engine then plan with.
 import json
 import os
 import tempfile
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -54,7 +54,7 @@ def _decode_x(samples: Dict[str, np.ndarray], threshold: int):
 
 
 def calibrate(base: Sequence[dict], prefill: Sequence[dict],
-              decode: Optional[Dict[str, np.ndarray]]) -> (List[dict], dict):
+              decode: Optional[Dict[str, np.ndarray]]) -> Tuple[List[dict], dict]:
     """New SIB records (one per base record's (dop, tp)) and a fit report:
     per degree, sample counts, coefficients and the max relative error of the
     fitted model on its own samples. Degrees without >= 3 samples of a phase
@@ -101,9 +101,9 @@ def _spread(ring: Sequence[int], n: int):
     return [(int(i), int(t)) for i, t in zip(ring, per) if t > 0]
 
 
-def measure(rt: "abi.Runtime", n_instances: int, prefill_lengths: Sequence[Sequence[int]],
+def measure(rt: "abi.Runtime", prefill_lengths: Sequence[Sequence[int]],
             decode_cfgs: Sequence[tuple], degrees: Sequence[int], repeats: int = 2,
-            seed: int = 7) -> (List[dict], Dict[str, np.ndarray]):
+            seed: int = 7) -> Tuple[List[dict], Dict[str, np.ndarray]]:
     """Prefill and decode sweeps on instances 0..d-1 of `rt` for each degree d.
     prefill_lengths: request length lists (one prefill each); decode_cfgs:
     (batch, context, masters) — the batch is prefilled on the ring, then

@@ -28,7 +28,7 @@ def test_calibrated_sib_drives_reference_scheduler(tmp_path):
 
     rt = abi.Runtime(abi.TINY, 8, devices=[0] * 8, kv_capacity=40000)
     pre, dec = sib.measure(
-        rt, 8,
+        rt,
         prefill_lengths=[[256], [1024], [2048], [512, 1536], [4096], [3000, 3000]],
         decode_cfgs=[(1, 512, 1), (4, 1024, 1), (8, 2048, 2), (16, 1024, 2), (16, 256, 1)],
         degrees=range(1, 9), repeats=2)

@@ -44,7 +44,7 @@ def main():
         cap = 40000
     t0 = time.time()
     rt = abi.Runtime(shape, len(devices), devices=devices, kv_capacity=cap)
-    pre, dec = sib.measure(rt, len(devices), lengths, dcfgs, degrees=range(1, len(devices) + 1),
+    pre, dec = sib.measure(rt, lengths, dcfgs, degrees=range(1, len(devices) + 1),
                            repeats=2)
     rt.close()
     recs, report = sib.calibrate(sib.load_sib(a.base), pre, dec)
