@@ -87,13 +87,16 @@ class EspTapPolicy final : public espsim::Policy {
   espsim::ScheduleDecision schedule(const espsim::SimState& state,
                                     const espsim::BandwidthModel& bw) override {
     reconcile(state);
-    verify(state);
+    if (verify_every_ > 0 && calls_++ % verify_every_ == 0) verify(state);
     espsim::ScheduleDecision d = inner_->schedule(state, bw);
     execute(state, d);
     ++decisions_;
     return d;
   }
 
+  // Page-table verification on every n-th schedule() call (1, the default:
+  // every call; 0: never — the tap then only reconciles and executes).
+  void set_verify_every(int64_t n) { verify_every_ = n; }
   int64_t decisions() const { return decisions_; }
   int64_t verified_requests() const { return verified_; }
 
@@ -246,6 +249,8 @@ class EspTapPolicy final : public espsim::Policy {
   std::set<espsim::RequestId> live_;
   int64_t decisions_ = 0;
   int64_t verified_ = 0;
+  int64_t verify_every_ = 1;
+  int64_t calls_ = 0;
 };
 
 }  // namespace esp_integration

@@ -4,7 +4,8 @@
 //   untapped : the reference alone (a counting decorator counts schedule() calls)
 //   tapped   : EspTapPolicy over a placement-only runtime — the drop-in's host
 //              cost per iteration (reconcile, page-table verification of every
-//              live request, executing each decision's page-table effects)
+//              live request, executing each decision's page-table effects),
+//              and again with verification off (set_verify_every(0))
 // Prints one JSON object. Built by oracle/Makefile into oracle/_ref/.
 // usage: control_plane_bench <default_sib.jsonl> [requests]
 #include <chrono>
@@ -91,16 +92,36 @@ int main(int argc, char** argv) {
   const double t_tap = seconds_since(t0);
   const bool same = plain.log().events() == tapped.log().events();
   esp_runtime_destroy(rt);
+
+  // The same with page-table verification off: the tap's execution cost alone.
+  esp_runtime* rt2 = nullptr;
+  if (esp_runtime_create(&cfg, instances, nullptr, cap, &rt2) != ESP_OK) {
+    std::cerr << "create: " << esp_last_error() << "\n";
+    return 2;
+  }
+  auto tap2 = std::make_unique<esp_integration::EspTapPolicy>(make_policy(parse_policy("esp")),
+                                                              rt2, /*with_tokens=*/false);
+  tap2->set_verify_every(0);
+  Engine tapped2(KvPool(instances, cap), model, Sib::load(sib_path), std::move(tap2), params);
+  tapped2.submit(trace);
+  t0 = std::chrono::steady_clock::now();
+  tapped2.run();
+  const double t_tap2 = seconds_since(t0);
+  const bool same2 = plain.log().events() == tapped2.log().events();
+  esp_runtime_destroy(rt2);
   const double it = static_cast<double>(cp->calls);
   std::printf(
       "{\"trace\": \"mixed, %lld requests at 1 req/s, seed 7, 8 instances x %lld slots, esp\", "
       "\"iterations\": %lld, \"events\": %zu, \"events_identical\": %s, "
       "\"untapped_ms\": %.3f, \"untapped_us_per_iteration\": %.3f, "
       "\"tapped_ms\": %.3f, \"tapped_us_per_iteration\": %.3f, "
-      "\"tap_overhead_us_per_iteration\": %.3f, \"page_table_checks\": %lld, \"threads\": 1}\n",
+      "\"tap_overhead_us_per_iteration\": %.3f, \"page_table_checks\": %lld, "
+      "\"tapped_no_verify_ms\": %.3f, \"tap_overhead_no_verify_us_per_iteration\": %.3f, "
+      "\"threads\": 1}\n",
       static_cast<long long>(spec.count), static_cast<long long>(cap),
       static_cast<long long>(cp->calls), plain.log().events().size(), same ? "true" : "false",
       t_plain * 1e3, t_plain * 1e6 / it, t_tap * 1e3, t_tap * 1e6 / it,
-      (t_tap - t_plain) * 1e6 / it, static_cast<long long>(tp->verified_requests()));
-  return same ? 0 : 1;
+      (t_tap - t_plain) * 1e6 / it, static_cast<long long>(tp->verified_requests()),
+      t_tap2 * 1e3, (t_tap2 - t_plain) * 1e6 / it);
+  return same && same2 ? 0 : 1;
 }
