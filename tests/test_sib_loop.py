@@ -134,3 +134,29 @@ def test_sib_records_round_trip(tmp_path):
     subprocess.run([DRIVER, "fit", str(out), str(fitted)], check=True)
     again = [json.loads(l) for l in fitted.read_text().splitlines() if l.strip()]
     assert len(again) == len(recs)
+
+
+def test_decode_design_matches_sib_decode_time():
+    """The decode fit's regressors are Sib::decode_time's (cost_model.cpp:175-187):
+    with the fitted coefficients, alpha + beta*x1 + gamma*x2 must equal the
+    runtime's restated decode_time (esp_sib_decode_time) for batches on both
+    sides of the compute-bound threshold and any masters / dop."""
+    import numpy as np
+
+    from paper_2404_09526_b200 import abi, sib
+
+    smp = {"dop": np.array([1, 2, 4, 8, 4, 2], np.int32),
+           "batch": np.array([1, 16, 64, 65, 128, 200], np.int32),
+           "masters": np.array([1, 2, 1, 2, 4, 3], np.int32),
+           "resident": np.array([4096, 70000, 300000, 900000, 1200000, 50000], np.int64),
+           "ms": np.zeros(6)}
+    x1, x2 = sib._decode_x(smp, 64)
+    rec = {"dop": 0, "tp": 1, "alpha_p": 1.0, "beta_p": 0.0, "gamma_p": 0.0, "alpha_d": 3.5,
+           "beta_d": 0.07, "gamma_d": 2e-5, "compute_bound_batch_threshold": 64,
+           "tipping_ms": 0.0}
+    for i in range(6):
+        r = dict(rec, dop=int(smp["dop"][i]))
+        want = abi.sib_decode_time([r], r["dop"], 1, int(smp["batch"][i]),
+                                   int(smp["resident"][i]), int(smp["masters"][i]))
+        got = 3.5 + 0.07 * x1[i] + 2e-5 * x2[i]
+        assert got == pytest.approx(want, rel=1e-12), (i, got, want)
