@@ -268,6 +268,27 @@ int esp_check_conservation(esp_runtime* rt);
 int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int32_t cap,
                        int32_t* n);
 
+/* Parity readback of a request's KV cache, one layer: K (after RoPE) and V
+ * rows in TOKEN order (position 0 first), wherever the page tables put them
+ * (any instance, any slot), as bf16 [n x hidden] into host buffers k_out /
+ * v_out of cap rows. *n = the request's KV token count; with cap < *n
+ * nothing is copied (size query). Device runtimes only (ESP_ERR_NO_DEVICE). */
+int esp_read_kv(esp_runtime* rt, int64_t request, int32_t layer, void* k_out, void* v_out,
+                int64_t cap, int64_t* n);
+
+/* Parity capture of the NEXT esp_prefill (single-request plan): the
+ * attention outputs (before the O projection) of the prompt positions
+ * pos[0..n) in every layer. esp_captured_attention then copies them as bf16
+ * [layers x n x hidden] (cap rows of hidden; *n_rows = layers * n; with
+ * cap < *n_rows nothing is copied). */
+int esp_capture_attention(esp_runtime* rt, const int64_t* pos, int64_t n);
+int esp_captured_attention(esp_runtime* rt, void* out, int64_t cap, int64_t* n_rows);
+
+/* 1 in *ok iff every mapped chunk of the instance's K and V slabs is
+ * read/write for CUDA device `device` (cuMemGetAccess) — the VMM mappings
+ * a cross-GPU ring / KV move dereferences from another device. */
+int esp_slab_access(const esp_runtime* rt, int32_t instance, int32_t device, int32_t* ok);
+
 /* Measured ProfileSample records ({"kind":"profile","dop","tp","lengths",
  * "measured_ms"}, cost_model.cpp:243-248) appended to a JSONL file. */
 int esp_dump_profiles(const esp_runtime* rt, const char* path);

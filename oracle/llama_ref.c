@@ -194,14 +194,122 @@ static void model_free(model* m) {
   free(m->vc);
 }
 
+/* Causal softmax attention of nq query rows (absolute positions qpos[],
+ * ascending; row i sees keys 0..qpos[i]) against the cache K/V [* x H]:
+ * per (head, row) s_j = q.k_j / sqrt(hd), p_j = exp(s_j - max) (two-pass,
+ * exact max), o = sum_j p_j v_j / sum_j p_j, rounded to bf16 when rb.
+ * Blocked for the CPU (the GPU path's tiling is irrelevant here): the keys of
+ * one head are transposed once to [hd][nk] so a block of query rows computes
+ * its scores vectorised over keys, and P.V vectorised over the head dim with
+ * each V row read once per block. */
+#define ATT_RB 16
+#define ATT_KC 64
+static void attend(const float* q, int64_t nq, const int64_t* qpos, const float* K,
+                   const float* V, int64_t H, int heads, int hd, int rb, float* out) {
+  if (nq <= 0) return;
+  const int64_t nk = qpos[nq - 1] + 1;
+  const int64_t nkp = (nk + ATT_KC - 1) / ATT_KC * ATT_KC;
+  float* KT = (float*)malloc(sizeof(float) * (size_t)heads * hd * nkp);
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int h = 0; h < heads; ++h) {
+    for (int d = 0; d < hd; ++d) {
+      float* dst = KT + ((int64_t)h * hd + d) * nkp;
+      for (int64_t j = 0; j < nk; ++j) dst[j] = K[j * H + (int64_t)h * hd + d];
+      for (int64_t j = nk; j < nkp; ++j) dst[j] = 0.f;
+    }
+  }
+  const float scale = 1.0f / sqrtf((float)hd);
+  const int64_t nb = (nq + ATT_RB - 1) / ATT_RB;
+#pragma omp parallel
+  {
+    float* sc = (float*)malloc(sizeof(float) * ATT_RB * nkp);
+#pragma omp for collapse(2) schedule(dynamic, 1)
+    for (int64_t bi = nb - 1; bi >= 0; --bi) { /* dearest (latest) blocks first */
+      for (int h = 0; h < heads; ++h) {
+        const int64_t r0 = bi * ATT_RB;
+        const int64_t r1 = r0 + ATT_RB < nq ? r0 + ATT_RB : nq;
+        const int64_t kmax = qpos[r1 - 1] + 1;
+        const float* kt = KT + (int64_t)h * hd * nkp;
+        double inv[ATT_RB];
+        for (int64_t r = r0; r < r1; ++r) {
+          const float* qv = q + r * H + (int64_t)h * hd;
+          float* srow = sc + (r - r0) * nkp;
+          const int64_t kr = qpos[r] + 1;
+          for (int64_t j0 = 0; j0 < kr; j0 += ATT_KC) {
+            float acc[ATT_KC];
+            for (int jj = 0; jj < ATT_KC; ++jj) acc[jj] = 0.f;
+            for (int d = 0; d < hd; ++d) {
+              const float qd = qv[d];
+              const float* kd = kt + (int64_t)d * nkp + j0;
+#pragma omp simd
+              for (int jj = 0; jj < ATT_KC; ++jj) acc[jj] += qd * kd[jj];
+            }
+            for (int jj = 0; jj < ATT_KC; ++jj) srow[j0 + jj] = acc[jj] * scale;
+          }
+          float mx = -3.0e38f;
+          for (int64_t j = 0; j < kr; ++j) mx = srow[j] > mx ? srow[j] : mx;
+          double sum = 0;
+          for (int64_t j = 0; j < kr; ++j) {
+            srow[j] = expf(srow[j] - mx);
+            sum += srow[j];
+          }
+          for (int64_t j = kr; j < kmax; ++j) srow[j] = 0.f; /* causal: unseen keys */
+          inv[r - r0] = 1.0 / sum;
+        }
+        float o[ATT_RB][128];
+        for (int64_t r = r0; r < r1; ++r) {
+          for (int d = 0; d < hd; ++d) o[r - r0][d] = 0.f;
+        }
+        for (int64_t j = 0; j < kmax; ++j) {
+          const float* vv = V + j * H + (int64_t)h * hd;
+          for (int64_t r = r0; r < r1; ++r) {
+            const float p = sc[(r - r0) * nkp + j];
+            float* orow = o[r - r0];
+#pragma omp simd
+            for (int d = 0; d < hd; ++d) orow[d] += p * vv[d];
+          }
+        }
+        for (int64_t r = r0; r < r1; ++r) {
+          float* dst = out + r * H + (int64_t)h * hd;
+          for (int d = 0; d < hd; ++d) {
+            const float v = (float)(o[r - r0][d] * inv[r - r0]);
+            dst[d] = rb ? bf16_round(v) : v;
+          }
+        }
+      }
+    }
+    free(sc);
+  }
+  free(KT);
+}
+
+/* Optional per-call captures of a prefill (parity at BASELINE sizes):
+ *   attn[l][i][:]   attention output (pre O-proj) of the row at position
+ *                   attn_pos[i] in layer l            (n_attn rows, nullable)
+ *   kcap/vcap[l][i] the cached K (after RoPE) / V of the row at kv_pos[i]
+ *                   in layer l                         (n_kv rows, nullable)
+ * With `last_only`, the LAST layer computes queries, attention, O and MLP
+ * only for the captured rows and the final row (logits need nothing else);
+ * every earlier layer is computed in full. */
+typedef struct {
+  int64_t n_attn;
+  const int64_t* attn_pos;
+  float* attn;
+  int64_t n_kv;
+  const int64_t* kv_pos;
+  float* kcap;
+  float* vcap;
+  int last_only;
+} probe_t;
+
 /* Runs T new tokens (positions len..len+T-1) through the model, appending
  * their K/V; writes fp32 logits of the LAST new token into `logits`. */
-static void forward(model* m, const int32_t* tok, int64_t T, float* logits) {
+static void forward(model* m, const int32_t* tok, int64_t T, float* logits, const probe_t* pr) {
   const llama_cfg* c = &m->c;
   const int64_t H = c->hidden, F = c->ffn, V = c->vocab;
   const int heads = c->heads, hd = c->head_dim;
   const int rb = m->rb;
-  const int64_t p0 = m->len;
+  const int64_t p0 = m->len, T0 = T;
   float* x = (float*)malloc(sizeof(float) * T * H);
   float* xn = (float*)malloc(sizeof(float) * T * H);
   float* q = (float*)malloc(sizeof(float) * T * H);
@@ -212,89 +320,102 @@ static void forward(model* m, const int32_t* tok, int64_t T, float* logits) {
   float* g = (float*)malloc(sizeof(float) * T * F);
   float* u = (float*)malloc(sizeof(float) * T * F);
   int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * T);
+  int64_t* sel = (int64_t*)malloc(sizeof(int64_t) * (T + 1)); /* last-layer rows (local) */
+  int64_t* selpos = (int64_t*)malloc(sizeof(int64_t) * (T + 1));
   for (int64_t t = 0; t < T; ++t) {
     pos[t] = p0 + t;
     memcpy(x + t * H, m->emb + (int64_t)tok[t] * H, sizeof(float) * H);
   }
-  const float scale = 1.0f / sqrtf((float)hd);
   for (int l = 0; l < c->layers; ++l) {
     layer_w* w = &m->L[l];
+    const int partial = pr && pr->last_only && l == c->layers - 1 && T > 1;
+    /* rows whose queries / outputs this layer needs (all, or the probes + last) */
+    int64_t ns = 0;
+    if (partial) {
+      char* want = (char*)calloc((size_t)T, 1);
+      for (int64_t i = 0; i < pr->n_attn; ++i) {
+        const int64_t t = pr->attn_pos[i] - p0;
+        if (t >= 0 && t < T) want[t] = 1;
+      }
+      want[T - 1] = 1;
+      for (int64_t t = 0; t < T; ++t) {
+        if (want[t]) sel[ns++] = t;
+      }
+      free(want);
+    } else {
+      for (int64_t t = 0; t < T; ++t) sel[ns++] = t;
+    }
+    for (int64_t i = 0; i < ns; ++i) selpos[i] = pos[sel[i]];
     rmsnorm(x, T, H, c->rms_eps, rb, xn);
-    gemm_nt(xn, T, H, w->wq, H, q);
     gemm_nt(xn, T, H, w->wk, H, k);
     gemm_nt(xn, T, H, w->wv, H, v);
-    rope_rows(q, T, heads, hd, pos, c->rope_theta);
     rope_rows(k, T, heads, hd, pos, c->rope_theta);
+    if (partial) { /* compact the selected rows */
+      for (int64_t i = 0; i < ns; ++i) {
+        memmove(xn + i * H, xn + sel[i] * H, sizeof(float) * H);
+        memmove(x + i * H, x + sel[i] * H, sizeof(float) * H);
+      }
+    }
+    gemm_nt(xn, ns, H, w->wq, H, q);
+    rope_rows(q, ns, heads, hd, selpos, c->rope_theta);
     if (rb) {
+      for (int64_t i = 0; i < ns * H; ++i) q[i] = bf16_round(q[i]);
       for (int64_t i = 0; i < T * H; ++i) {
-        q[i] = bf16_round(q[i]);
         k[i] = bf16_round(k[i]);
         v[i] = bf16_round(v[i]);
       }
     }
     memcpy(m->kc[l] + p0 * H, k, sizeof(float) * T * H);
     memcpy(m->vc[l] + p0 * H, v, sizeof(float) * T * H);
-    const float* K = m->kc[l];
-    const float* Vc = m->vc[l];
-#pragma omp parallel for collapse(2) schedule(dynamic, 8)
-    for (int64_t t = 0; t < T; ++t) {
-      for (int h = 0; h < heads; ++h) {
-        const int64_t nk = p0 + t + 1; /* causal: keys 0..pos */
-        const float* qv = q + t * H + (int64_t)h * hd;
-        float* sc = (float*)malloc(sizeof(float) * nk);
-        float mx = -3.0e38f;
-        for (int64_t j = 0; j < nk; ++j) {
-          const float* kv = K + j * H + (int64_t)h * hd;
-          float s = 0.f;
-#pragma omp simd reduction(+ : s)
-          for (int d = 0; d < hd; ++d) s += qv[d] * kv[d];
-          s *= scale;
-          sc[j] = s;
-          if (s > mx) mx = s;
-        }
-        double sum = 0;
-        for (int64_t j = 0; j < nk; ++j) {
-          sc[j] = expf(sc[j] - mx);
-          sum += sc[j];
-        }
-        float o[128];
-        for (int d = 0; d < hd; ++d) o[d] = 0.f;
-        for (int64_t j = 0; j < nk; ++j) {
-          const float p = sc[j];
-          const float* vv = Vc + j * H + (int64_t)h * hd;
-          for (int d = 0; d < hd; ++d) o[d] += p * vv[d];
-        }
-        float* dst = att + t * H + (int64_t)h * hd;
-        for (int d = 0; d < hd; ++d) {
-          const float r = (float)(o[d] / sum);
-          dst[d] = rb ? bf16_round(r) : r;
-        }
-        free(sc);
+    if (pr && pr->n_kv > 0 && pr->kcap) {
+      for (int64_t i = 0; i < pr->n_kv; ++i) {
+        const int64_t p = pr->kv_pos[i];
+        memcpy(pr->kcap + ((int64_t)l * pr->n_kv + i) * H, m->kc[l] + p * H, sizeof(float) * H);
+        memcpy(pr->vcap + ((int64_t)l * pr->n_kv + i) * H, m->vc[l] + p * H, sizeof(float) * H);
       }
     }
-    gemm_nt(att, T, H, w->wo, H, tmp);
-    for (int64_t i = 0; i < T * H; ++i) {
+    attend(q, ns, selpos, m->kc[l], m->vc[l], H, heads, hd, rb, att);
+    if (pr && pr->n_attn > 0 && pr->attn) {
+      for (int64_t i = 0; i < pr->n_attn; ++i) {
+        for (int64_t j = 0; j < ns; ++j) {
+          if (selpos[j] == pr->attn_pos[i]) {
+            memcpy(pr->attn + ((int64_t)l * pr->n_attn + i) * H, att + j * H, sizeof(float) * H);
+            break;
+          }
+        }
+      }
+    }
+    int64_t nr = ns;
+    const float* a_in = att;
+    if (partial) { /* only the final row continues to the logits */
+      memmove(x, x + (ns - 1) * H, sizeof(float) * H);
+      a_in = att + (ns - 1) * H;
+      nr = 1;
+    }
+    gemm_nt(a_in, nr, H, w->wo, H, tmp);
+    for (int64_t i = 0; i < nr * H; ++i) {
       const float r = x[i] + tmp[i];
       x[i] = rb ? bf16_round(r) : r;
     }
-    rmsnorm(x, T, H, c->rms_eps, rb, xn);
-    gemm_nt(xn, T, H, w->wg, F, g);
-    gemm_nt(xn, T, H, w->wu, F, u);
-    for (int64_t i = 0; i < T * F; ++i) {
+    rmsnorm(x, nr, H, c->rms_eps, rb, xn);
+    gemm_nt(xn, nr, H, w->wg, F, g);
+    gemm_nt(xn, nr, H, w->wu, F, u);
+    for (int64_t i = 0; i < nr * F; ++i) {
       const float a = g[i] / (1.0f + expf(-g[i])) * u[i];
       g[i] = rb ? bf16_round(a) : a;
     }
-    gemm_nt(g, T, F, w->wd, H, tmp);
-    for (int64_t i = 0; i < T * H; ++i) {
+    gemm_nt(g, nr, F, w->wd, H, tmp);
+    for (int64_t i = 0; i < nr * H; ++i) {
       const float r = x[i] + tmp[i];
       x[i] = rb ? bf16_round(r) : r;
     }
+    if (partial) T = 1; /* x now holds the final row only */
   }
   rmsnorm(x + (T - 1) * H, 1, H, c->rms_eps, rb, xn);
   gemm_nt(xn, 1, H, m->lm, V, logits);
-  m->len += T;
+  m->len = p0 + T0;
   free(x); free(xn); free(q); free(k); free(v); free(att); free(tmp); free(g); free(u);
-  free(pos);
+  free(pos); free(sel); free(selpos);
 }
 
 static int32_t argmax(const float* l, int64_t V) {
@@ -317,18 +438,88 @@ int llama_ref_generate(const llama_cfg* c, const int32_t* prompt, int64_t S, int
   model m;
   model_init(&m, c, S + n_steps + 1, emulate_bf16);
   float* lg = (float*)malloc(sizeof(float) * c->vocab);
-  forward(&m, prompt, S, lg);
+  forward(&m, prompt, S, lg, NULL);
   out_tokens[0] = argmax(lg, c->vocab);
   if (out_logits) memcpy(out_logits, lg, sizeof(float) * c->vocab);
   for (int s = 1; s <= n_steps; ++s) {
     int32_t in = forced ? forced[s - 1] : out_tokens[s - 1];
-    forward(&m, &in, 1, lg);
+    forward(&m, &in, 1, lg, NULL);
     out_tokens[s] = argmax(lg, c->vocab);
     if (out_logits) memcpy(out_logits + (int64_t)s * c->vocab, lg, sizeof(float) * c->vocab);
   }
   free(lg);
   model_free(&m);
   return 0;
+}
+
+/* Prefill only, with captures (see probe_t): attention outputs of the rows at
+ * attn_pos[n_attn] and the cached K/V rows at kv_pos[n_kv], per layer
+ * ([layers][n][hidden] fp32, nullable). last_only: the last layer computes
+ * only the captured rows and the final one. Writes the final row's logits
+ * (nullable) and returns its greedy token. */
+int32_t llama_ref_prefill_probe(const llama_cfg* c, const int32_t* prompt, int64_t S,
+                                int emulate_bf16, int64_t n_attn, const int64_t* attn_pos,
+                                float* attn_out, int64_t n_kv, const int64_t* kv_pos,
+                                float* k_out, float* v_out, int last_only, float* logits_out,
+                                int n_threads) {
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+  model m;
+  model_init(&m, c, S, emulate_bf16);
+  float* lg = (float*)malloc(sizeof(float) * c->vocab);
+  probe_t pr = {n_attn, attn_pos, attn_out, n_kv, kv_pos, k_out, v_out, last_only};
+  forward(&m, prompt, S, lg, &pr);
+  const int32_t tok = argmax(lg, c->vocab);
+  if (logits_out) memcpy(logits_out, lg, sizeof(float) * c->vocab);
+  free(lg);
+  model_free(&m);
+  return tok;
+}
+
+static float bf16_to_f32(uint16_t h) {
+  const uint32_t u = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+/* One decode step at position n_ctx for a request whose KV cache is GIVEN
+ * (bf16 [layers][n_ctx][hidden], token order, after RoPE) — the teacher-
+ * forced check of multi-master decoding: the cache is read back from the
+ * device, so the step's arithmetic (q, split-KV attention + LSE combine
+ * across instances, O, MLP, LM head) is checked on its own. Outputs (each
+ * nullable): logits [vocab], the step's new K/V rows [layers][hidden] and
+ * attention outputs [layers][hidden]. Returns the greedy token. */
+int32_t llama_ref_decode_cached(const llama_cfg* c, int64_t n_ctx, const uint16_t* k_cache,
+                                const uint16_t* v_cache, int32_t token, int emulate_bf16,
+                                float* logits_out, float* k_new, float* v_new, float* attn_out,
+                                int n_threads) {
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+  model m;
+  model_init(&m, c, n_ctx + 1, emulate_bf16);
+  const int64_t H = c->hidden;
+  for (int l = 0; l < c->layers; ++l) {
+    const uint16_t* ks = k_cache + (int64_t)l * n_ctx * H;
+    const uint16_t* vs = v_cache + (int64_t)l * n_ctx * H;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_ctx * H; ++i) {
+      m.kc[l][i] = bf16_to_f32(ks[i]);
+      m.vc[l][i] = bf16_to_f32(vs[i]);
+    }
+  }
+  m.len = n_ctx;
+  float* lg = (float*)malloc(sizeof(float) * c->vocab);
+  int64_t at = n_ctx;
+  float* kc = k_new ? k_new : (float*)malloc(sizeof(float) * c->layers * H);
+  float* vc = v_new ? v_new : (float*)malloc(sizeof(float) * c->layers * H);
+  probe_t pr = {attn_out ? 1 : 0, &at, attn_out, 1, &at, kc, vc, 0};
+  forward(&m, &token, 1, lg, &pr);
+  const int32_t tok = argmax(lg, c->vocab);
+  if (logits_out) memcpy(logits_out, lg, sizeof(float) * c->vocab);
+  if (!k_new) free(kc);
+  if (!v_new) free(vc);
+  free(lg);
+  model_free(&m);
+  return tok;
 }
 
 int llama_ref_max_threads(void) { return omp_get_max_threads(); }

@@ -42,8 +42,25 @@ def lib():
         h.llama_ref_generate.argtypes = [C.POINTER(LlamaCfg), C.POINTER(C.c_int32), C.c_int64,
                                          C.c_int, C.POINTER(C.c_int32), C.c_int,
                                          C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int]
+        i64p, f32p, i32p = C.POINTER(C.c_int64), C.POINTER(C.c_float), C.POINTER(C.c_int32)
+        h.llama_ref_prefill_probe.restype = C.c_int32
+        h.llama_ref_prefill_probe.argtypes = [C.POINTER(LlamaCfg), i32p, C.c_int64, C.c_int,
+                                              C.c_int64, i64p, f32p, C.c_int64, i64p, f32p, f32p,
+                                              C.c_int, f32p, C.c_int]
+        h.llama_ref_decode_cached.restype = C.c_int32
+        h.llama_ref_decode_cached.argtypes = [C.POINTER(LlamaCfg), C.c_int64,
+                                              C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
+                                              C.c_int32, C.c_int, f32p, f32p, f32p, f32p, C.c_int]
         _lib = h
     return _lib
+
+
+def _f32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float)) if a is not None else None
+
+
+def _i64(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int64)) if a is not None else None
 
 
 def cfg_from(shape) -> LlamaCfg:
@@ -72,3 +89,45 @@ def generate(shape, prompt, n_steps, forced=None, emulate_bf16=True, want_logits
         1 if emulate_bf16 else 0, out.ctypes.data_as(C.POINTER(C.c_int32)),
         lg.ctypes.data_as(C.POINTER(C.c_float)) if lg is not None else None, threads)
     return out, lg
+
+
+def prefill_probe(shape, prompt, attn_pos=(), kv_pos=(), emulate_bf16=True, last_only=True,
+                  threads=0):
+    """Dense prefill of `prompt` with captures (llama_ref.c:llama_ref_prefill_probe).
+    Returns (greedy token, logits[vocab], attn[layers, n_attn, hidden] or None,
+    k[layers, n_kv, hidden] or None, v[...] or None)."""
+    c = cfg_from(shape)
+    p = np.ascontiguousarray(np.asarray(prompt, np.int32))
+    ap = np.ascontiguousarray(np.asarray(sorted(attn_pos), np.int64))
+    kp = np.ascontiguousarray(np.asarray(kv_pos, np.int64))
+    L, H = shape.layers, shape.hidden
+    att = np.zeros((L, len(ap), H), np.float32) if len(ap) else None
+    kk = np.zeros((L, len(kp), H), np.float32) if len(kp) else None
+    vv = np.zeros((L, len(kp), H), np.float32) if len(kp) else None
+    lg = np.zeros(shape.vocab, np.float32)
+    tok = lib().llama_ref_prefill_probe(
+        C.byref(c), p.ctypes.data_as(C.POINTER(C.c_int32)), len(p), 1 if emulate_bf16 else 0,
+        len(ap), _i64(ap) if len(ap) else None, _f32(att), len(kp), _i64(kp) if len(kp) else None,
+        _f32(kk), _f32(vv), 1 if last_only else 0, _f32(lg), threads)
+    return int(tok), lg, att, kk, vv
+
+
+def decode_cached(shape, k_cache, v_cache, token, emulate_bf16=True, threads=0):
+    """One decode step over a GIVEN bf16 KV cache (uint16 [layers, n_ctx, hidden],
+    token order, after RoPE) at position n_ctx (llama_ref.c:llama_ref_decode_cached).
+    Returns (greedy token, logits[vocab], k_new[layers, hidden], v_new, attn[layers, hidden])."""
+    c = cfg_from(shape)
+    kc = np.ascontiguousarray(k_cache, np.uint16)
+    vc = np.ascontiguousarray(v_cache, np.uint16)
+    L, n_ctx, H = kc.shape
+    assert L == shape.layers and H == shape.hidden and vc.shape == kc.shape
+    lg = np.zeros(shape.vocab, np.float32)
+    kn = np.zeros((L, H), np.float32)
+    vn = np.zeros((L, H), np.float32)
+    att = np.zeros((L, H), np.float32)
+    u16 = C.POINTER(C.c_uint16)
+    tok = lib().llama_ref_decode_cached(C.byref(c), n_ctx, kc.ctypes.data_as(u16),
+                                        vc.ctypes.data_as(u16), int(token),
+                                        1 if emulate_bf16 else 0, _f32(lg), _f32(kn), _f32(vn),
+                                        _f32(att), threads)
+    return int(tok), lg, kn, vn, att

@@ -90,7 +90,8 @@ EXPORTED_SYMBOLS = [
     "esp_build_ring_schedule", "esp_proactive_scale_down", "esp_reactive_migrate",
     "esp_runtime_create", "esp_runtime_destroy", "esp_instance_info", "esp_prefill",
     "esp_decode_step", "esp_move_kv", "esp_free_request", "esp_query_placement",
-    "esp_check_conservation", "esp_request_tokens", "esp_dump_profiles",
+    "esp_check_conservation", "esp_request_tokens", "esp_read_kv", "esp_capture_attention",
+    "esp_captured_attention", "esp_slab_access", "esp_dump_profiles",
     "esp_decode_samples", "esp_fit_cost",
     "esp_launch_count", "esp_set_profiling", "esp_phase_times", "esp_k_gemm", "esp_k_ring_attention", "esp_k_decode_attention",
 ]
@@ -188,6 +189,12 @@ def lib() -> C.CDLL:
         h.esp_request_tokens.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
                                          C.c_int32, C.POINTER(C.c_int32)]
         h.esp_dump_profiles.argtypes = [C.c_void_p, C.c_char_p]
+        h.esp_read_kv.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.c_int64, C.POINTER(C.c_int64)]
+        h.esp_capture_attention.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64]
+        h.esp_captured_attention.argtypes = [C.c_void_p, C.c_void_p, C.c_int64,
+                                             C.POINTER(C.c_int64)]
+        h.esp_slab_access.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
         h.esp_decode_samples.argtypes = [C.c_void_p, C.POINTER(C.c_int32),
                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                          C.POINTER(C.c_int64), C.POINTER(C.c_double),
@@ -588,6 +595,36 @@ class Runtime:
                                        C.byref(n)))
         return [int(x) for x in out[:n.value]]
 
+    def read_kv(self, request, layer):
+        """(K, V) of one layer as uint16 (bf16 bits) [n_tokens, hidden], token order."""
+        n = C.c_int64()
+        check(lib().esp_read_kv(self._h, request, layer, None, None, 0, C.byref(n)))
+        k = np.zeros((n.value, self.shape.hidden), np.uint16)
+        v = np.zeros((n.value, self.shape.hidden), np.uint16)
+        check(lib().esp_read_kv(self._h, request, layer, k.ctypes.data, v.ctypes.data, n.value,
+                                C.byref(n)))
+        return k, v
+
+    def capture_attention(self, positions):
+        """Arms the next (single-request) prefill to capture the attention outputs
+        at these prompt positions in every layer; read them with captured_attention()."""
+        p = _arr(np.int64, positions)
+        self._cap_n = len(p)
+        check(lib().esp_capture_attention(self._h, _ptr(p, C.c_int64) if len(p) else None, len(p)))
+
+    def captured_attention(self) -> np.ndarray:
+        """uint16 (bf16 bits) [layers, n_positions, hidden] of the last armed prefill."""
+        n = C.c_int64()
+        check(lib().esp_captured_attention(self._h, None, 0, C.byref(n)))
+        out = np.zeros((n.value, self.shape.hidden), np.uint16)
+        check(lib().esp_captured_attention(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out.reshape(self.shape.layers, -1, self.shape.hidden)
+
+    def slab_access(self, instance, device) -> bool:
+        ok = C.c_int32()
+        check(lib().esp_slab_access(self._h, instance, device, C.byref(ok)))
+        return bool(ok.value)
+
     PHASES = ["embed", "rmsnorm", "qkv_gemm", "ring_attention", "o_gemm", "gate_up_gemm",
               "down_gemm", "lm_head", "argmax", "decode_attention", "lse_combine"]
 
@@ -666,3 +703,8 @@ def k_decode_attention(q_ptr, batch, k_slabs, v_slabs, slot_ptrs, n_slots, chunk
     cr = (C.c_int32 * n)(*chunk_req)
     check(lib().esp_k_decode_attention(q_ptr, batch, ks, vs, sp, ns, cr, n, out_ptr, heads,
                                        head_dim, stream))
+
+
+def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> float32."""
+    return (np.asarray(u16, np.uint16).astype(np.uint32) << 16).view(np.float32)

@@ -303,6 +303,36 @@ int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int
   return guarded([&] { rt->impl->request_tokens(request, out, cap, n); });
 }
 
+int esp_read_kv(esp_runtime* rt, int64_t request, int32_t layer, void* k_out, void* v_out,
+                int64_t cap, int64_t* n) {
+  return guarded([&] {
+    if (!rt || !n) throw esp::ConfigError("read_kv: null argument");
+    if (cap > 0 && (!k_out || !v_out)) throw esp::ConfigError("read_kv: null output");
+    rt->impl->read_kv(request, layer, k_out, v_out, cap, n);
+  });
+}
+
+int esp_capture_attention(esp_runtime* rt, const int64_t* pos, int64_t n) {
+  return guarded([&] {
+    if (!rt || (n > 0 && !pos) || n < 0) throw esp::ConfigError("capture_attention: bad argument");
+    rt->impl->capture_attention(pos, n);
+  });
+}
+
+int esp_captured_attention(esp_runtime* rt, void* out, int64_t cap, int64_t* n_rows) {
+  return guarded([&] {
+    if (!rt || !n_rows) throw esp::ConfigError("captured_attention: null argument");
+    rt->impl->captured_attention(out, cap, n_rows);
+  });
+}
+
+int esp_slab_access(const esp_runtime* rt, int32_t instance, int32_t device, int32_t* ok) {
+  return guarded([&] {
+    if (!rt || !ok) throw esp::ConfigError("slab_access: null argument");
+    *ok = rt->impl->slab_accessible(instance, device) ? 1 : 0;
+  });
+}
+
 int esp_dump_profiles(const esp_runtime* rt, const char* path) {
   return guarded([&] { rt->impl->dump_profiles(path); });
 }

@@ -366,7 +366,6 @@ void Runtime::prefill(const esp_prefill_args& a) {
       !a.retain_tokens) {
     throw ConfigError("prefill: null argument");
   }
-  if (d > k::kMaxRounds) throw ConfigError("prefill: dop exceeds 8");
   std::vector<InstanceId> ring(a.ring, a.ring + d);
   {
     std::set<InstanceId> seen;
@@ -402,6 +401,13 @@ void Runtime::prefill(const esp_prefill_args& a) {
     }
   }
   if (!devices_.empty() && !a.tokens) throw ConfigError("prefill: tokens required on a device runtime");
+  // The ring kernel keeps all d rounds of a segment in one work item; a
+  // placement-only runtime has no kernel and accepts any ring the reference
+  // plans (its ring tests go to d = 16).
+  if (!devices_.empty() && d > k::kMaxRounds) {
+    throw ConfigError("prefill: ESP degree " + std::to_string(d) + " exceeds the kernel's " +
+                      std::to_string(k::kMaxRounds) + " rounds");
+  }
   // One co-location domain: the batched single-domain pass. Several: ring
   // transport between domains (runtime_multi.cpp), where a token can only
   // be retained by a domain the ring passes through (proactive_scale_down's
@@ -448,6 +454,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
       PageList& pl = rr.pages[i];
       pl.slots.insert(pl.slots.end(), slots.begin(), slots.end());
       for (int32_t s : slots) {
+        pl.pos.push_back(static_cast<int32_t>(ts.size()));
         ts.push_back(i);  // resting instance id of the token
         tl.push_back(s);
       }
@@ -509,6 +516,14 @@ void Runtime::prefill(const esp_prefill_args& a) {
   }
   std::vector<int32_t> work_sorted;
   build_attention_work(segs, cfg_.heads, attn_pairs_, rows, cfg_.head_dim, work_sorted);
+  if (cap_armed_) {  // parity capture: stripe row of each captured position
+    if (n != 1) throw ConfigError("attention capture needs a single-request prefill");
+    for (size_t c = 0; c < cap_pos_.size(); ++c) {
+      const int64_t t = cap_pos_[c];
+      if (t < 0 || t >= a.input_lens[0]) throw ConfigError("capture position outside the prompt");
+      cap_add(dc.domain, row0[t % d][0] + static_cast<int32_t>(t / d), static_cast<int32_t>(c));
+    }
+  }
 
   // RoPE table covering every position of the batch.
   int64_t max_len = 0;
@@ -567,6 +582,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
             "d2h");
   }
   cuda_ok(cudaStreamSynchronize(s), "prefill");
+  if (cap_armed_) cap_finish();
   collect_phase_events();
   float ms = 0;
   cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
@@ -680,6 +696,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
                                 static_cast<int>(segs.size()),
                                 static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
     });
+    if (cap_armed_) cap_layer(dc, l, attn, s);
     NormFuse nf;
     if (fuse) {
       nf.ss_o = ss2;
@@ -769,6 +786,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
       const int32_t pos = static_cast<int32_t>(rr.kv_tokens());
       std::vector<int32_t> slot = take_slots(inst(m), 1);
       rr.pages[m].slots.push_back(slot[0]);
+      rr.pages[m].pos.push_back(pos);
       rows_v.push_back({r, m, in_tok[r], pos, slot[0]});
       for (const auto& kv : rr.pages) involved.push_back(kv.first);
     }
@@ -795,6 +813,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
       PageList& pl = rr.pages[i];
       pl.slots.insert(pl.slots.end(), sl.begin(), sl.end());
       for (int32_t x : sl) {
+        pl.pos.push_back(static_cast<int32_t>(p_prev + static_cast<int64_t>(ch_slot.size())));
         ch_slab.push_back(inst(i).slab);
         ch_slot.push_back(x);
         ch_inst.push_back(i);
@@ -1128,11 +1147,14 @@ void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t token
     check_cuda("move_kv");
     cuda_ok(cudaStreamSynchronize(dc.stream), "move_kv");
   }
+  const std::vector<int32_t> moving_pos(spl.pos.end() - tokens, spl.pos.end());
   spl.slots.resize(spl.slots.size() - static_cast<size_t>(tokens));
+  spl.pos.resize(spl.slots.size());
   if (spl.dev_n > static_cast<int64_t>(spl.slots.size())) spl.dev_n = static_cast<int64_t>(spl.slots.size());
   release_slots(src, moving);
   PageList& dpl = rr.pages[to];
   dpl.slots.insert(dpl.slots.end(), dslots.begin(), dslots.end());
+  dpl.pos.insert(dpl.pos.end(), moving_pos.begin(), moving_pos.end());
   if (spl.slots.empty()) {
     if (spl.dev) cudaFree(spl.dev);
     rr.pages.erase(from);
@@ -1245,6 +1267,113 @@ void Runtime::dump_profiles(const std::string& path) const {
     for (size_t i = 0; i < p.lengths.size(); ++i) out << (i ? ", " : "") << p.lengths[i];
     out << "], \"measured_ms\": " << std::setprecision(9) << p.ms << "}\n";
   }
+}
+
+// ---- parity readback -----------------------------------------------------------------
+void Runtime::read_kv(RequestId r, int layer, void* k_out, void* v_out, int64_t cap, int64_t* n) {
+  RequestRec& rr = req(r);
+  const int64_t total = rr.kv_tokens();
+  if (n) *n = total;
+  if (layer < 0 || layer >= cfg_.layers) throw ConfigError("read_kv: layer out of range");
+  if (devices_.empty()) throw NoDeviceError("read_kv needs a device runtime");
+  if (cap < total) return;  // size query
+  const size_t H = static_cast<size_t>(cfg_.hidden);
+  std::vector<uint16_t> kh, vh;
+  for (auto& [iid, pl] : rr.pages) {
+    const int64_t m = static_cast<int64_t>(pl.slots.size());
+    if (m == 0) continue;
+    InstanceRec& in = inst(iid);
+    DeviceCtx& dc = *devices_[static_cast<size_t>(in.domain)];
+    DeviceGuard g(dc.device);
+    cudaStream_t s = dc.stream;
+    sync_pages(pl, s);
+    std::vector<int32_t> zero(static_cast<size_t>(m), 0);
+    int32_t* d_slab = scratch<int32_t>(dc.ret_slab, static_cast<size_t>(m));
+    cuda_ok(cudaMemcpyAsync(d_slab, zero.data(), m * 4, cudaMemcpyHostToDevice, s), "h2d");
+    k::DecodeSlabs src{};
+    src.k[0] = in.layer_k(layer);
+    src.v[0] = in.layer_v(layer);
+    bf16* ko = scratch<bf16>(dc.kb, static_cast<size_t>(m) * H);
+    bf16* vo = scratch<bf16>(dc.vb, static_cast<size_t>(m) * H);
+    k::gather_rows(src, d_slab, pl.dev, static_cast<int>(m), ko, vo, static_cast<int>(H), s);
+    kh.resize(static_cast<size_t>(m) * H);
+    vh.resize(static_cast<size_t>(m) * H);
+    cuda_ok(cudaMemcpyAsync(kh.data(), ko, kh.size() * 2, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_ok(cudaMemcpyAsync(vh.data(), vo, vh.size() * 2, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_ok(cudaStreamSynchronize(s), "read_kv");
+    for (int64_t j = 0; j < m; ++j) {
+      const int64_t p = pl.pos[static_cast<size_t>(j)];
+      if (p < 0 || p >= total) throw InternalError("read_kv: token position out of range");
+      std::memcpy(static_cast<uint16_t*>(k_out) + p * H, kh.data() + j * H, H * 2);
+      std::memcpy(static_cast<uint16_t*>(v_out) + p * H, vh.data() + j * H, H * 2);
+    }
+  }
+}
+
+void Runtime::capture_attention(const int64_t* pos, int64_t n) {
+  if (devices_.empty()) throw NoDeviceError("capture_attention needs a device runtime");
+  cap_pos_.assign(pos, pos + n);
+  cap_armed_ = n > 0;
+  cap_host_.clear();
+  cap_rows_ = 0;
+}
+
+void Runtime::captured_attention(void* out, int64_t cap_rows, int64_t* n) {
+  if (n) *n = cap_rows_;
+  if (!out || cap_rows < cap_rows_) return;
+  std::memcpy(out, cap_host_.data(), cap_host_.size() * 2);
+}
+
+void Runtime::cap_add(int dom, int32_t row, int32_t idx) {
+  CapDomain& c = cap_dom_[dom];
+  c.rows.push_back(row);
+  c.idx.push_back(idx);
+}
+
+void Runtime::cap_layer(DeviceCtx& dc, int l, const bf16* attn, cudaStream_t s) {
+  auto it = cap_dom_.find(dc.domain);
+  if (it == cap_dom_.end() || it->second.rows.empty()) return;
+  CapDomain& c = it->second;
+  const int m = static_cast<int>(c.rows.size());
+  const size_t H = static_cast<size_t>(cfg_.hidden);
+  if (!c.d_rows) {
+    cuda_ok(cudaMalloc(&c.d_rows, static_cast<size_t>(m) * 4), "cudaMalloc(capture)");
+    cuda_ok(cudaMalloc(&c.d_buf, static_cast<size_t>(cfg_.layers) * m * H * 2), "cudaMalloc(capture)");
+    cuda_ok(cudaMemcpyAsync(c.d_rows, c.rows.data(), static_cast<size_t>(m) * 4,
+                            cudaMemcpyHostToDevice, s),
+            "h2d");
+  }
+  k::copy_rows(attn, c.d_rows, m, c.d_buf + static_cast<size_t>(l) * m * H, static_cast<int>(H), s);
+}
+
+void Runtime::cap_finish() {
+  const size_t H = static_cast<size_t>(cfg_.hidden), N = cap_pos_.size();
+  cap_host_.assign(static_cast<size_t>(cfg_.layers) * N * H, 0);
+  for (auto& [dom, c] : cap_dom_) {
+    const size_t m = c.rows.size();
+    if (m == 0 || !c.d_buf) continue;
+    DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+    DeviceGuard g(dc.device);
+    std::vector<uint16_t> h(static_cast<size_t>(cfg_.layers) * m * H);
+    cuda_ok(cudaMemcpy(h.data(), c.d_buf, h.size() * 2, cudaMemcpyDeviceToHost), "d2h");
+    for (int l = 0; l < cfg_.layers; ++l) {
+      for (size_t j = 0; j < m; ++j) {
+        std::memcpy(cap_host_.data() + (static_cast<size_t>(l) * N + c.idx[j]) * H,
+                    h.data() + (static_cast<size_t>(l) * m + j) * H, H * 2);
+      }
+    }
+    cudaFree(c.d_rows);
+    cudaFree(c.d_buf);
+  }
+  cap_dom_.clear();
+  cap_rows_ = static_cast<int64_t>(N) * cfg_.layers;
+  cap_armed_ = false;
+}
+
+bool Runtime::slab_accessible(InstanceId i, int device) const {
+  const InstanceRec& in = inst(i);
+  if (!in.k_slab) return false;
+  return in.k_slab->readable_writable_by(device) && in.v_slab->readable_writable_by(device);
 }
 
 }  // namespace esp

@@ -31,6 +31,7 @@ struct RingSegment;
 // synchronized device mirror the kernels read.
 struct PageList {
   std::vector<int32_t> slots;
+  std::vector<int32_t> pos;  // token position of each slot (parity readback only)
   int32_t* dev = nullptr;
   int64_t dev_cap = 0;
   int64_t dev_n = 0;  // prefix of `slots` already on the device
@@ -103,6 +104,17 @@ class Runtime {
   void instance_info(InstanceId i, int64_t* cap, int64_t* used) const;
   void check_conservation();
   void request_tokens(RequestId r, int32_t* out, int32_t cap, int32_t* n) const;
+  // Parity readback: the request's K/V rows of one layer in token order
+  // (host bf16 [n x hidden]); *n = the request's KV token count.
+  void read_kv(RequestId r, int layer, void* k_out, void* v_out, int64_t cap, int64_t* n);
+  // Arms the next prefill (single-request plan) to capture its attention
+  // outputs at token positions `pos` in every layer; captured() copies them
+  // out as host bf16 [layers x n x hidden].
+  void capture_attention(const int64_t* pos, int64_t n);
+  void captured_attention(void* out, int64_t cap_rows, int64_t* n);
+  // Devices whose access to every mapped chunk of the instance's K and V
+  // slabs is read/write (cuMemGetAccess).
+  bool slab_accessible(InstanceId i, int device) const;
   void dump_profiles(const std::string& path) const;
   const std::vector<DecodeProfileRec>& decode_profiles() const { return decode_profiles_; }
   bool placement_only() const { return devices_.empty(); }
@@ -184,6 +196,26 @@ class Runtime {
   void record_decode_profile(const std::vector<InstanceId>& members,
                              const std::vector<RequestId>& batch, int n_masters, double ms);
   bool profiling_ = false;
+  // Attention capture of the next prefill (parity tests): positions, and per
+  // co-location domain the local stripe rows holding them, the capture
+  // index of each, and a device buffer [layers x rows x hidden] bf16.
+  std::vector<int64_t> cap_pos_;
+  bool cap_armed_ = false;
+  std::vector<uint16_t> cap_host_;  // [layers x cap_pos_ x hidden]
+  int64_t cap_rows_ = 0;
+  struct CapDomain {
+    std::vector<int32_t> rows, idx;
+    int32_t* d_rows = nullptr;
+    k_bf16* d_buf = nullptr;
+  };
+  std::map<int, CapDomain> cap_dom_;
+  // During an armed prefill: local stripe row `row` of domain `dom` holds
+  // captured position number `idx`.
+  void cap_add(int dom, int32_t row, int32_t idx);
+  // After layer l's attention of domain dc: copy its captured rows.
+  void cap_layer(DeviceCtx& dc, int l, const k_bf16* attn, cudaStream_t s);
+  // After the prefill synchronized: gather the rows to the host and disarm.
+  void cap_finish();
   // K1 variant: v2 (two query tiles per CTA, P in TMEM) unless ESP_ATTN_V1=1.
   int attn_variant_ = 2;     // K1 variant (ESP_ATTN), set in the constructor
   bool attn_pairs_ = true;   // its work items are query-tile pairs

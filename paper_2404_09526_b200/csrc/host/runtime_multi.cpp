@@ -266,6 +266,17 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     }
     build_attention_work(p.segs, cfg_.heads, attn_pairs_, rows, cfg_.head_dim, p.work);
   }
+  if (cap_armed_) {  // parity capture: (domain, local stripe row) of each position
+    if (n != 1) throw ConfigError("attention capture needs a single-request prefill");
+    for (size_t c = 0; c < cap_pos_.size(); ++c) {
+      const int64_t t = cap_pos_[c];
+      if (t < 0 || t >= a.input_lens[0]) throw ConfigError("capture position outside the prompt");
+      const int i = static_cast<int>(t % d);
+      Part& p = parts[dom_of[i]];
+      cap_add(dom_of[i], p.local_row0[i] + (row0[i][0] - blk0[i]) + static_cast<int32_t>(t / d),
+              static_cast<int32_t>(c));
+    }
+  }
 
   int64_t max_len = 0;
   for (int r = 0; r < n; ++r) max_len = std::max(max_len, a.input_lens[r]);
@@ -427,6 +438,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
                                   static_cast<int>(p.segs.size()),
                                   static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
       });
+      if (cap_armed_) cap_layer(dc, l, attn, s);
       if (push) {  // peers may overwrite this gather buffer with the next layer
         cudaEvent_t e = sync_event(dc);
         cuda_ok(cudaEventRecord(e, s), "event");
@@ -486,6 +498,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
     ms_max = std::max<double>(ms_max, ms);
   }
+  if (cap_armed_) cap_finish();
   collect_phase_events();
   for (auto& [dom, p] : parts) {
     for (size_t j = 0; j < p.last.size(); ++j) {
@@ -1046,6 +1059,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
     cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
     ms_max = std::max<double>(ms_max, ms);
   }
+  if (cap_armed_) cap_finish();
   collect_phase_events();
   if (a.device_ms_out) *a.device_ms_out = ms_max;
   std::map<RequestId, std::pair<int, int>> where;  // request -> (domain, local row)

@@ -23,6 +23,7 @@ struct Vmm {
                   unsigned long long);
   CUresult (*unmap)(CUdeviceptr, size_t);
   CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*get_access)(unsigned long long*, const CUmemLocation*, CUdeviceptr);
   CUresult (*granularity)(size_t*, const CUmemAllocationProp*,
                           CUmemAllocationGranularity_flags);
 };
@@ -47,6 +48,7 @@ const Vmm& vmm() {
     entry("cuMemMap", x.map);
     entry("cuMemUnmap", x.unmap);
     entry("cuMemSetAccess", x.set_access);
+    entry("cuMemGetAccess", x.get_access);
     entry("cuMemGetAllocationGranularity", x.granularity);
     return x;
   }();
@@ -69,8 +71,13 @@ size_t round_up(size_t x, size_t g) { return (x + g - 1) / g * g; }
 
 }  // namespace
 
-void LazySlab::reserve(int device, int layers, int64_t capacity, size_t row_bytes) {
+void LazySlab::reserve(int device, int layers, int64_t capacity, size_t row_bytes,
+                       const std::vector<int>& peers) {
   device_ = device;
+  access_.assign(1, device);
+  for (int d : peers) {
+    if (std::find(access_.begin(), access_.end(), d) == access_.end()) access_.push_back(d);
+  }
   layers_ = layers;
   capacity_ = capacity;
   row_bytes_ = row_bytes;
@@ -87,9 +94,13 @@ void LazySlab::ensure(int64_t rows) {
   const size_t target = std::min(layer_stride_, std::max(need, round_up(mapped_ * 2, gran_)));
   const size_t grow = target - mapped_;
   const CUmemAllocationProp p = prop_for(device_);
-  CUmemAccessDesc acc{};
-  acc.location = p.location;
-  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  std::vector<CUmemAccessDesc> acc(access_.size());
+  for (size_t i = 0; i < access_.size(); ++i) {
+    acc[i] = CUmemAccessDesc{};
+    acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc[i].location.id = access_[i];
+    acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  }
   for (int l = 0; l < layers_; ++l) {
     const CUdeviceptr at = base_ + static_cast<CUdeviceptr>(l) * layer_stride_ + mapped_;
     CUmemGenericAllocationHandle h;
@@ -99,9 +110,24 @@ void LazySlab::ensure(int64_t rows) {
       throw CudaError("cuMemMap (KV slab) failed");
     }
     chunks_.push_back({h, at, grow});
-    ok(vmm().set_access(at, grow, &acc, 1), "cuMemSetAccess (KV slab)");
+    ok(vmm().set_access(at, grow, acc.data(), acc.size()), "cuMemSetAccess (KV slab)");
   }
   mapped_ = target;
+}
+
+bool LazySlab::readable_writable_by(int device) const {
+  if (chunks_.empty()) return false;
+  CUmemLocation loc{};
+  loc.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  loc.id = device;
+  for (const Chunk& c : chunks_) {
+    unsigned long long flags = 0;
+    if (vmm().get_access(&flags, &loc, c.at) != CUDA_SUCCESS ||
+        flags != CU_MEM_ACCESS_FLAGS_PROT_READWRITE) {
+      return false;
+    }
+  }
+  return true;
 }
 
 LazySlab::~LazySlab() {

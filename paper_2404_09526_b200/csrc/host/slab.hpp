@@ -8,6 +8,12 @@
 // A cluster whose instances are mostly empty (e.g. config 3: 8 instances x
 // 65,600 slots, KV resting on 2 survivors) then costs HBM only for resident
 // tokens.
+//
+// Peer access: cudaDeviceEnablePeerAccess does not cover cuMemCreate/cuMemMap
+// memory, so every chunk is mapped with one CUmemAccessDesc per device of the
+// runtime that can reach the owner (the owner first). The cross-domain paths
+// (push prefill into a survivor's slab on another GPU, chunk gathers, KV
+// moves) dereference slabs from those devices.
 #pragma once
 
 #include <cuda.h>
@@ -25,8 +31,11 @@ class LazySlab {
   LazySlab& operator=(const LazySlab&) = delete;
   ~LazySlab();
 
-  // Reserves layers x capacity rows of row_bytes on `device`.
-  void reserve(int device, int layers, int64_t capacity, size_t row_bytes);
+  // Reserves layers x capacity rows of row_bytes on `device`; every mapped
+  // chunk is read/write for `device` and each of `peers` (devices that
+  // access it over NVLink; duplicates and `device` itself are ignored).
+  void reserve(int device, int layers, int64_t capacity, size_t row_bytes,
+               const std::vector<int>& peers = {});
   // Maps physical memory so rows [0, rows) of every layer are backed.
   void ensure(int64_t rows);
 
@@ -34,9 +43,15 @@ class LazySlab {
   // Element (bf16) distance between consecutive layer regions.
   int64_t layer_stride_elems() const { return static_cast<int64_t>(layer_stride_ / 2); }
   size_t mapped_bytes() const { return mapped_ * static_cast<size_t>(layers_); }
+  // Devices granted access (owner first).
+  const std::vector<int>& access_devices() const { return access_; }
+  // cuMemGetAccess of `device` on every mapped chunk: true iff all of them
+  // are read/write for it (false when nothing is mapped yet).
+  bool readable_writable_by(int device) const;
 
  private:
   int device_ = -1;
+  std::vector<int> access_;
   int layers_ = 0;
   int64_t capacity_ = 0;
   size_t row_bytes_ = 0;

@@ -508,7 +508,22 @@ __global__ void gather_rows_kernel(const DecodeSlabs src, const int32_t* __restr
   }
 }
 
+__global__ void copy_rows_kernel(const bf16* __restrict__ src, const int32_t* __restrict__ rows,
+                                 bf16* __restrict__ dst, int hidden) {
+  const int64_t so = static_cast<int64_t>(rows[blockIdx.x]) * hidden;
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * hidden;
+  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
+    *reinterpret_cast<uint4*>(dst + d + c) = *reinterpret_cast<const uint4*>(src + so + c);
+  }
+}
+
 }  // namespace
+
+void copy_rows(const bf16* src, const int32_t* rows, int n, bf16* dst, int hidden, cudaStream_t s) {
+  if (n <= 0) return;
+  copy_rows_kernel<<<n, 128, 0, s>>>(src, rows, dst, hidden);
+  count_launch();
+}
 
 void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slot, int n,
                  bf16* out_k, bf16* out_v, int hidden, cudaStream_t s) {

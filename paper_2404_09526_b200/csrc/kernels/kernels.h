@@ -186,6 +186,9 @@ void retain_rows(const bf16* k, const bf16* v, const int32_t* rows, const int32_
 void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slot, int n,
                  bf16* out_k, bf16* out_v, int hidden, cudaStream_t s);
 
+// dst[i] = src[rows[i]] (bf16 rows of `hidden`; parity captures).
+void copy_rows(const bf16* src, const int32_t* rows, int n, bf16* dst, int hidden, cudaStream_t s);
+
 // ---- small fused ops --------------------------------------------------------
 // ss != null: also stores each row's sum of squares (fused-RMSNorm input).
 void embed(const int32_t* tokens, const bf16* table, bf16* x, int rows, int hidden,

@@ -99,29 +99,44 @@ class EspTapPolicy final : public espsim::Policy {
   void set_verify_every(int64_t n) { verify_every_ = n; }
   int64_t decisions() const { return decisions_; }
   int64_t verified_requests() const { return verified_; }
+  // Prefill plans passed in the restated fill order (vs map order).
+  int64_t fill_ordered_prefills() const { return fill_ordered_; }
 
  private:
   std::map<int32_t, int64_t> device_placement(espsim::RequestId r) const {
-    int32_t inst[64];
-    int64_t tok[64];
+    // esp_query_placement reports the full count; grow the buffer and ask
+    // again when a request spans more instances than it holds.
     int32_t n = 0;
-    check(esp_query_placement(rt_, r, inst, tok, 64, &n));
+    check(esp_query_placement(rt_, r, pl_inst_.data(), pl_tok_.data(),
+                              static_cast<int32_t>(pl_inst_.size()), &n));
+    if (n > static_cast<int32_t>(pl_inst_.size())) {
+      pl_inst_.resize(static_cast<size_t>(n));
+      pl_tok_.resize(static_cast<size_t>(n));
+      check(esp_query_placement(rt_, r, pl_inst_.data(), pl_tok_.data(), n, &n));
+    }
     std::map<int32_t, int64_t> m;
-    for (int32_t i = 0; i < std::min(n, 64); ++i) m[inst[i]] = tok[i];
+    for (int32_t i = 0; i < n; ++i) m[pl_inst_[static_cast<size_t>(i)]] = pl_tok_[static_cast<size_t>(i)];
     return m;
   }
 
   void reconcile(const espsim::SimState& s) {
+    // Pass 1: release every finished / rejected / evicted request first, so
+    // the displaced-KV moves of pass 2 can land in the slots they freed (the
+    // engine frees before it displaces, engine.cpp:119-166 / :587-648).
     for (auto it = live_.begin(); it != live_.end();) {
       const espsim::Request& q = s.requests[static_cast<size_t>(*it)];
       if (q.phase == espsim::Phase::kFinished || q.phase == espsim::Phase::kRejected ||
           q.placement.empty()) {
         check(esp_free_request(rt_, *it));  // finish / evict-and-recompute
         it = live_.erase(it);
-        continue;
+      } else {
+        ++it;
       }
-      // Engine-internal KV moves (displaced KV): surplus -> deficit.
-      auto have = device_placement(*it);
+    }
+    // Pass 2: engine-internal KV moves (displaced KV): surplus -> deficit.
+    for (espsim::RequestId r : live_) {
+      const espsim::Request& q = s.requests[static_cast<size_t>(r)];
+      auto have = device_placement(r);
       std::vector<std::pair<int32_t, int64_t>> surplus, deficit;
       std::set<int32_t> ids;
       for (auto& kv : have) ids.insert(kv.first);
@@ -135,12 +150,61 @@ class EspTapPolicy final : public espsim::Policy {
       size_t a = 0, b = 0;
       while (a < surplus.size() && b < deficit.size()) {
         const int64_t mv = std::min(surplus[a].second, deficit[b].second);
-        check(esp_move_kv(rt_, *it, surplus[a].first, deficit[b].first, mv));
+        check(esp_move_kv(rt_, r, surplus[a].first, deficit[b].first, mv));
         if ((surplus[a].second -= mv) == 0) ++a;
         if ((deficit[b].second -= mv) == 0) ++b;
       }
-      ++it;
     }
+  }
+
+  // The plan's placement pairs in TOKEN (fill) order: plan_prefill_scale_down
+  // (scheduler.cpp:663-713) lays each request's tokens contiguously over the
+  // survivors ordered by (free desc, id asc), one cursor across the batch.
+  // The PrefillPlan only keeps per-instance counts (a KvPlacement map), so
+  // the order is recomputed with the planner's restatement over the
+  // runtime's free slots (the scheduler's free_after view: migrations are
+  // already applied and DP batches own disjoint instances). Plans that
+  // another policy laid out differently keep their map order.
+  std::vector<std::vector<std::pair<int32_t, int64_t>>> fill_order(const espsim::SimState& s,
+                                                                   const espsim::PrefillPlan& p) {
+    const size_t n = p.requests.size(), d = p.instances.size();
+    std::vector<std::vector<std::pair<int32_t, int64_t>>> out(n);
+    for (size_t r = 0; r < n; ++r) {
+      for (const auto& kv : p.placement.at(p.requests[r])) out[r].push_back(kv);
+    }
+    std::vector<int32_t> inst(p.instances.begin(), p.instances.end());
+    std::vector<int64_t> free(d), lens(n);
+    for (size_t i = 0; i < d; ++i) {
+      int64_t cap = 0, used = 0;
+      check(esp_instance_info(rt_, inst[i], &cap, &used));
+      free[i] = cap - used;
+    }
+    for (size_t r = 0; r < n; ++r) lens[r] = s.requests[static_cast<size_t>(p.requests[r])].input_len;
+    std::vector<int32_t> dec(d), pi(n * d), pn(n);
+    std::vector<int64_t> pt(n * d);
+    int32_t nd = 0;
+    int64_t vol = 0;
+    if (esp_plan_prefill_scale_down(inst.data(), free.data(), static_cast<int32_t>(d), lens.data(),
+                                    static_cast<int32_t>(n), dec.data(), &nd, pi.data(), pt.data(),
+                                    pn.data(), &vol) != ESP_OK) {
+      return out;
+    }
+    std::vector<std::vector<std::pair<int32_t, int64_t>>> fill(n);
+    for (size_t r = 0; r < n; ++r) {
+      std::map<int32_t, int64_t> counts;
+      for (int32_t j = 0; j < pn[r]; ++j) {
+        fill[r].emplace_back(pi[r * d + j], pt[r * d + j]);
+        counts[pi[r * d + j]] += pt[r * d + j];
+      }
+      const auto& want = p.placement.at(p.requests[r]);
+      if (!std::equal(counts.begin(), counts.end(), want.begin(), want.end(),
+                      [](const auto& x, const auto& y) { return x.first == y.first && x.second == y.second; }) ||
+          counts.size() != want.size()) {
+        return out;
+      }
+    }
+    ++fill_ordered_;
+    return fill;
   }
 
   void verify(const espsim::SimState& s) {
@@ -173,12 +237,13 @@ class EspTapPolicy final : public espsim::Policy {
       std::vector<int64_t> ids(p.requests.begin(), p.requests.end()), lens;
       std::vector<int32_t> ring(p.instances.begin(), p.instances.end()), rn, ri, toks;
       std::vector<int64_t> rt;
-      for (espsim::RequestId r : p.requests) {
+      const auto order = fill_order(s, p);
+      for (size_t k = 0; k < p.requests.size(); ++k) {
+        const espsim::RequestId r = p.requests[k];
         const espsim::TokenCount n = s.requests[static_cast<size_t>(r)].input_len;
         lens.push_back(n);
-        const espsim::KvPlacement& pl = p.placement.at(r);
-        rn.push_back(static_cast<int32_t>(pl.size()));
-        for (const auto& [inst, tok] : pl) {
+        rn.push_back(static_cast<int32_t>(order[k].size()));
+        for (const auto& [inst, tok] : order[k]) {
           ri.push_back(inst);
           rt.push_back(tok);
         }
@@ -249,6 +314,9 @@ class EspTapPolicy final : public espsim::Policy {
   std::set<espsim::RequestId> live_;
   int64_t decisions_ = 0;
   int64_t verified_ = 0;
+  int64_t fill_ordered_ = 0;
+  mutable std::vector<int32_t> pl_inst_ = std::vector<int32_t>(16);
+  mutable std::vector<int64_t> pl_tok_ = std::vector<int64_t>(16);
   int64_t verify_every_ = 1;
   int64_t calls_ = 0;
 };

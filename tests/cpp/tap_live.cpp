@@ -61,9 +61,11 @@ int run(const char* policy, int instances, TokenCount cap, std::vector<TraceReco
       return 1;
     }
   }
-  std::printf("%s: %zu events identical, %lld decisions, %lld page-table checks\n", policy,
+  std::printf("%s: %zu events identical, %lld decisions, %lld page-table checks, "
+              "%lld prefills in fill order\n", policy,
               a.size(), static_cast<long long>(tp->decisions()),
-              static_cast<long long>(tp->verified_requests()));
+              static_cast<long long>(tp->verified_requests()),
+              static_cast<long long>(tp->fill_ordered_prefills()));
   esp_runtime_destroy(rt);
   return 0;
 }
@@ -84,6 +86,12 @@ int main(int argc, char** argv) {
   spec.seed = 7;
   rc |= run("esp", 8, 317000, gen_trace(spec), sib);
   rc |= run("static-hybrid:2", 8, 300000, {{0, 32768, 4}, {5, 1000, 3}}, sib);
+  // Tight pools: finishes, evictions and displaced-KV moves between two
+  // schedule() calls (the tap frees before it moves).
+  spec.requests_per_s = 4.0;
+  spec.count = 120;
+  spec.seed = 3;
+  rc |= run("esp", 4, 60000, gen_trace(spec), sib);
   // SURVEY §8 f3 baselines on the same data path: chunked prefill (chunks
   // ride on decode steps) and disaggregation (engine-internal handoff moves).
   spec.requests_per_s = 2.0;

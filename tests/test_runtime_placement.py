@@ -1,0 +1,24 @@
+"""Placement-only runtime (no GPU): page tables and slot counters for plans
+the reference accepts but the ring kernel could not run."""
+from paper_2404_09526_b200 import abi
+
+
+def test_placement_only_accepts_rings_wider_than_the_kernel():
+    """The reference's ring tests go to d = 16 (test_esp_mechanics.cpp:26-49);
+    kMaxRounds (8) only limits the device kernel, not the page tables."""
+    rt = abi.Runtime(abi.LWM_7B, 16, devices=None, kv_capacity=1000)
+    ring = list(range(16))
+    rt.prefill([4], [12000], ring, [[(15, 1000), (14, 1000)] + [(i, 1000) for i in range(10)]])
+    pl = rt.placement(4)
+    assert sum(pl.values()) == 12000 and len(pl) == 12
+    rt.check_conservation()
+    rt.free_request(4)
+    assert rt.kv_used() == [0] * 16
+
+
+def test_placement_query_beyond_64_instances():
+    """A request spread over more than 64 instances reads back completely."""
+    n = 80
+    rt = abi.Runtime(abi.TINY, n, devices=None, kv_capacity=10)
+    rt.prefill([1], [10 * n], [0], [[(i, 10) for i in range(n)]])
+    assert rt.placement(1) == {i: 10 for i in range(n)}

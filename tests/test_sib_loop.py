@@ -86,6 +86,37 @@ def test_fit_cost_matches_reference_fit(tmp_path):
             assert c_ours == pytest.approx(c_ref, rel=1e-7, abs=1e-15), (d, ours, ref[d])
     # dop 3 / 4 exercised the drop rule: some coefficient pinned at 0
     assert min(ref[3]) == 0.0 and min(ref[4]) == 0.0
+    # Independent of both QR implementations (ours and the Eigen shim the
+    # reference is built against): numpy's SVD least squares with the same
+    # active-set rule (cost_model.cpp:104-134) gives the same coefficients.
+    for d in truth:
+        sel = [(l, m) for dd, l, m in samples if dd == d]
+        x1 = np.array([sum(l) for l, _ in sel], np.float64)
+        x2 = np.array([sum(v * v for v in l) for l, _ in sel], np.float64)
+        y = np.array([m for _, m in sel], np.float64)
+        for c_np, c_ref in zip(_numpy_fit(x1, x2, y), ref[d]):
+            assert c_np == pytest.approx(c_ref, rel=1e-6, abs=1e-13), (d, c_np, ref[d])
+
+
+def _numpy_fit(x1, x2, y):
+    import numpy as np
+
+    A = np.stack([np.ones_like(x1), x1, x2], axis=1)
+    scale = np.linalg.norm(A, axis=0)
+    scale[scale == 0] = 1.0
+    A = A / scale
+    active = [0, 1, 2]
+    coef = np.zeros(3)
+    while active:
+        coef = np.zeros(3)
+        coef[active] = np.linalg.lstsq(A[:, active], y, rcond=None)[0]
+        worst = min(active, key=lambda c: coef[c])
+        if coef[worst] >= -1e-12:
+            break
+        active.remove(worst)
+    else:
+        coef = np.zeros(3)
+    return np.maximum(coef, 0.0) / scale
 
 
 def test_fit_cost_underdetermined():

@@ -34,7 +34,11 @@ def test_tap_policy_live(tmp_path):
     exe = _build(tmp_path)
     out = subprocess.run([str(exe), REF], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr + out.stdout
-    assert out.stdout.count("events identical") == 5, out.stdout
+    assert out.stdout.count("events identical") == 6, out.stdout
+    # ESP prefills are passed in the restated fill order (scheduler.cpp:694-709)
+    for line in out.stdout.splitlines():
+        if line.startswith("esp:"):
+            assert " 0 prefills in fill order" not in line, line
 
 
 @pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "proj", "src")), reason="reference absent")
@@ -47,6 +51,6 @@ def test_tap_policy_live_b200_sib(tmp_path):
     sib = os.path.join(ROOT, "profiles", "r01s2_sib_b200_7b.jsonl")
     out = subprocess.run([str(exe), REF, sib], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr + out.stdout
-    assert out.stdout.count("events identical") == 5, out.stdout
+    assert out.stdout.count("events identical") == 6, out.stdout
     base = subprocess.run([str(exe), REF], capture_output=True, text=True, timeout=600)
     assert base.stdout != out.stdout  # the measured SIB changes the plans
