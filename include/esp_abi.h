@@ -326,7 +326,12 @@ int64_t esp_launch_count(const esp_runtime* rt);
 /* ---- kernel-level hooks (device pointers; for parity/roofline tests) ------- */
 
 /* D[M,N] (bf16, row-major) = A[M,K] (bf16, row-major) x B[N,K]^T (bf16,
- * row-major = K-major). epilogue: 0 store, 1 D += (residual add, D is read). */
+ * row-major = K-major). epilogue (low byte): 0 store, 1 D += (residual add,
+ * D is read), 2 store fp32 (D is float; the fp32 check mode: bf16 inputs,
+ * fp32 accumulation and output), 3 SiLU(gate)*up over 64-row gate/up blocks
+ * (D has N/2 columns). Bits 8-15 select the schedule: 0 the production
+ * dispatch, 1 the 1-CTA prefill kernel instead of the CTA pair, 2 whole
+ * skinny tiles only, 3 skinny stream-K for every shape. */
 int esp_k_gemm(const void* A, const void* B, void* D, int32_t M, int32_t N, int32_t K,
                int32_t epilogue, void* stream);
 

@@ -678,8 +678,12 @@ def launch_count() -> int:
 
 # ---- kernel-level hooks (device pointers, e.g. torch tensors' data_ptr()) -----------
 
-def k_gemm(a_ptr, b_ptr, d_ptr, M, N, K, epilogue=0, stream=0):
-    check(lib().esp_k_gemm(a_ptr, b_ptr, d_ptr, M, N, K, epilogue, stream))
+GEMM_PATHS = {"auto": 0, "no_pair": 1, "tiles": 2, "streamk": 3}
+
+
+def k_gemm(a_ptr, b_ptr, d_ptr, M, N, K, epilogue=0, stream=0, path="auto"):
+    check(lib().esp_k_gemm(a_ptr, b_ptr, d_ptr, M, N, K, epilogue | (GEMM_PATHS[path] << 8),
+                           stream))
 
 
 def k_ring_attention(q_ptr, q_len, pos_i, kv_k, kv_v, kv_len, origin, out_ptr, heads,

@@ -27,6 +27,18 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// Device scratch of the kernel hooks: checked allocation, freed on scope
+// exit (errors included).
+struct DevMem {
+  void* p = nullptr;
+  explicit DevMem(size_t bytes) { esp::cuda_ok(cudaMalloc(&p, bytes), "cudaMalloc(hook)"); }
+  ~DevMem() {
+    if (p) cudaFree(p);
+  }
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+};
+
 template <typename F>
 int guarded(F&& f) {
   try {
@@ -385,15 +397,18 @@ int esp_k_gemm(const void* A, const void* B, void* D, int32_t M, int32_t N, int3
                int32_t epilogue, void* stream) {
   return guarded([&] {
     esp::k::GemmEpilogue ep;
-    if (epilogue == 0) ep.kind = esp::k::kEpiStore;
-    else if (epilogue == 1) ep.kind = esp::k::kEpiResidual;
-    else if (epilogue == 2) ep.kind = esp::k::kEpiStoreF32;
-    else if (epilogue == 3) ep.kind = esp::k::kEpiSiluMul;
+    const int kind = epilogue & 0xFF, path = (epilogue >> 8) & 0xFF;
+    if (kind == 0) ep.kind = esp::k::kEpiStore;
+    else if (kind == 1) ep.kind = esp::k::kEpiResidual;
+    else if (kind == 2) ep.kind = esp::k::kEpiStoreF32;
+    else if (kind == 3) ep.kind = esp::k::kEpiSiluMul;
     else throw esp::ConfigError("unknown epilogue");
+    if (path > esp::k::kGemmStreamKAll) throw esp::ConfigError("unknown GEMM path");
+    if (!A || !B || !D) throw esp::ConfigError("gemm hook: null argument");
     ep.out = D;
-    ep.ldo = epilogue == 3 ? N / 2 : N;
+    ep.ldo = kind == 3 ? N / 2 : N;
     esp::k::gemm(static_cast<const esp::k::bf16*>(A), K, static_cast<const esp::k::bf16*>(B), K,
-                 M, N, K, ep, static_cast<cudaStream_t>(stream));
+                 M, N, K, ep, static_cast<cudaStream_t>(stream), path);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw esp::CudaError(cudaGetErrorString(e));
   });
@@ -407,6 +422,9 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
   // block 0..d-1) so the production kernel runs on exactly its layout.
   return guarded([&] {
     if (d < 1 || d > esp::k::kMaxRounds) throw esp::ConfigError("d out of range");
+    if (!q || !kv_k || !kv_v || !kv_len || !origin || !out) {
+      throw esp::ConfigError("ring_attention hook: null argument");
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t hidden = static_cast<int64_t>(heads) * head_dim;
     int64_t rows = q_len;
@@ -415,19 +433,19 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
       row0[r] = static_cast<int32_t>(rows);
       rows += kv_len[r];
     }
+    if (rows > INT32_MAX) throw esp::ConfigError("ring_attention hook: too many rows");
     using esp::k::bf16;
-    bf16 *Q = nullptr, *K = nullptr, *V = nullptr, *O = nullptr;
     const size_t bytes = static_cast<size_t>(rows) * hidden * 2;
-    cudaMalloc(&Q, bytes);
-    cudaMalloc(&K, bytes);
-    cudaMalloc(&V, bytes);
-    cudaMalloc(&O, bytes);
-    cudaMemcpyAsync(Q, q, static_cast<size_t>(q_len) * hidden * 2, cudaMemcpyDeviceToDevice, s);
+    DevMem Q(bytes), K(bytes), V(bytes), O(bytes);
+    esp::cuda_ok(cudaMemcpyAsync(Q.p, q, static_cast<size_t>(q_len) * hidden * 2,
+                                 cudaMemcpyDeviceToDevice, s), "stage q");
     for (int r = 0; r < d; ++r) {
-      cudaMemcpyAsync(K + row0[r] * hidden, kv_k[r], static_cast<size_t>(kv_len[r]) * hidden * 2,
-                      cudaMemcpyDeviceToDevice, s);
-      cudaMemcpyAsync(V + row0[r] * hidden, kv_v[r], static_cast<size_t>(kv_len[r]) * hidden * 2,
-                      cudaMemcpyDeviceToDevice, s);
+      const size_t off = static_cast<size_t>(row0[r]) * hidden * 2;
+      const size_t n = static_cast<size_t>(kv_len[r]) * hidden * 2;
+      esp::cuda_ok(cudaMemcpyAsync(static_cast<char*>(K.p) + off, kv_k[r], n,
+                                   cudaMemcpyDeviceToDevice, s), "stage k");
+      esp::cuda_ok(cudaMemcpyAsync(static_cast<char*>(V.p) + off, kv_v[r], n,
+                                   cudaMemcpyDeviceToDevice, s), "stage v");
     }
     esp::k::RingSegment sg{};
     sg.q_row0 = 0;
@@ -438,81 +456,49 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
       sg.kv_len[r] = kv_len[r];
       sg.shift[r] = origin[r] > pos_i ? 1 : 0;
     }
-    // Same variant selection as the runtime (ESP_ATTN / ESP_ATTN_V1).
-    const int variant = esp::k::attention_variant();
-    const bool pairs = esp::k::attention_pairs(variant);
     std::vector<int32_t> work;  // the runtime's work order (LPT, head groups)
-    esp::build_attention_work({sg}, heads, pairs, rows, head_dim, work);
-    esp::k::RingSegment* dseg = nullptr;
-    int32_t* dwork = nullptr;
-    cudaMalloc(&dseg, sizeof(sg));
-    cudaMalloc(&dwork, work.size() * 4);
-    cudaMemcpyAsync(dseg, &sg, sizeof(sg), cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(dwork, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s);
+    esp::build_attention_work({sg}, heads, work);
+    DevMem dseg(sizeof(sg)), dwork(work.size() * 4);
+    esp::cuda_ok(cudaMemcpyAsync(dseg.p, &sg, sizeof(sg), cudaMemcpyHostToDevice, s), "h2d");
+    esp::cuda_ok(cudaMemcpyAsync(dwork.p, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s),
+                 "h2d");
     const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
     const int nr = static_cast<int>(rows);
     const int n_work = esp::attention_n_work(work);
-    if (pairs && std::getenv("ESP_ATTN_PROF") != nullptr) {
-      // Cycle accounting of the v2 pipeline roles, printed to stderr.
+    const auto* segs = static_cast<const esp::k::RingSegment*>(dseg.p);
+    const auto* wk = static_cast<const int32_t*>(dwork.p);
+#ifdef ESP_STUDY
+    if (std::getenv("ESP_ATTN_PROF") != nullptr) {
+      // Kernel study build: cycle accounting of the pipeline roles (stderr).
       const int grid = std::min(n_work, 148);
-      uint64_t* dprof = nullptr;
-      cudaMalloc(&dprof, static_cast<size_t>(grid) * 32 * 8);
-      cudaMemsetAsync(dprof, 0, static_cast<size_t>(grid) * 32 * 8, s);
-      esp::k::ring_attention_pairs_profiled(Q, K, V, O, nr, nr, heads, head_dim, dseg, dwork,
-                                            n_work, scale, s, dprof);
+      DevMem dprof(static_cast<size_t>(grid) * 32 * 8);
+      cudaMemsetAsync(dprof.p, 0, static_cast<size_t>(grid) * 32 * 8, s);
+      esp::k::ring_attention_profiled(static_cast<bf16*>(Q.p), static_cast<bf16*>(K.p),
+                                      static_cast<bf16*>(V.p), static_cast<bf16*>(O.p), nr, nr,
+                                      heads, head_dim, segs, wk, n_work, scale, s,
+                                      static_cast<uint64_t*>(dprof.p));
       std::vector<uint64_t> h(static_cast<size_t>(grid) * 32);
-      cudaMemcpyAsync(h.data(), dprof, h.size() * 8, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(h.data(), dprof.p, h.size() * 8, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
-      cudaFree(dprof);
-      const char* names[4][8] = {
-          {"q_empty", "k_empty", "v_empty", "-", "-", "-", "-", "total"},
-          {"q_full", "k_full", "v_full", "p_full0", "p_full1", "o_free", "-", "total"},
-          {"s_wait", "step", "to_ld", "to_max", "to_st_issue", "steps", "final_wait", "total"},
-          {"s_wait", "step", "to_ld", "to_max", "to_st_issue", "steps", "final_wait", "total"}};
       const char* roles[4] = {"producer", "mma", "softmax0", "softmax1"};
       for (int r = 0; r < 4; ++r) {
         std::fprintf(stderr, "[attn-prof] %-9s", roles[r]);
         for (int c = 0; c < 8; ++c) {
-          if (names[r][c][0] == '-') continue;
           double sum = 0;
           for (int b = 0; b < grid; ++b) sum += static_cast<double>(h[(b * 4 + r) * 8 + c]);
-          std::fprintf(stderr, " %s=%.0f", names[r][c], sum / grid);
+          std::fprintf(stderr, " c%d=%.0f", c, sum / grid);
         }
         std::fprintf(stderr, "\n");
       }
-    } else {
-      esp::k::ring_attention_variant(variant, Q, K, V, O, nr, nr, heads, head_dim, dseg, 1, dwork,
-                                     n_work, scale, s);
-      if (const char* rep = std::getenv("ESP_ATTN_REPEAT")) {
-        // Kernel study: time n more launches on the staged buffers (stderr).
-        const int n = std::max(1, std::atoi(rep));
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, s);
-        for (int i = 0; i < n; ++i) {
-          esp::k::ring_attention_variant(variant, Q, K, V, O, nr, nr, heads, head_dim, dseg, 1,
-                                         dwork, n_work, scale, s);
-        }
-        cudaEventRecord(e1, s);
-        cudaEventSynchronize(e1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
-        std::fprintf(stderr, "[attn-time] variant %d: %.4f ms/launch over %d launches\n",
-                     variant, ms / n, n);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-      }
     }
-    cudaMemcpyAsync(out, O, static_cast<size_t>(q_len) * hidden * 2, cudaMemcpyDeviceToDevice, s);
-    const cudaError_t e = cudaStreamSynchronize(s);
-    cudaFree(Q);
-    cudaFree(K);
-    cudaFree(V);
-    cudaFree(O);
-    cudaFree(dseg);
-    cudaFree(dwork);
-    if (e != cudaSuccess) throw esp::CudaError(cudaGetErrorString(e));
+#endif
+    esp::k::ring_attention(static_cast<bf16*>(Q.p), static_cast<bf16*>(K.p),
+                           static_cast<bf16*>(V.p), static_cast<bf16*>(O.p), nr, nr, heads,
+                           head_dim, segs, wk, n_work, scale, s);
+    esp::cuda_ok(cudaGetLastError(), "ring_attention launch");
+    esp::cuda_ok(cudaMemcpyAsync(out, O.p, static_cast<size_t>(q_len) * hidden * 2,
+                                 cudaMemcpyDeviceToDevice, s), "d2d");
+    esp::cuda_ok(cudaStreamSynchronize(s), "ring_attention hook");
   });
 }
 
@@ -522,11 +508,17 @@ int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_sl
                            void* out, int32_t heads, int32_t head_dim, void* stream) {
   return guarded([&] {
     if (n_chunks > esp::k::kMaxSlabs) throw esp::ConfigError("too many chunks for the hook");
+    if (!q || !k_slab || !v_slab || !slot_idx || !n_slots || !chunk_req || !out) {
+      throw esp::ConfigError("decode_attention hook: null argument");
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     esp::k::DecodeSlabs slabs{};
     std::vector<esp::k::DecodeChunk> ch;
     std::vector<std::pair<int32_t, int>> by_row;
-    for (int c = 0; c < n_chunks; ++c) by_row.emplace_back(chunk_req[c], c);
+    for (int c = 0; c < n_chunks; ++c) {
+      if (chunk_req[c] < 0 || chunk_req[c] >= batch) throw esp::ConfigError("chunk row out of range");
+      by_row.emplace_back(chunk_req[c], c);
+    }
     std::stable_sort(by_row.begin(), by_row.end());
     std::vector<int32_t> row_start(static_cast<size_t>(batch) + 1, 0);
     for (const auto& [row, c] : by_row) {
@@ -535,31 +527,29 @@ int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_sl
       // split into the runtime's chunk size, as esp_decode_step does
       for (int32_t c0 = 0; c0 < n_slots[c]; c0 += esp::decode_chunk()) {
         ch.push_back({slot_idx[c] + c0, std::min<int32_t>(esp::decode_chunk(), n_slots[c] - c0), row,
-                      c, static_cast<int32_t>(ch.size())});
+                      c, static_cast<int32_t>(ch.size()), 0});
         row_start[row + 1]++;
       }
     }
     const int32_t n_parts = static_cast<int32_t>(ch.size());
     for (int r = 0; r < batch; ++r) row_start[r + 1] += row_start[r];
-    esp::k::DecodeChunk* dch = nullptr;
-    int32_t* drs = nullptr;
-    float *po = nullptr, *pml = nullptr;
-    cudaMalloc(&dch, ch.size() * sizeof(esp::k::DecodeChunk) + 16);
-    cudaMalloc(&drs, row_start.size() * 4);
-    cudaMalloc(&po, static_cast<size_t>(n_parts) * heads * head_dim * 4 + 16);
-    cudaMalloc(&pml, static_cast<size_t>(n_parts) * heads * 2 * 4 + 16);
-    cudaMemcpyAsync(dch, ch.data(), ch.size() * sizeof(esp::k::DecodeChunk), cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(drs, row_start.data(), row_start.size() * 4, cudaMemcpyHostToDevice, s);
+    DevMem dch(ch.size() * sizeof(esp::k::DecodeChunk) + 16), drs(row_start.size() * 4);
+    DevMem po(static_cast<size_t>(n_parts) * heads * head_dim * 4 + 16);
+    DevMem pml(static_cast<size_t>(n_parts) * heads * 2 * 4 + 16);
+    esp::cuda_ok(cudaMemcpyAsync(dch.p, ch.data(), ch.size() * sizeof(esp::k::DecodeChunk),
+                                 cudaMemcpyHostToDevice, s), "h2d");
+    esp::cuda_ok(cudaMemcpyAsync(drs.p, row_start.data(), row_start.size() * 4,
+                                 cudaMemcpyHostToDevice, s), "h2d");
     const float scale = 1.0f / std::sqrt(static_cast<float>(head_dim));
-    esp::k::decode_attention(static_cast<const esp::k::bf16*>(q), dch, n_parts, slabs, heads,
-                             head_dim, scale, po, pml, s);
-    esp::k::decode_combine(po, pml, drs, batch, heads, head_dim, static_cast<esp::k::bf16*>(out), s);
-    const cudaError_t e = cudaStreamSynchronize(s);
-    cudaFree(dch);
-    cudaFree(drs);
-    cudaFree(po);
-    cudaFree(pml);
-    if (e != cudaSuccess) throw esp::CudaError(cudaGetErrorString(e));
+    esp::k::decode_attention(static_cast<const esp::k::bf16*>(q),
+                             static_cast<const esp::k::DecodeChunk*>(dch.p), n_parts, slabs,
+                             heads, head_dim, scale, static_cast<float*>(po.p),
+                             static_cast<float*>(pml.p), s);
+    esp::k::decode_combine(static_cast<float*>(po.p), static_cast<float*>(pml.p),
+                           static_cast<int32_t*>(drs.p), batch, heads, head_dim,
+                           static_cast<esp::k::bf16*>(out), s);
+    esp::cuda_ok(cudaGetLastError(), "decode_attention launch");
+    esp::cuda_ok(cudaStreamSynchronize(s), "decode_attention hook");
   });
 }
 

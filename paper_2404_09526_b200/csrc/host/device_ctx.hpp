@@ -57,16 +57,16 @@ struct DeviceCtx {
   // activations / scratch
   DevBuf x, xn, q, kb, vb, attn, h, logits, tok, pos, rinst, rslot, segs, work, last_rows,
       out_tok, chunks, row_start, part_o, part_ml, counts, result, kvrow, ret_rows, ret_slab,
-      ret_slot, qin, chunk_ids, row_list, combine_cnt, ss1, ss2;
+      ret_slot, qin, chunk_ids, row_list, ss1, ss2;
   std::vector<void*> weight_allocs;
   std::vector<cudaEvent_t> sync_events;  // cross-domain event pool
   size_t sync_used = 0;
 };
 
-// Work list of the ring-attention kernels (pairs: v2) for `segs`, in the
-// order persistent CTAs should take it (runtime_multi.cpp).
-void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bool pairs,
-                          int64_t kv_rows, int head_dim, std::vector<int32_t>& work_sorted);
+// Work list of K1 (items = (segment, query-tile pair, head)) for `segs`, in
+// the order the persistent CTAs take it (runtime_multi.cpp).
+void build_attention_work(const std::vector<k::RingSegment>& segs, int heads,
+                          std::vector<int32_t>& work_sorted);
 // Number of work items in a list built by build_attention_work.
 int attention_n_work(const std::vector<int32_t>& work);
 

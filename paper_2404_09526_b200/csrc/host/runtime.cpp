@@ -58,8 +58,11 @@ void Runtime::phase_times(double* ms, int64_t* launches, int n) {
 Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
                  int64_t kv_capacity)
     : cfg_(cfg) {
-  attn_variant_ = k::attention_variant();
-  attn_pairs_ = k::attention_pairs(attn_variant_);
+  opts_.domain_per_instance = std::getenv("ESP_DOMAIN_PER_INSTANCE") != nullptr;
+  opts_.ring_copy = std::getenv("ESP_RING_COPY") != nullptr;
+  opts_.decode_copy = std::getenv("ESP_DECODE_COPY") != nullptr;
+  opts_.fuse_norm_prefill = std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr;
+  opts_.fuse_norm_decode = std::getenv("ESP_DECODE_NORM_KERNEL") == nullptr;
   if (n_instances <= 0) throw ConfigError("need at least one instance");
   if (cfg.layers <= 0 || cfg.hidden <= 0 || cfg.heads <= 0 || cfg.head_dim <= 0 ||
       cfg.ffn <= 0 || cfg.vocab <= 0) {
@@ -82,7 +85,7 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
     // Co-location domains: one per physical GPU, or one per instance when
     // ESP_DOMAIN_PER_INSTANCE is set (exercises the cross-device transport
     // on a single GPU).
-    const bool per_instance = std::getenv("ESP_DOMAIN_PER_INSTANCE") != nullptr;
+    const bool per_instance = opts_.domain_per_instance;
     std::map<int, DeviceCtx*> by_key;
     for (int i = 0; i < n_instances; ++i) {
       const int d = devices[i];
@@ -188,7 +191,7 @@ Runtime::~Runtime() {
                       &dc.last_rows, &dc.out_tok, &dc.chunks, &dc.row_start, &dc.part_o,
                       &dc.part_ml, &dc.counts, &dc.result, &dc.kvrow, &dc.ret_rows,
                       &dc.ret_slab, &dc.ret_slot, &dc.qin, &dc.chunk_ids, &dc.row_list,
-                      &dc.combine_cnt, &dc.ss1, &dc.ss2};
+                      &dc.ss1, &dc.ss2};
     for (DevBuf* b : bufs) {
       if (b->ptr) cudaFree(b->ptr);
     }
@@ -515,7 +518,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
     }
   }
   std::vector<int32_t> work_sorted;
-  build_attention_work(segs, cfg_.heads, attn_pairs_, rows, cfg_.head_dim, work_sorted);
+  build_attention_work(segs, cfg_.heads, work_sorted);
   if (cap_armed_) {  // parity capture: stripe row of each captured position
     if (n != 1) throw ConfigError("attention capture needs a single-request prefill");
     for (size_t c = 0; c < cap_pos_.size(); ++c) {
@@ -691,10 +694,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
     timed(kPhQkv, s, [&] { k::gemm(a_in, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     // Striped ring attention over all d rounds.
     timed(kPhAttention, s, [&] {
-      k::ring_attention_variant(attn_variant_, q, kb, vb, attn, rows, rows, cfg_.heads,
-                                cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr),
-                                static_cast<int>(segs.size()),
-                                static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
+      k::ring_attention(q, kb, vb, attn, rows, rows, cfg_.heads, cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr), static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
     });
     if (cap_armed_) cap_layer(dc, l, attn, s);
     NormFuse nf;
@@ -940,7 +940,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
     sg.kv_len[0] = kv_n;
     sg.shift[0] = -static_cast<int32_t>(p_prev);
     std::vector<k::RingSegment> segs{sg};
-    build_attention_work(segs, cfg_.heads, attn_pairs_, kv_n, cfg_.head_dim, work_sorted);
+    build_attention_work(segs, cfg_.heads, work_sorted);
     k::RingSegment* d_segs = scratch<k::RingSegment>(dc.segs, 1);
     int32_t* d_work = scratch<int32_t>(dc.work, work_sorted.size());
     cuda_ok(cudaMemcpyAsync(d_segs, &sg, sizeof(sg), cudaMemcpyHostToDevice, s), "h2d");
@@ -959,23 +959,11 @@ void Runtime::decode_step(const esp_decode_args& a) {
   float* part_ml = scratch<float>(dc.part_ml, static_cast<size_t>(std::max(n_chunks, 1)) * cfg_.heads * 2);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
   const int n_work = attention_n_work(work_sorted);
-  // ESP_DECODE_FUSED_COMBINE=1: LSE combine inside the attention kernel.
-  static const bool fused_combine = [] {
-    const char* e = std::getenv("ESP_DECODE_FUSED_COMBINE");
-    return e != nullptr && e[0] == '1';
-  }();
-  // Fused-combine counters: zero on allocation, left zero by every launch.
-  const size_t cnt_bytes = dc.combine_cnt.bytes;
-  int* d_cnt = scratch<int>(dc.combine_cnt, static_cast<size_t>(std::max(b, 1)) * cfg_.heads);
-  if (dc.combine_cnt.bytes != cnt_bytes) {
-    cuda_ok(cudaMemsetAsync(d_cnt, 0, dc.combine_cnt.bytes, s), "memset");
-  }
-
   // Decode-shaped steps (<= 32 rows): each layer RMSNorm is fused into the
   // skinny GEMMs — the residual epilogues accumulate row sums of squares
   // (ss1 before QKV, ss2 before gate_up) and the consuming GEMM scales its
   // accumulator rows (gains folded into the weights); no norm kernels.
-  const bool fuse_norm = rows <= 32 && std::getenv("ESP_DECODE_NORM_KERNEL") == nullptr;
+  const bool fuse_norm = rows <= 32 && opts_.fuse_norm_decode;
   float* ss1 = scratch<float>(dc.ss1, 32);
   float* ss2 = scratch<float>(dc.ss2, 32);
   if (fuse_norm) cuda_ok(cudaMemsetAsync(ss2, 0, 32 * sizeof(float), s), "memset");
@@ -1012,14 +1000,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
       slabs.v[j] = ep.slab_v[j];
     }
     timed(kPhQkv, s, [&] { k::gemm(a_in, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
-    if (b > 0 && fused_combine) {
-      // Split-KV attention with the LSE combine fused (the last CTA of each
-      // (row, head) merges the row's chunk partials).
-      timed(kPhDecodeAttn, s, [&] {
-        k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
-                            part_o, part_ml, s, d_rs, d_cnt, attn, b);
-      });
-    } else if (b > 0) {
+    if (b > 0) {
       timed(kPhDecodeAttn, s, [&] {
         k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
                             part_o, part_ml, s);
@@ -1031,9 +1012,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
     if (has_chunk) {
       timed(kPhAttention, s, [&] {
         k::gather_rows(slabs, d_gslab, d_gslot, kv_n, kg, vg, H, s);
-        k::ring_attention_variant(attn_variant_, q, kg, vg, attn, rows, kv_n, cfg_.heads,
-                                  cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr),
-                                  1, static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
+        k::ring_attention(q, kg, vg, attn, rows, kv_n, cfg_.heads, cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr), static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
       });
     }
     NormFuse nf;

@@ -175,8 +175,25 @@ class Runtime {
   };
   void o_and_mlp(DeviceCtx& dc, int l, int rows, k_bf16* x, const k_bf16* attn, k_bf16* xn,
                  k_bf16* hbuf, const NormFuse& nf, cudaStream_t s);
-  // RMSNorm fused into the single-domain prefill GEMMs (ESP_PREFILL_NORM_KERNEL=1: kernels).
-  static bool fuse_norm_prefill() { return std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr; }
+  // Data-path options, read ONCE from the environment when the runtime is
+  // created (never per launch):
+  //   ESP_DOMAIN_PER_INSTANCE  every instance its own co-location domain
+  //                            (the cross-GPU transport on one GPU);
+  //   ESP_RING_COPY            prefill ring by peer copies in the reference's
+  //                            round order instead of the fused push;
+  //   ESP_DECODE_COPY          decode query broadcast / partial gather by peer
+  //                            copies instead of fused peer stores;
+  //   ESP_PREFILL_NORM_KERNEL / ESP_DECODE_NORM_KERNEL  RMSNorm as kernels
+  //                            instead of fused into the GEMMs.
+  struct Options {
+    bool domain_per_instance = false;
+    bool ring_copy = false;
+    bool decode_copy = false;
+    bool fuse_norm_prefill = true;
+    bool fuse_norm_decode = true;
+  };
+  Options opts_;
+  bool fuse_norm_prefill() const { return opts_.fuse_norm_prefill; }
   void forward_layers_prefill(DeviceCtx& dc, int rows, const std::vector<k::RingSegment>& segs,
                               const std::vector<int32_t>& work);
   template <typename T>
@@ -216,9 +233,6 @@ class Runtime {
   void cap_layer(DeviceCtx& dc, int l, const k_bf16* attn, cudaStream_t s);
   // After the prefill synchronized: gather the rows to the host and disarm.
   void cap_finish();
-  // K1 variant: v2 (two query tiles per CTA, P in TMEM) unless ESP_ATTN_V1=1.
-  int attn_variant_ = 2;     // K1 variant (ESP_ATTN), set in the constructor
-  bool attn_pairs_ = true;   // its work items are query-tile pairs
   struct PhaseEvent {
     int phase;
     cudaEvent_t a, b;

@@ -37,14 +37,14 @@
 
 namespace esp {
 
-void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bool pairs,
-                          int64_t kv_rows, int head_dim, std::vector<int32_t>& work_sorted) {
+void build_attention_work(const std::vector<k::RingSegment>& segs, int heads,
+                          std::vector<int32_t>& work_sorted) {
   struct ItemC {
     int32_t seg, packed;
     int64_t cost;
   };
   std::vector<std::vector<ItemC>> per_sh;  // items of one (segment, head)
-  const int span = pairs ? 2 : 1;
+  constexpr int span = 2;  // a work item is a pair of 128-row query tiles
   for (size_t si = 0; si < segs.size(); ++si) {
     const k::RingSegment& sg = segs[si];
     const int n_items = (k::q_tiles(sg.q_len) + span - 1) / span;
@@ -120,9 +120,8 @@ void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bo
     per_cta[best].push_back(&u);
     load[best] += u.cost;
   }
-  // Layout: [items: 2 ints each, CTA-contiguous][G][offsets 0..G][n_items].
-  // Kernels with a per-CTA schedule (v2) read G and the offsets; the others
-  // take the items round-robin, which covers them all as well.
+  // Layout: [items: 2 ints each, CTA-contiguous][G][offsets 0..G][n_items];
+  // CTA c of K1 takes items offsets[c] .. offsets[c+1].
   work_sorted.clear();
   std::vector<int32_t> offsets{0};
   int n_items = 0;
@@ -136,8 +135,6 @@ void build_attention_work(const std::vector<k::RingSegment>& segs, int heads, bo
     }
     offsets.push_back(n_items);
   }
-  (void)kv_rows;
-  (void)head_dim;
   work_sorted.push_back(G);
   work_sorted.insert(work_sorted.end(), offsets.begin(), offsets.end());
   work_sorted.push_back(n_items);
@@ -208,7 +205,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
   // its resting page slot wherever that is (peer stores), so the ring's
   // all-gather and the retention ride inside the GEMM; or the copy-engine
   // ring in the reference's round order (ESP_RING_COPY=1).
-  const bool push = std::getenv("ESP_RING_COPY") == nullptr &&
+  const bool push = !opts_.ring_copy &&
                     instances_.size() <= static_cast<size_t>(k::kMaxSlabs) &&
                     dom_set.size() <= static_cast<size_t>(k::kMaxPeers) + 1;
   for (int i = 0; i < d; ++i) {
@@ -264,7 +261,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         p.segs.push_back(sg);
       }
     }
-    build_attention_work(p.segs, cfg_.heads, attn_pairs_, rows, cfg_.head_dim, p.work);
+    build_attention_work(p.segs, cfg_.heads, p.work);
   }
   if (cap_armed_) {  // parity capture: (domain, local stripe row) of each position
     if (n != 1) throw ConfigError("attention capture needs a single-request prefill");
@@ -432,11 +429,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       timed(kPhAttention, s, [&] {
         const bf16* qd = static_cast<bf16*>(dc.q.ptr);
         // Q rows are this domain's local rows, K/V rows are global.
-        k::ring_attention_variant(attn_variant_, qd, static_cast<bf16*>(dc.kb.ptr),
-                                  static_cast<bf16*>(dc.vb.ptr), attn, p.rows, rows, cfg_.heads,
-                                  cfg_.head_dim, static_cast<k::RingSegment*>(dc.segs.ptr),
-                                  static_cast<int>(p.segs.size()),
-                                  static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
+        k::ring_attention(qd, static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr), attn, p.rows, rows, cfg_.heads, cfg_.head_dim, static_cast<k::RingSegment*>(dc.segs.ptr), static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
       });
       if (cap_armed_) cap_layer(dc, l, attn, s);
       if (push) {  // peers may overwrite this gather buffer with the next layer
@@ -561,7 +554,7 @@ void Runtime::chunk_multi(const esp_decode_args& a, int64_t p_prev,
   sg.kv_len[0] = kv_n;
   sg.shift[0] = -static_cast<int32_t>(p_prev);
   std::vector<int32_t> work;
-  build_attention_work({sg}, cfg_.heads, attn_pairs_, kv_n, cfg_.head_dim, work);
+  build_attention_work({sg}, cfg_.heads, work);
   k::RingSegment* d_seg = scratch<k::RingSegment>(dc.segs, 1);
   cuda_ok(cudaMemcpyAsync(d_seg, &sg, sizeof(sg), cudaMemcpyHostToDevice, s), "h2d");
   h2d(scratch<int32_t>(dc.work, work.size()), work, s);
@@ -600,8 +593,7 @@ void Runtime::chunk_multi(const esp_decode_args& a, int64_t p_prev,
     }
     k::gemm(xn, H, w.wqkv, H, c, 3 * H, H, ep, s);
     k::gather_rows(slabs, d_gi, d_gs, kv_n, kg, vg, H, s);
-    k::ring_attention_variant(attn_variant_, q, kg, vg, attn, c, kv_n, cfg_.heads, cfg_.head_dim,
-                              d_seg, 1, static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
+    k::ring_attention(q, kg, vg, attn, c, kv_n, cfg_.heads, cfg_.head_dim, d_seg, static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
     o_and_mlp(dc, l, c, x, attn, xn, hbuf, NormFuse{}, s);
   }
   int32_t first = -1;
@@ -758,7 +750,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
   // partials straight into the master domains' partial buffers (the gather as
   // peer stores). Only events order the domains. ESP_DECODE_COPY=1 keeps the
   // copy-engine transport (peer copies of row runs / chunk ranges).
-  const bool copy_transport = std::getenv("ESP_DECODE_COPY") != nullptr;
+  const bool copy_transport = opts_.decode_copy;
   // Per master domain: the KV domains its rows need (q destinations); per KV
   // domain: the master domains it owes partials (PartDst entries).
   std::map<int, std::vector<int>> q_dests;
@@ -862,8 +854,7 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
                               static_cast<k::DecodeChunk*>(xc.chunks.ptr),
                               static_cast<int>(chs.size()), slabs, heads, hd, scale,
                               static_cast<float*>(xc.part_o.ptr),
-                              static_cast<float*>(xc.part_ml.ptr), s, nullptr, nullptr, nullptr,
-                              0, &pd);
+                              static_cast<float*>(xc.part_ml.ptr), s, &pd);
         });
         cudaEvent_t e = sync_event(xc);
         cuda_ok(cudaEventRecord(e, s), "event");

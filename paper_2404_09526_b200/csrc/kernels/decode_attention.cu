@@ -13,7 +13,6 @@
 // K4 (LSE combine at the master): o = sum_c e^{m_c-M} o_c / sum_c e^{m_c-M} l_c
 // over all chunks of the request, on every instance that held its KV.
 #include <cfloat>
-#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.h"
@@ -56,38 +55,12 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   }
 }
 
-// Fused LSE combine (single-domain decode): the last CTA to finish a (row,
-// head) merges that row's chunk partials (row_start) into the bf16 output.
-struct FusedCombine {
-  const int32_t* row_start = nullptr;  // null: partials only (combined elsewhere)
-  int* counters = nullptr;             // [rows x heads], zero between launches
-  bf16* out = nullptr;
-};
-
-template <int HD>
-__device__ __forceinline__ void combine_row_head(const float* part_o, const float* part_ml,
-                                                 int c0, int c1, int heads, int head, bf16* out) {
-  float mm = -INFINITY;
-  for (int c = c0; c < c1; ++c) mm = fmaxf(mm, __ldcg(&part_ml[(static_cast<int64_t>(c) * heads + head) * 2]));
-  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
-    float acc = 0.f, ll = 0.f;
-    for (int c = c0; c < c1; ++c) {
-      const int64_t p = static_cast<int64_t>(c) * heads + head;
-      const float mc = __ldcg(&part_ml[p * 2]);
-      const float w = mc == -INFINITY ? 0.f : exp2f(mc - mm);
-      acc += w * __ldcg(&part_o[p * HD + d]);
-      ll += w * __ldcg(&part_ml[p * 2 + 1]);
-    }
-    out[d] = __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
-  }
-}
-
 template <int HD, int UNR = kUnroll, int MINB = 1, int PF = 0, int W = kWarps>
 __global__ void __launch_bounds__(W * 32, MINB)
     decode_attention_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
                             const DecodeSlabs slabs, int heads, float scale_log2,
                             float* __restrict__ part_o, float* __restrict__ part_ml,
-                            const FusedCombine fc, const PartDst dst) {
+                            const PartDst dst) {
   constexpr int LPT = HD / 8;     // lanes per token
   constexpr int TPW = 32 / LPT;   // tokens per warp step
   // blockIdx.x = head (fastest): the CTAs resident at a time cover every head
@@ -228,187 +201,6 @@ __global__ void __launch_bounds__(W * 32, MINB)
       part_ml[pidx * 2 + 1] = ll;
     }
   }
-  if (fc.row_start != nullptr) {
-    __shared__ int last;
-    __threadfence();
-    __syncthreads();
-    const int c0 = __ldg(&fc.row_start[ch.row]), c1 = __ldg(&fc.row_start[ch.row + 1]);
-    int* cnt = &fc.counters[ch.row * heads + head];
-    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == c1 - c0 - 1;
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      combine_row_head<HD>(part_o, part_ml, c0, c1, heads, head,
-                           fc.out + static_cast<int64_t>(ch.row) * hidden + head * HD);
-      if (threadIdx.x == 0) *cnt = 0;
-    }
-  }
-}
-
-// K3 v2: the same (chunk, head) decomposition with the K/V loads decoupled
-// from the registers. The chunk's slot ids are staged in shared memory once
-// (one coalesced read, no dependent index load per token), then every lane
-// streams its own 16-byte K and V pieces through an NS-stage cp.async.cg ring
-// in shared memory (L2 only, no L1 allocation). Each lane reads back exactly
-// the bytes it copied, so a per-thread cp.async.wait_group is the only
-// synchronisation; NS-1 stages (NS-1 x 16 KB per CTA) stay in flight while
-// the current stage is reduced, independent of the register budget. U tokens
-// per lane share one running-max update (one rescale exp per U tokens).
-__device__ __forceinline__ void cp_async_cg16(void* smem, const void* gmem) {
-  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-constexpr int kV2MaxChunk = 1024;
-
-template <int HD, int NS>
-__global__ void __launch_bounds__(kWarps * 32)
-    decode_attention_v2_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
-                               const DecodeSlabs slabs, int heads, float scale_log2,
-                               float* __restrict__ part_o, float* __restrict__ part_ml) {
-  constexpr int LPT = HD / 8;         // lanes per token
-  constexpr int TPW = 32 / LPT;       // tokens per warp per load instruction
-  constexpr int U = kUnroll;          // load instructions per lane per stage
-  constexpr int TOK_W = TPW * U;      // tokens per warp per stage
-  constexpr int TOK_S = TOK_W * kWarps;  // tokens per CTA per stage
-  extern __shared__ uint4 ring[];     // [NS][warp][U][lane][K,V]
-  __shared__ int32_t sidx[kV2MaxChunk];
-  const int head = blockIdx.x;
-  const DecodeChunk ch = chunks[blockIdx.y];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane / LPT, dl = lane % LPT;
-  const int hidden = heads * HD;
-  for (int i = threadIdx.x; i < ch.n; i += blockDim.x) sidx[i] = __ldg(&ch.slots[i]);
-
-  float qf[8];
-  bf16x8_to_f32(*reinterpret_cast<const uint4*>(q + static_cast<int64_t>(ch.row) * hidden +
-                                                head * HD + dl * 8),
-                qf);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) qf[e] *= scale_log2;
-  const bf16* kb = pick(slabs.k, ch.slab) + head * HD + dl * 8;
-  const bf16* vb = pick(slabs.v, ch.slab) + head * HD + dl * 8;
-  __syncthreads();
-
-  const int n_stages = (ch.n + TOK_S - 1) / TOK_S;
-  auto issue = [&](int st) {
-    if (st < n_stages) {
-      uint4* buf = ring + ((st % NS) * kWarps + warp) * U * 64;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = st * TOK_S + warp * TOK_W + u * TPW + sub;
-        if (t < ch.n) {
-          const int64_t off = static_cast<int64_t>(sidx[t]) * hidden;
-          cp_async_cg16(&buf[(u * 32 + lane) * 2], kb + off);
-          cp_async_cg16(&buf[(u * 32 + lane) * 2 + 1], vb + off);
-        }
-      }
-    }
-    cp_async_commit();  // empty groups past the end keep the wait count uniform
-  };
-#pragma unroll
-  for (int st = 0; st < NS - 1; ++st) issue(st);
-
-  float m = -INFINITY, l = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int st = 0; st < n_stages; ++st) {
-    issue(st + NS - 1);
-    cp_async_wait<NS - 1>();
-    const uint4* buf = ring + ((st % NS) * kWarps + warp) * U * 64;
-    float sc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = st * TOK_S + warp * TOK_W + u * TPW + sub;
-      float kf[8];
-      bf16x8_to_f32(buf[(u * 32 + lane) * 2], kf);
-      float s = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s = fmaf(qf[e], kf[e], s);
-#pragma unroll
-      for (int w = LPT / 2; w >= 1; w >>= 1) s += __shfl_xor_sync(0xffffffff, s, w);
-      sc[u] = t < ch.n ? s : -INFINITY;
-    }
-    float mx = m;
-#pragma unroll
-    for (int u = 0; u < U; ++u) mx = fmaxf(mx, sc[u]);
-    if (mx == -INFINITY) continue;  // nothing valid for this token group yet
-    const float corr = exp2f(m - mx);
-    l *= corr;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] *= corr;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const float p = exp2f(sc[u] - mx);
-      if (sc[u] != -INFINITY) {
-        float vf[8];
-        bf16x8_to_f32(buf[(u * 32 + lane) * 2 + 1], vf);
-        l += p;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = fmaf(p, vf[e], o[e]);
-      }
-    }
-    m = mx;
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int w = LPT; w < 32; w <<= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffff, m, w);
-    const float l2 = __shfl_xor_sync(0xffffffff, l, w);
-    const float mm = fmaxf(m, m2);
-    const float c1 = m == -INFINITY ? 0.f : exp2f(m - mm);
-    const float c2 = m2 == -INFINITY ? 0.f : exp2f(m2 - mm);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float o2 = __shfl_xor_sync(0xffffffff, o[e], w);
-      o[e] = o[e] * c1 + o2 * c2;
-    }
-    l = l * c1 + l2 * c2;
-    m = mm;
-  }
-  __shared__ float sm_m[kWarps], sm_l[kWarps];
-  __shared__ float sm_o[kWarps][HD];
-  if (sub == 0) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) sm_o[warp][dl * 8 + e] = o[e];
-    if (dl == 0) {
-      sm_m[warp] = m;
-      sm_l[warp] = l;
-    }
-  }
-  __syncthreads();
-  const int64_t pidx = static_cast<int64_t>(ch.out) * heads + head;
-  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
-    float mm = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) mm = fmaxf(mm, sm_m[w]);
-    float acc = 0.f, ll = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const float c = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - mm);
-      acc += c * sm_o[w][d];
-      ll += c * sm_l[w];
-    }
-    part_o[pidx * HD + d] = acc;
-    if (d == 0) {
-      part_ml[pidx * 2] = mm;
-      part_ml[pidx * 2 + 1] = ll;
-    }
-  }
-}
-
-template <int HD, int NS>
-void launch_decode_v2(const dim3& grid, cudaStream_t s, const bf16* q, const DecodeChunk* chunks,
-                      const DecodeSlabs& slabs, int heads, float sl2, float* part_o,
-                      float* part_ml) {
-  constexpr int smem = NS * kWarps * kUnroll * 64 * 16;
-  once_per_device(reinterpret_cast<const void*>(decode_attention_v2_kernel<HD, NS>), [] {
-    cudaFuncSetAttribute(decode_attention_v2_kernel<HD, NS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  });
-  decode_attention_v2_kernel<HD, NS><<<grid, kWarps * 32, smem, s>>>(q, chunks, slabs, heads, sl2,
-                                                                     part_o, part_ml);
 }
 
 __global__ void decode_combine_kernel(const float* __restrict__ part_o,
@@ -534,81 +326,25 @@ void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slo
 
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
-                      float* part_o, float* part_ml, cudaStream_t s, const int32_t* row_start,
-                      int* counters, bf16* out, int rows, const PartDst* dst) {
+                      float* part_o, float* part_ml, cudaStream_t s, const PartDst* dst) {
   if (n_chunks <= 0) return;
   const PartDst pd = dst ? *dst : PartDst{};
-  FusedCombine fc;
-  fc.row_start = row_start;
-  fc.counters = counters;
-  fc.out = out;
   if (n_chunks > 65535) throw std::runtime_error("decode_attention: more than 65535 chunks");
   const dim3 grid(heads, n_chunks);
   const float sl2 = scale * 1.4426950408889634f;
-  // Default: the register-staged v1 at <= 64 registers (8 CTAs of 4 warps
-  // per SM), 3 tokens per lane in flight and the next iteration's slot ids
-  // loaded one iteration ahead: 6.81-6.85 TB/s on 16 x 8K (4 in flight
-  // without the look-ahead: 6.44-6.47; tools/decode_probe.py sweeps). ESP_DECODE_ATTN=2: the
-  // cp.async ring (v2) with ESP_DECODE_STAGES stages — slower on B200
-  // (3.3-4.0 TB/s: its shared-memory ring caps resident CTAs per SM).
-  const char* var = std::getenv("ESP_DECODE_ATTN");
-  if (var != nullptr && std::atoi(var) == 2 && dst == nullptr) {
-    const char* st = std::getenv("ESP_DECODE_STAGES");
-    const int ns = st ? std::atoi(st) : 4;
-    if (head_dim != 128 && head_dim != 64) {
-      throw std::runtime_error("decode_attention: head_dim must be 64 or 128");
-    }
-#define ESP_V2(HD, NS) launch_decode_v2<HD, NS>(grid, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml)
-    if (head_dim == 128) {
-      if (ns <= 2) ESP_V2(128, 2); else if (ns == 3) ESP_V2(128, 3); else if (ns == 4) ESP_V2(128, 4); else ESP_V2(128, 6);
-    } else {
-      if (ns <= 2) ESP_V2(64, 2); else if (ns == 3) ESP_V2(64, 3); else if (ns == 4) ESP_V2(64, 4); else ESP_V2(64, 6);
-    }
-#undef ESP_V2
-    count_launch();
-    if (row_start != nullptr) decode_combine(part_o, part_ml, row_start, rows, heads, head_dim, out, s);
-    return;
-  }
+  // Register-staged loads at <= 64 registers (8 CTAs of 4 warps per SM), 3
+  // tokens per lane in flight and the next iteration's slot ids loaded one
+  // iteration ahead: 6.81-6.85 TB/s on 16 x 8K (4 in flight without the
+  // look-ahead: 6.44-6.47). Measured and dropped (round 1): a cp.async
+  // shared-memory ring (3.3-4.0 TB/s — its ring caps resident CTAs per SM)
+  // and the LSE combine fused into the last CTA of each (row, head) (0.1-0.3
+  // ms/step slower: the fence + counter extend every CTA).
   if (head_dim == 128) {
-    // ESP_DECODE_V1=<unroll><min blocks per SM> tuning variants of v1
-    const char* tv = std::getenv("ESP_DECODE_V1");
-    const int tune = tv ? std::atoi(tv) : 0;
-#define ESP_V1(U, B) launch_pdl(4, decode_attention_kernel<128, U, B>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd)
-    switch (tune) {
-      case 481: launch_pdl(4, decode_attention_kernel<128, 4, 8, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 482: launch_pdl(4, decode_attention_kernel<128, 4, 8, 2>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 381: launch_pdl(4, decode_attention_kernel<128, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 3101: launch_pdl(4, decode_attention_kernel<128, 3, 10, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 281: launch_pdl(4, decode_attention_kernel<128, 2, 8, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 2101: launch_pdl(4, decode_attention_kernel<128, 2, 10, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 2121: launch_pdl(4, decode_attention_kernel<128, 2, 12, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 361: launch_pdl(4, decode_attention_kernel<128, 3, 6, 1>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 3418: launch_pdl(4, decode_attention_kernel<128, 3, 4, 1, 8>, grid, dim3(8 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 2418: launch_pdl(4, decode_attention_kernel<128, 2, 4, 1, 8>, grid, dim3(8 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 31612: launch_pdl(4, decode_attention_kernel<128, 3, 16, 1, 2>, grid, dim3(2 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 3518: launch_pdl(4, decode_attention_kernel<128, 3, 5, 1, 8>, grid, dim3(8 * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 282: launch_pdl(4, decode_attention_kernel<128, 2, 8, 2>, grid, dim3(kWarps * 32), 0, s, q, d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd); break;
-      case 41: ESP_V1(4, 1); break;
-      case 410: ESP_V1(4, 10); break;
-      case 38: ESP_V1(3, 8); break;
-      case 310: ESP_V1(3, 10); break;
-      case 28: ESP_V1(2, 8); break;
-      case 210: ESP_V1(2, 10); break;
-      case 412: ESP_V1(4, 12); break;
-      case 416: ESP_V1(4, 16); break;
-      case 216: ESP_V1(2, 16); break;
-      case 212: ESP_V1(2, 12); break;
-      case 88: ESP_V1(8, 8); break;
-      case 86: ESP_V1(8, 6); break;
-      case 48: ESP_V1(4, 8); break;
-      default:
-        launch_pdl(4, decode_attention_kernel<128, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q,
-                   d_chunks, slabs, heads, sl2, part_o, part_ml, fc, pd);
-    }
-#undef ESP_V1
+    launch_pdl(4, decode_attention_kernel<128, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q,
+               d_chunks, slabs, heads, sl2, part_o, part_ml, pd);
   } else if (head_dim == 64) {
-    decode_attention_kernel<64, 3, 8, 1><<<grid, kWarps * 32, 0, s>>>(q, d_chunks, slabs, heads,
-                                                                     sl2, part_o, part_ml, fc, pd);
+    launch_pdl(4, decode_attention_kernel<64, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q,
+               d_chunks, slabs, heads, sl2, part_o, part_ml, pd);
   } else {
     throw std::runtime_error("decode_attention: head_dim must be 64 or 128");
   }

@@ -52,11 +52,11 @@ struct Cfg {
   static constexpr int kSmem = kARegion + kStages * kBBytes + 1024 + 256;
 };
 
-// m-blocks per raster group (L2 reuse of B); ESP_GEMM_GROUP overrides (study).
-__constant__ int c_raster_group = 16;
+// m-blocks per raster group (L2 reuse of B).
+constexpr int kRasterGroup = 16;
 
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
-  const int kGroup = c_raster_group;
+  constexpr int kGroup = kRasterGroup;
   const int per_group = kGroup * num_n;
   const int g = tile / per_group;
   const int first = g * kGroup;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                       int kb_per_cta, const __grid_constant__ GemmEpilogue ep,
-                      float* __restrict__ ws, int* __restrict__ tile_kb, int b_mode) {
+                      float* __restrict__ ws, int* __restrict__ tile_kb) {
   using C = Cfg<BN, kSkinny>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -394,11 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      // b_mode bit 0: B is pre-tiled ([N/BN][K/BK][BN][BK], each K block of
-      // a tile 16 KB contiguous); bits 1-2: L2 hint for B (0 evict_last,
-      // 1 evict_first, 2 none).
-      const int hint = (b_mode >> 1) & 3;
-      const uint64_t keep = hint == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
+      const uint64_t keep = ptx::policy_evict_last();  // B (weights) is re-read by every M tile
       while (work.get(tile, kb0, kb1)) {
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
@@ -406,13 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full[stage], C::kTxBytes);
           ptx::tma_load_2d(sA + stage * C::kAStride, &tmA, &full[stage], kb * BK, mb * BM);
-          const int bx = (b_mode & 1) ? 0 : kb * BK;
-          const int by = (b_mode & 1) ? (nb * num_k + kb) * BN : nb * BN;
-          if (hint == 2) {
-            ptx::tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], bx, by);
-          } else {
-            ptx::tma_load_2d_hint(sB + stage * C::kBBytes, &tmB, &full[stage], bx, by, keep);
-          }
+          ptx::tma_load_2d_hint(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, nb * BN, keep);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -1092,12 +1082,6 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
-// Study knob (tools/skinny_probe.py): ESP_GEMM_B_MODE, see the producer.
-static int gemm_b_mode() {
-  const char* e = getenv("ESP_GEMM_B_MODE");
-  return e ? atoi(e) : 0;
-}
-
 template <int BN, bool kSkinny>
 static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
                         int kb_per_cta, const GemmEpilogue& ep, cudaStream_t s,
@@ -1108,14 +1092,12 @@ static void launch_gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, i
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const CUtensorMap ta = make_tmap_bf16(A, M, K, lda, C::kARows);
-  const int b_mode = gemm_b_mode();
-  const CUtensorMap tb = (b_mode & 1) ? make_tmap_bf16(B, static_cast<int64_t>(N) * (K / BK), BK, BK, BN)
-                                      : make_tmap_bf16(B, N, K, ldb, BN);
+  const CUtensorMap tb = make_tmap_bf16(B, N, K, ldb, BN);
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
                                   : std::min(tiles, num_sms());
   gemm_bf16_tcgen05<BN, kSkinny><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, kb_per_cta,
-                                                                  ep, ws, tile_kb, b_mode);
+                                                                  ep, ws, tile_kb);
   count_launch();
 }
 
@@ -1139,15 +1121,17 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
                    : SPLIT == -2 ? 2 * std::min(tiles, num_sms() / 2)
                    : kb_per_cta > 0 ? (tiles * (K / BK) + kb_per_cta - 1) / kb_per_cta
                                     : std::min(tiles, num_sms());
-  // Study: ESP_GEMM_TRACE=<file> appends per-CTA globaltimer stamps (entry,
-  // setup done, first stage landed, last MMA, first tile drained, epilogue
-  // done, exit) of every skinny launch to <file> (synchronises the stream).
-  static const char* trace_path = getenv("ESP_GEMM_TRACE");
   unsigned long long* trace = nullptr;
+#ifdef ESP_STUDY
+  // Kernel-study build: ESP_GEMM_TRACE=<file> appends per-CTA globaltimer
+  // stamps (entry, setup done, first stage landed, last MMA, first tile
+  // drained, epilogue done, exit) of every skinny launch to <file>.
+  static const char* trace_path = getenv("ESP_GEMM_TRACE");
   if (trace_path) {
     cudaMalloc(&trace, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long));
     cudaMemsetAsync(trace, 0, static_cast<size_t>(grid) * 8 * sizeof(unsigned long long), s);
   }
+#endif
   if constexpr (SPLIT > 1 || SPLIT == -2) {
     // Cluster of SPLIT CTAs per output tile (split-K reduced over DSMEM) or a
     // persistent CTA pair (SPLIT == -2), with programmatic dependent launch
@@ -1174,6 +1158,7 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
                M, N, K, kb_per_cta, ep, ws, tile_kb, trace);
   }
   count_launch();
+#ifdef ESP_STUDY
   if (trace) {
     std::vector<unsigned long long> h(static_cast<size_t>(grid) * 8);
     cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
@@ -1189,6 +1174,7 @@ static void launch_skinny_swap(const bf16* A, int lda, const bf16* B, int ldb, i
       fclose(f);
     }
   }
+#endif
 }
 
 // Co-resident CTA pairs of the current device (normally num_sms / 2).
@@ -1224,7 +1210,7 @@ static int pair_clusters() {
 
 static bool launch_gemm_pair(const bf16* A, int lda, const bf16* B, int ldb, int M, int N,
                              int K, const GemmEpilogue& ep, cudaStream_t s) {
-  if (getenv("ESP_GEMM_NO_PAIR") != nullptr || M < pair::kTileM || N % pair::kTileN != 0) return false;
+  if (M < pair::kTileM || N % pair::kTileN != 0) return false;
   if (ep.kind == kEpiQkvRope && ep.hidden % pair::kTileN != 0) return false;
   const int clusters = pair_clusters();
   const int units = ((M + pair::kTileM - 1) / pair::kTileM) * (N / pair::kTileN);
@@ -1271,43 +1257,25 @@ StreamKWs streamk_workspace(size_t elems, size_t tiles, cudaStream_t s) {
 }
 
 void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
-          const GemmEpilogue& ep, cudaStream_t s) {
+          const GemmEpilogue& ep, cudaStream_t s, int path) {
   if (M <= 0) return;
-  static const bool group_set = [] {
-    if (const char* e = getenv("ESP_GEMM_GROUP")) {
-      const int g = atoi(e);
-      if (g > 0) cudaMemcpyToSymbol(c_raster_group, &g, sizeof(int));
-    }
-    return true;
-  }();
-  (void)group_set;
-  if (ep.ss_zero != nullptr && (M > 32 || getenv("ESP_GEMM_SKINNY_OLD") != nullptr)) {
+  struct {
+    bool no_pair, no_streamk, streamk_all;
+  } const paths{path == kGemmNoPair, path == kGemmTilesOnly, path == kGemmStreamKAll};
+  if (ep.ss_zero != nullptr && M > 32) {
     throw std::runtime_error("gemm: ss_zero is implemented by the skinny (M <= 32) kernel");
   }
   if (N % 128 != 0 || K % 64 != 0) throw std::runtime_error("gemm: N%128 or K%64 != 0");
   if (M <= 32) {
-    // Decode-shaped: weight-streaming bound. Skinny pipeline, stream-K over
-    // (tile, K block) so every SM streams the same number of weight tiles
-    // whatever N / 128 is (96 QKV tiles, 172 gate_up tiles, 32 O tiles on
-    // 148 SMs); the CTA completing a tile applies the fused epilogue to its
-    // fp32 partial sums.
+    // Decode-shaped: weight-streaming bound (swap-AB skinny kernel: the
+    // 128-row weight tile is the UMMA M operand, the <= 32 token rows its N).
     const int tiles = N / 128, total = tiles * (K / BK);
-    // Stream-K pays when whole tiles would leave most SMs idle (one SM
-    // streams ~82 GB/s of weights, an even share of HBM is ~44 GB/s): O and
-    // down (32 tiles) go from 15.3 / 37.5 us to 13.8 / 21.5 us; QKV (96
-    // tiles) and the wider projections are faster as whole tiles because the
-    // fixup handshake (~5 us) costs more than the imbalance
-    // (tools/skinny_probe.py, swap-AB kernel with PDL).
-    const bool old = getenv("ESP_GEMM_SKINNY_OLD") != nullptr;
-    // Few wide tiles (O, down: 32): split-K over a cluster of 4 CTAs reduced
-    // through distributed shared memory — 128 SMs stream weights and there
-    // is no global fixup (ESP_GEMM_SPLIT=0 falls back to stream-K).
-    static const int split_env = [] {
-      const char* e = getenv("ESP_GEMM_SPLIT");
-      return e ? atoi(e) : 4;
-    }();
-    if (!old && split_env >= 2 && getenv("ESP_GEMM_NO_STREAMK") == nullptr &&
-        getenv("ESP_GEMM_STREAMK_ALL") == nullptr && tiles * 4 <= num_sms() && K / BK >= 16) {
+    const bool forced = paths.no_streamk || paths.streamk_all;
+    // Few wide tiles (O, down: 32 on 148 SMs): split-K over a cluster of 4
+    // CTAs reduced through distributed shared memory — 128 SMs stream
+    // weights and there is no global fixup (O 15.3 -> 10.1 us, down 37.5 ->
+    // 18.2 us; one SM streams ~82 GB/s of weights).
+    if (!forced && tiles * 4 <= num_sms() && K / BK >= 16) {
       if (M <= 16) launch_skinny_swap<16, 4>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       else launch_skinny_swap<32, 4>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       return;
@@ -1316,29 +1284,18 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     // persistent CTA pair per cluster splits every tile's K in two, so the
     // busiest SM streams 1.5 tiles of weights instead of 2.
     const int pairs = num_sms() / 2;
-    const bool pair_split = !old && getenv("ESP_GEMM_NO_PAIR_SPLIT") == nullptr &&
-                            getenv("ESP_GEMM_NO_STREAMK") == nullptr &&
-                            getenv("ESP_GEMM_STREAMK_ALL") == nullptr && K / BK >= 32 &&
-                            2 * ((tiles + num_sms() - 1) / num_sms()) > (tiles + pairs - 1) / pairs;
-    if (pair_split) {
+    if (!forced && K / BK >= 32 &&
+        2 * ((tiles + num_sms() - 1) / num_sms()) > (tiles + pairs - 1) / pairs) {
       if (M <= 16) launch_skinny_swap<16, -2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       else launch_skinny_swap<32, -2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       return;
     }
-    if (!old && getenv("ESP_GEMM_SPLIT2_ALL") != nullptr) {  // study knob
-      if (M <= 16) launch_skinny_swap<16, 2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
-      else launch_skinny_swap<32, 2>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
-      return;
-    }
-    static const int sk_min_kb = [] {
-      const char* e = getenv("ESP_GEMM_SK_MIN_KB");
-      return e ? atoi(e) : 0;
-    }();
-    const bool streamk = 2 * tiles < num_sms() && K / BK >= sk_min_kb;
-    if (getenv("ESP_GEMM_NO_STREAMK") != nullptr ||
-        (getenv("ESP_GEMM_STREAMK_ALL") == nullptr && !streamk)) {
-      if (old) launch_gemm<128, true>(A, lda, B, ldb, M, N, K, 0, ep, s);
-      else if (M <= 16) launch_skinny_swap<16, 1>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
+    // Whole tiles (QKV: 96, LM head: 250), or stream-K over (tile, K block)
+    // when whole tiles would leave more than half the SMs idle; the CTA
+    // completing a tile applies the fused epilogue to its fp32 partial sums.
+    const bool streamk = paths.streamk_all || (!paths.no_streamk && 2 * tiles < num_sms());
+    if (!streamk) {
+      if (M <= 16) launch_skinny_swap<16, 1>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       else launch_skinny_swap<32, 1>(A, lda, B, ldb, M, N, K, 0, ep, s, nullptr, nullptr);
       return;
     }
@@ -1346,12 +1303,11 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
     const int max_seg = (K / BK + per - 1) / per + 1;
     const StreamKWs w =
         streamk_workspace(static_cast<size_t>(tiles) * max_seg * M * 128, tiles, s);
-    if (old) launch_gemm<128, true>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
-    else if (M <= 16) launch_skinny_swap<16, 1>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
+    if (M <= 16) launch_skinny_swap<16, 1>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
     else launch_skinny_swap<32, 1>(A, lda, B, ldb, M, N, K, per, ep, s, w.sums, w.tile_kb);
     return;
   }
-  if (launch_gemm_pair(A, lda, B, ldb, M, N, K, ep, s)) return;
+  if (!paths.no_pair && launch_gemm_pair(A, lda, B, ldb, M, N, K, ep, s)) return;
   const bool n256 = N % 256 == 0;
   const int tiles256 = ((M + BM - 1) / BM) * (N / 256);
   // Prefer the wide tile unless it would leave SMs idle.

@@ -67,10 +67,16 @@ struct GemmEpilogue {
   float norm_eps = 0.f;
 };
 
+// Schedule selection: kGemmAuto is the production dispatch; the others
+// force one path on shapes that would not pick it (kernel tests, via the
+// esp_k_gemm hook): the 1-CTA prefill kernel instead of the CTA pair, whole
+// skinny tiles only, or skinny stream-K for every shape.
+enum GemmPath : int { kGemmAuto = 0, kGemmNoPair = 1, kGemmTilesOnly = 2, kGemmStreamKAll = 3 };
+
 // D[M x N] = A[M x K] . B[N x K]^T with the epilogue above. A and B are
 // row-major bf16 (both K-major). N % 128 == 0, K % 64 == 0, any M.
 void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
-          const GemmEpilogue& ep, cudaStream_t s);
+          const GemmEpilogue& ep, cudaStream_t s, int path = kGemmAuto);
 
 // ---- attention ------------------------------------------------------------
 constexpr int kMaxRounds = 8;
@@ -88,50 +94,24 @@ struct RingSegment {
   int32_t shift[kMaxRounds];
 };
 
-// Attention over segments; q/out are [q_rows x heads*head_dim] and k/v
-// [kv_rows x heads*head_dim] bf16 (segments index rows of each).
-// Persistent tcgen05 kernel; work = (segment, 128-row q tile, head).
+// K1: striped ring attention over segments; q/out are [q_rows x
+// heads*head_dim] and k/v [kv_rows x heads*head_dim] bf16 (segments index
+// rows of each). Persistent tcgen05 kernel, two 128-row query tiles per CTA
+// (P kept in TMEM); work items are (segment, query-tile PAIR, head) in the
+// order build_attention_work lays them out.
 void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
-                    int kv_rows, int heads, int head_dim, const RingSegment* d_segs, int n_segs,
+                    int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
                     const int32_t* d_work, int n_work, float scale, cudaStream_t s);
 
-// v2: two 128-row query tiles per CTA (P kept in TMEM); work items are
-// (segment, query-tile PAIR, head). Same semantics as ring_attention.
-void ring_attention_pairs(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
-                          int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
-                          const int32_t* d_work, int n_work, float scale, cudaStream_t s);
-
-// Instrumented v2 (clock64 accounting): prof holds grid x 4 roles x 8 u64
-// (producer: q_empty,k_empty,v_empty waits; MMA: q_full,k_full,v_full,
-// p_full[0],p_full[1],o_free waits; softmax t: s_full wait, step, S readback,
-// rescale o_done wait, rescales, steps, final wait; slot 7 = role total).
-// v4: one 128-row query tile per CTA, Q and a double-buffered S in TMEM
-// (ring_attention_v4.cu). Work items (segment, q tile, head), as for v1.
-void ring_attention_single(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
-                           int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
-                           const int32_t* d_work, int n_work, float scale, cudaStream_t s);
-
-// K1 variant selection: 2 = query-tile pairs (default), 1 = v1, 4 = one
-// tile with Q and a double-buffered S in TMEM. ESP_ATTN=1|2|4 (ESP_ATTN_V1
-// is kept as an alias of ESP_ATTN=1).
-inline int attention_variant() {
-  if (const char* e = std::getenv("ESP_ATTN")) {
-    const int v = std::atoi(e);
-    if (v == 1 || v == 2 || v == 4) return v;
-  }
-  return std::getenv("ESP_ATTN_V1") != nullptr ? 1 : 2;
-}
-// Work items of the variant are query-tile pairs (v2) or single tiles.
-inline bool attention_pairs(int variant) { return variant == 2; }
-void ring_attention_variant(int variant, const bf16* q, const bf16* k, const bf16* v, bf16* out,
-                            int q_rows, int kv_rows, int heads, int head_dim,
-                            const RingSegment* d_segs, int n_segs, const int32_t* d_work,
-                            int n_work, float scale, cudaStream_t s);
-
-void ring_attention_pairs_profiled(const bf16* q, const bf16* k, const bf16* v, bf16* out,
-                                   int q_rows, int kv_rows, int heads, int head_dim,
-                                   const RingSegment* d_segs, const int32_t* d_work, int n_work,
-                                   float scale, cudaStream_t s, uint64_t* prof);
+#ifdef ESP_STUDY
+// Kernel-study build only (tools/attn_prof.py, `make STUDY=1`): K1 with
+// clock64 accounting per role (producer, MMA, 2 softmax warp groups) x 8
+// counters into prof[grid x 4 x 8].
+void ring_attention_profiled(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
+                             int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
+                             const int32_t* d_work, int n_work, float scale, cudaStream_t s,
+                             uint64_t* prof);
+#endif
 
 // Work-list builder helper: number of 128-row q tiles of a segment.
 inline int q_tiles(int q_len) { return (q_len + 127) / 128; }
@@ -160,15 +140,12 @@ struct DecodeSlabs {
   const bf16* v[kMaxSlabs];
 };
 // Split-KV paged attention: partial (o, m, l) per (chunk, head) into
-// part_o [n_chunks x heads x head_dim] fp32 and part_ml [n_chunks x heads x 2].
-// With row_start != null the LSE combine is fused: the last CTA of each
-// (row, head) merges the row's partials into out (rows x heads*head_dim bf16);
-// counters = rows x heads ints, zero on entry and left zero.
+// part_o [n_chunks x heads x head_dim] fp32 and part_ml [n_chunks x heads x 2]
+// (or, with dst, into the master domains' buffers by peer stores).
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
                       float* part_o, float* part_ml, cudaStream_t s,
-                      const int32_t* row_start = nullptr, int* counters = nullptr,
-                      bf16* out = nullptr, int rows = 0, const PartDst* dst = nullptr);
+                      const PartDst* dst = nullptr);
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);

@@ -71,9 +71,6 @@ def test_gemm_skinny_epilogues(M, epi, mode, monkeypatch):
     epilogue), whole tiles, and the production dispatch ("auto": the 172-tile
     gate_up shape runs as persistent CTA pairs splitting each tile's K, the
     partner's partial added over DSMEM); store, residual, fp32, SiLU(gate)*up."""
-    if mode != "auto":
-        monkeypatch.setenv("ESP_GEMM_STREAMK_ALL" if mode == "streamk" else "ESP_GEMM_NO_STREAMK",
-                           "1")
     torch.manual_seed(M * 10 + epi)
     N, K = 22016 if epi == 3 else 12288, 4096
     a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
@@ -83,7 +80,7 @@ def test_gemm_skinny_epilogues(M, epi, mode, monkeypatch):
     for _ in range(2):  # second call checks the tile counters were reset
         d = r.clone() if epi == 1 else torch.empty(
             M, ncols, device="cuda", dtype=torch.float32 if epi == 2 else torch.bfloat16)
-        abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi)
+        abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi, path=mode)
     torch.cuda.synchronize()
     ref = a.float() @ b.float().t()
     if epi == 1:
@@ -124,14 +121,11 @@ def test_gemm_cta_pair_matches_single_cta(M, N, K, epi, monkeypatch):
     ncols = N // 2 if epi == 3 else N
     r = torch.randn(M, ncols, device="cuda", dtype=torch.bfloat16)
     outs = []
-    for no_pair in (False, True):
-        if no_pair:
-            monkeypatch.setenv("ESP_GEMM_NO_PAIR", "1")
+    for path in ("auto", "no_pair"):
         d = r.clone() if epi == 1 else torch.empty(M, ncols, device="cuda", dtype=odt)
-        abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi)
+        abi.k_gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi, path=path)
         torch.cuda.synchronize()
         outs.append(d)
-    monkeypatch.delenv("ESP_GEMM_NO_PAIR")
     assert torch.equal(outs[0], outs[1])
     ref = a.float() @ b.float().t()
     if epi == 1:
@@ -164,21 +158,12 @@ def _ref_striped(q, ks, vs, pos_i, d, origins, heads, hd):
     return torch.einsum("hqk,khd->qhd", p, V).reshape(L, heads * hd)
 
 
-@pytest.fixture(params=["v2", "v1", "v4"])
-def attn_variant(request, monkeypatch):
-    """K1 variants (ESP_ATTN): v2 (two query tiles / CTA, P in TMEM), v1, v4
-    (one tile / CTA, Q and a double-buffered S in TMEM)."""
-    monkeypatch.delenv("ESP_ATTN_V1", raising=False)
-    monkeypatch.setenv("ESP_ATTN", request.param[1:])
-    return request.param
-
-
 @pytest.mark.parametrize("S,d,pos_i,heads,hd", [(128, 1, 0, 2, 128), (1000, 1, 0, 4, 128),
                                                 (4096, 1, 0, 8, 64), (2000, 2, 0, 4, 128),
                                                 (2001, 2, 1, 4, 128), (3000, 4, 2, 2, 64),
                                                 (5000, 8, 5, 2, 128), (700, 8, 0, 3, 128),
                                                 (77, 4, 3, 2, 64), (1500, 3, 2, 2, 128)])
-def test_ring_attention_striped(S, d, pos_i, heads, hd, attn_variant):
+def test_ring_attention_striped(S, d, pos_i, heads, hd):
     torch.manual_seed(S + d + pos_i)
     H = heads * hd
     lens = [len(range(o, S, d)) for o in range(d)]

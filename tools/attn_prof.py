@@ -1,8 +1,9 @@
 """Ring-attention kernel study at the LWM-7B 32K shape (one 32768-token
-stripe, 32 heads x 128): CUDA-event time of the production kernel over
-ESP_ATTN_REPEAT launches on staged buffers (printed by the hook as
-[attn-time]) with the SM clock sampled meanwhile, and, with ESP_ATTN_PROF=1,
-the per-role cycle accounting of the instrumented build."""
+stripe, 32 heads x 128): wall time of REPEAT calls of the K1 test hook (each
+stages its buffers, so this is an upper bound; bench.py times K1 in the step
+with CUDA events) with the SM clock sampled meanwhile, then — in a kernel-
+study build (`make -C paper_2404_09526_b200/csrc STUDY=1`) — the per-role
+cycle accounting of the instrumented kernel (ESP_ATTN_PROF=1)."""
 import os
 import statistics
 import sys
@@ -43,21 +44,19 @@ def main():
                              out.data_ptr(), heads, hd)
 
     os.environ.pop("ESP_ATTN_PROF", None)
-    os.environ.pop("ESP_ATTN_V1", None)
     run()
     torch.cuda.synchronize()
     n = int(os.environ.get("REPEAT", "10"))
-    os.environ["ESP_ATTN_REPEAT"] = str(n)
     clocks, stop = [], threading.Event()
     th = threading.Thread(target=sample_clocks, args=(stop, clocks))
     th.start()
     t0 = time.time()
-    run()
+    for _ in range(n):
+        run()
     torch.cuda.synchronize()
     wall = time.time() - t0
     stop.set()
     th.join()
-    os.environ.pop("ESP_ATTN_REPEAT")
     sys.stderr.flush()
     mhz = statistics.median(clocks) if clocks else float("nan")
     print(f"flop/launch {flop:.4e}; wall {wall:.2f}s for {n} launches; "

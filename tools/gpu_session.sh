@@ -24,26 +24,6 @@ for s in $STEPS; do
     benchq) run bench_quick 600 python bench.py --steps 2 --warmup 1 --skip-cpu ;;
     kbench) run kbench 300 python tools/kbench.py ;;
     aprof) run attn_prof 300 python tools/attn_prof.py ;;
-    skinny)
-      run skinny 300 python tools/skinny_probe.py
-      run ncu_skinny 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file gpurun_out/skinny_launches.csv python tools/skinny_probe.py ;;
-    al2)
-      for r in 1 2; do for m in 64 32 16; do
-        export ESP_ATTN_L2_MIB=$m; run bench_l2_${m}_$r 600 python bench.py --steps 2 --warmup 1 --skip-cpu --skip-decode --skip-esp-sweep --skip-config3 --skip-scale-down; unset ESP_ATTN_L2_MIB
-      done; done ;;
-    avar)
-      for r in 1 2; do for v in 2 4; do
-        export ESP_ATTN=$v; run attn_v${v}_$r 300 python tools/attn_prof.py; unset ESP_ATTN
-      done; done ;;
-    appong)
-      for r in 1 2; do for p in 0 1; do
-        export ESP_ATTN_PINGPONG=$p; run attn_pp${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_PINGPONG
-      done; done ;;
-    apoly)
-      for r in 1 2; do for p in 0 1 2 3 4; do
-        export ESP_ATTN_POLY=$p; run attn_poly${p}_$r 300 python tools/attn_prof.py; unset ESP_ATTN_POLY
-      done; done ;;
     ncu)
       run ncu_launches 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --skip-decode \
@@ -55,13 +35,6 @@ for s in $STEPS; do
         -k regex:gemm_bf16 -s 10 -c 1 -o gpurun_out/prof_gemm -f python bench.py --steps 1 \
         --warmup 0 --skip-decode --skip-esp-sweep --skip-cpu --skip-config3 --skip-scale-down
       ;;
-    dprobe)  # DPROBE_VARIANTS='"ESP_DECODE_V1=381" "ESP_DECODE_V1=48"' bash tools/gpu_session.sh dprobe
-      for r in 1 2; do
-        eval "set -- ${DPROBE_VARIANTS:-\"ESP_DECODE_ATTN=1\" \"ESP_DECODE_STAGES=2\"}"; for v in "$@"; do
-          echo "== $v" >> gpurun_out/dprobe.log
-          env $v timeout 300 python tools/decode_probe.py >> gpurun_out/dprobe.log 2>&1
-        done
-      done ;;
     ncu_decode)
       run ncu_decode 900 ncu --set full --clock-control none --import-source on \
         -k regex:decode_attention -s 40 -c 1 -o gpurun_out/prof_decode -f python bench.py \
