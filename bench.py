@@ -1,22 +1,30 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 ESP data path (BASELINE.json metric: prefill & decode
-tokens/s at ESP 1/2/4/8 on B200; % roofline; vs CPU reference).
+tokens/s at ESP 1/2/4/8 B200; % roofline; vs CPU reference).
 
-Workload (N=1): BASELINE config 2 — LWM-7B shape (Llama-2-7B arch, bf16,
+N = 1 (default): BASELINE config 2 — LWM-7B shape (Llama-2-7B arch, bf16,
 random init), single-request 32K-token ESP prefill at ESP degree 1 on one
-B200, with proactive retention of every token's K/V into its resting page
-slot. One step = one full prefill pass (32 layers + LM head + greedy token).
-Also reported in the same line: decode (config 4 scaled to one GPU: batch 16 x
-8K-token contexts, split-KV paged attention + LSE combine) and ESP degrees
-2/4/8 realised as co-located instances on the one GPU.
+B200, every token's K/V retained in its page slot. One step = one full
+prefill pass (32 layers + LM head + greedy token). The same line reports
+decode (config 4 scaled to one GPU: batch 16 x 8K contexts, split-KV paged
+attention + LSE combine; key "decode", last in the line), ESP degrees 2/4/8 as
+co-located instances, config 3 (128K, 8 -> 2 scale-down), the cross-domain
+transports and the CPU baselines (the dense oracle on the host cores).
+
+N > 1 (torchrun, one process per GPU): ESP degree N ACROSS the N GPUs — the
+reference's own config-2 plan (tests/golden/scenario_config2_32k_d<N>.jsonl:
+ring [0..N-1], every token retained on instance 0) executed by the
+single-process multi-device runtime (the reference engine drives all
+instances from one process, engine.hpp:45), launched by rank 0 as a child
+process over all N GPUs; plus N-way multi-master decode, an NVLink P2P copy
+peak, and — on all ranks — the NCCL send/recv ring of one layer's K/V blocks
+(the transport baseline). Total work is fixed (one request):
+scaling "strong". The other ranks wait on a gloo barrier (no GPU work) while
+the child runs. If the multi-GPU run fails, the line says so
+("esp_multi_gpu".error) and falls back to N independent single-GPU replicas
+(scaling "weak").
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-
-N > 1 (torchrun, one process per GPU): each rank runs the same single-GPU
-workload as an independent replica (this build does not shard one request
-across processes yet — DESIGN.md "multi-GPU"), so scaling is "weak" and value
-is the sum over ranks of per-rank throughput, computed from the max-over-ranks
-step time.
 """
 from __future__ import annotations
 
@@ -124,15 +132,17 @@ def dist_init():
         # CPU-only world-size-2 tests of this harness.
         use_nccl = (torch.cuda.is_available() and torch.cuda.device_count() >= world and
                     os.environ.get("ESP_BENCH_GLOO") is None)
+        import datetime
+        tmo = datetime.timedelta(minutes=60)  # rank 0's multi-GPU child may run for minutes
         if use_nccl:
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
             try:
-                dist.init_process_group("nccl")
+                dist.init_process_group("nccl", timeout=tmo)
             except Exception as e:  # report, then keep the run alive on gloo
                 print(f"nccl init failed ({str(e)[:120]}); using gloo", file=sys.stderr)
                 use_nccl = False
         if not use_nccl:
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=tmo)
         return rank, world, dist
     return rank, world, None
 
@@ -154,17 +164,20 @@ def barrier(dist):
 
 # ---- CPU baseline: the dense oracle on the host cores --------------------------
 
-def cpu_sample(default_tokens=512):
+CPU_S = 8192  # tokens of the CPU sample (both arms)
+
+
+def cpu_sample(S_CPU=None):
     """One bounded sample of the workload on the host: ONE of the 32 LWM-7B
-    layers prefilling S_CPU tokens (dense fp32 oracle, all host threads), then
-    FLOP-extrapolated to the full 32-layer, 32768-token prefill. The GPU arm's
-    cpu_baseline uses 2048 tokens (~10 s on 16 cores); each reference-arm step
-    512 (~1 s) so a K-step run stays within minutes."""
+    layers prefilling S_CPU = 8192 tokens (dense fp32 oracle, all host
+    threads; ~10-25 s), FLOP-extrapolated to the full 32-layer, 32768-token
+    prefill. Both arms use this same sample."""
     import numpy as np
 
     from oracle import llama_ref
     from paper_2404_09526_b200.abi import ModelShape
-    S_CPU = int(os.environ.get("ESP_BENCH_CPU_TOKENS", str(default_tokens)))
+    if S_CPU is None:
+        S_CPU = int(os.environ.get("ESP_BENCH_CPU_TOKENS", str(CPU_S)))
     shape = ModelShape(layers=1, hidden=H, heads=32, head_dim=128, ffn=F, vocab=V)
     prompt = np.random.default_rng(7).integers(0, V, S_CPU).astype(np.int32)
     threads = os.cpu_count() or 1
@@ -181,20 +194,75 @@ def cpu_sample(default_tokens=512):
                         f"32-layer 32768-token prefill"))
 
 
+def cpu_decode_sample(b=16, ctx=8192):
+    """CPU decode baseline: one fp32 decode step of b requests over ctx-token
+    caches through the oracle, timed at 1 and 2 LWM-7B layers (model setup
+    excluded) and extrapolated to 32 layers: t = fixed + 32 * per_layer."""
+    from oracle import llama_ref
+    from paper_2404_09526_b200.abi import ModelShape
+    threads = os.cpu_count() or 1
+    t = {}
+    for layers in (1, 2):
+        shape = ModelShape(layers=layers, hidden=H, heads=32, head_dim=128, ffn=F, vocab=V)
+        t[layers] = llama_ref.decode_sample_ms(shape, ctx, b, threads)
+    per_layer = max(t[2] - t[1], 1e-3)
+    total = (t[1] - per_layer) + L * per_layer
+    return dict(value=b / (total / 1e3), unit="tokens/s", cores=threads, kind="port",
+                ms_per_step=total,
+                sample=(f"dense fp32 oracle decode, batch {b} x {ctx}-token caches, 1 and 2 "
+                        f"LWM-7B layers ({t[1]:.0f} / {t[2]:.0f} ms), extrapolated to 32 layers"))
+
+
+def cpu_config1():
+    """BASELINE config 1 in full on the host (§4 of BASELINE.md): tiny model,
+    4096-token prompt + 64 greedy decode steps through the dense oracle."""
+    import numpy as np
+
+    from oracle import llama_ref
+    from paper_2404_09526_b200.abi import TINY
+    threads = os.cpu_count() or 1
+    prompt = np.random.default_rng(1).integers(0, V, 4096).astype(np.int32)
+    t0 = time.perf_counter()
+    llama_ref.generate(TINY, prompt, 64, emulate_bf16=False, want_logits=False, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "tokens": 4096 + 64, "cores": threads, "kind": "port",
+            "sample": "config 1 in full: tiny Llama (2 layers, d=512, 8 heads), 4096-token "
+                      "prefill + 64 decode steps, dense fp32 oracle"}
+
+
+def workload_config(args, n):
+    """The `config` both arms print (same workload, same keys)."""
+    if n == 1:
+        return {"workload": f"config2: LWM-7B shape (32L, H=4096, 32x128 heads, FFN 11008, "
+                            f"V=32000, random init) single-request {args.seq}-token ESP prefill, "
+                            f"ESP degree 1, proactive retention into page slots",
+                "seq_len": args.seq, "esp_degree": 1, "parallelism": "esp1",
+                "l2": "inputs larger than L2 (13.5 GB weights, 256 MB activations per pass)"}
+    return {"workload": f"config2: LWM-7B shape single-request {args.seq}-token ESP prefill at "
+                        f"ESP degree {n} across {n} GPUs (the reference's plan: ring "
+                        f"[0..{n - 1}], every token retained on instance 0)",
+            "seq_len": args.seq, "esp_degree": n, "parallelism": f"esp{n}",
+            "l2": "inputs larger than L2 (13.5 GB weights per GPU)"}
+
+
 def run_reference(args):
     rank, world, dist = dist_init()
     if rank != 0:
         return
+    n = max(world, args.gpus)
+    # warm-up steps: a small sample (thread pool, page faults); timed steps:
+    # the same 8192-token sample as the GPU arm's cpu_baseline
     for _ in range(args.warmup):
-        cpu_sample()
+        cpu_sample(512)
     vals = [cpu_sample() for _ in range(args.steps)]
     v = statistics.median([x["value"] for x in vals])
     cb = dict(vals[-1])
     cb["value"] = v
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": "config2: LWM-7B shape 32K-token prefill (CPU port, sampled)"},
+            "higher_is_better": True, "scaling": "weak" if n == 1 else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, n),
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -204,6 +272,18 @@ def run_reference(args):
 
 def run_gpu(args):
     rank, world, dist = dist_init()
+    n = max(world, args.gpus)
+    if n == 1:
+        line = single_gpu(args, rank, world, dist)
+    else:
+        line = multi_gpu(args, rank, world, dist, n)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def single_gpu(args, rank, world, dist, fallback_note=None):
+    """Config 2 at ESP degree 1 on this rank's GPU (world > 1: the replica
+    fallback, value summed over ranks from the max-over-ranks step time)."""
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import numpy as np
     import torch
@@ -256,16 +336,16 @@ def run_gpu(args):
     total_phase_ms = sum(v[0] for v in phases.values())
     shares = {p: round(v[0] / total_phase_ms, 4) for p, v in phases.items() if v[1] > 0}
 
+    config = workload_config(args, 1)
+    if world > 1:
+        config["parallelism"] = f"replicas x{world}"
+        config["workload"] += f" ({world} independent replicas: {fallback_note})"
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": f"config2: LWM-7B shape (32L, H=4096, 32x128 heads, FFN 11008, "
-                               f"V=32000, random init) single-request {S}-token ESP prefill, ESP "
-                               f"degree 1 per GPU, proactive retention into page slots",
-                   "seq_len": S, "esp_degree": 1, "parallelism": f"replicas x{world}",
-                   "l2": "inputs larger than L2 (13.5 GB weights, 256 MB activations per pass)"},
+        "config": config,
         "roofline": {"bound": "tensor", "kernel": "ring_attention_tcgen05",
                      "achieved": att_achieved, "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": att_achieved / tf_sust,
@@ -285,8 +365,14 @@ def run_gpu(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if rank == 0 and not args.skip_decode:
-        line["decode"] = bench_decode(rt, abi, args, np, hbm)
+    if world > 1:
+        rt.close()
+        return line if rank == 0 else None
+    decode = None
+    if not args.skip_decode:
+        decode = bench_decode(rt, abi, args, np, hbm)
+        line["decode_detail"] = {k: v for k, v in decode.items()
+                                 if k not in ("value", "unit", "ms_per_step", "e2e", "roofline")}
     if rank == 0 and not args.skip_esp_sweep:
         line["esp_degrees"] = bench_esp_sweep(abi, args, np, tf_sust)
     if rank == 0 and not args.skip_decode and not args.skip_esp_sweep:
@@ -299,14 +385,34 @@ def run_gpu(args):
         line["scale_down"] = bench_scale_down(abi, args, np)
         line["transport"] = bench_transport(abi, args, np)
     rt.close()
-    if rank == 0 and not args.skip_cpu:
+    if not args.skip_cpu:
         try:
-            line["cpu_baseline"] = cpu_sample(2048)
+            line["cpu_baseline"] = cpu_sample()
         except Exception as e:  # report, never hide
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        extra = {}
+        for key, fn in (("decode", cpu_decode_sample), ("config1", cpu_config1)):
+            try:
+                extra[key] = fn()
+            except Exception as e:  # report, never hide
+                extra[key] = {"error": str(e)[:200]}
+        line["cpu_baselines_more"] = extra
         line["control_plane"] = control_plane()
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    if not args.skip_decode:
+        try:
+            line["config1_gpu"] = bench_config1(abi, np)
+        except Exception as e:  # report, never hide
+            line["config1_gpu"] = {"error": str(e)[:200]}
+    if decode is not None:
+        # the decode phase of the metric, last in the line: value, roofline
+        # and e2e through the C-ABI (BASELINE: "prefill & decode tokens/s")
+        line["decode"] = {k: decode[k] for k in ("value", "unit", "ms_per_step", "roofline", "e2e")}
+        line["decode"]["config"] = decode["config"]
+        cpu_dec = line.get("cpu_baselines_more", {}).get("decode", {})
+        if cpu_dec.get("value"):
+            line["decode"]["cpu_baseline"] = {"value": cpu_dec["value"], "unit": "tokens/s",
+                                              "cores": cpu_dec["cores"], "kind": "port"}
+    return line
 
 
 def control_plane():
@@ -376,6 +482,30 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
                          "algorithmic": f"K+V bytes of one layer = 2*H*2*sum(ctx) = {kv_bytes / L:.4e} B per launch"},
             "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
             "phase_ms": {p: round(v[0] / max(len(ms), 1), 4) for p, v in ph.items() if v[1] > 0}}
+
+
+def bench_config1(abi, np):
+    """BASELINE config 1 in full on the GPU (the CPU oracle runs the same in
+    cpu_baselines_more.config1): tiny model, 4096-token prompt prefilled as
+    a 2-instance ring with scale-down onto instance 0, then 64 greedy decode
+    steps; device time of the whole request and host wall through the C-ABI."""
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    prompt = np.random.default_rng(1).integers(0, V, 4096).astype(np.int32)
+    res = None
+    for it in range(2):  # warm-up, then timed
+        rt = abi.Runtime(abi.TINY, 2, devices=[dev, dev], kv_capacity=200000)
+        t0 = time.perf_counter()
+        _, _, pre_ms = rt.prefill([0], [4096], [0, 1], [[(0, 4096)]], tokens=prompt)
+        dec_ms = 0.0
+        for _ in range(64):
+            dec_ms += rt.decode_step([0], [0], [0])[2]
+        wall = time.perf_counter() - t0
+        rt.close()
+        res = {"seconds_wall": wall, "prefill_ms": pre_ms, "decode_ms_64_steps": dec_ms,
+               "tokens": 4096 + 64,
+               "config": "config 1: tiny Llama, 4096-token ESP prefill over 2 instances "
+                         "(scale-down 2->1) + 64 decode steps, one GPU"}
+    return res
 
 
 def bench_chunked(abi, args, np):
@@ -470,15 +600,16 @@ def bench_config3(abi, args, np, tf_sust):
     prompt = np.random.default_rng(3).integers(0, V, S).astype(np.int32)
     retain = [[(0, 65600), (1, 65472)]]
     ms = []
-    for k in range(2):  # one warm-up, one timed
+    for k in range(4):  # one warm-up, three timed
         _, _, t = rt.prefill([k], [S], list(range(8)), retain, tokens=prompt)
         placement = rt.placement(k)
         rt.free_request(k)
         if k > 0:
             ms.append(t)
     rt.close()
-    step = ms[0]
+    step = statistics.median(ms)
     return {"tokens_per_s": S / (step / 1e3), "ms_per_step": step,
+            "ms_samples": [round(x, 2) for x in ms],
             "tflops": prefill_flops(S) / (step / 1e3) / 1e12,
             "frac": prefill_flops(S) / (step / 1e3) / 1e12 / tf_sust,
             "placement_after_prefill": placement,
@@ -661,6 +792,270 @@ def bench_esp_sweep(abi, args, np, tf_sust):
     return out
 
 
+# ---- N > 1: ESP across GPUs ---------------------------------------------------------
+
+def multi_gpu(args, rank, world, dist, n):
+    """ESP degree n across n GPUs (see the module docstring)."""
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    nccl = None
+    if dist is not None and dist.get_backend() == "nccl":
+        try:
+            nccl = nccl_ring_baseline(args, rank, world, dist)
+        except Exception as e:  # report, never hide
+            nccl = {"error": str(e)[:300]}
+    import datetime
+    cpu_group = (dist.new_group(backend="gloo", timeout=datetime.timedelta(minutes=60))
+                 if dist is not None else None)
+    res = None
+    if rank == 0:
+        res = run_child(args, n)
+    if dist is not None:
+        box = [res]
+        dist.broadcast_object_list(box, src=0, group=cpu_group)  # CPU-side wait
+        res = box[0]
+    if res is None or "error" in res:
+        note = f"ESP across {n} GPUs failed: {(res or {}).get('error', 'no result')[:200]}"
+        line = single_gpu(args, rank, world, dist, fallback_note=note)
+        if line is not None:
+            line["esp_multi_gpu"] = {"error": note}
+            if nccl is not None:
+                line["nccl_ring_baseline"] = nccl
+        return line
+    if rank != 0:
+        return None
+    pre = res["prefill"]
+    line = {
+        "metric": METRIC, "value": pre["tokens_per_s"], "unit": "tokens/s", "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": pre["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic", "config": workload_config(args, n),
+        "roofline": pre["roofline"],
+        "e2e": pre["e2e"], "gpu_launches": pre["gpu_launches"], "clocks": res["clocks"],
+        "transport": {k: res[k] for k in ("nvlink_p2p", "ring") if k in res},
+        "nccl_ring_baseline": nccl,
+        "decode": res.get("decode"),
+    }
+    return line
+
+
+def nccl_ring_baseline(args, rank, world, dist, device="cuda"):
+    """The transport baseline: one layer's K/V stripe blocks
+    (S/world rows x H, bf16, K and V) travel the ring for world-1 rounds with
+    send/recv grouped per round (batch_isend_irecv = ncclGroupStart/End on
+    NCCL), in the reference's round order (esp_mechanics.cpp:59-68): in round
+    r rank i forwards the block that started at rank (i - r) mod world to
+    i + 1. Timed with CUDA events on the current stream (wall clock on a CPU
+    gloo group), max over ranks. Also checks that every rank ends holding the
+    block of origin (i + 1) mod world."""
+    import torch
+
+    rows = max(1, args.seq // world)
+    cols = H if device == "cuda" else 64
+    dt = torch.bfloat16 if device == "cuda" else torch.float32
+    blk = torch.full((2, rows, cols), float(rank), device=device, dtype=dt)
+    nxt = torch.empty_like(blk)
+    send_to, recv_from = (rank + 1) % world, (rank - 1) % world
+
+    def ring():
+        cur, other = blk, nxt
+        for _ in range(world - 1):
+            ops = [dist.P2POp(dist.isend, cur, send_to), dist.P2POp(dist.irecv, other, recv_from)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            cur, other = other, cur
+        return cur
+
+    last = ring()
+    got = float(last[0, 0, 0].item())
+    if got != float((rank + 1) % world):
+        raise RuntimeError(f"ring delivered origin {got}, expected {(rank + 1) % world}")
+    for _ in range(2):
+        ring()
+    reps = 10
+    if device == "cuda":
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            ring()
+        e1.record()
+        torch.cuda.synchronize()
+        local_ms = e0.elapsed_time(e1) / reps
+    else:
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            ring()
+        local_ms = (time.perf_counter() - t0) * 1e3 / reps
+    ms = reduce_max(local_ms, dist)
+    sent = (world - 1) * blk.numel() * blk.element_size()  # bytes each rank sends per layer
+    return {"ms_per_layer": ms, "bytes_sent_per_gpu_per_layer": sent,
+            "gbs_per_gpu": sent / (ms / 1e3) / 1e9,
+            "ms_for_32_layers": 32 * ms,
+            "config": f"{world} ranks, {rows} rows x {cols} x (K,V) per block, "
+                      f"{world - 1} rounds of grouped send/recv"}
+
+
+def run_child(args, n):
+    """Rank 0: the multi-device runtime over GPUs 0..n-1 in a child process
+    (a device fault there cannot take the harness down)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--esp-child", "--gpus", str(n),
+           "--steps", str(args.steps), "--warmup", str(args.warmup), "--seq", str(args.seq),
+           "--devices", args.devices or ",".join(str(i) for i in range(n))]
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK",
+              "ROLE_RANK", "TORCHELASTIC_RUN_ID"):
+        env.pop(k, None)
+    try:
+        p = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=args.child_timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": f"child timed out after {args.child_timeout} s"}
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    if p.returncode != 0 or not lines:
+        return {"error": f"child rc={p.returncode}: {(p.stderr or p.stdout)[-400:]}"}
+    return json.loads(lines[-1])
+
+
+def esp_child(args):
+    """ESP degree n across GPUs (--devices: instance i on GPU devices[i]; on a
+    one-GPU box `--devices 0,0,0,0` with ESP_DOMAIN_PER_INSTANCE=1 runs the
+    same cross-domain code path). Prints one JSON object."""
+    import numpy as np
+    import torch
+
+    from paper_2404_09526_b200 import abi
+    devs = [int(x) for x in args.devices.split(",")]
+    n = len(devs)
+    hbm, tf_burst, tf_sust, _ = peaks()
+    S = args.seq
+    out = {}
+    # The reference's own plan for config 2 at this degree (ring [0..n-1],
+    # retention onto instance 0), from the recorded scenario when present.
+    retain = [[(0, S)]]
+    gold = os.path.join(ROOT, "tests", "golden", f"scenario_config2_32k_d{n}.jsonl")
+    if os.path.exists(gold) and S == 32768:
+        with open(gold) as f:
+            for l in f:
+                j = json.loads(l)
+                if j.get("kind") == "step" and j["decision"]["prefills"]:
+                    pl = j["decision"]["prefills"][0]["placement"]["0"]
+                    retain = [[tuple(x) for x in pl]]
+                    break
+    rt = abi.Runtime(abi.LWM_7B, n, devices=devs, kv_capacity=S + 64)
+    prompt = np.random.default_rng(7).integers(0, V, S).astype(np.int32)
+    for w in range(args.warmup):
+        rt.prefill([1000 + w], [S], list(range(n)), retain, tokens=prompt)
+        rt.free_request(1000 + w)
+    launches0 = abi.launch_count()
+    dev_ms, wall_ms = [], []
+    with ClockSampler(devs[0]) as clk:
+        for k in range(args.steps):
+            t0 = time.perf_counter()
+            _, _, ms = rt.prefill([k], [S], list(range(n)), retain, tokens=prompt)
+            wall_ms.append((time.perf_counter() - t0) * 1e3)
+            dev_ms.append(ms)
+            rt.free_request(k)
+    launches = abi.launch_count() - launches0
+    stats = rt.last_prefill_stats()
+    rt.phase_times()
+    rt.set_profiling(True)
+    rt.prefill([99], [S], list(range(n)), retain, tokens=prompt)
+    rt.set_profiling(False)
+    ph = rt.phase_times()
+    rt.free_request(99)
+    att_ms, att_n = ph["ring_attention"]
+    att_avg = att_ms / max(att_n, 1)
+    # each GPU's K1 launch covers its stripe: ~1/n of the layer's causal work
+    att_flop = attn_flops_per_layer(S) / n
+    att_tf = att_flop / (att_avg / 1e3) / 1e12
+    step = statistics.median(dev_ms)
+    wall = statistics.median(wall_ms)
+    out["prefill"] = {
+        "tokens_per_s": S / (step / 1e3), "ms_per_step": step, "ms_samples": dev_ms,
+        "e2e": {"value": S / (wall / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": S * 4,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": launches,
+        "step_tflops_per_gpu": prefill_flops(S) / (step / 1e3) / 1e12 / n,
+        "roofline": {"bound": "tensor", "kernel": "ring_attention_tcgen05 (per GPU)",
+                     "achieved": att_tf, "peak": tf_sust, "unit": "TFLOP/s",
+                     "frac": att_tf / tf_sust, "traffic": None,
+                     "algorithmic": f"2*H*S*(S+1)/n = {att_flop:.4e} FLOP per launch, avg "
+                                    f"launch {att_avg:.3f} ms"},
+        "retention": retain[0],
+    }
+    out["ring"] = {"ring_volume_tokens": stats["ring_volume_tokens"],
+                   "cross_gpu_tokens": stats["cross_domain_tokens"],
+                   "nvlink_bytes_per_prefill": stats["nvlink_bytes"],
+                   "nvlink_bytes_per_gpu_per_layer": stats["nvlink_bytes"] / max(n, 1) / L,
+                   "transient_buffer_tokens": stats["transient_buffer_tokens"],
+                   "extra_migration_tokens": stats["extra_migration_tokens"]}
+    rt.close()
+    out["clocks"] = clk.summary()
+    # N-way multi-master decode: b requests x ctx tokens spread over the n
+    # instances (GPUs), every instance a master of b/n requests.
+    try:
+        b, ctx = args.decode_batch, args.decode_ctx
+        share = ctx // n
+        rt = abi.Runtime(abi.LWM_7B, n, devices=devs,
+                         kv_capacity=b * share + b * (args.steps + args.warmup + 8))
+        rng = np.random.default_rng(17)
+        members = list(range(n))
+        for r in range(b):
+            rt.prefill([r], [share * n], members, [[(i, share) for i in members]],
+                       tokens=rng.integers(0, V, share * n).astype(np.int32))
+        dec = {}
+        for k_m in sorted({n, 1}):
+            masters = members[:k_m]
+            for _ in range(args.warmup):
+                rt.decode_step(members, masters, list(range(b)))
+            ms = [rt.decode_step(members, masters, list(range(b)))[2] for _ in range(args.steps)]
+            st = statistics.median(ms)
+            dec[f"masters_{k_m}"] = {"tokens_per_s": b / (st / 1e3), "ms_per_step": st}
+        rt.close()
+        dec["config"] = f"batch {b} x {share * n} tokens, KV {share}/request on each of {n} GPUs"
+        out["decode"] = dec
+    except Exception as e:  # report, never hide
+        out["decode"] = {"error": str(e)[:300]}
+    # NVLink peak: P2P copies GPU0 -> GPU1 (and both ways at once).
+    phys = sorted(set(devs))
+    if len(phys) >= 2:
+        a, bdev = phys[0], phys[1]
+        x = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{a}")
+        y = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{bdev}")
+        x2 = torch.empty_like(y)
+        y2 = torch.empty_like(x)
+        def timed(fn, dev):
+            with torch.cuda.device(dev):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                fn()
+                torch.cuda.synchronize(a)
+                torch.cuda.synchronize(bdev)
+                e0.record()
+                for _ in range(5):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize(a)
+                torch.cuda.synchronize(bdev)
+                return e0.elapsed_time(e1) / 5
+        uni = timed(lambda: y.copy_(x, non_blocking=True), a)
+        s_b = torch.cuda.Stream(device=bdev)
+        def both():
+            y.copy_(x, non_blocking=True)
+            with torch.cuda.stream(s_b):
+                y2.copy_(x2, non_blocking=True)
+        bi = timed(both, a)
+        out["nvlink_p2p"] = {"gpus": [a, bdev], "unidirectional_gbs": (1 << 30) / (uni / 1e3) / 1e9,
+                             "bidirectional_gbs": 2 * (1 << 30) / (bi / 1e3) / 1e9,
+                             "how": "torch copy_ of 1 GiB between GPUs (cudaMemcpyPeer over "
+                                    "NVLink/NVSwitch), 5 reps, CUDA events"}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -675,8 +1070,14 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-config3", action="store_true")
     ap.add_argument("--skip-scale-down", action="store_true")
+    ap.add_argument("--esp-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--devices", default="",
+                    help="N > 1: instance -> GPU list for the ESP run (default 0..N-1)")
+    ap.add_argument("--child-timeout", type=int, default=1800)
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.esp_child:
+        esp_child(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)

@@ -268,6 +268,30 @@ int esp_check_conservation(esp_runtime* rt);
 int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int32_t cap,
                        int32_t* n);
 
+/* The ring and scale-down the last esp_prefill executed, as the reference's
+ * mechanics account them (through the runtime's restatements of
+ * build_ring_schedule, esp_mechanics.cpp:45-70, and proactive_scale_down,
+ * :78-136):
+ *   ring_volume_tokens       RingSchedule::total_comm_volume = (d-1) * sum
+ *   cross_domain_tokens      the part of it whose hops cross co-location
+ *                            domains (GPUs): NVLink traffic, per K or V row
+ *                            and layer
+ *   nvlink_bytes             cross_domain_tokens * 2 (K, V) * hidden * 2 B
+ *                            * layers: the ring's NVLink bytes of the pass
+ *   transient_buffer_tokens  ceil(sum / d), the circulating stripe
+ *   extra_migration_tokens   0 whenever the resting instances are ring
+ *                            members (retention rides the ring), else -1
+ *   device_ms                device time of the pass (max over GPUs) */
+typedef struct esp_prefill_stats {
+  int64_t ring_volume_tokens;
+  int64_t cross_domain_tokens;
+  int64_t nvlink_bytes;
+  int64_t transient_buffer_tokens;
+  int64_t extra_migration_tokens;
+  double device_ms;
+} esp_prefill_stats;
+int esp_last_prefill_stats(const esp_runtime* rt, esp_prefill_stats* out);
+
 /* Parity readback of a request's KV cache, one layer: K (after RoPE) and V
  * rows in TOKEN order (position 0 first), wherever the page tables put them
  * (any instance, any slot), as bf16 [n x hidden] into host buffers k_out /
@@ -345,11 +369,14 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
 
 /* Split-KV paged decode attention + LSE combine over n_chunks chunks of
  * slots: request b's query q[b], chunk c reads slots slot_idx[c][0..n) from
- * slab (k_slab, v_slab rows of heads*head_dim bf16). */
+ * slab (k_slab, v_slab rows of heads*head_dim bf16). out: [batch x
+ * heads*head_dim] bf16, or fp32 with out_f32 = 1 (the fp32 check mode: the
+ * kernels accumulate and combine in fp32; only the output rounding differs). */
 int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_slab,
                            const void* const* v_slab, const int32_t* const* slot_idx,
                            const int32_t* n_slots, const int32_t* chunk_req, int32_t n_chunks,
-                           void* out, int32_t heads, int32_t head_dim, void* stream);
+                           void* out, int32_t heads, int32_t head_dim, int32_t out_f32,
+                           void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -208,6 +208,47 @@ static void attend(const float* q, int64_t nq, const int64_t* qpos, const float*
                    const float* V, int64_t H, int heads, int hd, int rb, float* out) {
   if (nq <= 0) return;
   const int64_t nk = qpos[nq - 1] + 1;
+  if (nq < ATT_RB) { /* decode-sized: keys read row by row, no transpose */
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t r = 0; r < nq; ++r) {
+      for (int h = 0; h < heads; ++h) {
+        const int64_t kr = qpos[r] + 1;
+        const float* qv = q + r * H + (int64_t)h * hd;
+        float* sc = (float*)malloc(sizeof(float) * kr);
+        const float scale = 1.0f / sqrtf((float)hd);
+        float mx = -3.0e38f;
+        for (int64_t j = 0; j < kr; ++j) {
+          const float* kv = K + j * H + (int64_t)h * hd;
+          float acc = 0.f;
+#pragma omp simd reduction(+ : acc)
+          for (int d = 0; d < hd; ++d) acc += qv[d] * kv[d];
+          sc[j] = acc * scale;
+          mx = sc[j] > mx ? sc[j] : mx;
+        }
+        double sum = 0;
+        for (int64_t j = 0; j < kr; ++j) {
+          sc[j] = expf(sc[j] - mx);
+          sum += sc[j];
+        }
+        float o[128];
+        for (int d = 0; d < hd; ++d) o[d] = 0.f;
+        for (int64_t j = 0; j < kr; ++j) {
+          const float p = sc[j];
+          const float* vv = V + j * H + (int64_t)h * hd;
+#pragma omp simd
+          for (int d = 0; d < hd; ++d) o[d] += p * vv[d];
+        }
+        float* dst = out + r * H + (int64_t)h * hd;
+        const double inv = 1.0 / sum;
+        for (int d = 0; d < hd; ++d) {
+          const float v = (float)(o[d] * inv);
+          dst[d] = rb ? bf16_round(v) : v;
+        }
+        free(sc);
+      }
+    }
+    return;
+  }
   const int64_t nkp = (nk + ATT_KC - 1) / ATT_KC * ATT_KC;
   float* KT = (float*)malloc(sizeof(float) * (size_t)heads * hd * nkp);
 #pragma omp parallel for collapse(2) schedule(static)
@@ -520,6 +561,37 @@ int32_t llama_ref_decode_cached(const llama_cfg* c, int64_t n_ctx, const uint16_
   free(lg);
   model_free(&m);
   return tok;
+}
+
+/* CPU decode baseline (bench.py cpu_baseline.decode): one decode step of a
+ * batch of `batch` requests, each over its own n_ctx-token cache (random bf16
+ * values; every request reads n_ctx x layers x 2 rows, as on the GPU), the
+ * model built once outside the timed region. Returns the wall ms of one
+ * step (all requests, all layers, LM head) or -1. */
+double llama_ref_decode_sample(const llama_cfg* c, int64_t n_ctx, int batch, int n_threads) {
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+  model m;
+  model_init(&m, c, n_ctx + 1, 0);
+  const int64_t H = c->hidden;
+  for (int l = 0; l < c->layers; ++l) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_ctx * H; ++i) {
+      const uint64_t h = splitmix64((uint64_t)i ^ ((uint64_t)l << 40));
+      m.kc[l][i] = bf16_round((float)(int32_t)(h & 0xFFFF) / 32768.0f - 1.0f);
+      m.vc[l][i] = bf16_round((float)(int32_t)((h >> 16) & 0xFFFF) / 32768.0f - 1.0f);
+    }
+  }
+  float* lg = (float*)malloc(sizeof(float) * c->vocab);
+  const double t0 = omp_get_wtime();
+  for (int b = 0; b < batch; ++b) {
+    m.len = n_ctx;
+    int32_t tok = (int32_t)(b * 7919 % c->vocab);
+    forward(&m, &tok, 1, lg, NULL);
+  }
+  const double ms = (omp_get_wtime() - t0) * 1e3;
+  free(lg);
+  model_free(&m);
+  return ms;
 }
 
 int llama_ref_max_threads(void) { return omp_get_max_threads(); }

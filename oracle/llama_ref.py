@@ -51,6 +51,9 @@ def lib():
         h.llama_ref_decode_cached.argtypes = [C.POINTER(LlamaCfg), C.c_int64,
                                               C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
                                               C.c_int32, C.c_int, f32p, f32p, f32p, f32p, C.c_int]
+        h.llama_ref_decode_sample.restype = C.c_double
+        h.llama_ref_decode_sample.argtypes = [C.POINTER(LlamaCfg), C.c_int64, C.c_int, C.c_int]
+        h.llama_ref_max_threads.restype = C.c_int
         _lib = h
     return _lib
 
@@ -131,3 +134,9 @@ def decode_cached(shape, k_cache, v_cache, token, emulate_bf16=True, threads=0):
                                         1 if emulate_bf16 else 0, _f32(lg), _f32(kn), _f32(vn),
                                         _f32(att), threads)
     return int(tok), lg, kn, vn, att
+
+
+def decode_sample_ms(shape, n_ctx, batch, threads=0) -> float:
+    """Wall ms of one fp32 decode step of `batch` requests over n_ctx-token
+    caches (llama_ref.c:llama_ref_decode_sample), model setup excluded."""
+    return float(lib().llama_ref_decode_sample(C.byref(cfg_from(shape)), n_ctx, batch, threads))

@@ -90,7 +90,7 @@ EXPORTED_SYMBOLS = [
     "esp_build_ring_schedule", "esp_proactive_scale_down", "esp_reactive_migrate",
     "esp_runtime_create", "esp_runtime_destroy", "esp_instance_info", "esp_prefill",
     "esp_decode_step", "esp_move_kv", "esp_free_request", "esp_query_placement",
-    "esp_check_conservation", "esp_request_tokens", "esp_read_kv", "esp_capture_attention",
+    "esp_check_conservation", "esp_request_tokens", "esp_last_prefill_stats", "esp_read_kv", "esp_capture_attention",
     "esp_captured_attention", "esp_slab_access", "esp_dump_profiles",
     "esp_decode_samples", "esp_fit_cost",
     "esp_launch_count", "esp_set_profiling", "esp_phase_times", "esp_k_gemm", "esp_k_ring_attention", "esp_k_decode_attention",
@@ -128,6 +128,14 @@ class PrefillArgs(C.Structure):
         ("first_token_out", C.POINTER(C.c_int32)),
         ("logits_out", C.POINTER(C.c_float)),
         ("device_ms_out", C.POINTER(C.c_double)),
+    ]
+
+
+class PrefillStats(C.Structure):
+    _fields_ = [
+        ("ring_volume_tokens", C.c_int64), ("cross_domain_tokens", C.c_int64),
+        ("nvlink_bytes", C.c_int64), ("transient_buffer_tokens", C.c_int64),
+        ("extra_migration_tokens", C.c_int64), ("device_ms", C.c_double),
     ]
 
 
@@ -189,6 +197,7 @@ def lib() -> C.CDLL:
         h.esp_request_tokens.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
                                          C.c_int32, C.POINTER(C.c_int32)]
         h.esp_dump_profiles.argtypes = [C.c_void_p, C.c_char_p]
+        h.esp_last_prefill_stats.argtypes = [C.c_void_p, C.POINTER(PrefillStats)]
         h.esp_read_kv.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                   C.c_int64, C.POINTER(C.c_int64)]
         h.esp_capture_attention.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64]
@@ -214,7 +223,7 @@ def lib() -> C.CDLL:
                                              C.POINTER(C.c_void_p),
                                              C.POINTER(C.c_void_p), C.POINTER(C.c_int32),
                                              C.POINTER(C.c_int32), C.c_int32, C.c_void_p,
-                                             C.c_int32, C.c_int32, C.c_void_p]
+                                             C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
         _lib_handle = h
     return _lib_handle
 
@@ -595,6 +604,13 @@ class Runtime:
                                        C.byref(n)))
         return [int(x) for x in out[:n.value]]
 
+    def last_prefill_stats(self) -> Dict[str, float]:
+        """Ring volume, cross-GPU share, NVLink bytes, transient buffer and extra
+        migration of the last prefill (esp_last_prefill_stats)."""
+        st = PrefillStats()
+        check(lib().esp_last_prefill_stats(self._h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in PrefillStats._fields_}
+
     def read_kv(self, request, layer):
         """(K, V) of one layer as uint16 (bf16 bits) [n_tokens, hidden], token order."""
         n = C.c_int64()
@@ -698,7 +714,7 @@ def k_ring_attention(q_ptr, q_len, pos_i, kv_k, kv_v, kv_len, origin, out_ptr, h
 
 
 def k_decode_attention(q_ptr, batch, k_slabs, v_slabs, slot_ptrs, n_slots, chunk_req,
-                       out_ptr, heads, head_dim, stream=0):
+                       out_ptr, heads, head_dim, stream=0, out_f32=False):
     n = len(k_slabs)
     ks = (C.c_void_p * n)(*k_slabs)
     vs = (C.c_void_p * n)(*v_slabs)
@@ -706,7 +722,7 @@ def k_decode_attention(q_ptr, batch, k_slabs, v_slabs, slot_ptrs, n_slots, chunk
     ns = (C.c_int32 * n)(*n_slots)
     cr = (C.c_int32 * n)(*chunk_req)
     check(lib().esp_k_decode_attention(q_ptr, batch, ks, vs, sp, ns, cr, n, out_ptr, heads,
-                                       head_dim, stream))
+                                       head_dim, 1 if out_f32 else 0, stream))
 
 
 def bf16_to_f32(u16: np.ndarray) -> np.ndarray:

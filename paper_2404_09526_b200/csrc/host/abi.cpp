@@ -315,6 +315,13 @@ int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int
   return guarded([&] { rt->impl->request_tokens(request, out, cap, n); });
 }
 
+int esp_last_prefill_stats(const esp_runtime* rt, esp_prefill_stats* out) {
+  return guarded([&] {
+    if (!rt || !out) throw esp::ConfigError("last_prefill_stats: null argument");
+    *out = rt->impl->last_prefill_stats();
+  });
+}
+
 int esp_read_kv(esp_runtime* rt, int64_t request, int32_t layer, void* k_out, void* v_out,
                 int64_t cap, int64_t* n) {
   return guarded([&] {
@@ -505,7 +512,8 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
 int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_slab,
                            const void* const* v_slab, const int32_t* const* slot_idx,
                            const int32_t* n_slots, const int32_t* chunk_req, int32_t n_chunks,
-                           void* out, int32_t heads, int32_t head_dim, void* stream) {
+                           void* out, int32_t heads, int32_t head_dim, int32_t out_f32,
+                           void* stream) {
   return guarded([&] {
     if (n_chunks > esp::k::kMaxSlabs) throw esp::ConfigError("too many chunks for the hook");
     if (!q || !k_slab || !v_slab || !slot_idx || !n_slots || !chunk_req || !out) {
@@ -545,9 +553,15 @@ int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_sl
                              static_cast<const esp::k::DecodeChunk*>(dch.p), n_parts, slabs,
                              heads, head_dim, scale, static_cast<float*>(po.p),
                              static_cast<float*>(pml.p), s);
-    esp::k::decode_combine(static_cast<float*>(po.p), static_cast<float*>(pml.p),
-                           static_cast<int32_t*>(drs.p), batch, heads, head_dim,
-                           static_cast<esp::k::bf16*>(out), s);
+    if (out_f32) {
+      esp::k::decode_combine_f32(static_cast<float*>(po.p), static_cast<float*>(pml.p),
+                                 static_cast<int32_t*>(drs.p), batch, heads, head_dim,
+                                 static_cast<float*>(out), s);
+    } else {
+      esp::k::decode_combine(static_cast<float*>(po.p), static_cast<float*>(pml.p),
+                             static_cast<int32_t*>(drs.p), batch, heads, head_dim,
+                             static_cast<esp::k::bf16*>(out), s);
+    }
     esp::cuda_ok(cudaGetLastError(), "decode_attention launch");
     esp::cuda_ok(cudaStreamSynchronize(s), "decode_attention hook");
   });

@@ -403,6 +403,47 @@ void Runtime::prefill(const esp_prefill_args& a) {
       throw CapacityError(i, "prefill placement overflows instance " + std::to_string(i));
     }
   }
+  // The ring the kernels walk and the scale-down its retention realises,
+  // through the planner's restatements of the reference mechanics
+  // (build_ring_schedule esp_mechanics.cpp:45-70, proactive_scale_down
+  // :78-136): ring volume, the part of it that crosses GPUs, and zero extra
+  // migration whenever the resting instances are ring members.
+  {
+    std::vector<Tokens> seg(static_cast<size_t>(d), 0);
+    for (int r = 0; r < n; ++r) {
+      for (int i = 0; i < d; ++i) {
+        seg[static_cast<size_t>(i)] += a.input_lens[r] > i ? (a.input_lens[r] - i + d - 1) / d : 0;
+      }
+    }
+    const RingSchedule rs = build_ring_schedule(ring, seg);
+    esp_prefill_stats st{};
+    st.ring_volume_tokens = rs.total_comm_volume();
+    for (const auto& round : rs.rounds) {
+      for (const RingTransfer& t : round) {
+        if (!devices_.empty() && inst(t.from).domain != inst(t.to).domain) st.cross_domain_tokens += t.volume;
+      }
+    }
+    st.nvlink_bytes = st.cross_domain_tokens * 2 * cfg_.hidden * 2 * cfg_.layers;
+    const std::set<InstanceId> ring_set(ring.begin(), ring.end());
+    FillOrder rest;
+    std::vector<InstanceId> targets;
+    bool inside = true;
+    for (const auto& [i, t] : need) {
+      if (t == 0) continue;
+      inside = inside && ring_set.count(i) > 0;
+      rest.emplace_back(i, t);
+      targets.push_back(i);
+    }
+    st.extra_migration_tokens = -1;
+    if (inside && !targets.empty()) {
+      std::map<InstanceId, Tokens> free;
+      for (InstanceId i : ring) free[i] = inst(i).capacity - inst(i).used;
+      const ScaleDownResult sd = proactive_scale_down(rs, ring, targets, rest, free);
+      st.extra_migration_tokens = sd.extra_migration_volume;
+      st.transient_buffer_tokens = sd.transient_buffer_tokens;
+    }
+    last_prefill_ = st;
+  }
   if (!devices_.empty() && !a.tokens) throw ConfigError("prefill: tokens required on a device runtime");
   // The ring kernel keeps all d rounds of a segment in one work item; a
   // placement-only runtime has no kernel and accepts any ring the reference
@@ -590,6 +631,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
   float ms = 0;
   cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
   if (a.device_ms_out) *a.device_ms_out = ms;
+  last_prefill_.device_ms = ms;
   for (int r = 0; r < n; ++r) {
     requests_[a.request_ids[r]].tokens.push_back(first[r]);
     if (a.first_token_out) a.first_token_out[r] = first[r];

@@ -104,6 +104,7 @@ class Runtime {
   void instance_info(InstanceId i, int64_t* cap, int64_t* used) const;
   void check_conservation();
   void request_tokens(RequestId r, int32_t* out, int32_t cap, int32_t* n) const;
+  const esp_prefill_stats& last_prefill_stats() const { return last_prefill_; }
   // Parity readback: the request's K/V rows of one layer in token order
   // (host bf16 [n x hidden]); *n = the request's KV token count.
   void read_kv(RequestId r, int layer, void* k_out, void* v_out, int64_t cap, int64_t* n);
@@ -213,6 +214,7 @@ class Runtime {
   void record_decode_profile(const std::vector<InstanceId>& members,
                              const std::vector<RequestId>& batch, int n_masters, double ms);
   bool profiling_ = false;
+  esp_prefill_stats last_prefill_{};
   // Attention capture of the next prefill (parity tests): positions, and per
   // co-location domain the local stripe rows holding them, the capture
   // index of each, and a device buffer [layers x rows x hidden] bf16.

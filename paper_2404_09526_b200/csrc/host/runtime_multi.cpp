@@ -504,6 +504,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     }
   }
   if (a.device_ms_out) *a.device_ms_out = ms_max;
+  last_prefill_.device_ms = ms_max;
   for (int r = 0; r < n; ++r) {
     requests_[a.request_ids[r]].tokens.push_back(first[r]);
     if (a.first_token_out) a.first_token_out[r] = first[r];

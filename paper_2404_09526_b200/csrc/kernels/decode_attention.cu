@@ -14,6 +14,7 @@
 // over all chunks of the request, on every instance that held its KV.
 #include <cfloat>
 #include <stdexcept>
+#include <type_traits>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -203,12 +204,14 @@ __global__ void __launch_bounds__(W * 32, MINB)
   }
 }
 
+// OutT = bf16 (the data path) or float (the fp32 check mode of the hook).
+template <typename OutT>
 __global__ void decode_combine_kernel(const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml,
                                       const int32_t* __restrict__ row_start,
                                       const int32_t* __restrict__ chunk_ids,
                                       const int32_t* __restrict__ rows, int heads, int hd,
-                                      bf16* __restrict__ out) {
+                                      OutT* __restrict__ out) {
   ptx::griddep_wait();
   ptx::griddep_launch();
   const int orow = blockIdx.x, head = blockIdx.y;
@@ -262,8 +265,12 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
       const float wc = c < kMaxC ? sw[c] : (mc == -INFINITY ? 0.f : exp2f(mc - mm));
       acc += wc * part_o[p * hd + d];
     }
-    out[static_cast<int64_t>(orow) * heads * hd + head * hd + d] =
-        __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
+    const float r = ll > 0.f ? acc / ll : 0.f;
+    if constexpr (std::is_same_v<OutT, float>) {
+      out[static_cast<int64_t>(orow) * heads * hd + head * hd + d] = r;
+    } else {
+      out[static_cast<int64_t>(orow) * heads * hd + head * hd + d] = __float2bfloat16_rn(r);
+    }
   }
 }
 
@@ -354,9 +361,17 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s) {
   if (rows <= 0) return;
-  launch_pdl(8, decode_combine_kernel, dim3(rows, heads), dim3(head_dim), 0, s, part_o, part_ml,
-             row_start, static_cast<const int32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
-             heads, head_dim, out);
+  launch_pdl(8, decode_combine_kernel<bf16>, dim3(rows, heads), dim3(head_dim), 0, s, part_o,
+             part_ml, row_start, static_cast<const int32_t*>(nullptr),
+             static_cast<const int32_t*>(nullptr), heads, head_dim, out);
+  count_launch();
+}
+
+void decode_combine_f32(const float* part_o, const float* part_ml, const int32_t* row_start,
+                        int rows, int heads, int head_dim, float* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  decode_combine_kernel<float><<<dim3(rows, heads), dim3(head_dim), 0, s>>>(
+      part_o, part_ml, row_start, nullptr, nullptr, heads, head_dim, out);
   count_launch();
 }
 
@@ -364,7 +379,7 @@ void decode_combine_rows(const float* part_o, const float* part_ml, const int32_
                          const int32_t* chunk_ids, const int32_t* rows, int n, int heads,
                          int head_dim, bf16* out, cudaStream_t s) {
   if (n <= 0) return;
-  launch_pdl(8, decode_combine_kernel, dim3(n, heads), dim3(head_dim), 0, s, part_o, part_ml, row_start,
+  launch_pdl(8, decode_combine_kernel<bf16>, dim3(n, heads), dim3(head_dim), 0, s, part_o, part_ml, row_start,
                                                             chunk_ids, rows, heads, head_dim, out);
   count_launch();
 }

@@ -149,6 +149,9 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);
+// The same with fp32 output (the fp32 check mode of the decode-attention hook).
+void decode_combine_f32(const float* part_o, const float* part_ml, const int32_t* row_start,
+                        int rows, int heads, int head_dim, float* out, cudaStream_t s);
 // Same, for a subset of rows: out row i combines global row rows[i], whose
 // partials are chunk_ids[row_start[g] .. row_start[g+1]).
 void decode_combine_rows(const float* part_o, const float* part_ml, const int32_t* row_start,

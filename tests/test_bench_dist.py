@@ -59,3 +59,30 @@ def test_reference_arm_under_torchrun_prints_once():
     assert j["impl"] == "reference" and j["n_gpus"] == 2
     assert j["cpu_baseline"]["kind"] == "port" and j["value"] > 0
     assert j["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _ring_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), ESP_BENCH_GLOO="1")
+    import argparse
+
+    import bench
+    r, w, d = bench.dist_init()
+    res = bench.nccl_ring_baseline(argparse.Namespace(seq=64), r, w, d, device="cpu")
+    out[rank] = res
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_baseline_round_order_gloo(world):
+    """The send/recv ring baseline (bench.nccl_ring_baseline) on CPU/gloo:
+    world-1 rounds of grouped send/recv deliver each rank the block of origin
+    rank+1 (the ring's last round, esp_mechanics.cpp:59-68); the time is the
+    max over ranks (same value on every rank)."""
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_ring_worker, args=(world, port, out), nprocs=world, join=True)
+        assert len(out) == world
+        assert len({round(out[r]["ms_per_layer"], 9) for r in range(world)}) == 1
+        assert out[0]["bytes_sent_per_gpu_per_layer"] == (world - 1) * 2 * (64 // world) * 64 * 4

@@ -24,12 +24,25 @@ with the GPU's own other modes:
     oracle teacher-forced on the device's own KV cache (read back in token
     order): logits, greedy token, the appended K/V rows.
 
-Tolerance (written here): rel-L2 = ||gpu - ref||_2 / ||ref||_2
-<= 1e-2 for logits, attention outputs and K/V rows; greedy tokens equal
-unless the reference's top-1 leads the chosen token by < 2e-2 (a bf16
-near-tie). Both sides round to bf16 at the same points; the remaining
-difference is summation order (fp32 accumulation in different orders) and
-P rounded to bf16 before P.V on the tensor cores (the oracle keeps P fp32).
+Tolerance (written here). Both sides compute in bf16 with fp32
+accumulation and round at the same points, in different orders; what bf16
+arithmetic itself can reach is measured, not assumed: the oracle runs the same
+input a second time in fp32 (no rounding), and floor = rel-L2(oracle-bf16,
+oracle-fp32) is the bf16 noise of the computation (at 2 LWM-7B layers, 32K:
+~1.2e-2 on logits and layer-1 quantities, ~3e-3 on layer-0 ones — random-init
+residual streams are dominated by the MLP, whose bf16 rounding noise the next
+layer amplifies). With rel-L2 = ||a - b||_2 / ||b||_2:
+  * vs the fp32 oracle:  rel-L2(gpu, oracle-fp32) <= 1.5 * floor + 1e-3
+    (the device is as close to exact arithmetic as bf16 allows);
+  * vs the bf16 oracle:  rel-L2(gpu, oracle-bf16) <= max(1e-2, 2 * floor)
+    (two independent bf16 roundings differ by up to ~sqrt(2) * floor);
+  * greedy tokens equal unless the fp32 oracle's top-1 leads the chosen
+    token by < 2e-2 (a bf16 near-tie).
+The fp32 check mode of the kernels (bf16 operands, fp32 accumulation AND
+fp32 output: K5 GEMM epilogue 2, K3+K4 with out_f32) is held to 1e-5 against
+fp64 (tests at the end of this file); K1 rounds P to bf16 before the
+tensor-core P.V, so its bound against fp64 is 5e-3 (2^-8 per probability,
+averaged over the keys).
 """
 import os
 
@@ -56,6 +69,15 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
 
 
+def check_close(name, gpu, ref16, ref32, report):
+    """The stated tolerance (module docstring) for one quantity."""
+    floor = rel_l2(ref16, ref32)
+    e16, e32 = rel_l2(gpu, ref16), rel_l2(gpu, ref32)
+    report.append(f"{name}: vs bf16 {e16:.2e}, vs fp32 {e32:.2e}, floor {floor:.2e}")
+    assert e32 <= 1.5 * floor + 1e-3, (name, e32, floor)
+    assert e16 <= max(REL_TOL, 2.0 * floor), (name, e16, floor)
+
+
 def check_token(tok, ref_tok, ref_lg):
     gap = float(ref_lg.max() - ref_lg[tok])
     assert tok == ref_tok or gap < TIE_GAP, (tok, ref_tok, gap)
@@ -68,10 +90,13 @@ def config2_oracle():
     attn_pos = np.unique(np.concatenate([[0, 1, 2, S2 - 2, S2 - 1],
                                          rng.choice(S2, 187, replace=False)]))
     kv_pos = np.unique(np.concatenate([[0, S2 - 1], rng.choice(S2, 254, replace=False)]))
-    tok, lg, att, kk, vv = llama_ref.prefill_probe(LWM7B_2L, prompt, attn_pos=attn_pos,
-                                                   kv_pos=kv_pos, last_only=True)
-    return dict(prompt=prompt, attn_pos=attn_pos, kv_pos=kv_pos, tok=tok, lg=lg, att=att,
-                k=kk, v=vv)
+    out = dict(prompt=prompt, attn_pos=attn_pos, kv_pos=kv_pos)
+    for mode, emu in (("bf16", True), ("fp32", False)):
+        tok, lg, att, kk, vv = llama_ref.prefill_probe(LWM7B_2L, prompt, attn_pos=attn_pos,
+                                                       kv_pos=kv_pos, last_only=True,
+                                                       emulate_bf16=emu)
+        out[mode] = dict(tok=tok, lg=lg, att=att, k=kk, v=vv)
+    return out
 
 
 @pytest.mark.parametrize("mode", ["d1", "d8_colocated", "d4_domains"])
@@ -96,25 +121,23 @@ def test_config2_32k_prefill_vs_oracle(config2_oracle, mode, monkeypatch):
                               want_logits=True)
     assert rt.placement(3) == {i: t for i, t in retain}
     rt.check_conservation()
-    e_lg = rel_l2(lg[0], o["lg"])
-    check_token(int(first[0]), o["tok"], o["lg"])
+    o16, o32 = o["bf16"], o["fp32"]
+    report = []
+    check_token(int(first[0]), o32["tok"], o32["lg"])
     att = abi.bf16_to_f32(rt.captured_attention())
-    errs = {}
-    for l in range(LWM7B_2L.layers):
-        errs[f"attn{l}"] = rel_l2(att[l], o["att"][l])
-        k, v = rt.read_kv(3, l)
-        assert k.shape == (S2, LWM7B_2L.hidden)
-        errs[f"k{l}"] = rel_l2(abi.bf16_to_f32(k[o["kv_pos"]]), o["k"][l])
-        errs[f"v{l}"] = rel_l2(abi.bf16_to_f32(v[o["kv_pos"]]), o["v"][l])
+    reads = [rt.read_kv(3, l) for l in range(LWM7B_2L.layers)]
     rt.close()
-    print(f"config2 32K {mode}: logits rel-L2 {e_lg:.2e}, " +
-          ", ".join(f"{k} {v:.2e}" for k, v in errs.items()))
-    assert e_lg <= REL_TOL, e_lg
-    for k, v in errs.items():
-        assert v <= REL_TOL, (k, v)
+    check_close("logits", lg[0], o16["lg"], o32["lg"], report)
+    for l in range(LWM7B_2L.layers):
+        check_close(f"attn{l}", att[l], o16["att"][l], o32["att"][l], report)
+        k, v = reads[l]
+        assert k.shape == (S2, LWM7B_2L.hidden)
+        check_close(f"k{l}", abi.bf16_to_f32(k[o["kv_pos"]]), o16["k"][l], o32["k"][l], report)
+        check_close(f"v{l}", abi.bf16_to_f32(v[o["kv_pos"]]), o16["v"][l], o32["v"][l], report)
+    print(f"config2 32K {mode}: " + "; ".join(report))
 
 
-def _k1_case(S, d, pos_i, q_scale, seed):
+def _k1_case(S, d, pos_i, q_scale, seed, ref_dtype="float32"):
     torch = pytest.importorskip("torch")
     heads, hd = 32, 128
     H = heads * hd
@@ -139,15 +162,16 @@ def _k1_case(S, d, pos_i, q_scale, seed):
     scale = hd ** -0.5
     for h in range(heads):
         sl = slice(h * hd, (h + 1) * hd)
-        qh = qs[rows.cuda(), sl].float()
-        kh = K[:, sl].float()
-        vh = V[:, sl].float()
+        rd = getattr(torch, ref_dtype)
+        qh = qs[rows.cuda(), sl].to(rd)
+        kh = K[:, sl].to(rd)
+        vh = V[:, sl].to(rd)
         s = (qh @ kh.T) * scale
         qpos = rows.cuda() * d + pos_i
         mask = torch.arange(S, device="cuda")[None, :] > qpos[:, None]
         s.masked_fill_(mask, float("-inf"))
         ref = torch.softmax(s, dim=-1) @ vh
-        got = out[rows.cuda(), sl].float()
+        got = out[rows.cuda(), sl].to(rd)
         errs.append((torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item())
         # peaky: the largest probability of a row is far from uniform
         if h == 0:
@@ -195,22 +219,87 @@ def test_config4_lwm7b_multi_master_decode_vs_oracle(transport, monkeypatch):
             i = list(dd["batch"]).index(r)
             kc = np.stack([pre[r][l][0] for l in range(shape.layers)])
             vc = np.stack([pre[r][l][1] for l in range(shape.layers)])
-            ref_tok, ref_lg, kn, vn, _ = llama_ref.decode_cached(shape, kc, vc, ins[i])
-            e_lg = rel_l2(lg[i], ref_lg)
-            check_token(int(out[i]), ref_tok, ref_lg)
+            ref16 = llama_ref.decode_cached(shape, kc, vc, ins[i], emulate_bf16=True)
+            ref32 = llama_ref.decode_cached(shape, kc, vc, ins[i], emulate_bf16=False)
+            rep = []
+            check_token(int(out[i]), ref32[0], ref32[1])
+            check_close("logits", lg[i], ref16[1], ref32[1], rep)
             for l in range(shape.layers):
                 k1, v1 = rt.read_kv(r, l)
                 assert k1.shape[0] == kc.shape[1] + 1
                 assert np.array_equal(k1[:-1], kc[l]) and np.array_equal(v1[:-1], vc[l])
-                ek = rel_l2(abi.bf16_to_f32(k1[-1]), kn[l])
-                ev = rel_l2(abi.bf16_to_f32(v1[-1]), vn[l])
-                assert ek <= REL_TOL and ev <= REL_TOL, (r, l, ek, ev)
-            report.append((tuple(dd["masters"]), r, e_lg))
-            assert e_lg <= REL_TOL, (dd["masters"], r, e_lg)
+                check_close(f"k_new{l}", abi.bf16_to_f32(k1[-1]), ref16[2][l], ref32[2][l], rep)
+                check_close(f"v_new{l}", abi.bf16_to_f32(v1[-1]), ref16[3][l], ref32[3][l], rep)
+            report.append(f"masters {tuple(dd['masters'])} req {r}: " + ", ".join(rep))
 
     replay.replay(rt, path, on_decode=on_decode)
     rt.check_conservation()
     rt.close()
-    print(f"config4 LWM-7B geometry {transport}: " +
-          ", ".join(f"masters {m} req {r}: logits rel-L2 {e:.2e}" for m, r, e in report))
+    print(f"config4 LWM-7B geometry {transport}: " + " | ".join(report))
     assert len(report) == 6
+
+
+# ---- fp32 check mode of the kernels -------------------------------------------------
+
+def test_decode_attention_fp32_check_mode():
+    """K3 + K4 with fp32 output against fp64 on the same bf16 q/K/V: split-KV
+    partials over two slabs (random page slots, uneven chunk counts), LSE
+    combine — rel-L2 <= 1e-5 (north_star's fp32 check-mode bound)."""
+    torch = pytest.importorskip("torch")
+    heads, hd, cap = 32, 128, 20000
+    H = heads * hd
+    torch.manual_seed(5)
+    ks = [torch.randn(cap, H, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    vs = [torch.randn(cap, H, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    b = 3
+    q = (torch.randn(b, H, device="cuda") * 3).to(torch.bfloat16)
+    g = torch.Generator().manual_seed(1)
+    chunks = []
+    for r in range(b):
+        for inst in range(2):
+            n = [9000, 1, 4096][r] if inst == 0 else [333, 7000, 0][r]
+            if n:
+                chunks.append((r, inst, torch.randperm(cap, generator=g)[:n].to(torch.int32).cuda()))
+    out = torch.empty(b, H, device="cuda", dtype=torch.float32)
+    abi.k_decode_attention(q.data_ptr(), b, [ks[c[1]].data_ptr() for c in chunks],
+                           [vs[c[1]].data_ptr() for c in chunks], [c[2].data_ptr() for c in chunks],
+                           [c[2].numel() for c in chunks], [c[0] for c in chunks], out.data_ptr(),
+                           heads, hd, out_f32=True)
+    torch.cuda.synchronize()
+    worst = 0.0
+    for r in range(b):
+        K = torch.cat([ks[c[1]][c[2].long()] for c in chunks if c[0] == r]).double()
+        V = torch.cat([vs[c[1]][c[2].long()] for c in chunks if c[0] == r]).double()
+        qq = q[r].double().view(heads, hd)
+        s_ = torch.einsum("hd,khd->hk", qq, K.view(-1, heads, hd)) / hd ** 0.5
+        ref = torch.einsum("hk,khd->hd", torch.softmax(s_, -1), V.view(-1, heads, hd)).reshape(H)
+        worst = max(worst, (torch.linalg.norm(out[r].double() - ref) / torch.linalg.norm(ref)).item())
+    print(f"K3+K4 fp32 check mode: rel-L2 {worst:.2e}")
+    assert worst <= 1e-5, worst
+
+
+def test_gemm_fp32_check_mode():
+    """K5 with the fp32 epilogue (bf16 operands, fp32 accumulation and output)
+    against fp64 at the LWM-7B projection shapes, prefill (CTA pair) and
+    decode (skinny) schedules — rel-L2 <= 1e-5."""
+    torch = pytest.importorskip("torch")
+    torch.manual_seed(3)
+    for M, N, K in ((4096, 4096, 4096), (16, 12288, 4096), (1, 32000, 4096), (300, 22016, 4096)):
+        a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+        d = torch.empty(M, N, device="cuda", dtype=torch.float32)
+        abi.k_gemm(a.data_ptr(), w.data_ptr(), d.data_ptr(), M, N, K, 2)
+        torch.cuda.synchronize()
+        ref = a.double() @ w.double().t()
+        err = (torch.linalg.norm(d.double() - ref) / torch.linalg.norm(ref)).item()
+        print(f"K5 fp32 check mode {M}x{N}x{K}: rel-L2 {err:.2e}")
+        assert err <= 1e-5, (M, N, K, err)
+
+
+@pytest.mark.parametrize("S,d,pos_i", [(8192, 1, 0), (16384, 4, 1)])
+def test_k1_bound_against_fp64(S, d, pos_i):
+    """K1's stated bound: P rounded to bf16 for the tensor-core P.V, all else
+    fp32 — rel-L2 <= 5e-3 against fp64 on every sampled row set."""
+    err, _ = _k1_case(S, d, pos_i, q_scale=1.0, seed=7 + S, ref_dtype="float64")
+    print(f"K1 vs fp64 S={S} d={d}: rel-L2 {err:.2e}")
+    assert err <= 5e-3, err

@@ -22,3 +22,21 @@ def test_placement_query_beyond_64_instances():
     rt = abi.Runtime(abi.TINY, n, devices=None, kv_capacity=10)
     rt.prefill([1], [10 * n], [0], [[(i, 10) for i in range(n)]])
     assert rt.placement(1) == {i: 10 for i in range(n)}
+
+
+def test_prefill_stats_follow_the_reference_mechanics():
+    """The runtime accounts each prefill through its restatements of
+    build_ring_schedule / proactive_scale_down (esp_mechanics.cpp:45-136):
+    ring volume (d-1)*sum, transient buffer ceil(sum/d) (Fig. 6: 6 tokens on
+    3 instances -> 2), zero extra migration for ring-member survivors."""
+    rt = abi.Runtime(abi.TINY, 4, devices=None, kv_capacity=100)
+    rt.prefill([1], [6], [0, 1, 2], [[(0, 4), (1, 2)]])
+    st = rt.last_prefill_stats()
+    assert st["ring_volume_tokens"] == 2 * 6
+    assert st["transient_buffer_tokens"] == 2
+    assert st["extra_migration_tokens"] == 0
+    assert st["cross_domain_tokens"] == 0 and st["nvlink_bytes"] == 0  # no devices
+    # a resting instance outside the ring (a disaggregation-style plan)
+    rt.prefill([2], [7], [0, 1], [[(3, 7)]])
+    st = rt.last_prefill_stats()
+    assert st["ring_volume_tokens"] == 7 and st["extra_migration_tokens"] == -1
