@@ -61,6 +61,12 @@ struct DeviceCtx {
   std::vector<void*> weight_allocs;
   std::vector<cudaEvent_t> sync_events;  // cross-domain event pool
   size_t sync_used = 0;
+  // Ring-transport arrival counters of this domain (one slot per source
+  // domain, incremented by the sources' QKV epilogues over NVLink) and the
+  // running totals the host expects in each (monotonic across layers and
+  // prefills, so no reset races with a source that runs ahead).
+  unsigned long long* arrive = nullptr;
+  unsigned long long arrive_expect[k::kMaxWaitSrc] = {};
 };
 
 // Work list of K1 (items = (segment, query-tile pair, head)) for `segs`, in

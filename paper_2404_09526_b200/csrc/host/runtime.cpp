@@ -60,6 +60,7 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
     : cfg_(cfg) {
   opts_.domain_per_instance = std::getenv("ESP_DOMAIN_PER_INSTANCE") != nullptr;
   opts_.ring_copy = std::getenv("ESP_RING_COPY") != nullptr;
+  opts_.force_arrival = std::getenv("ESP_RING_ARRIVAL") != nullptr;
   opts_.decode_copy = std::getenv("ESP_DECODE_COPY") != nullptr;
   opts_.fuse_norm_prefill = std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr;
   opts_.fuse_norm_decode = std::getenv("ESP_DECODE_NORM_KERNEL") == nullptr;
@@ -196,6 +197,7 @@ Runtime::~Runtime() {
       if (b->ptr) cudaFree(b->ptr);
     }
     if (dc.rope) cudaFree(dc.rope);
+    if (dc.arrive) cudaFree(dc.arrive);
     for (cudaEvent_t e : dc.sync_events) cudaEventDestroy(e);
     if (dc.e0) cudaEventDestroy(dc.e0);
     if (dc.e1) cudaEventDestroy(dc.e1);

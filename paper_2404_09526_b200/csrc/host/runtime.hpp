@@ -185,9 +185,14 @@ class Runtime {
   //   ESP_DECODE_COPY          decode query broadcast / partial gather by peer
   //                            copies instead of fused peer stores;
   //   ESP_PREFILL_NORM_KERNEL / ESP_DECODE_NORM_KERNEL  RMSNorm as kernels
-  //                            instead of fused into the GEMMs.
+  //                            instead of fused into the GEMMs;
+  //   ESP_RING_ARRIVAL         (tests) arrival counters also between domains
+  //                            of one GPU, IN ADDITION to the event wait there
+  //                            (so the counting is checked where a spinning
+  //                            K1 could otherwise starve the source's GEMM).
   struct Options {
     bool domain_per_instance = false;
+    bool force_arrival = false;
     bool ring_copy = false;
     bool decode_copy = false;
     bool fuse_norm_prefill = true;

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -243,6 +244,19 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     }
     p.rows += blk0[i + 1] - blk0[i];
   }
+  // Cross-GPU arrivals: destination `dst` waits for source `src`'s K/V
+  // blocks on the device (arrival counter polled by K1's producer) when they
+  // sit on different GPUs and the source's QKV runs the tcgen05 kernels that
+  // signal (> 32 rows). Otherwise — same GPU (ESP_DOMAIN_PER_INSTANCE: a
+  // spinning K1 could starve the source's GEMM of SMs), skinny sources or
+  // the copy ring — the stream waits for the source's QKV event instead.
+  auto same_gpu = [&](int a, int b) {
+    return devices_[static_cast<size_t>(a)]->device == devices_[static_cast<size_t>(b)]->device;
+  };
+  auto use_ctr = [&](int src, int dst) {
+    return push && src != dst && src < k::kMaxWaitSrc && parts[src].rows > 32 &&
+           (!same_gpu(src, dst) || opts_.force_arrival);
+  };
   for (auto& [dom, p] : parts) {
     for (int i : p.positions) {
       for (int r = 0; r < n; ++r) {
@@ -257,6 +271,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
           sg.kv_row0[rd] = row0[o][r];
           sg.kv_len[rd] = stripe_len(o, r);
           sg.shift[rd] = o > i ? 1 : 0;
+          sg.wait_src[rd] = use_ctr(dom_of[o], dom) ? dom_of[o] + 1 : 0;
         }
         p.segs.push_back(sg);
       }
@@ -300,34 +315,60 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     scratch<bf16>(dc.q, lr * H);
     scratch<bf16>(dc.attn, lr * H);
     scratch<bf16>(dc.h, lr * F);
-    scratch<bf16>(dc.kb, static_cast<size_t>(rows) * H);  // gather buffers: every block
-    scratch<bf16>(dc.vb, static_cast<size_t>(rows) * H);
+    // Gather buffers hold every block of the layer; the push transport
+    // double-buffers them by layer parity, so a source may store layer l+1
+    // while this domain's K1 still reads layer l.
+    const size_t nbuf = push ? 2 : 1;
+    scratch<bf16>(dc.kb, nbuf * static_cast<size_t>(rows) * H);
+    scratch<bf16>(dc.vb, nbuf * static_cast<size_t>(rows) * H);
+    if (fuse_norm_prefill()) {
+      scratch<float>(dc.ss1, lr);
+      scratch<float>(dc.ss2, lr);
+    }
+    if (push && !dc.arrive) {
+      cuda_ok(cudaMalloc(&dc.arrive, k::kMaxWaitSrc * sizeof(unsigned long long)), "cudaMalloc(arrive)");
+      cuda_ok(cudaMemsetAsync(dc.arrive, 0, k::kMaxWaitSrc * sizeof(unsigned long long), s), "memset");
+      std::fill(std::begin(dc.arrive_expect), std::end(dc.arrive_expect), 0ull);
+    }
     cuda_ok(cudaEventRecord(dc.e0, s), "event");
     if (p.rows > 0) {
       timed(kPhEmbed, s, [&] {
         k::embed(static_cast<int32_t*>(dc.tok.ptr), dc.embed, static_cast<bf16*>(dc.x.ptr),
-                 p.rows, H, s);
+                 p.rows, H, s, fuse_norm_prefill() ? static_cast<float*>(dc.ss1.ptr) : nullptr);
       });
     }
   }
+  // Source domains' arrival counters must exist before any epilogue
+  // signals them (allocation above is stream-ordered per domain).
+  if (push) {
+    for (auto& [dom, p] : parts) {
+      DeviceGuard g(devices_[static_cast<size_t>(dom)]->device);
+      cuda_ok(cudaStreamSynchronize(devices_[static_cast<size_t>(dom)]->stream), "arrive init");
+    }
+  }
+  const bool fuse = fuse_norm_prefill();
 
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
   std::map<int, std::vector<cudaEvent_t>> readers;  // copies reading a domain's gather buffer
-  std::map<int, cudaEvent_t> attn_done;  // push: domain's attention of the previous layer
+  // push: attn_done[dom][parity] = dom's K1 of the last layer that read that
+  // gather-buffer parity (peers may overwrite it once it has completed)
+  std::map<int, std::array<cudaEvent_t, 2>> attn_done;
   for (int l = 0; l < cfg_.layers; ++l) {
+    const int par = push ? (l & 1) : 0;
+    const size_t boff = static_cast<size_t>(par) * rows * H;
     std::map<int, cudaEvent_t> qkv_done;  // push: domain's QKV (and its pushes) of this layer
     std::map<int, std::vector<cudaEvent_t>> ready;  // domain -> block -> event (nullptr: absent)
     for (auto& [dom, p] : parts) ready[dom].assign(static_cast<size_t>(d), nullptr);
-    // 1. per-domain norm + QKV (+RoPE, + retention at the origin).
+    // 1. per-domain QKV (+RoPE, + retention, + the push to every peer's gather buffer).
     for (auto& [dom, p] : parts) {
       DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
       DeviceGuard g(dc.device);
       cudaStream_t s = dc.stream;
       for (cudaEvent_t e : readers[dom]) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
       readers[dom].clear();
-      if (push) {  // peers' gather buffers are free once their previous attention is done
-        for (auto& [od, e] : attn_done) {
-          if (od != dom) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
+      if (push) {  // peers' buffers of this parity are free once their K1 of layer l-2 is done
+        for (auto& [od, ev] : attn_done) {
+          if (od != dom && ev[par] != nullptr) cuda_ok(cudaStreamWaitEvent(s, ev[par], 0), "wait");
         }
       }
       if (p.rows == 0) {  // empty stripes (prompt shorter than the ring): nothing to send
@@ -340,12 +381,14 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       const LayerW& w = dc.layers[l];
       bf16* x = static_cast<bf16*>(dc.x.ptr);
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-      timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, p.rows, H, cfg_.rms_eps, s); });
+      if (!fuse) {
+        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, p.rows, H, cfg_.rms_eps, s); });
+      }
       k::GemmEpilogue ep;
       ep.kind = k::kEpiQkvRope;
       ep.q_out = static_cast<bf16*>(dc.q.ptr);
-      ep.k_out = static_cast<bf16*>(dc.kb.ptr);
-      ep.v_out = static_cast<bf16*>(dc.vb.ptr);
+      ep.k_out = static_cast<bf16*>(dc.kb.ptr) + boff;
+      ep.v_out = static_cast<bf16*>(dc.vb.ptr) + boff;
       ep.kv_rows = static_cast<int32_t*>(dc.kvrow.ptr);
       ep.pos = static_cast<int32_t*>(dc.pos.ptr);
       ep.rope = dc.rope;
@@ -353,6 +396,11 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       ep.head_dim = cfg_.head_dim;
       ep.row_inst = static_cast<int32_t*>(dc.rinst.ptr);
       ep.row_slot = static_cast<int32_t*>(dc.rslot.ptr);
+      if (fuse) {
+        ep.ss_in = static_cast<float*>(dc.ss1.ptr);
+        ep.norm_dim = H;
+        ep.norm_eps = cfg_.rms_eps;
+      }
       if (push) {
         for (size_t j = 0; j < instances_.size(); ++j) {
           ep.slab_k[j] = instances_[j].layer_k(l);
@@ -361,9 +409,10 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         for (auto& [od, op] : parts) {
           if (od == dom) continue;
           DeviceCtx& pc = *devices_[static_cast<size_t>(od)];
-          ep.k_peer[ep.n_peer] = static_cast<bf16*>(pc.kb.ptr);
-          ep.v_peer[ep.n_peer] = static_cast<bf16*>(pc.vb.ptr);
+          ep.k_peer[ep.n_peer] = static_cast<bf16*>(pc.kb.ptr) + boff;
+          ep.v_peer[ep.n_peer] = static_cast<bf16*>(pc.vb.ptr) + boff;
           ++ep.n_peer;
+          if (use_ctr(dom, od)) ep.arrive[ep.n_arrive++] = pc.arrive + dom;
         }
       } else {
         for (size_t j = 0; j < dc.slabs.size(); ++j) {
@@ -371,7 +420,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
           ep.slab_v[j] = instances_[dc.slabs[j]].layer_v(l);
         }
       }
-      timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, p.rows, 3 * H, H, ep, s); });
+      timed(kPhQkv, s, [&] { k::gemm(fuse ? x : xn, H, w.wqkv, H, p.rows, 3 * H, H, ep, s); });
       cudaEvent_t e = sync_event(dc);
       cuda_ok(cudaEventRecord(e, s), "event");
       for (int i : p.positions) ready[dom][i] = e;
@@ -400,15 +449,27 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         readers[src].push_back(e);
       }
     }
-    // 3. retention on pass, attention, O, MLP — all local to each domain.
+    // 3. retention on pass (copy mode), attention, O, MLP — local to each domain.
     for (auto& [dom, p] : parts) {
       DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
       DeviceGuard g(dc.device);
       cudaStream_t s = dc.stream;
-      if (push) {  // every domain's K/V rows must have landed here
+      k::RingWait wait;
+      bool any_wait = false;
+      if (push) {
+        // Every other domain's K/V rows must have landed here: by its QKV
+        // event, or on the device through its arrival counter (K1 starts on
+        // its own block while remote blocks still stream in over NVLink).
         for (auto& [od, e] : qkv_done) {
-          if (od != dom) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
+          if (od == dom) continue;
+          if (use_ctr(od, dom)) {
+            dc.arrive_expect[od] += static_cast<unsigned long long>(parts[od].rows) * 2 * H;
+            wait.target[od] = dc.arrive_expect[od];
+            any_wait = true;
+          }
+          if (!use_ctr(od, dom) || same_gpu(od, dom)) cuda_ok(cudaStreamWaitEvent(s, e, 0), "wait");
         }
+        wait.ctr = dc.arrive;
       }
       k::DecodeSlabs slabs{};
       for (size_t j = 0; j < dc.slabs.size(); ++j) {
@@ -420,7 +481,6 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
                      static_cast<int32_t*>(dc.ret_slot.ptr), static_cast<int>(p.ret_rows.size()),
                      slabs, H, s);
       if (p.rows == 0) continue;
-      const LayerW& w = dc.layers[l];
       bf16* x = static_cast<bf16*>(dc.x.ptr);
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
       bf16* attn = static_cast<bf16*>(dc.attn.ptr);
@@ -429,15 +489,26 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       timed(kPhAttention, s, [&] {
         const bf16* qd = static_cast<bf16*>(dc.q.ptr);
         // Q rows are this domain's local rows, K/V rows are global.
-        k::ring_attention(qd, static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr), attn, p.rows, rows, cfg_.heads, cfg_.head_dim, static_cast<k::RingSegment*>(dc.segs.ptr), static_cast<int32_t*>(dc.work.ptr), n_work, scale, s);
+        k::ring_attention(qd, static_cast<bf16*>(dc.kb.ptr) + boff,
+                          static_cast<bf16*>(dc.vb.ptr) + boff, attn, p.rows, rows, cfg_.heads,
+                          cfg_.head_dim, static_cast<k::RingSegment*>(dc.segs.ptr),
+                          static_cast<int32_t*>(dc.work.ptr), n_work, scale, s,
+                          any_wait ? &wait : nullptr);
       });
       if (cap_armed_) cap_layer(dc, l, attn, s);
-      if (push) {  // peers may overwrite this gather buffer with the next layer
+      if (push) {  // peers may overwrite this parity of the gather buffer after this
         cudaEvent_t e = sync_event(dc);
         cuda_ok(cudaEventRecord(e, s), "event");
-        attn_done[dom] = e;
+        auto it = attn_done.find(dom);
+        if (it == attn_done.end()) it = attn_done.emplace(dom, std::array<cudaEvent_t, 2>{nullptr, nullptr}).first;
+        it->second[par] = e;
       }
-      o_and_mlp(dc, l, p.rows, x, attn, xn, hbuf, NormFuse{}, s);
+      NormFuse nf;
+      if (fuse) {
+        nf.ss_o = static_cast<float*>(dc.ss2.ptr);
+        nf.ss_d = static_cast<float*>(dc.ss1.ptr);
+      }
+      o_and_mlp(dc, l, p.rows, x, attn, xn, hbuf, nf, s);
     }
   }
 
@@ -739,9 +810,15 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
     scratch<bf16>(dc.q, nl * H);
     scratch<bf16>(dc.attn, nl * H);
     scratch<bf16>(dc.h, nl * F);
+    // sums of squares for the fused RMSNorm (used when fuse_dec below holds)
+    float* ss1 = nullptr;
+    if (opts_.fuse_norm_decode && !opts_.decode_copy && nl <= 32) {
+      ss1 = scratch<float>(dc.ss1, 32);
+      cuda_ok(cudaMemsetAsync(scratch<float>(dc.ss2, 32), 0, 32 * sizeof(float), s), "memset");
+    }
     timed(kPhEmbed, s, [&] {
       k::embed(static_cast<int32_t*>(dc.tok.ptr), dc.embed, static_cast<bf16*>(dc.x.ptr),
-               static_cast<int>(nl), H, s);
+               static_cast<int>(nl), H, s, ss1);
     });
   }
   const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
@@ -767,9 +844,20 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
   for (auto& [xd, v] : part_dests) {
     if (static_cast<int>(v.size()) > k::kMaxPartDst) fused = false;
   }
+  // Fused transport: a KV domain that is also a master computes the chunks
+  // of its OWN rows first, in a launch that needs only its own QKV, while the
+  // other masters' queries are still on their way (the query
+  // exchange overlapped with local attention); the rest follows once they
+  // have landed. own_n[xd] = number of leading own-row chunks.
+  std::map<int, int> own_n;
   if (fused) {
-    // chunk -> index of its master domain in the KV domain's PartDst table
     for (auto& [xd, chs] : xchunks) {
+      std::stable_partition(chs.begin(), chs.end(),
+                            [&](const k::DecodeChunk& ch) { return mdom[ch.row] == xd; });
+      int own = 0;
+      for (const k::DecodeChunk& ch : chs) own += mdom[ch.row] == xd ? 1 : 0;
+      own_n[xd] = own;
+      // chunk -> index of its master domain in the KV domain's PartDst table
       const std::vector<int>& pdv = part_dests[xd];
       for (k::DecodeChunk& ch : chs) {
         const int md = mdom[ch.row];
@@ -780,6 +868,16 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
       h2d(static_cast<k::DecodeChunk*>(xc.chunks.ptr), chs, xc.stream);
     }
   }
+  // RMSNorm fused into the masters' skinny GEMMs (<= 32 rows per master),
+  // exactly as the single-domain decode: sums of squares accumulate in the
+  // residual epilogues, the consuming GEMM scales its rows.
+  const bool fuse_dec = fused && opts_.fuse_norm_decode && [&] {
+    for (auto& [md, rs] : mrows) {
+      if (rs.size() > 32) return false;
+    }
+    return true;
+  }();
+  // (the masters' embeddings above already stored the sums of squares)
   if (fused) {
     std::map<int, cudaEvent_t> att_done, comb_done;  // previous layer's
     for (int l = 0; l < cfg_.layers; ++l) {
@@ -796,9 +894,17 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         const LayerW& w = dc.layers[l];
         bf16* x = static_cast<bf16*>(dc.x.ptr);
         bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-        timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
+        if (!fuse_dec) {
+          timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, nl, H, cfg_.rms_eps, s); });
+        }
         k::GemmEpilogue ep;
         ep.kind = k::kEpiQkvRope;
+        if (fuse_dec) {
+          ep.ss_in = static_cast<float*>(dc.ss1.ptr);
+          ep.ss_zero = static_cast<float*>(dc.ss2.ptr);
+          ep.norm_dim = H;
+          ep.norm_eps = cfg_.rms_eps;
+        }
         ep.q_out = static_cast<bf16*>(dc.q.ptr);
         ep.pos = static_cast<int32_t*>(dc.pos.ptr);
         ep.rope = dc.rope;
@@ -823,12 +929,13 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
           ep.slab_k[j] = instances_[dc.slabs[j]].layer_k(l);
           ep.slab_v[j] = instances_[dc.slabs[j]].layer_v(l);
         }
-        timed(kPhQkv, s, [&] { k::gemm(xn, H, w.wqkv, H, nl, 3 * H, H, ep, s); });
+        timed(kPhQkv, s, [&] { k::gemm(fuse_dec ? x : xn, H, w.wqkv, H, nl, 3 * H, H, ep, s); });
         cudaEvent_t e = sync_event(dc);
         cuda_ok(cudaEventRecord(e, s), "event");
         q_ready[md] = e;
       }
-      // 2. KV domains: split-KV partials pushed to the masters' buffers.
+      // 2. KV domains: split-KV partials pushed to the masters' buffers —
+      // own rows first (no cross-domain wait), then the other masters' rows.
       std::map<int, cudaEvent_t> att_now;
       for (auto& [xd, chs] : xchunks) {
         DeviceCtx& xc = *devices_[static_cast<size_t>(xd)];
@@ -837,26 +944,35 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         k::PartDst pd;
         const std::vector<int>& pdv = part_dests[xd];
         for (size_t i = 0; i < pdv.size(); ++i) {
-          const int md = pdv[i];
-          DeviceCtx& mc = *devices_[static_cast<size_t>(md)];
+          DeviceCtx& mc = *devices_[static_cast<size_t>(pdv[i])];
           pd.o[i] = static_cast<float*>(mc.part_o.ptr);
           pd.ml[i] = static_cast<float*>(mc.part_ml.ptr);
-          cuda_ok(cudaStreamWaitEvent(s, q_ready[md], 0), "wait");
-          // the master's combine of the previous layer has read its partials
-          if (comb_done.count(md)) cuda_ok(cudaStreamWaitEvent(s, comb_done[md], 0), "wait");
         }
         k::DecodeSlabs slabs{};
         for (size_t j = 0; j < xc.slabs.size(); ++j) {
           slabs.k[j] = instances_[xc.slabs[j]].layer_k(l);
           slabs.v[j] = instances_[xc.slabs[j]].layer_v(l);
         }
-        timed(kPhDecodeAttn, s, [&] {
-          k::decode_attention(static_cast<bf16*>(xc.qin.ptr),
-                              static_cast<k::DecodeChunk*>(xc.chunks.ptr),
-                              static_cast<int>(chs.size()), slabs, heads, hd, scale,
-                              static_cast<float*>(xc.part_o.ptr),
-                              static_cast<float*>(xc.part_ml.ptr), s, &pd);
-        });
+        const int own = own_n[xd], n_ch = static_cast<int>(chs.size());
+        auto attend = [&](int c0, int c1) {
+          if (c1 <= c0) return;
+          timed(kPhDecodeAttn, s, [&] {
+            k::decode_attention(static_cast<bf16*>(xc.qin.ptr),
+                                static_cast<k::DecodeChunk*>(xc.chunks.ptr) + c0, c1 - c0, slabs,
+                                heads, hd, scale, static_cast<float*>(xc.part_o.ptr),
+                                static_cast<float*>(xc.part_ml.ptr), s, &pd);
+          });
+        };
+        // own rows: this domain's QKV is earlier on its stream; its own
+        // combine of the previous layer too (stream order)
+        attend(0, own);
+        for (int md : pdv) {
+          if (md == xd) continue;
+          cuda_ok(cudaStreamWaitEvent(s, q_ready[md], 0), "wait");
+          // the master's combine of the previous layer has read its partials
+          if (comb_done.count(md)) cuda_ok(cudaStreamWaitEvent(s, comb_done[md], 0), "wait");
+        }
+        attend(own, n_ch);
         cudaEvent_t e = sync_event(xc);
         cuda_ok(cudaEventRecord(e, s), "event");
         att_now[xd] = e;
@@ -885,7 +1001,13 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         cudaEvent_t e = sync_event(mc);
         cuda_ok(cudaEventRecord(e, s), "event");
         comb_now[md] = e;
-        o_and_mlp(mc, l, nl, x, attn, xn, hbuf, NormFuse{}, s);
+        NormFuse nf;
+        if (fuse_dec) {
+          nf.ss_o = static_cast<float*>(mc.ss2.ptr);
+          nf.ss_d = static_cast<float*>(mc.ss1.ptr);
+          nf.zero_in_kernel = true;
+        }
+        o_and_mlp(mc, l, nl, x, attn, xn, hbuf, nf, s);
       }
       comb_done = comb_now;
     }

@@ -308,6 +308,23 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
   }
 }
 
+// Arrival signal of the fused ring transport (GemmEpilogue.arrive): called by
+// the CTA's 128 epilogue threads after each output tile. When the tile was a
+// K or V tile of a QKV epilogue with peers, every thread's peer stores are
+// made visible system-wide, the 128 threads meet at a named barrier, and one
+// thread adds rows x cols to each peer's counter slot of this source domain.
+// Uniform per CTA, so the barrier is reached by all 128 threads or none.
+__device__ __forceinline__ void signal_arrival(const GemmEpilogue& ep, int n0, int rows_valid,
+                                               int cols) {
+  if (ep.kind != kEpiQkvRope || ep.n_arrive == 0 || n0 < ep.hidden) return;
+  __threadfence_system();
+  ptx::named_bar_sync(2, 128);
+  if ((threadIdx.x & 127) == 0 && rows_valid > 0) {
+    const unsigned long long add = static_cast<unsigned long long>(rows_valid) * cols;
+    for (int p = 0; p < ep.n_arrive; ++p) atomicAdd_system(ep.arrive[p], add);
+  }
+}
+
 // Work of one persistent CTA: whole output tiles round-robin (kb_per_cta ==
 // 0), or stream-K (kb_per_cta > 0): the (tile, K block) space is cut into
 // equal contiguous ranges of kb_per_cta K blocks, one per CTA, each range
@@ -462,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         epilogue_tile<BN>(ep, TmemAcc{tacc}, m, m < M, nb, N);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
+        signal_arrival(ep, nb * BN, min(BM, M - mb * BM), BN);
         continue;
       }
       // Stream-K: store this segment's fp32 partial rows in its own
@@ -1021,6 +1039,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(tempty_lead + acc * 8);
+      signal_arrival(ep, nb * kTileN,
+                     min(kRows, M - (mb * kTileM + static_cast<int>(rank) * kRows)), kTileN);
     }
   }
   ptx::tc_fence_before();

@@ -49,6 +49,13 @@ struct GemmEpilogue {
   int n_peer = 0;
   bf16* k_peer[kMaxPeers] = {};
   bf16* v_peer[kMaxPeers] = {};
+  // Arrival counters of that transport: after a CTA stored a K or V tile to
+  // the peers, one system-scope atomic per peer adds rows x columns to
+  // arrive[p] (the peer's counter slot of this source domain); the peer's
+  // ring-attention producer waits for the layer's running total before it
+  // loads this source's blocks (RingWait) — no host or stream round trip.
+  int n_arrive = 0;
+  unsigned long long* arrive[kMaxPeers] = {};
   // Multi-master decode across domains: q rows go to row q_rows[m] of q_out
   // and of every q_peer (the query broadcast fused into the QKV epilogue).
   const int32_t* q_rows = nullptr;
@@ -92,6 +99,19 @@ struct RingSegment {
   int32_t kv_row0[kMaxRounds];
   int32_t kv_len[kMaxRounds];
   int32_t shift[kMaxRounds];
+  // 0: round r's block is already resident; s + 1: it is stored by source
+  // domain s over NVLink and the producer waits on RingWait slot s first.
+  int32_t wait_src[kMaxRounds];
+};
+
+// Arrival waits of one ring-attention launch (cross-GPU push transport):
+// ctr[s] is this domain's counter of the K/V bytes-units source domain s has
+// stored into its gather buffer (GemmEpilogue.arrive), target[s] the running
+// total that completes the blocks this launch reads.
+constexpr int kMaxWaitSrc = 16;
+struct RingWait {
+  const unsigned long long* ctr = nullptr;
+  unsigned long long target[kMaxWaitSrc] = {};
 };
 
 // K1: striped ring attention over segments; q/out are [q_rows x
@@ -101,7 +121,8 @@ struct RingSegment {
 // order build_attention_work lays them out.
 void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
                     int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
-                    const int32_t* d_work, int n_work, float scale, cudaStream_t s);
+                    const int32_t* d_work, int n_work, float scale, cudaStream_t s,
+                    const RingWait* wait = nullptr);
 
 #ifdef ESP_STUDY
 // Kernel-study build only (tools/attn_prof.py, `make STUDY=1`): K1 with

@@ -350,4 +350,23 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+
+// Cross-GPU flag protocol of the ring transport: a system-scope acquire load
+// of a counter another GPU increments, and the proxy fence that orders the
+// generic-proxy data writes it published before this thread's TMA
+// (async-proxy) reads of them.
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 }  // namespace esp::ptx

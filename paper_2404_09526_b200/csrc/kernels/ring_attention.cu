@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ out,
                       int hidden, const RingSegment* __restrict__ segs,
                       const int32_t* __restrict__ work, int n_work, float scale_log2,
-                      uint64_t* __restrict__ prof) {
+                      uint64_t* __restrict__ prof, const __grid_constant__ RingWait wait) {
   using C = Cfg2<HD>;
   uint64_t prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const uint64_t prof_t_begin = kProf ? clock64() : 0;
@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------------------------------------------------- producer
       int ks = 0, vs = 0;
       uint32_t kph = 0, vph = 0, items = 0;
+      uint32_t arrived = 0;  // source domains whose blocks of this launch have landed
       for (int w = w_begin; w < w_end; ++w, ++items) {
         const Item it = load_item(work, w, segs);
         const RingSegment* sg = &segs[it.seg];
@@ -264,6 +265,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         Steps st;
         for (st.begin(sg, it); st.valid(); st.next()) {
           const int row = st.kv_row();
+          const int src = sg->wait_src[st.r] - 1;
+          if (src >= 0 && !(arrived >> src & 1u)) {
+            // The round's block comes from another GPU's QKV epilogue (peer
+            // stores + system-scope counter): wait for the layer's total,
+            // then order those generic-proxy writes before our TMA reads.
+            const uint64_t t0 = ptx::globaltimer_ns();
+            while (ptx::ld_acquire_sys_u64(wait.ctr + src) < wait.target[src]) {
+              __nanosleep(128);
+              // a source that never arrives is a bug: fail the launch
+              // (an error the host sees) rather than hang the GPU
+              if (ptx::globaltimer_ns() - t0 > 20000000000ull) __trap();
+            }
+            ptx::fence_proxy_async_global();
+            arrived |= 1u << src;
+          }
           ESP_PROF_WAIT(1, ptx::mbar_wait(&k_empty[ks], kph ^ 1));
           ptx::mbar_expect_tx(&k_full[ks], C::kKvBytes);
           for (int b = 0; b < C::kBoxes; ++b) {
@@ -591,7 +607,7 @@ int sm_count2() {
 template <int HD, bool kProf, int kPoly8>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
-             cudaStream_t s, uint64_t* prof) {
+             cudaStream_t s, uint64_t* prof, const RingWait& wait) {
   using C = Cfg2<HD>;
   once_per_device(reinterpret_cast<const void*>(ring_attention_v2<HD, kProf, kPoly8>), [] {
     cudaFuncSetAttribute(ring_attention_v2<HD, kProf, kPoly8>,
@@ -603,24 +619,25 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
   const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
   ring_attention_v2<HD, kProf, kPoly8><<<grid, kThreads, C::kSmem, s>>>(
-      tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof);
+      tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof, wait);
   count_launch();
 }
 
 template <bool kProf>
 void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
                int heads, int head_dim, const RingSegment* d_segs, const int32_t* d_work,
-               int n_work, float scale, cudaStream_t s, uint64_t* prof) {
+               int n_work, float scale, cudaStream_t s, uint64_t* prof,
+               const RingWait& wait = RingWait{}) {
   if (n_work <= 0) return;
   if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
   // Exponentials computed on the FMA pipe, in eighths of each row's keys
   // (MUFU/FMA balance; 1 in 8 measured best in the step, r01_attn_poly_sweep.txt).
   if (head_dim == 128) {
     launch2<128, kProf, kDefaultPoly8>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work,
-                                       n_work, scale, s, prof);
+                                       n_work, scale, s, prof, wait);
   } else if (head_dim == 64) {
     launch2<64, kProf, kDefaultPoly8>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work,
-                                      n_work, scale, s, prof);
+                                      n_work, scale, s, prof, wait);
   } else {
     throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
   }
@@ -630,9 +647,10 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
 
 void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
                     int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
-                    const int32_t* d_work, int n_work, float scale, cudaStream_t s) {
+                    const int32_t* d_work, int n_work, float scale, cudaStream_t s,
+                    const RingWait* wait) {
   dispatch2<false>(q, k, v, out, q_rows, kv_rows, heads, head_dim, d_segs, d_work, n_work, scale,
-                   s, nullptr);
+                   s, nullptr, wait ? *wait : RingWait{});
 }
 
 #ifdef ESP_STUDY

@@ -27,7 +27,8 @@ LOGIT_TOL = 5e-2
 TIE_GAP = 2e-2
 
 
-@pytest.fixture(autouse=True, params=["colocated", "domain_push", "domain_copy"])
+@pytest.fixture(autouse=True, params=["colocated", "domain_push", "domain_copy",
+                                      "domain_arrival"])
 def transport(request, monkeypatch):
     """colocated: instances of one GPU share buffers (zero-copy ring).
     domain_*: every instance is its own co-location domain (ESP_DOMAIN_PER_
@@ -39,7 +40,14 @@ def transport(request, monkeypatch):
     domain_copy (ESP_RING_COPY, ESP_DECODE_COPY): the ring moves K/V blocks by
     peer copies in the reference's round order and remote-origin tokens are
     retained on pass; decode broadcasts queries / gathers partials by peer
-    copies."""
+    copies. domain_arrival: the push transport with the device-side arrival
+    counters (each QKV epilogue adds its K/V stores to the peers' counters,
+    K1's producer polls them before loading a remote block); on one GPU the
+    stream also waits for the source's event, so this checks the counting,
+    not the concurrency (ESP_RING_ARRIVAL)."""
+    monkeypatch.delenv("ESP_RING_ARRIVAL", raising=False)
+    if request.param == "domain_arrival":
+        monkeypatch.setenv("ESP_RING_ARRIVAL", "1")
     if request.param.startswith("domain"):
         monkeypatch.setenv("ESP_DOMAIN_PER_INSTANCE", "1")
     else:
@@ -358,7 +366,7 @@ def test_config4_multi_master_decode_tiny(transport):
     tables equal the engine's at every step; every step's logits equal those
     of the same requests decoded on ONE instance with ONE master (split-KV
     over 4-5 instances + multi-master LSE combine == dense), teacher-forced."""
-    if transport == "domain_copy":
+    if transport in ("domain_copy", "domain_arrival"):
         pytest.skip("8 domains x 64K-token activations: covered co-located and with push")
     path = os.path.join(GOLD, "scenario_config4_decode.jsonl")
     head, _, _ = replay.load(path)

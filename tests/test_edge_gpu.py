@@ -103,3 +103,23 @@ def test_capacity_and_master_full_errors():
     rt.check_conservation()
     out, _, _ = rt.decode_step([0, 1], [1], [1])  # master with room: the append goes to 1
     assert rt.placement(1) == {0: 100, 1: 1}
+
+
+def test_kv_slabs_mapped_for_every_runtime_gpu():
+    """The VMM-backed KV slabs grant read/write to every GPU of the runtime
+    (cuMemGetAccess on every mapped chunk), so a cross-GPU push into a
+    survivor's slab, a chunk gather or a KV move never faults. On a one-GPU
+    box: the owner; with >= 2 GPUs: instance 0's slab from GPU 1 as well,
+    after a ring prefill whose K/V rest on instance 0."""
+    import torch
+
+    n_gpu = torch.cuda.device_count()
+    devs = [0, 1] if n_gpu >= 2 else [0, 0]
+    p = prompt(700, 9)
+    rt = abi.Runtime(abi.TINY, 2, devices=devs, kv_capacity=1024)
+    rt.prefill([0], [700], [0, 1], [[(0, 700)]], tokens=p)
+    for dev in sorted(set(devs)):
+        assert rt.slab_access(0, dev), dev
+    st = rt.last_prefill_stats()
+    assert st["ring_volume_tokens"] == 700 and st["extra_migration_tokens"] == 0
+    rt.close()

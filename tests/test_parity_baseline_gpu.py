@@ -99,14 +99,17 @@ def config2_oracle():
     return out
 
 
-@pytest.mark.parametrize("mode", ["d1", "d8_colocated", "d4_domains"])
+@pytest.mark.parametrize("mode", ["d1", "d8_colocated", "d4_domains", "d4_domains_arrival"])
 def test_config2_32k_prefill_vs_oracle(config2_oracle, mode, monkeypatch):
     o = config2_oracle
-    if mode == "d4_domains":
+    monkeypatch.delenv("ESP_RING_ARRIVAL", raising=False)
+    if mode.startswith("d4_domains"):
         monkeypatch.setenv("ESP_DOMAIN_PER_INSTANCE", "1")
+        if mode.endswith("arrival"):  # device-side arrival counters of the push transport
+            monkeypatch.setenv("ESP_RING_ARRIVAL", "1")
     else:
         monkeypatch.delenv("ESP_DOMAIN_PER_INSTANCE", raising=False)
-    d = {"d1": 1, "d8_colocated": 8, "d4_domains": 4}[mode]
+    d = {"d1": 1, "d8_colocated": 8, "d4_domains": 4, "d4_domains_arrival": 4}[mode]
     if d == 1:
         retain = [(0, S2)]
         cap = S2
