@@ -349,7 +349,7 @@ def single_gpu(args, rank, world, dist, fallback_note=None):
         "roofline": {"bound": "tensor", "kernel": "ring_attention_tcgen05",
                      "achieved": att_achieved, "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": att_achieved / tf_sust,
-                     "traffic": ncu_traffic("ring_attention_v2"),
+                     "traffic": ncu_traffic("ring_attention_tcgen05"),
                      "traffic_note": "DRAM bytes per launch from profiles/kernel_traffic.json "
                                      "(ncu --set full, 32K d=1); algorithmic Q+K+V+O = "
                                      f"{4 * S * H * 2:.3e} B",
@@ -467,6 +467,19 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
     att_avg = att_ms / max(att_n, 1)
     att_gbs = (kv_bytes / L) / (att_avg / 1e3) / 1e9
     rt.close()
+    # Weight streaming in the step: the same batch at a 64-token context, where
+    # the KV is negligible and the step is the 196 projection GEMMs (+ LM
+    # head) streaming 13.48 GB of weights; no per-phase events (PDL intact).
+    rt = abi.Runtime(abi.LWM_7B, 1, devices=[int(os.environ.get("LOCAL_RANK", "0"))],
+                     kv_capacity=b * (64 + 2 * args.steps + args.warmup + 8))
+    for r in range(b):
+        rt.prefill([r], [64], [0], [[(0, 64)]], tokens=rng.integers(0, V, 64).astype(np.int32))
+    for _ in range(args.warmup):
+        rt.decode_step([0], [0], list(range(b)))
+    short = statistics.median([rt.decode_step([0], [0], list(range(b)))[2]
+                               for _ in range(max(3, args.steps))])
+    rt.close()
+    w_gbs = w_bytes / (short / 1e3) / 1e9
     wall_step = sum(wall) / len(wall)
     return {"value": b / (step / 1e3), "unit": "tokens/s", "ms_per_step": step,
             "e2e": {"value": b / (wall_step / 1e3), "unit": "tokens/s",
@@ -481,6 +494,10 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
                          "traffic": ncu_traffic("decode_attention_kernel"),
                          "algorithmic": f"K+V bytes of one layer = 2*H*2*sum(ctx) = {kv_bytes / L:.4e} B per launch"},
             "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
+            "weight_streaming": {"ms_per_step": short, "weight_bytes": w_bytes,
+                                 "achieved_gbs": w_gbs, "frac": w_gbs / hbm,
+                                 "config": f"batch {b} x 64-token contexts: the step is the "
+                                           "projection GEMMs + LM head streaming the weights"},
             "phase_ms": {p: round(v[0] / max(len(ms), 1), 4) for p, v in ph.items() if v[1] > 0}}
 
 
@@ -586,6 +603,10 @@ def bench_decode_degrees(abi, args, np, hbm):
         out[str(d)] = {"tokens_per_s": b / (step / 1e3), "ms_per_step": step,
                        "masters": len(masters),
                        "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
+            "weight_streaming": {"ms_per_step": short, "weight_bytes": w_bytes,
+                                 "achieved_gbs": w_gbs, "frac": w_gbs / hbm,
+                                 "config": f"batch {b} x 64-token contexts: the step is the "
+                                           "projection GEMMs + LM head streaming the weights"},
                        "instances": f"{d} co-located on 1 GPU, KV {share} tokens/request/instance"}
     return out
 
@@ -630,7 +651,24 @@ def bench_scale_down(abi, args, np):
     prompt = np.random.default_rng(11).integers(0, V, S).astype(np.int32)
     share = S // d
     spread = [[(i, share) for i in range(d)]]
-    onto2 = [[(0, S // 2), (1, S - S // 2)]]
+    # The reactive baseline as the reference plans it (reactive_migrate,
+    # esp_mechanics.cpp:138-218, through the runtime's restatement): even
+    # shares on every ring member, then the dropped members' tokens move to
+    # the survivors, most-free first.
+    rm = abi.reactive_migrate(list(range(d)), [0, 1], S, {i: S for i in range(d)})
+    assert rm["feasible"] and rm["per_source_headroom"] == share, rm
+    final = dict(rm["final_placement"])
+    onto2 = [[(0, final[0]), (1, final[1])]]
+    moves, deficit = [], {t: final[t] - share for t in (0, 1)}
+    for src in range(2, d):
+        left = share
+        for t in (0, 1):
+            mv = min(left, deficit[t])
+            if mv > 0:
+                moves.append((src, t, mv))
+                deficit[t] -= mv
+                left -= mv
+    assert sum(m[2] for m in moves) == rm["migration_volume"]
     t_spread, t_scale, t_move, rid = [], [], [], 0
     rounds = 5  # one warm-up round, then alternating timed rounds (medians)
     for it in range(rounds):
@@ -641,16 +679,16 @@ def bench_scale_down(abi, args, np):
             if retain is spread:
                 # reactive baseline: move instances 2..7's tokens to 0 / 1
                 t0 = time.perf_counter()
-                for src in range(2, d):
-                    rt.move_kv(rid, src, src % 2, share)
+                for src, dst, mv in moves:
+                    rt.move_kv(rid, src, dst, mv)
                 if it:
                     t_move.append((time.perf_counter() - t0) * 1e3)
                 placement = rt.placement(rid)
-                assert sorted(placement.items()) == [(0, S // 2), (1, S - S // 2)], placement
+                assert placement == final, (placement, final)
             rt.free_request(rid)
             rid += 1
     rt.close()
-    moved = (d - 2) * share
+    moved = rm["migration_volume"]
     med = statistics.median
     extra = med(t_scale) - med(t_spread)
     return {"config": f"LWM-7B {S}-token prefill, ring of {d} co-located instances, "

@@ -86,7 +86,7 @@ void gemm(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
           const GemmEpilogue& ep, cudaStream_t s, int path = kGemmAuto);
 
 // ---- attention ------------------------------------------------------------
-constexpr int kMaxRounds = 8;
+constexpr int kMaxRounds = 16;  // ESP degree of one ring (the reference tests d <= 16)
 
 // One (ring position, request) segment of striped ring attention: the local
 // query stripe rows [q_row0, q_row0+q_len) meet, in round r, the KV stripe

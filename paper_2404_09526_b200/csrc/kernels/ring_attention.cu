@@ -173,7 +173,7 @@ struct Steps {
 
 template <int HD, bool kProf, int kPoly8>
 __global__ void __launch_bounds__(kThreads, 1)
-    ring_attention_v2(const __grid_constant__ CUtensorMap tmQ,
+    ring_attention_tcgen05(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ out,
                       int hidden, const RingSegment* __restrict__ segs,
@@ -609,8 +609,8 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s, uint64_t* prof, const RingWait& wait) {
   using C = Cfg2<HD>;
-  once_per_device(reinterpret_cast<const void*>(ring_attention_v2<HD, kProf, kPoly8>), [] {
-    cudaFuncSetAttribute(ring_attention_v2<HD, kProf, kPoly8>,
+  once_per_device(reinterpret_cast<const void*>(ring_attention_tcgen05<HD, kProf, kPoly8>), [] {
+    cudaFuncSetAttribute(ring_attention_tcgen05<HD, kProf, kPoly8>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const int hidden = heads * HD;
@@ -618,7 +618,7 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
   const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
   const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
-  ring_attention_v2<HD, kProf, kPoly8><<<grid, kThreads, C::kSmem, s>>>(
+  ring_attention_tcgen05<HD, kProf, kPoly8><<<grid, kThreads, C::kSmem, s>>>(
       tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof, wait);
   count_launch();
 }

@@ -235,7 +235,7 @@ def test_lwm7b_layer_shape_vs_oracle():
     check_against_oracle(shape, prompt, toks, lgs)
 
 
-@pytest.mark.parametrize("d", [1, 2, 4, 8])
+@pytest.mark.parametrize("d", [1, 2, 4, 8, 16])
 def test_esp_degree_invariance(d):
     """The same prompt prefilled at ESP degree d (striped ring over d
     co-located instances, retention onto 2 survivors) gives the oracle's
