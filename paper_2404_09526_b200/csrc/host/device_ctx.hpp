@@ -17,6 +17,8 @@
 #include "../kernels/kernels.h"
 #include <cstdlib>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "errors.hpp"
 #include "runtime.hpp"
 
@@ -81,6 +83,15 @@ inline void cuda_ok(cudaError_t e, const char* what) {
     throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
   }
 }
+
+// NVTX range for the duration of a scope (header-only NVTX v3: a no-op
+// unless a profiler injects itself). One range per ABI call and per layer.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct DeviceGuard {
   int prev = -1;

@@ -365,6 +365,7 @@ DeviceCtx& Runtime::device_of(const std::vector<InstanceId>& ids, const char* wh
 
 // ---- prefill -------------------------------------------------------------------
 void Runtime::prefill(const esp_prefill_args& a) {
+  NvtxRange nvtx("esp_prefill");
   const int n = a.n_requests, d = a.dop;
   if (n <= 0 || d <= 0) throw InternalError("prefill plan without requests or instances");
   if (!a.request_ids || !a.input_lens || !a.ring || !a.retain_n || !a.retain_instance ||
@@ -708,6 +709,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
   float* ss2 = fuse ? scratch<float>(dc.ss2, rows) : nullptr;
   const bf16* a_in = fuse ? x : xn;
   for (int l = 0; l < cfg_.layers; ++l) {
+    NvtxRange nvtx_layer("prefill layer");
     const LayerW& w = dc.layers[l];
     if (!fuse) {
       timed(kPhNorm, s, [&] { k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s); });
@@ -752,6 +754,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
 
 // ---- decode ----------------------------------------------------------------------
 void Runtime::decode_step(const esp_decode_args& a) {
+  NvtxRange nvtx("esp_decode_step");
   const int b = a.batch_size;
   const bool has_chunk = a.chunk_tokens > 0;
   if (b <= 0 && !has_chunk) throw InternalError("decode step with neither batch nor chunk");
@@ -1137,6 +1140,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
 
 // ---- KV moves, frees, readback -------------------------------------------------------
 void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t tokens) {
+  NvtxRange nvtx("esp_move_kv");
   RequestRec& rr = req(r);
   InstanceRec& src = inst(from);
   InstanceRec& dst = inst(to);

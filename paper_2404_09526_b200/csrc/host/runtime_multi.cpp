@@ -354,6 +354,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
   // gather-buffer parity (peers may overwrite it once it has completed)
   std::map<int, std::array<cudaEvent_t, 2>> attn_done;
   for (int l = 0; l < cfg_.layers; ++l) {
+    NvtxRange nvtx_layer("prefill layer (cross-domain)");
     const int par = push ? (l & 1) : 0;
     const size_t boff = static_cast<size_t>(par) * rows * H;
     std::map<int, cudaEvent_t> qkv_done;  // push: domain's QKV (and its pushes) of this layer

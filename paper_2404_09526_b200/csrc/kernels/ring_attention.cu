@@ -425,6 +425,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int shift = sg->shift[st.r];
         const int kv_len = sg->kv_len[st.r];
         ESP_PROF_WAIT(0, ptx::mbar_wait(&s_full[t], cnt & 1));
+        // Observe every o_done phase (the previous step's P.V): it completed
+        // before this S did (tcgen05 ops retire in issue order), so this never
+        // blocks, and no barrier phase goes unobserved (compute-sanitizer
+        // synccheck; the lazy rescale below relies on the same ordering).
+        if (cnt > 0) ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
         const uint64_t prof_t_step = kProf ? clock64() : 0;
         ptx::tc_fence_after();
         uint32_t s[128];
