@@ -603,10 +603,6 @@ def bench_decode_degrees(abi, args, np, hbm):
         out[str(d)] = {"tokens_per_s": b / (step / 1e3), "ms_per_step": step,
                        "masters": len(masters),
                        "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
-            "weight_streaming": {"ms_per_step": short, "weight_bytes": w_bytes,
-                                 "achieved_gbs": w_gbs, "frac": w_gbs / hbm,
-                                 "config": f"batch {b} x 64-token contexts: the step is the "
-                                           "projection GEMMs + LM head streaming the weights"},
                        "instances": f"{d} co-located on 1 GPU, KV {share} tokens/request/instance"}
     return out
 
@@ -1035,6 +1031,55 @@ def esp_child(args):
                    "extra_migration_tokens": stats["extra_migration_tokens"]}
     rt.close()
     out["clocks"] = clk.summary()
+    # Migration hidden over NVLink (SURVEY §8 d, a7 vs a8): the same prefill
+    # retaining onto the reactive plan's final placement (proactive: the
+    # ring carries every token past its survivor, extra NVLink bytes 0) vs a
+    # spread placement followed by the reactive baseline's KV moves from the
+    # dropped instances to the survivors (K8 copies between GPUs).
+    try:
+        if n >= 3:
+            rm = abi.reactive_migrate(list(range(n)), [0, 1], S, {i: S for i in range(n)})
+            final = dict(rm["final_placement"])
+            share = rm["per_source_headroom"]
+            spread = [[(i, min(share, S - i * share)) for i in range(n) if S - i * share > 0]]
+            onto2 = [[(0, final[0]), (1, final[1])]]
+            rt = abi.Runtime(abi.LWM_7B, n, devices=devs, kv_capacity=S + 64)
+            t_sp, t_rt, t_mv = [], [], []
+            for it in range(1 + max(2, args.steps)):
+                _, _, t = rt.prefill([2 * it], [S], list(range(n)), onto2, tokens=prompt)
+                rt.free_request(2 * it)
+                if it:
+                    t_rt.append(t)
+                _, _, t = rt.prefill([2 * it + 1], [S], list(range(n)), spread, tokens=prompt)
+                if it:
+                    t_sp.append(t)
+                deficit = {0: final[0] - spread[0][0][1], 1: final[1] - spread[0][1][1]}
+                t0 = time.perf_counter()
+                for src, tok in spread[0][2:]:
+                    left = tok
+                    for dst in (0, 1):
+                        mv = min(left, deficit[dst])
+                        if mv > 0:
+                            rt.move_kv(2 * it + 1, src, dst, mv)
+                            deficit[dst] -= mv
+                            left -= mv
+                if it:
+                    t_mv.append((time.perf_counter() - t0) * 1e3)
+                assert rt.placement(2 * it + 1) == final
+                rt.free_request(2 * it + 1)
+            rt.close()
+            med = statistics.median
+            extra = med(t_rt) - med(t_sp)
+            out["scale_down"] = {
+                "t_prefill_retain_ms": med(t_rt), "t_prefill_spread_ms": med(t_sp),
+                "t_reactive_move_ms": med(t_mv), "moved_tokens": rm["migration_volume"],
+                "moved_bytes": rm["migration_volume"] * 2 * L * H * 2,
+                "move_gbs": rm["migration_volume"] * 2 * L * H * 2 / (med(t_mv) / 1e3) / 1e9,
+                "retention_overhead_pct": 100.0 * extra / med(t_sp),
+                "migration_hidden": max(0.0, min(1.0, 1.0 - extra / med(t_mv))),
+                "config": f"LWM-7B {S}-token prefill over {n} instances, scale-down {n}->2"}
+    except Exception as e:  # report, never hide
+        out["scale_down"] = {"error": str(e)[:300]}
     # N-way multi-master decode: b requests x ctx tokens spread over the n
     # instances (GPUs), every instance a master of b/n requests.
     try:

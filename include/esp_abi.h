@@ -366,6 +366,14 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
                          const void* const* kv_k, const void* const* kv_v,
                          const int32_t* kv_len, const int32_t* origin, void* out,
                          int32_t heads, int32_t head_dim, void* stream);
+/* The same, for kernel timing: stages once, then launches K1 `repeats`
+ * times back to back between CUDA events on `stream`; *ms_per_launch =
+ * their average (staging excluded). */
+int esp_k_ring_attention_timed(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
+                               const void* const* kv_k, const void* const* kv_v,
+                               const int32_t* kv_len, const int32_t* origin, void* out,
+                               int32_t heads, int32_t head_dim, int32_t repeats,
+                               float* ms_per_launch, void* stream);
 
 /* Split-KV paged decode attention + LSE combine over n_chunks chunks of
  * slots: request b's query q[b], chunk c reads slots slot_idx[c][0..n) from

@@ -15,7 +15,8 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libesp_b200.so")
+# ESP_LIB: a kernel-study build of the same library (tools only).
+LIB_PATH = os.environ.get("ESP_LIB") or os.path.join(_HERE, "libesp_b200.so")
 
 ESP_OK = 0
 ESP_ERR_CONFIG = -1
@@ -93,7 +94,8 @@ EXPORTED_SYMBOLS = [
     "esp_check_conservation", "esp_request_tokens", "esp_last_prefill_stats", "esp_read_kv", "esp_capture_attention",
     "esp_captured_attention", "esp_slab_access", "esp_dump_profiles",
     "esp_decode_samples", "esp_fit_cost",
-    "esp_launch_count", "esp_set_profiling", "esp_phase_times", "esp_k_gemm", "esp_k_ring_attention", "esp_k_decode_attention",
+    "esp_launch_count", "esp_set_profiling", "esp_phase_times", "esp_k_gemm", "esp_k_ring_attention", "esp_k_ring_attention_timed",
+    "esp_k_decode_attention",
 ]
 
 
@@ -219,6 +221,11 @@ def lib() -> C.CDLL:
                                            C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                            C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                            C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        h.esp_k_ring_attention_timed.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                                 C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.POINTER(C.c_float), C.c_void_p]
         h.esp_k_decode_attention.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p),
                                              C.POINTER(C.c_void_p),
                                              C.POINTER(C.c_void_p), C.POINTER(C.c_int32),
@@ -711,6 +718,21 @@ def k_ring_attention(q_ptr, q_len, pos_i, kv_k, kv_v, kv_len, origin, out_ptr, h
     og = (C.c_int32 * d)(*origin)
     check(lib().esp_k_ring_attention(q_ptr, q_len, pos_i, d, kk, vv, kl, og, out_ptr, heads,
                                      head_dim, stream))
+
+
+def k_ring_attention_timed(q_ptr, q_len, pos_i, kv_k, kv_v, kv_len, origin, out_ptr, heads,
+                           head_dim, repeats, stream=0) -> float:
+    """K1 launched `repeats` times back to back on staged buffers; returns the
+    average ms per launch (CUDA events, staging excluded)."""
+    d = len(kv_k)
+    kk = (C.c_void_p * d)(*kv_k)
+    vv = (C.c_void_p * d)(*kv_v)
+    kl = (C.c_int32 * d)(*kv_len)
+    og = (C.c_int32 * d)(*origin)
+    ms = C.c_float()
+    check(lib().esp_k_ring_attention_timed(q_ptr, q_len, pos_i, d, kk, vv, kl, og, out_ptr, heads,
+                                           head_dim, repeats, C.byref(ms), stream))
+    return float(ms.value)
 
 
 def k_decode_attention(q_ptr, batch, k_slabs, v_slabs, slot_ptrs, n_slots, chunk_req,

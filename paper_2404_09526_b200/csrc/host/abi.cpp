@@ -425,9 +425,19 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
                          const void* const* kv_k, const void* const* kv_v, const int32_t* kv_len,
                          const int32_t* origin, void* out, int32_t heads, int32_t head_dim,
                          void* stream) {
+  return esp_k_ring_attention_timed(q, q_len, pos_i, d, kv_k, kv_v, kv_len, origin, out, heads,
+                                    head_dim, 1, nullptr, stream);
+}
+
+int esp_k_ring_attention_timed(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
+                               const void* const* kv_k, const void* const* kv_v,
+                               const int32_t* kv_len, const int32_t* origin, void* out,
+                               int32_t heads, int32_t head_dim, int32_t repeats,
+                               float* ms_per_launch, void* stream) {
   // Test hook: stages q and the d KV blocks into one buffer (rows: q, then
   // block 0..d-1) so the production kernel runs on exactly its layout.
   return guarded([&] {
+    if (repeats < 1) throw esp::ConfigError("repeats must be >= 1");
     if (d < 1 || d > esp::k::kMaxRounds) throw esp::ConfigError("d out of range");
     if (!q || !kv_k || !kv_v || !kv_len || !origin || !out) {
       throw esp::ConfigError("ring_attention hook: null argument");
@@ -499,10 +509,27 @@ int esp_k_ring_attention(const void* q, int32_t q_len, int32_t pos_i, int32_t d,
       }
     }
 #endif
-    esp::k::ring_attention(static_cast<bf16*>(Q.p), static_cast<bf16*>(K.p),
-                           static_cast<bf16*>(V.p), static_cast<bf16*>(O.p), nr, nr, heads,
-                           head_dim, segs, wk, n_work, scale, s);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ms_per_launch) {
+      esp::cuda_ok(cudaEventCreate(&e0), "event");
+      esp::cuda_ok(cudaEventCreate(&e1), "event");
+      esp::cuda_ok(cudaEventRecord(e0, s), "event");
+    }
+    for (int i = 0; i < repeats; ++i) {
+      esp::k::ring_attention(static_cast<bf16*>(Q.p), static_cast<bf16*>(K.p),
+                             static_cast<bf16*>(V.p), static_cast<bf16*>(O.p), nr, nr, heads,
+                             head_dim, segs, wk, n_work, scale, s);
+    }
     esp::cuda_ok(cudaGetLastError(), "ring_attention launch");
+    if (ms_per_launch) {
+      esp::cuda_ok(cudaEventRecord(e1, s), "event");
+      esp::cuda_ok(cudaEventSynchronize(e1), "event");
+      float ms = 0.f;
+      esp::cuda_ok(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+      *ms_per_launch = ms / static_cast<float>(repeats);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
     esp::cuda_ok(cudaMemcpyAsync(out, O.p, static_cast<size_t>(q_len) * hidden * 2,
                                  cudaMemcpyDeviceToDevice, s), "d2d");
     esp::cuda_ok(cudaStreamSynchronize(s), "ring_attention hook");

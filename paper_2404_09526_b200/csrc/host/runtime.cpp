@@ -116,12 +116,18 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
         if (a == b) continue;
         int can = 0;
         cudaDeviceCanAccessPeer(&can, a, b);
-        if (can) {
-          DeviceGuard g(a);
-          const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
-          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_ok(e, "peer access");
-          cudaGetLastError();
+        if (!can) {
+          // The cross-GPU executors store into and load from peer memory
+          // (push transport, retention into a remote survivor, K8 moves):
+          // refuse GPUs that cannot reach each other instead of faulting.
+          throw ConfigError("GPU " + std::to_string(a) + " cannot access GPU " +
+                            std::to_string(b) + " (no peer access): one runtime needs "
+                            "NVLink/NVSwitch (or PCIe P2P) between all of its GPUs");
         }
+        DeviceGuard g(a);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_ok(e, "peer access");
+        cudaGetLastError();
       }
     }
     const int64_t bpt = kv_bytes_per_token(cfg.layers, cfg.hidden, cfg.heads, 2);

@@ -638,6 +638,20 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
   // Exponentials computed on the FMA pipe, in eighths of each row's keys
   // (MUFU/FMA balance; 1 in 8 measured best in the step, r01_attn_poly_sweep.txt).
   if (head_dim == 128) {
+#ifdef ESP_STUDY
+    // kernel-study build: ESP_ATTN_POLY = eighths of the exponentials on the FMA pipe
+    static const int poly = [] {
+      const char* e = std::getenv("ESP_ATTN_POLY");
+      return e ? std::atoi(e) : kDefaultPoly8;
+    }();
+    switch (poly) {
+      case 0: launch2<128, kProf, 0>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
+      case 2: launch2<128, kProf, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
+      case 3: launch2<128, kProf, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
+      case 4: launch2<128, kProf, 4>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
+      default: break;
+    }
+#endif
     launch2<128, kProf, kDefaultPoly8>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work,
                                        n_work, scale, s, prof, wait);
   } else if (head_dim == 64) {
