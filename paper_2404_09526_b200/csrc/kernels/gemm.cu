@@ -1084,9 +1084,34 @@ int num_sms() {
 }  // namespace
 
 // bf16 [rows x cols] row-major (row pitch ld elements), box box_rows x 64,
-// 128-byte swizzle (the UMMA K-major SW128 canonical layout).
+// 128-byte swizzle (the UMMA K-major SW128 canonical layout). The encoding
+// is a pure function of its arguments, so it is memoised per host thread: a
+// decode step launches ~200 GEMMs over the same weight and activation
+// buffers, and re-encoding two maps per launch costs host time the PDL
+// chain then waits for.
 CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t ld,
                            int box_rows) {
+  struct Key {
+    const void* base;
+    int64_t rows, cols, ld;
+    int box;
+    bool operator==(const Key& o) const {
+      return base == o.base && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      size_t h = std::hash<const void*>()(k.base);
+      for (int64_t v : {k.rows, k.cols, k.ld, static_cast<int64_t>(k.box)}) {
+        h ^= std::hash<int64_t>()(v) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+      }
+      return h;
+    }
+  };
+  thread_local std::unordered_map<Key, CUtensorMap, Hash> cache;
+  const Key key{base, rows, cols, ld, box_rows};
+  if (auto it = cache.find(key); it != cache.end()) return it->second;
+  if (cache.size() > 8192) cache.clear();
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
@@ -1099,6 +1124,7 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   if (r != CUDA_SUCCESS) {
     throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
   }
+  cache.emplace(key, m);
   return m;
 }
 
