@@ -40,7 +40,7 @@ constexpr int kStages = 2;   // V stages
 constexpr int kKStages = ESP_K1_KSTAGES;  // K stages (3 measured: no gain, 6.91-7.01 vs 6.76-6.96 ms)
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;
-constexpr int kDefaultPoly8 = 1;
+constexpr int kDefaultPoly8 = 2;  // in-step A/B (profiles/r02_poly_ab.txt): 2 > 0 > 1
 
 template <int HD>
 struct Cfg2 {
@@ -636,7 +636,7 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
   if (n_work <= 0) return;
   if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
   // Exponentials computed on the FMA pipe, in eighths of each row's keys
-  // (MUFU/FMA balance; 1 in 8 measured best in the step, r01_attn_poly_sweep.txt).
+  // (MUFU/FMA balance: 2 in 8 measured best in the step in round 2, r02_poly_ab.txt).
   if (head_dim == 128) {
 #ifdef ESP_STUDY
     // kernel-study build: ESP_ATTN_POLY = eighths of the exponentials on the FMA pipe
