@@ -875,7 +875,10 @@ def multi_gpu(args, rank, world, dist, n):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic", "config": workload_config(args, n),
         "roofline": pre["roofline"],
+        "kernels": {"step_tflops_per_gpu": pre["step_tflops_per_gpu"],
+                    "step_frac_of_n_peaks": pre["step_frac_of_n_peaks"]},
         "e2e": pre["e2e"], "gpu_launches": pre["gpu_launches"], "clocks": res["clocks"],
+        "scale_down": res.get("scale_down"),
         "transport": {k: res[k] for k in ("nvlink_p2p", "ring") if k in res},
         "nccl_ring_baseline": nccl,
         "decode": res.get("decode"),
@@ -1022,6 +1025,7 @@ def esp_child(args):
                 "d2h_bytes_per_step": 4},
         "gpu_launches": launches,
         "step_tflops_per_gpu": prefill_flops(S) / (step / 1e3) / 1e12 / n,
+        "step_frac_of_n_peaks": prefill_flops(S) / (step / 1e3) / 1e12 / (n * tf_sust),
         "roofline": {"bound": "tensor", "kernel": "ring_attention_tcgen05 (per GPU)",
                      "achieved": att_tf, "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": att_tf / tf_sust, "traffic": None,

@@ -38,23 +38,8 @@ constexpr int kStages = 2;   // V stages
 #define ESP_K1_KSTAGES 2
 #endif
 constexpr int kKStages = ESP_K1_KSTAGES;  // K stages (3 measured: no gain, 6.91-7.01 vs 6.76-6.96 ms)
-// kHalves = 1: 12 warps — warp 0 TMA producer, 1 MMA issuer, 2 TMEM
-// allocator, 3 idle, then two softmax warpgroups (one per query tile, a
-// thread owns a row's 128 keys), registers moved to them with setmaxnreg.
-// kHalves = 2: 18 warps — warp 0 producer, 1 MMA issuer + TMEM allocator,
-// then four softmax warpgroups of 4 consecutive warps (two per tile, a thread
-// owns 64 keys of a row; the halves exchange the row max through shared
-// memory each step): twice the softmax warps per scheduler to hide MUFU /
-// FMA latency and half the per-thread critical path, at 112 registers each
-// (65536 / 576) without setmaxnreg.
-template <int kHalves>
-__host__ __device__ constexpr int threads_of() { return kHalves == 1 ? 384 : 576; }
-template <int kHalves>
-__host__ __device__ constexpr uint32_t soft_warp0() { return kHalves == 1 ? 4 : 2; }
-template <int kHalves>
-__host__ __device__ constexpr uint32_t alloc_warp() { return kHalves == 1 ? 2 : 1; }
+constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;
-constexpr int kDefaultHalves = 1;
 constexpr int kDefaultPoly8 = 2;  // in-step A/B (profiles/r02_poly_ab.txt): 2 > 0 > 1
 
 template <int HD>
@@ -62,11 +47,7 @@ struct Cfg2 {
   static constexpr int kBoxes = HD / 64;
   static constexpr int kQBytes = BM * HD * 2;
   static constexpr int kKvBytes = BN * HD * 2;
-  // + the split softmax's row-max / row-sum exchange: [2 parities][2 tiles]
-  // [2 halves][128 rows] floats
-  static constexpr int kXchgBytes = 2 * 2 * 2 * BM * 4;
-  static constexpr int kSmem =
-      2 * kQBytes + (kKStages + kStages) * kKvBytes + 1024 + 512 + kXchgBytes;
+  static constexpr int kSmem = 2 * kQBytes + (kKStages + kStages) * kKvBytes + 1024 + 512;
 };
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): half the FMA-pipe
@@ -190,8 +171,8 @@ struct Steps {
     }                                              \
   } while (0)
 
-template <int HD, bool kProf, int kPoly8, int kHalves>
-__global__ void __launch_bounds__(threads_of<kHalves>(), 1)
+template <int HD, bool kProf, int kPoly8>
+__global__ void __launch_bounds__(kThreads, 1)
     ring_attention_tcgen05(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ out,
@@ -225,7 +206,6 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
   uint64_t* o_done = p_full + 4;         // [2]
   uint64_t* o_free = o_done + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
-  float* xchg = reinterpret_cast<float*>(bars + 64);  // [parity][tile][half][row]
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   if (warp == 0 && lane == 0) {
@@ -247,11 +227,11 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
       ptx::mbar_init(&p_full[2 * t], 128);
       ptx::mbar_init(&p_full[2 * t + 1], 128);
       ptx::mbar_init(&o_done[t], 1);
-      ptx::mbar_init(&o_free[t], 128 * kHalves);
+      ptx::mbar_init(&o_free[t], 128);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == alloc_warp<kHalves>()) ptx::tmem_alloc<512>(tmem_slot);
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -264,8 +244,8 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
   const uint32_t t_s[2] = {tmem, tmem + BN};
   const uint32_t t_o[2] = {tmem + 2 * BN, tmem + 2 * BN + HD};
 
-  if (warp < soft_warp0<kHalves>()) {
-    if constexpr (kHalves == 1) ptx::setmaxnreg_dec<104>();
+  if (warp < 4) {
+    ptx::setmaxnreg_dec<104>();
     if (warp == 0 && lane == 0) {
       // ---------------------------------------------------------- producer
       int ks = 0, vs = 0;
@@ -389,11 +369,7 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
                 for (int k = 4 * half; k < 4 * half + 4; ++k) {
                   const uint64_t dv = ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024);
                   if (leader) {
-                    // P of keys [16k, 16k+16): packed over the first 32
-                    // columns of S (kHalves = 1) or over the first 32
-                    // columns of each key half's own 64 (kHalves = 2)
-                    const uint32_t pcol = kHalves == 1 ? k * 8 : (k >> 2) * 64 + (k & 3) * 8;
-                    ptx::umma_f16_ts(t_o[t], t_s[t] + pcol, dv, idesc_o,
+                    ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8, dv, idesc_o,
                                      (!first_pv[t] || k != 0) ? 1u : 0u);
                   }
                 }
@@ -425,118 +401,15 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
       if (lane == 0) prof_store(1);
     }
   } else {
-    if constexpr (kHalves == 1) ptx::setmaxnreg_inc<192>();
+    ptx::setmaxnreg_inc<192>();
     // ------------------------------------------------------------ softmax
-    // Warpgroup sw = warp/4 - 1 handles query tile t = sw & 1 and key half
-    // h = sw >> 1 (kHalves = 2) of every S tile; with kHalves = 1 one
-    // warpgroup per tile owns all 128 keys.
-    constexpr int NC = BN / kHalves;  // S columns (keys) per thread per step
-    const int sw = static_cast<int>((warp - soft_warp0<kHalves>()) >> 2);
-    const int t = sw & 1;
-    const int h = kHalves == 2 ? (sw >> 1) : 0;
+    const int t = (warp >= 8) ? 1 : 0;
     // this tile's TMEM columns (runtime t: no array indexing -> no local memory)
     const uint32_t ts_t = tmem + t * BN, to_t = tmem + 2 * BN + t * HD;
     const uint32_t quad = warp & 3;
     const int row = static_cast<int>(quad * 32 + lane);
     const uint32_t lane_off = (quad * 32) << 16;
-    // exchange slots of this thread's row (kHalves = 2): own / partner half
-    auto xslot = [&](int par, int half) { return xchg + ((par * 2 + t) * 2 + half) * BM + row; };
     uint32_t cnt = 0;
-    // One softmax step of a key half (kHalves = 2), in two 32-key chunks so a
-    // thread holds 32 S values at a time (registers: 112 per thread at 18
-    // warps). Pass 1 reads S for the half's partial row max, the halves
-    // exchange it; pass 2 re-reads S (TMEM reads are cheap), exponentiates
-    // and packs P into the first 32 columns of the half's OWN 64 (no half
-    // overwrites S the other still reads).
-    const uint32_t s_half = ts_t + lane_off + h * NC;
-    auto split_step = [&](int b0, int shift, int kv_len, int a, float& m_run, float& l_run,
-                          int j) {
-      const int lim = min(a - shift - b0, kv_len - 1 - b0);  // key b0 + c visible iff c <= lim
-      ptx::tc_fence_after();
-      float mx = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(s_half + 32 * k, v);
-        ptx::tmem_wait_ld();
-        float m8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float x0 = 32 * k + e <= lim ? __uint_as_float(v[e]) : -INFINITY;
-          float x1 = 32 * k + 8 + e <= lim ? __uint_as_float(v[8 + e]) : -INFINITY;
-          float x2 = 32 * k + 16 + e <= lim ? __uint_as_float(v[16 + e]) : -INFINITY;
-          float x3 = 32 * k + 24 + e <= lim ? __uint_as_float(v[24 + e]) : -INFINITY;
-          m8[e] = fmax3(fmaxf(x0, x1), x2, x3);
-        }
-        mx = fmax3(mx, fmax3(m8[0], m8[1], m8[2]),
-                   fmax3(fmaxf(m8[3], m8[4]), fmaxf(m8[5], m8[6]), m8[7]));
-      }
-      // the row max over both key halves (slots double-buffered by step parity)
-      *xslot(cnt & 1, h) = mx;
-      ptx::named_bar_sync(1 + t, 256);
-      mx = fmaxf(mx, *xslot(cnt & 1, h ^ 1));
-      const float m_tile = mx * scale_log2;
-      const float m_new = fmaxf(m_run, m_tile);
-      const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY)
-                                             : (m_new > m_run + kRescaleThreshold);
-      float alpha = 1.f;
-      if (need) {
-        alpha = m_run == -INFINITY ? 0.f : ptx::ex2(m_run - m_new);
-        m_run = m_new;
-      }
-      const float m_sub = m_run == -INFINITY ? 0.f : m_run;
-      if (j > 0 && __any_sync(0xffffffff, need)) {
-        ptx::tc_fence_after();
-#pragma unroll 1
-        for (int c = h * (HD / 2); c < (h + 1) * (HD / 2); c += 32) {
-          uint32_t o[32];
-          ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          ptx::tmem_st_32x32b_x32(to_t + lane_off + c, o);
-        }
-      }
-      const uint64_t scale2 = f2pack(scale_log2, scale_log2);
-      const uint64_t negm2 = f2pack(-m_sub, -m_sub);
-      uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(s_half + 32 * k, v);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int key = 32 * k + 2 * c;
-          const float s0 = key <= lim ? __uint_as_float(v[2 * c]) : -INFINITY;
-          const float s1 = key + 1 <= lim ? __uint_as_float(v[2 * c + 1]) : -INFINITY;
-          float x0, x1, p0, p1;
-          f2unpack(ffma2(f2pack(s0, s1), scale2, negm2), x0, x1);
-          if ((((16 * k + c) * kPoly8) & 7) < kPoly8) {
-            exp2_fma2(x0, x1, p0, p1);
-          } else {
-            p0 = ptx::ex2(x0);
-            p1 = ptx::ex2(x1);
-          }
-          if (c & 1) {
-            sum2b = fadd2(sum2b, f2pack(p0, p1));
-          } else {
-            sum2a = fadd2(sum2a, f2pack(p0, p1));
-          }
-          pk[c] = ptx::pack_bf16(p0, p1);
-        }
-        // packed P of keys [32k, 32k+32) of this half -> columns [16k, 16k+16)
-        // of the half's own region (S chunk 0 there is consumed by now)
-        ptx::tmem_st_32x32b_x16(s_half + 16 * k, pk);
-      }
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&p_full[2 * t + h]);
-      float sa0, sa1;
-      f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
-      l_run = l_run * alpha + (sa0 + sa1);
-    };
     for (int w = w_begin; w < w_end; ++w) {
       const Item it = load_item(work, w, segs);
       if (t == 1 && !it.act1) continue;
@@ -548,7 +421,7 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
       Steps st;
       for (st.begin(sg, it); st.valid(); st.next()) {
         if (t == 0 && !st.active0()) continue;
-        const int b0 = st.tt * BN + h * NC;  // first key of this thread's columns
+        const int b0 = st.tt * BN;
         const int shift = sg->shift[st.r];
         const int kv_len = sg->kv_len[st.r];
         ESP_PROF_WAIT(0, ptx::mbar_wait(&s_full[t], cnt & 1));
@@ -559,25 +432,19 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
         if (cnt > 0) ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
         const uint64_t prof_t_step = kProf ? clock64() : 0;
         ptx::tc_fence_after();
-        if constexpr (kHalves == 2) {
-          split_step(b0, shift, kv_len, a, m_run, l_run, j);
-          ++cnt;
-          ++j;
-          continue;
-        }
-        uint32_t s[NC];
+        uint32_t s[128];
 #pragma unroll
-        for (int c = 0; c < NC / 32; ++c) {
+        for (int c = 0; c < 4; ++c) {
           uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]);
-          ptx::tmem_ld_32x32b_x32(ts_t + lane_off + h * NC + 32 * c, chunk);
+          ptx::tmem_ld_32x32b_x32(ts_t + lane_off + 32 * c, chunk);
         }
         ptx::tmem_wait_ld();
         if constexpr (kProf) prof_acc[2] += clock64() - prof_t_step;  // S readback
-        const bool full_tile = (b0 + NC - 1 <= q0 - shift) && (b0 + NC <= kv_len);
+        const bool full_tile = (b0 + BN - 1 <= q0 - shift) && (b0 + BN <= kv_len);
         const int lim = min(a - shift - b0, kv_len - 1 - b0);  // visible iff c <= lim
         if (!full_tile) {
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
+          for (int c = 0; c < 128; ++c) {
             if (c > lim) s[c] = __float_as_uint(-INFINITY);
           }
         }
@@ -587,10 +454,10 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             mx8[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]),
-                           __uint_as_float(s[NC - 8 + k]));
+                           __uint_as_float(s[120 + k]));
           }
 #pragma unroll
-          for (int c = 16; c < NC - 8; c += 16) {
+          for (int c = 16; c < 120; c += 16) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               mx8[k] = fmax3(mx8[k], __uint_as_float(s[c + k]), __uint_as_float(s[c + 8 + k]));
@@ -599,13 +466,13 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
           return fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
                        fmaxf(mx8[6], mx8[7]));
         };
-        // O *= f in TMEM (this thread's HD / kHalves columns). O holds
-        // PV_{j-1}, complete (o_done observed above); rare: a row max grew
-        // past the threshold.
+        // O *= f in TMEM. O holds PV_{j-1}, complete once o_done of the
+        // previous step fired (rare: a row max grew past the threshold).
         auto rescale_o = [&](float f) {
+          ptx::mbar_wait(&o_done[t], (cnt - 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll 1
-          for (int c = h * (HD / kHalves); c < (h + 1) * (HD / kHalves); c += 32) {
+          for (int c = 0; c < HD; c += 32) {
             uint32_t o[32];
             ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
             ptx::tmem_wait_ld();
@@ -615,7 +482,7 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
           }
         };
         // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
-        // precede the write of s[c], c <= 2c), then P over S_t in TMEM, in
+        // precede the write of s[c], c <= 2c), then P over S_t in TMEM, in two
         // halves of 64 keys: the MMA warp starts PV on keys 0..63 while keys
         // 64..127 are still being exponentiated.
         const uint64_t scale2 = f2pack(scale_log2, scale_log2);
@@ -642,10 +509,9 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
             s[c] = ptx::pack_bf16(p0, p1);
           }
         };
-        // packed P of key half `half` -> TMEM columns [32 half, 32 half + 32)
-        auto store_half = [&](int half, int src) {
+        auto store_half = [&](int half) {
           ptx::tmem_st_32x32b_x32(ts_t + lane_off + 32 * half,
-                                  *reinterpret_cast<uint32_t(*)[32]>(&s[src]));
+                                  *reinterpret_cast<uint32_t(*)[32]>(&s[32 * half]));
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           ptx::mbar_arrive(&p_full[2 * t + half]);
@@ -655,7 +521,7 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
         // first half's P store and arrive.
         auto pin_half1 = [&]() {
 #pragma unroll
-          for (int c = 64; c < NC; c += 16) {
+          for (int c = 64; c < 128; c += 16) {
             asm volatile(""
                          : "+r"(s[c]), "+r"(s[c + 1]), "+r"(s[c + 2]), "+r"(s[c + 3]),
                            "+r"(s[c + 4]), "+r"(s[c + 5]), "+r"(s[c + 6]), "+r"(s[c + 7]),
@@ -678,10 +544,10 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
           const float m_sub = m_run == -INFINITY ? 0.f : m_run;
           if (j > 0 && __any_sync(0xffffffff, need)) rescale_o(alpha);
           exp_half(0, m_sub);
-          store_half(0, 0);
+          store_half(0);
           pin_half1();
           exp_half(1, m_sub);
-          store_half(1, 32);
+          store_half(1);
           if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P stored
           float sa0, sa1;
           f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
@@ -697,22 +563,11 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
       // Final O / l for this tile's rows.
       ESP_PROF_WAIT(6, ptx::mbar_wait(&o_done[t], (cnt - 1) & 1));
       ptx::tc_fence_after();
-      float l_tot = l_run;
-      if constexpr (kHalves == 2) {
-        // both halves' partial row sums, through the parity the LAST step did
-        // not use (the partner read it before passing the last step's
-        // barrier, so it is free; the last step's own parity may still be
-        // being read)
-        *xslot(cnt & 1, h) = l_run;
-        ptx::named_bar_sync(1 + t, 256);
-        l_tot += *xslot(cnt & 1, h ^ 1);
-        ptx::named_bar_sync(1 + t, 256);  // read before the next item's max reuses the slot
-      }
       const bool valid = a < sg->q_len;
-      const float inv_l = l_tot > 0.f ? 1.f / l_tot : 0.f;
+      const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
       bf16* orow = out + static_cast<int64_t>(sg->q_row0 + a) * hidden + it.head * HD;
 #pragma unroll 1
-      for (int c = h * (HD / kHalves); c < (h + 1) * (HD / kHalves); c += 32) {
+      for (int c = 0; c < HD; c += 32) {
         uint32_t o[32];
         ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
         ptx::tmem_wait_ld();
@@ -734,11 +589,11 @@ __global__ void __launch_bounds__(threads_of<kHalves>(), 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&o_free[t]);
     }
-    if (quad == 0 && lane == 0 && h == 0) prof_store(2 + t);
+    if (quad == 0 && lane == 0) prof_store(2 + t);
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == alloc_warp<kHalves>()) {
+  if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
@@ -754,21 +609,21 @@ int sm_count2() {
   return n;
 }
 
-template <int HD, bool kProf, int kPoly8, int kHalves = kDefaultHalves>
+template <int HD, bool kProf, int kPoly8>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s, uint64_t* prof, const RingWait& wait) {
   using C = Cfg2<HD>;
-  auto* kern = ring_attention_tcgen05<HD, kProf, kPoly8, kHalves>;
-  once_per_device(reinterpret_cast<const void*>(kern), [kern] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  once_per_device(reinterpret_cast<const void*>(ring_attention_tcgen05<HD, kProf, kPoly8>), [] {
+    cudaFuncSetAttribute(ring_attention_tcgen05<HD, kProf, kPoly8>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const int hidden = heads * HD;
   const CUtensorMap tq = make_tmap_bf16(q, q_rows, hidden, hidden, BM);
   const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
   const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
-  kern<<<grid, threads_of<kHalves>(), C::kSmem, s>>>(
+  ring_attention_tcgen05<HD, kProf, kPoly8><<<grid, kThreads, C::kSmem, s>>>(
       tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof, wait);
   count_launch();
 }
@@ -784,24 +639,11 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
   // (MUFU/FMA balance: 2 in 8 measured best in the step in round 2, r02_poly_ab.txt).
   if (head_dim == 128) {
 #ifdef ESP_STUDY
-    // kernel-study build: ESP_ATTN_POLY = eighths of the exponentials on the
-    // FMA pipe; ESP_ATTN_HALVES = softmax warpgroups per query tile
+    // kernel-study build: ESP_ATTN_POLY = eighths of the exponentials on the FMA pipe
     static const int poly = [] {
       const char* e = std::getenv("ESP_ATTN_POLY");
       return e ? std::atoi(e) : kDefaultPoly8;
     }();
-    static const int halves = [] {
-      const char* e = std::getenv("ESP_ATTN_HALVES");
-      return e ? std::atoi(e) : kDefaultHalves;
-    }();
-    if (halves == 2 && poly == 2) {
-      launch2<128, kProf, 2, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait);
-      return;
-    }
-    if (halves == 2 && poly == 1) {
-      launch2<128, kProf, 1, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait);
-      return;
-    }
     switch (poly) {
       case 0: launch2<128, kProf, 0>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
       case 2: launch2<128, kProf, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
