@@ -306,6 +306,62 @@ def test_config5_mixed_trace_tiny():
     assert stats["decode_tok"] >= 2027
 
 
+def test_config5_mixed_trace_lwm7b_geometry(transport):
+    """BASELINE config 5 at LWM-7B layer geometry (H=4096, 32 x 128 heads,
+    FFN 11008, V=32000; 2 of the 32 layers so the trace's resident KV fits one
+    GPU): the reference ESP scheduler's decisions on the mixed trace (24
+    requests of 5..311,945 tokens, 8 instances x 317,000 slots) executed with
+    the production kernels. Page tables equal the engine's at every
+    schedule(); the short requests' first tokens and logits match the dense
+    oracle (bf16-emulation mode)."""
+    if transport != "colocated":
+        pytest.skip("one transport mode is enough at 7B geometry (the tiny replay covers all)")
+    shape = abi.ModelShape(layers=2, hidden=4096, heads=32, head_dim=128, ffn=11008,
+                           vocab=32000)
+    path = os.path.join(GOLD, "scenario_config5_mixed.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(shape, head["instances"], devices=devices(head["instances"]),
+                     kv_capacity=head["kv_capacity"])
+    lens = {r["id"]: r["input_len"] for r in head["requests"]}
+    checked = {r for r, n in lens.items() if 20 <= n <= 600}
+    logits = {r: [] for r in checked}
+    tokens = {r: [] for r in checked}
+    stats = {"prefill_tok": 0, "prefill_ms": 0.0, "decode_tok": 0, "decode_ms": 0.0}
+
+    def on_prefill(p, retain):
+        toks = np.concatenate([replay.prompt_tokens(r, n) for r, n in zip(p["requests"], p["input_lens"])])
+        want = any(r in checked for r in p["requests"])
+        first, lg, ms = rt.prefill(p["requests"], p["input_lens"], p["instances"], retain,
+                                   tokens=toks, want_logits=want)
+        stats["prefill_tok"] += int(sum(p["input_lens"]))
+        stats["prefill_ms"] += ms
+        for i, r in enumerate(p["requests"]):
+            if r in checked:
+                logits[r].append(lg[i])
+                tokens[r].append(int(first[i]))
+
+    def on_decode(d, members):
+        want = any(r in checked and len(logits[r]) <= 2 for r in d["batch"])
+        out, lg, ms = rt.decode_step(members, d["masters"], d["batch"], want_logits=want)
+        stats["decode_tok"] += len(d["batch"])
+        stats["decode_ms"] += ms
+        for i, r in enumerate(d["batch"]):
+            if r in checked and len(logits[r]) <= 2:
+                logits[r].append(lg[i])
+                tokens[r].append(int(out[i]))
+
+    replay.replay(rt, path, on_prefill=on_prefill, on_decode=on_decode)
+    rt.check_conservation()
+    rt.close()
+    assert checked
+    for r in sorted(checked):
+        check_against_oracle(shape, replay.prompt_tokens(r, lens[r]), tokens[r], logits[r])
+    print(f"config5 LWM-7B geometry (2 layers): prefill {stats['prefill_tok']} tok in "
+          f"{stats['prefill_ms']:.1f} ms, decode {stats['decode_tok']} tok in "
+          f"{stats['decode_ms']:.1f} ms")
+    assert stats["decode_tok"] >= 2027
+
+
 def test_chunked_prefill_baseline_tiny(transport):
     """SURVEY §8 f3, chunked prefill (policies.cpp:297-405): the reference's
     "chunked:512" decisions, where 512-token prompt chunks ride on decode
