@@ -79,8 +79,61 @@ static float* make_weight(const llama_cfg* c, int tensor, int layer, int64_t row
   return w;
 }
 
-/* Y[t][o] = sum_k X[t][k] * W[o][k]  (nn.Linear layout), 4x4 register blocks. */
+/* Y[t][o] = sum_k X[t][k] * W[o][k] for many rows: W transposed once into
+ * WT[k][o] (o padded to 16), then per 16-output panel (a thread's WT panel
+ * stays in its L2 while it walks every row block) a 6 x 16 register tile
+ * accumulates X[t][k] * WT[k][o..o+15] over k. */
+#define GEMM_MR 6
+#define GEMM_NR 16
+static void gemm_nt_panels(const float* X, int64_t T, int64_t K, const float* W, int64_t O,
+                           float* Y) {
+  const int64_t Op = (O + GEMM_NR - 1) / GEMM_NR * GEMM_NR;
+  float* WT = (float*)malloc(sizeof(float) * K * Op);
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t kb = 0; kb < K; kb += 32) {
+    for (int64_t ob = 0; ob < Op; ob += 32) {
+      for (int64_t k = kb; k < kb + 32 && k < K; ++k) {
+        for (int64_t o = ob; o < ob + 32 && o < Op; ++o) {
+          WT[k * Op + o] = o < O ? W[o * K + k] : 0.f;
+        }
+      }
+    }
+  }
+  const int64_t np = Op / GEMM_NR;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t p = 0; p < np; ++p) {
+    const int64_t o0 = p * GEMM_NR;
+    for (int64_t t0 = 0; t0 < T; t0 += GEMM_MR) {
+      float acc[GEMM_MR][GEMM_NR];
+      const float* xr[GEMM_MR];
+      for (int r = 0; r < GEMM_MR; ++r) {
+        xr[r] = X + (t0 + r < T ? t0 + r : t0) * K;
+        for (int c = 0; c < GEMM_NR; ++c) acc[r][c] = 0.f;
+      }
+      const float* wk = WT + o0;
+      for (int64_t k = 0; k < K; ++k, wk += Op) {
+#pragma GCC unroll 6
+        for (int r = 0; r < GEMM_MR; ++r) {
+          const float xv = xr[r][k];
+#pragma omp simd
+          for (int c = 0; c < GEMM_NR; ++c) acc[r][c] += xv * wk[c];
+        }
+      }
+      for (int r = 0; r < GEMM_MR && t0 + r < T; ++r) {
+        for (int c = 0; c < GEMM_NR && o0 + c < O; ++c) Y[(t0 + r) * O + o0 + c] = acc[r][c];
+      }
+    }
+  }
+  free(WT);
+}
+
+/* Y[t][o] = sum_k X[t][k] * W[o][k]  (nn.Linear layout). Few rows (decode,
+ * LM head of one row): 4x4 blocks of dot products, the weights streamed once. */
 static void gemm_nt(const float* X, int64_t T, int64_t K, const float* W, int64_t O, float* Y) {
+  if (T >= 64) {
+    gemm_nt_panels(X, T, K, W, O, Y);
+    return;
+  }
   const int64_t tb = (T + 3) / 4, ob = (O + 3) / 4;
 #pragma omp parallel for collapse(2) schedule(dynamic, 4)
   for (int64_t oi = 0; oi < ob; ++oi) {

@@ -43,9 +43,12 @@ def test_decode_cached_matches_generate():
     assert t == tok[1]
     assert np.array_equal(l, lg[1])
     # the step's own K/V row equals what a prefill of prompt + token caches
+    # (up to summation order: the many-row prefill GEMM blocks differently,
+    # and bf16 rounding of K/V may flip a last bit)
     full = np.concatenate([prompt, [tok[0]]]).astype(np.int32)
     _, _, _, K2, V2 = llama_ref.prefill_probe(shape, full, kv_pos=[S])
-    assert np.array_equal(kn, K2[:, 0]) and np.array_equal(vn, V2[:, 0])
+    for a, b in ((kn, K2[:, 0]), (vn, V2[:, 0])):
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 5e-3
 
 
 def test_fp32_mode_is_the_unrounded_forward():
