@@ -338,9 +338,11 @@ int esp_fit_cost(const double* x1, const double* x2, const double* y, int64_t n,
 /* Per-phase device timing (CUDA events around each launch on the runtime's
  * stream) while profiling is on. Phases: 0 embed, 1 rmsnorm, 2 QKV GEMM(+RoPE
  * +ring write+retention), 3 ring attention, 4 O GEMM, 5 gate_up GEMM, 6 down
- * GEMM, 7 LM head, 8 argmax, 9 decode attention, 10 LSE combine.
+ * GEMM, 7 LM head, 8 argmax, 9 decode attention, 10 LSE combine; and, always
+ * recorded, 11 host enqueue (host wall ms of each single-domain prefill /
+ * decode step from the call's entry to its last stream operation).
  * esp_phase_times returns and resets the accumulated ms / launch counts. */
-#define ESP_N_PHASES 11
+#define ESP_N_PHASES 12
 int esp_set_profiling(esp_runtime* rt, int32_t on);
 int esp_phase_times(esp_runtime* rt, double* ms, int64_t* launches, int32_t n);
 

@@ -649,7 +649,8 @@ class Runtime:
         return bool(ok.value)
 
     PHASES = ["embed", "rmsnorm", "qkv_gemm", "ring_attention", "o_gemm", "gate_up_gemm",
-              "down_gemm", "lm_head", "argmax", "decode_attention", "lse_combine"]
+              "down_gemm", "lm_head", "argmax", "decode_attention", "lse_combine",
+              "host_enqueue"]
 
     def set_profiling(self, on: bool):
         check(lib().esp_set_profiling(self._h, 1 if on else 0))

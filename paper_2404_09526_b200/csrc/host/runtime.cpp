@@ -372,6 +372,7 @@ DeviceCtx& Runtime::device_of(const std::vector<InstanceId>& ids, const char* wh
 // ---- prefill -------------------------------------------------------------------
 void Runtime::prefill(const esp_prefill_args& a) {
   NvtxRange nvtx("esp_prefill");
+  const auto host_t0 = std::chrono::steady_clock::now();
   const int n = a.n_requests, d = a.dop;
   if (n <= 0 || d <= 0) throw InternalError("prefill plan without requests or instances");
   if (!a.request_ids || !a.input_lens || !a.ring || !a.retain_n || !a.retain_instance ||
@@ -626,6 +627,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
   int32_t* d_out = scratch<int32_t>(dc.out_tok, n);
   timed(kPhArgmax, s, [&] { k::argmax_rows(logits, n, cfg_.vocab, d_out, s); });
   cuda_ok(cudaEventRecord(dc.e1, s), "event");
+  note_host_enqueue(host_t0);
   check_cuda("prefill launch");
   std::vector<int32_t> first(static_cast<size_t>(n));
   cuda_ok(cudaMemcpyAsync(first.data(), d_out, n * 4, cudaMemcpyDeviceToHost, s), "d2h");
@@ -761,6 +763,7 @@ void Runtime::forward_layers_prefill(DeviceCtx& dc, int rows,
 // ---- decode ----------------------------------------------------------------------
 void Runtime::decode_step(const esp_decode_args& a) {
   NvtxRange nvtx("esp_decode_step");
+  const auto host_t0 = std::chrono::steady_clock::now();
   const int b = a.batch_size;
   const bool has_chunk = a.chunk_tokens > 0;
   if (b <= 0 && !has_chunk) throw InternalError("decode step with neither batch nor chunk");
@@ -1100,6 +1103,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
     timed(kPhArgmax, s, [&] { k::argmax_rows(logits, n_out, cfg_.vocab, d_out, s); });
   }
   cuda_ok(cudaEventRecord(dc.e1, s), "event");
+  note_host_enqueue(host_t0);
   check_cuda("decode launch");
   std::vector<int32_t> out(static_cast<size_t>(std::max(n_out, 1)));
   if (n_out > 0) {

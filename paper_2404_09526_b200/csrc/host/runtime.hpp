@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+
 #include <cstdint>
 #include <cstdlib>
 #include <map>
@@ -125,7 +127,7 @@ class Runtime {
   // Phases of the data path timed with CUDA events when profiling is on.
   enum Phase {
     kPhEmbed = 0, kPhNorm, kPhQkv, kPhAttention, kPhOProj, kPhGateUp, kPhDown, kPhLmHead,
-    kPhArgmax, kPhDecodeAttn, kPhCombine, kPhCount
+    kPhArgmax, kPhDecodeAttn, kPhCombine, kPhHostEnqueue, kPhCount
   };
 
  private:
@@ -207,6 +209,13 @@ class Runtime {
   template <typename F>
   void timed(int phase, cudaStream_t s, F&& f);
   void collect_phase_events();
+  // Host wall ms from a call's entry to its last stream operation (phase
+  // kPhHostEnqueue, recorded whether or not profiling is on).
+  void note_host_enqueue(std::chrono::steady_clock::time_point t0) {
+    phase_ms_[kPhHostEnqueue] +=
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    phase_n_[kPhHostEnqueue] += 1;
+  }
   void* upload(DeviceCtx& dc, const void* src, size_t bytes);
   void check_cuda(const char* what);
 
