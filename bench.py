@@ -712,9 +712,12 @@ def bench_transport(abi, args, np):
     """Cross-domain ESP transport on one GPU (ESP_DOMAIN_PER_INSTANCE=1: every
     instance its own domain, the multi-GPU code path): a d-instance ring
     prefill with the fused push (K/V all-gather + retention as peer stores in
-    the QKV epilogue) vs the copy-engine ring (ESP_RING_COPY). Both move the
-    same (d-1)/d of every K/V block per domain; on one GPU the 'peer' is HBM,
-    so this measures transport overhead, not NVLink bandwidth."""
+    the QKV epilogue) vs the copy-engine ring (ESP_RING_COPY) vs the windowed
+    ring (ESP_RING_WINDOW: own block + 2 receive slots per GPU, one K1 launch
+    per round with the softmax state carried). All move the same (d-1)/d of
+    every K/V block per domain; on one GPU the 'peer' is HBM, so this
+    measures transport overhead, not NVLink bandwidth. kv_ring_rows = K/V
+    ring-buffer rows one GPU holds."""
     S, d = min(args.seq, 16384), 4
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     prompt = np.random.default_rng(13).integers(0, V, S).astype(np.int32)
@@ -724,14 +727,16 @@ def bench_transport(abi, args, np):
                      f"each (one GPU)",
            "ring_bytes_per_layer": (d - 1) * S * H * 2 * 2}
     saved = {k: os.environ.get(k) for k in ("ESP_DOMAIN_PER_INSTANCE", "ESP_RING_COPY",
-                                            "ESP_DECODE_COPY")}
+                                            "ESP_DECODE_COPY", "ESP_RING_WINDOW")}
     try:
         os.environ["ESP_DOMAIN_PER_INSTANCE"] = "1"
-        for mode in ("push", "copy"):
+        for mode in ("push", "copy", "window"):
+            os.environ.pop("ESP_RING_COPY", None)
+            os.environ.pop("ESP_RING_WINDOW", None)
             if mode == "copy":
                 os.environ["ESP_RING_COPY"] = "1"
-            else:
-                os.environ.pop("ESP_RING_COPY", None)
+            elif mode == "window":
+                os.environ["ESP_RING_WINDOW"] = "1"
             rt = abi.Runtime(abi.LWM_7B, d, devices=[dev] * d, kv_capacity=share + 64)
             ms = []
             for k in range(2):
@@ -739,9 +744,11 @@ def bench_transport(abi, args, np):
                 rt.free_request(k)
                 if k:
                     ms.append(t)
+            out[f"{mode}_kv_ring_rows"] = rt.last_prefill_stats()["kv_ring_rows"]
             rt.close()
             out[f"{mode}_ms"] = ms[0]
             out[f"{mode}_tokens_per_s"] = S / (ms[0] / 1e3)
+        os.environ.pop("ESP_RING_WINDOW", None)
         # Fused-push prefill across d domains (d = 2 / 4 / 8) against the
         # same ring co-located: the cost of the cross-domain executor.
         os.environ.pop("ESP_RING_COPY", None)

@@ -51,7 +51,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define ESP_ABI_VERSION 2
+#define ESP_ABI_VERSION 3
 
 /* ---- error codes (reference types.hpp:48-109) --------------------------- */
 enum esp_status {
@@ -281,7 +281,12 @@ int esp_request_tokens(const esp_runtime* rt, int64_t request, int32_t* out, int
  *   transient_buffer_tokens  ceil(sum / d), the circulating stripe
  *   extra_migration_tokens   0 whenever the resting instances are ring
  *                            members (retention rides the ring), else -1
- *   device_ms                device time of the pass (max over GPUs) */
+ *   device_ms                device time of the pass (max over GPUs)
+ *   kv_ring_rows             (ABI 3) K/V rows of ring buffer one GPU held
+ *                            (max over GPUs): every block of the layer on
+ *                            one GPU or with the all-gather push (x2 layer
+ *                            parities); own block + 2 receive slots, O(S/d),
+ *                            with the windowed ring */
 typedef struct esp_prefill_stats {
   int64_t ring_volume_tokens;
   int64_t cross_domain_tokens;
@@ -289,6 +294,7 @@ typedef struct esp_prefill_stats {
   int64_t transient_buffer_tokens;
   int64_t extra_migration_tokens;
   double device_ms;
+  int64_t kv_ring_rows;
 } esp_prefill_stats;
 int esp_last_prefill_stats(const esp_runtime* rt, esp_prefill_stats* out);
 

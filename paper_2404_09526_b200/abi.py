@@ -138,6 +138,7 @@ class PrefillStats(C.Structure):
         ("ring_volume_tokens", C.c_int64), ("cross_domain_tokens", C.c_int64),
         ("nvlink_bytes", C.c_int64), ("transient_buffer_tokens", C.c_int64),
         ("extra_migration_tokens", C.c_int64), ("device_ms", C.c_double),
+        ("kv_ring_rows", C.c_int64),
     ]
 
 

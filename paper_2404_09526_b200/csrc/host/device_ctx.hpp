@@ -59,7 +59,10 @@ struct DeviceCtx {
   // activations / scratch
   DevBuf x, xn, q, kb, vb, attn, h, logits, tok, pos, rinst, rslot, segs, work, last_rows,
       out_tok, chunks, row_start, part_o, part_ml, counts, result, kvrow, ret_rows, ret_slab,
-      ret_slot, qin, chunk_ids, row_list, ss1, ss2;
+      ret_slot, qin, chunk_ids, row_list, ss1, ss2, carry_o, carry_ml;
+  // Side stream of the windowed ring: peer copies of the next round's block
+  // run here while K1 of the current round runs on `stream`.
+  cudaStream_t comm = nullptr;
   std::vector<void*> weight_allocs;
   std::vector<cudaEvent_t> sync_events;  // cross-domain event pool
   size_t sync_used = 0;

@@ -60,6 +60,7 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
     : cfg_(cfg) {
   opts_.domain_per_instance = std::getenv("ESP_DOMAIN_PER_INSTANCE") != nullptr;
   opts_.ring_copy = std::getenv("ESP_RING_COPY") != nullptr;
+  if (const char* w = std::getenv("ESP_RING_WINDOW")) opts_.ring_window = std::atoi(w);
   opts_.force_arrival = std::getenv("ESP_RING_ARRIVAL") != nullptr;
   opts_.decode_copy = std::getenv("ESP_DECODE_COPY") != nullptr;
   opts_.fuse_norm_prefill = std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr;
@@ -208,6 +209,7 @@ Runtime::~Runtime() {
     if (dc.e0) cudaEventDestroy(dc.e0);
     if (dc.e1) cudaEventDestroy(dc.e1);
     if (dc.stream) cudaStreamDestroy(dc.stream);
+    if (dc.comm) cudaStreamDestroy(dc.comm);
   }
 }
 
@@ -643,6 +645,7 @@ void Runtime::prefill(const esp_prefill_args& a) {
   cuda_ok(cudaEventElapsedTime(&ms, dc.e0, dc.e1), "elapsed");
   if (a.device_ms_out) *a.device_ms_out = ms;
   last_prefill_.device_ms = ms;
+  last_prefill_.kv_ring_rows = rows;
   for (int r = 0; r < n; ++r) {
     requests_[a.request_ids[r]].tokens.push_back(first[r]);
     if (a.first_token_out) a.first_token_out[r] = first[r];
@@ -1057,13 +1060,18 @@ void Runtime::decode_step(const esp_decode_args& a) {
     }
     timed(kPhQkv, s, [&] { k::gemm(a_in, H, w.wqkv, H, rows, 3 * H, H, ep, s); });
     if (b > 0) {
+      // One chunk per row (every request's KV <= decode_chunk() slots on one
+      // instance): K3 normalises its partial in place, no K4 launch.
+      const bool direct = n_chunks == b;
       timed(kPhDecodeAttn, s, [&] {
         k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
-                            part_o, part_ml, s);
+                            part_o, part_ml, s, nullptr, direct ? attn : nullptr);
       });
-      timed(kPhCombine, s, [&] {
-        k::decode_combine(part_o, part_ml, d_rs, b, cfg_.heads, cfg_.head_dim, attn, s);
-      });
+      if (!direct) {
+        timed(kPhCombine, s, [&] {
+          k::decode_combine(part_o, part_ml, d_rs, b, cfg_.heads, cfg_.head_dim, attn, s);
+        });
+      }
     }
     if (has_chunk) {
       timed(kPhAttention, s, [&] {

@@ -184,6 +184,11 @@ class Runtime {
   //                            (the cross-GPU transport on one GPU);
   //   ESP_RING_COPY            prefill ring by peer copies in the reference's
   //                            round order instead of the fused push;
+  //   ESP_RING_WINDOW=1 / =0   prefill ring over an O(S/d) window (own block +
+  //                            two receive slots, one K1 launch per round with
+  //                            the softmax state carried) always / never;
+  //                            default: when the all-gather buffers would
+  //                            exceed kWindowAutoBytes;
   //   ESP_DECODE_COPY          decode query broadcast / partial gather by peer
   //                            copies instead of fused peer stores;
   //   ESP_PREFILL_NORM_KERNEL / ESP_DECODE_NORM_KERNEL  RMSNorm as kernels
@@ -196,6 +201,7 @@ class Runtime {
     bool domain_per_instance = false;
     bool force_arrival = false;
     bool ring_copy = false;
+    int ring_window = -1;  // 1 always, 0 never, -1 when the all-gather would not fit
     bool decode_copy = false;
     bool fuse_norm_prefill = true;
     bool fuse_norm_decode = true;

@@ -62,6 +62,10 @@ void build_attention_work(const std::vector<k::RingSegment>& segs, int heads,
     for (int hd = 0; hd < heads; ++hd) {
       std::vector<ItemC> v;
       for (int qi = 0; qi < n_items; ++qi) {
+        // An item that sees no KV tile (a one-row stripe against a later
+        // origin's block, windowed ring) has no work: K1 would wait for a
+        // tile that never comes. Its rows keep their carried state.
+        if (cost[qi] == 0) continue;
         v.push_back({static_cast<int32_t>(si), (qi << 8) | hd, cost[qi]});
       }
       per_sh.push_back(std::move(v));
@@ -198,6 +202,10 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     std::vector<k::RingSegment> segs;
     std::vector<int32_t> work;
     std::vector<std::pair<int, int32_t>> last;  // (request index, local row)
+    // windowed ring: per round, the segments / work of that round's launch
+    std::vector<std::vector<k::RingSegment>> wsegs;
+    std::vector<std::vector<int32_t>> wwork;
+    std::vector<size_t> seg_off, work_off;
   };
   std::map<int, Part> parts;
   for (int dom : dom_set) parts[dom];
@@ -206,7 +214,21 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
   // its resting page slot wherever that is (peer stores), so the ring's
   // all-gather and the retention ride inside the GEMM; or the copy-engine
   // ring in the reference's round order (ESP_RING_COPY=1).
-  const bool push = !opts_.ring_copy &&
+  // Windowed ring (O(S/d) per GPU): every domain holds one
+  // ring position, its own K/V block and two receive slots. In round r the
+  // block of origin (i - r) mod d arrives from position i-1 (a peer copy on
+  // a side stream, the reference's round order, esp_mechanics.cpp:59-68)
+  // while K1 runs round r-1 on the other slot; K1 runs once per round and
+  // carries its online-softmax state (O, max, sum) between rounds in HBM.
+  // Chosen when the all-gather buffers (two layer parities of every block)
+  // would exceed kWindowAutoBytes, or forced by ESP_RING_WINDOW.
+  constexpr size_t kWindowAutoBytes = static_cast<size_t>(8) << 30;
+  const size_t gather_bytes = static_cast<size_t>(2) * 2 * rows * H * sizeof(bf16);
+  const bool window = d > 1 && dom_set.size() == static_cast<size_t>(d) && !opts_.ring_copy &&
+                      instances_.size() <= static_cast<size_t>(k::kMaxSlabs) &&
+                      (opts_.ring_window == 1 ||
+                       (opts_.ring_window < 0 && gather_bytes > kWindowAutoBytes));
+  const bool push = !window && !opts_.ring_copy &&
                     instances_.size() <= static_cast<size_t>(k::kMaxSlabs) &&
                     dom_set.size() <= static_cast<size_t>(k::kMaxPeers) + 1;
   for (int i = 0; i < d; ++i) {
@@ -222,7 +244,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         p.tok.push_back(a.tokens[tok_base[r] + t]);
         p.pos.push_back(static_cast<int32_t>(t));
         p.kvrow.push_back(g);
-        if (push) {  // retained by the origin's QKV epilogue, local or peer store
+        if (push || window) {  // retained by the origin's QKV epilogue, local or peer store
           p.rinst.push_back(static_cast<int32_t>(tok_inst[r][static_cast<size_t>(t)]));
           p.rslot.push_back(slot);
         } else if (rest.domain == dom_of[i]) {  // retained at the origin, in the QKV epilogue
@@ -257,7 +279,35 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     return push && src != dst && src < k::kMaxWaitSrc && parts[src].rows > 32 &&
            (!same_gpu(src, dst) || opts_.force_arrival);
   };
+  int32_t max_blk = 0;
+  for (int o = 0; o < d; ++o) max_blk = std::max(max_blk, blk0[o + 1] - blk0[o]);
   for (auto& [dom, p] : parts) {
+    if (window) {  // one launch per round: round rd meets the block of origin (i - rd) mod d
+      const int i = p.positions[0];
+      p.wsegs.assign(static_cast<size_t>(d), {});
+      p.wwork.assign(static_cast<size_t>(d), {});
+      for (int rd = 0; rd < d; ++rd) {
+        const int o = RingSchedule::origin(i, rd, d);
+        for (int r = 0; r < n; ++r) {
+          const int32_t ql = stripe_len(i, r), kl = stripe_len(o, r);
+          if (ql == 0 || kl == 0) continue;
+          k::RingSegment sg{};
+          sg.q_row0 = row0[i][r] - blk0[i];
+          sg.q_len = ql;
+          sg.n_rounds = 1;
+          sg.kv_row0[0] = row0[o][r] - blk0[o];
+          sg.kv_len[0] = kl;
+          sg.shift[0] = o > i ? 1 : 0;
+          p.wsegs[rd].push_back(sg);
+        }
+        build_attention_work(p.wsegs[rd], cfg_.heads, p.wwork[rd]);
+        p.seg_off.push_back(p.segs.size());
+        p.segs.insert(p.segs.end(), p.wsegs[rd].begin(), p.wsegs[rd].end());
+        p.work_off.push_back(p.work.size());
+        p.work.insert(p.work.end(), p.wwork[rd].begin(), p.wwork[rd].end());
+      }
+      continue;
+    }
     for (int i : p.positions) {
       for (int r = 0; r < n; ++r) {
         const int32_t ql = stripe_len(i, r);
@@ -292,6 +342,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
 
   int64_t max_len = 0;
   for (int r = 0; r < n; ++r) max_len = std::max(max_len, a.input_lens[r]);
+  int64_t ring_rows_max = 0;
   // Per-domain setup: uploads, embedding.
   for (auto& [dom, p] : parts) {
     DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
@@ -318,9 +369,18 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
     // Gather buffers hold every block of the layer; the push transport
     // double-buffers them by layer parity, so a source may store layer l+1
     // while this domain's K1 still reads layer l.
+    // The windowed ring holds its own block and two receive slots instead.
     const size_t nbuf = push ? 2 : 1;
-    scratch<bf16>(dc.kb, nbuf * static_cast<size_t>(rows) * H);
-    scratch<bf16>(dc.vb, nbuf * static_cast<size_t>(rows) * H);
+    const size_t kv_rows_buf = window ? lr + 2 * static_cast<size_t>(std::max(max_blk, 1))
+                                      : nbuf * static_cast<size_t>(rows);
+    scratch<bf16>(dc.kb, kv_rows_buf * H);
+    ring_rows_max = std::max<int64_t>(ring_rows_max, static_cast<int64_t>(kv_rows_buf));
+    scratch<bf16>(dc.vb, kv_rows_buf * H);
+    if (window) {
+      scratch<float>(dc.carry_o, lr * H);
+      scratch<float2>(dc.carry_ml, lr * cfg_.heads);
+      if (!dc.comm) cuda_ok(cudaStreamCreateWithFlags(&dc.comm, cudaStreamNonBlocking), "stream");
+    }
     if (fuse_norm_prefill()) {
       scratch<float>(dc.ss1, lr);
       scratch<float>(dc.ss2, lr);
@@ -353,6 +413,14 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
   // push: attn_done[dom][parity] = dom's K1 of the last layer that read that
   // gather-buffer parity (peers may overwrite it once it has completed)
   std::map<int, std::array<cudaEvent_t, 2>> attn_done;
+  // windowed ring, per domain and receive slot: the K1 round that last read
+  // the slot, and the copy that last forwarded from it (the next receive
+  // into the slot waits for both, across layers)
+  std::map<int, std::array<cudaEvent_t, 2>> win_k1, win_fwd;
+  for (auto& [dom, p] : parts) {
+    win_k1[dom] = {nullptr, nullptr};
+    win_fwd[dom] = {nullptr, nullptr};
+  }
   for (int l = 0; l < cfg_.layers; ++l) {
     NvtxRange nvtx_layer("prefill layer (cross-domain)");
     const int par = push ? (l & 1) : 0;
@@ -390,7 +458,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       ep.q_out = static_cast<bf16*>(dc.q.ptr);
       ep.k_out = static_cast<bf16*>(dc.kb.ptr) + boff;
       ep.v_out = static_cast<bf16*>(dc.vb.ptr) + boff;
-      ep.kv_rows = static_cast<int32_t*>(dc.kvrow.ptr);
+      ep.kv_rows = window ? nullptr : static_cast<int32_t*>(dc.kvrow.ptr);
       ep.pos = static_cast<int32_t*>(dc.pos.ptr);
       ep.rope = dc.rope;
       ep.hidden = H;
@@ -402,12 +470,13 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         ep.norm_dim = H;
         ep.norm_eps = cfg_.rms_eps;
       }
-      if (push) {
+      if (push || window) {
         for (size_t j = 0; j < instances_.size(); ++j) {
           ep.slab_k[j] = instances_[j].layer_k(l);
           ep.slab_v[j] = instances_[j].layer_v(l);
         }
         for (auto& [od, op] : parts) {
+          if (window) break;  // blocks travel by the round copies below
           if (od == dom) continue;
           DeviceCtx& pc = *devices_[static_cast<size_t>(od)];
           ep.k_peer[ep.n_peer] = static_cast<bf16*>(pc.kb.ptr) + boff;
@@ -428,7 +497,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       qkv_done[dom] = e;
     }
     // 2. ring transport in the reference's round order (copy mode only).
-    for (int r = 0; !push && r + 1 < d; ++r) {
+    for (int r = 0; !push && !window && r + 1 < d; ++r) {
       for (int i = 0; i < d; ++i) {
         const int o = RingSchedule::origin(i, r, d);
         const int src = dom_of[i], dst = dom_of[(i + 1) % d];
@@ -448,6 +517,78 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
         cuda_ok(cudaEventRecord(e, dd.stream), "event");
         ready[dst][o] = e;
         readers[src].push_back(e);
+      }
+    }
+    // 2b. windowed ring: round-major across domains, so every event a copy or
+    // launch waits on is recorded before the wait is enqueued.
+    if (window) {
+      auto slot_ptr = [&](DevBuf& b, const Part& pp, int sl) {
+        return static_cast<bf16*>(b.ptr) +
+               (static_cast<size_t>(std::max(pp.rows, 1)) + static_cast<size_t>(sl) * max_blk) * H;
+      };
+      auto launch_round = [&](int dom, Part& p, int rd, const bf16* kp, const bf16* vp, int kv_n) {
+        if (p.rows == 0 || attention_n_work(p.wwork[rd]) == 0) return;
+        DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+        k::RingCarry cy;
+        cy.o = static_cast<float*>(dc.carry_o.ptr);
+        cy.ml = static_cast<float2*>(dc.carry_ml.ptr);
+        cy.carry_in = rd > 0 ? 1 : 0;
+        timed(kPhAttention, dc.stream, [&] {
+          k::ring_attention(static_cast<bf16*>(dc.q.ptr), kp, vp, static_cast<bf16*>(dc.attn.ptr),
+                            p.rows, std::max(kv_n, 1), cfg_.heads, cfg_.head_dim,
+                            static_cast<k::RingSegment*>(dc.segs.ptr) + p.seg_off[rd],
+                            static_cast<int32_t*>(dc.work.ptr) + p.work_off[rd],
+                            attention_n_work(p.wwork[rd]), scale, dc.stream, nullptr, &cy);
+        });
+      };
+      for (auto& [dom, p] : parts) {  // round 0: the own block, as soon as QKV is done
+        DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+        DeviceGuard g(dc.device);
+        launch_round(dom, p, 0, static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr), p.rows);
+      }
+      std::vector<cudaEvent_t> landed_prev(static_cast<size_t>(d), nullptr);
+      for (int r = 1; r < d; ++r) {
+        std::vector<cudaEvent_t> landed(static_cast<size_t>(d), nullptr);
+        for (auto& [dom, p] : parts) {  // block of origin (i - r) mod d: position i-1 -> i
+          const int i = p.positions[0];
+          const int sp_i = (i - 1 + d) % d, src = dom_of[sp_i];
+          const int o = RingSchedule::origin(i, r, d);
+          DeviceCtx& sd = *devices_[static_cast<size_t>(src)];
+          DeviceCtx& dd = *devices_[static_cast<size_t>(dom)];
+          Part& sp = parts[src];
+          DeviceGuard g(dd.device);
+          const int sl = r & 1;
+          cuda_ok(cudaStreamWaitEvent(dd.comm, r == 1 ? qkv_done[src] : landed_prev[sp_i], 0), "wait");
+          for (cudaEvent_t e : {win_k1[dom][sl], win_fwd[dom][sl]}) {
+            if (e != nullptr) cuda_ok(cudaStreamWaitEvent(dd.comm, e, 0), "wait");
+          }
+          const size_t bytes = static_cast<size_t>(blk0[o + 1] - blk0[o]) * H * sizeof(bf16);
+          const bf16* sk = r == 1 ? static_cast<bf16*>(sd.kb.ptr) : slot_ptr(sd.kb, sp, (r - 1) & 1);
+          const bf16* sv = r == 1 ? static_cast<bf16*>(sd.vb.ptr) : slot_ptr(sd.vb, sp, (r - 1) & 1);
+          peer_copy(slot_ptr(dd.kb, p, sl), dd.device, sk, sd.device, bytes, dd.comm);
+          peer_copy(slot_ptr(dd.vb, p, sl), dd.device, sv, sd.device, bytes, dd.comm);
+          cudaEvent_t e = sync_event(dd);
+          cuda_ok(cudaEventRecord(e, dd.comm), "event");
+          landed[i] = e;
+          if (r == 1) {
+            readers[src].push_back(e);  // the source's next QKV overwrites its own block
+          } else {
+            win_fwd[src][(r - 1) & 1] = e;  // its next receive into that slot waits for this
+          }
+        }
+        for (auto& [dom, p] : parts) {  // round r on the slot that just landed
+          const int i = p.positions[0];
+          const int o = RingSchedule::origin(i, r, d);
+          DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
+          DeviceGuard g(dc.device);
+          cuda_ok(cudaStreamWaitEvent(dc.stream, landed[i], 0), "wait");
+          launch_round(dom, p, r, slot_ptr(dc.kb, p, r & 1), slot_ptr(dc.vb, p, r & 1),
+                       blk0[o + 1] - blk0[o]);
+          cudaEvent_t e = sync_event(dc);
+          cuda_ok(cudaEventRecord(e, dc.stream), "event");
+          win_k1[dom][r & 1] = e;
+        }
+        landed_prev = landed;
       }
     }
     // 3. retention on pass (copy mode), attention, O, MLP — local to each domain.
@@ -487,7 +628,14 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
       bf16* attn = static_cast<bf16*>(dc.attn.ptr);
       bf16* hbuf = static_cast<bf16*>(dc.h.ptr);
       const int n_work = attention_n_work(p.work);
-      timed(kPhAttention, s, [&] {
+      if (window) {  // every round done (stream order): normalise the carry
+        k::RingCarry cy;
+        cy.o = static_cast<float*>(dc.carry_o.ptr);
+        cy.ml = static_cast<float2*>(dc.carry_ml.ptr);
+        timed(kPhAttention, s, [&] {
+          k::ring_attention_finalize(cy, attn, p.rows, cfg_.heads, cfg_.head_dim, s);
+        });
+      } else timed(kPhAttention, s, [&] {
         const bf16* qd = static_cast<bf16*>(dc.q.ptr);
         // Q rows are this domain's local rows, K/V rows are global.
         k::ring_attention(qd, static_cast<bf16*>(dc.kb.ptr) + boff,
@@ -577,6 +725,7 @@ void Runtime::prefill_multi(const esp_prefill_args& a, const std::vector<Instanc
   }
   if (a.device_ms_out) *a.device_ms_out = ms_max;
   last_prefill_.device_ms = ms_max;
+  last_prefill_.kv_ring_rows = ring_rows_max;
   for (int r = 0; r < n; ++r) {
     requests_[a.request_ids[r]].tokens.push_back(first[r]);
     if (a.first_token_out) a.first_token_out[r] = first[r];

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(W * 32, MINB)
     decode_attention_kernel(const bf16* __restrict__ q, const DecodeChunk* __restrict__ chunks,
                             const DecodeSlabs slabs, int heads, float scale_log2,
                             float* __restrict__ part_o, float* __restrict__ part_ml,
-                            const PartDst dst) {
+                            const PartDst dst, bf16* __restrict__ direct_out) {
   constexpr int LPT = HD / 8;     // lanes per token
   constexpr int TPW = 32 / LPT;   // tokens per warp step
   // blockIdx.x = head (fastest): the CTAs resident at a time cover every head
@@ -180,6 +180,23 @@ __global__ void __launch_bounds__(W * 32, MINB)
   }
   __syncthreads();
   (void)ci;
+  if (direct_out != nullptr) {  // the row's only chunk: normalise here, no combine
+    for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+      float mm = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < W; ++w) mm = fmaxf(mm, sm_m[w]);
+      float acc = 0.f, ll = 0.f;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float c = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - mm);
+        acc += c * sm_o[w][d];
+        ll += c * sm_l[w];
+      }
+      direct_out[static_cast<int64_t>(ch.row) * hidden + head * HD + d] =
+          __float2bfloat16_rn(ll > 0.f ? acc / ll : 0.f);
+    }
+    return;
+  }
   const int64_t pidx = static_cast<int64_t>(ch.out) * heads + head;
   if (dst.o[0] != nullptr) {  // fused partial gather: store to the master's buffers
     part_o = pick(dst.o, ch.dst);
@@ -333,7 +350,8 @@ void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slo
 
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
-                      float* part_o, float* part_ml, cudaStream_t s, const PartDst* dst) {
+                      float* part_o, float* part_ml, cudaStream_t s, const PartDst* dst,
+                      bf16* direct_out) {
   if (n_chunks <= 0) return;
   const PartDst pd = dst ? *dst : PartDst{};
   if (n_chunks > 65535) throw std::runtime_error("decode_attention: more than 65535 chunks");
@@ -348,10 +366,10 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
   // ms/step slower: the fence + counter extend every CTA).
   if (head_dim == 128) {
     launch_pdl(4, decode_attention_kernel<128, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q,
-               d_chunks, slabs, heads, sl2, part_o, part_ml, pd);
+               d_chunks, slabs, heads, sl2, part_o, part_ml, pd, direct_out);
   } else if (head_dim == 64) {
     launch_pdl(4, decode_attention_kernel<64, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q,
-               d_chunks, slabs, heads, sl2, part_o, part_ml, pd);
+               d_chunks, slabs, heads, sl2, part_o, part_ml, pd, direct_out);
   } else {
     throw std::runtime_error("decode_attention: head_dim must be 64 or 128");
   }

@@ -114,6 +114,18 @@ struct RingWait {
   unsigned long long target[kMaxWaitSrc] = {};
 };
 
+// Online-softmax state carried between ring-attention launches (the
+// windowed ring: one launch per round over an O(S/d) block window). o is
+// [q_rows x heads*head_dim] fp32, the unnormalised output; ml is [q_rows x
+// heads] float2 (running max in log2 units, running sum). A launch with a
+// carry writes o/ml instead of the bf16 output; carry_in makes it start
+// from them; ring_attention_finalize writes out = o / l.
+struct RingCarry {
+  float* o = nullptr;
+  float2* ml = nullptr;
+  int carry_in = 0;
+};
+
 // K1: striped ring attention over segments; q/out are [q_rows x
 // heads*head_dim] and k/v [kv_rows x heads*head_dim] bf16 (segments index
 // rows of each). Persistent tcgen05 kernel, two 128-row query tiles per CTA
@@ -122,7 +134,10 @@ struct RingWait {
 void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
                     int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
                     const int32_t* d_work, int n_work, float scale, cudaStream_t s,
-                    const RingWait* wait = nullptr);
+                    const RingWait* wait = nullptr, const RingCarry* carry = nullptr);
+// out[r, :] = o[r, :] / l (bf16) for rows [0, rows) of a carry.
+void ring_attention_finalize(const RingCarry& carry, bf16* out, int rows, int heads,
+                             int head_dim, cudaStream_t s);
 
 #ifdef ESP_STUDY
 // Kernel-study build only (tools/attn_prof.py, `make STUDY=1`): K1 with
@@ -163,10 +178,13 @@ struct DecodeSlabs {
 // Split-KV paged attention: partial (o, m, l) per (chunk, head) into
 // part_o [n_chunks x heads x head_dim] fp32 and part_ml [n_chunks x heads x 2]
 // (or, with dst, into the master domains' buffers by peer stores).
+// direct_out: every row has exactly one chunk (short contexts on one
+// instance), so each CTA's partial IS the row's attention: it is normalised
+// and stored as bf16 [rows x heads*head_dim] and no combine is needed.
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
                       float* part_o, float* part_ml, cudaStream_t s,
-                      const PartDst* dst = nullptr);
+                      const PartDst* dst = nullptr, bf16* direct_out = nullptr);
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);

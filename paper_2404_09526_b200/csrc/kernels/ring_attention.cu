@@ -171,14 +171,15 @@ struct Steps {
     }                                              \
   } while (0)
 
-template <int HD, bool kProf, int kPoly8>
+template <int HD, bool kProf, int kPoly8, bool kCarry>
 __global__ void __launch_bounds__(kThreads, 1)
     ring_attention_tcgen05(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, bf16* __restrict__ out,
                       int hidden, const RingSegment* __restrict__ segs,
                       const int32_t* __restrict__ work, int n_work, float scale_log2,
-                      uint64_t* __restrict__ prof, const __grid_constant__ RingWait wait) {
+                      uint64_t* __restrict__ prof, const __grid_constant__ RingWait wait,
+                      const __grid_constant__ RingCarry carry) {
   using C = Cfg2<HD>;
   uint64_t prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const uint64_t prof_t_begin = kProf ? clock64() : 0;
@@ -205,7 +206,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = s_full + 2;         // [2 tiles][2 key halves]
   uint64_t* o_done = p_full + 4;         // [2]
   uint64_t* o_free = o_done + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint64_t* o_init = o_free + 2;         // [2] carried O stored into TMEM (carry_in)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_init + 2);
+  const bool cin = kCarry && carry.carry_in != 0;
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   if (warp == 0 && lane == 0) {
@@ -228,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&p_full[2 * t + 1], 128);
       ptx::mbar_init(&o_done[t], 1);
       ptx::mbar_init(&o_free[t], 128);
+      ptx::mbar_init(&o_init[t], 128);
     }
     ptx::fence_barrier_init();
   }
@@ -360,7 +364,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             if (a_now[t]) {
-              if (first_pv[t]) ESP_PROF_WAIT(5, ptx::mbar_wait(&o_free[t], (titems[t] & 1) ^ 1));
+              if (first_pv[t]) {
+                ESP_PROF_WAIT(5, ptx::mbar_wait(&o_free[t], (titems[t] & 1) ^ 1));
+                // windowed ring: the carried O is in TMEM before P.V adds to it
+                if (cin) ptx::mbar_wait(&o_init[t], titems[t] & 1);
+              }
 #pragma unroll
               for (int half = 0; half < 2; ++half) {
                 ESP_PROF_WAIT(3 + t, ptx::mbar_wait(&p_full[2 * t + half], cnt[t] & 1));
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const uint64_t dv = ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024);
                   if (leader) {
                     ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8, dv, idesc_o,
-                                     (!first_pv[t] || k != 0) ? 1u : 0u);
+                                     (!first_pv[t] || k != 0 || cin) ? 1u : 0u);
                   }
                 }
               }
@@ -417,6 +425,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int q0 = (it.q0[0] + t * BM);
       const int a = q0 + row;
       float m_run = -INFINITY, l_run = 0.f;
+      const int64_t crow = static_cast<int64_t>(sg->q_row0 + a);
+      if (cin) {
+        // Windowed ring: resume from the state the previous round's launch
+        // left (unnormalised O in fp32, running max and sum), O into TMEM.
+        const bool ok = a < sg->q_len;
+        if (ok) {
+          const float2 ml = carry.ml[crow * (hidden / HD) + it.head];
+          m_run = ml.x;
+          l_run = ml.y;
+        }
+        const float4* src = reinterpret_cast<const float4*>(carry.o + crow * hidden + it.head * HD);
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t o[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 v4 = ok ? src[c / 4 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            o[4 * i] = __float_as_uint(v4.x);
+            o[4 * i + 1] = __float_as_uint(v4.y);
+            o[4 * i + 2] = __float_as_uint(v4.z);
+            o[4 * i + 3] = __float_as_uint(v4.w);
+          }
+          ptx::tmem_st_32x32b_x32(to_t + lane_off + c, o);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&o_init[t]);
+      }
       int j = 0;
       Steps st;
       for (st.begin(sg, it); st.valid(); st.next()) {
@@ -542,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             m_run = m_new;
           }
           const float m_sub = m_run == -INFINITY ? 0.f : m_run;
-          if (j > 0 && __any_sync(0xffffffff, need)) rescale_o(alpha);
+          if ((j > 0 || cin) && __any_sync(0xffffffff, need)) rescale_o(alpha);
           exp_half(0, m_sub);
           store_half(0);
           pin_half1();
@@ -565,9 +601,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const bool valid = a < sg->q_len;
       const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-      bf16* orow = out + static_cast<int64_t>(sg->q_row0 + a) * hidden + it.head * HD;
+      bf16* orow = out + crow * hidden + it.head * HD;
+      if (kCarry) {
+        // Windowed ring: hand the unnormalised state to the next round.
+        float4* dst = reinterpret_cast<float4*>(carry.o + crow * hidden + it.head * HD);
 #pragma unroll 1
-      for (int c = 0; c < HD; c += 32) {
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t o[32];
+          ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
+          ptx::tmem_wait_ld();
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              dst[c / 4 + i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                                           __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+            }
+          }
+        }
+        if (valid) carry.ml[crow * (hidden / HD) + it.head] = make_float2(m_run, l_run);
+      }
+#pragma unroll 1
+      for (int c = 0; c < HD && !kCarry; c += 32) {
         uint32_t o[32];
         ptx::tmem_ld_32x32b_x32(to_t + lane_off + c, o);
         ptx::tmem_wait_ld();
@@ -609,13 +663,13 @@ int sm_count2() {
   return n;
 }
 
-template <int HD, bool kProf, int kPoly8>
+template <int HD, bool kProf, int kPoly8, bool kCarry = false>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
-             cudaStream_t s, uint64_t* prof, const RingWait& wait) {
+             cudaStream_t s, uint64_t* prof, const RingWait& wait, const RingCarry& carry) {
   using C = Cfg2<HD>;
-  once_per_device(reinterpret_cast<const void*>(ring_attention_tcgen05<HD, kProf, kPoly8>), [] {
-    cudaFuncSetAttribute(ring_attention_tcgen05<HD, kProf, kPoly8>,
+  once_per_device(reinterpret_cast<const void*>(ring_attention_tcgen05<HD, kProf, kPoly8, kCarry>), [] {
+    cudaFuncSetAttribute(ring_attention_tcgen05<HD, kProf, kPoly8, kCarry>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const int hidden = heads * HD;
@@ -623,8 +677,8 @@ void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
   const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
   const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
-  ring_attention_tcgen05<HD, kProf, kPoly8><<<grid, kThreads, C::kSmem, s>>>(
-      tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof, wait);
+  ring_attention_tcgen05<HD, kProf, kPoly8, kCarry><<<grid, kThreads, C::kSmem, s>>>(
+      tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof, wait, carry);
   count_launch();
 }
 
@@ -632,11 +686,24 @@ template <bool kProf>
 void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
                int heads, int head_dim, const RingSegment* d_segs, const int32_t* d_work,
                int n_work, float scale, cudaStream_t s, uint64_t* prof,
-               const RingWait& wait = RingWait{}) {
+               const RingWait& wait = RingWait{}, const RingCarry& carry = RingCarry{}) {
   if (n_work <= 0) return;
   if (heads > 255) throw std::runtime_error("ring_attention: heads > 255");
   // Exponentials computed on the FMA pipe, in eighths of each row's keys
   // (MUFU/FMA balance: 2 in 8 measured best in the step in round 2, r02_poly_ab.txt).
+  if (carry.o != nullptr) {  // windowed ring: the carry variant (kCarry)
+    if (kProf) throw std::runtime_error("ring_attention: no profiled carry variant");
+    if (head_dim == 128) {
+      launch2<128, false, kDefaultPoly8, true>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work,
+                                               n_work, scale, s, prof, wait, carry);
+    } else if (head_dim == 64) {
+      launch2<64, false, kDefaultPoly8, true>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work,
+                                              n_work, scale, s, prof, wait, carry);
+    } else {
+      throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
+    }
+    return;
+  }
   if (head_dim == 128) {
 #ifdef ESP_STUDY
     // kernel-study build: ESP_ATTN_POLY = eighths of the exponentials on the FMA pipe
@@ -645,18 +712,18 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
       return e ? std::atoi(e) : kDefaultPoly8;
     }();
     switch (poly) {
-      case 0: launch2<128, kProf, 0>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
-      case 2: launch2<128, kProf, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
-      case 3: launch2<128, kProf, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
-      case 4: launch2<128, kProf, 4>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait); return;
+      case 0: launch2<128, kProf, 0>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 2: launch2<128, kProf, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 3: launch2<128, kProf, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 4: launch2<128, kProf, 4>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       default: break;
     }
 #endif
     launch2<128, kProf, kDefaultPoly8>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work,
-                                       n_work, scale, s, prof, wait);
+                                       n_work, scale, s, prof, wait, carry);
   } else if (head_dim == 64) {
     launch2<64, kProf, kDefaultPoly8>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work,
-                                      n_work, scale, s, prof, wait);
+                                      n_work, scale, s, prof, wait, carry);
   } else {
     throw std::runtime_error("ring_attention: head_dim must be 64 or 128");
   }
@@ -667,9 +734,34 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
 void ring_attention(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows,
                     int kv_rows, int heads, int head_dim, const RingSegment* d_segs,
                     const int32_t* d_work, int n_work, float scale, cudaStream_t s,
-                    const RingWait* wait) {
+                    const RingWait* wait, const RingCarry* carry) {
   dispatch2<false>(q, k, v, out, q_rows, kv_rows, heads, head_dim, d_segs, d_work, n_work, scale,
-                   s, nullptr, wait ? *wait : RingWait{});
+                   s, nullptr, wait ? *wait : RingWait{}, carry ? *carry : RingCarry{});
+}
+
+namespace {
+// One CTA per row, one thread per 4 columns: out = o / l of the row's head.
+__global__ void ring_finalize_kernel(const float* __restrict__ o, const float2* __restrict__ ml,
+                                     bf16* __restrict__ out, int hidden, int head_dim) {
+  const int64_t row = blockIdx.x;
+  const int heads = hidden / head_dim;
+  for (int c = threadIdx.x * 4; c < hidden; c += blockDim.x * 4) {
+    const float l = ml[row * heads + c / head_dim].y;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const float4 v = *reinterpret_cast<const float4*>(o + row * hidden + c);
+    uint2 w;
+    w.x = ptx::pack_bf16(v.x * inv, v.y * inv);
+    w.y = ptx::pack_bf16(v.z * inv, v.w * inv);
+    *reinterpret_cast<uint2*>(out + row * hidden + c) = w;
+  }
+}
+}  // namespace
+
+void ring_attention_finalize(const RingCarry& carry, bf16* out, int rows, int heads, int head_dim,
+                             cudaStream_t s) {
+  if (rows <= 0) return;
+  ring_finalize_kernel<<<rows, 256, 0, s>>>(carry.o, carry.ml, out, heads * head_dim, head_dim);
+  count_launch();
 }
 
 #ifdef ESP_STUDY
@@ -678,7 +770,7 @@ void ring_attention_profiled(const bf16* q, const bf16* k, const bf16* v, bf16* 
                              const int32_t* d_work, int n_work, float scale, cudaStream_t s,
                              uint64_t* prof) {
   dispatch2<true>(q, k, v, out, q_rows, kv_rows, heads, head_dim, d_segs, d_work, n_work, scale,
-                  s, prof);
+                  s, prof);  // (no carry)
 }
 #endif
 

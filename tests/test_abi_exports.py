@@ -20,7 +20,7 @@ def test_header_symbols_exported():
 
 
 def test_abi_version_and_errors():
-    assert abi.lib().esp_abi_version() == 2
+    assert abi.lib().esp_abi_version() == 3
     try:
         abi.plan_prefill_scale_down([0], [5], [6])
     except abi.InfeasiblePlanError as e:

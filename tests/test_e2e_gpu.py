@@ -28,7 +28,7 @@ TIE_GAP = 2e-2
 
 
 @pytest.fixture(autouse=True, params=["colocated", "domain_push", "domain_copy",
-                                      "domain_arrival"])
+                                      "domain_arrival", "domain_window"])
 def transport(request, monkeypatch):
     """colocated: instances of one GPU share buffers (zero-copy ring).
     domain_*: every instance is its own co-location domain (ESP_DOMAIN_PER_
@@ -44,8 +44,15 @@ def transport(request, monkeypatch):
     counters (each QKV epilogue adds its K/V stores to the peers' counters,
     K1's producer polls them before loading a remote block); on one GPU the
     stream also waits for the source's event, so this checks the counting,
-    not the concurrency (ESP_RING_ARRIVAL)."""
+    not the concurrency (ESP_RING_ARRIVAL). domain_window: the windowed ring
+    (ESP_RING_WINDOW=1): each domain keeps its own K/V block and two receive
+    slots, blocks move one hop per round by peer copies on a side stream, K1
+    runs once per round carrying its softmax state in HBM; decode as push."""
     monkeypatch.delenv("ESP_RING_ARRIVAL", raising=False)
+    if request.param == "domain_window":
+        monkeypatch.setenv("ESP_RING_WINDOW", "1")
+    else:
+        monkeypatch.delenv("ESP_RING_WINDOW", raising=False)
     if request.param == "domain_arrival":
         monkeypatch.setenv("ESP_RING_ARRIVAL", "1")
     if request.param.startswith("domain"):

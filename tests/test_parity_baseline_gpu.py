@@ -99,17 +99,22 @@ def config2_oracle():
     return out
 
 
-@pytest.mark.parametrize("mode", ["d1", "d8_colocated", "d4_domains", "d4_domains_arrival"])
+@pytest.mark.parametrize("mode", ["d1", "d8_colocated", "d4_domains", "d4_domains_arrival",
+                                  "d4_domains_window"])
 def test_config2_32k_prefill_vs_oracle(config2_oracle, mode, monkeypatch):
     o = config2_oracle
     monkeypatch.delenv("ESP_RING_ARRIVAL", raising=False)
+    monkeypatch.delenv("ESP_RING_WINDOW", raising=False)
+    if mode.endswith("window"):  # O(S/d) windowed ring, one K1 launch per round
+        monkeypatch.setenv("ESP_RING_WINDOW", "1")
     if mode.startswith("d4_domains"):
         monkeypatch.setenv("ESP_DOMAIN_PER_INSTANCE", "1")
         if mode.endswith("arrival"):  # device-side arrival counters of the push transport
             monkeypatch.setenv("ESP_RING_ARRIVAL", "1")
     else:
         monkeypatch.delenv("ESP_DOMAIN_PER_INSTANCE", raising=False)
-    d = {"d1": 1, "d8_colocated": 8, "d4_domains": 4, "d4_domains_arrival": 4}[mode]
+    d = {"d1": 1, "d8_colocated": 8, "d4_domains": 4, "d4_domains_arrival": 4,
+         "d4_domains_window": 4}[mode]
     if d == 1:
         retain = [(0, S2)]
         cap = S2
@@ -124,6 +129,11 @@ def test_config2_32k_prefill_vs_oracle(config2_oracle, mode, monkeypatch):
                               want_logits=True)
     assert rt.placement(3) == {i: t for i, t in retain}
     rt.check_conservation()
+    ring_rows = rt.last_prefill_stats()["kv_ring_rows"]
+    if mode.endswith("window"):  # own block + 2 receive slots per GPU: O(S/d)
+        assert ring_rows <= 3 * (-(-S2 // d)), ring_rows
+    elif mode.startswith("d4_domains"):  # all-gather push: every block, 2 layer parities
+        assert ring_rows == 2 * S2, ring_rows
     o16, o32 = o["bf16"], o["fp32"]
     report = []
     check_token(int(first[0]), o32["tok"], o32["lg"])
