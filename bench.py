@@ -1045,9 +1045,37 @@ def esp_child(args):
                    "nvlink_bytes_per_prefill": stats["nvlink_bytes"],
                    "nvlink_bytes_per_gpu_per_layer": stats["nvlink_bytes"] / max(n, 1) / L,
                    "transient_buffer_tokens": stats["transient_buffer_tokens"],
-                   "extra_migration_tokens": stats["extra_migration_tokens"]}
+                   "extra_migration_tokens": stats["extra_migration_tokens"],
+                   "kv_ring_rows_per_gpu": stats["kv_ring_rows"]}
     rt.close()
     out["clocks"] = clk.summary()
+    # The windowed ring on the same plan (ESP_RING_WINDOW=1): own block + two
+    # receive slots per GPU (O(S/n) K/V), blocks forwarded one hop per round
+    # by peer copies on a side stream, one K1 launch per round with the
+    # softmax state carried; the default above is the all-gather push.
+    if n > 1:
+        saved_w = os.environ.get("ESP_RING_WINDOW")
+        os.environ["ESP_RING_WINDOW"] = "1"
+        try:
+            rt = abi.Runtime(abi.LWM_7B, n, devices=devs, kv_capacity=S + 64)
+            wms = []
+            for k in range(1 + max(2, args.steps)):
+                _, _, ms = rt.prefill([500 + k], [S], list(range(n)), retain, tokens=prompt)
+                rt.free_request(500 + k)
+                if k:
+                    wms.append(ms)
+            wst = rt.last_prefill_stats()
+            rt.close()
+            out["prefill_window"] = {"tokens_per_s": S / (statistics.median(wms) / 1e3),
+                                     "ms_per_step": statistics.median(wms), "ms_samples": wms,
+                                     "kv_ring_rows_per_gpu": wst["kv_ring_rows"]}
+        except Exception as e:  # noqa: BLE001 — report, keep the line
+            out["prefill_window"] = {"error": str(e)[:300]}
+        finally:
+            if saved_w is None:
+                os.environ.pop("ESP_RING_WINDOW", None)
+            else:
+                os.environ["ESP_RING_WINDOW"] = saved_w
     # Migration hidden over NVLink (SURVEY §8 d, a7 vs a8): the same prefill
     # retaining onto the reactive plan's final placement (proactive: the
     # ring carries every token past its survivor, extra NVLink bytes 0) vs a
