@@ -33,7 +33,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int kStages = 2;   // V stages
+constexpr int kVStagesDefault = 2;  // V stages
+constexpr int kPartsDefault = 4;    // P stored (and P.V issued) in this many key parts:
+                                    // in-step A/B 4 vs 2: K1 +2.7 % (r02_k1_parts_study.txt)
 #ifndef ESP_K1_KSTAGES
 #define ESP_K1_KSTAGES 2
 #endif
@@ -42,12 +44,12 @@ constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;
 constexpr int kDefaultPoly8 = 2;  // in-step A/B (profiles/r02_poly_ab.txt): 2 > 0 > 1
 
-template <int HD>
+template <int HD, int kVSt>
 struct Cfg2 {
   static constexpr int kBoxes = HD / 64;
   static constexpr int kQBytes = BM * HD * 2;
   static constexpr int kKvBytes = BN * HD * 2;
-  static constexpr int kSmem = 2 * kQBytes + (kKStages + kStages) * kKvBytes + 1024 + 512;
+  static constexpr int kSmem = 2 * kQBytes + (kKStages + kVSt) * kKvBytes + 1024 + 512;
 };
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): half the FMA-pipe
@@ -171,7 +173,7 @@ struct Steps {
     }                                              \
   } while (0)
 
-template <int HD, bool kProf, int kPoly8, bool kCarry>
+template <int HD, bool kProf, int kPoly8, bool kCarry, int kParts, int kStages>
 __global__ void __launch_bounds__(kThreads, 1)
     ring_attention_tcgen05(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
@@ -180,7 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const int32_t* __restrict__ work, int n_work, float scale_log2,
                       uint64_t* __restrict__ prof, const __grid_constant__ RingWait wait,
                       const __grid_constant__ RingCarry carry) {
-  using C = Cfg2<HD>;
+  using C = Cfg2<HD, kStages>;
+  static_assert(kParts == 2 || kParts == 4 || kParts == 8, "P parts");
+  constexpr int kCP = 64 / kParts;  // packed bf16x2 P columns per part (2 keys each)
   uint64_t prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const uint64_t prof_t_begin = kProf ? clock64() : 0;
   auto prof_store = [&](int role) {
@@ -203,8 +207,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* v_full = k_empty + kKStages;
   uint64_t* v_empty = v_full + kStages;
   uint64_t* s_full = v_empty + kStages;  // [2] per query tile
-  uint64_t* p_full = s_full + 2;         // [2 tiles][2 key halves]
-  uint64_t* o_done = p_full + 4;         // [2]
+  uint64_t* p_full = s_full + 2;         // [2 tiles][kParts key parts]
+  uint64_t* o_done = p_full + 2 * kParts;  // [2]
   uint64_t* o_free = o_done + 2;         // [2]
   uint64_t* o_init = o_free + 2;         // [2] carried O stored into TMEM (carry_in)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_init + 2);
@@ -227,8 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[2 * t], 128);
-      ptx::mbar_init(&p_full[2 * t + 1], 128);
+      for (int p = 0; p < kParts; ++p) ptx::mbar_init(&p_full[kParts * t + p], 128);
       ptx::mbar_init(&o_done[t], 1);
       ptx::mbar_init(&o_free[t], 128);
       ptx::mbar_init(&o_init[t], 128);
@@ -370,11 +373,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (cin) ptx::mbar_wait(&o_init[t], titems[t] & 1);
               }
 #pragma unroll
-              for (int half = 0; half < 2; ++half) {
-                ESP_PROF_WAIT(3 + t, ptx::mbar_wait(&p_full[2 * t + half], cnt[t] & 1));
+              for (int part = 0; part < kParts; ++part) {
+                ESP_PROF_WAIT(3 + t, ptx::mbar_wait(&p_full[kParts * t + part], cnt[t] & 1));
                 ptx::tc_fence_after();
 #pragma unroll
-                for (int k = 4 * half; k < 4 * half + 4; ++k) {
+                for (int k = part * (8 / kParts); k < (part + 1) * (8 / kParts); ++k) {
                   const uint64_t dv = ptx::make_sdesc_sw128(v_addr + k * 2048, BN * 128, 1024);
                   if (leader) {
                     ptx::umma_f16_ts(t_o[t], t_s[t] + k * 8, dv, idesc_o,
@@ -518,15 +521,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
         // P in place: s[c] <- bf16x2(p[2c], p[2c+1]) (reads of s[2c], s[2c+1]
-        // precede the write of s[c], c <= 2c), then P over S_t in TMEM, in two
-        // halves of 64 keys: the MMA warp starts PV on keys 0..63 while keys
-        // 64..127 are still being exponentiated.
+        // precede the write of s[c], c <= 2c), then P over S_t in TMEM, in
+        // kParts parts of 128/kParts keys: the MMA warp starts P.V on the
+        // first keys while the later ones are still being exponentiated.
         const uint64_t scale2 = f2pack(scale_log2, scale_log2);
         uint64_t sum2a = f2pack(0.f, 0.f), sum2b = f2pack(0.f, 0.f);
-        auto exp_half = [&](int half, float m_sub) {
+        auto exp_part = [&](int part, float m_sub) {
           const uint64_t negm2 = f2pack(-m_sub, -m_sub);
 #pragma unroll
-          for (int c = 32 * half; c < 32 * half + 32; ++c) {
+          for (int c = kCP * part; c < kCP * part + kCP; ++c) {
             float x0, x1, p0, p1;
             f2unpack(ffma2(f2pack(__uint_as_float(s[2 * c]), __uint_as_float(s[2 * c + 1])),
                            scale2, negm2),
@@ -545,19 +548,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             s[c] = ptx::pack_bf16(p0, p1);
           }
         };
-        auto store_half = [&](int half) {
-          ptx::tmem_st_32x32b_x32(ts_t + lane_off + 32 * half,
-                                  *reinterpret_cast<uint32_t(*)[32]>(&s[32 * half]));
+        auto store_part = [&](int part) {
+          if constexpr (kCP == 32) {
+            ptx::tmem_st_32x32b_x32(ts_t + lane_off + kCP * part,
+                                    *reinterpret_cast<uint32_t(*)[32]>(&s[kCP * part]));
+          } else if constexpr (kCP == 8) {
+            ptx::tmem_st_32x32b_x8(ts_t + lane_off + kCP * part,
+                                   *reinterpret_cast<uint32_t(*)[8]>(&s[kCP * part]));
+          } else {
+            ptx::tmem_st_32x32b_x16(ts_t + lane_off + kCP * part,
+                                    *reinterpret_cast<uint32_t(*)[16]>(&s[kCP * part]));
+          }
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&p_full[2 * t + half]);
+          ptx::mbar_arrive(&p_full[kParts * t + part]);
         };
-        // Keys 64..127 are still in registers; an empty volatile asm that
-        // "modifies" them pins the second half's exponentials after the
-        // first half's P store and arrive.
-        auto pin_half1 = [&]() {
+        // The raw scores of the later parts are still in registers; an empty
+        // volatile asm that "modifies" them pins their exponentials after the
+        // earlier part's P store and arrive.
+        auto pin_from = [&](int c0) {
 #pragma unroll
-          for (int c = 64; c < 128; c += 16) {
+          for (int c = c0; c < 128; c += 16) {
             asm volatile(""
                          : "+r"(s[c]), "+r"(s[c + 1]), "+r"(s[c + 2]), "+r"(s[c + 3]),
                            "+r"(s[c + 4]), "+r"(s[c + 5]), "+r"(s[c + 6]), "+r"(s[c + 7]),
@@ -579,11 +590,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const float m_sub = m_run == -INFINITY ? 0.f : m_run;
           if ((j > 0 || cin) && __any_sync(0xffffffff, need)) rescale_o(alpha);
-          exp_half(0, m_sub);
-          store_half(0);
-          pin_half1();
-          exp_half(1, m_sub);
-          store_half(1);
+#pragma unroll
+          for (int part = 0; part < kParts; ++part) {
+            exp_part(part, m_sub);
+            store_part(part);
+            if (part + 1 < kParts) pin_from(2 * kCP * (part + 1));
+          }
           if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P stored
           float sa0, sa1;
           f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
@@ -663,21 +675,22 @@ int sm_count2() {
   return n;
 }
 
-template <int HD, bool kProf, int kPoly8, bool kCarry = false>
+template <int HD, bool kProf, int kPoly8, bool kCarry = false, int kParts = kPartsDefault,
+          int kVSt = kVStagesDefault>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s, uint64_t* prof, const RingWait& wait, const RingCarry& carry) {
-  using C = Cfg2<HD>;
-  once_per_device(reinterpret_cast<const void*>(ring_attention_tcgen05<HD, kProf, kPoly8, kCarry>), [] {
-    cudaFuncSetAttribute(ring_attention_tcgen05<HD, kProf, kPoly8, kCarry>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  using C = Cfg2<HD, kVSt>;
+  auto* kern = ring_attention_tcgen05<HD, kProf, kPoly8, kCarry, kParts, kVSt>;
+  once_per_device(reinterpret_cast<const void*>(kern), [kern] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
   const int hidden = heads * HD;
   const CUtensorMap tq = make_tmap_bf16(q, q_rows, hidden, hidden, BM);
   const CUtensorMap tk = make_tmap_bf16(k, kv_rows, hidden, hidden, BN);
   const CUtensorMap tv = make_tmap_bf16(v, kv_rows, hidden, hidden, BN);
   const int grid = n_work < sm_count2() ? n_work : sm_count2();
-  ring_attention_tcgen05<HD, kProf, kPoly8, kCarry><<<grid, kThreads, C::kSmem, s>>>(
+  kern<<<grid, kThreads, C::kSmem, s>>>(
       tq, tk, tv, out, hidden, segs, work, n_work, scale * 1.4426950408889634f, prof, wait, carry);
   count_launch();
 }
@@ -711,6 +724,16 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
       const char* e = std::getenv("ESP_ATTN_POLY");
       return e ? std::atoi(e) : kDefaultPoly8;
     }();
+    // ESP_K1_PARTS2 / ESP_K1_PARTS8: P in 2 / 8 key parts; ESP_K1_VST3: three V stages
+    static const int var = (std::getenv("ESP_K1_PARTS2") ? 1 : 0) | (std::getenv("ESP_K1_PARTS8") ? 2 : 0) |
+                           (std::getenv("ESP_K1_VST3") ? 4 : 0);
+    switch (var) {
+      case 1: launch2<128, kProf, kDefaultPoly8, false, 2, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 2: launch2<128, kProf, kDefaultPoly8, false, 8, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 4: launch2<128, kProf, kDefaultPoly8, false, 4, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 6: launch2<128, kProf, kDefaultPoly8, false, 8, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      default: break;
+    }
     switch (poly) {
       case 0: launch2<128, kProf, 0>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       case 2: launch2<128, kProf, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
