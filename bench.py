@@ -462,7 +462,7 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
     step = sum(ms) / len(ms)
     ctx_now = ctx + args.warmup + args.steps + 1
     kv_bytes = 2.0 * L * H * 2 * b * ctx_now
-    w_bytes = 2.0 * (L * (4 * H * H + 3 * H * F) + 2 * V * H)
+    w_bytes = 2.0 * (L * (4 * H * H + 3 * H * F) + V * H)  # projections + LM head (embed: b rows)
     att_ms, att_n = ph["decode_attention"]
     att_avg = att_ms / max(att_n, 1)
     att_gbs = (kv_bytes / L) / (att_avg / 1e3) / 1e9
@@ -481,6 +481,10 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
     rt.close()
     w_gbs = w_bytes / (short / 1e3) / 1e9
     wall_step = sum(wall) / len(wall)
+    gp = bench_gemm_phase(abi, b)
+    gp_gbs = w_bytes / (gp["ms_per_step"] / 1e3) / 1e9
+    gp.update({"weight_bytes": w_bytes, "achieved_gbs": gp_gbs, "frac": gp_gbs / hbm,
+               "rest_of_short_step_ms": short - gp["ms_per_step"]})
     return {"value": b / (step / 1e3), "unit": "tokens/s", "ms_per_step": step,
             "e2e": {"value": b / (wall_step / 1e3), "unit": "tokens/s",
                     "ms_per_step": wall_step, "h2d_bytes_per_step": 4 * b,
@@ -498,7 +502,62 @@ def bench_decode(rt_prefill, abi, args, np, hbm):
                                  "achieved_gbs": w_gbs, "frac": w_gbs / hbm,
                                  "config": f"batch {b} x 64-token contexts: the step is the "
                                            "projection GEMMs + LM head streaming the weights"},
+            "gemm_phase": gp,
             "phase_ms": {p: round(v[0] / max(len(ms), 1), 4) for p, v in ph.items() if v[1] > 0}}
+
+
+def bench_gemm_phase(abi, b):
+    """The decode step's GEMM phase alone: one layer's four projections (QKV,
+    O, gate_up, down) through the production skinny dispatch, back to back
+    with PDL as in the step, weights rotated over 8 copies (3.2 GB, so every
+    call streams from HBM), x 32 layers, plus the LM head; CUDA events."""
+    import torch
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    copies, reps = 8, 48
+    shapes = [("qkv", 3 * H, H, 0, "x", "q"), ("o", H, H, 1, "attn", "x"),
+              ("gate_up", 2 * F, H, 3, "x", "h"), ("down", H, F, 1, "h", "x")]
+    w = {n: [torch.randn(N, K, device=dev, dtype=torch.bfloat16) * 0.02 for _ in range(copies)]
+         for n, N, K, _, _, _ in shapes}
+    buf = {"x": torch.randn(b, H, device=dev, dtype=torch.bfloat16),
+           "attn": torch.randn(b, H, device=dev, dtype=torch.bfloat16),
+           "h": torch.randn(b, F, device=dev, dtype=torch.bfloat16),
+           "q": torch.randn(b, 3 * H, device=dev, dtype=torch.bfloat16)}
+    lm = torch.randn(V, H, device=dev, dtype=torch.bfloat16) * 0.02
+    logits = torch.empty(b, V, device=dev, dtype=torch.float32)
+    lib = abi.lib()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    calls = [[(buf[a].data_ptr(), w[n][i].data_ptr(), buf[d].data_ptr(), b, N, K, e, stream)
+              for n, N, K, e, a, d in shapes] for i in range(copies)]
+
+    def layer(i):
+        for c in calls[i % copies]:
+            lib.esp_k_gemm(*c)
+
+    def timed(fn, n):
+        for i in range(8):
+            fn(i)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(n):
+            fn(i)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / n
+    per = {}
+    for j, (n, N, K, e, a, d) in enumerate(shapes):
+        us = timed(lambda i, j=j: lib.esp_k_gemm(*calls[i % copies][j]), reps) * 1e3
+        per[n] = {"us": round(us, 2), "GBps": round(2.0 * N * K / us / 1e3, 1)}
+    layer_ms = timed(layer, reps)
+    lm_ms = timed(lambda i: lib.esp_k_gemm(buf["x"].data_ptr(), lm.data_ptr(), logits.data_ptr(),
+                                           b, V, H, 2, stream), 16)
+    del w, buf, lm, logits
+    torch.cuda.empty_cache()
+    return {"ms_per_step": L * layer_ms + lm_ms, "layer_us": layer_ms * 1e3,
+            "lm_head_us": lm_ms * 1e3, "per_gemm": per,
+            "config": f"{b} rows: QKV, O, gate_up, down back to back (PDL) x {L} layers + LM head, "
+                      "production dispatch, 8 rotating weight copies (HBM-resident)"}
 
 
 def bench_config1(abi, np):
@@ -599,7 +658,7 @@ def bench_decode_degrees(abi, args, np, hbm):
         rt.close()
         step = sum(ms) / len(ms)
         kv_bytes = 2.0 * L * H * 2 * b * (share * d + args.warmup + steps // 2 + 1)
-        w_bytes = 2.0 * (L * (4 * H * H + 3 * H * F) + 2 * V * H)
+        w_bytes = 2.0 * (L * (4 * H * H + 3 * H * F) + V * H)  # projections + LM head (embed: b rows)
         out[str(d)] = {"tokens_per_s": b / (step / 1e3), "ms_per_step": step,
                        "masters": len(masters),
                        "step_hbm_frac": (kv_bytes + w_bytes) / (step / 1e3) / 1e9 / hbm,
