@@ -68,6 +68,16 @@ float llama_ref_weight(uint64_t seed, int tensor, int layer, int64_t row, int64_
   return bf16_round(x);
 }
 
+/* A whole synthetic tensor [rows x cols] (tests: loading the same weights
+ * into an independent implementation). */
+void llama_ref_weights(uint64_t seed, int tensor, int layer, int64_t rows, int64_t cols,
+                       float* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t k = 0; k < cols; ++k) out[r * cols + k] = llama_ref_weight(seed, tensor, layer, r, k, cols);
+  }
+}
+
 static float* make_weight(const llama_cfg* c, int tensor, int layer, int64_t rows, int64_t cols) {
   float* w = (float*)malloc(sizeof(float) * rows * cols);
 #pragma omp parallel for schedule(static)

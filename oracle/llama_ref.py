@@ -54,6 +54,8 @@ def lib():
         h.llama_ref_decode_sample.restype = C.c_double
         h.llama_ref_decode_sample.argtypes = [C.POINTER(LlamaCfg), C.c_int64, C.c_int, C.c_int]
         h.llama_ref_max_threads.restype = C.c_int
+        h.llama_ref_weights.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_float)]
         _lib = h
     return _lib
 
@@ -73,6 +75,17 @@ def cfg_from(shape) -> LlamaCfg:
 
 def weight(seed, tensor, layer, row, col, cols) -> float:
     return float(lib().llama_ref_weight(seed, tensor, layer, row, col, cols))
+
+
+TENSORS = {"embed": 1, "q": 2, "k": 3, "v": 4, "o": 5, "gate": 6, "up": 7, "down": 8, "lm_head": 9}
+
+
+def weights(shape, tensor, layer, rows, cols) -> np.ndarray:
+    """The synthetic tensor `tensor` of `layer` as float32 [rows x cols]
+    (bf16-valued: the device and the oracle both use the bf16 rounding)."""
+    out = np.empty((rows, cols), np.float32)
+    lib().llama_ref_weights(shape.weight_seed, TENSORS[tensor], layer, rows, cols, _f32(out))
+    return out
 
 
 def generate(shape, prompt, n_steps, forced=None, emulate_bf16=True, want_logits=True,
