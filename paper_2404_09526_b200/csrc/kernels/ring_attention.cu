@@ -173,7 +173,7 @@ struct Steps {
     }                                              \
   } while (0)
 
-template <int HD, bool kProf, int kPoly8, bool kCarry, int kParts, int kStages>
+template <int HD, bool kProf, int kPoly8, bool kCarry, int kParts, int kStages, int kVar>
 __global__ void __launch_bounds__(kThreads, 1)
     ring_attention_tcgen05(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
@@ -548,7 +548,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             s[c] = ptx::pack_bf16(p0, p1);
           }
         };
-        auto store_part = [&](int part) {
+        auto signal_part = [&](int part) {
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&p_full[kParts * t + part]);
+        };
+        auto issue_part = [&](int part) {
           if constexpr (kCP == 32) {
             ptx::tmem_st_32x32b_x32(ts_t + lane_off + kCP * part,
                                     *reinterpret_cast<uint32_t(*)[32]>(&s[kCP * part]));
@@ -559,9 +564,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_st_32x32b_x16(ts_t + lane_off + kCP * part,
                                     *reinterpret_cast<uint32_t(*)[16]>(&s[kCP * part]));
           }
-          ptx::tmem_wait_st();
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&p_full[kParts * t + part]);
         };
         // The raw scores of the later parts are still in registers; an empty
         // volatile asm that "modifies" them pins their exponentials after the
@@ -593,9 +595,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int part = 0; part < kParts; ++part) {
             exp_part(part, m_sub);
-            store_part(part);
+            if constexpr ((kVar & 1) != 0) {
+              // late signal: part - 1's store has landed while this part's
+              // exponentials ran, so its wait::st returns at once
+              if (part > 0) signal_part(part - 1);
+              issue_part(part);
+            } else {
+              issue_part(part);
+              signal_part(part);
+            }
             if (part + 1 < kParts) pin_from(2 * kCP * (part + 1));
           }
+          if constexpr ((kVar & 1) != 0) signal_part(kParts - 1);
           if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P stored
           float sa0, sa1;
           f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
@@ -676,12 +687,12 @@ int sm_count2() {
 }
 
 template <int HD, bool kProf, int kPoly8, bool kCarry = false, int kParts = kPartsDefault,
-          int kVSt = kVStagesDefault>
+          int kVSt = kVStagesDefault, int kVar = 0>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s, uint64_t* prof, const RingWait& wait, const RingCarry& carry) {
   using C = Cfg2<HD, kVSt>;
-  auto* kern = ring_attention_tcgen05<HD, kProf, kPoly8, kCarry, kParts, kVSt>;
+  auto* kern = ring_attention_tcgen05<HD, kProf, kPoly8, kCarry, kParts, kVSt, kVar>;
   once_per_device(reinterpret_cast<const void*>(kern), [kern] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
@@ -726,12 +737,13 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
     }();
     // ESP_K1_PARTS2 / ESP_K1_PARTS8: P in 2 / 8 key parts; ESP_K1_VST3: three V stages
     static const int var = (std::getenv("ESP_K1_PARTS2") ? 1 : 0) | (std::getenv("ESP_K1_PARTS8") ? 2 : 0) |
-                           (std::getenv("ESP_K1_VST3") ? 4 : 0);
+                           (std::getenv("ESP_K1_VST3") ? 4 : 0) | (std::getenv("ESP_K1_LATESIG") ? 8 : 0);
     switch (var) {
       case 1: launch2<128, kProf, kDefaultPoly8, false, 2, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       case 2: launch2<128, kProf, kDefaultPoly8, false, 8, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       case 4: launch2<128, kProf, kDefaultPoly8, false, 4, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       case 6: launch2<128, kProf, kDefaultPoly8, false, 8, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 8: launch2<128, kProf, kDefaultPoly8, false, kPartsDefault, kVStagesDefault, 1>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       default: break;
     }
     switch (poly) {
