@@ -80,20 +80,30 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 }
 
 // 2^x for a pair on the FMA/ALU pipes (x <= 2^7): round-to-nearest split
-// x = n + f with the 1.5*2^23 trick, Taylor cubic for 2^f on [-1/2, 1/2]
-// (rel. err < 7e-4, under the bf16 rounding P gets anyway), 2^n by adding n
+// x = n + f with the 1.5*2^23 trick, a polynomial for 2^f on [-1/2, 1/2]
+// (minimax quadratic; Taylor cubic in the study build), 2^n by adding n
 // to the exponent field. Used for kPoly8/8 of the softmax exponentials so the
 // MUFU (ex2) pipe (16/clk/SM, shared by both softmax warpgroups) stops being
 // the co-bottleneck with the tensor core.
+template <bool kCubic>
 __device__ __forceinline__ void exp2_fma2(float x0, float x1, float& p0, float& p1) {
   const uint64_t x = f2pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
   const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
   const uint64_t t = fadd2(x, magic);
   const uint64_t r = fadd2(t, f2pack(-12582912.0f, -12582912.0f));
   const uint64_t f = ffma2(r, f2pack(-1.0f, -1.0f), x);
-  uint64_t p = ffma2(f2pack(0.0555041087f, 0.0555041087f), f, f2pack(0.240226507f, 0.240226507f));
-  p = ffma2(p, f, f2pack(0.693147181f, 0.693147181f));
-  p = ffma2(p, f, f2pack(1.0f, 1.0f));
+  uint64_t p;
+  if constexpr (kCubic) {  // Taylor cubic, rel. err < 7.9e-4
+    p = ffma2(f2pack(0.0555041087f, 0.0555041087f), f, f2pack(0.240226507f, 0.240226507f));
+    p = ffma2(p, f, f2pack(0.693147181f, 0.693147181f));
+    p = ffma2(p, f, f2pack(1.0f, 1.0f));
+  } else {
+    // minimax quadratic on [-1/2, 1/2]: rel. err < 1.73e-3, under the bf16
+    // half ulp (1.95e-3) P is rounded to anyway; one FFMA2 per pair less
+    // (in-step A/B vs the cubic: K1 +1 %, r02_k1_parts_study.txt)
+    p = ffma2(f2pack(0.2384257f, 0.2384257f), f, f2pack(0.70344281f, 0.70344281f));
+    p = ffma2(p, f, f2pack(1.00044296f, 1.00044296f));
+  }
   float t0, t1, q0, q1;
   f2unpack(t, t0, t1);
   f2unpack(p, q0, q1);
@@ -173,7 +183,7 @@ struct Steps {
     }                                              \
   } while (0)
 
-template <int HD, bool kProf, int kPoly8, bool kCarry, int kParts, int kStages, int kVar>
+template <int HD, bool kProf, int kPoly8, bool kCarry, int kParts, int kStages, bool kCubic>
 __global__ void __launch_bounds__(kThreads, 1)
     ring_attention_tcgen05(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
@@ -535,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            scale2, negm2),
                      x0, x1);
             if (((c * kPoly8) & 7) < kPoly8) {
-              exp2_fma2(x0, x1, p0, p1);  // kPoly8 pairs in 8 on the FMA pipe
+              exp2_fma2<kCubic>(x0, x1, p0, p1);  // kPoly8 pairs in 8 on the FMA pipe
             } else {
               p0 = ptx::ex2(x0);
               p1 = ptx::ex2(x1);
@@ -595,18 +605,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int part = 0; part < kParts; ++part) {
             exp_part(part, m_sub);
-            if constexpr ((kVar & 1) != 0) {
-              // late signal: part - 1's store has landed while this part's
-              // exponentials ran, so its wait::st returns at once
-              if (part > 0) signal_part(part - 1);
-              issue_part(part);
-            } else {
-              issue_part(part);
-              signal_part(part);
-            }
+            issue_part(part);
+            signal_part(part);
             if (part + 1 < kParts) pin_from(2 * kCP * (part + 1));
           }
-          if constexpr ((kVar & 1) != 0) signal_part(kParts - 1);
           if constexpr (kProf) prof_acc[4] += clock64() - prof_t_step;  // ..through P stored
           float sa0, sa1;
           f2unpack(fadd2(sum2a, sum2b), sa0, sa1);
@@ -687,12 +689,12 @@ int sm_count2() {
 }
 
 template <int HD, bool kProf, int kPoly8, bool kCarry = false, int kParts = kPartsDefault,
-          int kVSt = kVStagesDefault, int kVar = 0>
+          int kVSt = kVStagesDefault, bool kCubic = false>
 void launch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_rows, int kv_rows,
              int heads, const RingSegment* segs, const int32_t* work, int n_work, float scale,
              cudaStream_t s, uint64_t* prof, const RingWait& wait, const RingCarry& carry) {
   using C = Cfg2<HD, kVSt>;
-  auto* kern = ring_attention_tcgen05<HD, kProf, kPoly8, kCarry, kParts, kVSt, kVar>;
+  auto* kern = ring_attention_tcgen05<HD, kProf, kPoly8, kCarry, kParts, kVSt, kCubic>;
   once_per_device(reinterpret_cast<const void*>(kern), [kern] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   });
@@ -735,15 +737,16 @@ void dispatch2(const bf16* q, const bf16* k, const bf16* v, bf16* out, int q_row
       const char* e = std::getenv("ESP_ATTN_POLY");
       return e ? std::atoi(e) : kDefaultPoly8;
     }();
-    // ESP_K1_PARTS2 / ESP_K1_PARTS8: P in 2 / 8 key parts; ESP_K1_VST3: three V stages
+    // ESP_K1_PARTS2 / ESP_K1_PARTS8: P in 2 / 8 key parts; ESP_K1_VST3: three V
+    // stages; ESP_K1_CUBIC: the cubic exponential polynomial
     static const int var = (std::getenv("ESP_K1_PARTS2") ? 1 : 0) | (std::getenv("ESP_K1_PARTS8") ? 2 : 0) |
-                           (std::getenv("ESP_K1_VST3") ? 4 : 0) | (std::getenv("ESP_K1_LATESIG") ? 8 : 0);
+                           (std::getenv("ESP_K1_VST3") ? 4 : 0) | (std::getenv("ESP_K1_CUBIC") ? 8 : 0);
     switch (var) {
       case 1: launch2<128, kProf, kDefaultPoly8, false, 2, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       case 2: launch2<128, kProf, kDefaultPoly8, false, 8, 2>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       case 4: launch2<128, kProf, kDefaultPoly8, false, 4, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       case 6: launch2<128, kProf, kDefaultPoly8, false, 8, 3>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
-      case 8: launch2<128, kProf, kDefaultPoly8, false, kPartsDefault, kVStagesDefault, 1>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
+      case 8: launch2<128, kProf, kDefaultPoly8, false, kPartsDefault, kVStagesDefault, true>(q, k, v, out, q_rows, kv_rows, heads, d_segs, d_work, n_work, scale, s, prof, wait, carry); return;
       default: break;
     }
     switch (poly) {
