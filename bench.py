@@ -384,6 +384,8 @@ def single_gpu(args, rank, world, dist, fallback_note=None):
     if rank == 0 and not args.skip_scale_down:
         line["scale_down"] = bench_scale_down(abi, args, np)
         line["transport"] = bench_transport(abi, args, np)
+    if rank == 0 and not args.skip_esp_sweep:
+        line["esp_per_gpu_share"] = bench_per_gpu_share(args)
     rt.close()
     if not args.skip_cpu:
         try:
@@ -558,6 +560,24 @@ def bench_gemm_phase(abi, b):
             "lm_head_us": lm_ms * 1e3, "per_gemm": per,
             "config": f"{b} rows: QKV, O, gate_up, down back to back (PDL) x {L} layers + LM head, "
                       "production dispatch, 8 rotating weight copies (HBM-resident)"}
+
+
+def bench_per_gpu_share(args):
+    """What ONE GPU of an ESP ring of degree d computes for config 2, timed on
+    this GPU with the production kernels (tools/per_gpu_share.py): the four
+    GEMMs at S/d rows and K1 for one ring position over d blocks. Projects the
+    compute side of `--gpus d` (the NVLink ring is overlapped with K1 by the
+    arrival counters and not included)."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import per_gpu_share
+        res = per_gpu_share.measure((1, 2, 4, 8), args.seq)
+        res["note"] = ("per-GPU share of an ESP prefill at degree d measured on one B200: "
+                       "GEMMs at S/d rows + K1 of one ring position; compute_scaling_efficiency = "
+                       "t(1) / (d * t(d)); NVLink transport excluded (overlapped with K1)")
+        return res
+    except Exception as e:  # report, never hide
+        return {"error": str(e)[:200]}
 
 
 def bench_config1(abi, np):
