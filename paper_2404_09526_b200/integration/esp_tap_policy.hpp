@@ -98,6 +98,9 @@ class EspTapPolicy final : public espsim::Policy {
   // every call; 0: never — the tap then only reconciles and executes).
   void set_verify_every(int64_t n) { verify_every_ = n; }
   int64_t decisions() const { return decisions_; }
+  // Requests whose device page table reconcile() had to query (the engine's
+  // placement differed from what the tap's own operations predict).
+  int64_t reconcile_queries() const { return queried_; }
   int64_t verified_requests() const { return verified_; }
   // Prefill plans passed in the restated fill order (vs map order).
   int64_t fill_ordered_prefills() const { return fill_ordered_; }
@@ -128,14 +131,23 @@ class EspTapPolicy final : public espsim::Policy {
       if (q.phase == espsim::Phase::kFinished || q.phase == espsim::Phase::kRejected ||
           q.placement.empty()) {
         check(esp_free_request(rt_, *it));  // finish / evict-and-recompute
+        known_.erase(*it);
         it = live_.erase(it);
       } else {
         ++it;
       }
     }
     // Pass 2: engine-internal KV moves (displaced KV): surplus -> deficit.
+    // known_ mirrors what the tap itself did to the device (prefill
+    // placements, appends at the master assign_masters picks, moves); a
+    // request whose engine placement equals it needs no device query. Any
+    // other difference (an engine-internal move, or a mirror that is off) is
+    // resolved against the device's own page table, so the mirror is only a
+    // shortcut, never the source of truth.
     for (espsim::RequestId r : live_) {
       const espsim::Request& q = s.requests[static_cast<size_t>(r)];
+      auto kn = known_.find(r);
+      if (kn != known_.end() && same_placement(kn->second, q.placement)) continue;
       auto have = device_placement(r);
       std::vector<std::pair<int32_t, int64_t>> surplus, deficit;
       std::set<int32_t> ids;
@@ -154,7 +166,23 @@ class EspTapPolicy final : public espsim::Policy {
         if ((surplus[a].second -= mv) == 0) ++a;
         if ((deficit[b].second -= mv) == 0) ++b;
       }
+      known_[r] = std::map<int32_t, int64_t>(q.placement.begin(), q.placement.end());
+      ++queried_;
     }
+  }
+
+  template <class P>
+  static bool same_placement(const std::map<int32_t, int64_t>& a, const P& b) {
+    if (a.size() != b.size()) return false;
+    auto i = a.begin();
+    for (const auto& kv : b) {
+      if (i->first != kv.first || i->second != kv.second) return false;
+      ++i;
+    }
+    return true;
+  }
+  static void add_tokens(std::map<int32_t, int64_t>& m, int32_t inst, int64_t n) {
+    if ((m[inst] += n) == 0) m.erase(inst);
   }
 
   // The plan's placement pairs in TOKEN (fill) order: plan_prefill_scale_down
@@ -231,6 +259,11 @@ class EspTapPolicy final : public espsim::Policy {
     for (const espsim::MigrationPlan& m : d.migrations) {
       for (const espsim::KvMove& mv : m.moves) {
         check(esp_move_kv(rt_, mv.request, mv.from, mv.to, mv.tokens));
+        auto kn = known_.find(mv.request);
+        if (kn != known_.end()) {
+          add_tokens(kn->second, mv.from, -mv.tokens);
+          add_tokens(kn->second, mv.to, mv.tokens);
+        }
       }
     }
     for (const espsim::PrefillPlan& p : d.prefills) {
@@ -243,9 +276,12 @@ class EspTapPolicy final : public espsim::Policy {
         const espsim::TokenCount n = s.requests[static_cast<size_t>(r)].input_len;
         lens.push_back(n);
         rn.push_back(static_cast<int32_t>(order[k].size()));
+        auto& kn = known_[r];
+        kn.clear();
         for (const auto& [inst, tok] : order[k]) {
           ri.push_back(inst);
           rt.push_back(tok);
+          add_tokens(kn, inst, tok);
         }
         if (with_tokens_) {
           auto t = tokens_(r, n);
@@ -290,6 +326,8 @@ class EspTapPolicy final : public espsim::Policy {
           ci.push_back(inst);
           ct.push_back(tok);
         }
+        auto& kn = known_[p.chunk_request];
+        for (const auto& [inst, tok] : p.chunk_placement) add_tokens(kn, inst, tok);
         a.chunk_request = p.chunk_request;
         a.chunk_tokens = p.chunk_tokens;
         a.chunk_n = static_cast<int32_t>(ci.size());
@@ -304,6 +342,17 @@ class EspTapPolicy final : public espsim::Policy {
         live_.insert(p.chunk_request);
       }
       check(esp_decode_step(rt_, &a));
+      // the step appended one token per batch request at its master
+      // (assign_masters, esp_mechanics.cpp:220-238, as the runtime does)
+      if (!batch.empty()) {
+        std::vector<int32_t> master_of(batch.size());
+        check(esp_assign_masters(batch.data(), static_cast<int32_t>(batch.size()), masters.data(),
+                                 static_cast<int32_t>(masters.size()), master_of.data()));
+        for (size_t i = 0; i < batch.size(); ++i) {
+          auto kn = known_.find(batch[i]);
+          if (kn != known_.end()) add_tokens(kn->second, master_of[i], 1);
+        }
+      }
     }
   }
 
@@ -312,6 +361,8 @@ class EspTapPolicy final : public espsim::Policy {
   bool with_tokens_;
   TokenSource tokens_;
   std::set<espsim::RequestId> live_;
+  std::map<espsim::RequestId, std::map<int32_t, int64_t>> known_;
+  int64_t queried_ = 0;
   int64_t decisions_ = 0;
   int64_t verified_ = 0;
   int64_t fill_ordered_ = 0;
