@@ -27,16 +27,28 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
 
 
-@pytest.mark.parametrize("shape,S,d,steps", [
-    (abi.TINY, 1024, 2, 4),
-    (abi.ModelShape(layers=1, hidden=4096, heads=32, head_dim=128, ffn=11008, vocab=512), 2048, 4, 2),
-], ids=["tiny_d2", "lwm7b_layer_d4"])
-def test_device_vs_hf_llama(shape, S, d, steps):
+@pytest.mark.parametrize("shape,S,d,steps,domains", [
+    (abi.TINY, 1024, 2, 4, False),
+    (abi.ModelShape(layers=1, hidden=4096, heads=32, head_dim=128, ffn=11008, vocab=512), 2048, 4, 2,
+     False),
+    (abi.ModelShape(layers=2, hidden=4096, heads=32, head_dim=128, ffn=11008, vocab=32000), 4096, 4,
+     2, True),
+], ids=["tiny_d2", "lwm7b_layer_d4", "lwm7b_2layers_4k_d4_domains"])
+def test_device_vs_hf_llama(shape, S, d, steps, domains, monkeypatch):
+    """domains: one transport domain per instance (the cross-GPU push path:
+    K/V all-gathered by peer stores from the QKV epilogue, arrival counters,
+    multi-master decode with the query broadcast and partial gather)."""
+    if domains:
+        monkeypatch.setenv("ESP_DOMAIN_PER_INSTANCE", "1")
+        monkeypatch.setenv("ESP_RING_ARRIVAL", "1")
     prompt = np.random.default_rng(17).integers(0, shape.vocab, S).astype(np.int32)
     rt = abi.Runtime(shape, d, devices=[0] * d, kv_capacity=2 * S + 64)
     try:
-        # ring over d instances; every token retained on instance 0 (scale-down d -> 1)
-        first, lg0, _ = rt.prefill([0], [S], list(range(d)), [[(0, S)]], tokens=prompt,
+        # ring over d instances; every token retained on instance 0 (scale-down
+        # d -> 1), or across domains on instances d-1 and 0 (d -> 2: the decode
+        # then gathers split-KV partials from another domain)
+        retain = [[(d - 1, S // 3), (0, S - S // 3)]] if domains else [[(0, S)]]
+        first, lg0, _ = rt.prefill([0], [S], list(range(d)), retain, tokens=prompt,
                                    want_logits=True)
         toks, logits = [int(first[0])], [lg0[0]]
         for _ in range(steps):
