@@ -62,10 +62,11 @@ int run(const char* policy, int instances, TokenCount cap, std::vector<TraceReco
     }
   }
   std::printf("%s: %zu events identical, %lld decisions, %lld page-table checks, "
-              "%lld prefills in fill order\n", policy,
+              "%lld prefills in fill order, %lld reconcile queries\n", policy,
               a.size(), static_cast<long long>(tp->decisions()),
               static_cast<long long>(tp->verified_requests()),
-              static_cast<long long>(tp->fill_ordered_prefills()));
+              static_cast<long long>(tp->fill_ordered_prefills()),
+              static_cast<long long>(tp->reconcile_queries()));
   esp_runtime_destroy(rt);
   return 0;
 }

@@ -39,6 +39,16 @@ def test_tap_policy_live(tmp_path):
     for line in out.stdout.splitlines():
         if line.startswith("esp:"):
             assert " 0 prefills in fill order" not in line, line
+    # The tap's mirror of its own page-table effects spares the device query
+    # for all but the requests the engine moved itself: the disaggregation
+    # handoff (engine.cpp:194-244) shows up as queries, the other policies
+    # need (almost) none.
+    for line in out.stdout.splitlines():
+        checks = int(line.split(" page-table checks")[0].split()[-1])
+        queries = int(line.split(" reconcile queries")[0].split()[-1])
+        assert queries <= max(1, checks // 100), line
+        if line.startswith("disagg"):
+            assert queries > 0, line
 
 
 @pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "proj", "src")), reason="reference absent")
