@@ -73,3 +73,39 @@ def test_device_vs_hf_llama(shape, S, d, steps, domains, monkeypatch):
         top = int(np.argmax(ref))
         assert toks[s] == top or ref[top] - ref[toks[s]] < TIE_GAP, (s, toks[s], top)
     print("\n".join(report))
+
+
+def test_config1_in_full_vs_hf_llama():
+    """BASELINE config 1 exactly as the CPU reference runs it: the tiny model,
+    a 4096-token prompt prefilled as a 2-instance ESP ring with scale-down
+    onto instance 0, then 64 greedy decode steps — every one of the 65 logits
+    rows against HF LlamaForCausalLM (fp32) over the full sequence, with the
+    measured-floor rule; greedy tokens equal up to bf16 near-ties."""
+    shape, S, steps = abi.TINY, 4096, 64
+    prompt = np.random.default_rng(1).integers(0, shape.vocab, S).astype(np.int32)
+    rt = abi.Runtime(shape, 2, devices=[0, 0], kv_capacity=200000)
+    try:
+        first, lg0, _ = rt.prefill([0], [S], [0, 1], [[(0, S)]], tokens=prompt, want_logits=True)
+        toks, logits = [int(first[0])], [lg0[0]]
+        for _ in range(steps):
+            out, lg, _ = rt.decode_step([0], [0], [0], want_logits=True)
+            toks.append(int(out[0]))
+            logits.append(lg[0])
+        rt.check_conservation()
+    finally:
+        rt.close()
+    _, ref16 = llama_ref.generate(shape, prompt, steps, forced=toks[:steps], emulate_bf16=True)
+    model = _hf_model(shape)
+    seq = np.concatenate([prompt, np.asarray(toks[:steps], np.int32)]).astype(np.int64)
+    with torch.no_grad():
+        hf = model(torch.from_numpy(seq)[None]).logits[0].numpy()
+    worst = 0.0
+    for s in range(steps + 1):
+        ref = hf[S - 1 + s]
+        floor = rel_l2(ref16[s], ref)
+        err = rel_l2(logits[s], ref)
+        worst = max(worst, err / (1.5 * floor + 1e-3))
+        assert err <= 1.5 * floor + 1e-3, (s, err, floor)
+        top = int(np.argmax(ref))
+        assert toks[s] == top or ref[top] - ref[toks[s]] < TIE_GAP, (s, toks[s], top)
+    print(f"config 1 vs HF: worst err / bound = {worst:.2f} over {steps + 1} positions")
