@@ -186,6 +186,19 @@ typedef struct esp_model_config {
 int esp_runtime_create(const esp_model_config* cfg, int32_t n_instances,
                        const int32_t* instance_device, int64_t kv_capacity_tokens,
                        esp_runtime** out);
+/* Tensor-parallel instances (StrategyKey.tp, types.hpp:36-41;
+ * the paper's TP = 2 x ESP = 4): every instance spans tp GPUs,
+ * plane r on plane_device[r] holding heads [r heads/tp, (r+1) heads/tp) of
+ * its KV and the Megatron shards of the weights (QKV / gate_up column-
+ * parallel, O / down row-parallel, all-reduced over peer memory). Slot ids,
+ * page tables and counters are those of a tp = 1 runtime, so every other
+ * entry point keeps its meaning; ESP rings run co-located inside each plane.
+ * tp in 2..8 dividing heads, hidden / tp % 128 == 0, ffn / tp % 64 == 0;
+ * kv_capacity_tokens > 0. Not supported with tp > 1: KV moves, KV readback,
+ * attention capture, chunked-prefill chunks (ESP_ERR_CONFIG). */
+int esp_runtime_create_tp(const esp_model_config* cfg, int32_t n_instances, int32_t tp,
+                          const int32_t* plane_device, int64_t kv_capacity_tokens,
+                          esp_runtime** out);
 void esp_runtime_destroy(esp_runtime* rt);
 
 int esp_instance_info(const esp_runtime* rt, int32_t instance, int64_t* capacity,

@@ -89,7 +89,7 @@ EXPORTED_SYMBOLS = [
     "esp_plan_prefill_scale_down", "esp_sib_prefill_time", "esp_sib_decode_time",
     "esp_plan_decode_step", "esp_assign_masters", "esp_decode_step_comm",
     "esp_build_ring_schedule", "esp_proactive_scale_down", "esp_reactive_migrate",
-    "esp_runtime_create", "esp_runtime_destroy", "esp_instance_info", "esp_prefill",
+    "esp_runtime_create", "esp_runtime_create_tp", "esp_runtime_destroy", "esp_instance_info", "esp_prefill",
     "esp_decode_step", "esp_move_kv", "esp_free_request", "esp_query_placement",
     "esp_check_conservation", "esp_request_tokens", "esp_last_prefill_stats", "esp_read_kv", "esp_capture_attention",
     "esp_captured_attention", "esp_slab_access", "esp_dump_profiles",
@@ -187,6 +187,9 @@ def lib() -> C.CDLL:
         h.esp_runtime_create.argtypes = [C.POINTER(ModelConfig), C.c_int32,
                                          C.POINTER(C.c_int32), C.c_int64,
                                          C.POINTER(C.c_void_p)]
+        h.esp_runtime_create_tp.argtypes = [C.POINTER(ModelConfig), C.c_int32, C.c_int32,
+                                            C.POINTER(C.c_int32), C.c_int64,
+                                            C.POINTER(C.c_void_p)]
         h.esp_prefill.argtypes = [C.c_void_p, C.POINTER(PrefillArgs)]
         h.esp_decode_step.argtypes = [C.c_void_p, C.POINTER(DecodeArgs)]
         h.esp_move_kv.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int64]
@@ -467,11 +470,24 @@ class Runtime:
     """Elastic instances over one token-granular paged KV pool (esp_runtime)."""
 
     def __init__(self, shape: ModelShape, n_instances: int,
-                 devices: Optional[Sequence[int]] = None, kv_capacity: int = 0):
+                 devices: Optional[Sequence[int]] = None, kv_capacity: int = 0,
+                 tp_planes: Optional[Sequence[int]] = None):
+        """tp_planes: tensor-parallel runtime (esp_runtime_create_tp) — every
+        instance spans len(tp_planes) GPUs, plane r on GPU tp_planes[r];
+        `devices` must then be None."""
         self.shape = shape
         self.n_instances = n_instances
         cfg = shape.c()
         h = C.c_void_p()
+        if tp_planes is not None:
+            if devices is not None:
+                raise ValueError("tp_planes and devices are exclusive")
+            self._devs = _arr(np.int32, tp_planes)
+            check(lib().esp_runtime_create_tp(C.byref(cfg), n_instances, len(tp_planes),
+                                              _ptr(self._devs, C.c_int32), kv_capacity,
+                                              C.byref(h)))
+            self._h = h
+            return
         if devices is None:
             dev_ptr = None
         else:

@@ -274,6 +274,23 @@ int esp_runtime_create(const esp_model_config* cfg, int32_t n_instances,
   });
 }
 
+int esp_runtime_create_tp(const esp_model_config* cfg, int32_t n_instances, int32_t tp,
+                          const int32_t* plane_device, int64_t kv_capacity_tokens,
+                          esp_runtime** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (!cfg) throw esp::ConfigError("null model config");
+    auto* rt = new esp_runtime{nullptr};
+    try {
+      rt->impl = new esp::Runtime(*cfg, n_instances, tp, plane_device, kv_capacity_tokens);
+    } catch (...) {
+      delete rt;
+      throw;
+    }
+    *out = rt;
+  });
+}
+
 void esp_runtime_destroy(esp_runtime* rt) {
   if (!rt) return;
   delete rt->impl;

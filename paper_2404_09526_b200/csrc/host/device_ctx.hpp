@@ -60,6 +60,11 @@ struct DeviceCtx {
   DevBuf x, xn, q, kb, vb, attn, h, logits, tok, pos, rinst, rslot, segs, work, last_rows,
       out_tok, chunks, row_start, part_o, part_ml, counts, result, kvrow, ret_rows, ret_slab,
       ret_slot, qin, chunk_ids, row_list, ss1, ss2, carry_o, carry_ml;
+  // Tensor parallelism (runtime_tp.cpp): this plane's fp32 partials of the
+  // row-parallel O / down projections, read by every plane's all-reduce, and
+  // the events marking them written.
+  DevBuf tp_po, tp_pd;
+  cudaEvent_t tp_ev_o = nullptr, tp_ev_d = nullptr;
   // Side stream of the windowed ring: peer copies of the next round's block
   // run here while K1 of the current round runs on `stream`.
   cudaStream_t comm = nullptr;

@@ -58,13 +58,7 @@ void Runtime::phase_times(double* ms, int64_t* launches, int n) {
 Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
                  int64_t kv_capacity)
     : cfg_(cfg) {
-  opts_.domain_per_instance = std::getenv("ESP_DOMAIN_PER_INSTANCE") != nullptr;
-  opts_.ring_copy = std::getenv("ESP_RING_COPY") != nullptr;
-  if (const char* w = std::getenv("ESP_RING_WINDOW")) opts_.ring_window = std::atoi(w);
-  opts_.force_arrival = std::getenv("ESP_RING_ARRIVAL") != nullptr;
-  opts_.decode_copy = std::getenv("ESP_DECODE_COPY") != nullptr;
-  opts_.fuse_norm_prefill = std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr;
-  opts_.fuse_norm_decode = std::getenv("ESP_DECODE_NORM_KERNEL") == nullptr;
+  read_options();
   if (n_instances <= 0) throw ConfigError("need at least one instance");
   if (cfg.layers <= 0 || cfg.hidden <= 0 || cfg.heads <= 0 || cfg.head_dim <= 0 ||
       cfg.ffn <= 0 || cfg.vocab <= 0) {
@@ -175,6 +169,16 @@ Runtime::Runtime(const esp_model_config& cfg, int n_instances, const int32_t* de
   }
 }
 
+void Runtime::read_options() {
+  opts_.domain_per_instance = std::getenv("ESP_DOMAIN_PER_INSTANCE") != nullptr;
+  opts_.ring_copy = std::getenv("ESP_RING_COPY") != nullptr;
+  if (const char* w = std::getenv("ESP_RING_WINDOW")) opts_.ring_window = std::atoi(w);
+  opts_.force_arrival = std::getenv("ESP_RING_ARRIVAL") != nullptr;
+  opts_.decode_copy = std::getenv("ESP_DECODE_COPY") != nullptr;
+  opts_.fuse_norm_prefill = std::getenv("ESP_PREFILL_NORM_KERNEL") == nullptr;
+  opts_.fuse_norm_decode = std::getenv("ESP_DECODE_NORM_KERNEL") == nullptr;
+}
+
 Runtime::~Runtime() {
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (const PhaseEvent& pe : pending_) {
@@ -189,6 +193,8 @@ Runtime::~Runtime() {
   for (auto& in : instances_) {
     in.k_slab.reset();
     in.v_slab.reset();
+    in.tp_k.clear();
+    in.tp_v.clear();
   }
   for (auto& dcp : devices_) {
     DeviceCtx& dc = *dcp;
@@ -199,13 +205,15 @@ Runtime::~Runtime() {
                       &dc.last_rows, &dc.out_tok, &dc.chunks, &dc.row_start, &dc.part_o,
                       &dc.part_ml, &dc.counts, &dc.result, &dc.kvrow, &dc.ret_rows,
                       &dc.ret_slab, &dc.ret_slot, &dc.qin, &dc.chunk_ids, &dc.row_list,
-                      &dc.ss1, &dc.ss2};
+                      &dc.ss1, &dc.ss2, &dc.tp_po, &dc.tp_pd};
     for (DevBuf* b : bufs) {
       if (b->ptr) cudaFree(b->ptr);
     }
     if (dc.rope) cudaFree(dc.rope);
     if (dc.arrive) cudaFree(dc.arrive);
     for (cudaEvent_t e : dc.sync_events) cudaEventDestroy(e);
+    if (dc.tp_ev_o) cudaEventDestroy(dc.tp_ev_o);
+    if (dc.tp_ev_d) cudaEventDestroy(dc.tp_ev_d);
     if (dc.e0) cudaEventDestroy(dc.e0);
     if (dc.e1) cudaEventDestroy(dc.e1);
     if (dc.stream) cudaStreamDestroy(dc.stream);
@@ -310,6 +318,11 @@ std::vector<int32_t> Runtime::take_slots(InstanceRec& in, int64_t n) {
       DeviceGuard g(in.device);
       in.k_slab->ensure(top);
       in.v_slab->ensure(top);
+      for (size_t p = 0; p < in.tp_k.size(); ++p) {  // the other planes' head shards
+        DeviceGuard gp(devices_[p + 1]->device);
+        in.tp_k[p]->ensure(top);
+        in.tp_v[p]->ensure(top);
+      }
       in.high_water = top;
     }
   }
@@ -372,6 +385,54 @@ DeviceCtx& Runtime::device_of(const std::vector<InstanceId>& ids, const char* wh
 }
 
 // ---- prefill -------------------------------------------------------------------
+Runtime::StripePlan Runtime::plan_stripes(const esp_prefill_args& a,
+                                          const std::vector<std::vector<int32_t>>& tok_slab,
+                                          const std::vector<std::vector<int32_t>>& tok_slot,
+                                          const std::vector<int64_t>& tok_base) const {
+  const int n = a.n_requests, d = a.dop;
+  StripePlan sp;
+  // Stripe rows: ring-position-major, then request, then stripe index
+  // (token t of request r lives at position t mod d, stripe index t / d).
+  sp.row0.assign(static_cast<size_t>(d), std::vector<int32_t>(static_cast<size_t>(n)));
+  for (int i = 0; i < d; ++i) {
+    for (int r = 0; r < n; ++r) {
+      sp.row0[i][r] = sp.rows;
+      const int64_t len = a.input_lens[r];
+      for (int64_t t = i; t < len; t += d) {
+        sp.tok.push_back(a.tokens[tok_base[r] + t]);
+        sp.pos.push_back(static_cast<int32_t>(t));
+        sp.inst.push_back(inst(tok_slab[r][static_cast<size_t>(t)]).slab);
+        sp.slot.push_back(tok_slot[r][static_cast<size_t>(t)]);
+        ++sp.rows;
+      }
+    }
+  }
+  auto stripe_len = [&](int i, int r) -> int32_t {
+    const int64_t len = a.input_lens[r];
+    return len > i ? static_cast<int32_t>((len - i + d - 1) / d) : 0;
+  };
+  // Ring segments: position i meets, in round rd, the block of origin
+  // (i - rd) mod d (build_ring_schedule, esp_mechanics.cpp:59-68).
+  for (int i = 0; i < d; ++i) {
+    for (int r = 0; r < n; ++r) {
+      const int32_t ql = stripe_len(i, r);
+      if (ql == 0) continue;
+      k::RingSegment sg{};
+      sg.q_row0 = sp.row0[i][r];
+      sg.q_len = ql;
+      sg.n_rounds = d;
+      for (int rd = 0; rd < d; ++rd) {
+        const int o = RingSchedule::origin(i, rd, d);
+        sg.kv_row0[rd] = sp.row0[o][r];
+        sg.kv_len[rd] = stripe_len(o, r);
+        sg.shift[rd] = o > i ? 1 : 0;
+      }
+      sp.segs.push_back(sg);
+    }
+  }
+  return sp;
+}
+
 void Runtime::prefill(const esp_prefill_args& a) {
   NvtxRange nvtx("esp_prefill");
   const auto host_t0 = std::chrono::steady_clock::now();
@@ -518,6 +579,10 @@ void Runtime::prefill(const esp_prefill_args& a) {
     off += a.retain_n[r];
   }
   if (devices_.empty()) return;  // placement-only: page tables are the whole effect
+  if (tp_ > 1) {
+    prefill_tp(a, tok_slab, tok_slot, tok_base);
+    return;
+  }
   if (multi) {
     prefill_multi(a, ring, tok_slab, tok_slot, tok_base);
     return;
@@ -528,48 +593,10 @@ void Runtime::prefill(const esp_prefill_args& a) {
   cudaStream_t s = dc.stream;
   const int H = cfg_.hidden;
 
-  // Stripe rows: ring-position-major, then request, then stripe index
-  // (token t of request r lives at position t mod d, stripe index t / d).
-  std::vector<std::vector<int32_t>> row0(static_cast<size_t>(d), std::vector<int32_t>(static_cast<size_t>(n)));
-  std::vector<int32_t> h_tok, h_pos, h_inst, h_slot;
-  int rows = 0;
-  for (int i = 0; i < d; ++i) {
-    for (int r = 0; r < n; ++r) {
-      row0[i][r] = rows;
-      const int64_t len = a.input_lens[r];
-      for (int64_t t = i; t < len; t += d) {
-        h_tok.push_back(a.tokens[tok_base[r] + t]);
-        h_pos.push_back(static_cast<int32_t>(t));
-        h_inst.push_back(inst(tok_slab[r][static_cast<size_t>(t)]).slab);
-        h_slot.push_back(tok_slot[r][static_cast<size_t>(t)]);
-        ++rows;
-      }
-    }
-  }
-  auto stripe_len = [&](int i, int r) -> int32_t {
-    const int64_t len = a.input_lens[r];
-    return len > i ? static_cast<int32_t>((len - i + d - 1) / d) : 0;
-  };
-  // Ring segments: position i meets, in round rd, the block of origin
-  // (i - rd) mod d (build_ring_schedule, esp_mechanics.cpp:59-68).
-  std::vector<k::RingSegment> segs;
-  for (int i = 0; i < d; ++i) {
-    for (int r = 0; r < n; ++r) {
-      const int32_t ql = stripe_len(i, r);
-      if (ql == 0) continue;
-      k::RingSegment sg{};
-      sg.q_row0 = row0[i][r];
-      sg.q_len = ql;
-      sg.n_rounds = d;
-      for (int rd = 0; rd < d; ++rd) {
-        const int o = RingSchedule::origin(i, rd, d);
-        sg.kv_row0[rd] = row0[o][r];
-        sg.kv_len[rd] = stripe_len(o, r);
-        sg.shift[rd] = o > i ? 1 : 0;
-      }
-      segs.push_back(sg);
-    }
-  }
+  const StripePlan sp = plan_stripes(a, tok_slab, tok_slot, tok_base);
+  const std::vector<std::vector<int32_t>>& row0 = sp.row0;
+  const std::vector<k::RingSegment>& segs = sp.segs;
+  const int rows = sp.rows;
   std::vector<int32_t> work_sorted;
   build_attention_work(segs, cfg_.heads, work_sorted);
   if (cap_armed_) {  // parity capture: stripe row of each captured position
@@ -592,10 +619,10 @@ void Runtime::prefill(const esp_prefill_args& a) {
   int32_t* d_slot = scratch<int32_t>(dc.rslot, rows);
   k::RingSegment* d_segs = scratch<k::RingSegment>(dc.segs, segs.size());
   int32_t* d_work = scratch<int32_t>(dc.work, work_sorted.size());
-  cuda_ok(cudaMemcpyAsync(d_tok, h_tok.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
-  cuda_ok(cudaMemcpyAsync(d_pos, h_pos.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
-  cuda_ok(cudaMemcpyAsync(d_inst, h_inst.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
-  cuda_ok(cudaMemcpyAsync(d_slot, h_slot.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_tok, sp.tok.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_pos, sp.pos.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_inst, sp.inst.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_ok(cudaMemcpyAsync(d_slot, sp.slot.data(), rows * 4, cudaMemcpyHostToDevice, s), "h2d");
   cuda_ok(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(k::RingSegment),
                           cudaMemcpyHostToDevice, s),
           "h2d");
@@ -889,6 +916,12 @@ void Runtime::decode_step(const esp_decode_args& a) {
     if (a.chunk_first_token_out) *a.chunk_first_token_out = -1;
     return;
   }
+  if (tp_ > 1) {
+    if (has_chunk) throw ConfigError("decode_step: a chunked-prefill chunk with tp > 1");
+    const double ms = decode_tp(a, rows_v);
+    if (b > 0) record_decode_profile(members, batch, a.n_masters, ms);
+    return;
+  }
   if (single_domain(involved) == nullptr) {
     double ms_dec = 0, ms_chunk = 0;
     if (b > 0) {
@@ -1158,6 +1191,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
 
 // ---- KV moves, frees, readback -------------------------------------------------------
 void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t tokens) {
+  if (tp_ > 1) throw ConfigError("move_kv is not supported with tp > 1");
   NvtxRange nvtx("esp_move_kv");
   RequestRec& rr = req(r);
   InstanceRec& src = inst(from);
@@ -1316,6 +1350,7 @@ void Runtime::dump_profiles(const std::string& path) const {
 
 // ---- parity readback -----------------------------------------------------------------
 void Runtime::read_kv(RequestId r, int layer, void* k_out, void* v_out, int64_t cap, int64_t* n) {
+  if (tp_ > 1) throw ConfigError("read_kv is not supported with tp > 1");
   RequestRec& rr = req(r);
   const int64_t total = rr.kv_tokens();
   if (n) *n = total;
@@ -1356,6 +1391,7 @@ void Runtime::read_kv(RequestId r, int layer, void* k_out, void* v_out, int64_t 
 }
 
 void Runtime::capture_attention(const int64_t* pos, int64_t n) {
+  if (tp_ > 1) throw ConfigError("attention capture is not supported with tp > 1");
   if (devices_.empty()) throw NoDeviceError("capture_attention needs a device runtime");
   cap_pos_.assign(pos, pos + n);
   cap_armed_ = n > 0;

@@ -68,6 +68,17 @@ struct InstanceRec {
   k_bf16* layer_v(int l) const {
     return static_cast<k_bf16*>(v_slab->base()) + static_cast<int64_t>(l) * v_slab->layer_stride_elems();
   }
+  // Tensor-parallel runtimes (tp > 1): the head shards of planes 1..tp-1
+  // (plane 0's shard is k_slab / v_slab); same slot ids on every plane.
+  std::vector<std::unique_ptr<LazySlab>> tp_k, tp_v;
+  k_bf16* plane_k(int plane, int l) const {
+    const LazySlab& sl = plane == 0 ? *k_slab : *tp_k[static_cast<size_t>(plane - 1)];
+    return static_cast<k_bf16*>(sl.base()) + static_cast<int64_t>(l) * sl.layer_stride_elems();
+  }
+  k_bf16* plane_v(int plane, int l) const {
+    const LazySlab& sl = plane == 0 ? *v_slab : *tp_v[static_cast<size_t>(plane - 1)];
+    return static_cast<k_bf16*>(sl.base()) + static_cast<int64_t>(l) * sl.layer_stride_elems();
+  }
 };
 
 struct DevBuf {
@@ -96,7 +107,14 @@ class Runtime {
  public:
   Runtime(const esp_model_config& cfg, int n_instances, const int32_t* devices,
           int64_t kv_capacity);
+  // Tensor-parallel instances: every instance spans the `tp`
+  // planes (plane r on GPU plane_devices[r]) — heads [r H/tp, (r+1) H/tp)
+  // of its KV and the matching Megatron shards of the weights live on plane
+  // r; ESP rings run co-located inside each plane (runtime_tp.cpp).
+  Runtime(const esp_model_config& cfg, int n_instances, int tp, const int32_t* plane_devices,
+          int64_t kv_capacity);
   ~Runtime();
+  int tp() const { return tp_; }
 
   void prefill(const esp_prefill_args& a);
   void decode_step(const esp_decode_args& a);
@@ -142,6 +160,24 @@ class Runtime {
   // The single domain holding all `ids`, or nullptr when they span domains.
   DeviceCtx* single_domain(const std::vector<InstanceId>& ids);
   void init_device(DeviceCtx& dc, const DeviceCtx* share_weights);
+  void read_options();  // environment, once per runtime
+  // Tensor parallelism (runtime_tp.cpp): plane `rank`'s weight shards.
+  void init_device_tp(DeviceCtx& dc, int rank);
+  // Stripe layout of a single-domain ESP prefill: rows ring-position-major,
+  // then request, then stripe index; the K1 ring segments over them.
+  struct StripePlan {
+    std::vector<std::vector<int32_t>> row0;  // [ring position][request] first row
+    std::vector<int32_t> tok, pos, inst, slot;  // per row: token, position, resting slab / slot
+    std::vector<k::RingSegment> segs;
+    int rows = 0;
+  };
+  StripePlan plan_stripes(const esp_prefill_args& a,
+                          const std::vector<std::vector<int32_t>>& tok_inst,
+                          const std::vector<std::vector<int32_t>>& tok_slot,
+                          const std::vector<int64_t>& tok_base) const;
+  void prefill_tp(const esp_prefill_args& a, const std::vector<std::vector<int32_t>>& tok_inst,
+                  const std::vector<std::vector<int32_t>>& tok_slot,
+                  const std::vector<int64_t>& tok_base);
   void ensure_rope(DeviceCtx& dc, int64_t max_pos);
   // Cross-domain executors (runtime_multi.cpp): ring transport by peer
   // copies + events, retention on pass, query broadcast / partial gather.
@@ -162,6 +198,7 @@ class Runtime {
                    const std::vector<std::pair<InstanceId, int32_t>>& chunk_slots, double* ms);
   void decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows,
                     const std::vector<RequestId>& batch);
+  double decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>& rows);
   // The second half of a layer after attention: O projection (+ residual),
   // RMSNorm, gate_up (SiLU·up), down projection (+ residual), on `rows` rows
   // of dc's x / attn / xn / h buffers. Norm handling:
@@ -226,6 +263,7 @@ class Runtime {
   void check_cuda(const char* what);
 
   esp_model_config cfg_;
+  int tp_ = 1;  // tensor-parallel degree of every instance (planes = devices_)
   std::vector<InstanceRec> instances_;
   std::map<RequestId, RequestRec> requests_;
   std::vector<std::unique_ptr<DeviceCtx>> devices_;  // empty: placement-only

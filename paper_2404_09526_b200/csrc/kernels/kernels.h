@@ -219,6 +219,20 @@ void argmax_rows(const float* logits, int rows, int vocab, int32_t* out, cudaStr
 void rope_table(float2* table, int max_pos, int head_dim, float theta, cudaStream_t s);
 void init_weight(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor, int layer,
                  int layout, cudaStream_t s);
+// A window of a synthetic tensor (tensor-parallel weight shard): logical rows
+// row_off.. (layout 1: q|k|v regions of `part` rows each), cols col_off.. of
+// cols_total (misc.cu:init_weight_kernel).
+void init_weight_shard(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor,
+                       int layer, int layout, int64_t part, int64_t row_off, int64_t col_off,
+                       int64_t cols_total, cudaStream_t s);
+// Tensor parallelism: x (bf16, elems) += sum over the planes' fp32 partials
+// (device pointers, any GPU of the runtime), summed in plane order.
+constexpr int kMaxTp = 8;
+struct TpParts {
+  const float* p[kMaxTp] = {};
+  int n = 0;
+};
+void tp_reduce_residual(bf16* x, const TpParts& parts, int64_t elems, cudaStream_t s);
 void fill_bf16(bf16* dst, int64_t n, float v, cudaStream_t s);
 // w[r][c] *= gamma[c] (fold a norm gain into the consuming projection).
 void scale_cols(bf16* w, int64_t rows, int64_t cols, const bf16* gamma, cudaStream_t s);

@@ -3,7 +3,9 @@
 // table, seeded synthetic weights, and the page-table / KV-slot utilities
 // (device-side conservation recount, KV slot moves).
 #include <atomic>
+#include <algorithm>
 #include <cfloat>
+#include <stdexcept>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -175,23 +177,52 @@ __global__ void rope_table_kernel(float2* table, int max_pos, int half, float th
 
 // layout 0: plain [rows x cols]; 1: fused QKV [3*cols x cols] (q|k|v rows);
 // 2: gate_up [rows x cols] in 128-row blocks of 64 gate + 64 up rows.
+// A tensor-parallel shard is a window of the logical tensor: destination
+// row pr / col c is logical row row_off + pr (layout 1: region pr / part,
+// row row_off + pr % part; layout 2: physical row row_off + pr of the
+// interleaved layout) and logical col col_off + c of cols_total.
 __global__ void init_weight_kernel(bf16* dst, int64_t rows, int64_t cols, uint64_t seed,
-                                   int tensor, int layer, int layout) {
+                                   int tensor, int layer, int layout, int64_t part,
+                                   int64_t row_off, int64_t col_off, int64_t cols_total) {
   const int64_t n = rows * cols;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t pr = i / cols, c = i % cols;
     int t = tensor;
-    int64_t lr = pr;
+    int64_t lr = row_off + pr;
     if (layout == 1) {
-      t = tensor + static_cast<int>(pr / cols);  // Q, K, V ids are consecutive
-      lr = pr % cols;
+      t = tensor + static_cast<int>(pr / part);  // Q, K, V ids are consecutive
+      lr = row_off + pr % part;
     } else if (layout == 2) {
-      const int64_t blk = pr / 128, w = pr % 128;
+      const int64_t g = row_off + pr, blk = g / 128, w = g % 128;
       t = w < 64 ? kTensorGate : kTensorUp;
       lr = blk * 64 + (w % 64);
     }
-    dst[i] = __float2bfloat16_rn(synthetic_weight(seed, t, layer, lr, c, cols));
+    dst[i] = __float2bfloat16_rn(synthetic_weight(seed, t, layer, lr, col_off + c, cols_total));
+  }
+}
+
+// Tensor-parallel all-reduce of a row-parallel projection (O, down), fused
+// with the residual: x += sum of the planes' fp32 partials, in plane order
+// (every plane computes the same bits), read over NVLink where the partials
+// live on other GPUs.
+__global__ void tp_reduce_residual_kernel(bf16* __restrict__ x, TpParts parts, int64_t n4) {
+  ptx::griddep_wait();  // the partials come from the row-parallel GEMMs
+  ptx::griddep_launch();
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(parts.p[0])[i];
+    for (int q = 1; q < parts.n; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(parts.p[q])[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    uint2* xp = reinterpret_cast<uint2*>(x) + i;
+    const uint2 old = *xp;
+    const float2 a = ptx::unpack_bf16(old.x), b = ptx::unpack_bf16(old.y);
+    *xp = make_uint2(ptx::pack_bf16(a.x + acc.x, a.y + acc.y), ptx::pack_bf16(b.x + acc.z, b.y + acc.w));
   }
 }
 
@@ -280,7 +311,25 @@ void rope_table(float2* table, int max_pos, int head_dim, float theta, cudaStrea
 
 void init_weight(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor, int layer,
                  int layout, cudaStream_t s) {
-  init_weight_kernel<<<4096, 256, 0, s>>>(dst, rows, cols, seed, tensor, layer, layout);
+  init_weight_kernel<<<4096, 256, 0, s>>>(dst, rows, cols, seed, tensor, layer, layout, cols, 0,
+                                          0, cols);
+  count_launch();
+}
+
+void init_weight_shard(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor,
+                       int layer, int layout, int64_t part, int64_t row_off, int64_t col_off,
+                       int64_t cols_total, cudaStream_t s) {
+  init_weight_kernel<<<4096, 256, 0, s>>>(dst, rows, cols, seed, tensor, layer, layout, part,
+                                          row_off, col_off, cols_total);
+  count_launch();
+}
+
+void tp_reduce_residual(bf16* x, const TpParts& parts, int64_t elems, cudaStream_t s) {
+  if (elems <= 0) return;
+  if (elems % 4 != 0) throw std::runtime_error("tp_reduce_residual: elems % 4 != 0");
+  const int64_t n4 = elems / 4;
+  const int grid = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 148 * 16));
+  launch_pdl(2, tp_reduce_residual_kernel, dim3(grid), dim3(256), 0, s, x, parts, n4);
   count_launch();
 }
 

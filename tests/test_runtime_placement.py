@@ -1,5 +1,7 @@
 """Placement-only runtime (no GPU): page tables and slot counters for plans
 the reference accepts but the ring kernel could not run."""
+import pytest
+
 from paper_2404_09526_b200 import abi
 
 
@@ -40,3 +42,12 @@ def test_prefill_stats_follow_the_reference_mechanics():
     rt.prefill([2], [7], [0, 1], [[(3, 7)]])
     st = rt.last_prefill_stats()
     assert st["ring_volume_tokens"] == 7 and st["extra_migration_tokens"] == -1
+
+
+@pytest.mark.parametrize("tp,cap", [(3, 4096), (1, 4096), (16, 4096), (2, 0)])
+def test_tp_runtime_rejects_bad_configs(tp, cap):
+    """esp_runtime_create_tp validates before touching a device: tp must be
+    2..8 and divide the heads with 128-multiple hidden shards, and the
+    capacity must be given (ConfigError, no CUDA needed)."""
+    with pytest.raises(abi.ConfigError):
+        abi.Runtime(abi.TINY, 2, kv_capacity=cap, tp_planes=[0] * tp)

@@ -1,0 +1,82 @@
+"""Tensor-parallel instances (paper TP = 2 x ESP = 4,
+PAPER.md:450): every instance spans tp planes (here all on GPU 0, one stream
+each), plane r holding heads [r H/tp, (r+1) H/tp) of the KV and the Megatron
+weight shards; the O / down partials are all-reduced across the planes.
+ESP ring prefill with proactive scale-down and multi-master decode run on
+top, unchanged. Checked against the dense CPU oracle with the measured-floor
+rule of tests/test_e2e_gpu.py (the oracle is itself pinned to HF Llama,
+tests/test_oracle_hf.py)."""
+import numpy as np
+import pytest
+
+from paper_2404_09526_b200 import abi
+from tests.test_e2e_gpu import check_against_oracle
+
+pytestmark = pytest.mark.gpu
+LWM7B_2L = abi.ModelShape(layers=2, hidden=4096, heads=32, head_dim=128, ffn=11008, vocab=32000)
+
+
+@pytest.mark.parametrize("shape,tp,d,S,steps", [
+    (abi.TINY, 2, 2, 1500, 4),
+    (abi.TINY, 4, 1, 700, 3),
+    (LWM7B_2L, 2, 2, 2048, 2),
+], ids=["tiny_tp2_esp2", "tiny_tp4_esp1", "lwm7b_2layers_tp2_esp2"])
+def test_tp_prefill_decode_vs_oracle(shape, tp, d, S, steps):
+    prompt = np.random.default_rng(tp * 10 + d).integers(0, shape.vocab, S).astype(np.int32)
+    rt = abi.Runtime(shape, max(d, 2), kv_capacity=2 * S + 64, tp_planes=[0] * tp)
+    try:
+        ring = list(range(d))
+        # retention onto 2 survivors when the ring has them (scale-down d -> 2)
+        retain = [[(d - 1, S // 3), (0, S - S // 3)]] if d > 1 else [[(0, S)]]
+        first, lg0, _ = rt.prefill([7], [S], ring, retain, tokens=prompt, want_logits=True)
+        assert rt.placement(7) == {i: t for i, t in retain[0]}
+        toks, logits = [int(first[0])], [lg0[0]]
+        members = sorted({i for i, _ in retain[0]})
+        for _ in range(steps):
+            out, lg, _ = rt.decode_step(members, [0], [7], want_logits=True)
+            toks.append(int(out[0]))
+            logits.append(lg[0])
+        rt.check_conservation()
+    finally:
+        rt.close()
+    check_against_oracle(shape, prompt, toks, logits)
+
+
+def test_tp_multi_request_two_masters():
+    """Two requests decoded together by two masters (requests dealt by
+    assign_masters), KV of each on both instances, tp = 2: each request's
+    logits against the oracle."""
+    shape, tp = abi.TINY, 2
+    rt = abi.Runtime(shape, 2, kv_capacity=8192, tp_planes=[0] * tp)
+    rng = np.random.default_rng(5)
+    prompts = {r: rng.integers(0, shape.vocab, n).astype(np.int32) for r, n in ((0, 900), (1, 1300))}
+    toks = {r: [] for r in prompts}
+    logits = {r: [] for r in prompts}
+    try:
+        for r, p in prompts.items():
+            S = len(p)
+            first, lg, _ = rt.prefill([r], [S], [0, 1], [[(0, S // 2), (1, S - S // 2)]], tokens=p,
+                                      want_logits=True)
+            toks[r].append(int(first[0]))
+            logits[r].append(lg[0])
+        for _ in range(3):
+            out, lg, _ = rt.decode_step([0, 1], [0, 1], [0, 1], want_logits=True)
+            for i, r in enumerate((0, 1)):
+                toks[r].append(int(out[i]))
+                logits[r].append(lg[i])
+        rt.check_conservation()
+    finally:
+        rt.close()
+    for r, p in prompts.items():
+        check_against_oracle(shape, p, toks[r], logits[r])
+
+
+def test_tp_unsupported_entry_points_fail_loudly():
+    rt = abi.Runtime(abi.TINY, 2, kv_capacity=4096, tp_planes=[0, 0])
+    try:
+        p = np.random.default_rng(1).integers(0, abi.TINY.vocab, 300).astype(np.int32)
+        rt.prefill([1], [300], [0, 1], [[(0, 300)]], tokens=p)
+        with pytest.raises(abi.ConfigError):
+            rt.move_kv(1, 0, 1, 10)
+    finally:
+        rt.close()
