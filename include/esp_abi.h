@@ -194,8 +194,9 @@ int esp_runtime_create(const esp_model_config* cfg, int32_t n_instances,
  * page tables and counters are those of a tp = 1 runtime, so every other
  * entry point keeps its meaning; ESP rings run co-located inside each plane.
  * tp in 2..8 dividing heads, hidden / tp % 128 == 0, ffn / tp % 64 == 0;
- * kv_capacity_tokens > 0. Not supported with tp > 1: KV moves, KV readback,
- * attention capture, chunked-prefill chunks (ESP_ERR_CONFIG). */
+ * kv_capacity_tokens > 0 (KV moves copy every plane's shard). Not supported
+ * with tp > 1: KV readback, attention capture, chunked-prefill chunks
+ * (ESP_ERR_CONFIG). */
 int esp_runtime_create_tp(const esp_model_config* cfg, int32_t n_instances, int32_t tp,
                           const int32_t* plane_device, int64_t kv_capacity_tokens,
                           esp_runtime** out);

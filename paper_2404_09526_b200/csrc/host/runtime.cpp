@@ -1191,7 +1191,6 @@ void Runtime::decode_step(const esp_decode_args& a) {
 
 // ---- KV moves, frees, readback -------------------------------------------------------
 void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t tokens) {
-  if (tp_ > 1) throw ConfigError("move_kv is not supported with tp > 1");
   NvtxRange nvtx("esp_move_kv");
   RequestRec& rr = req(r);
   InstanceRec& src = inst(from);
@@ -1206,7 +1205,28 @@ void Runtime::move_kv(RequestId r, InstanceId from, InstanceId to, int64_t token
   PageList& spl = it->second;
   std::vector<int32_t> moving(spl.slots.end() - tokens, spl.slots.end());
   std::vector<int32_t> dslots = take_slots(dst, tokens);
-  if (!devices_.empty()) {
+  if (tp_ > 1) {
+    // Tensor-parallel instances: every plane moves its own head shard.
+    for (auto& pc : devices_) {
+      DeviceCtx& dc = *pc;
+      const int r = dc.domain;
+      DeviceGuard g(dc.device);
+      int32_t* d_a = scratch<int32_t>(dc.tok, static_cast<size_t>(tokens));
+      int32_t* d_b = scratch<int32_t>(dc.pos, static_cast<size_t>(tokens));
+      cuda_ok(cudaMemcpyAsync(d_a, moving.data(), tokens * 4, cudaMemcpyHostToDevice, dc.stream), "h2d");
+      cuda_ok(cudaMemcpyAsync(d_b, dslots.data(), tokens * 4, cudaMemcpyHostToDevice, dc.stream), "h2d");
+      const LazySlab& ss = r == 0 ? *src.k_slab : *src.tp_k[static_cast<size_t>(r - 1)];
+      const LazySlab& ds = r == 0 ? *dst.k_slab : *dst.tp_k[static_cast<size_t>(r - 1)];
+      k::copy_slots(src.plane_k(r, 0), src.plane_v(r, 0), d_a, dst.plane_k(r, 0),
+                    dst.plane_v(r, 0), d_b, static_cast<int>(tokens), cfg_.layers,
+                    ss.layer_stride_elems(), ds.layer_stride_elems(), cfg_.hidden / tp_, dc.stream);
+    }
+    check_cuda("move_kv");
+    for (auto& pc : devices_) {
+      DeviceGuard g(pc->device);
+      cuda_ok(cudaStreamSynchronize(pc->stream), "move_kv");
+    }
+  } else if (!devices_.empty()) {
     // The copy runs on the destination domain's stream and reads the source
     // slab directly (same GPU, or a peer over NVLink with peer access on).
     DeviceCtx& sdc = *devices_[static_cast<size_t>(src.domain)];

@@ -6,11 +6,14 @@ ESP ring prefill with proactive scale-down and multi-master decode run on
 top, unchanged. Checked against the dense CPU oracle with the measured-floor
 rule of tests/test_e2e_gpu.py (the oracle is itself pinned to HF Llama,
 tests/test_oracle_hf.py)."""
+import os
+
 import numpy as np
 import pytest
 
 from paper_2404_09526_b200 import abi
-from tests.test_e2e_gpu import check_against_oracle
+from tests import replay
+from tests.test_e2e_gpu import GOLD, Recorder, check_against_oracle
 
 pytestmark = pytest.mark.gpu
 LWM7B_2L = abi.ModelShape(layers=2, hidden=4096, heads=32, head_dim=128, ffn=11008, vocab=32000)
@@ -71,12 +74,34 @@ def test_tp_multi_request_two_masters():
         check_against_oracle(shape, p, toks[r], logits[r])
 
 
+@pytest.mark.parametrize("scenario", ["config1_tiny", "tiny_multi", "tiny_preempt"])
+def test_tp_replays_reference_scenarios(scenario):
+    """The reference engine's recorded decisions (tests/golden/scenario_*.jsonl:
+    config 1; 8 requests with varlen ring prefills, multi-master decode and
+    scale-up/down; a trace whose engine displaces paused KV onto group mates)
+    executed on a tp = 2 runtime: page tables equal the engine's at every
+    schedule() (tests/replay.py), KV moves copy every plane's shard, and every
+    request's logits match the oracle."""
+    path = os.path.join(GOLD, f"scenario_{scenario}.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], kv_capacity=head["kv_capacity"],
+                     tp_planes=[0, 0])
+    rec = Recorder(rt)
+    try:
+        replay.replay(rt, path, on_prefill=rec.prefill, on_decode=rec.decode, conservation=True)
+    finally:
+        rt.close()
+    for r, lgs in rec.logits.items():
+        toks = [int(np.argmax(l)) for l in lgs]
+        check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)
+
+
 def test_tp_unsupported_entry_points_fail_loudly():
     rt = abi.Runtime(abi.TINY, 2, kv_capacity=4096, tp_planes=[0, 0])
     try:
         p = np.random.default_rng(1).integers(0, abi.TINY.vocab, 300).astype(np.int32)
         rt.prefill([1], [300], [0, 1], [[(0, 300)]], tokens=p)
         with pytest.raises(abi.ConfigError):
-            rt.move_kv(1, 0, 1, 10)
+            rt.read_kv(1, 0)
     finally:
         rt.close()
