@@ -386,6 +386,7 @@ def single_gpu(args, rank, world, dist, fallback_note=None):
         line["transport"] = bench_transport(abi, args, np)
     if rank == 0 and not args.skip_esp_sweep:
         line["esp_per_gpu_share"] = bench_per_gpu_share(args)
+        line["tp_one_gpu"] = bench_tp(abi, args, np)
     rt.close()
     if not args.skip_cpu:
         try:
@@ -560,6 +561,41 @@ def bench_gemm_phase(abi, b):
             "lm_head_us": lm_ms * 1e3, "per_gemm": per,
             "config": f"{b} rows: QKV, O, gate_up, down back to back (PDL) x {L} layers + LM head, "
                       "production dispatch, 8 rotating weight copies (HBM-resident)"}
+
+
+def bench_tp(abi, args, np):
+    """Tensor-parallel instances (runtime_tp.cpp) on ONE GPU: the
+    16K-token LWM-7B prefill at ESP degree 2 and a b=16 decode step, tp = 1
+    vs tp = 2 and 4 planes co-located on this GPU (each plane a stream with
+    half / a quarter of the heads and FFN columns). The planes share the one
+    GPU, so the difference is what TP adds (the fused all-reduces, smaller
+    GEMMs and attention launches), not the multi-GPU speed-up."""
+    S, d, b, ctx = 16384, 2, 16, 2048
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    prompt = np.random.default_rng(17).integers(0, V, S).astype(np.int32)
+    out = {"config": f"LWM-7B {S}-token prefill at ESP {d} (retention onto instance 0) and a "
+                     f"b={b} x {ctx} decode step, planes co-located on one GPU"}
+    try:
+        for tp in (1, 2, 4):
+            kw = {"tp_planes": [dev] * tp} if tp > 1 else {"devices": [dev] * d}
+            rt = abi.Runtime(abi.LWM_7B, d, kv_capacity=S + b * (ctx + 16), **kw)
+            ms = []
+            for k in range(3):
+                _, _, t = rt.prefill([k], [S], list(range(d)), [[(0, S)]], tokens=prompt)
+                rt.free_request(k)
+                if k:
+                    ms.append(t)
+            rng = np.random.default_rng(3)
+            for r in range(b):
+                rt.prefill([100 + r], [ctx], [0], [[(0, ctx)]],
+                           tokens=rng.integers(0, V, ctx).astype(np.int32))
+            dec = [rt.decode_step([0], [0], [100 + r for r in range(b)])[2] for _ in range(4)][1:]
+            rt.close()
+            out[f"tp{tp}"] = {"prefill_ms": statistics.median(ms),
+                              "decode_ms_per_step": statistics.median(dec)}
+    except Exception as e:  # report, never hide
+        out["error"] = str(e)[:200]
+    return out
 
 
 def bench_per_gpu_share(args):
