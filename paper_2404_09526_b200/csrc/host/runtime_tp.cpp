@@ -8,8 +8,8 @@
 // plane's heads / FFN columns), O and down row-parallel. Per layer the two
 // row-parallel projections write fp32 partials of the full hidden width; each
 // plane then adds ALL planes' partials, in plane order, to its replicated
-// residual stream (k::tp_reduce_residual, reading the other planes' partials
-// over NVLink) — every plane computes the same bits, so no broadcast follows.
+// residual stream (k::tp_reduce_residual_norm, reading the other planes'
+// partials over NVLink, fused with the next RMSNorm) — every plane computes the same bits, so no broadcast follows.
 // Attention needs no exchange: K1 / K3 run on the plane's own heads. The ESP
 // machinery is unchanged inside a plane: the ring prefill (striped rows,
 // retention into resting page slots) and multi-master split-KV decode run
@@ -239,7 +239,9 @@ void Runtime::prefill_tp(const esp_prefill_args& a,
       cudaStream_t s = dc.stream;
       bf16* x = static_cast<bf16*>(dc.x.ptr);
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-      k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s);
+      // layer 0 normalises the embeddings; later layers' xn came with the
+      // previous layer's down all-reduce
+      if (l == 0) k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s);
       k::GemmEpilogue ep;
       ep.kind = k::kEpiQkvRope;
       ep.q_out = static_cast<bf16*>(dc.q.ptr);
@@ -343,8 +345,7 @@ static void tp_dense_half(Runtime* /*self*/, std::vector<std::unique_ptr<DeviceC
     cudaStream_t s = dc.stream;
     bf16* x = static_cast<bf16*>(dc.x.ptr);
     bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-    k::tp_reduce_residual(x, po, static_cast<int64_t>(rows) * H, s);
-    k::rmsnorm(x, nullptr, nullptr, xn, rows, H, eps, s);
+    k::tp_reduce_residual_norm(x, po, xn, rows, H, eps, s);  // + the gate_up input norm
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = dc.h.ptr;
@@ -358,11 +359,11 @@ static void tp_dense_half(Runtime* /*self*/, std::vector<std::unique_ptr<DeviceC
     cuda_ok(cudaEventRecord(dc.tp_ev_d, s), "event");
   }
   wait_planes(planes, &DeviceCtx::tp_ev_d);
-  for (auto& pc : planes) {
+  for (auto& pc : planes) {  // + the next layer's QKV input norm
     DeviceCtx& dc = *pc;
     DeviceGuard g(dc.device);
-    k::tp_reduce_residual(static_cast<bf16*>(dc.x.ptr), pd, static_cast<int64_t>(rows) * H,
-                          dc.stream);
+    k::tp_reduce_residual_norm(static_cast<bf16*>(dc.x.ptr), pd, static_cast<bf16*>(dc.xn.ptr), rows,
+                               H, eps, dc.stream);
   }
 }
 
@@ -445,7 +446,7 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
       bf16* x = static_cast<bf16*>(dc.x.ptr);
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
       bf16* q = static_cast<bf16*>(dc.q.ptr);
-      k::rmsnorm(x, nullptr, nullptr, xn, b, H, cfg_.rms_eps, s);
+      if (l == 0) k::rmsnorm(x, nullptr, nullptr, xn, b, H, cfg_.rms_eps, s);
       k::GemmEpilogue ep;
       ep.kind = k::kEpiQkvRope;
       ep.q_out = q;

@@ -225,14 +225,17 @@ void init_weight(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tenso
 void init_weight_shard(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int tensor,
                        int layer, int layout, int64_t part, int64_t row_off, int64_t col_off,
                        int64_t cols_total, cudaStream_t s);
-// Tensor parallelism: x (bf16, elems) += sum over the planes' fp32 partials
-// (device pointers, any GPU of the runtime), summed in plane order.
+// Tensor parallelism: the planes' fp32 partials of a row-parallel GEMM
+// (device pointers, any GPU of the runtime).
 constexpr int kMaxTp = 8;
 struct TpParts {
   const float* p[kMaxTp] = {};
   int n = 0;
 };
-void tp_reduce_residual(bf16* x, const TpParts& parts, int64_t elems, cudaStream_t s);
+// x (rows x hidden) += the partials summed in plane order, then xn =
+// rmsnorm(x) with unit gain — one pass, the row kept in registers.
+void tp_reduce_residual_norm(bf16* x, const TpParts& parts, bf16* xn, int rows, int hidden,
+                             float eps, cudaStream_t s);
 void fill_bf16(bf16* dst, int64_t n, float v, cudaStream_t s);
 // w[r][c] *= gamma[c] (fold a norm gain into the consuming projection).
 void scale_cols(bf16* w, int64_t rows, int64_t cols, const bf16* gamma, cudaStream_t s);

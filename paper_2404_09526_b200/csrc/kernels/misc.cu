@@ -202,30 +202,6 @@ __global__ void init_weight_kernel(bf16* dst, int64_t rows, int64_t cols, uint64
   }
 }
 
-// Tensor-parallel all-reduce of a row-parallel projection (O, down), fused
-// with the residual: x += sum of the planes' fp32 partials, in plane order
-// (every plane computes the same bits), read over NVLink where the partials
-// live on other GPUs.
-__global__ void tp_reduce_residual_kernel(bf16* __restrict__ x, TpParts parts, int64_t n4) {
-  ptx::griddep_wait();  // the partials come from the row-parallel GEMMs
-  ptx::griddep_launch();
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float4 acc = reinterpret_cast<const float4*>(parts.p[0])[i];
-    for (int q = 1; q < parts.n; ++q) {
-      const float4 v = reinterpret_cast<const float4*>(parts.p[q])[i];
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
-    }
-    uint2* xp = reinterpret_cast<uint2*>(x) + i;
-    const uint2 old = *xp;
-    const float2 a = ptx::unpack_bf16(old.x), b = ptx::unpack_bf16(old.y);
-    *xp = make_uint2(ptx::pack_bf16(a.x + acc.x, a.y + acc.y), ptx::pack_bf16(b.x + acc.z, b.y + acc.w));
-  }
-}
-
 __global__ void fill_kernel(bf16* dst, int64_t n, float v) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -324,14 +300,92 @@ void init_weight_shard(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int
   count_launch();
 }
 
-void tp_reduce_residual(bf16* x, const TpParts& parts, int64_t elems, cudaStream_t s) {
-  if (elems <= 0) return;
-  if (elems % 4 != 0) throw std::runtime_error("tp_reduce_residual: elems % 4 != 0");
-  const int64_t n4 = elems / 4;
-  const int grid = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 148 * 16));
-  launch_pdl(2, tp_reduce_residual_kernel, dim3(grid), dim3(256), 0, s, x, parts, n4);
+// Tensor-parallel all-reduce of a row-parallel projection (O, down), fused
+// with the residual and the next layer norm (unit gain: gains are folded into
+// the consuming projections): x += the planes' fp32 partials summed in plane
+// order (every plane computes the same bits; the other planes' partials are
+// read over NVLink); one CTA per row, the row's new
+// residual kept in registers, xn = x_new * rsqrt(mean(x_new^2) + eps) exactly
+// as rmsnorm_kernel computes it from the stored bf16 x.
+template <int kPer>  // 8-column groups per thread
+__global__ void tp_reduce_norm_kernel(bf16* __restrict__ x, TpParts parts, bf16* __restrict__ xn,
+                                      int hidden, float eps) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * hidden;
+  uint4 keep[kPer];
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int c = (threadIdx.x + u * blockDim.x) * 8;
+    if (c >= hidden) break;
+    // the planes' partials in plane order, then the residual
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int q = 0; q < parts.n; ++q) {
+      const float4* pp = reinterpret_cast<const float4*>(parts.p[q] + base + c);
+      const float4 a = pp[0], b = pp[1];
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+      acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+    }
+    const uint4 xv = *reinterpret_cast<const uint4*>(x + base + c);
+    const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&xv);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(xp[j]);
+      acc[2 * j] = f.x + acc[2 * j];
+      acc[2 * j + 1] = f.y + acc[2 * j + 1];
+    }
+    uint4 o;
+    o.x = ptx::pack_bf16(acc[0], acc[1]);
+    o.y = ptx::pack_bf16(acc[2], acc[3]);
+    o.z = ptx::pack_bf16(acc[4], acc[5]);
+    o.w = ptx::pack_bf16(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(x + base + c) = o;
+    keep[u] = o;
+    const __nv_bfloat162* op = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(op[j]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  }
+  __shared__ float red[32];
+  for (int w = 16; w >= 1; w >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, w);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int w = 16; w >= 1; w >>= 1) t += __shfl_xor_sync(0xffffffff, t, w);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / static_cast<float>(hidden) + eps);
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int c = (threadIdx.x + u * blockDim.x) * 8;
+    if (c >= hidden) break;
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&keep[u]);
+    uint4 o;
+    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(p[j]);
+      op[j] = __floats2bfloat162_rn(f.x * inv, f.y * inv);
+    }
+    *reinterpret_cast<uint4*>(xn + base + c) = o;
+  }
+}
+
+void tp_reduce_residual_norm(bf16* x, const TpParts& parts, bf16* xn, int rows, int hidden,
+                             float eps, cudaStream_t s) {
+  if (rows <= 0) return;
+  if (hidden % 8 != 0 || hidden > 256 * 8 * 4) {
+    throw std::runtime_error("tp_reduce_residual_norm: hidden % 8 or > 8192");
+  }
+  launch_pdl(2, tp_reduce_norm_kernel<4>, dim3(rows), dim3(256), 0, s, x, parts, xn, hidden, eps);
   count_launch();
 }
+
 
 void scale_cols(bf16* w, int64_t rows, int64_t cols, const bf16* gamma, cudaStream_t s) {
   scale_cols_kernel<<<2048, 256, 0, s>>>(w, rows, cols, gamma);
