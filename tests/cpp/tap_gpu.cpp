@@ -24,7 +24,7 @@ using namespace espsim;
 namespace {
 
 int run(const char* name, const char* policy, int instances, TokenCount cap, bool exact_output,
-        std::vector<TraceRecord> trace, const std::string& sib_path) {
+        std::vector<TraceRecord> trace, const std::string& sib_path, int tp_degree = 1) {
   EngineParams params;
   params.exact_output_reservation = exact_output;
   params.bandwidth_tokens_per_ms = 800;
@@ -38,7 +38,13 @@ int run(const char* name, const char* policy, int instances, TokenCount cap, boo
   esp_model_config cfg{2, 512, 8, 64, 1536, 32000, 1e-5f, 10000.f, 1234};
   std::vector<int32_t> devices(static_cast<size_t>(instances), 0);
   esp_runtime* rt = nullptr;
-  if (esp_runtime_create(&cfg, instances, devices.data(), cap, &rt) != ESP_OK) {
+  // tp > 1: tensor-parallel instances (every instance spans tp planes, here
+  // all on GPU 0) — the engine and the tap are unchanged.
+  std::vector<int32_t> planes(static_cast<size_t>(tp_degree), 0);
+  const int made = tp_degree > 1
+                       ? esp_runtime_create_tp(&cfg, instances, tp_degree, planes.data(), cap, &rt)
+                          : esp_runtime_create(&cfg, instances, devices.data(), cap, &rt);
+  if (made != ESP_OK) {
     std::cerr << "create: " << esp_last_error() << "\n";
     return 2;
   }
@@ -126,5 +132,17 @@ int main(int argc, char** argv) {
   spec.seed = 5;
   rc |= run("chunked_48", "chunked:2048", 8, 160000, true, gen_trace(spec), sib);
   rc |= run("disagg_48", "disagg:2+6", 8, 160000, true, gen_trace(spec), sib);
+  // the same engine and tap over tensor-parallel instances
+  // (tp = 2 planes): config 1, the config-5 mixed trace, disaggregation with
+  // its handoff KV moves.
+  rc |= run("config1_tp2", "esp", 2, 200000, true, {{0, 4096, 64}}, sib, 2);
+  spec.requests_per_s = 0.5;
+  spec.count = 24;
+  spec.seed = 7;
+  rc |= run("config5_mixed_tp2", "esp", 8, 317000, false, gen_trace(spec), sib, 2);
+  spec.requests_per_s = 1.0;
+  spec.count = 48;
+  spec.seed = 5;
+  rc |= run("disagg_48_tp2", "disagg:2+6", 8, 160000, true, gen_trace(spec), sib, 2);
   return rc;
 }

@@ -4,7 +4,8 @@ scheduler, prebuilt in this container from /root/reference into oracle/_ref/
 around the reference's own policy and a DEVICE runtime — every prefill,
 decode step (with any chunked-prefill chunk) and KV move of configs 1 and 5, a
 denser mixed trace, and the chunked-prefill and disaggregation baselines
- executes real sm_100a kernels; page tables are verified at
+ executes real sm_100a kernels — also over tensor-parallel
+instances (tp = 2 planes); page tables are verified at
 every schedule() call and the event log must equal the untapped run's.
 Skipped only if the prebuilt binary is absent (build() was not run where
 /root/reference exists)."""
@@ -25,4 +26,4 @@ def test_reference_engine_drives_device_runtime():
     out = subprocess.run([EXE, SIB], capture_output=True, text=True, timeout=900)
     print(out.stdout)
     assert out.returncode == 0, out.stderr + out.stdout
-    assert out.stdout.count("events identical") == 6, out.stdout
+    assert out.stdout.count("events identical") == 9, out.stdout
