@@ -1004,6 +1004,7 @@ def multi_gpu(args, rank, world, dist, n):
         "transport": {k: res[k] for k in ("nvlink_p2p", "ring") if k in res},
         "nccl_ring_baseline": nccl,
         "decode": res.get("decode"),
+        "tensor_parallel": res.get("tensor_parallel"),
     }
     return line
 
@@ -1265,6 +1266,39 @@ def esp_child(args):
         out["decode"] = dec
     except Exception as e:  # report, never hide
         out["decode"] = {"error": str(e)[:300]}
+    # Tensor-parallel instances across GPUs: tp planes on the
+    # first tp GPUs, the per-layer all-reduces over NVLink peer reads; tp = 1
+    # on GPU devs[0] is the same work on one GPU.
+    saved_dom = os.environ.pop("ESP_DOMAIN_PER_INSTANCE", None)  # TP instances share domain 0
+    try:
+        tpo = {}
+        S_tp, b_tp, ctx_tp = min(16384, S), 16, 2048
+        for tp in [t for t in (1, 2, 4) if t <= n]:
+            kw = {"tp_planes": devs[:tp]} if tp > 1 else {"devices": [devs[0]] * 2}
+            rt = abi.Runtime(abi.LWM_7B, 2, kv_capacity=S_tp + b_tp * (ctx_tp + 16), **kw)
+            ms = []
+            for k in range(3):
+                _, _, t = rt.prefill([k], [S_tp], [0, 1], [[(0, S_tp)]], tokens=prompt[:S_tp])
+                rt.free_request(k)
+                if k:
+                    ms.append(t)
+            rng = np.random.default_rng(3)
+            for r in range(b_tp):
+                rt.prefill([100 + r], [ctx_tp], [0], [[(0, ctx_tp)]],
+                           tokens=rng.integers(0, V, ctx_tp).astype(np.int32))
+            dec = [rt.decode_step([0], [0], [100 + r for r in range(b_tp)])[2]
+                   for _ in range(4)][1:]
+            rt.close()
+            tpo[f"tp{tp}"] = {"planes": devs[:tp], "prefill_ms": statistics.median(ms),
+                              "decode_ms_per_step": statistics.median(dec)}
+        tpo["config"] = (f"LWM-7B {S_tp}-token prefill at ESP 2 (retention onto instance 0) and "
+                         f"a b={b_tp} x {ctx_tp} decode step; tp planes on GPUs listed")
+        out["tensor_parallel"] = tpo
+    except Exception as e:  # report, never hide
+        out["tensor_parallel"] = {"error": str(e)[:300]}
+    finally:
+        if saved_dom is not None:
+            os.environ["ESP_DOMAIN_PER_INSTANCE"] = saved_dom
     # NVLink peak: P2P copies GPU0 -> GPU1 (and both ways at once).
     phys = sorted(set(devs))
     if len(phys) >= 2:

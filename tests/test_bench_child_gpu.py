@@ -33,5 +33,8 @@ def test_esp_child_four_domains_one_gpu():
     assert ring["extra_migration_tokens"] == 0
     assert "error" not in j.get("prefill_window", {}), j.get("prefill_window")
     assert j["prefill_window"]["kv_ring_rows_per_gpu"] <= 3 * (4096 // 4)
+    tpo = j["tensor_parallel"]
+    assert "error" not in tpo, tpo
+    assert set(tpo) >= {"tp1", "tp2", "tp4"} and all(tpo[f"tp{t}"]["prefill_ms"] > 0 for t in (1, 2, 4))
     for key in ("scale_down", "decode"):
         assert key in j and "error" not in (j[key] or {}), (key, j.get(key))
