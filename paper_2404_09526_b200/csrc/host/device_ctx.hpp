@@ -64,7 +64,7 @@ struct DeviceCtx {
   // row-parallel O / down projections, read by every plane's all-reduce, and
   // the events marking them written.
   DevBuf tp_po, tp_pd;
-  cudaEvent_t tp_ev_o = nullptr, tp_ev_d = nullptr;
+  cudaEvent_t tp_ev_o = nullptr, tp_ev_d = nullptr, tp_ev_r = nullptr;
   // Side stream of the windowed ring: peer copies of the next round's block
   // run here while K1 of the current round runs on `stream`.
   cudaStream_t comm = nullptr;

@@ -214,6 +214,7 @@ Runtime::~Runtime() {
     for (cudaEvent_t e : dc.sync_events) cudaEventDestroy(e);
     if (dc.tp_ev_o) cudaEventDestroy(dc.tp_ev_o);
     if (dc.tp_ev_d) cudaEventDestroy(dc.tp_ev_d);
+    if (dc.tp_ev_r) cudaEventDestroy(dc.tp_ev_r);
     if (dc.e0) cudaEventDestroy(dc.e0);
     if (dc.e1) cudaEventDestroy(dc.e1);
     if (dc.stream) cudaStreamDestroy(dc.stream);

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <set>
 
@@ -118,6 +119,7 @@ void Runtime::init_device_tp(DeviceCtx& dc, int rank) {
   cuda_ok(cudaEventCreate(&dc.e1), "event");
   cuda_ok(cudaEventCreateWithFlags(&dc.tp_ev_o, cudaEventDisableTiming), "event");
   cuda_ok(cudaEventCreateWithFlags(&dc.tp_ev_d, cudaEventDisableTiming), "event");
+  cuda_ok(cudaEventCreateWithFlags(&dc.tp_ev_r, cudaEventDisableTiming), "event");
   const int64_t H = cfg_.hidden, F = cfg_.ffn, V = cfg_.vocab;
   const int64_t Hs = H / tp_, Fs = F / tp_;
   auto alloc = [&](int64_t n) {
@@ -227,8 +229,10 @@ void Runtime::prefill_tp(const esp_prefill_args& a,
     scratch<bf16>(dc.vb, static_cast<size_t>(rows) * Hs);
     scratch<bf16>(dc.attn, static_cast<size_t>(rows) * Hs);
     scratch<bf16>(dc.h, static_cast<size_t>(rows) * Fs);
-    scratch<float>(dc.tp_po, static_cast<size_t>(rows) * H);
-    scratch<float>(dc.tp_pd, static_cast<size_t>(rows) * H);
+    // reduce-scatter layout: tp blocks of ceil(rows / tp) rows
+    const size_t part_rows = static_cast<size_t>((rows + t - 1) / t) * t;
+    scratch<float>(dc.tp_po, part_rows * H);
+    scratch<float>(dc.tp_pd, part_rows * H);
     k::embed(d_tok, dc.embed, x, rows, H, s, nullptr);
   }
   for (int l = 0; l < cfg_.layers; ++l) {
@@ -319,52 +323,94 @@ void Runtime::prefill_tp(const esp_prefill_args& a,
   profiles_.push_back(ProfileRec{d, std::vector<int64_t>(a.input_lens, a.input_lens + n), ms});
 }
 
+// Rows per plane from which the all-reduces run as a reduce-scatter + all-
+// gather (prefill) instead of every plane reducing every row (decode).
+constexpr int kTpScatterRows = 128;
+
 static void tp_dense_half(Runtime* /*self*/, std::vector<std::unique_ptr<DeviceCtx>>& planes,
                           int l, int rows, int H, int F, int tp, float eps) {
   const int Hs = H / tp, Fs = F / tp;
-  k::TpParts po, pd;
-  for (auto& pc : planes) {
-    po.p[po.n++] = static_cast<const float*>(pc->tp_po.ptr);
-    pd.p[pd.n++] = static_cast<const float*>(pc->tp_pd.ptr);
-  }
+  // Reduce-scatter mode: row block q (R rows) of every plane's partial is
+  // stored by the GEMM epilogue straight into plane q's receive buffer, at
+  // block p for source plane p (peer stores while the GEMM runs); plane q
+  // then reduces its block locally and stores x to itself and plane 0 (the
+  // LM head's plane) and xn to every plane. All-reduce mode: each plane
+  // stores its own partial and every plane reduces every row, reading the
+  // others' partials.
+  // ESP_TP_ALLREDUCE=1: all-reduce mode at every row count (the bit-identity
+  // check of tests/test_tp_gpu.py — both modes sum in plane order)
+  const bool rs = rows >= kTpScatterRows * tp && std::getenv("ESP_TP_ALLREDUCE") == nullptr;
+  const int R = (rows + tp - 1) / tp;
+  auto partial = [&](int p, const bf16* a, int K, const bf16* w, DevBuf DeviceCtx::*buf) {
+    DeviceCtx& dc = *planes[p];
+    k::GemmEpilogue e;
+    e.kind = k::kEpiStoreF32;
+    e.ldo = H;
+    if (rs) {
+      e.route_rows = R;
+      for (int q = 0; q < tp; ++q) {
+        e.route[q] = static_cast<float*>(((*planes[q]).*buf).ptr) + static_cast<int64_t>(p) * R * H;
+      }
+    } else {
+      e.out = (dc.*buf).ptr;
+    }
+    k::gemm(a, K, w, K, rows, H, K, e, dc.stream);
+  };
+  auto reduce = [&](int p, DevBuf DeviceCtx::*buf) {
+    DeviceCtx& dc = *planes[p];
+    k::TpParts parts;
+    bf16* xo[k::kMaxTp];
+    bf16* xno[k::kMaxTp];
+    bf16* x = static_cast<bf16*>(dc.x.ptr);
+    if (rs) {
+      const int r0 = p * R, n = std::min(rows, r0 + R) - r0;
+      if (n <= 0) return;
+      const int64_t off = static_cast<int64_t>(r0) * H;
+      for (int q = 0; q < tp; ++q) {
+        parts.p[parts.n++] = static_cast<const float*>((dc.*buf).ptr) + static_cast<int64_t>(q) * R * H;
+        xno[q] = static_cast<bf16*>(planes[q]->xn.ptr) + off;
+      }
+      xo[0] = x + off;
+      int nx = 1;
+      if (p != 0) xo[nx++] = static_cast<bf16*>(planes[0]->x.ptr) + off;
+      k::tp_reduce_residual_norm(x + off, parts, xo, nx, xno, tp, n, H, eps, dc.stream);
+    } else {
+      for (auto& pc : planes) parts.p[parts.n++] = static_cast<const float*>(((*pc).*buf).ptr);
+      xo[0] = x;
+      xno[0] = static_cast<bf16*>(dc.xn.ptr);
+      k::tp_reduce_residual_norm(x, parts, xo, 1, xno, 1, rows, H, eps, dc.stream);
+    }
+    if (rs) cuda_ok(cudaEventRecord(dc.tp_ev_r, dc.stream), "event");
+  };
+  auto reduce_all = [&](DevBuf DeviceCtx::*buf) {
+    for (int p = 0; p < tp; ++p) {
+      DeviceGuard g(planes[p]->device);
+      reduce(p, buf);
+    }
+    if (rs) wait_planes(planes, &DeviceCtx::tp_ev_r);  // the all-gather has landed
+  };
   // O: attn (rows x Hs) . Wo_shard (H x Hs)^T -> fp32 partial (rows x H)
-  for (auto& pc : planes) {
-    DeviceCtx& dc = *pc;
+  for (int p = 0; p < tp; ++p) {
+    DeviceCtx& dc = *planes[p];
     DeviceGuard g(dc.device);
-    k::GemmEpilogue eo;
-    eo.kind = k::kEpiStoreF32;
-    eo.out = dc.tp_po.ptr;
-    eo.ldo = H;
-    k::gemm(static_cast<bf16*>(dc.attn.ptr), Hs, dc.layers[l].wo, Hs, rows, H, Hs, eo, dc.stream);
+    partial(p, static_cast<bf16*>(dc.attn.ptr), Hs, dc.layers[l].wo, &DeviceCtx::tp_po);
     cuda_ok(cudaEventRecord(dc.tp_ev_o, dc.stream), "event");
   }
   wait_planes(planes, &DeviceCtx::tp_ev_o);
-  for (auto& pc : planes) {
-    DeviceCtx& dc = *pc;
+  reduce_all(&DeviceCtx::tp_po);  // + the gate_up input norm
+  for (int p = 0; p < tp; ++p) {
+    DeviceCtx& dc = *planes[p];
     DeviceGuard g(dc.device);
-    cudaStream_t s = dc.stream;
-    bf16* x = static_cast<bf16*>(dc.x.ptr);
-    bf16* xn = static_cast<bf16*>(dc.xn.ptr);
-    k::tp_reduce_residual_norm(x, po, xn, rows, H, eps, s);  // + the gate_up input norm
     k::GemmEpilogue eg;
     eg.kind = k::kEpiSiluMul;
     eg.out = dc.h.ptr;
     eg.ldo = Fs;
-    k::gemm(xn, H, dc.layers[l].wgu, H, rows, 2 * Fs, H, eg, s);
-    k::GemmEpilogue ed;
-    ed.kind = k::kEpiStoreF32;
-    ed.out = dc.tp_pd.ptr;
-    ed.ldo = H;
-    k::gemm(static_cast<bf16*>(dc.h.ptr), Fs, dc.layers[l].wd, Fs, rows, H, Fs, ed, s);
-    cuda_ok(cudaEventRecord(dc.tp_ev_d, s), "event");
+    k::gemm(static_cast<bf16*>(dc.xn.ptr), H, dc.layers[l].wgu, H, rows, 2 * Fs, H, eg, dc.stream);
+    partial(p, static_cast<bf16*>(dc.h.ptr), Fs, dc.layers[l].wd, &DeviceCtx::tp_pd);
+    cuda_ok(cudaEventRecord(dc.tp_ev_d, dc.stream), "event");
   }
   wait_planes(planes, &DeviceCtx::tp_ev_d);
-  for (auto& pc : planes) {  // + the next layer's QKV input norm
-    DeviceCtx& dc = *pc;
-    DeviceGuard g(dc.device);
-    k::tp_reduce_residual_norm(static_cast<bf16*>(dc.x.ptr), pd, static_cast<bf16*>(dc.xn.ptr), rows,
-                               H, eps, dc.stream);
-  }
+  reduce_all(&DeviceCtx::tp_pd);  // + the next layer's QKV input norm
 }
 
 double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>& rows_v) {
@@ -434,8 +480,9 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
     scratch<bf16>(dc.h, static_cast<size_t>(b) * Fs);
     scratch<float>(dc.part_o, static_cast<size_t>(std::max(n_chunks, 1)) * hs * cfg_.head_dim);
     scratch<float>(dc.part_ml, static_cast<size_t>(std::max(n_chunks, 1)) * hs * 2);
-    scratch<float>(dc.tp_po, static_cast<size_t>(b) * H);
-    scratch<float>(dc.tp_pd, static_cast<size_t>(b) * H);
+    const size_t part_rows = static_cast<size_t>((b + t - 1) / t) * t;  // reduce-scatter layout
+    scratch<float>(dc.tp_po, part_rows * H);
+    scratch<float>(dc.tp_pd, part_rows * H);
     k::embed(d_tok, dc.embed, x, b, H, s, nullptr);
   }
   for (int l = 0; l < cfg_.layers; ++l) {

@@ -162,7 +162,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const Acc&
 #pragma unroll
         for (int i = 0; i < 32; ++i) atomicAdd(d + i, __uint_as_float(r[i]));
       } else if (ep.kind == kEpiStoreF32) {
-        float4* d = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + off);
+        float* row = ep.route_rows > 0
+                         ? ep.route[m / ep.route_rows] +
+                               static_cast<int64_t>(m % ep.route_rows) * ep.ldo
+                         : static_cast<float*>(ep.out) + static_cast<int64_t>(m) * ep.ldo;
+        float4* d = reinterpret_cast<float4*>(row + nb * BN + c);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           d[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),

@@ -16,6 +16,7 @@ using bf16 = __nv_bfloat16;
 
 constexpr int kMaxSlabs = 16;  // instances co-located on one device
 constexpr int kMaxPeers = 7;   // other transport domains of one ESP ring
+constexpr int kMaxTp = 8;      // tensor-parallel planes of one instance
 
 enum EpiKind : int {
   kEpiStore = 0,     // D = acc (bf16)
@@ -72,6 +73,12 @@ struct GemmEpilogue {
   float* ss_zero = nullptr;
   int norm_dim = 0;
   float norm_eps = 0.f;
+  // Reduce-scatter fused into the fp32 store (tensor-parallel planes): with
+  // route_rows > 0, row m of a kEpiStoreF32 tile goes to route[m /
+  // route_rows] + (m % route_rows) * ldo — row block q lands, by peer store
+  // from the epilogue, in plane q's receive buffer while the GEMM runs.
+  int route_rows = 0;
+  float* route[kMaxTp] = {};
 };
 
 // Schedule selection: kGemmAuto is the production dispatch; the others
@@ -226,16 +233,19 @@ void init_weight_shard(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int
                        int layer, int layout, int64_t part, int64_t row_off, int64_t col_off,
                        int64_t cols_total, cudaStream_t s);
 // Tensor parallelism: the planes' fp32 partials of a row-parallel GEMM
-// (device pointers, any GPU of the runtime).
-constexpr int kMaxTp = 8;
+// (device pointers, any GPU of the runtime; row r of part q at p[q] + r*hidden).
 struct TpParts {
   const float* p[kMaxTp] = {};
   int n = 0;
 };
-// x (rows x hidden) += the partials summed in plane order, then xn =
-// rmsnorm(x) with unit gain — one pass, the row kept in registers.
-void tp_reduce_residual_norm(bf16* x, const TpParts& parts, bf16* xn, int rows, int hidden,
-                             float eps, cudaStream_t s);
+// x_new = x (rows x hidden) + the partials summed in plane order, xn =
+// rmsnorm(x_new) with unit gain — one pass, the row kept in registers. x_new
+// is stored to every pointer of x_out (x itself may be one of them), xn to
+// every pointer of xn_out (1..8 each; peer pointers: the all-gather of a
+// reduce-scatter fused into its reduction).
+void tp_reduce_residual_norm(const bf16* x, const TpParts& parts, bf16* const* x_out, int n_x,
+                             bf16* const* xn_out, int n_xn, int rows, int hidden, float eps,
+                             cudaStream_t s);
 void fill_bf16(bf16* dst, int64_t n, float v, cudaStream_t s);
 // w[r][c] *= gamma[c] (fold a norm gain into the consuming projection).
 void scale_cols(bf16* w, int64_t rows, int64_t cols, const bf16* gamma, cudaStream_t s);

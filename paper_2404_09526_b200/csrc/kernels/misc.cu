@@ -304,11 +304,18 @@ void init_weight_shard(bf16* dst, int64_t rows, int64_t cols, uint64_t seed, int
 // with the residual and the next layer norm (unit gain: gains are folded into
 // the consuming projections): x += the planes' fp32 partials summed in plane
 // order (every plane computes the same bits; the other planes' partials are
-// read over NVLink); one CTA per row, the row's new
+// read over NVLink) — or, as the second half of a reduce-scatter, one row
+// block whose partials the GEMM epilogues already stored here, x and xn then
+// stored to every plane that needs them (the all-gather); one CTA per row, the row's new
 // residual kept in registers, xn = x_new * rsqrt(mean(x_new^2) + eps) exactly
 // as rmsnorm_kernel computes it from the stored bf16 x.
+struct TpOuts {
+  bf16* p[kMaxTp];
+  int n;
+};
+
 template <int kPer>  // 8-column groups per thread
-__global__ void tp_reduce_norm_kernel(bf16* __restrict__ x, TpParts parts, bf16* __restrict__ xn,
+__global__ void tp_reduce_norm_kernel(const bf16* x, TpParts parts, TpOuts x_out, TpOuts xn_out,
                                       int hidden, float eps) {
   ptx::griddep_wait();
   ptx::griddep_launch();
@@ -340,7 +347,7 @@ __global__ void tp_reduce_norm_kernel(bf16* __restrict__ x, TpParts parts, bf16*
     o.y = ptx::pack_bf16(acc[2], acc[3]);
     o.z = ptx::pack_bf16(acc[4], acc[5]);
     o.w = ptx::pack_bf16(acc[6], acc[7]);
-    *reinterpret_cast<uint4*>(x + base + c) = o;
+    for (int q = 0; q < x_out.n; ++q) *reinterpret_cast<uint4*>(x_out.p[q] + base + c) = o;
     keep[u] = o;
     const __nv_bfloat162* op = reinterpret_cast<const __nv_bfloat162*>(&o);
 #pragma unroll
@@ -372,17 +379,27 @@ __global__ void tp_reduce_norm_kernel(bf16* __restrict__ x, TpParts parts, bf16*
       const float2 f = __bfloat1622float2(p[j]);
       op[j] = __floats2bfloat162_rn(f.x * inv, f.y * inv);
     }
-    *reinterpret_cast<uint4*>(xn + base + c) = o;
+    for (int q = 0; q < xn_out.n; ++q) *reinterpret_cast<uint4*>(xn_out.p[q] + base + c) = o;
   }
 }
 
-void tp_reduce_residual_norm(bf16* x, const TpParts& parts, bf16* xn, int rows, int hidden,
-                             float eps, cudaStream_t s) {
+void tp_reduce_residual_norm(const bf16* x, const TpParts& parts, bf16* const* x_out, int n_x,
+                             bf16* const* xn_out, int n_xn, int rows, int hidden, float eps,
+                             cudaStream_t s) {
   if (rows <= 0) return;
   if (hidden % 8 != 0 || hidden > 256 * 8 * 4) {
     throw std::runtime_error("tp_reduce_residual_norm: hidden % 8 or > 8192");
   }
-  launch_pdl(2, tp_reduce_norm_kernel<4>, dim3(rows), dim3(256), 0, s, x, parts, xn, hidden, eps);
+  if (n_x < 1 || n_x > kMaxTp || n_xn < 1 || n_xn > kMaxTp) {
+    throw std::runtime_error("tp_reduce_residual_norm: 1..8 outputs");
+  }
+  TpOuts xo{}, xno{};
+  for (int q = 0; q < n_x; ++q) xo.p[q] = x_out[q];
+  for (int q = 0; q < n_xn; ++q) xno.p[q] = xn_out[q];
+  xo.n = n_x;
+  xno.n = n_xn;
+  launch_pdl(2, tp_reduce_norm_kernel<4>, dim3(rows), dim3(256), 0, s, x, parts, xo, xno, hidden,
+             eps);
   count_launch();
 }
 

@@ -48,6 +48,34 @@ def test_tp_prefill_decode_vs_oracle(shape, tp, d, S, steps):
     check_against_oracle(shape, prompt, toks, logits)
 
 
+@pytest.mark.parametrize("tp,lens", [(2, (1027, 333)), (4, (1031,))], ids=["tp2_ragged", "tp4_ragged"])
+def test_tp_reduce_scatter_bit_identical_to_all_reduce(tp, lens, monkeypatch):
+    """Prefill (rows >= 128 per plane) runs the all-reduces as a reduce-scatter
+    fused into the O / down GEMM epilogues (row block q stored into plane q's
+    buffer) + a reduction that stores x / xn to the planes; decode rows take
+    the all-reduce. Both sum the partials in plane order, so the logits are
+    bit-identical to forcing the all-reduce everywhere — here on row counts
+    tp does not divide, two requests in one prefill."""
+    shape = abi.TINY
+    rng = np.random.default_rng(29)
+    prompts = [rng.integers(0, shape.vocab, n).astype(np.int32) for n in lens]
+    outs = []
+    for force in (False, True):
+        if force:
+            monkeypatch.setenv("ESP_TP_ALLREDUCE", "1")
+        rt = abi.Runtime(shape, 2, kv_capacity=8192, tp_planes=[0] * tp)
+        try:
+            ids = list(range(len(lens)))
+            first, lg, _ = rt.prefill(ids, list(lens), [0, 1], [[(0, n)] for n in lens],
+                                      tokens=np.concatenate(prompts), want_logits=True)
+            dec = rt.decode_step([0], [0], ids, want_logits=True)
+            outs.append((np.asarray(first).copy(), np.asarray(lg).copy(), np.asarray(dec[1]).copy()))
+        finally:
+            rt.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
 def test_tp_multi_request_two_masters():
     """Two requests decoded together by two masters (requests dealt by
     assign_masters), KV of each on both instances, tp = 2: each request's
