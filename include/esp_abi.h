@@ -194,9 +194,9 @@ int esp_runtime_create(const esp_model_config* cfg, int32_t n_instances,
  * page tables and counters are those of a tp = 1 runtime, so every other
  * entry point keeps its meaning; ESP rings run co-located inside each plane.
  * tp in 2..8 dividing heads, hidden / tp % 128 == 0, ffn / tp % 64 == 0;
- * kv_capacity_tokens > 0 (KV moves copy every plane's shard). Not supported
- * with tp > 1: KV readback, attention capture, chunked-prefill chunks
- * (ESP_ERR_CONFIG). */
+ * kv_capacity_tokens > 0 (KV moves copy every plane's shard; KV readback
+ * assembles the planes' column shards). Not supported with tp > 1:
+ * attention capture, chunked-prefill chunks (ESP_ERR_CONFIG). */
 int esp_runtime_create_tp(const esp_model_config* cfg, int32_t n_instances, int32_t tp,
                           const int32_t* plane_device, int64_t kv_capacity_tokens,
                           esp_runtime** out);
@@ -315,7 +315,8 @@ int esp_last_prefill_stats(const esp_runtime* rt, esp_prefill_stats* out);
 /* Parity readback of a request's KV cache, one layer: K (after RoPE) and V
  * rows in TOKEN order (position 0 first), wherever the page tables put them
  * (any instance, any slot), as bf16 [n x hidden] into host buffers k_out /
- * v_out of cap rows. *n = the request's KV token count; with cap < *n
+ * v_out of cap rows (tp > 1: plane p's head shard in columns [p hidden/tp,
+ * (p+1) hidden/tp)). *n = the request's KV token count; with cap < *n
  * nothing is copied (size query). Device runtimes only (ESP_ERR_NO_DEVICE). */
 int esp_read_kv(esp_runtime* rt, int64_t request, int32_t layer, void* k_out, void* v_out,
                 int64_t cap, int64_t* n);

@@ -1371,42 +1371,52 @@ void Runtime::dump_profiles(const std::string& path) const {
 
 // ---- parity readback -----------------------------------------------------------------
 void Runtime::read_kv(RequestId r, int layer, void* k_out, void* v_out, int64_t cap, int64_t* n) {
-  if (tp_ > 1) throw ConfigError("read_kv is not supported with tp > 1");
   RequestRec& rr = req(r);
   const int64_t total = rr.kv_tokens();
   if (n) *n = total;
   if (layer < 0 || layer >= cfg_.layers) throw ConfigError("read_kv: layer out of range");
   if (devices_.empty()) throw NoDeviceError("read_kv needs a device runtime");
   if (cap < total) return;  // size query
+  // tp > 1: plane p holds columns [p H/tp, (p+1) H/tp) of every slot (same
+  // slot ids on every plane); the page list lives on plane 0's GPU.
   const size_t H = static_cast<size_t>(cfg_.hidden);
+  const size_t Hc = H / static_cast<size_t>(tp_);
   std::vector<uint16_t> kh, vh;
   for (auto& [iid, pl] : rr.pages) {
     const int64_t m = static_cast<int64_t>(pl.slots.size());
     if (m == 0) continue;
     InstanceRec& in = inst(iid);
-    DeviceCtx& dc = *devices_[static_cast<size_t>(in.domain)];
-    DeviceGuard g(dc.device);
-    cudaStream_t s = dc.stream;
-    sync_pages(pl, s);
-    std::vector<int32_t> zero(static_cast<size_t>(m), 0);
-    int32_t* d_slab = scratch<int32_t>(dc.ret_slab, static_cast<size_t>(m));
-    cuda_ok(cudaMemcpyAsync(d_slab, zero.data(), m * 4, cudaMemcpyHostToDevice, s), "h2d");
-    k::DecodeSlabs src{};
-    src.k[0] = in.layer_k(layer);
-    src.v[0] = in.layer_v(layer);
-    bf16* ko = scratch<bf16>(dc.kb, static_cast<size_t>(m) * H);
-    bf16* vo = scratch<bf16>(dc.vb, static_cast<size_t>(m) * H);
-    k::gather_rows(src, d_slab, pl.dev, static_cast<int>(m), ko, vo, static_cast<int>(H), s);
-    kh.resize(static_cast<size_t>(m) * H);
-    vh.resize(static_cast<size_t>(m) * H);
-    cuda_ok(cudaMemcpyAsync(kh.data(), ko, kh.size() * 2, cudaMemcpyDeviceToHost, s), "d2h");
-    cuda_ok(cudaMemcpyAsync(vh.data(), vo, vh.size() * 2, cudaMemcpyDeviceToHost, s), "d2h");
-    cuda_ok(cudaStreamSynchronize(s), "read_kv");
-    for (int64_t j = 0; j < m; ++j) {
-      const int64_t p = pl.pos[static_cast<size_t>(j)];
-      if (p < 0 || p >= total) throw InternalError("read_kv: token position out of range");
-      std::memcpy(static_cast<uint16_t*>(k_out) + p * H, kh.data() + j * H, H * 2);
-      std::memcpy(static_cast<uint16_t*>(v_out) + p * H, vh.data() + j * H, H * 2);
+    {
+      DeviceCtx& home = *devices_[static_cast<size_t>(tp_ > 1 ? 0 : in.domain)];
+      DeviceGuard g(home.device);
+      sync_pages(pl, home.stream);
+      cuda_ok(cudaStreamSynchronize(home.stream), "read_kv pages");
+    }
+    for (int p = 0; p < tp_; ++p) {
+      DeviceCtx& dc = *devices_[static_cast<size_t>(tp_ > 1 ? p : in.domain)];
+      DeviceGuard g(dc.device);
+      cudaStream_t s = dc.stream;
+      std::vector<int32_t> zero(static_cast<size_t>(m), 0);
+      int32_t* d_slab = scratch<int32_t>(dc.ret_slab, static_cast<size_t>(m));
+      cuda_ok(cudaMemcpyAsync(d_slab, zero.data(), m * 4, cudaMemcpyHostToDevice, s), "h2d");
+      k::DecodeSlabs src{};
+      src.k[0] = in.plane_k(p, layer);
+      src.v[0] = in.plane_v(p, layer);
+      bf16* ko = scratch<bf16>(dc.kb, static_cast<size_t>(m) * Hc);
+      bf16* vo = scratch<bf16>(dc.vb, static_cast<size_t>(m) * Hc);
+      k::gather_rows(src, d_slab, pl.dev, static_cast<int>(m), ko, vo, static_cast<int>(Hc), s);
+      kh.resize(static_cast<size_t>(m) * Hc);
+      vh.resize(static_cast<size_t>(m) * Hc);
+      cuda_ok(cudaMemcpyAsync(kh.data(), ko, kh.size() * 2, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_ok(cudaMemcpyAsync(vh.data(), vo, vh.size() * 2, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_ok(cudaStreamSynchronize(s), "read_kv");
+      for (int64_t j = 0; j < m; ++j) {
+        const int64_t q = pl.pos[static_cast<size_t>(j)];
+        if (q < 0 || q >= total) throw InternalError("read_kv: token position out of range");
+        const size_t off = static_cast<size_t>(q) * H + static_cast<size_t>(p) * Hc;
+        std::memcpy(static_cast<uint16_t*>(k_out) + off, kh.data() + j * Hc, Hc * 2);
+        std::memcpy(static_cast<uint16_t*>(v_out) + off, vh.data() + j * Hc, Hc * 2);
+      }
     }
   }
 }

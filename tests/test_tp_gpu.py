@@ -127,12 +127,42 @@ def test_tp_replays_reference_scenarios(scenario):
         check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)
 
 
+def test_tp_read_kv_assembles_plane_shards():
+    """read_kv on tp planes: plane p's slab holds columns [p H/tp, (p+1) H/tp)
+    of every slot; the readback assembles them per token position and agrees
+    with tp = 1's to bf16 rounding (layer 0: the same QKV dot products on a
+    smaller GEMM shape, a few ulp apart; a misplaced shard would be O(1) off).
+    A KV move (every plane's shard copied) leaves the readback unchanged."""
+    shape = abi.TINY
+    S = 700
+    p = np.random.default_rng(4).integers(0, shape.vocab, S).astype(np.int32)
+    reads = {}
+    for tp in (1, 2):
+        kw = {"tp_planes": [0] * tp} if tp > 1 else {"devices": [0, 0]}
+        rt = abi.Runtime(shape, 2, kv_capacity=4096, **kw)
+        try:
+            rt.prefill([1], [S], [0, 1], [[(1, 300), (0, S - 300)]], tokens=p)
+            reads[tp] = [rt.read_kv(1, l) for l in range(shape.layers)]
+            if tp > 1:
+                rt.move_kv(1, 1, 0, 300)
+                assert rt.placement(1) == {0: S}
+                moved = [rt.read_kv(1, l) for l in range(shape.layers)]
+                for (k0, v0), (k1, v1) in zip(reads[tp], moved):
+                    assert np.array_equal(k0, k1) and np.array_equal(v0, v1)
+        finally:
+            rt.close()
+    for l in range(shape.layers):
+        for a, b in zip(reads[1][l], reads[2][l]):
+            assert a.shape == b.shape == (S, shape.hidden)
+            fa, fb = abi.bf16_to_f32(a), abi.bf16_to_f32(b)
+            tol = 5e-3 if l == 0 else 2e-2
+            assert np.linalg.norm(fa - fb) <= tol * np.linalg.norm(fa), l
+
+
 def test_tp_unsupported_entry_points_fail_loudly():
     rt = abi.Runtime(abi.TINY, 2, kv_capacity=4096, tp_planes=[0, 0])
     try:
-        p = np.random.default_rng(1).integers(0, abi.TINY.vocab, 300).astype(np.int32)
-        rt.prefill([1], [300], [0, 1], [[(0, 300)]], tokens=p)
         with pytest.raises(abi.ConfigError):
-            rt.read_kv(1, 0)
+            rt.capture_attention([0])
     finally:
         rt.close()
