@@ -918,9 +918,19 @@ void Runtime::decode_step(const esp_decode_args& a) {
     return;
   }
   if (tp_ > 1) {
-    if (has_chunk) throw ConfigError("decode_step: a chunked-prefill chunk with tp > 1");
-    const double ms = decode_tp(a, rows_v);
-    if (b > 0) record_decode_profile(members, batch, a.n_masters, ms);
+    TpChunk tc;
+    if (has_chunk) {
+      tc.c = c;
+      tc.p_prev = p_prev;
+      tc.kv_slab = prev_slab;
+      tc.kv_slot = prev_slot;
+      tc.kv_slab.insert(tc.kv_slab.end(), ch_slab.begin(), ch_slab.end());
+      tc.kv_slot.insert(tc.kv_slot.end(), ch_slot.begin(), ch_slot.end());
+      tc.ch_slab = ch_slab;
+      tc.ch_slot = ch_slot;
+    }
+    const double ms = decode_tp(a, rows_v, tc);
+    if (b > 0 && !has_chunk) record_decode_profile(members, batch, a.n_masters, ms);
     return;
   }
   if (single_domain(involved) == nullptr) {

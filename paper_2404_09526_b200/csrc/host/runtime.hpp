@@ -198,7 +198,16 @@ class Runtime {
                    const std::vector<std::pair<InstanceId, int32_t>>& chunk_slots, double* ms);
   void decode_multi(const esp_decode_args& a, const std::vector<DecodeRow>& rows,
                     const std::vector<RequestId>& batch);
-  double decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>& rows);
+  // A chunked-prefill chunk riding on a tp decode step: earlier KV (slab,
+  // slot) in any order, then the chunk's own slots in token order.
+  struct TpChunk {
+    int c = 0;
+    int64_t p_prev = 0;
+    std::vector<int32_t> kv_slab, kv_slot;  // p_prev + c entries
+    std::vector<int32_t> ch_slab, ch_slot;  // c entries
+  };
+  double decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>& rows,
+                   const TpChunk& chunk);
   // The second half of a layer after attention: O projection (+ residual),
   // RMSNorm, gate_up (SiLU·up), down projection (+ residual), on `rows` rows
   // of dc's x / attn / xn / h buffers. Norm handling:

@@ -413,8 +413,9 @@ static void tp_dense_half(Runtime* /*self*/, std::vector<std::unique_ptr<DeviceC
   reduce_all(&DeviceCtx::tp_pd);  // + the next layer's QKV input norm
 }
 
-double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>& rows_v) {
-  const int b = static_cast<int>(rows_v.size()), t = tp_;
+double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>& rows_v,
+                          const TpChunk& ck) {
+  const int b = static_cast<int>(rows_v.size()), t = tp_, c = ck.c, rows = b + c;
   const int H = cfg_.hidden, F = cfg_.ffn, Hs = H / t, Fs = F / t, hs = cfg_.heads / t;
   DeviceCtx& d0 = *devices_[0];
   // Split-KV work (as on one GPU): every instance holding a request's KV
@@ -450,8 +451,31 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
     h_row_start.push_back(static_cast<int32_t>(chunks.size()));
     cuda_ok(cudaEventRecord(d0.e0, d0.stream), "event");
   }
+  // Chunk rows (a chunked prefill riding on the step): their K/V go to the
+  // chunk's slots from the QKV epilogue; attention over the gathered earlier
+  // KV + the chunk as one causal segment offset by p_prev (as on tp = 1).
+  for (int i = 0; i < c; ++i) {
+    h_tok.push_back(a.chunk_token_ids[i]);
+    h_pos.push_back(static_cast<int32_t>(ck.p_prev + i));
+    h_inst.push_back(ck.ch_slab[static_cast<size_t>(i)]);
+    h_slot.push_back(ck.ch_slot[static_cast<size_t>(i)]);
+  }
+  const int kv_n = static_cast<int>(ck.p_prev) + c;
+  std::vector<int32_t> work_sorted;
+  k::RingSegment sg{};
+  if (c > 0) {
+    sg.q_row0 = b;
+    sg.q_len = c;
+    sg.n_rounds = 1;
+    sg.kv_row0[0] = 0;
+    sg.kv_len[0] = kv_n;
+    sg.shift[0] = -static_cast<int32_t>(ck.p_prev);
+    std::vector<k::RingSegment> segs{sg};
+    build_attention_work(segs, hs, work_sorted);
+  }
+  const int n_work = attention_n_work(work_sorted);
   const int n_chunks = static_cast<int>(chunks.size());
-  int64_t max_pos = 1;
+  int64_t max_pos = std::max<int64_t>(1, ck.p_prev + c);
   for (const DecodeRow& rw : rows_v) max_pos = std::max<int64_t>(max_pos, rw.pos + 1);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
   for (auto& pc : devices_) {
@@ -460,30 +484,38 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
     cudaStream_t s = dc.stream;
     if (&dc != &d0) cuda_ok(cudaStreamWaitEvent(s, d0.e0, 0), "tp start");  // page uploads
     ensure_rope(dc, max_pos);
-    int32_t* d_tok = scratch<int32_t>(dc.tok, b);
-    cuda_ok(cudaMemcpyAsync(d_tok, h_tok.data(), b * 4, cudaMemcpyHostToDevice, s), "h2d");
-    cuda_ok(cudaMemcpyAsync(scratch<int32_t>(dc.pos, b), h_pos.data(), b * 4,
-                            cudaMemcpyHostToDevice, s), "h2d");
-    cuda_ok(cudaMemcpyAsync(scratch<int32_t>(dc.rinst, b), h_inst.data(), b * 4,
-                            cudaMemcpyHostToDevice, s), "h2d");
-    cuda_ok(cudaMemcpyAsync(scratch<int32_t>(dc.rslot, b), h_slot.data(), b * 4,
-                            cudaMemcpyHostToDevice, s), "h2d");
-    cuda_ok(cudaMemcpyAsync(scratch<int32_t>(dc.row_start, b + 1), h_row_start.data(), (b + 1) * 4,
-                            cudaMemcpyHostToDevice, s), "h2d");
+    auto up = [&](DevBuf& buf, const std::vector<int32_t>& v) {
+      cuda_ok(cudaMemcpyAsync(scratch<int32_t>(buf, std::max<size_t>(v.size(), 1)), v.data(),
+                              v.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
+    };
+    up(dc.tok, h_tok);
+    up(dc.pos, h_pos);
+    up(dc.rinst, h_inst);
+    up(dc.rslot, h_slot);
+    up(dc.row_start, h_row_start);
     cuda_ok(cudaMemcpyAsync(scratch<k::DecodeChunk>(dc.chunks, std::max(n_chunks, 1)), chunks.data(),
                             chunks.size() * sizeof(k::DecodeChunk), cudaMemcpyHostToDevice, s),
             "h2d");
-    bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(b) * H);
-    scratch<bf16>(dc.xn, static_cast<size_t>(b) * H);
-    scratch<bf16>(dc.q, static_cast<size_t>(b) * Hs);
-    scratch<bf16>(dc.attn, static_cast<size_t>(b) * Hs);
-    scratch<bf16>(dc.h, static_cast<size_t>(b) * Fs);
+    if (c > 0) {
+      up(dc.ret_slab, ck.kv_slab);
+      up(dc.ret_slot, ck.kv_slot);
+      cuda_ok(cudaMemcpyAsync(scratch<k::RingSegment>(dc.segs, 1), &sg, sizeof(sg),
+                              cudaMemcpyHostToDevice, s), "h2d");
+      up(dc.work, work_sorted);
+      scratch<bf16>(dc.kb, static_cast<size_t>(kv_n) * Hs);
+      scratch<bf16>(dc.vb, static_cast<size_t>(kv_n) * Hs);
+    }
+    bf16* x = scratch<bf16>(dc.x, static_cast<size_t>(rows) * H);
+    scratch<bf16>(dc.xn, static_cast<size_t>(rows) * H);
+    scratch<bf16>(dc.q, static_cast<size_t>(rows) * Hs);
+    scratch<bf16>(dc.attn, static_cast<size_t>(rows) * Hs);
+    scratch<bf16>(dc.h, static_cast<size_t>(rows) * Fs);
     scratch<float>(dc.part_o, static_cast<size_t>(std::max(n_chunks, 1)) * hs * cfg_.head_dim);
     scratch<float>(dc.part_ml, static_cast<size_t>(std::max(n_chunks, 1)) * hs * 2);
-    const size_t part_rows = static_cast<size_t>((b + t - 1) / t) * t;  // reduce-scatter layout
+    const size_t part_rows = static_cast<size_t>((rows + t - 1) / t) * t;  // reduce-scatter layout
     scratch<float>(dc.tp_po, part_rows * H);
     scratch<float>(dc.tp_pd, part_rows * H);
-    k::embed(d_tok, dc.embed, x, b, H, s, nullptr);
+    k::embed(static_cast<const int32_t*>(dc.tok.ptr), dc.embed, x, rows, H, s, nullptr);
   }
   for (int l = 0; l < cfg_.layers; ++l) {
     for (auto& pc : devices_) {
@@ -493,7 +525,7 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
       bf16* x = static_cast<bf16*>(dc.x.ptr);
       bf16* xn = static_cast<bf16*>(dc.xn.ptr);
       bf16* q = static_cast<bf16*>(dc.q.ptr);
-      if (l == 0) k::rmsnorm(x, nullptr, nullptr, xn, b, H, cfg_.rms_eps, s);
+      if (l == 0) k::rmsnorm(x, nullptr, nullptr, xn, rows, H, cfg_.rms_eps, s);
       k::GemmEpilogue ep;
       ep.kind = k::kEpiQkvRope;
       ep.q_out = q;
@@ -511,19 +543,32 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
         slabs.k[j] = ep.slab_k[j];
         slabs.v[j] = ep.slab_v[j];
       }
-      k::gemm(xn, H, dc.layers[l].wqkv, H, b, 3 * Hs, H, ep, s);
+      k::gemm(xn, H, dc.layers[l].wqkv, H, rows, 3 * Hs, H, ep, s);
       bf16* attn = static_cast<bf16*>(dc.attn.ptr);
-      const bool direct = n_chunks == b;  // one chunk per row: K3 normalises in place
-      k::decode_attention(q, static_cast<const k::DecodeChunk*>(dc.chunks.ptr), n_chunks, slabs, hs,
-                          cfg_.head_dim, scale, static_cast<float*>(dc.part_o.ptr),
-                          static_cast<float*>(dc.part_ml.ptr), s, nullptr, direct ? attn : nullptr);
-      if (!direct) {
-        k::decode_combine(static_cast<float*>(dc.part_o.ptr), static_cast<float*>(dc.part_ml.ptr),
-                          static_cast<const int32_t*>(dc.row_start.ptr), b, hs, cfg_.head_dim,
-                          attn, s);
+      if (b > 0) {
+        const bool direct = n_chunks == b;  // one chunk per row: K3 normalises in place
+        k::decode_attention(q, static_cast<const k::DecodeChunk*>(dc.chunks.ptr), n_chunks, slabs,
+                            hs, cfg_.head_dim, scale, static_cast<float*>(dc.part_o.ptr),
+                            static_cast<float*>(dc.part_ml.ptr), s, nullptr,
+                            direct ? attn : nullptr);
+        if (!direct) {
+          k::decode_combine(static_cast<float*>(dc.part_o.ptr),
+                            static_cast<float*>(dc.part_ml.ptr),
+                            static_cast<const int32_t*>(dc.row_start.ptr), b, hs, cfg_.head_dim,
+                            attn, s);
+        }
+      }
+      if (c > 0) {
+        bf16* kg = static_cast<bf16*>(dc.kb.ptr);
+        bf16* vg = static_cast<bf16*>(dc.vb.ptr);
+        k::gather_rows(slabs, static_cast<const int32_t*>(dc.ret_slab.ptr),
+                       static_cast<const int32_t*>(dc.ret_slot.ptr), kv_n, kg, vg, Hs, s);
+        k::ring_attention(q, kg, vg, attn, rows, kv_n, hs, cfg_.head_dim,
+                          static_cast<const k::RingSegment*>(dc.segs.ptr),
+                          static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
       }
     }
-    tp_dense_half(this, devices_, l, b, H, F, t, cfg_.rms_eps);
+    tp_dense_half(this, devices_, l, rows, H, F, t, cfg_.rms_eps);
   }
   for (auto& pc : devices_) {
     if (pc.get() == &d0) continue;
@@ -532,25 +577,39 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
     DeviceGuard g0(d0.device);
     cuda_ok(cudaStreamWaitEvent(d0.stream, pc->tp_ev_d, 0), "tp end");
   }
+  // Output rows: the decode rows, then the chunk's last token when the chunk
+  // completes the prompt (its first generated token, engine.cpp:570-579).
+  const bool chunk_out = c > 0 && a.chunk_final != 0;
+  const int n_out = b + (chunk_out ? 1 : 0);
+  std::vector<int32_t> out_rows(static_cast<size_t>(b));
+  for (int i = 0; i < b; ++i) out_rows[i] = i;
+  if (chunk_out) out_rows.push_back(rows - 1);
   DeviceGuard g(d0.device);
   cudaStream_t s = d0.stream;
+  int32_t* d_out_rows = scratch<int32_t>(d0.last_rows, std::max(n_out, 1));
+  cuda_ok(cudaMemcpyAsync(d_out_rows, out_rows.data(), n_out * 4, cudaMemcpyHostToDevice, s), "h2d");
   bf16* xn = static_cast<bf16*>(d0.xn.ptr);
-  k::rmsnorm(static_cast<bf16*>(d0.x.ptr), nullptr, d0.final_norm, xn, b, H, cfg_.rms_eps, s);
-  float* logits = scratch<float>(d0.logits, static_cast<size_t>(b) * cfg_.vocab);
-  k::GemmEpilogue ef;
-  ef.kind = k::kEpiStoreF32;
-  ef.out = logits;
-  ef.ldo = cfg_.vocab;
-  k::gemm(xn, H, d0.lm_head, H, b, cfg_.vocab, H, ef, s);
-  int32_t* d_out = scratch<int32_t>(d0.out_tok, b);
-  k::argmax_rows(logits, b, cfg_.vocab, d_out, s);
+  float* logits = scratch<float>(d0.logits, static_cast<size_t>(std::max(n_out, 1)) * cfg_.vocab);
+  int32_t* d_out = scratch<int32_t>(d0.out_tok, std::max(n_out, 1));
+  if (n_out > 0) {
+    k::rmsnorm(static_cast<bf16*>(d0.x.ptr), n_out == rows ? nullptr : d_out_rows, d0.final_norm,
+               xn, n_out, H, cfg_.rms_eps, s);
+    k::GemmEpilogue ef;
+    ef.kind = k::kEpiStoreF32;
+    ef.out = logits;
+    ef.ldo = cfg_.vocab;
+    k::gemm(xn, H, d0.lm_head, H, n_out, cfg_.vocab, H, ef, s);
+    k::argmax_rows(logits, n_out, cfg_.vocab, d_out, s);
+  }
   cuda_ok(cudaEventRecord(d0.e1, s), "event");
   check_cuda("tp decode launch");
-  std::vector<int32_t> out(static_cast<size_t>(b));
-  cuda_ok(cudaMemcpyAsync(out.data(), d_out, b * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  std::vector<int32_t> out(static_cast<size_t>(std::max(n_out, 1)));
+  if (n_out > 0) {
+    cuda_ok(cudaMemcpyAsync(out.data(), d_out, n_out * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  }
   std::vector<float> lg;
-  if (a.logits_out) {
-    lg.resize(static_cast<size_t>(b) * cfg_.vocab);
+  if ((a.logits_out && b > 0) || (chunk_out && a.chunk_logits_out)) {
+    lg.resize(static_cast<size_t>(n_out) * cfg_.vocab);
     cuda_ok(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
   }
   for (auto& pc : devices_) {
@@ -573,6 +632,18 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
       std::copy(lg.begin() + static_cast<int64_t>(ri) * cfg_.vocab,
                 lg.begin() + static_cast<int64_t>(ri + 1) * cfg_.vocab,
                 a.logits_out + static_cast<int64_t>(i) * cfg_.vocab);
+    }
+  }
+  if (c > 0) {
+    if (chunk_out) {
+      requests_[a.chunk_request].tokens.push_back(out[b]);
+      if (a.chunk_first_token_out) *a.chunk_first_token_out = out[b];
+      if (a.chunk_logits_out) {
+        std::copy(lg.begin() + static_cast<int64_t>(b) * cfg_.vocab,
+                  lg.begin() + static_cast<int64_t>(b + 1) * cfg_.vocab, a.chunk_logits_out);
+      }
+    } else if (a.chunk_first_token_out) {
+      *a.chunk_first_token_out = -1;
     }
   }
   return ms;

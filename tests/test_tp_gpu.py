@@ -127,6 +127,40 @@ def test_tp_replays_reference_scenarios(scenario):
         check_against_oracle(abi.TINY, rec.prompts[r], toks, lgs)
 
 
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_chunked_prefill_replay(tp):
+    """The reference's "chunked:512" decisions (scenario_tiny_chunked.jsonl,
+    policies.cpp:297-405) on tp planes: prompt chunks ride on decode steps
+    (engine.cpp:432-462), each chunk's rows attend per plane over its head
+    shard of the gathered earlier KV + the chunk (one causal segment offset
+    by the chunk start); tokens and logits against the dense oracle."""
+    path = os.path.join(GOLD, "scenario_tiny_chunked.jsonl")
+    head, _, _ = replay.load(path)
+    rt = abi.Runtime(abi.TINY, head["instances"], kv_capacity=head["kv_capacity"],
+                     tp_planes=[0] * tp)
+    prompts = {r["id"]: replay.prompt_tokens(r["id"], r["input_len"]) for r in head["requests"]}
+    toks = {r: [] for r in prompts}
+    logits = {r: [] for r in prompts}
+
+    def on_decode(d, members):
+        ch = replay.chunk_of(d, prompts.get(d["chunk_request"]))
+        out, lg, _ = rt.decode_step(members, d["masters"], d["batch"], want_logits=True, chunk=ch)
+        for i, r in enumerate(d["batch"]):
+            toks[r].append(int(out[i]))
+            logits[r].append(lg[i])
+        if ch is not None and ch["final"]:
+            toks[ch["request"]].append(ch["first_token"])
+            logits[ch["request"]].append(ch["logits"])
+
+    try:
+        replay.replay(rt, path, on_decode=on_decode, conservation=True)
+    finally:
+        rt.close()
+    for r, p in prompts.items():
+        assert toks[r], r
+        check_against_oracle(abi.TINY, p, toks[r], logits[r])
+
+
 def test_tp_read_kv_assembles_plane_shards():
     """read_kv on tp planes: plane p's slab holds columns [p H/tp, (p+1) H/tp)
     of every slot; the readback assembles them per token position and agrees
