@@ -195,9 +195,8 @@ int esp_runtime_create(const esp_model_config* cfg, int32_t n_instances,
  * entry point keeps its meaning; ESP rings run co-located inside each plane.
  * tp in 2..8 dividing heads, hidden / tp % 128 == 0, ffn / tp % 64 == 0;
  * kv_capacity_tokens > 0 (KV moves copy every plane's shard; KV readback
- * assembles the planes' column shards; chunked-prefill chunks run per
- * plane over their head shard). Not supported with tp > 1: attention
- * capture (ESP_ERR_CONFIG). */
+ * and attention capture assemble the planes' column shards; chunked-
+ * prefill chunks run per plane over their head shard). */
 int esp_runtime_create_tp(const esp_model_config* cfg, int32_t n_instances, int32_t tp,
                           const int32_t* plane_device, int64_t kv_capacity_tokens,
                           esp_runtime** out);

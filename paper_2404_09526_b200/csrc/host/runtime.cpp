@@ -1432,7 +1432,6 @@ void Runtime::read_kv(RequestId r, int layer, void* k_out, void* v_out, int64_t 
 }
 
 void Runtime::capture_attention(const int64_t* pos, int64_t n) {
-  if (tp_ > 1) throw ConfigError("attention capture is not supported with tp > 1");
   if (devices_.empty()) throw NoDeviceError("capture_attention needs a device runtime");
   cap_pos_.assign(pos, pos + n);
   cap_armed_ = n > 0;
@@ -1457,7 +1456,7 @@ void Runtime::cap_layer(DeviceCtx& dc, int l, const bf16* attn, cudaStream_t s) 
   if (it == cap_dom_.end() || it->second.rows.empty()) return;
   CapDomain& c = it->second;
   const int m = static_cast<int>(c.rows.size());
-  const size_t H = static_cast<size_t>(cfg_.hidden);
+  const size_t H = static_cast<size_t>(cfg_.hidden / tp_);  // tp > 1: this plane's head columns
   if (!c.d_rows) {
     cuda_ok(cudaMalloc(&c.d_rows, static_cast<size_t>(m) * 4), "cudaMalloc(capture)");
     cuda_ok(cudaMalloc(&c.d_buf, static_cast<size_t>(cfg_.layers) * m * H * 2), "cudaMalloc(capture)");
@@ -1470,18 +1469,20 @@ void Runtime::cap_layer(DeviceCtx& dc, int l, const bf16* attn, cudaStream_t s) 
 
 void Runtime::cap_finish() {
   const size_t H = static_cast<size_t>(cfg_.hidden), N = cap_pos_.size();
+  const size_t Hc = H / static_cast<size_t>(tp_);  // tp > 1: domain = plane, its head columns
   cap_host_.assign(static_cast<size_t>(cfg_.layers) * N * H, 0);
   for (auto& [dom, c] : cap_dom_) {
     const size_t m = c.rows.size();
     if (m == 0 || !c.d_buf) continue;
     DeviceCtx& dc = *devices_[static_cast<size_t>(dom)];
     DeviceGuard g(dc.device);
-    std::vector<uint16_t> h(static_cast<size_t>(cfg_.layers) * m * H);
+    std::vector<uint16_t> h(static_cast<size_t>(cfg_.layers) * m * Hc);
     cuda_ok(cudaMemcpy(h.data(), c.d_buf, h.size() * 2, cudaMemcpyDeviceToHost), "d2h");
+    const size_t col = tp_ > 1 ? static_cast<size_t>(dom) * Hc : 0;
     for (int l = 0; l < cfg_.layers; ++l) {
       for (size_t j = 0; j < m; ++j) {
-        std::memcpy(cap_host_.data() + (static_cast<size_t>(l) * N + c.idx[j]) * H,
-                    h.data() + (static_cast<size_t>(l) * m + j) * H, H * 2);
+        std::memcpy(cap_host_.data() + (static_cast<size_t>(l) * N + c.idx[j]) * H + col,
+                    h.data() + (static_cast<size_t>(l) * m + j) * Hc, Hc * 2);
       }
     }
     cudaFree(c.d_rows);

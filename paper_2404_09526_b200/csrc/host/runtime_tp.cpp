@@ -187,11 +187,20 @@ void Runtime::prefill_tp(const esp_prefill_args& a,
                          const std::vector<std::vector<int32_t>>& tok_slab,
                          const std::vector<std::vector<int32_t>>& tok_slot,
                          const std::vector<int64_t>& tok_base) {
-  if (cap_armed_) throw ConfigError("attention capture is not supported with tp > 1");
   const int n = a.n_requests, d = a.dop, t = tp_;
   const int H = cfg_.hidden, F = cfg_.ffn, Hs = H / t, Fs = F / t, hs = cfg_.heads / t;
   const StripePlan sp = plan_stripes(a, tok_slab, tok_slot, tok_base);
   const int rows = sp.rows;
+  if (cap_armed_) {  // parity capture: the same stripe rows on every plane (its head columns)
+    if (n != 1) throw ConfigError("attention capture needs a single-request prefill");
+    for (size_t c = 0; c < cap_pos_.size(); ++c) {
+      const int64_t tt = cap_pos_[c];
+      if (tt < 0 || tt >= a.input_lens[0]) throw ConfigError("capture position outside the prompt");
+      for (int p = 0; p < t; ++p) {
+        cap_add(p, sp.row0[tt % d][0] + static_cast<int32_t>(tt / d), static_cast<int32_t>(c));
+      }
+    }
+  }
   std::vector<int32_t> work_sorted;
   build_attention_work(sp.segs, hs, work_sorted);
   const int n_work = attention_n_work(work_sorted);
@@ -268,6 +277,7 @@ void Runtime::prefill_tp(const esp_prefill_args& a,
                         static_cast<bf16*>(dc.vb.ptr), static_cast<bf16*>(dc.attn.ptr), rows, rows,
                         hs, cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr),
                         static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
+      if (cap_armed_) cap_layer(dc, l, static_cast<bf16*>(dc.attn.ptr), s);
     }
     tp_dense_half(this, devices_, l, rows, H, F, t, cfg_.rms_eps);
   }
@@ -311,6 +321,7 @@ void Runtime::prefill_tp(const esp_prefill_args& a,
     DeviceGuard gp(pc->device);
     cuda_ok(cudaStreamSynchronize(pc->stream), "tp prefill");
   }
+  if (cap_armed_) cap_finish();
   float ms = 0;
   cuda_ok(cudaEventElapsedTime(&ms, d0.e0, d0.e1), "elapsed");
   if (a.device_ms_out) *a.device_ms_out = ms;

@@ -193,10 +193,26 @@ def test_tp_read_kv_assembles_plane_shards():
             assert np.linalg.norm(fa - fb) <= tol * np.linalg.norm(fa), l
 
 
-def test_tp_unsupported_entry_points_fail_loudly():
-    rt = abi.Runtime(abi.TINY, 2, kv_capacity=4096, tp_planes=[0, 0])
-    try:
-        with pytest.raises(abi.ConfigError):
-            rt.capture_attention([0])
-    finally:
-        rt.close()
+def test_tp_attention_capture_assembles_plane_shards():
+    """Attention capture on tp planes: each plane copies its head columns of
+    the captured stripe rows after K1; the capture assembles them per
+    position and agrees with tp = 1's to bf16 rounding (a misplaced shard or
+    stripe row would be O(1) off)."""
+    shape, S, d = abi.TINY, 900, 2
+    p = np.random.default_rng(8).integers(0, shape.vocab, S).astype(np.int32)
+    pos = [0, 1, 7, 450, 451, S - 1]
+    caps = {}
+    for tp in (1, 2):
+        kw = {"tp_planes": [0] * tp} if tp > 1 else {"devices": [0] * d}
+        rt = abi.Runtime(shape, d, kv_capacity=4096, **kw)
+        try:
+            rt.capture_attention(pos)
+            rt.prefill([1], [S], list(range(d)), [[(0, S)]], tokens=p)
+            caps[tp] = abi.bf16_to_f32(rt.captured_attention())
+        finally:
+            rt.close()
+    assert caps[1].shape == caps[2].shape == (shape.layers, len(pos), shape.hidden)
+    for l in range(shape.layers):
+        a, b = caps[1][l], caps[2][l]
+        tol = 1e-2 if l == 0 else 3e-2
+        assert np.linalg.norm(a - b) <= tol * np.linalg.norm(a), l
