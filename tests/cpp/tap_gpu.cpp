@@ -133,8 +133,8 @@ int main(int argc, char** argv) {
   rc |= run("chunked_48", "chunked:2048", 8, 160000, true, gen_trace(spec), sib);
   rc |= run("disagg_48", "disagg:2+6", 8, 160000, true, gen_trace(spec), sib);
   // the same engine and tap over tensor-parallel instances
-  // (tp = 2 planes): config 1, the config-5 mixed trace, disaggregation with
-  // its handoff KV moves.
+  // (tp = 2 planes): config 1, the config-5 mixed trace, chunked prefill
+  // (chunks on tp decode steps), disaggregation with its handoff KV moves.
   rc |= run("config1_tp2", "esp", 2, 200000, true, {{0, 4096, 64}}, sib, 2);
   spec.requests_per_s = 0.5;
   spec.count = 24;
@@ -143,6 +143,7 @@ int main(int argc, char** argv) {
   spec.requests_per_s = 1.0;
   spec.count = 48;
   spec.seed = 5;
+  rc |= run("chunked_48_tp2", "chunked:2048", 8, 160000, true, gen_trace(spec), sib, 2);
   rc |= run("disagg_48_tp2", "disagg:2+6", 8, 160000, true, gen_trace(spec), sib, 2);
   return rc;
 }

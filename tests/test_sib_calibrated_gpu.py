@@ -52,7 +52,7 @@ def test_calibrated_sib_drives_reference_scheduler(tmp_path):
     out = subprocess.run([EXE, path], capture_output=True, text=True, timeout=900)
     print(out.stdout)
     assert out.returncode == 0, out.stderr + out.stdout
-    assert out.stdout.count("events identical") == 9, out.stdout
+    assert out.stdout.count("events identical") == 10, out.stdout
 
 
 SIB_7B = os.path.join(ROOT, "profiles", "r01s2_sib_b200_7b.jsonl")
@@ -69,4 +69,4 @@ def test_lwm7b_calibrated_sib_tap():
     out = subprocess.run([EXE, SIB_7B], capture_output=True, text=True, timeout=900)
     print(out.stdout)
     assert out.returncode == 0, out.stderr + out.stdout
-    assert out.stdout.count("events identical") == 9, out.stdout
+    assert out.stdout.count("events identical") == 10, out.stdout

@@ -26,4 +26,4 @@ def test_reference_engine_drives_device_runtime():
     out = subprocess.run([EXE, SIB], capture_output=True, text=True, timeout=900)
     print(out.stdout)
     assert out.returncode == 0, out.stderr + out.stdout
-    assert out.stdout.count("events identical") == 9, out.stdout
+    assert out.stdout.count("events identical") == 10, out.stdout
