@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <stdexcept>
+#include <type_traits>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -314,12 +315,29 @@ struct TpOuts {
   int n;
 };
 
-template <int kPer>  // 8-column groups per thread
+template <int kPer, int kNP>  // 8-column groups per thread, partials (planes)
 __global__ void tp_reduce_norm_kernel(const bf16* x, TpParts parts, TpOuts x_out, TpOuts xn_out,
                                       int hidden, float eps) {
   ptx::griddep_wait();
   ptx::griddep_launch();
   const int64_t base = static_cast<int64_t>(blockIdx.x) * hidden;
+  // every load of the row slice issued before the first add (kPer x kNP x 32 B
+  // of partials + kPer x 16 B of x in flight per thread)
+  float4 pa[kPer][kNP][2];
+  uint4 xs[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int c = (threadIdx.x + u * blockDim.x) * 8;
+    if (c < hidden) {
+#pragma unroll
+      for (int q = 0; q < kNP; ++q) {
+        const float4* pp = reinterpret_cast<const float4*>(parts.p[q] + base + c);
+        pa[u][q][0] = pp[0];
+        pa[u][q][1] = pp[1];
+      }
+      xs[u] = *reinterpret_cast<const uint4*>(x + base + c);
+    }
+  }
   uint4 keep[kPer];
   float ss = 0.f;
 #pragma unroll
@@ -328,13 +346,13 @@ __global__ void tp_reduce_norm_kernel(const bf16* x, TpParts parts, TpOuts x_out
     if (c >= hidden) break;
     // the planes' partials in plane order, then the residual
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int q = 0; q < parts.n; ++q) {
-      const float4* pp = reinterpret_cast<const float4*>(parts.p[q] + base + c);
-      const float4 a = pp[0], b = pp[1];
+#pragma unroll
+    for (int q = 0; q < kNP; ++q) {
+      const float4 a = pa[u][q][0], b = pa[u][q][1];
       acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
       acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
     }
-    const uint4 xv = *reinterpret_cast<const uint4*>(x + base + c);
+    const uint4 xv = xs[u];
     const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&xv);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -347,7 +365,10 @@ __global__ void tp_reduce_norm_kernel(const bf16* x, TpParts parts, TpOuts x_out
     o.y = ptx::pack_bf16(acc[2], acc[3]);
     o.z = ptx::pack_bf16(acc[4], acc[5]);
     o.w = ptx::pack_bf16(acc[6], acc[7]);
-    for (int q = 0; q < x_out.n; ++q) *reinterpret_cast<uint4*>(x_out.p[q] + base + c) = o;
+#pragma unroll
+    for (int q = 0; q < kMaxTp; ++q) {  // unrolled: the pointer table stays in the param bank
+      if (q < x_out.n) *reinterpret_cast<uint4*>(x_out.p[q] + base + c) = o;
+    }
     keep[u] = o;
     const __nv_bfloat162* op = reinterpret_cast<const __nv_bfloat162*>(&o);
 #pragma unroll
@@ -379,7 +400,10 @@ __global__ void tp_reduce_norm_kernel(const bf16* x, TpParts parts, TpOuts x_out
       const float2 f = __bfloat1622float2(p[j]);
       op[j] = __floats2bfloat162_rn(f.x * inv, f.y * inv);
     }
-    for (int q = 0; q < xn_out.n; ++q) *reinterpret_cast<uint4*>(xn_out.p[q] + base + c) = o;
+#pragma unroll
+    for (int q = 0; q < kMaxTp; ++q) {
+      if (q < xn_out.n) *reinterpret_cast<uint4*>(xn_out.p[q] + base + c) = o;
+    }
   }
 }
 
@@ -398,8 +422,27 @@ void tp_reduce_residual_norm(const bf16* x, const TpParts& parts, bf16* const* x
   for (int q = 0; q < n_xn; ++q) xno.p[q] = xn_out[q];
   xo.n = n_x;
   xno.n = n_xn;
-  launch_pdl(2, tp_reduce_norm_kernel<4>, dim3(rows), dim3(256), 0, s, x, parts, xo, xno, hidden,
-             eps);
+  auto go = [&](auto kern) {
+    launch_pdl(2, kern, dim3(rows), dim3(256), 0, s, x, parts, xo, xno, hidden, eps);
+  };
+  const int per = (hidden + 2047) / 2048;  // 8-column groups per thread at 256 threads
+  auto by_np = [&](auto per_c) {
+    constexpr int P = decltype(per_c)::value;
+    switch (parts.n) {
+      case 1: go(tp_reduce_norm_kernel<P, 1>); break;
+      case 2: go(tp_reduce_norm_kernel<P, 2>); break;
+      case 3: go(tp_reduce_norm_kernel<P, 3>); break;
+      case 4: go(tp_reduce_norm_kernel<P, 4>); break;
+      case 5: go(tp_reduce_norm_kernel<P, 5>); break;
+      case 6: go(tp_reduce_norm_kernel<P, 6>); break;
+      case 7: go(tp_reduce_norm_kernel<P, 7>); break;
+      case 8: go(tp_reduce_norm_kernel<P, 8>); break;
+      default: throw std::runtime_error("tp_reduce_residual_norm: 1..8 partials");
+    }
+  };
+  if (per <= 1) by_np(std::integral_constant<int, 1>{});
+  else if (per == 2) by_np(std::integral_constant<int, 2>{});
+  else by_np(std::integral_constant<int, 4>{});
   count_launch();
 }
 
