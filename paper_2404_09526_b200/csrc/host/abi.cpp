@@ -584,6 +584,8 @@ int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_sl
       }
     }
     const int32_t n_parts = static_cast<int32_t>(ch.size());
+    int max_n = 0;  // the short-chunk kernel when every chunk is <= 64 tokens
+    for (const auto& c : ch) max_n = std::max(max_n, static_cast<int>(c.n));
     for (int r = 0; r < batch; ++r) row_start[r + 1] += row_start[r];
     DevMem dch(ch.size() * sizeof(esp::k::DecodeChunk) + 16), drs(row_start.size() * 4);
     DevMem po(static_cast<size_t>(n_parts) * heads * head_dim * 4 + 16);
@@ -596,7 +598,7 @@ int esp_k_decode_attention(const void* q, int32_t batch, const void* const* k_sl
     esp::k::decode_attention(static_cast<const esp::k::bf16*>(q),
                              static_cast<const esp::k::DecodeChunk*>(dch.p), n_parts, slabs,
                              heads, head_dim, scale, static_cast<float*>(po.p),
-                             static_cast<float*>(pml.p), s);
+                             static_cast<float*>(pml.p), s, nullptr, nullptr, max_n);
     if (out_f32) {
       esp::k::decode_combine_f32(static_cast<float*>(po.p), static_cast<float*>(pml.p),
                                  static_cast<int32_t*>(drs.p), batch, heads, head_dim,

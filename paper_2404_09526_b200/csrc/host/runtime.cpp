@@ -1001,6 +1001,8 @@ void Runtime::decode_step(const esp_decode_args& a) {
     h_slot.push_back(ch_slot[i]);
   }
   const int n_chunks = static_cast<int>(chunks.size());
+  int max_chunk = 0;
+  for (const k::DecodeChunk& ch : chunks) max_chunk = std::max(max_chunk, static_cast<int>(ch.n));
   int64_t max_pos = p_prev + c;
   for (const Row& rw : rows_v) max_pos = std::max<int64_t>(max_pos, rw.pos + 1);
   ensure_rope(dc, max_pos);
@@ -1109,7 +1111,7 @@ void Runtime::decode_step(const esp_decode_args& a) {
       const bool direct = n_chunks == b;
       timed(kPhDecodeAttn, s, [&] {
         k::decode_attention(q, d_chunks, n_chunks, slabs, cfg_.heads, cfg_.head_dim, scale,
-                            part_o, part_ml, s, nullptr, direct ? attn : nullptr);
+                            part_o, part_ml, s, nullptr, direct ? attn : nullptr, max_chunk);
       });
       if (!direct) {
         timed(kPhCombine, s, [&] {

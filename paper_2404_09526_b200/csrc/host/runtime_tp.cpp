@@ -486,6 +486,8 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
   }
   const int n_work = attention_n_work(work_sorted);
   const int n_chunks = static_cast<int>(chunks.size());
+  int max_chunk = 0;
+  for (const k::DecodeChunk& ch : chunks) max_chunk = std::max(max_chunk, static_cast<int>(ch.n));
   int64_t max_pos = std::max<int64_t>(1, ck.p_prev + c);
   for (const DecodeRow& rw : rows_v) max_pos = std::max<int64_t>(max_pos, rw.pos + 1);
   const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
@@ -561,7 +563,7 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
         k::decode_attention(q, static_cast<const k::DecodeChunk*>(dc.chunks.ptr), n_chunks, slabs,
                             hs, cfg_.head_dim, scale, static_cast<float*>(dc.part_o.ptr),
                             static_cast<float*>(dc.part_ml.ptr), s, nullptr,
-                            direct ? attn : nullptr);
+                            direct ? attn : nullptr, max_chunk);
         if (!direct) {
           k::decode_combine(static_cast<float*>(dc.part_o.ptr),
                             static_cast<float*>(dc.part_ml.ptr),

@@ -351,7 +351,7 @@ void gather_rows(const DecodeSlabs& src, const int32_t* slab, const int32_t* slo
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
                       float* part_o, float* part_ml, cudaStream_t s, const PartDst* dst,
-                      bf16* direct_out) {
+                      bf16* direct_out, int max_chunk) {
   if (n_chunks <= 0) return;
   const PartDst pd = dst ? *dst : PartDst{};
   if (n_chunks > 65535) throw std::runtime_error("decode_attention: more than 65535 chunks");
@@ -364,7 +364,31 @@ void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
   // shared-memory ring (3.3-4.0 TB/s — its ring caps resident CTAs per SM)
   // and the LSE combine fused into the last CTA of each (row, head) (0.1-0.3
   // ms/step slower: the fence + counter extend every CTA).
-  if (head_dim == 128) {
+  // Latency-bound launches (the whole grid fits in one wave of 4 CTAs per
+  // SM, e.g. b = 16 requests at contexts <= 512 tokens: 512 CTAs): 8 warps x
+  // 2 tokens x 4 unrolled = 64 tokens' K/V loads in flight per CTA per
+  // iteration (24 in the default kernel). Measured LWM-7B decode steps:
+  // b = 16 at 64-token contexts 3.18 -> 3.13 ms, 200: 3.46 -> 3.33, 400:
+  // 3.93 -> 3.59; b = 1 at 8K 4.6-4.8 -> 4.25-4.29; b = 4 at 2K 4.23 -> 4.27
+  // (even); at b = 16 x 8K (8192 CTAs, throughput-bound) the default
+  // kernel's 8 CTAs per SM with the slot-id look-ahead win (13.9-14.2 vs 15.0).
+  static const int n_sm = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return v;
+  }();
+  const bool one_wave = static_cast<int64_t>(heads) * n_chunks <= 4LL * n_sm;
+  if (max_chunk > 0 && one_wave && (head_dim == 128 || head_dim == 64)) {
+    if (head_dim == 128) {
+      launch_pdl(4, decode_attention_kernel<128, 4, 4, 0, 8>, grid, dim3(8 * 32), 0, s, q,
+                 d_chunks, slabs, heads, sl2, part_o, part_ml, pd, direct_out);
+    } else {
+      launch_pdl(4, decode_attention_kernel<64, 2, 4, 0, 8>, grid, dim3(8 * 32), 0, s, q,
+                 d_chunks, slabs, heads, sl2, part_o, part_ml, pd, direct_out);
+    }
+  } else if (head_dim == 128) {
     launch_pdl(4, decode_attention_kernel<128, 3, 8, 1>, grid, dim3(kWarps * 32), 0, s, q,
                d_chunks, slabs, heads, sl2, part_o, part_ml, pd, direct_out);
   } else if (head_dim == 64) {

@@ -188,10 +188,14 @@ struct DecodeSlabs {
 // direct_out: every row has exactly one chunk (short contexts on one
 // instance), so each CTA's partial IS the row's attention: it is normalised
 // and stored as bf16 [rows x heads*head_dim] and no combine is needed.
+// max_chunk: the longest chunk in tokens when the caller knows it (0 =
+// unknown: the default kernel); a grid that fits in one wave then takes an
+// 8-warp CTA with 64 tokens' K/V loads in flight per iteration.
 void decode_attention(const bf16* q, const DecodeChunk* d_chunks, int n_chunks,
                       const DecodeSlabs& slabs, int heads, int head_dim, float scale,
                       float* part_o, float* part_ml, cudaStream_t s,
-                      const PartDst* dst = nullptr, bf16* direct_out = nullptr);
+                      const PartDst* dst = nullptr, bf16* direct_out = nullptr,
+                      int max_chunk = 0);
 // LSE combine of the partials of each row (chunks row_start[r]..row_start[r+1]).
 void decode_combine(const float* part_o, const float* part_ml, const int32_t* row_start,
                     int rows, int heads, int head_dim, bf16* out, cudaStream_t s);
