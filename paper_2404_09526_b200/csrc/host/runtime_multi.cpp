@@ -1106,11 +1106,13 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         const int own = own_n[xd], n_ch = static_cast<int>(chs.size());
         auto attend = [&](int c0, int c1) {
           if (c1 <= c0) return;
+          int max_n = 0;
+          for (int c = c0; c < c1; ++c) max_n = std::max(max_n, static_cast<int>(chs[c].n));
           timed(kPhDecodeAttn, s, [&] {
             k::decode_attention(static_cast<bf16*>(xc.qin.ptr),
                                 static_cast<k::DecodeChunk*>(xc.chunks.ptr) + c0, c1 - c0, slabs,
                                 heads, hd, scale, static_cast<float*>(xc.part_o.ptr),
-                                static_cast<float*>(xc.part_ml.ptr), s, &pd);
+                                static_cast<float*>(xc.part_ml.ptr), s, &pd, nullptr, max_n);
           });
         };
         // own rows: this domain's QKV is earlier on its stream; its own
@@ -1232,11 +1234,14 @@ void Runtime::decode_multi(const esp_decode_args& a, const std::vector<DecodeRow
         slabs.k[j] = instances_[xc.slabs[j]].layer_k(l);
         slabs.v[j] = instances_[xc.slabs[j]].layer_v(l);
       }
+      int max_n = 0;
+      for (const k::DecodeChunk& c : chs) max_n = std::max(max_n, static_cast<int>(c.n));
       timed(kPhDecodeAttn, s, [&] {
         k::decode_attention(static_cast<bf16*>(xc.qin.ptr),
                             static_cast<k::DecodeChunk*>(xc.chunks.ptr),
                             static_cast<int>(chs.size()), slabs, heads, hd, scale,
-                            static_cast<float*>(xc.part_o.ptr), static_cast<float*>(xc.part_ml.ptr), s);
+                            static_cast<float*>(xc.part_o.ptr), static_cast<float*>(xc.part_ml.ptr), s,
+                            nullptr, nullptr, max_n);
       });
       cudaEvent_t e = sync_event(xc);
       cuda_ok(cudaEventRecord(e, s), "event");
