@@ -1029,10 +1029,24 @@ void Runtime::decode_step(const esp_decode_args& a) {
   int32_t* d_gslab = nullptr;
   int32_t* d_gslot = nullptr;
   std::vector<int32_t> work_sorted;
+  // The request's slots in token order are often one ascending run on one
+  // slab (one instance, a fresh free list): K1 then reads K/V straight from
+  // the slab rows — no per-layer gather into contiguous buffers.
+  int run_slab = -1, run_slot0 = 0;
   if (has_chunk) {
     std::vector<int32_t> gslab = prev_slab, gslot = prev_slot;
     gslab.insert(gslab.end(), ch_slab.begin(), ch_slab.end());
     gslot.insert(gslot.end(), ch_slot.begin(), ch_slot.end());
+    // (earlier tokens may sit in any order — every one precedes the chunk;
+    // the chunk's own rows must follow at kv rows p_prev + j)
+    bool run = !gslot.empty();
+    for (size_t i = 0; run && i < gslot.size(); ++i) {
+      run = gslab[i] == gslab[0] && gslot[i] == gslot[0] + static_cast<int32_t>(i);
+    }
+    if (run) {
+      run_slab = gslab[0];
+      run_slot0 = gslot[0];
+    }
     d_gslab = scratch<int32_t>(dc.ret_slab, kv_n);
     d_gslot = scratch<int32_t>(dc.ret_slot, kv_n);
     cuda_ok(cudaMemcpyAsync(d_gslab, gslab.data(), kv_n * 4, cudaMemcpyHostToDevice, s), "h2d");
@@ -1068,6 +1082,15 @@ void Runtime::decode_step(const esp_decode_args& a) {
   // skinny GEMMs — the residual epilogues accumulate row sums of squares
   // (ss1 before QKV, ss2 before gate_up) and the consuming GEMM scales its
   // accumulator rows (gains folded into the weights); no norm kernels.
+  // Output buffers sized before the timed region: growing them after the
+  // layers are enqueued (the final chunk adds a row) would put a
+  // synchronising cudaFree / cudaMalloc inside the step.
+  {
+    const size_t n_out_max = static_cast<size_t>(b + (has_chunk ? 1 : 0));
+    scratch<int32_t>(dc.last_rows, std::max<size_t>(n_out_max, 1));
+    scratch<float>(dc.logits, std::max<size_t>(n_out_max, 1) * cfg_.vocab);
+    scratch<int32_t>(dc.out_tok, std::max<size_t>(n_out_max, 1));
+  }
   const bool fuse_norm = rows <= 32 && opts_.fuse_norm_decode;
   float* ss1 = scratch<float>(dc.ss1, 32);
   float* ss2 = scratch<float>(dc.ss2, 32);
@@ -1121,8 +1144,17 @@ void Runtime::decode_step(const esp_decode_args& a) {
     }
     if (has_chunk) {
       timed(kPhAttention, s, [&] {
-        k::gather_rows(slabs, d_gslab, d_gslot, kv_n, kg, vg, H, s);
-        k::ring_attention(q, kg, vg, attn, rows, kv_n, cfg_.heads, cfg_.head_dim, static_cast<const k::RingSegment*>(dc.segs.ptr), static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
+        const bf16* kr = kg;
+        const bf16* vr = vg;
+        if (run_slab >= 0) {
+          kr = slabs.k[run_slab] + static_cast<int64_t>(run_slot0) * H;
+          vr = slabs.v[run_slab] + static_cast<int64_t>(run_slot0) * H;
+        } else {
+          k::gather_rows(slabs, d_gslab, d_gslot, kv_n, kg, vg, H, s);
+        }
+        k::ring_attention(q, kr, vr, attn, rows, kv_n, cfg_.heads, cfg_.head_dim,
+                          static_cast<const k::RingSegment*>(dc.segs.ptr),
+                          static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);
       });
     }
     NormFuse nf;

@@ -472,6 +472,11 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
     h_slot.push_back(ck.ch_slot[static_cast<size_t>(i)]);
   }
   const int kv_n = static_cast<int>(ck.p_prev) + c;
+  // one ascending slot run on one slab: K1 reads the slab rows directly
+  bool run = c > 0;
+  for (size_t i = 0; run && i < ck.kv_slot.size(); ++i) {
+    run = ck.kv_slab[i] == ck.kv_slab[0] && ck.kv_slot[i] == ck.kv_slot[0] + static_cast<int32_t>(i);
+  }
   std::vector<int32_t> work_sorted;
   k::RingSegment sg{};
   if (c > 0) {
@@ -528,6 +533,12 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
     const size_t part_rows = static_cast<size_t>((rows + t - 1) / t) * t;  // reduce-scatter layout
     scratch<float>(dc.tp_po, part_rows * H);
     scratch<float>(dc.tp_pd, part_rows * H);
+    if (&dc == &d0) {  // output buffers sized before the layers (no cudaFree mid-step)
+      const size_t n_out_max = static_cast<size_t>(b + (c > 0 ? 1 : 0));
+      scratch<int32_t>(dc.last_rows, std::max<size_t>(n_out_max, 1));
+      scratch<float>(dc.logits, std::max<size_t>(n_out_max, 1) * cfg_.vocab);
+      scratch<int32_t>(dc.out_tok, std::max<size_t>(n_out_max, 1));
+    }
     k::embed(static_cast<const int32_t*>(dc.tok.ptr), dc.embed, x, rows, H, s, nullptr);
   }
   for (int l = 0; l < cfg_.layers; ++l) {
@@ -572,10 +583,16 @@ double Runtime::decode_tp(const esp_decode_args& a, const std::vector<DecodeRow>
         }
       }
       if (c > 0) {
-        bf16* kg = static_cast<bf16*>(dc.kb.ptr);
-        bf16* vg = static_cast<bf16*>(dc.vb.ptr);
-        k::gather_rows(slabs, static_cast<const int32_t*>(dc.ret_slab.ptr),
-                       static_cast<const int32_t*>(dc.ret_slot.ptr), kv_n, kg, vg, Hs, s);
+        const bf16* kg = static_cast<bf16*>(dc.kb.ptr);
+        const bf16* vg = static_cast<bf16*>(dc.vb.ptr);
+        if (run) {
+          kg = slabs.k[ck.kv_slab[0]] + static_cast<int64_t>(ck.kv_slot[0]) * Hs;
+          vg = slabs.v[ck.kv_slab[0]] + static_cast<int64_t>(ck.kv_slot[0]) * Hs;
+        } else {
+          k::gather_rows(slabs, static_cast<const int32_t*>(dc.ret_slab.ptr),
+                         static_cast<const int32_t*>(dc.ret_slot.ptr), kv_n,
+                         static_cast<bf16*>(dc.kb.ptr), static_cast<bf16*>(dc.vb.ptr), Hs, s);
+        }
         k::ring_attention(q, kg, vg, attn, rows, kv_n, hs, cfg_.head_dim,
                           static_cast<const k::RingSegment*>(dc.segs.ptr),
                           static_cast<const int32_t*>(dc.work.ptr), n_work, scale, s);

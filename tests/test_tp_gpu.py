@@ -216,3 +216,34 @@ def test_tp_attention_capture_assembles_plane_shards():
         a, b = caps[1][l], caps[2][l]
         tol = 1e-2 if l == 0 else 3e-2
         assert np.linalg.norm(a - b) <= tol * np.linalg.norm(a), l
+
+
+@pytest.mark.parametrize("tp", [1, 2])
+def test_chunk_only_steps_contiguous_slots(tp):
+    """A prompt prefilled only by chunks (chunk-only decode steps, no decode
+    batch) on a fresh instance: its slots form one ascending run, so the
+    chunk attention reads K/V straight from the slab rows instead of
+    gathering them (the fast path of the chunked-prefill baseline); then two
+    decode steps. First token + logits against the dense oracle."""
+    shape, S, C = abi.TINY, 1300, 512
+    prompt = np.random.default_rng(31).integers(0, shape.vocab, S).astype(np.int32)
+    kw = {"tp_planes": [0] * tp} if tp > 1 else {"devices": [0]}
+    rt = abi.Runtime(shape, 1, kv_capacity=4096, **kw)
+    toks, logits = [], []
+    try:
+        for p0 in range(0, S, C):
+            n = min(C, S - p0)
+            ch = {"request": 5, "placement": [(0, n)], "tokens": prompt[p0:p0 + n],
+                  "final": p0 + n == S}
+            rt.decode_step([0], [], [], want_logits=True, chunk=ch)
+            if ch["final"]:
+                toks.append(int(ch["first_token"]))
+                logits.append(np.asarray(ch["logits"]).reshape(-1))
+        for _ in range(2):
+            out, lg, _ = rt.decode_step([0], [0], [5], want_logits=True)
+            toks.append(int(out[0]))
+            logits.append(lg[0])
+        rt.check_conservation()
+    finally:
+        rt.close()
+    check_against_oracle(shape, prompt, toks, logits)
