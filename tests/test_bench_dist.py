@@ -73,7 +73,7 @@ def _ring_worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_ring_baseline_round_order_gloo(world):
     """The send/recv ring baseline (bench.nccl_ring_baseline) on CPU/gloo:
     world-1 rounds of grouped send/recv deliver each rank the block of origin
